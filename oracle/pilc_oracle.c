@@ -1,0 +1,173 @@
+/*
+ * PILC CPU oracle -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C restatement of the reference's compiled hot loops
+ * (/root/reference/pkg/src/pixelcodec/_kernels.py), used by tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * as the checker. The product (paper_2206_05279_b200) never links this.
+ *
+ * Deliberately written like the reference: one bit per inner iteration for
+ * the coder, raster order for the inverse predictor. Pinned against the
+ * reference's own outputs by tests/test_oracle.py (tests/golden/ fixtures).
+ *
+ * Build: oracle/Makefile  (gcc -O2 -ffp-contract=off -fopenmp -shared)
+ * -ffp-contract=off is part of the contract: the reference accumulates the
+ * predictor in float32 without FMA (_kernels.py:82-88).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+/* _kernels.py:20-40 (encode_lane). Symbols are read at syms[i*stride],
+ * i = n-1 .. 0 (reverse order); bits are pushed LSB-first into buf, which
+ * the caller zero-fills and sizes for n*(M+1) bits. Returns the final state. */
+int64_t oracle_encode_lane(const uint8_t *syms, const uint16_t *ds, int64_t n,
+                           int64_t stride, const uint16_t *delta,
+                           const uint16_t *phi, int64_t X, int M, uint8_t *buf,
+                           int64_t *nbits_out) {
+    int64_t state = (int64_t)1 << M;
+    int64_t pos = 0;
+    for (int64_t i = n - 1; i >= 0; --i) {
+        int64_t d = ds[i * stride];
+        int64_t x = syms[i * stride];
+        int64_t b = ((int64_t)delta[d * X + x] + state) >> M;
+        for (int64_t j = 0; j < b; ++j) {
+            int64_t bit = (state >> j) & 1;
+            buf[pos >> 3] |= (uint8_t)(bit << (pos & 7));
+            ++pos;
+        }
+        state = (state >> b) + (int64_t)phi[d * X + x];
+    }
+    *nbits_out = pos;
+    return state;
+}
+
+/* _kernels.py:43-63 (decode_lane). Returns the end state (-1 on underflow)
+ * and the number of unread bits in *rem. Output at out[i*stride]. */
+int64_t oracle_decode_lane(int64_t state, const uint8_t *buf, int64_t nbits,
+                           const uint16_t *ds, int64_t n, int64_t stride,
+                           const uint8_t *theta, const uint8_t *bcnt,
+                           const uint16_t *nxt, int M, uint8_t *out,
+                           int64_t *rem) {
+    const int64_t base = (int64_t)1 << M;
+    const int64_t T = base;
+    int64_t pos = nbits;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t idx = state - base;
+        int64_t d = ds[i * stride];
+        out[i * stride] = theta[d * T + idx];
+        int64_t b = bcnt[d * T + idx];
+        if (pos < b) {
+            *rem = pos;
+            return -1;
+        }
+        int64_t v = 0;
+        for (int64_t k = 0; k < b; ++k) {
+            --pos;
+            v = (v << 1) | ((buf[pos >> 3] >> (pos & 7)) & 1);
+        }
+        state = (int64_t)nxt[d * T + idx] + v;
+    }
+    *rem = pos;
+    return state;
+}
+
+/* _kernels.py:68-79 (_round_mod256): f64 round-half-away, fmod 256. */
+static int64_t round_mod256(float p32) {
+    double p = (double)p32;
+    double r = p >= 0.0 ? floor(p + 0.5) : ceil(p - 0.5);
+    double m = fmod(r, 256.0);
+    if (m < 0.0) m += 256.0;
+    return (int64_t)m;
+}
+
+/* _kernels.py:82-88 (_predict3): f32, left to right, bias last, no FMA. */
+static int64_t predict3(float c0, float c1, float c2, const float *w, float b) {
+    float acc = w[0] * c0;
+    acc = acc + w[1] * c1;
+    acc = acc + w[2] * c2;
+    acc = acc + b;
+    return round_mod256(acc);
+}
+
+#define PX(img, u, v, c) (img)[((int64_t)(u) * W + (v)) * 3 + (c)]
+
+/* predictor.py:173-195 (predictions + forward_residual), stock k=3 layout
+ * (predictor.py:36-40): R <- (ul, up, left); G,B <- (left, prev-left,
+ * prev-here); zero outside the image. One image per OpenMP iteration. */
+void oracle_twar_forward(const uint8_t *img, int64_t N, int H, int W,
+                         const float *w9, const float *b3, uint8_t *res) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t n = 0; n < N; ++n) {
+        const uint8_t *x = img + n * (int64_t)H * W * 3;
+        uint8_t *t = res + n * (int64_t)H * W * 3;
+        for (int u = 0; u < H; ++u)
+            for (int v = 0; v < W; ++v)
+                for (int c = 0; c < 3; ++c) {
+                    float c0, c1, c2;
+                    if (c == 0) {
+                        c0 = (u > 0 && v > 0) ? (float)PX(x, u - 1, v - 1, 0) : 0.f;
+                        c1 = u > 0 ? (float)PX(x, u - 1, v, 0) : 0.f;
+                        c2 = v > 0 ? (float)PX(x, u, v - 1, 0) : 0.f;
+                    } else {
+                        c0 = v > 0 ? (float)PX(x, u, v - 1, c) : 0.f;
+                        c1 = v > 0 ? (float)PX(x, u, v - 1, c - 1) : 0.f;
+                        c2 = (float)PX(x, u, v, c - 1);
+                    }
+                    int64_t pred = predict3(c0, c1, c2, w9 + 3 * c, b3[c]);
+                    PX(t, u, v, c) = (uint8_t)(((int64_t)PX(x, u, v, c) - pred + 128) & 0xFF);
+                }
+    }
+}
+
+/* _kernels.py:91-112 (seq_decode3), batched like seq_decode3_batch
+ * (_kernels.py:173-176). Optional shift plane undoes recentring first
+ * (logistic.py:166-168): t = (coded + shift - 128) & 255. */
+void oracle_twar_decode(const uint8_t *coded, const uint8_t *shift, int64_t N,
+                        int H, int W, const float *w9, const float *b3,
+                        uint8_t *out) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t n = 0; n < N; ++n) {
+        const int64_t off = n * (int64_t)H * W * 3;
+        const uint8_t *r = coded + off;
+        const uint8_t *sh = shift ? shift + off : 0;
+        uint8_t *o = out + off;
+#define RES(u, v, c) ((int64_t)(sh ? (uint8_t)((PX(r, u, v, c) + PX(sh, u, v, c) - 128) & 0xFF) : PX(r, u, v, c)))
+        for (int u = 0; u < H; ++u)
+            for (int v = 0; v < W; ++v) {
+                float c0 = (u > 0 && v > 0) ? (float)PX(o, u - 1, v - 1, 0) : 0.f;
+                float c1 = u > 0 ? (float)PX(o, u - 1, v, 0) : 0.f;
+                float c2 = v > 0 ? (float)PX(o, u, v - 1, 0) : 0.f;
+                int64_t pred = predict3(c0, c1, c2, w9, b3[0]);
+                PX(o, u, v, 0) = (uint8_t)((RES(u, v, 0) - 128 + pred) & 0xFF);
+            }
+        for (int c = 1; c < 3; ++c)
+            for (int u = 0; u < H; ++u)
+                for (int v = 0; v < W; ++v) {
+                    float c0 = v > 0 ? (float)PX(o, u, v - 1, c) : 0.f;
+                    float c1 = v > 0 ? (float)PX(o, u, v - 1, c - 1) : 0.f;
+                    float c2 = (float)PX(o, u, v, c - 1);
+                    int64_t pred = predict3(c0, c1, c2, w9 + 3 * c, b3[c]);
+                    PX(o, u, v, c) = (uint8_t)((RES(u, v, c) - 128 + pred) & 0xFF);
+                }
+#undef RES
+    }
+}
+
+/* Batched lanes for the CPU baseline: image i owns syms[i*n .. i*n+n),
+ * lane l takes symbols l, l+L, ... (tables.py:202-223). Per-lane scratch
+ * of cap bytes; outputs nbits/state per (image, lane). */
+void oracle_encode_batch(const uint8_t *syms, const uint16_t *ds, int64_t N,
+                         int64_t n, int64_t L, const uint16_t *delta,
+                         const uint16_t *phi, int64_t X, int M, uint8_t *scratch,
+                         int64_t cap, int64_t *nbits, int64_t *states) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t k = 0; k < N * L; ++k) {
+        int64_t img = k / L, lane = k % L;
+        int64_t cnt = lane < n ? (n - lane + L - 1) / L : 0;
+        uint8_t *buf = scratch + k * cap;
+        memset(buf, 0, (size_t)cap);
+        states[k] = oracle_encode_lane(syms + img * n + lane, ds + img * n + lane,
+                                       cnt, L, delta, phi, X, M, buf, &nbits[k]);
+    }
+}
