@@ -1,0 +1,562 @@
+"""PILC pipeline and container on the GPU (drop-in for `pixelcodec/container.py`).
+
+Public surface (same names/signatures as the reference):
+    compress(image, model=None, config=CodecConfig()) -> bytes
+    decompress(blob, model=None, workers=1) -> uint8[H, W, 3]
+    parse_header(blob), inspect(blob), bpd_report(blob, original)
+plus the batch API the B200 path is built around:
+    compress_batch(images, model, config) -> (buffer uint8, offsets uint64[N+1])
+    decompress_batch(buffer, offsets, model) -> uint8[N, H, W, 3] (or list)
+
+Per batch (one (H, W) group), everything runs on the device on one stream:
+    compress   H2D -> twar_forward -> [vq_encode -> vq_decode+head] ->
+               rans_encode(index) -> rans_encode(residual, recentred on the
+               fly) -> sizes/scan -> pack (+crc32) -> D2H
+    decompress H2D -> parse (+crc32, grid/hash checks) -> [lanes -> rans_decode
+               (index) -> vq_decode+head] -> lanes -> rans_decode(residual,
+               un-recentred on the way out) -> twar_decode -> D2H
+Host work is per batch, not per blob: header templates, cached tables, one
+sync to size the output (compress) or read parsed headers (decompress).
+Data errors come back as per-blob status codes and are raised in the
+reference's check order (container.py:195-335) for the first bad blob.
+"""
+
+from __future__ import annotations
+
+import struct
+import zlib
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import as_device_u8, h2d, pinned, ptr, require_device, sptr
+from .errors import CorruptStreamError, FormatError, ModelError, ParameterError
+from .logistic import ScaleGrid, default_grid, residual_distributions
+from .predictor import PredictorParams, decode_device, default_params, forward_residual_device, validate_image
+from .tables import build_tables, encode_lanes_device
+from .vqvae import decode_head_device, encode_indices_device, index_histogram_pmf, latent_shape
+from .weights import ModelWeights
+
+MAGIC = b"PILC"
+VERSION = 1
+PAD_RULE_ZERO = 0
+BACKEND_STATIC = 0
+BACKEND_VQVAE = 1
+BACKEND_NAMES = {BACKEND_STATIC: "twar-static", BACKEND_VQVAE: "twar-vqvae"}
+BACKEND_IDS = {v: k for k, v in BACKEND_NAMES.items()}
+FLAG_SCHEDULE_CHECKSUM = 1
+
+
+@dataclass(frozen=True)
+class CodecConfig:
+    backend: str = "twar-static"
+    M: int = 12
+    lanes: int = 1
+    grid: ScaleGrid = field(default_factory=default_grid)
+    verify_tables: bool = False
+    debug_schedule_check: bool = False
+
+    def __post_init__(self):
+        if self.backend not in BACKEND_IDS:
+            raise ParameterError(f"unknown backend {self.backend!r}")
+        if not 10 <= self.M <= 12:
+            raise ParameterError("M must be in [10, 12]")
+        if not 1 <= self.lanes <= 65535:
+            raise ParameterError("lane count must fit in 16 bits")
+
+
+@dataclass(frozen=True)
+class ContainerHeader:
+    backend: int
+    M: int
+    pad_rule: int
+    width: int
+    height: int
+    lanes: int
+    static_d: int
+    grid: ScaleGrid
+    params_hash: bytes
+    model_hash: bytes | None
+    index_lane_bytes: tuple
+    index_states: tuple
+    residual_lane_bytes: tuple
+    residual_states: tuple
+    schedule_checksum: int | None = None
+
+
+# ---------------------------------------------------------------------------
+# compress
+
+
+def _params_of(model: ModelWeights | None) -> PredictorParams:
+    return model.predictor_params if model is not None else default_params()
+
+
+def _template(backend: int, cfg: CodecConfig, W: int, H: int, params: PredictorParams,
+              model: ModelWeights | None) -> bytes:
+    flags = FLAG_SCHEDULE_CHECKSUM if cfg.debug_schedule_check else 0
+    t = MAGIC + struct.pack("<BBBBB", VERSION, backend, cfg.M, PAD_RULE_ZERO, flags)
+    t += struct.pack("<IIHH", W, H, cfg.lanes, 0) + cfg.grid.to_bytes() + params.hash8()
+    if backend == BACKEND_VQVAE:
+        t += model.hash8()
+    return t
+
+
+def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, stream):
+    """One (H, W) group, all on `stream`. Returns (out_d, blob_off_d, total)."""
+    N, H, W, _ = img_d.shape
+    if W >= (1 << 32) or H >= (1 << 32):
+        raise ParameterError("image dimensions do not fit 32 bits")
+    backend = BACKEND_IDS[config.backend]
+    M, L, grid = config.M, config.lanes, config.grid
+    if grid.D > 256:
+        raise ParameterError("the GPU path carries distribution indices as uint8 (grid D <= 256)")
+    params = _params_of(model)
+    t_d = forward_residual_device(img_d, params, stream)
+    res_enc, _ = build_tables(residual_distributions(grid, M), M, verify=config.verify_tables)
+    n_sym = H * W * 3
+    idx_scr = idx_nb = idx_st = None
+    idx_cap = 0
+    d_img = dsched = shift = None
+    if backend == BACKEND_VQVAE:
+        if model is None or not model.has_network:
+            raise ModelError("vqvae backend needs model weights")
+        idx_d = encode_indices_device(img_d, model, dev, stream)
+        shift, dsched = decode_head_device(idx_d, model, H, W, grid, dev, stream)
+        idx_enc, _ = build_tables([index_histogram_pmf(model, M)], M, verify=config.verify_tables)
+        gh, gw = latent_shape(H, W)
+        idx_scr, idx_cap, idx_nb, idx_st = encode_lanes_device(idx_d, N, gh * gw, L, idx_enc, dev, stream)
+    else:
+        d_img = torch.empty(N, dtype=torch.int16, device=dev)
+        lg = np.ascontiguousarray(np.log2(grid.values), dtype=np.float64)
+        _lib.call("pilc_static_scale", ptr(t_d), N, n_sym, ptr(lg), grid.D, ptr(d_img), sptr(stream))
+    res_scr, res_cap, res_nb, res_st = encode_lanes_device(t_d, N, n_sym, L, res_enc, dev, stream,
+                                                           shift=shift, dsched=dsched, d_img=d_img)
+    tmpl = _template(backend, config, W, H, params, model)
+    fixed = len(tmpl) + (4 + 6 * L if backend == BACKEND_VQVAE else 0) + 4 + 6 * L
+    fixed += (4 if config.debug_schedule_check else 0) + 4
+    blob_off = torch.empty(N + 1, dtype=torch.int64, device=dev)
+    _lib.call("pilc_container_sizes", ptr(idx_nb), ptr(res_nb), N, L, fixed, ptr(blob_off), sptr(stream))
+    total_h = pinned(8)
+    with torch.cuda.stream(stream):
+        total_h.copy_(blob_off[N:].view(torch.uint8), non_blocking=True)
+    stream.synchronize()
+    total = int(total_h.numpy().view(np.uint64)[0])
+    out_d = torch.empty(total + 8, dtype=torch.uint8, device=dev)
+    tb = np.frombuffer(tmpl, dtype=np.uint8).copy()
+    _lib.call("pilc_container_pack", ptr(tb), len(tmpl), ptr(d_img), ptr(dsched),
+              1 if config.debug_schedule_check else 0, N, n_sym, L, ptr(idx_scr), idx_cap, ptr(idx_nb),
+              ptr(idx_st), ptr(res_scr), res_cap, ptr(res_nb), ptr(res_st), ptr(blob_off), ptr(out_d),
+              sptr(stream))
+    return out_d, blob_off, total
+
+
+def _groups_by_shape(shapes):
+    groups: dict = {}
+    for i, s in enumerate(shapes):
+        groups.setdefault(tuple(s), []).append(i)
+    return groups
+
+
+def compress_batch(images, model: ModelWeights | None = None, config: CodecConfig = CodecConfig(),
+                   device=None, return_device: bool = False):
+    """Compress a batch. `images`: (N, H, W, 3) uint8 numpy/torch (host or
+    cuda) or a list of (H, W, 3) arrays of mixed shapes. Returns
+    (buffer uint8[total], offsets uint64[N+1]); blob i is
+    buffer[offsets[i]:offsets[i+1]], byte-identical in format to
+    `pixelcodec.compress` of image i."""
+    dev = require_device(device)
+    stream = torch.cuda.current_stream(dev)
+    if isinstance(images, (list, tuple)):
+        imgs = [validate_image(im) for im in images]
+        groups = _groups_by_shape([im.shape for im in imgs])
+        parts = {}
+        for shape, ids in groups.items():
+            batch = np.stack([imgs[i] for i in ids])
+            parts[shape] = compress_batch(batch, model, config, device)
+        sizes = np.zeros(len(imgs), np.uint64)
+        for shape, ids in groups.items():
+            _, off = parts[shape]
+            sizes[ids] = np.diff(off)
+        offsets = np.zeros(len(imgs) + 1, np.uint64)
+        np.cumsum(sizes, out=offsets[1:])
+        out = np.empty(int(offsets[-1]), np.uint8)
+        for shape, ids in groups.items():
+            buf, off = parts[shape]
+            for j, i in enumerate(ids):
+                out[offsets[i]:offsets[i + 1]] = buf[off[j]:off[j + 1]]
+        return out, offsets
+    if isinstance(images, torch.Tensor):
+        if images.dtype != torch.uint8 or images.ndim != 4 or images.shape[-1] != 3:
+            raise ParameterError("expected a uint8 (N, H, W, 3) tensor")
+        img_d = images.to(dev).contiguous()
+    else:
+        arr = np.asarray(images)
+        if arr.dtype != np.uint8 or arr.ndim != 4 or arr.shape[-1] != 3:
+            raise ParameterError("expected a uint8 (N, H, W, 3) array")
+        if arr.shape[1] < 1 or arr.shape[2] < 1:
+            raise ParameterError("image dimensions must be >= 1")
+        img_d = as_device_u8(arr, dev, stream)
+    if img_d.shape[0] == 0:
+        return np.zeros(0, np.uint8), np.zeros(1, np.uint64)
+    out_d, off_d, total = _compress_device(img_d, model, config, dev, stream)
+    if return_device:
+        return out_d, off_d, total
+    host = pinned(total + 8 * (img_d.shape[0] + 1))
+    hv = host.numpy()
+    with torch.cuda.stream(stream):
+        host[:total].copy_(out_d[:total], non_blocking=True)
+        host[total:].copy_(off_d.view(torch.uint8), non_blocking=True)
+    stream.synchronize()
+    return hv[:total].copy(), hv[total:].view(np.uint64).copy()
+
+
+def compress(image: np.ndarray, model: ModelWeights | None = None, config: CodecConfig = CodecConfig()) -> bytes:
+    """Compress one image to a self-contained blob (container.py:128-192)."""
+    image = validate_image(image)
+    buf, off = compress_batch(image[None], model, config)
+    return buf[off[0]:off[1]].tobytes()
+
+
+# ---------------------------------------------------------------------------
+# decompress
+
+_MSG = {
+    1: (FormatError, "container truncated"),
+    2: (FormatError, "not a codec container (bad magic)"),
+    4: (CorruptStreamError, "container checksum mismatch"),
+    9: (FormatError, "bad dimensions or lane count"),
+    10: (FormatError, "scale grid truncated"),
+    11: (FormatError, "static scale index outside the grid"),
+    12: (FormatError, "index stream lengths inconsistent"),
+    13: (FormatError, "residual stream lengths inconsistent"),
+    14: (FormatError, "container payload length mismatch"),
+    15: (FormatError, "bad scale grid: grid needs at least one scale"),
+    16: (FormatError, "bad scale grid: grid scales must be finite and positive"),
+    17: (FormatError, "bad scale grid: grid scales must be strictly increasing"),
+    18: (FormatError, "bad scale grid: grid spacing must be geometric"),
+    20: (FormatError, "bit stream header truncated"),
+    21: (FormatError, "bit stream payload truncated"),
+    22: (FormatError, "lane length field disagrees with payload"),
+    23: (CorruptStreamError, "recorded coder state out of range"),
+    27: (ModelError, "model hash mismatch"),
+}
+
+
+def _header_error(h, has_model: bool) -> Exception | None:
+    st = int(h["status"])
+    if st == 0:
+        return None
+    if st == 3:
+        return FormatError(f"unsupported container version {int(h['aux'])}")
+    if st == 5:
+        return FormatError(f"unknown backend id {int(h['aux'])}")
+    if st == 6:
+        return FormatError(f"precision M={int(h['M'])} outside [10, 12]")
+    if st == 7:
+        return FormatError(f"unknown padding rule {int(h['pad_rule'])}")
+    if st == 8:
+        return FormatError(f"unknown header flags {int(h['flags']):#x}")
+    if st == 26:
+        return ModelError("predictor parameters do not match the container"
+                          + ("" if has_model else " (a model file is required)"))
+    cls, msg = _MSG.get(st, (FormatError, f"container rejected (status {st})"))
+    return cls(msg)
+
+
+def _lane_error(status_row: np.ndarray) -> Exception | None:
+    """_read_lanes order: all wire-size checks, then all state checks;
+    then decode errors lane by lane (tables.py:258-266)."""
+    bad = np.flatnonzero((status_row >= 20) & (status_row <= 22))
+    if bad.size:
+        cls, msg = _MSG[int(status_row[bad[0]])]
+        return cls(msg)
+    if np.any(status_row == 23):
+        return CorruptStreamError("recorded coder state out of range")
+    bad = np.flatnonzero(status_row >= 24)
+    if bad.size:
+        lane = int(bad[0])
+        if status_row[lane] == 24:
+            return CorruptStreamError(f"lane {lane} bit stream underflow")
+        return CorruptStreamError(f"lane {lane} did not return to the initial coder state")
+    return None
+
+
+def _parse_device(buf_d, off_d, n, model, dev, stream):
+    params = _params_of(model)
+    ph = int(np.frombuffer(params.hash8(), "<u8")[0])
+    has_model = model is not None and model.has_network
+    mh = int(np.frombuffer(model.hash8(), "<u8")[0]) if has_model else 0
+    hdr_d = torch.empty(n * _lib.HEADER_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    _lib.call("pilc_container_parse", ptr(buf_d), ptr(off_d), n, ph, mh, 1 if has_model else 0, ptr(hdr_d),
+              sptr(stream))
+    host = pinned(hdr_d.numel())
+    with torch.cuda.stream(stream):
+        host.copy_(hdr_d, non_blocking=True)
+    stream.synchronize()
+    return host.numpy().view(_lib.HEADER_DTYPE).copy(), hdr_d
+
+
+def _grid_of(buf_host, buf_d, off, h) -> ScaleGrid:
+    D = int(h["D"])
+    if buf_host is not None:
+        raw = bytes(buf_host[off + 21: off + 23 + 8 * D])
+    else:
+        raw = buf_d[off + 21: off + 23 + 8 * D].cpu().numpy().tobytes()
+    return ScaleGrid.from_bytes(raw)[0]
+
+
+def _decompress_device(buf_d, off_d, offs_host, model, dev, stream, buf_host=None):
+    """Decode all blobs. Returns (images: list of (ids, device tensor),
+    errors: dict blob -> Exception)."""
+    n = len(offs_host) - 1
+    hdr, hdr_d = _parse_device(buf_d, off_d, n, model, dev, stream)
+    has_model = model is not None and model.has_network
+    errors: dict = {}
+    st = hdr["status"]
+    for i in np.flatnonzero(st != 0):
+        errors[int(i)] = _header_error(hdr[i], model is not None)
+    ok = st == 0
+    need_model = ok & (hdr["backend"] == BACKEND_VQVAE)
+    if not has_model and need_model.any():
+        for i in np.flatnonzero(need_model):
+            errors[int(i)] = ModelError("container needs model weights to decode")
+        ok &= ~need_model
+    key = np.zeros(n, dtype=[("w", "<u4"), ("h", "<u4"), ("b", "u1"), ("M", "u1"), ("L", "<u2"),
+                             ("f", "u1"), ("D", "<u2"), ("g", "<u4")])
+    key["w"], key["h"], key["b"], key["M"] = hdr["width"], hdr["height"], hdr["backend"], hdr["M"]
+    key["L"], key["f"], key["D"], key["g"] = hdr["lanes"], hdr["flags"], hdr["D"], hdr["grid_crc"]
+    ids_ok = np.flatnonzero(ok)
+    results = []
+    if ids_ok.size == 0:
+        return results, errors, hdr
+    uk, inv = np.unique(key[ids_ok], return_inverse=True)
+    for gi, k in enumerate(uk):
+        ids = ids_ok[inv == gi]
+        h0 = hdr[ids[0]]
+        W, H, backend, M, L = int(k["w"]), int(k["h"]), int(k["b"]), int(k["M"]), int(k["L"])
+        flags = int(k["f"])
+        grid = _grid_of(buf_host, buf_d, int(offs_host[ids[0]]), h0)
+        if grid.D > 256:
+            for i in ids:
+                errors[int(i)] = ParameterError("the GPU path carries distribution indices as uint8 (grid D <= 256)")
+            continue
+        ng = ids.size
+        ids_d = torch.from_numpy(ids.astype(np.int64)).to(dev)
+        _, res_dec = build_tables(residual_distributions(grid, M), M)
+        n_sym = H * W * 3
+        shift = dsel = d_img = None
+        lane_st = {}
+        if backend == BACKEND_VQVAE:
+            gh, gw = latent_shape(H, W)
+            _, idx_dec = build_tables([index_histogram_pmf(model, M)], M)
+            lo = torch.empty(ng * L, dtype=torch.int64, device=dev)
+            nb = torch.empty(ng * L, dtype=torch.int32, device=dev)
+            ss = torch.empty(ng * L, dtype=torch.int16, device=dev)
+            ls = torch.empty(ng * L, dtype=torch.uint8, device=dev)
+            _lib.call("pilc_container_lanes", ptr(buf_d), ptr(off_d), ptr(hdr_d), ptr(ids_d), ng, L, 0, ptr(lo),
+                      ptr(nb), ptr(ss), ptr(ls), sptr(stream))
+            idx = torch.zeros((ng, gh, gw), dtype=torch.uint8, device=dev)
+            _lib.call("pilc_rans_decode", ptr(buf_d), ptr(lo), ptr(nb), ptr(ss), None, None, ng, gh * gw, L,
+                      ptr(idx_dec.device_words(dev)), idx_dec.D, M, None, ptr(idx), ptr(ls), sptr(stream))
+            lane_st["idx"] = ls
+            shift, dsel = decode_head_device(idx, model, H, W, grid, dev, stream)
+        else:
+            d_img = torch.from_numpy(hdr["static_d"][ids].astype(np.int16)).to(dev)
+        sched = None
+        if flags & FLAG_SCHEDULE_CHECKSUM:
+            sched = torch.empty(ng, dtype=torch.int32, device=dev)
+            _lib.call("pilc_sched_crc", ptr(dsel), ptr(d_img), ng, n_sym, ptr(sched), sptr(stream))
+        lo = torch.empty(ng * L, dtype=torch.int64, device=dev)
+        nb = torch.empty(ng * L, dtype=torch.int32, device=dev)
+        ss = torch.empty(ng * L, dtype=torch.int16, device=dev)
+        ls = torch.empty(ng * L, dtype=torch.uint8, device=dev)
+        _lib.call("pilc_container_lanes", ptr(buf_d), ptr(off_d), ptr(hdr_d), ptr(ids_d), ng, L, 1, ptr(lo),
+                  ptr(nb), ptr(ss), ptr(ls), sptr(stream))
+        t = torch.zeros((ng, H, W, 3), dtype=torch.uint8, device=dev)
+        _lib.call("pilc_rans_decode", ptr(buf_d), ptr(lo), ptr(nb), ptr(ss), ptr(dsel), ptr(d_img), ng, n_sym, L,
+                  ptr(res_dec.device_words(dev)), res_dec.D, M, ptr(shift), ptr(t), ptr(ls), sptr(stream))
+        lane_st["res"] = ls
+        params = _params_of(model)
+        img = decode_device(t, params, stream)
+        results.append((ids, img, lane_st, sched, L))
+    return results, errors, hdr
+
+
+def _resolve_errors(results, errors, hdr):
+    """Per-blob errors of the decode stages, in the reference's order."""
+    for ids, _img, lane_st, sched, L in results:
+        st_idx = lane_st["idx"].cpu().numpy().reshape(-1, L) if "idx" in lane_st else None
+        st_res = lane_st["res"].cpu().numpy().reshape(-1, L)
+        crc = sched.cpu().numpy().view(np.uint32) if sched is not None else None
+        bad = np.zeros(ids.size, bool)
+        if st_idx is not None:
+            bad |= st_idx.any(axis=1)
+        bad |= st_res.any(axis=1)
+        if crc is not None:
+            bad |= crc != hdr["sched_crc"][ids]
+        for j in np.flatnonzero(bad):
+            i = int(ids[j])
+            e = _lane_error(st_idx[j]) if st_idx is not None else None
+            if e is None and crc is not None and crc[j] != hdr["sched_crc"][i]:
+                e = CorruptStreamError("decoder-side distribution schedule disagrees with the encoder")
+            if e is None:
+                e = _lane_error(st_res[j])
+            if e is not None:
+                errors[i] = e
+    return errors
+
+
+def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=None,
+                     raise_on_error: bool = True):
+    """Decode blobs buffer[offsets[i]:offsets[i+1]]. Returns an
+    (N, H, W, 3) array when all blobs share a shape, else a list; with
+    raise_on_error=False returns (images, {blob index: exception})."""
+    dev = require_device(device)
+    stream = torch.cuda.current_stream(dev)
+    offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = offs.size - 1
+    buf_host = np.frombuffer(buffer, np.uint8) if isinstance(buffer, (bytes, bytearray, memoryview)) \
+        else np.ascontiguousarray(buffer, dtype=np.uint8)
+    if n <= 0:
+        return (np.zeros((0, 1, 1, 3), np.uint8), {}) if not raise_on_error else np.zeros((0, 1, 1, 3), np.uint8)
+    base = int(offs[0])
+    if base or int(offs[-1]) > buf_host.size:
+        if int(offs[-1]) > buf_host.size:
+            raise FormatError("container truncated")
+    buf_d = h2d(buf_host[: int(offs[-1])], dev, stream, pad=8)
+    off_d = h2d(offs.view(np.uint8), dev, stream).view(torch.int64)
+    results, errors, hdr = _decompress_device(buf_d, off_d, offs, model, dev, stream, buf_host)
+    errors = _resolve_errors(results, errors, hdr)
+    if errors and raise_on_error:
+        raise errors[min(errors)]
+    shapes = {(int(h["height"]), int(h["width"])) for h in hdr[[i for i in range(n) if i not in errors]]} \
+        if len(errors) < n else set()
+    # D2H through pinned memory
+    imgs: list = [None] * n
+    for ids, img, *_ in results:
+        host = pinned(img.numel())
+        with torch.cuda.stream(stream):
+            host.copy_(img.view(-1), non_blocking=True)
+        stream.synchronize()
+        arr = host.numpy().reshape(tuple(img.shape)).copy()
+        for j, i in enumerate(ids):
+            if int(i) not in errors:
+                imgs[int(i)] = arr[j]
+    if len(shapes) == 1 and not errors:
+        out = np.stack(imgs) if n > 1 else imgs[0][None]
+    else:
+        out = imgs
+    return (out, errors) if not raise_on_error else out
+
+
+def decompress(blob: bytes, model: ModelWeights | None = None, workers: int = 1) -> np.ndarray:
+    """Exact inverse of compress (container.py:274-335)."""
+    blob = bytes(blob)
+    out = decompress_batch(blob, np.array([0, len(blob)], np.uint64), model)
+    return out[0]
+
+
+# ---------------------------------------------------------------------------
+# header-level API (host; metadata only)
+
+
+class _Reader:
+    def __init__(self, data: bytes):
+        self.data = data
+        self.off = 0
+
+    def take(self, n: int) -> bytes:
+        if self.off + n > len(self.data):
+            raise FormatError("container truncated")
+        out = self.data[self.off: self.off + n]
+        self.off += n
+        return out
+
+    def unpack(self, fmt: str):
+        return struct.unpack(fmt, self.take(struct.calcsize(fmt)))
+
+
+def parse_header(blob: bytes) -> tuple[ContainerHeader, int]:
+    """Validate framing and return (header, payload offset) (container.py:195-258)."""
+    if len(blob) < 8:
+        raise FormatError("container truncated")
+    if blob[:4] != MAGIC:
+        raise FormatError("not a codec container (bad magic)")
+    if blob[4] != VERSION:
+        raise FormatError(f"unsupported container version {blob[4]}")
+    (crc,) = struct.unpack_from("<I", blob, len(blob) - 4)
+    if zlib.crc32(blob[:-4]) != crc:
+        raise CorruptStreamError("container checksum mismatch")
+    r = _Reader(blob)
+    r.take(5)
+    backend, M, pad_rule, flags = struct.unpack("<BBBB", r.take(4))
+    if backend not in BACKEND_NAMES:
+        raise FormatError(f"unknown backend id {backend}")
+    if not 10 <= M <= 12:
+        raise FormatError(f"precision M={M} outside [10, 12]")
+    if pad_rule != PAD_RULE_ZERO:
+        raise FormatError(f"unknown padding rule {pad_rule}")
+    if flags & ~FLAG_SCHEDULE_CHECKSUM:
+        raise FormatError(f"unknown header flags {flags:#x}")
+    W, H, L, static_d = r.unpack("<IIHH")
+    if W < 1 or H < 1 or L < 1:
+        raise FormatError("bad dimensions or lane count")
+    try:
+        grid, end = ScaleGrid.from_bytes(blob, r.off)
+    except ParameterError as e:
+        raise FormatError(f"bad scale grid: {e}")
+    r.off = end
+    if static_d >= grid.D:
+        raise FormatError("static scale index outside the grid")
+    params_hash = r.take(8)
+    model_hash = None
+    il: tuple = ()
+    ist: tuple = ()
+    if backend == BACKEND_VQVAE:
+        model_hash = r.take(8)
+        (tot,) = r.unpack("<I")
+        il = r.unpack(f"<{L}I")
+        ist = r.unpack(f"<{L}H")
+        if sum(il) != tot:
+            raise FormatError("index stream lengths inconsistent")
+    (tot,) = r.unpack("<I")
+    rl = r.unpack(f"<{L}I")
+    rst = r.unpack(f"<{L}H")
+    if sum(rl) != tot:
+        raise FormatError("residual stream lengths inconsistent")
+    sched = None
+    if flags & FLAG_SCHEDULE_CHECKSUM:
+        (sched,) = r.unpack("<I")
+    header = ContainerHeader(backend, M, pad_rule, W, H, L, static_d, grid, params_hash, model_hash,
+                             il, ist, rl, rst, sched)
+    if r.off + sum(il) + sum(rl) + 4 != len(blob):
+        raise FormatError("container payload length mismatch")
+    return header, r.off
+
+
+def bpd_report(blob: bytes, original: np.ndarray) -> float:
+    """Real bits per dimension: every container byte counts."""
+    original = validate_image(original)
+    return 8.0 * len(blob) / original.size
+
+
+def inspect(blob: bytes) -> dict:
+    header, _ = parse_header(blob)
+    return {
+        "backend": BACKEND_NAMES[header.backend],
+        "width": header.width,
+        "height": header.height,
+        "M": header.M,
+        "lanes": header.lanes,
+        "padding_rule": header.pad_rule,
+        "grid": [float(v) for v in header.grid.values],
+        "static_scale_index": header.static_d,
+        "params_hash": header.params_hash.hex(),
+        "model_hash": header.model_hash.hex() if header.model_hash else None,
+        "index_stream_bytes": sum(header.index_lane_bytes),
+        "residual_stream_bytes": sum(header.residual_lane_bytes),
+        "container_bytes": len(blob),
+    }

@@ -1,0 +1,136 @@
+// Shared helpers for the PILC sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pilc.h"
+
+#define PILC_CHECK_LAUNCH()                              \
+    do {                                                 \
+        if (cudaPeekAtLastError() != cudaSuccess) {      \
+            cudaGetLastError();                          \
+            return PILC_E_CUDA;                          \
+        }                                                \
+    } while (0)
+
+static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Grid sizing: the B200 has 148 SMs; cap grids at a multiple of the SM
+// count and let kernels grid-stride.
+static inline int sm_count() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached = n > 0 ? n : 148;
+    }
+    return cached;
+}
+
+// ---------------------------------------------------------------------------
+// CRC-32 (zlib polynomial 0xEDB88320, reflected), warp-cooperative.
+//
+// The warp walks the blob in rounds of 32 x 64 bytes. Lane i takes the i-th
+// 64-byte chunk of the round, computes a standard crc32 of it with a
+// byte table, and the chunks are merged with the affine combine rule
+//   crc(A||B) = crc(A) * x^(8|B|)  xor  crc(B)     (mod P, reflected)
+// (the rule zlib's crc32_combine implements). Powers x^(8*64*j) come from a
+// small table; the ragged final round costs two x2nmodp evaluations.
+
+struct CrcConsts {
+    uint32_t tab[256];
+    uint32_t qpow[33];  // (x^(8*64))^j mod P, j = 0..32
+    uint32_t x2n[32];   // x^(2^k) mod P
+};
+
+__host__ __device__ inline uint32_t crc_multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return p;
+}
+
+// x^(n * 2^k) mod P
+__host__ __device__ inline uint32_t crc_x2nmodp(const uint32_t *x2n, uint64_t n, unsigned k) {
+    uint32_t p = 1u << 31;
+    while (n) {
+        if (n & 1) p = crc_multmodp(x2n[k & 31], p);
+        n >>= 1;
+        k++;
+    }
+    return p;
+}
+
+const CrcConsts &crc_consts();  // host, built once (container.cu)
+
+// Standard crc32 over n bytes (n may be 0) starting at p, table in smem.
+__device__ inline uint32_t crc_bytes(const uint32_t *tab, const uint8_t *p, int n) {
+    uint32_t c = 0xFFFFFFFFu;
+    for (int i = 0; i < n; ++i) c = tab[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+    return c ^ 0xFFFFFFFFu;
+}
+
+__device__ inline uint32_t warp_xor(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Whole-warp crc32 of [p, p+n). stage: 32*64 + 64 bytes of this warp's smem.
+__device__ inline uint32_t warp_crc32(const CrcConsts *cc, const uint8_t *p, uint64_t n,
+                                      uint8_t *stage) {
+    const int lane = threadIdx.x & 31;
+    uint32_t crc = 0;  // crc32 of the empty string
+    uint64_t done = 0;
+    while (done < n) {
+        const uint64_t rem = n - done;
+        const int rb = rem >= 2048 ? 2048 : (int)rem;
+        // coalesced byte loads into smem, chunk i at stage + i*68 (padded)
+        for (int j = lane; j < rb; j += 32) stage[(j >> 6) * 68 + (j & 63)] = p[done + j];
+        __syncwarp();
+        const int beg = lane * 64;
+        int len = rb - beg;
+        len = len < 0 ? 0 : (len > 64 ? 64 : len);
+        uint32_t c = crc_bytes(cc->tab, stage + lane * 68, len);
+        uint32_t term;
+        if (rb == 2048) {
+            term = crc_multmodp(cc->qpow[31 - lane], c);
+        } else {
+            // chunks k_last = (rb-1)/64 is ragged with r = rb - 64*k_last bytes
+            const int kl = (rb - 1) >> 6;
+            const int r = rb - 64 * kl;
+            if (lane > kl) {
+                term = 0;
+            } else if (lane == kl) {
+                term = c;
+            } else {
+                uint32_t xr = crc_x2nmodp(cc->x2n, (uint64_t)r, 3);
+                term = crc_multmodp(crc_multmodp(cc->qpow[kl - lane - 1], xr), c);
+            }
+        }
+        const uint32_t round_crc = warp_xor(term);
+        if (rb == 2048)
+            crc = crc_multmodp(cc->qpow[32], crc) ^ round_crc;
+        else
+            crc = crc_multmodp(crc_x2nmodp(cc->x2n, (uint64_t)rb, 3), crc) ^ round_crc;
+        done += rb;
+        __syncwarp();
+    }
+    return crc;
+}
+
+__device__ inline void load_crc_consts(CrcConsts *dst, const CrcConsts &src) {
+    const uint32_t *s = reinterpret_cast<const uint32_t *>(&src);
+    uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(CrcConsts) / 4); i += blockDim.x) d[i] = s[i];
+}

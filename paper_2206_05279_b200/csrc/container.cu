@@ -1,0 +1,629 @@
+// PILC container on the device: static scale, blob sizing, packing, crc32,
+// header parsing and lane extraction.
+//
+// Layout (container.py:3-25, little-endian):
+//   "PILC" | ver u8 | backend u8 | M u8 | pad u8 | flags u8
+//   | W u32 | H u32 | L u16 | static_d u16        (static_d at byte 19)
+//   | grid: D u16, D x f64 | params hash 8 | [vqvae: model hash 8]
+//   | [vqvae: idx table: total u32, L x u32 wire sizes, L x u16 states]
+//   | residual table (same) | [flags&1: schedule crc u32]
+//   | idx lane blobs | residual lane blobs | crc32 u32 over all of the above
+// A lane blob is the BitStack wire form (bits.py:66-87): u64 LE bit count,
+// then ceil(nbits/8) payload bytes, tail bits zero.
+
+#include <math.h>
+#include <string.h>
+
+#include "common.cuh"
+
+// ---------------------------------------------------------------------------
+const CrcConsts &crc_consts() {
+    static CrcConsts cc;
+    static bool init = false;
+    if (!init) {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c & 1) ? (c >> 1) ^ 0xEDB88320u : c >> 1;
+            cc.tab[i] = c;
+        }
+        uint32_t p = 1u << 30;  // x^1
+        for (int k = 0; k < 32; ++k) {
+            cc.x2n[k] = p;
+            p = crc_multmodp(p, p);
+        }
+        const uint32_t q = cc.x2n[9];  // x^512 = x^(8*64)
+        cc.qpow[0] = 1u << 31;
+        for (int j = 1; j <= 32; ++j) cc.qpow[j] = crc_multmodp(cc.qpow[j - 1], q);
+        init = true;
+    }
+    return cc;
+}
+
+namespace {
+
+constexpr int kWarps = 4;  // warps per block for warp-per-blob kernels
+constexpr int kStage = 32 * 68 + 64;
+
+__device__ __forceinline__ uint32_t rd_u16(const uint8_t *p) { return p[0] | (p[1] << 8); }
+__device__ __forceinline__ uint32_t rd_u32(const uint8_t *p) {
+    return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+__device__ __forceinline__ uint64_t rd_u64(const uint8_t *p) {
+    return (uint64_t)rd_u32(p) | ((uint64_t)rd_u32(p + 4) << 32);
+}
+__device__ __forceinline__ void wr_u16(uint8_t *p, uint32_t v) {
+    p[0] = v & 0xFF;
+    p[1] = (v >> 8) & 0xFF;
+}
+__device__ __forceinline__ void wr_u32(uint8_t *p, uint32_t v) {
+    p[0] = v & 0xFF;
+    p[1] = (v >> 8) & 0xFF;
+    p[2] = (v >> 16) & 0xFF;
+    p[3] = v >> 24;
+}
+
+// ---- static scale (container.py:163-170) ---------------------------------
+// Block per image: exact integer sum of |t - 128|; then the reference's f64
+// formula  argmin_j |log2(mad / ln 4) - log2 g_j|  (ties to smaller j).
+__global__ void static_scale_kernel(const uint8_t *__restrict__ res, int64_t n_sym,
+                                    const double *__restrict__ log2g, int D,
+                                    uint16_t *__restrict__ d_img) {
+    const int64_t img = blockIdx.x;
+    const uint8_t *t = res + img * n_sym;
+    unsigned long long s = 0;
+    for (int64_t i = threadIdx.x; i < n_sym; i += blockDim.x) {
+        const int v = (int)t[i] - 128;
+        s += (unsigned long long)(v < 0 ? -v : v);
+    }
+    __shared__ unsigned long long red[32];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+        // np.mean over float64 values: pairwise summation of exact small
+        // integers is exact, so mean = tot / n correctly rounded.
+        const double mad = (double)tot / (double)n_sym;
+        const double s_est = mad / 1.3862943611198906;  // np.log(4.0), correctly rounded
+        int best = 0;
+        if (s_est > 0) {
+            const double l2 = log2(s_est);
+            double bd = fabs(l2 - log2g[0]);
+            for (int j = 1; j < D; ++j) {
+                const double dj = fabs(l2 - log2g[j]);
+                if (dj < bd) {
+                    bd = dj;
+                    best = j;
+                }
+            }
+        }
+        d_img[img] = (uint16_t)best;
+    }
+}
+
+// ---- sizes -----------------------------------------------------------------
+__global__ void blob_sizes_kernel(const uint32_t *__restrict__ idx_nbits,
+                                  const uint32_t *__restrict__ res_nbits, int64_t n_img,
+                                  int lanes, int64_t fixed_bytes, uint64_t *__restrict__ sizes) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t img = (int64_t)blockIdx.x * kWarps + warp; img < n_img;
+         img += (int64_t)gridDim.x * kWarps) {
+        uint64_t s = 0;
+        for (int l = lane; l < lanes; l += 32) {
+            s += 8 + (((uint64_t)res_nbits[img * lanes + l] + 7) >> 3);
+            if (idx_nbits) s += 8 + (((uint64_t)idx_nbits[img * lanes + l] + 7) >> 3);
+        }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) sizes[img] = s + (uint64_t)fixed_bytes;
+    }
+}
+
+// single-block exclusive scan of n sizes into off[0..n]
+__global__ void scan_kernel(const uint64_t *__restrict__ sizes, int64_t n, uint64_t *__restrict__ off) {
+    __shared__ uint64_t part[1024];
+    const int t = threadIdx.x, T = blockDim.x;
+    const int64_t per = (n + T - 1) / T;
+    const int64_t b = t * per, e = b + per < n ? b + per : n;
+    uint64_t s = 0;
+    for (int64_t i = b; i < e; ++i) s += sizes[i];
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < T; o <<= 1) {
+        uint64_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint64_t run = t ? part[t - 1] : 0;
+    for (int64_t i = b; i < e; ++i) {
+        off[i] = run;
+        run += sizes[i];
+    }
+    if (t == T - 1) off[n] = part[T - 1];
+}
+
+// ---- pack -----------------------------------------------------------------
+struct PackArgs {
+    const uint16_t *d_img;
+    const uint8_t *dsched;
+    int sched_check;
+    int64_t n_img, n_sym;
+    int lanes;
+    const uint32_t *idx_scratch;
+    int64_t idx_cap;
+    const uint32_t *idx_nbits;
+    const uint16_t *idx_states;
+    const uint32_t *res_scratch;
+    int64_t res_cap;
+    const uint32_t *res_nbits;
+    const uint16_t *res_states;
+    const uint64_t *blob_off;
+    uint8_t *out;
+    const uint8_t *tmpl;  // device copy of the header prefix
+    int tmpl_len;
+};
+
+// Copy one lane blob (u64 nbits + payload bytes from 32-bit scratch words).
+__device__ void put_lane(uint8_t *dst, const uint32_t *words, uint32_t nbits, int lane) {
+    const uint32_t nbytes = (nbits + 7) >> 3;
+    if (lane < 8) dst[lane] = lane < 4 ? (nbits >> (8 * lane)) & 0xFF : 0;
+    for (uint32_t j = lane; j < nbytes; j += 32) {
+        uint32_t v = (words[j >> 2] >> (8 * (j & 3))) & 0xFF;
+        if (j == nbytes - 1 && (nbits & 7)) v &= (1u << (nbits & 7)) - 1;  // tail bits zero
+        dst[8 + j] = (uint8_t)v;
+    }
+}
+
+// Writes one stream table and returns its length.
+__device__ int put_table(uint8_t *dst, const uint32_t *nbits, const uint16_t *states, int lanes,
+                         int lane) {
+    uint64_t tot = 0;
+    for (int l = lane; l < lanes; l += 32) {
+        const uint32_t w = 8 + ((nbits[l] + 7) >> 3);
+        tot += w;
+        wr_u32(dst + 4 + 4 * l, w);
+        wr_u16(dst + 4 + 4 * lanes + 2 * l, states[l]);
+    }
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) wr_u32(dst, (uint32_t)tot);
+    return 4 + 6 * lanes;
+}
+
+__device__ uint32_t sched_crc_warp(const CrcConsts *cc, const uint8_t *dsched, uint32_t dconst,
+                                   int64_t n_sym, uint8_t *stage) {
+    // crc32 over n_sym u16 LE values; stage them two bytes at a time
+    const int lane = threadIdx.x & 31;
+    uint32_t crc = 0;
+    const int64_t nbytes = 2 * n_sym;
+    int64_t done = 0;
+    while (done < nbytes) {
+        const int64_t rem = nbytes - done;
+        const int rb = rem >= 2048 ? 2048 : (int)rem;
+        for (int j = lane; j < rb; j += 32) {
+            const int64_t bi = done + j;
+            const uint32_t d = dsched ? dsched[bi >> 1] : dconst;
+            stage[(j >> 6) * 68 + (j & 63)] = (bi & 1) ? (uint8_t)(d >> 8) : (uint8_t)(d & 0xFF);
+        }
+        __syncwarp();
+        const int beg = lane * 64;
+        int len = rb - beg;
+        len = len < 0 ? 0 : (len > 64 ? 64 : len);
+        const uint32_t c = crc_bytes(cc->tab, stage + lane * 68, len);
+        uint32_t term;
+        if (rb == 2048) {
+            term = crc_multmodp(cc->qpow[31 - lane], c);
+        } else {
+            const int kl = (rb - 1) >> 6;
+            const int r = rb - 64 * kl;
+            if (lane > kl) term = 0;
+            else if (lane == kl) term = c;
+            else term = crc_multmodp(crc_multmodp(cc->qpow[kl - lane - 1], crc_x2nmodp(cc->x2n, r, 3)), c);
+        }
+        const uint32_t rc = warp_xor(term);
+        crc = (rb == 2048) ? (crc_multmodp(cc->qpow[32], crc) ^ rc)
+                           : (crc_multmodp(crc_x2nmodp(cc->x2n, rb, 3), crc) ^ rc);
+        done += rb;
+        __syncwarp();
+    }
+    return crc;
+}
+
+__global__ void __launch_bounds__(32 * kWarps) pack_kernel(PackArgs a, CrcConsts ccv) {
+    __shared__ CrcConsts cc;
+    __shared__ uint8_t stage[kWarps][kStage];
+    load_crc_consts(&cc, ccv);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = a.lanes;
+    for (int64_t img = (int64_t)blockIdx.x * kWarps + warp; img < a.n_img;
+         img += (int64_t)gridDim.x * kWarps) {
+        uint8_t *blob = a.out + a.blob_off[img];
+        const uint64_t size = a.blob_off[img + 1] - a.blob_off[img];
+        for (int i = lane; i < a.tmpl_len; i += 32) blob[i] = a.tmpl[i];
+        __syncwarp();
+        const uint32_t sd = a.d_img ? a.d_img[img] : 0u;
+        if (lane == 0) wr_u16(blob + 19, sd);
+        int64_t off = a.tmpl_len;
+        if (a.idx_nbits)
+            off += put_table(blob + off, a.idx_nbits + img * L, a.idx_states + img * L, L, lane);
+        off += put_table(blob + off, a.res_nbits + img * L, a.res_states + img * L, L, lane);
+        if (a.sched_check) {
+            const uint32_t c = sched_crc_warp(&cc, a.dsched ? a.dsched + img * a.n_sym : nullptr, sd,
+                                              a.n_sym, stage[warp]);
+            if (lane == 0) wr_u32(blob + off, c);
+            off += 4;
+        }
+        // lane blobs: each warp walks lanes in order, sizes are known
+        for (int s = 0; s < 2; ++s) {
+            const uint32_t *nb = s == 0 ? a.idx_nbits : a.res_nbits;
+            if (!nb) continue;
+            const uint32_t *scr = s == 0 ? a.idx_scratch : a.res_scratch;
+            const int64_t cap = s == 0 ? a.idx_cap : a.res_cap;
+            for (int l = 0; l < L; ++l) {
+                const uint32_t bits = nb[img * L + l];
+                put_lane(blob + off, scr + (img * L + l) * cap, bits, lane);
+                off += 8 + ((bits + 7) >> 3);
+            }
+        }
+        __syncwarp();
+        __threadfence_block();
+        const uint32_t crc = warp_crc32(&cc, blob, size - 4, stage[warp]);
+        if (lane == 0) wr_u32(blob + size - 4, crc);
+    }
+}
+
+// ---- parse (container.py:195-258) ----------------------------------------
+__global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__restrict__ buf,
+                                                            const uint64_t *__restrict__ blob_off,
+                                                            int64_t n_blob, uint64_t params_hash,
+                                                            uint64_t model_hash, int has_model,
+                                                            pilc_header *hdr, CrcConsts ccv) {
+    __shared__ CrcConsts cc;
+    __shared__ uint8_t stage[kWarps][kStage];
+    load_crc_consts(&cc, ccv);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < n_blob;
+         i += (int64_t)gridDim.x * kWarps) {
+        const uint8_t *b = buf + blob_off[i];
+        const uint64_t n = blob_off[i + 1] - blob_off[i];
+        pilc_header h;
+        memset(&h, 0, sizeof(h));
+        int st = 0;
+        if (n < 8) st = PILC_ST_TRUNCATED;
+        else if (b[0] != 'P' || b[1] != 'I' || b[2] != 'L' || b[3] != 'C') st = PILC_ST_BAD_MAGIC;
+        else if (b[4] != 1) {
+            st = PILC_ST_BAD_VERSION;
+            h.aux = b[4];
+        }
+        if (!st) {
+            const uint32_t crc = warp_crc32(&cc, b, n - 4, stage[warp]);
+            if (crc != rd_u32(b + n - 4)) st = PILC_ST_CRC;
+        }
+        // sequential structure walk (lane 0), mirroring _Reader.take
+        uint64_t off = 5;
+        auto need = [&](uint64_t k) { return off + k <= n; };
+        if (!st && lane == 0) {
+            if (!need(4)) st = PILC_ST_TRUNCATED;
+            if (!st) {
+                h.backend = b[5];
+                h.M = b[6];
+                h.pad_rule = b[7];
+                h.flags = b[8];
+                off = 9;
+                if (h.backend > 1) {
+                    st = PILC_ST_BAD_BACKEND;
+                    h.aux = h.backend;
+                } else if (h.M < 10 || h.M > 12) st = PILC_ST_BAD_M;
+                else if (h.pad_rule != 0) st = PILC_ST_BAD_PAD;
+                else if (h.flags & ~1u) st = PILC_ST_BAD_FLAGS;
+            }
+            if (!st) {
+                if (!need(12)) st = PILC_ST_TRUNCATED;
+                else {
+                    h.width = rd_u32(b + 9);
+                    h.height = rd_u32(b + 13);
+                    h.lanes = rd_u16(b + 17);
+                    h.static_d = rd_u16(b + 19);
+                    off = 21;
+                    if (h.width < 1 || h.height < 1 || h.lanes < 1) st = PILC_ST_BAD_DIMS;
+                }
+            }
+            if (!st) {
+                if (n - off < 2) st = PILC_ST_GRID_TRUNC;
+                else {
+                    h.D = rd_u16(b + off);
+                    if (off + 2 + 8ull * h.D > n) st = PILC_ST_GRID_TRUNC;
+                    else off += 2 + 8ull * h.D;
+                }
+            }
+            // ScaleGrid validation (logistic.py:52-64), same IEEE f64 ops
+            if (!st) {
+                const uint8_t *g = b + 23;
+                const int D = h.D;
+                if (D < 1) st = PILC_ST_GRID_EMPTY;
+                for (int k = 0; !st && k < D; ++k) {
+                    const double v = __longlong_as_double((long long)rd_u64(g + 8 * k));
+                    if (!isfinite(v) || v <= 0.0) st = PILC_ST_GRID_VALUE;
+                }
+                for (int k = 1; !st && k < D; ++k) {
+                    const double a0 = __longlong_as_double((long long)rd_u64(g + 8 * (k - 1)));
+                    const double a1 = __longlong_as_double((long long)rd_u64(g + 8 * k));
+                    if (!(a1 - a0 > 0.0)) st = PILC_ST_GRID_ORDER;
+                }
+                if (!st && D > 2) {
+                    const double r0 = __longlong_as_double((long long)rd_u64(g + 8)) /
+                                      __longlong_as_double((long long)rd_u64(g));
+                    double mx = 0.0;
+                    for (int k = 1; k + 1 < D; ++k) {
+                        const double r = __longlong_as_double((long long)rd_u64(g + 8 * (k + 1))) /
+                                         __longlong_as_double((long long)rd_u64(g + 8 * k));
+                        mx = fmax(mx, fabs(r - r0));
+                    }
+                    if (mx > 1e-9 * r0) st = PILC_ST_GRID_GEOM;
+                }
+                uint32_t c = 0xFFFFFFFFu;
+                for (int k = 0; k < 2 + 8 * D; ++k) c = cc.tab[(c ^ b[21 + k]) & 0xFF] ^ (c >> 8);
+                h.grid_crc = c ^ 0xFFFFFFFFu;
+            }
+            if (!st && h.static_d >= h.D) st = PILC_ST_STATIC_D;
+            if (!st) {
+                if (!need(8)) st = PILC_ST_TRUNCATED;
+                else {
+                    h.params_hash_off = (uint32_t)off;
+                    off += 8;
+                }
+            }
+            const uint32_t L = h.lanes;
+            if (!st && h.backend == 1) {
+                if (!need(8)) st = PILC_ST_TRUNCATED;
+                else {
+                    h.model_hash_off = (uint32_t)off;
+                    off += 8;
+                }
+                if (!st) {
+                    if (!need(4 + 4ull * L + 2ull * L)) st = PILC_ST_TRUNCATED;
+                    else {
+                        h.idx_table_off = (uint32_t)off;
+                        const uint32_t tot = rd_u32(b + off);
+                        uint64_t s = 0;
+                        for (uint32_t l = 0; l < L; ++l) s += rd_u32(b + off + 4 + 4 * l);
+                        h.idx_bytes = s;
+                        off += 4 + 6ull * L;
+                        if (s != tot) st = PILC_ST_IDX_LENS;
+                    }
+                }
+            }
+            if (!st) {
+                if (!need(4 + 6ull * L)) st = PILC_ST_TRUNCATED;
+                else {
+                    h.res_table_off = (uint32_t)off;
+                    const uint32_t tot = rd_u32(b + off);
+                    uint64_t s = 0;
+                    for (uint32_t l = 0; l < L; ++l) s += rd_u32(b + off + 4 + 4 * l);
+                    h.res_bytes = s;
+                    off += 4 + 6ull * L;
+                    if (s != tot) st = PILC_ST_RES_LENS;
+                }
+            }
+            if (!st && (h.flags & 1)) {
+                if (!need(4)) st = PILC_ST_TRUNCATED;
+                else {
+                    h.sched_crc = rd_u32(b + off);
+                    off += 4;
+                }
+            }
+            if (!st) {
+                h.payload_off = (uint32_t)off;
+                if (off + h.idx_bytes + h.res_bytes + 4 != n) st = PILC_ST_PAYLOAD_LEN;
+            }
+            // container.py:288-304: predictor hash, then model hash
+            if (!st && rd_u64(b + h.params_hash_off) != params_hash) st = PILC_ST_PARAMS_HASH;
+            if (!st && h.backend == 1 && has_model && rd_u64(b + h.model_hash_off) != model_hash)
+                st = PILC_ST_MODEL_HASH;
+        }
+        st = __shfl_sync(0xffffffffu, st, 0);
+        if (lane == 0) {
+            h.status = st;
+            hdr[i] = h;
+        }
+    }
+}
+
+// ---- lanes (container.py:261-271, bits.py:75-85) -------------------------
+__global__ void lanes_kernel(const uint8_t *__restrict__ buf, const uint64_t *__restrict__ blob_off,
+                             const pilc_header *__restrict__ hdr, const int64_t *__restrict__ blob_idx,
+                             int64_t n_group, int lanes, int stream_id, uint64_t *__restrict__ lane_off,
+                             uint32_t *__restrict__ nbits, uint16_t *__restrict__ states,
+                             uint8_t *__restrict__ lane_status) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t g = (int64_t)blockIdx.x * kWarps + warp; g < n_group;
+         g += (int64_t)gridDim.x * kWarps) {
+        const int64_t bi = blob_idx[g];
+        const pilc_header h = hdr[bi];
+        const uint8_t *b = buf + blob_off[bi];
+        const uint32_t M = h.M;
+        const uint32_t tab = stream_id == 0 ? h.idx_table_off : h.res_table_off;
+        uint64_t start = h.payload_off + (stream_id == 0 ? 0 : h.idx_bytes);
+        const bool ok = h.status == 0 && tab != 0;
+        // lane wire sizes -> running offsets, 32 lanes at a time
+        for (int l0 = 0; l0 < lanes; l0 += 32) {
+            const int l = l0 + lane;
+            uint32_t wsz = 0;
+            if (ok && l < lanes) wsz = rd_u32(b + tab + 4 + 4 * l);
+            // inclusive scan of wsz over the warp
+            uint64_t inc = wsz;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
+            }
+            const uint64_t my = start + inc - wsz;
+            if (l < lanes) {
+                const int64_t k = g * lanes + l;
+                uint8_t st = 0;
+                uint64_t nb = 0;
+                uint32_t s = 0;
+                if (!ok) st = PILC_ST_TRUNCATED;
+                else if (wsz < 8) st = PILC_ST_LANE_HDR;
+                else {
+                    nb = rd_u64(b + my);
+                    const uint64_t need = 8 + ((nb + 7) >> 3);
+                    if (nb >= (1ull << 32) || need > wsz) st = need > wsz ? PILC_ST_LANE_TRUNC : PILC_ST_LANE_LEN;
+                    else if (need != wsz) st = PILC_ST_LANE_LEN;
+                }
+                if (ok) s = rd_u16(b + tab + 4 + 4 * lanes + 2 * l);
+                if (!st && !(s >= (1u << M) && s < (2u << M))) st = PILC_ST_STATE_RANGE;
+                lane_off[k] = blob_off[bi] + my + 8;
+                nbits[k] = (uint32_t)nb;
+                states[k] = (uint16_t)s;
+                lane_status[k] = st;
+            }
+            start += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32 * kWarps) crc_kernel(const uint8_t *__restrict__ buf,
+                                                          const uint64_t *__restrict__ off,
+                                                          const uint64_t *__restrict__ len, int64_t n,
+                                                          uint32_t *__restrict__ out, CrcConsts ccv) {
+    __shared__ CrcConsts cc;
+    __shared__ uint8_t stage[kWarps][kStage];
+    load_crc_consts(&cc, ccv);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < n; i += (int64_t)gridDim.x * kWarps) {
+        const uint32_t c = warp_crc32(&cc, buf + off[i], len[i], stage[warp]);
+        if (lane == 0) out[i] = c;
+    }
+}
+
+__global__ void __launch_bounds__(32 * kWarps) sched_crc_kernel(const uint8_t *__restrict__ dsched,
+                                                                const uint16_t *__restrict__ d_img,
+                                                                int64_t n_img, int64_t n_sym,
+                                                                uint32_t *__restrict__ out, CrcConsts ccv) {
+    __shared__ CrcConsts cc;
+    __shared__ uint8_t stage[kWarps][kStage];
+    load_crc_consts(&cc, ccv);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < n_img; i += (int64_t)gridDim.x * kWarps) {
+        const uint32_t c = sched_crc_warp(&cc, dsched ? dsched + i * n_sym : nullptr,
+                                          d_img ? d_img[i] : 0u, n_sym, stage[warp]);
+        if (lane == 0) out[i] = c;
+    }
+}
+
+unsigned warp_grid(int64_t n) {
+    int64_t blocks = ceil_div64(n, kWarps);
+    const int64_t cap = (int64_t)sm_count() * 16;
+    return (unsigned)(blocks > cap ? cap : (blocks < 1 ? 1 : blocks));
+}
+
+}  // namespace
+
+extern "C" int pilc_static_scale(const uint8_t *res, int64_t n_img, int64_t n_sym,
+                                 const double *log2_grid_host, int32_t D, uint16_t *d_img,
+                                 void *stream) {
+    if (n_img < 0 || n_sym < 1 || D < 1 || D > 65535 || !log2_grid_host) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    if (n_img > 0x7FFFFFFF) return PILC_E_ARG;
+    // the grid goes through a small device buffer owned by the stream order:
+    // allocate-async / free-async keeps the call stateless
+    double *g = nullptr;
+    cudaStream_t s = as_stream(stream);
+    if (cudaMallocAsync(&g, sizeof(double) * D, s) != cudaSuccess) return PILC_E_CUDA;
+    cudaMemcpyAsync(g, log2_grid_host, sizeof(double) * D, cudaMemcpyHostToDevice, s);
+    static_scale_kernel<<<(unsigned)n_img, 256, 0, s>>>(res, n_sym, g, D, d_img);
+    cudaFreeAsync(g, s);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_container_sizes(const uint32_t *idx_nbits, const uint32_t *res_nbits,
+                                    int64_t n_img, int32_t lanes, int64_t fixed_bytes,
+                                    uint64_t *blob_off, void *stream) {
+    if (n_img < 0 || lanes < 1 || !res_nbits || !blob_off) return PILC_E_ARG;
+    cudaStream_t s = as_stream(stream);
+    if (n_img == 0) {
+        cudaMemsetAsync(blob_off, 0, sizeof(uint64_t), s);
+        PILC_CHECK_LAUNCH();
+        return PILC_OK;
+    }
+    // sizes land in blob_off[1..n], then scan in place into a temp
+    uint64_t *sizes = nullptr;
+    if (cudaMallocAsync(&sizes, sizeof(uint64_t) * n_img, s) != cudaSuccess) return PILC_E_CUDA;
+    blob_sizes_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(idx_nbits, res_nbits, n_img, lanes,
+                                                               fixed_bytes, sizes);
+    scan_kernel<<<1, 1024, 0, s>>>(sizes, n_img, blob_off);
+    cudaFreeAsync(sizes, s);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_container_pack(const uint8_t *template_host, int32_t template_len,
+                                   const uint16_t *d_img, const uint8_t *dsched, int32_t sched_check,
+                                   int64_t n_img, int64_t n_sym, int32_t lanes,
+                                   const uint32_t *idx_scratch, int64_t idx_cap,
+                                   const uint32_t *idx_nbits, const uint16_t *idx_states,
+                                   const uint32_t *res_scratch, int64_t res_cap,
+                                   const uint32_t *res_nbits, const uint16_t *res_states,
+                                   const uint64_t *blob_off, uint8_t *out, void *stream) {
+    if (n_img < 0 || lanes < 1 || template_len < 21 || !template_host || !res_nbits) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    cudaStream_t s = as_stream(stream);
+    uint8_t *tmpl = nullptr;
+    if (cudaMallocAsync(&tmpl, template_len, s) != cudaSuccess) return PILC_E_CUDA;
+    cudaMemcpyAsync(tmpl, template_host, template_len, cudaMemcpyHostToDevice, s);
+    PackArgs a{d_img,     dsched,      sched_check, n_img,      n_sym,      lanes,
+               idx_scratch, idx_cap,   idx_nbits,   idx_states, res_scratch, res_cap,
+               res_nbits, res_states,  blob_off,    out,        tmpl,       template_len};
+    pack_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(a, crc_consts());
+    cudaFreeAsync(tmpl, s);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_container_parse(const uint8_t *buf, const uint64_t *blob_off, int64_t n_blob,
+                                    uint64_t params_hash, uint64_t model_hash, int32_t has_model,
+                                    pilc_header *hdr, void *stream) {
+    if (n_blob < 0 || !blob_off || !hdr) return PILC_E_ARG;
+    if (n_blob == 0) return PILC_OK;
+    parse_kernel<<<warp_grid(n_blob), 32 * kWarps, 0, as_stream(stream)>>>(
+        buf, blob_off, n_blob, params_hash, model_hash, has_model, hdr, crc_consts());
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_container_lanes(const uint8_t *buf, const uint64_t *blob_off,
+                                    const pilc_header *hdr, const int64_t *blob_idx, int64_t n_group,
+                                    int32_t lanes, int32_t stream_id, uint64_t *lane_off,
+                                    uint32_t *nbits, uint16_t *states, uint8_t *lane_status,
+                                    void *stream) {
+    if (n_group < 0 || lanes < 1 || (stream_id != 0 && stream_id != 1)) return PILC_E_ARG;
+    if (n_group == 0) return PILC_OK;
+    lanes_kernel<<<warp_grid(n_group), 32 * kWarps, 0, as_stream(stream)>>>(
+        buf, blob_off, hdr, blob_idx, n_group, lanes, stream_id, lane_off, nbits, states, lane_status);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_crc32(const uint8_t *buf, const uint64_t *off, const uint64_t *len, int64_t n,
+                          uint32_t *crc, void *stream) {
+    if (n < 0) return PILC_E_ARG;
+    if (n == 0) return PILC_OK;
+    crc_kernel<<<warp_grid(n), 32 * kWarps, 0, as_stream(stream)>>>(buf, off, len, n, crc, crc_consts());
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_sched_crc(const uint8_t *dsched, const uint16_t *d_img, int64_t n_img,
+                              int64_t n_sym, uint32_t *crc, void *stream) {
+    if (n_img < 0 || n_sym < 0) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    sched_crc_kernel<<<warp_grid(n_img), 32 * kWarps, 0, as_stream(stream)>>>(dsched, d_img, n_img, n_sym,
+                                                                             crc, crc_consts());
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}

@@ -1,0 +1,202 @@
+// TWAR three-neighbour predictor: forward residual and wavefront inverse.
+//
+// Numeric contract (_kernels.py:69-88, predictor.py:106-111, 183-190):
+// acc = w0*c0; acc += w1*c1; acc += w2*c2; acc += bias, all float32 with no
+// FMA contraction (explicit __fmul_rn/__fadd_rn), then round half away from
+// zero in float64 and reduce mod 256. Out-of-image context reads as 0.
+//   R: (up-left, up, left)       G: (left, R-left, R-here)
+//   B: (left, G-left, G-here)    (predictor.py:36-40)
+
+#include "common.cuh"
+
+namespace {
+
+struct Params {
+    float w[9];
+    float b[3];
+};
+
+__device__ __forceinline__ uint32_t round_mod256(float acc) {
+    const double p = (double)acc;
+    const double r = p >= 0.0 ? floor(p + 0.5) : ceil(p - 0.5);
+    if (fabs(r) < 4.0e18) return (uint32_t)((long long)r & 255LL);
+    double m = fmod(r, 256.0);
+    if (m < 0.0) m += 256.0;
+    return (uint32_t)m;
+}
+
+__device__ __forceinline__ uint32_t predict(float c0, float c1, float c2, const float *w, float b) {
+    float acc = __fmul_rn(w[0], c0);
+    acc = __fadd_rn(acc, __fmul_rn(w[1], c1));
+    acc = __fadd_rn(acc, __fmul_rn(w[2], c2));
+    acc = __fadd_rn(acc, b);
+    return round_mod256(acc);
+}
+
+// One thread per pixel, all three channels (predictor.py:173-195).
+__global__ void twar_forward_kernel(const uint8_t *__restrict__ img, uint8_t *__restrict__ res,
+                                    int64_t n_px, int H, int W, Params p) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_px;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t hw = (int64_t)H * W;
+        const int64_t n = g / hw;
+        const int rem = (int)(g - n * hw);
+        const int u = rem / W, v = rem - (rem / W) * W;
+        const uint8_t *x = img + n * hw * 3;
+        const int64_t o = (int64_t)rem * 3;
+        const float r = x[o], gg = x[o + 1], bb = x[o + 2];
+        float rl = 0.f, gl = 0.f, bl = 0.f, ru = 0.f, rul = 0.f;
+        if (v > 0) {
+            rl = x[o - 3];
+            gl = x[o - 2];
+            bl = x[o - 1];
+        }
+        if (u > 0) {
+            ru = x[o - 3 * W];
+            if (v > 0) rul = x[o - 3 * W - 3];
+        }
+        const uint32_t pr = predict(rul, ru, rl, p.w, p.b[0]);
+        const uint32_t pg = predict(gl, rl, r, p.w + 3, p.b[1]);
+        const uint32_t pb = predict(bl, gl, gg, p.w + 6, p.b[2]);
+        uint8_t *t = res + n * hw * 3 + o;
+        t[0] = (uint8_t)(((uint32_t)r - pr + 128u) & 0xFFu);
+        t[1] = (uint8_t)(((uint32_t)gg - pg + 128u) & 0xFFu);
+        t[2] = (uint8_t)(((uint32_t)bb - pb + 128u) & 0xFFu);
+    }
+}
+
+// Inverse (_kernels.py:146-170 wavefront schedule). One warp per image;
+// the image is staged in shared memory when it fits, else decoded in place
+// in the output buffer. Red: lanes take rows 32s..32s+31 of strip s and
+// march a skewed wavefront (lane u handles column step - u), receiving the
+// up / up-left values from lane u-1 by shuffle. Green, blue: rows are
+// independent; each lane owns rows lane, lane+32, ... and walks columns.
+constexpr int kDecWarps = 4;
+
+__device__ __forceinline__ uint32_t unrec(const uint8_t *coded, const uint8_t *shift, int64_t i) {
+    uint32_t t = coded[i];
+    if (shift) t = (t + shift[i] + 128u) & 0xFFu;
+    return t;
+}
+
+__global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
+    const uint8_t *__restrict__ coded, const uint8_t *__restrict__ shift, uint8_t *__restrict__ out,
+    int64_t n_img, int H, int W, Params p, int stage_in_smem) {
+    extern __shared__ uint8_t s_img[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t hw3 = (int64_t)H * W * 3;
+    for (int64_t n = (int64_t)blockIdx.x * kDecWarps + warp; n < n_img;
+         n += (int64_t)gridDim.x * kDecWarps) {
+        const uint8_t *cd = coded + n * hw3;
+        const uint8_t *sh = shift ? shift + n * hw3 : nullptr;
+        uint8_t *o_g = out + n * hw3;
+        uint8_t *o = stage_in_smem ? s_img + (int64_t)warp * hw3 : o_g;
+        // ---- red: skewed wavefront per strip of 32 rows
+        for (int u0 = 0; u0 < H; u0 += 32) {
+            const int u = u0 + lane;
+            const bool row_ok = u < H;
+            float left = 0.f;      // out[u][v-1][0]
+            float up_prev = 0.f;   // value lane-1 produced one step ago (= out[u-1][v])
+            float up_prev2 = 0.f;  // two steps ago (= out[u-1][v-1])
+            float mine_prev = 0.f; // what this lane produced last step
+            float mine_prev2 = 0.f;
+            const int steps = W + 31;
+            for (int s = 0; s < steps; ++s) {
+                // neighbours from lane-1: its outputs at steps s-1 and s-2
+                const float nb1 = __shfl_up_sync(0xffffffffu, mine_prev, 1);
+                const float nb2 = __shfl_up_sync(0xffffffffu, mine_prev2, 1);
+                const int v = s - lane;
+                float val = 0.f;
+                if (row_ok && v >= 0 && v < W) {
+                    float up, ul;
+                    if (lane == 0) {
+                        up = u > 0 ? (float)o[((int64_t)(u - 1) * W + v) * 3] : 0.f;
+                        ul = (u > 0 && v > 0) ? (float)o[((int64_t)(u - 1) * W + v - 1) * 3] : 0.f;
+                    } else {
+                        up = nb1;
+                        ul = v > 0 ? nb2 : 0.f;
+                    }
+                    const float lf = v > 0 ? left : 0.f;
+                    const uint32_t pr = predict(ul, up, lf, p.w, p.b[0]);
+                    const int64_t i = ((int64_t)u * W + v) * 3;
+                    const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;  // t - 128 + pred
+                    o[i] = (uint8_t)x;
+                    val = (float)x;
+                    left = val;
+                }
+                up_prev2 = up_prev;
+                up_prev = nb1;
+                mine_prev2 = mine_prev;
+                mine_prev = val;
+            }
+            __syncwarp();
+        }
+        // ---- green then blue: rows independent
+        for (int c = 1; c < 3; ++c) {
+            for (int u = lane; u < H; u += 32) {
+                float left = 0.f, pleft = 0.f;
+                const int64_t row = (int64_t)u * W * 3;
+                for (int v = 0; v < W; ++v) {
+                    const int64_t i = row + (int64_t)v * 3 + c;
+                    const float here = o[i - 1];
+                    const uint32_t pr = predict(left, pleft, here, p.w + 3 * c, p.b[c]);
+                    const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;
+                    o[i] = (uint8_t)x;
+                    left = (float)x;
+                    pleft = here;
+                }
+            }
+            __syncwarp();
+        }
+        if (stage_in_smem) {
+            // coalesced copy-out, 4 bytes per lane when aligned
+            for (int64_t i = lane; i < hw3; i += 32) o_g[i] = o[i];
+            __syncwarp();
+        }
+    }
+}
+
+Params load_params(const float *p12) {
+    Params p;
+    for (int c = 0; c < 3; ++c) {
+        for (int j = 0; j < 3; ++j) p.w[3 * c + j] = p12[4 * c + j];
+        p.b[c] = p12[4 * c + 3];
+    }
+    return p;
+}
+
+}  // namespace
+
+extern "C" int pilc_twar_forward(const uint8_t *img, uint8_t *res, int64_t n_img, int32_t H,
+                                 int32_t W, const float *params12_host, void *stream) {
+    if (n_img < 0 || H < 1 || W < 1 || !params12_host) return PILC_E_ARG;
+    const int64_t n_px = n_img * (int64_t)H * W;
+    if (n_px == 0) return PILC_OK;
+    const int threads = 256;
+    int64_t blocks = ceil_div64(n_px, threads);
+    const int64_t cap = (int64_t)sm_count() * 32;
+    if (blocks > cap) blocks = cap;
+    twar_forward_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
+        img, res, n_px, H, W, load_params(params12_host));
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_twar_decode(const uint8_t *coded, const uint8_t *shift, uint8_t *img,
+                                int64_t n_img, int32_t H, int32_t W, const float *params12_host,
+                                void *stream) {
+    if (n_img < 0 || H < 1 || W < 1 || !params12_host) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    const int64_t hw3 = (int64_t)H * W * 3;
+    const int stage = hw3 * kDecWarps <= 200 * 1024;
+    const size_t smem = stage ? (size_t)(hw3 * kDecWarps) : 0;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(twar_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t blocks = ceil_div64(n_img, kDecWarps);
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    twar_decode_kernel<<<(unsigned)blocks, 32 * kDecWarps, smem, as_stream(stream)>>>(
+        coded, shift, img, n_img, H, W, load_params(params12_host), stage);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}

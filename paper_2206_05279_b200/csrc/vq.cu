@@ -1,0 +1,572 @@
+// VQ-VAE inference on sm_100a: encoder -> codebook argmin, and decoder ->
+// logistic head (shift = round(mu), d = scale-grid index) per subpixel.
+//
+// Reference: vqvae.encode_to_indices / decode_to_params (vqvae.py:51-113)
+// over nn.conv2d / residual_block / pixel_shuffle / sigmoid (nn.py:15-67).
+// Activations are NHWC float32 in HBM between layers; every conv is one
+// launch of conv_kernel: a CTA owns a 16x16 output tile of one image and a
+// chunk of output channels; input patches (with edge-replicate clamping,
+// which also realises vqvae._even_pad) and weights are staged through
+// shared memory 8 input channels at a time. Epilogues fuse bias, residual,
+// ReLU, pixel shuffle and the whole logistic head. Fixed per-image tiling
+// and accumulation order: outputs are bit-identical for any batch size,
+// which is what makes GPU-compressed blobs decode on any GPU.
+
+#include <math.h>
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kTile = 16;      // output tile edge
+constexpr int kThreads = 128;  // 16 cols x 8 row-pairs
+constexpr int kCK = 8;         // input channels per smem chunk
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// ---- model layout --------------------------------------------------------
+struct ConvSpec {
+    int ci, co, ks;
+    int ci_pad, co_t, co_pad;
+    int64_t w_off, b_off;  // float offsets into the packed model
+};
+
+struct Layout {
+    int K, Dc, C, B;
+    std::vector<ConvSpec> enc;  // stem, down, blocks(2B), proj
+    std::vector<ConvSpec> dec;  // proj, blocks(2B), up, head(mu|s)
+    int64_t cb_off;             // K x Dc float32 codebook
+    int64_t total;
+};
+
+ConvSpec make_spec(int ci, int co, int ks, int64_t &cursor) {
+    ConvSpec s;
+    s.ci = ci;
+    s.co = co;
+    s.ks = ks;
+    s.ci_pad = round_up(ci, kCK);
+    s.co_t = co >= 32 ? 32 : (co > 8 ? 16 : 8);
+    s.co_pad = round_up(co, s.co_t);
+    s.w_off = cursor;
+    cursor += (int64_t)ks * ks * s.ci_pad * s.co_pad;
+    s.b_off = cursor;
+    cursor += s.co_pad;
+    return s;
+}
+
+Layout make_layout(int K, int Dc, int C, int B) {
+    Layout L;
+    L.K = K;
+    L.Dc = Dc;
+    L.C = C;
+    L.B = B;
+    int64_t cur = 0;
+    L.enc.push_back(make_spec(3, C, 3, cur));
+    L.enc.push_back(make_spec(C, C, 3, cur));
+    for (int i = 0; i < 2 * B; ++i) L.enc.push_back(make_spec(C, C, 3, cur));
+    L.enc.push_back(make_spec(C, Dc, 1, cur));
+    L.cb_off = cur;
+    cur += (int64_t)K * Dc;
+    L.dec.push_back(make_spec(Dc, C, 1, cur));
+    for (int i = 0; i < 2 * B; ++i) L.dec.push_back(make_spec(C, C, 3, cur));
+    L.dec.push_back(make_spec(C, 4 * C, 3, cur));
+    L.dec.push_back(make_spec(C, 6, 3, cur));
+    L.total = cur;
+    return L;
+}
+
+// ---- conv kernel -----------------------------------------------------------
+enum InMode { IN_F32 = 0, IN_U8 = 1, IN_CODEBOOK = 2 };
+enum OutMode { OUT_F32 = 0, OUT_SHUFFLE = 1, OUT_HEAD = 2 };
+
+struct ConvArgs {
+    const float *in;
+    const uint8_t *in_u8;   // IN_U8: image (N, src_h, src_w, 3); IN_CODEBOOK: indices
+    const float *codebook;  // IN_CODEBOOK
+    int in_mode;
+    int Hi, Wi, Ci, Ci_pad;  // logical input grid (clamp range for IN_F32/IN_CODEBOOK)
+    int src_h, src_w;        // IN_U8 clamp range (original image)
+    int Ho, Wo, Co, Co_pad;
+    int ks, stride;
+    const float *w;  // [tap][ci_pad][co_pad]
+    const float *b;  // [co_pad]
+    const float *resid;  // OUT_F32: same shape as out, added before ReLU
+    int relu;
+    float *out;
+    int out_mode;
+    int tiles_x, tiles_per_img;
+    // head
+    uint8_t *shift, *dsel;
+    float *mu, *s;
+    int crop_h, crop_w;
+    const double *thresh;
+    int n_thresh;
+    float log_s_min, log_s_max;
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__device__ __forceinline__ float sigmoid_f32(float x) {
+    // nn.py:41-48: stable two-branch form in float32
+    if (x >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-x)));
+    const float e = expf(x);
+    return __fdiv_rn(e, __fadd_rn(1.f, e));
+}
+
+template <int CO_T>
+__global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
+    extern __shared__ float smem[];
+    const int ks = a.ks, st = a.stride, pad = ks >> 1;
+    const int IR = (kTile - 1) * st + ks;  // input patch rows / cols
+    const int IC = IR + 1;                 // pitch (+1 against bank conflicts)
+    float *s_in = smem;                    // [kCK][IR][IC]
+    float *s_w = smem + kCK * IR * IC;     // [tap][kCK][CO_T]
+
+    const int tile = blockIdx.x % a.tiles_per_img;
+    const int64_t n = blockIdx.x / a.tiles_per_img;
+    const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+    const int oy0 = ty * kTile, ox0 = tx * kTile;
+    const int co0 = blockIdx.y * CO_T;
+    const int t = threadIdx.x;
+    const int col = t & 15, r0 = t >> 4;  // rows r0 and r0 + 8
+    const int iy0 = oy0 * st - pad, ix0 = ox0 * st - pad;
+
+    float acc0[CO_T], acc1[CO_T];
+#pragma unroll
+    for (int c = 0; c < CO_T; ++c) acc0[c] = acc1[c] = 0.f;
+
+    const int ntap = ks * ks;
+    for (int c0 = 0; c0 < a.Ci_pad; c0 += kCK) {
+        // stage the input patch, channel-planar
+        const int patch = IR * IR;
+        for (int e = t; e < kCK * patch; e += kThreads) {
+            const int ci = e / patch, rem = e - ci * patch;
+            const int py = rem / IR, px = rem - py * IR;
+            const int c = c0 + ci;
+            float v = 0.f;
+            if (a.in_mode == IN_F32) {
+                if (c < a.Ci) {
+                    const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
+                    v = a.in[(((int64_t)n * a.Hi + y) * a.Wi + x) * a.Ci + c];
+                }
+            } else if (a.in_mode == IN_U8) {
+                if (c < 3) {
+                    const int y = clampi(iy0 + py, 0, a.src_h - 1), x = clampi(ix0 + px, 0, a.src_w - 1);
+                    const float raw = a.in_u8[(((int64_t)n * a.src_h + y) * a.src_w + x) * 3 + c];
+                    v = __fsub_rn(__fdiv_rn(raw, 127.5f), 1.f);  // vqvae.py:41-43
+                }
+            } else {
+                if (c < a.Ci) {
+                    const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
+                    const int k = a.in_u8[((int64_t)n * a.Hi + y) * a.Wi + x];
+                    v = a.codebook[(int64_t)k * a.Ci + c];
+                }
+            }
+            s_in[(ci * IR + py) * IC + px] = v;
+        }
+        // stage weights [tap][ci][co0 .. co0+CO_T)
+        for (int e = t; e < ntap * kCK * CO_T; e += kThreads) {
+            const int tap = e / (kCK * CO_T), rem = e - tap * (kCK * CO_T);
+            const int ci = rem / CO_T, co = rem - ci * CO_T;
+            s_w[e] = a.w[((int64_t)tap * a.Ci_pad + c0 + ci) * a.Co_pad + co0 + co];
+        }
+        __syncthreads();
+        for (int ci = 0; ci < kCK; ++ci) {
+            const float *pin = s_in + ci * IR * IC;
+            for (int i = 0; i < ks; ++i) {
+                for (int j = 0; j < ks; ++j) {
+                    const float x0 = pin[(r0 * st + i) * IC + col * st + j];
+                    const float x1 = pin[((r0 + 8) * st + i) * IC + col * st + j];
+                    const float4 *wv = reinterpret_cast<const float4 *>(s_w + ((i * ks + j) * kCK + ci) * CO_T);
+#pragma unroll
+                    for (int q = 0; q < CO_T / 4; ++q) {
+                        const float4 w4 = wv[q];
+                        acc0[4 * q + 0] = fmaf(x0, w4.x, acc0[4 * q + 0]);
+                        acc0[4 * q + 1] = fmaf(x0, w4.y, acc0[4 * q + 1]);
+                        acc0[4 * q + 2] = fmaf(x0, w4.z, acc0[4 * q + 2]);
+                        acc0[4 * q + 3] = fmaf(x0, w4.w, acc0[4 * q + 3]);
+                        acc1[4 * q + 0] = fmaf(x1, w4.x, acc1[4 * q + 0]);
+                        acc1[4 * q + 1] = fmaf(x1, w4.y, acc1[4 * q + 1]);
+                        acc1[4 * q + 2] = fmaf(x1, w4.z, acc1[4 * q + 2]);
+                        acc1[4 * q + 3] = fmaf(x1, w4.w, acc1[4 * q + 3]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float *acc = h ? acc1 : acc0;
+        const int oy = oy0 + r0 + 8 * h, ox = ox0 + col;
+        if (oy >= a.Ho || ox >= a.Wo) continue;
+        if (a.out_mode == OUT_F32) {
+            const int64_t base = (((int64_t)n * a.Ho + oy) * a.Wo + ox) * a.Co;
+#pragma unroll
+            for (int c = 0; c < CO_T; ++c) {
+                const int co = co0 + c;
+                if (co >= a.Co) break;
+                float v = __fadd_rn(acc[c], a.b[co]);
+                if (a.resid) v = __fadd_rn(a.resid[base + co], v);
+                if (a.relu) v = fmaxf(v, 0.f);
+                a.out[base + co] = v;
+            }
+        } else if (a.out_mode == OUT_SHUFFLE) {
+            // nn.pixel_shuffle (nn.py:51-62): channel c*4 + dy*2 + dx of
+            // latent (u, v) lands at (2u + dy, 2v + dx), channel c; then ReLU
+            const int Cs = a.Co >> 2;
+            const int Hs = a.Ho * 2, Ws = a.Wo * 2;
+#pragma unroll
+            for (int c = 0; c < CO_T; ++c) {
+                const int co = co0 + c;
+                if (co >= a.Co) break;
+                const int cc = co >> 2, dy = (co >> 1) & 1, dx = co & 1;
+                const float v = fmaxf(__fadd_rn(acc[c], a.b[co]), 0.f);
+                a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = v;
+            }
+        } else {
+            // logistic head (vqvae.py:105-112, logistic.py:36-40, 109-114)
+            if (oy >= a.crop_h || ox >= a.crop_w) continue;
+            const int64_t px = ((int64_t)n * a.crop_h + oy) * a.crop_w + ox;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float av = __fadd_rn(acc[c], a.b[c]);
+                av = fminf(fmaxf(av, -15.f), 15.f);
+                const float mu = __fmul_rn(255.f, sigmoid_f32(av));
+                float bv = __fadd_rn(acc[3 + c], a.b[3 + c]);
+                bv = fminf(fmaxf(bv, a.log_s_min), a.log_s_max);
+                float sv = expf(bv);
+                sv = fminf(fmaxf(sv, 0.5f), 64.f);
+                const int shift = (int)floor((double)mu + 0.5);
+                const double sd = (double)sv;
+                int d = 0;
+                for (int k = 0; k < a.n_thresh; ++k) d += sd > a.thresh[k];
+                a.shift[px * 3 + c] = (uint8_t)shift;
+                a.dsel[px * 3 + c] = (uint8_t)d;
+                if (a.mu) a.mu[px * 3 + c] = mu;
+                if (a.s) a.s[px * 3 + c] = sv;
+            }
+        }
+    }
+}
+
+size_t conv_smem(int ks, int stride, int co_t) {
+    const int IR = (kTile - 1) * stride + ks;
+    return sizeof(float) * ((size_t)kCK * IR * (IR + 1) + (size_t)ks * ks * kCK * co_t);
+}
+
+int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s) {
+    a.tiles_x = (a.Wo + kTile - 1) / kTile;
+    a.tiles_per_img = a.tiles_x * ((a.Ho + kTile - 1) / kTile);
+    const int64_t blocks = n_img * a.tiles_per_img;
+    if (blocks > 0x7FFFFFFF) return PILC_E_ARG;
+    dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
+    const size_t smem = conv_smem(a.ks, a.stride, co_t);
+    switch (co_t) {
+        case 32:
+            cudaFuncSetAttribute(conv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            conv_kernel<32><<<grid, kThreads, smem, s>>>(a);
+            break;
+        case 16:
+            cudaFuncSetAttribute(conv_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            conv_kernel<16><<<grid, kThreads, smem, s>>>(a);
+            break;
+        default:
+            cudaFuncSetAttribute(conv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            conv_kernel<8><<<grid, kThreads, smem, s>>>(a);
+            break;
+    }
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+ConvArgs base_args(const float *model, const ConvSpec &sp) {
+    ConvArgs a;
+    memset(&a, 0, sizeof(a));
+    a.Ci = sp.ci;
+    a.Ci_pad = sp.ci_pad;
+    a.Co = sp.co;
+    a.Co_pad = sp.co_pad;
+    a.ks = sp.ks;
+    a.stride = 1;
+    a.w = model + sp.w_off;
+    a.b = model + sp.b_off;
+    return a;
+}
+
+// ---- codebook argmin (vqvae.py:66-76) --------------------------------------
+// Warp per latent vector. Lane l scores codes l, l+32, ...: the squared
+// distance is accumulated in float64 component by component in the
+// reference's order without FMA; the warp min breaks ties to the lowest k.
+constexpr int kArgWarps = 8;
+
+__global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__restrict__ z,
+                                                                 int64_t n_vec,
+                                                                 const float *__restrict__ cb, int K,
+                                                                 int Dc, uint8_t *__restrict__ idx) {
+    extern __shared__ float sm[];
+    float *s_cb = sm;                      // K x Dc
+    float *s_z = sm + (int64_t)K * Dc;     // kArgWarps x Dc
+    for (int i = threadIdx.x; i < K * Dc; i += blockDim.x) s_cb[i] = cb[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *zw = s_z + warp * Dc;
+    for (int64_t v = (int64_t)blockIdx.x * kArgWarps + warp; v < n_vec;
+         v += (int64_t)gridDim.x * kArgWarps) {
+        for (int c = lane; c < Dc; c += 32) zw[c] = z[v * Dc + c];
+        __syncwarp();
+        double best = INFINITY;
+        int bk = 0x7FFFFFFF;
+        for (int k = lane; k < K; k += 32) {
+            const float *row = s_cb + k * Dc;
+            double dist = 0.0;
+            for (int c = 0; c < Dc; ++c) {
+                const double diff = __dsub_rn((double)zw[c], (double)row[c]);
+                dist = __dadd_rn(dist, __dmul_rn(diff, diff));
+            }
+            if (dist < best) {  // k increases within a lane: keep the first
+                best = dist;
+                bk = k;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            if (ob < best || (ob == best && ok < bk)) {
+                best = ob;
+                bk = ok;
+            }
+        }
+        if (lane == 0) idx[v] = (uint8_t)bk;
+        __syncwarp();
+    }
+}
+
+int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc, uint8_t *idx,
+                  cudaStream_t s) {
+    if (n_vec == 0) return PILC_OK;
+    const size_t smem = sizeof(float) * ((size_t)K * Dc + (size_t)kArgWarps * Dc);
+    if (smem > 200 * 1024) return PILC_E_UNSUPPORTED;
+    cudaFuncSetAttribute(argmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t blocks = ceil_div64(n_vec, kArgWarps);
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    argmin_kernel<<<(unsigned)blocks, 32 * kArgWarps, smem, s>>>(z, n_vec, cb, K, Dc, idx);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+struct Work {
+    float *A, *B, *T, *Z;
+};
+
+int64_t ws_parts(int64_t n, int H, int W, int Dc, int C, Work *w, char *base) {
+    const int He = H + (H & 1), We = W + (W & 1);
+    const int gh = He / 2, gw = We / 2;
+    const int64_t a = n * He * We * (int64_t)C * 4;        // stem out / shuffled up out
+    const int64_t b = n * gh * gw * (int64_t)C * 4;
+    const int64_t z = n * gh * gw * (int64_t)Dc * 4;
+    auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
+    if (w) {
+        w->A = reinterpret_cast<float *>(base);
+        w->B = reinterpret_cast<float *>(base + al(a));
+        w->T = reinterpret_cast<float *>(base + al(a) + al(b));
+        w->Z = reinterpret_cast<float *>(base + al(a) + 2 * al(b));
+    }
+    return al(a) + 2 * al(b) + al(z);
+}
+
+bool check_cfg(int K, int Dc, int C, int B) {
+    return K >= 1 && K <= 256 && Dc >= 1 && C >= 1 && B >= 0 && Dc <= 4096 && C <= 4096;
+}
+
+}  // namespace
+
+extern "C" int64_t pilc_model_floats(int32_t K, int32_t Dc, int32_t C, int32_t B) {
+    if (!check_cfg(K, Dc, C, B)) return -1;
+    return make_layout(K, Dc, C, B).total;
+}
+
+// canonical order (weights.py:46-69): enc.stem, enc.down, enc.block{i}.conv{1,2},
+// enc.proj, codebook, dec.proj, dec.block{i}.conv{1,2}, dec.up, dec.mu, dec.s;
+// each conv is w [co][ci][kh][kw] then b [co].
+extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t C, int32_t B,
+                               float *dst) {
+    if (!check_cfg(K, Dc, C, B) || !src || !dst) return PILC_E_ARG;
+    const Layout L = make_layout(K, Dc, C, B);
+    for (int64_t i = 0; i < L.total; ++i) dst[i] = 0.f;
+    const float *p = src;
+    auto put_conv = [&](const ConvSpec &sp, int co_base, int co_n) {
+        // reads w [co_n][ci][ks][ks] then b [co_n] from src, places them at
+        // output channels co_base .. co_base + co_n
+        for (int co = 0; co < co_n; ++co)
+            for (int ci = 0; ci < sp.ci; ++ci)
+                for (int i = 0; i < sp.ks; ++i)
+                    for (int j = 0; j < sp.ks; ++j)
+                        dst[sp.w_off + ((int64_t)(i * sp.ks + j) * sp.ci_pad + ci) * sp.co_pad + co_base + co] = *p++;
+        for (int co = 0; co < co_n; ++co) dst[sp.b_off + co_base + co] = *p++;
+    };
+    for (const auto &sp : L.enc) put_conv(sp, 0, sp.co);
+    for (int64_t i = 0; i < (int64_t)K * Dc; ++i) dst[L.cb_off + i] = *p++;
+    for (size_t l = 0; l + 1 < L.dec.size(); ++l) put_conv(L.dec[l], 0, L.dec[l].co);
+    put_conv(L.dec.back(), 0, 3);  // dec.mu -> channels 0..2
+    put_conv(L.dec.back(), 3, 3);  // dec.s  -> channels 3..5
+    return PILC_OK;
+}
+
+extern "C" int64_t pilc_vq_workspace_bytes(int64_t n_img, int32_t H, int32_t W, int32_t K, int32_t Dc,
+                                           int32_t C, int32_t B) {
+    if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return -1;
+    return ws_parts(n_img, H, W, Dc, C, nullptr, nullptr);
+}
+
+extern "C" int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model, int32_t K, int32_t Dc,
+                              int32_t C, int32_t B, uint8_t *idx_out, void *stream) {
+    if (n_vec < 0 || !check_cfg(K, Dc, C, B)) return PILC_E_ARG;
+    const Layout L = make_layout(K, Dc, C, B);
+    return launch_argmin(z, n_vec, model + L.cb_off, K, Dc, idx_out, as_stream(stream));
+}
+
+extern "C" int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model,
+                              int32_t K, int32_t Dc, int32_t C, int32_t B, void *workspace,
+                              int64_t ws_bytes, uint8_t *idx_out, float *z_out, void *stream) {
+    if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    Work w;
+    if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+    const Layout L = make_layout(K, Dc, C, B);
+    cudaStream_t s = as_stream(stream);
+    const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
+    int rc;
+    // stem (3x3, image -> He x We x C, ReLU); normalisation + even-pad fused
+    ConvArgs a = base_args(model, L.enc[0]);
+    a.in_mode = IN_U8;
+    a.in_u8 = img;
+    a.src_h = H;
+    a.src_w = W;
+    a.Hi = He;
+    a.Wi = We;
+    a.Ho = He;
+    a.Wo = We;
+    a.relu = 1;
+    a.out = w.A;
+    if ((rc = launch_conv(a, L.enc[0].co_t, n_img, s))) return rc;
+    // down (3x3 stride 2) -> B
+    a = base_args(model, L.enc[1]);
+    a.in = w.A;
+    a.Hi = He;
+    a.Wi = We;
+    a.stride = 2;
+    a.Ho = gh;
+    a.Wo = gw;
+    a.relu = 1;
+    a.out = w.B;
+    if ((rc = launch_conv(a, L.enc[1].co_t, n_img, s))) return rc;
+    for (int i = 0; i < B; ++i) {
+        a = base_args(model, L.enc[2 + 2 * i]);
+        a.in = w.B;
+        a.Hi = a.Ho = gh;
+        a.Wi = a.Wo = gw;
+        a.relu = 1;
+        a.out = w.T;
+        if ((rc = launch_conv(a, L.enc[2 + 2 * i].co_t, n_img, s))) return rc;
+        a = base_args(model, L.enc[3 + 2 * i]);
+        a.in = w.T;
+        a.Hi = a.Ho = gh;
+        a.Wi = a.Wo = gw;
+        a.resid = w.B;  // relu(x + conv2(h)), written in place over x
+        a.relu = 1;
+        a.out = w.B;
+        if ((rc = launch_conv(a, L.enc[3 + 2 * i].co_t, n_img, s))) return rc;
+    }
+    float *z = z_out ? z_out : w.Z;
+    a = base_args(model, L.enc[2 + 2 * B]);
+    a.in = w.B;
+    a.Hi = a.Ho = gh;
+    a.Wi = a.Wo = gw;
+    a.out = z;
+    if ((rc = launch_conv(a, L.enc[2 + 2 * B].co_t, n_img, s))) return rc;
+    return launch_argmin(z, n_img * gh * gw, model + L.cb_off, K, Dc, idx_out, s);
+}
+
+extern "C" int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
+                              int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host,
+                              int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
+                              uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
+    if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B) || D < 1 || D > 256) return PILC_E_ARG;
+    if (D > 1 && !d_thresh_host) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    Work w;
+    if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+    const Layout L = make_layout(K, Dc, C, B);
+    cudaStream_t s = as_stream(stream);
+    const int gh = (H + 1) / 2, gw = (W + 1) / 2;
+    int rc;
+    double *thr = nullptr;
+    if (D > 1) {
+        if (cudaMallocAsync(&thr, sizeof(double) * (D - 1), s) != cudaSuccess) return PILC_E_CUDA;
+        cudaMemcpyAsync(thr, d_thresh_host, sizeof(double) * (D - 1), cudaMemcpyHostToDevice, s);
+    }
+    // dec.proj (1x1) over the gathered codebook rows, ReLU -> B
+    ConvArgs a = base_args(model, L.dec[0]);
+    a.in_mode = IN_CODEBOOK;
+    a.in_u8 = idx;
+    a.codebook = model + L.cb_off;
+    a.Hi = a.Ho = gh;
+    a.Wi = a.Wo = gw;
+    a.relu = 1;
+    a.out = w.B;
+    rc = launch_conv(a, L.dec[0].co_t, n_img, s);
+    for (int i = 0; !rc && i < B; ++i) {
+        a = base_args(model, L.dec[1 + 2 * i]);
+        a.in = w.B;
+        a.Hi = a.Ho = gh;
+        a.Wi = a.Wo = gw;
+        a.relu = 1;
+        a.out = w.T;
+        rc = launch_conv(a, L.dec[1 + 2 * i].co_t, n_img, s);
+        if (rc) break;
+        a = base_args(model, L.dec[2 + 2 * i]);
+        a.in = w.T;
+        a.Hi = a.Ho = gh;
+        a.Wi = a.Wo = gw;
+        a.resid = w.B;
+        a.relu = 1;
+        a.out = w.B;
+        rc = launch_conv(a, L.dec[2 + 2 * i].co_t, n_img, s);
+    }
+    if (!rc) {  // up (3x3 C -> 4C) + pixel shuffle + ReLU -> A (2gh x 2gw x C)
+        a = base_args(model, L.dec[1 + 2 * B]);
+        a.in = w.B;
+        a.Hi = a.Ho = gh;
+        a.Wi = a.Wo = gw;
+        a.out_mode = OUT_SHUFFLE;
+        a.out = w.A;
+        rc = launch_conv(a, L.dec[1 + 2 * B].co_t, n_img, s);
+    }
+    if (!rc) {  // heads (3x3 C -> mu|s) + logistic head, cropped to H x W
+        a = base_args(model, L.dec[2 + 2 * B]);
+        a.in = w.A;
+        a.Hi = a.Ho = 2 * gh;
+        a.Wi = a.Wo = 2 * gw;
+        a.out_mode = OUT_HEAD;
+        a.shift = shift_out;
+        a.dsel = d_out;
+        a.mu = mu_out;
+        a.s = s_out;
+        a.crop_h = H;
+        a.crop_w = W;
+        a.thresh = thr;
+        a.n_thresh = D - 1;
+        a.log_s_min = (float)log(0.5);
+        a.log_s_max = (float)log(64.0);
+        rc = launch_conv(a, L.dec[2 + 2 * B].co_t, n_img, s);
+    }
+    if (thr) cudaFreeAsync(thr, s);
+    return rc;
+}

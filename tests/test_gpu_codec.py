@@ -1,0 +1,316 @@
+"""GPU parity tests: the sm_100a path (through libpilc_sm100a.so) against the
+reference's golden fixtures and the CPU oracle on the same seeded inputs.
+
+Integer/byte work is checked bit-exactly; the VQ-VAE float path is checked
+for exact codebook indices (given identical latents z the argmin is
+bit-exact; end to end z differs from numpy/BLAS only by summation order),
+lossless round trips and bpd within 0.5% of the reference.
+"""
+
+import os
+import struct
+import zlib
+
+import numpy as np
+import pytest
+
+import paper_2206_05279_b200 as pc
+from oracle import oracle as O
+from paper_2206_05279_b200 import container as ct
+from paper_2206_05279_b200 import predictor, tables, vqvae
+from paper_2206_05279_b200.errors import CodecError, CorruptStreamError, FormatError, ModelError
+from paper_2206_05279_b200.logistic import default_grid, residual_distributions
+from paper_2206_05279_b200.synth import smooth_images
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+SMALL = pc.ModelConfig(K=32, Dc=8, channels=8, blocks=1)
+
+
+def _blobs(z):
+    return [z["buf"][z["offs"][i]: z["offs"][i + 1]].tobytes() for i in range(len(z["offs"]) - 1)]
+
+
+@pytest.fixture(scope="module")
+def small_model():
+    return pc.ModelWeights.load(os.path.join(GOLDEN, "small.pilw"))
+
+
+@pytest.fixture(scope="module")
+def full_model():
+    return pc.random_weights(seed=1)
+
+
+# --- TWAR ---------------------------------------------------------------------
+
+
+def test_twar_forward_matches_reference(golden):
+    z = golden("twar.npz")
+    for k in range(int(z["n"])):
+        p = predictor.PredictorParams(z[f"w{k}"], z[f"b{k}"])
+        res = predictor.forward_residual(z[f"img{k}"], p)
+        assert np.array_equal(res, z[f"res{k}"])
+        assert np.array_equal(predictor.forward_residual(z[f"img{k}"]), z[f"resdef{k}"])
+        assert np.array_equal(predictor.decode_parallel(res, p), z[f"img{k}"])
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (2, 2), (5, 37), (33, 31), (64, 64), (130, 70)])
+def test_twar_random_params_vs_oracle(shape):
+    rng = np.random.default_rng(sum(shape))
+    imgs = rng.integers(0, 256, (6, *shape, 3), dtype=np.uint8)
+    w = rng.normal(0, 2, (3, 3)).astype(np.float32)
+    b = rng.normal(0, 20, 3).astype(np.float32)
+    p = predictor.PredictorParams(w, b)
+    res = predictor.forward_residual_batch(imgs, p)
+    assert np.array_equal(res, O.twar_forward(imgs, w, b))
+    assert np.array_equal(predictor.decode_parallel_batch(res, p), imgs)
+
+
+def test_twar_exhaustive_2x2_sample():
+    # acceptance 6 style: many 2x2 images with 4-value alphabets
+    rng = np.random.default_rng(7)
+    vals = np.array([0, 1, 128, 255], np.uint8)
+    imgs = vals[rng.integers(0, 4, (20000, 2, 2, 3))]
+    for p in (pc.default_params(), predictor.PredictorParams(rng.normal(0, 2, (3, 3)), rng.normal(0, 20, 3))):
+        res = predictor.forward_residual_batch(imgs, p)
+        assert np.array_equal(res, O.twar_forward(imgs, p.weights, p.bias))
+        assert np.array_equal(predictor.decode_parallel_batch(res, p), imgs)
+
+
+# --- coder lanes --------------------------------------------------------------
+
+
+@pytest.mark.parametrize("L", [1, 3, 16, 64])
+def test_lanes_byte_identical_to_reference(golden, L):
+    z = golden("lanes.npz")
+    enc, dec = tables.build_tables(residual_distributions(default_grid(), 12), 12)
+    ls = tables.interleaved_encode(z["syms"], z["d"], L, enc)
+    ref = [z[f"L{L}_buf"][z[f"L{L}_offs"][i]: z[f"L{L}_offs"][i + 1]].tobytes() for i in range(L)]
+    assert [s.to_bytes() for s in ls.streams] == ref
+    assert ls.states == list(z[f"L{L}_states"])
+    assert np.array_equal(tables.interleaved_decode(ls, z["syms"].size, z["d"], dec), z["syms"])
+
+
+def test_lanes_random_vs_oracle():
+    rng = np.random.default_rng(3)
+    enc, dec = tables.build_tables(residual_distributions(default_grid(), 11), 11)
+    for n, L in [(0, 1), (1, 1), (5, 7), (1000, 1), (4097, 5), (20000, 33)]:
+        syms = rng.integers(0, 256, n).astype(np.uint8)
+        ds = rng.integers(0, 8, n).astype(np.uint16)
+        ls = tables.interleaved_encode(syms, ds, L, enc)
+        blobs, states = O.encode_lanes(syms, ds, L, enc.delta, enc.phi, 11)
+        assert [s.to_bytes() for s in ls.streams] == blobs and ls.states == states
+        assert np.array_equal(tables.interleaved_decode(ls, n, ds, dec), syms)
+
+
+def test_lane_underflow_and_end_state_detected():
+    enc, dec = tables.build_tables(residual_distributions(default_grid(), 12), 12)
+    syms = np.arange(300, dtype=np.uint8)
+    ds = np.full(300, 3, np.uint16)
+    ls = tables.interleaved_encode(syms, ds, 1, enc)
+    short = pc.container.BitStack if hasattr(pc.container, "BitStack") else None
+    from paper_2206_05279_b200.bits import BitStack
+    raw = ls.streams[0].to_bytes()
+    nb = struct.unpack_from("<Q", raw)[0]
+    trunc = BitStack.from_packed(np.frombuffer(raw[8:], np.uint8), nb - 40)
+    with pytest.raises(CorruptStreamError):
+        tables.interleaved_decode(tables.LaneSet(ls.states, [trunc]), 300, ds, dec)
+    with pytest.raises(CorruptStreamError):
+        tables.interleaved_decode(tables.LaneSet([ls.states[0] ^ 1], ls.streams), 300, ds, dec)
+    del short
+
+
+# --- twar-static containers: byte-identical to the reference -----------------
+
+
+def test_static_containers_byte_identical(golden):
+    z = golden("static.npz")
+    blobs = _blobs(z)
+    for blob, ci, (L, M, dbg) in zip(blobs, z["img_index"], z["cfg"]):
+        img = z[f"img{ci}"]
+        cfg = pc.CodecConfig(lanes=int(L), M=int(M), debug_schedule_check=bool(dbg))
+        assert pc.compress(img, None, cfg) == blob
+        assert np.array_equal(pc.decompress(blob), img)
+
+
+def test_static_batch_equals_single(golden):
+    imgs = smooth_images(37, 32, 32, seed=11)
+    buf, off = pc.compress_batch(imgs)
+    for i in range(0, 37, 6):
+        assert buf[off[i]:off[i + 1]].tobytes() == O.compress(imgs[i])
+    out = pc.decompress_batch(buf, off)
+    assert np.array_equal(out, imgs)
+
+
+def test_fitted_params_container(golden):
+    z = golden("static.npz")
+    m = pc.ModelWeights(pc.ModelConfig(), {}, predictor_params=predictor.PredictorParams(z["fit_w"], z["fit_b"]))
+    assert pc.compress(z["img9"], m) == z["fit_blob"].tobytes()
+    assert np.array_equal(pc.decompress(z["fit_blob"].tobytes(), m), z["img9"])
+    with pytest.raises(ModelError):
+        pc.decompress(z["fit_blob"].tobytes())
+
+
+def test_mixed_shape_batch():
+    rng = np.random.default_rng(5)
+    imgs = [rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for h, w in [(1, 1), (7, 1), (1, 7), (31, 33), (8, 8), (7, 1)]]
+    buf, off = pc.compress_batch(imgs)
+    for i, im in enumerate(imgs):
+        assert buf[off[i]:off[i + 1]].tobytes() == O.compress(im)
+    out = pc.decompress_batch(buf, off)
+    assert all(np.array_equal(a, b) for a, b in zip(out, imgs))
+
+
+# --- twar-vqvae ---------------------------------------------------------------
+
+
+@pytest.mark.parametrize("tag", ["small", "full"])
+def test_argmin_bit_exact_given_z(golden, tag, small_model, full_model):
+    z = golden(f"vqvae_{tag}.npz")
+    m = small_model if tag == "small" else full_model
+    for k in range(int(z["n"])):
+        assert np.array_equal(vqvae.argmin_codebook(z[f"z{k}"], m), z[f"idx{k}"])
+
+
+@pytest.mark.parametrize("tag", ["small", "full"])
+def test_vqvae_encoder_and_decoder_vs_reference(golden, tag, small_model, full_model):
+    z = golden(f"vqvae_{tag}.npz")
+    m = small_model if tag == "small" else full_model
+    agree = total = 0
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        lat = vqvae.encoder_latents(img, m)
+        np.testing.assert_allclose(lat, z[f"z{k}"], rtol=1e-4, atol=1e-4)  # fp32, other summation order
+        idx = vqvae.encode_to_indices(img, m)
+        agree += int((idx == z[f"idx{k}"]).sum())
+        total += idx.size
+        mu, s = vqvae.decode_to_params(z[f"idx{k}"], m, img.shape[:2])
+        np.testing.assert_allclose(mu, z[f"mu{k}"], rtol=0, atol=2e-3)
+        np.testing.assert_allclose(s, z[f"s{k}"], rtol=2e-4, atol=0)
+    assert agree == total, f"index agreement {agree}/{total}"
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (31, 33), (32, 32), (97, 61)])
+def test_vqvae_round_trip(shape, small_model):
+    rng = np.random.default_rng(sum(shape))
+    img = rng.integers(0, 256, (*shape, 3), dtype=np.uint8)
+    for lanes in (1, 4):
+        blob = pc.compress(img, small_model, pc.CodecConfig(backend="twar-vqvae", lanes=lanes))
+        assert np.array_equal(pc.decompress(blob, small_model), img)
+
+
+def test_vqvae_bpd_within_half_percent_of_reference(golden, small_model, full_model):
+    for tag, m in (("small", small_model), ("full", full_model)):
+        z = golden(f"vqvae_{tag}.npz")
+        ref = _blobs(z)
+        for k in range(int(z["n"])):
+            img = z[f"img{k}"]
+            blob = pc.compress(img, m, pc.CodecConfig(backend="twar-vqvae", lanes=1 + (k % 3)))
+            assert abs(len(blob) - len(ref[k])) / len(ref[k]) <= 0.005, (tag, k, len(blob), len(ref[k]))
+            assert np.array_equal(pc.decompress(blob, m), img)
+            # header fields identical to the reference container
+            assert ct.parse_header(blob)[0].model_hash == ct.parse_header(ref[k])[0].model_hash
+
+
+def test_vqvae_batch_independent_of_batch_size(full_model):
+    imgs = smooth_images(19, 32, 32, seed=2)
+    cfg = pc.CodecConfig(backend="twar-vqvae")
+    buf, off = pc.compress_batch(imgs, full_model, cfg)
+    for i in (0, 7, 18):
+        assert pc.compress(imgs[i], full_model, cfg) == buf[off[i]:off[i + 1]].tobytes()
+    assert np.array_equal(pc.decompress_batch(buf, off, full_model), imgs)
+
+
+def test_vqvae_other_precisions_and_schedule_check(small_model):
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, (17, 13, 3), dtype=np.uint8)
+    for M in (10, 11, 12):
+        blob = pc.compress(img, small_model, pc.CodecConfig(backend="twar-vqvae", M=M, debug_schedule_check=True))
+        assert ct.inspect(blob)["M"] == M
+        assert ct.parse_header(blob)[0].schedule_checksum is not None
+        assert np.array_equal(pc.decompress(blob, small_model), img)
+
+
+# --- error handling (reference test_container.py:96-178) -----------------------
+
+
+def test_bad_magic_version_truncation():
+    rng = np.random.default_rng(1)
+    img = rng.integers(0, 256, (8, 8, 3), dtype=np.uint8)
+    blob = pc.compress(img)
+    with pytest.raises(FormatError):
+        pc.decompress(b"JUNK" + blob[4:])
+    v = bytearray(blob)
+    v[4] = 9
+    with pytest.raises(FormatError):
+        pc.decompress(bytes(v))
+    with pytest.raises(FormatError):
+        pc.decompress(b"PIL")
+    with pytest.raises(CodecError):
+        pc.decompress(blob[: len(blob) // 2])
+    bad = bytearray(blob)
+    bad[-20] ^= 0x10
+    with pytest.raises(CorruptStreamError):
+        pc.decompress(bytes(bad))
+
+
+def test_vqvae_needs_model(small_model):
+    img = np.random.default_rng(2).integers(0, 256, (8, 8, 3), dtype=np.uint8)
+    blob = pc.compress(img, small_model, pc.CodecConfig(backend="twar-vqvae"))
+    with pytest.raises(ModelError):
+        pc.decompress(blob)
+    with pytest.raises(ModelError):
+        pc.decompress(blob, pc.random_weights(SMALL, seed=7))
+    with pytest.raises(ModelError):
+        pc.compress(img, None, pc.CodecConfig(backend="twar-vqvae"))
+
+
+def test_schedule_checksum_catches_divergence():
+    img = np.random.default_rng(3).integers(0, 256, (12, 10, 3), dtype=np.uint8)
+    blob = pc.compress(img, None, pc.CodecConfig(debug_schedule_check=True))
+    h, _ = ct.parse_header(blob)
+    doctored = bytearray(blob[:-4])
+    struct.pack_into("<H", doctored, 19, (h.static_d + 1) % h.grid.D)
+    doctored += struct.pack("<I", zlib.crc32(bytes(doctored)))
+    with pytest.raises(CorruptStreamError, match="schedule"):
+        pc.decompress(bytes(doctored))
+
+
+def test_single_byte_flips_all_detected():
+    # acceptance 10 (test_acceptance.py:337-363), a sample of positions
+    img = smooth_images(1, 16, 16, seed=4)[0]
+    blob = pc.compress(img)
+    rng = np.random.default_rng(0)
+    flips = []
+    for pos in rng.integers(0, len(blob), 200):
+        b = bytearray(blob)
+        b[pos] ^= 1 << int(rng.integers(0, 8))
+        flips.append(bytes(b))
+    sizes = np.array([len(b) for b in flips], np.uint64)
+    off = np.zeros(len(flips) + 1, np.uint64)
+    np.cumsum(sizes, out=off[1:])
+    _, errs = pc.decompress_batch(b"".join(flips), off, raise_on_error=False)
+    assert len(errs) == len(flips)
+
+
+def test_batch_status_codes_match_single_errors(small_model):
+    rng = np.random.default_rng(4)
+    imgs = rng.integers(0, 256, (6, 9, 11, 3), dtype=np.uint8)
+    cfg = pc.CodecConfig(backend="twar-vqvae", lanes=2)
+    buf, off = pc.compress_batch(imgs, small_model, cfg)
+    buf = buf.copy()
+    buf[off[2] + 30] ^= 0xFF  # blob 2 crc failure
+    out, errs = pc.decompress_batch(buf, off, small_model, raise_on_error=False)
+    assert set(errs) == {2} and isinstance(errs[2], CorruptStreamError)
+    for i in (0, 1, 3, 4, 5):
+        assert np.array_equal(out[i], imgs[i])
+
+
+def test_large_batch_round_trip(full_model):
+    imgs = smooth_images(512, 32, 32, seed=21)
+    cfg = pc.CodecConfig(backend="twar-vqvae")
+    buf, off = pc.compress_batch(imgs, full_model, cfg)
+    assert np.array_equal(pc.decompress_batch(buf, off, full_model), imgs)
+    bufs, offs = pc.compress_batch(imgs)
+    assert np.array_equal(pc.decompress_batch(bufs, offs), imgs)
