@@ -233,6 +233,18 @@ int pilc_crc32(const uint8_t *buf, const uint64_t *off, const uint64_t *len,
 int pilc_sched_crc(const uint8_t *dsched, const uint16_t *d_img, int64_t n_img,
                    int64_t n_sym, uint32_t *crc, void *stream);
 
+/* ---- launch accounting -----------------------------------------------------
+ * Every kernel launch is counted; with timing enabled each launch is also
+ * bracketed by CUDA events on its stream, with its algorithmic work units
+ * (conv/argmin: FLOPs; coder: symbols; predictor: subpixels; container:
+ * blobs). Used by bench.py for the live roofline. */
+void pilc_prof_reset(int32_t enable_timing);
+int64_t pilc_prof_launches(void);
+int32_t pilc_prof_categories(void);
+const char *pilc_prof_name(int32_t cat);
+int pilc_prof_read(int32_t cat, int64_t *launches, double *total_ms,
+                   double *units);
+
 #ifdef __cplusplus
 }
 #endif

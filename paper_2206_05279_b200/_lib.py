@@ -40,6 +40,11 @@ _SIGS = {
     "pilc_container_lanes": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
     "pilc_crc32": (ctypes.c_int, [P, P, P, I64, P, P]),
     "pilc_sched_crc": (ctypes.c_int, [P, P, I64, I64, P, P]),
+    "pilc_prof_reset": (None, [I32]),
+    "pilc_prof_launches": (I64, []),
+    "pilc_prof_categories": (I32, []),
+    "pilc_prof_name": (ctypes.c_char_p, [I32]),
+    "pilc_prof_read": (ctypes.c_int, [I32, P, P, P]),
 }
 
 # pilc_header (include/pilc.h), 72 bytes
@@ -96,6 +101,26 @@ def call(name: str, *args) -> int:
     if rc != 0:
         raise LibraryError(f"{name} failed with status {rc} ({['OK', 'E_ARG', 'E_CUDA', 'E_UNSUPPORTED'][rc] if rc < 4 else rc})")
     return rc
+
+
+def prof_reset(timing: bool) -> None:
+    load().pilc_prof_reset(1 if timing else 0)
+
+
+def prof_launches() -> int:
+    return int(load().pilc_prof_launches())
+
+
+def prof_read() -> dict:
+    """{kernel: (launches, total_ms, work_units)} since the last reset."""
+    lib = load()
+    out = {}
+    for c in range(lib.pilc_prof_categories()):
+        n, ms, u = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        call("pilc_prof_read", c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(u))
+        if n.value:
+            out[lib.pilc_prof_name(c).decode()] = (n.value, ms.value, u.value)
+    return out
 
 
 def version() -> str:

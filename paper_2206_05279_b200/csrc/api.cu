@@ -1,5 +1,84 @@
 // Library identity and device check.
+#include <atomic>
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
+
+namespace {
+const char *kCatNames[PROF_NCAT] = {"conv_kernel",        "argmin_kernel",  "rans_encode_kernel",
+                                    "rans_decode_kernel", "twar_forward_kernel", "twar_decode_kernel",
+                                    "static_scale_kernel", "blob_sizes+scan", "pack_kernel",
+                                    "parse_kernel",       "lanes_kernel",   "crc_kernel",
+                                    "sched_crc_kernel"};
+struct Rec {
+    int cat;
+    cudaEvent_t e0, e1;
+    double units;
+};
+std::atomic<long long> g_launches{0};
+std::atomic<int> g_timing{0};
+std::mutex g_mu;
+std::vector<Rec> g_recs;
+}  // namespace
+
+void *prof_begin(int cat, cudaStream_t s, double units) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (!g_timing.load(std::memory_order_relaxed)) return nullptr;
+    Rec *r = new Rec{cat, nullptr, nullptr, units};
+    cudaEventCreate(&r->e0);
+    cudaEventCreate(&r->e1);
+    cudaEventRecord(r->e0, s);
+    return r;
+}
+
+void prof_end(void *tok, cudaStream_t s) {
+    if (!tok) return;
+    Rec *r = static_cast<Rec *>(tok);
+    cudaEventRecord(r->e1, s);
+    std::lock_guard<std::mutex> g(g_mu);
+    g_recs.push_back(*r);
+    delete r;
+}
+
+extern "C" void pilc_prof_reset(int32_t enable_timing) {
+    std::lock_guard<std::mutex> g(g_mu);
+    for (auto &r : g_recs) {
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    g_recs.clear();
+    g_launches.store(0);
+    g_timing.store(enable_timing ? 1 : 0);
+}
+
+extern "C" int64_t pilc_prof_launches(void) { return g_launches.load(); }
+
+extern "C" int32_t pilc_prof_categories(void) { return PROF_NCAT; }
+
+extern "C" const char *pilc_prof_name(int32_t cat) {
+    return (cat >= 0 && cat < PROF_NCAT) ? kCatNames[cat] : "";
+}
+
+extern "C" int pilc_prof_read(int32_t cat, int64_t *launches, double *total_ms, double *units) {
+    if (cat < 0 || cat >= PROF_NCAT) return PILC_E_ARG;
+    std::lock_guard<std::mutex> g(g_mu);
+    int64_t n = 0;
+    double ms = 0, u = 0;
+    for (auto &r : g_recs) {
+        if (r.cat != cat) continue;
+        if (cudaEventSynchronize(r.e1) != cudaSuccess) return PILC_E_CUDA;
+        float t = 0;
+        cudaEventElapsedTime(&t, r.e0, r.e1);
+        ++n;
+        ms += t;
+        u += r.units;
+    }
+    *launches = n;
+    *total_ms = ms;
+    *units = u;
+    return PILC_OK;
+}
 
 extern "C" const char *pilc_version(void) { return "pilc-sm100a 0.1.0"; }
 

@@ -14,6 +14,35 @@
         }                                                \
     } while (0)
 
+// ---- launch accounting / live per-kernel timing (pilc_prof_* in pilc.h) ----
+// Every kernel launch goes through a ProfScope: it bumps the launch counter
+// and, when timing is enabled, brackets the launch with CUDA events on the
+// launching stream together with the launch's algorithmic work units.
+enum ProfCat {
+    PROF_CONV = 0,
+    PROF_ARGMIN,
+    PROF_RANS_ENC,
+    PROF_RANS_DEC,
+    PROF_TWAR_FWD,
+    PROF_TWAR_DEC,
+    PROF_STATIC_SCALE,
+    PROF_SIZES,
+    PROF_PACK,
+    PROF_PARSE,
+    PROF_LANES,
+    PROF_CRC,
+    PROF_SCHED_CRC,
+    PROF_NCAT
+};
+void *prof_begin(int cat, cudaStream_t s, double units);
+void prof_end(void *tok, cudaStream_t s);
+struct ProfScope {
+    void *tok;
+    cudaStream_t s;
+    ProfScope(int cat, cudaStream_t st, double units) : s(st) { tok = prof_begin(cat, st, units); }
+    ~ProfScope() { prof_end(tok, s); }
+};
+
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 static inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -535,7 +535,10 @@ extern "C" int pilc_static_scale(const uint8_t *res, int64_t n_img, int64_t n_sy
     cudaStream_t s = as_stream(stream);
     if (cudaMallocAsync(&g, sizeof(double) * D, s) != cudaSuccess) return PILC_E_CUDA;
     cudaMemcpyAsync(g, log2_grid_host, sizeof(double) * D, cudaMemcpyHostToDevice, s);
-    static_scale_kernel<<<(unsigned)n_img, 256, 0, s>>>(res, n_sym, g, D, d_img);
+{
+        ProfScope _ps(PROF_STATIC_SCALE, s, (double)n_img * n_sym);
+        static_scale_kernel<<<(unsigned)n_img, 256, 0, s>>>(res, n_sym, g, D, d_img);
+    }
     cudaFreeAsync(g, s);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
@@ -554,9 +557,12 @@ extern "C" int pilc_container_sizes(const uint32_t *idx_nbits, const uint32_t *r
     // sizes land in blob_off[1..n], then scan in place into a temp
     uint64_t *sizes = nullptr;
     if (cudaMallocAsync(&sizes, sizeof(uint64_t) * n_img, s) != cudaSuccess) return PILC_E_CUDA;
-    blob_sizes_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(idx_nbits, res_nbits, n_img, lanes,
+{
+        ProfScope _ps(PROF_SIZES, s, (double)n_img);
+        blob_sizes_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(idx_nbits, res_nbits, n_img, lanes,
                                                                fixed_bytes, sizes);
     scan_kernel<<<1, 1024, 0, s>>>(sizes, n_img, blob_off);
+    }
     cudaFreeAsync(sizes, s);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
@@ -579,7 +585,10 @@ extern "C" int pilc_container_pack(const uint8_t *template_host, int32_t templat
     PackArgs a{d_img,     dsched,      sched_check, n_img,      n_sym,      lanes,
                idx_scratch, idx_cap,   idx_nbits,   idx_states, res_scratch, res_cap,
                res_nbits, res_states,  blob_off,    out,        tmpl,       template_len};
-    pack_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(a, crc_consts());
+{
+        ProfScope _ps(PROF_PACK, s, (double)n_img);
+        pack_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(a, crc_consts());
+    }
     cudaFreeAsync(tmpl, s);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
@@ -590,8 +599,11 @@ extern "C" int pilc_container_parse(const uint8_t *buf, const uint64_t *blob_off
                                     pilc_header *hdr, void *stream) {
     if (n_blob < 0 || !blob_off || !hdr) return PILC_E_ARG;
     if (n_blob == 0) return PILC_OK;
-    parse_kernel<<<warp_grid(n_blob), 32 * kWarps, 0, as_stream(stream)>>>(
+{
+        ProfScope _ps(PROF_PARSE, as_stream(stream), (double)n_blob);
+        parse_kernel<<<warp_grid(n_blob), 32 * kWarps, 0, as_stream(stream)>>>(
         buf, blob_off, n_blob, params_hash, model_hash, has_model, hdr, crc_consts());
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
@@ -603,8 +615,11 @@ extern "C" int pilc_container_lanes(const uint8_t *buf, const uint64_t *blob_off
                                     void *stream) {
     if (n_group < 0 || lanes < 1 || (stream_id != 0 && stream_id != 1)) return PILC_E_ARG;
     if (n_group == 0) return PILC_OK;
-    lanes_kernel<<<warp_grid(n_group), 32 * kWarps, 0, as_stream(stream)>>>(
+{
+        ProfScope _ps(PROF_LANES, as_stream(stream), (double)n_group * lanes);
+        lanes_kernel<<<warp_grid(n_group), 32 * kWarps, 0, as_stream(stream)>>>(
         buf, blob_off, hdr, blob_idx, n_group, lanes, stream_id, lane_off, nbits, states, lane_status);
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
@@ -613,7 +628,10 @@ extern "C" int pilc_crc32(const uint8_t *buf, const uint64_t *off, const uint64_
                           uint32_t *crc, void *stream) {
     if (n < 0) return PILC_E_ARG;
     if (n == 0) return PILC_OK;
-    crc_kernel<<<warp_grid(n), 32 * kWarps, 0, as_stream(stream)>>>(buf, off, len, n, crc, crc_consts());
+{
+        ProfScope _ps(PROF_CRC, as_stream(stream), (double)n);
+        crc_kernel<<<warp_grid(n), 32 * kWarps, 0, as_stream(stream)>>>(buf, off, len, n, crc, crc_consts());
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
@@ -622,8 +640,11 @@ extern "C" int pilc_sched_crc(const uint8_t *dsched, const uint16_t *d_img, int6
                               int64_t n_sym, uint32_t *crc, void *stream) {
     if (n_img < 0 || n_sym < 0) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
-    sched_crc_kernel<<<warp_grid(n_img), 32 * kWarps, 0, as_stream(stream)>>>(dsched, d_img, n_img, n_sym,
+{
+        ProfScope _ps(PROF_SCHED_CRC, as_stream(stream), (double)n_img * n_sym);
+        sched_crc_kernel<<<warp_grid(n_img), 32 * kWarps, 0, as_stream(stream)>>>(dsched, d_img, n_img, n_sym,
                                                                              crc, crc_consts());
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

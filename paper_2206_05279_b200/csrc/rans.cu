@@ -167,9 +167,12 @@ extern "C" int pilc_rans_encode(const uint8_t *syms, const uint8_t *shift, const
     int64_t blocks = ceil_div64(total, kThreads);
     const int64_t cap = (int64_t)sm_count() * 16;
     if (blocks > cap) blocks = cap;
-    rans_encode_kernel<<<(unsigned)blocks, kThreads, smem, as_stream(stream)>>>(
+{
+        ProfScope _ps(PROF_RANS_ENC, as_stream(stream), (double)n_img * n_sym);
+        rans_encode_kernel<<<(unsigned)blocks, kThreads, smem, as_stream(stream)>>>(
         syms, shift, dsched, d_img, n_img, n_sym, lanes, enc_tab, D, X, M, in_smem, scratch,
         lane_cap, nbits, states);
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
@@ -194,9 +197,12 @@ extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, co
     const int64_t per_sm = in_smem ? (tab_bytes > 96 * 1024 ? 1 : (tab_bytes > 48 * 1024 ? 2 : 8)) : 16;
     const int64_t cap = (int64_t)sm_count() * per_sm;
     if (blocks > cap) blocks = cap;
-    rans_decode_kernel<<<(unsigned)blocks, kThreads, smem, as_stream(stream)>>>(
+{
+        ProfScope _ps(PROF_RANS_DEC, as_stream(stream), (double)n_img * n_sym);
+        rans_decode_kernel<<<(unsigned)blocks, kThreads, smem, as_stream(stream)>>>(
         buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, in_smem,
         unshift, out, lane_status);
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

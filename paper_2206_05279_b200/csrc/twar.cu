@@ -176,8 +176,11 @@ extern "C" int pilc_twar_forward(const uint8_t *img, uint8_t *res, int64_t n_img
     int64_t blocks = ceil_div64(n_px, threads);
     const int64_t cap = (int64_t)sm_count() * 32;
     if (blocks > cap) blocks = cap;
-    twar_forward_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
+{
+        ProfScope _ps(PROF_TWAR_FWD, as_stream(stream), 3.0 * n_px);
+        twar_forward_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
         img, res, n_px, H, W, load_params(params12_host));
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
@@ -195,8 +198,11 @@ extern "C" int pilc_twar_decode(const uint8_t *coded, const uint8_t *shift, uint
     int64_t blocks = ceil_div64(n_img, kDecWarps);
     const int64_t cap = (int64_t)sm_count() * 16;
     if (blocks > cap) blocks = cap;
-    twar_decode_kernel<<<(unsigned)blocks, 32 * kDecWarps, smem, as_stream(stream)>>>(
+{
+        ProfScope _ps(PROF_TWAR_DEC, as_stream(stream), (double)n_img * hw3);
+        twar_decode_kernel<<<(unsigned)blocks, 32 * kDecWarps, smem, as_stream(stream)>>>(
         coded, shift, img, n_img, H, W, load_params(params12_host), stage);
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

@@ -267,6 +267,9 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s) {
     if (blocks > 0x7FFFFFFF) return PILC_E_ARG;
     dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
     const size_t smem = conv_smem(a.ks, a.stride, co_t);
+    // algorithmic FLOPs of this conv (true channel counts, no padding)
+    const double flops = 2.0 * n_img * a.Ho * a.Wo * (double)a.Co * a.Ci * a.ks * a.ks;
+    ProfScope _ps(PROF_CONV, s, flops);
     switch (co_t) {
         case 32:
             cudaFuncSetAttribute(conv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -356,7 +359,10 @@ int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc,
     int64_t blocks = ceil_div64(n_vec, kArgWarps);
     const int64_t cap = (int64_t)sm_count() * 8;
     if (blocks > cap) blocks = cap;
-    argmin_kernel<<<(unsigned)blocks, 32 * kArgWarps, smem, s>>>(z, n_vec, cb, K, Dc, idx);
+{
+        ProfScope _ps(PROF_ARGMIN, s, 3.0 * n_vec * K * Dc);
+        argmin_kernel<<<(unsigned)blocks, 32 * kArgWarps, smem, s>>>(z, n_vec, cb, K, Dc, idx);
+    }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

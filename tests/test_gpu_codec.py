@@ -116,8 +116,12 @@ def test_lane_underflow_and_end_state_detected():
     trunc = BitStack.from_packed(np.frombuffer(raw[8:], np.uint8), nb - 40)
     with pytest.raises(CorruptStreamError):
         tables.interleaved_decode(tables.LaneSet(ls.states, [trunc]), 300, ds, dec)
-    with pytest.raises(CorruptStreamError):
-        tables.interleaved_decode(tables.LaneSet([ls.states[0] ^ 1], ls.streams), 300, ds, dec)
+    with pytest.raises(CorruptStreamError):  # recorded state outside [2^M, 2^(M+1))
+        tables.interleaved_decode(tables.LaneSet([(1 << 12) - 1], ls.streams), 300, ds, dec)
+    # an extra leading bit is left unconsumed -> end-state check
+    extra = BitStack.from_packed(np.frombuffer(raw[8:] + b"\x00", np.uint8), nb + 1)
+    with pytest.raises(CorruptStreamError, match="initial coder state|underflow"):
+        tables.interleaved_decode(tables.LaneSet(ls.states, [extra]), 300, ds, dec)
     del short
 
 
