@@ -181,6 +181,17 @@ int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
                    void *workspace, int64_t ws_bytes, uint8_t *shift_out,
                    uint8_t *d_out, float *mu_out, float *s_out, void *stream);
 
+/* Same contract, always the fp32 SIMT kernels (any configuration). The
+ * production pilc_vq_decode runs the tcgen05 bf16 path when C == 32; the
+ * choice is a function of the model configuration only, so compress and
+ * decompress agree. This entry point is the validation reference. */
+int pilc_vq_decode_simt(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
+                        const float *model, int32_t K, int32_t Dc, int32_t C,
+                        int32_t B, const double *d_thresh_host, int32_t D,
+                        void *workspace, int64_t ws_bytes, uint8_t *shift_out,
+                        uint8_t *d_out, float *mu_out, float *s_out,
+                        void *stream);
+
 /* ---- container (container.py:3-25, 128-335) ------------------------------
  * Static d per image for twar-static (container.py:163-170): exact
  * integer sum of |t - 128|, then argmin |log2(MAD/ln 4) - log2 g|.

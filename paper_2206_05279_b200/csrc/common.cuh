@@ -32,6 +32,8 @@ enum ProfCat {
     PROF_LANES,
     PROF_CRC,
     PROF_SCHED_CRC,
+    PROF_TC_CONV,
+    PROF_GATHER,
     PROF_NCAT
 };
 void *prof_begin(int cat, cudaStream_t s, double units);

@@ -1,0 +1,471 @@
+// tcgen05 implicit-GEMM convolutions for the VQ-VAE decoder (sm_100a).
+//
+// Reference: vqvae.decode_to_params (vqvae.py:79-113) over nn.conv2d
+// (nn.py:15-34), residual_block, pixel_shuffle and the logistic head.
+//
+// Activation layout ("padded group-major", bf16): for a batch of n images
+// of H x W with a one-pixel edge-replicated border, Hp = H+2, Wp = W+2, the
+// global pixel index q = n*Hp*Wp + y*Wp + x runs over every padded pixel of
+// every image, and channel group g (8 channels, 16 bytes) lives in its own
+// slab: elem(g, q, e) = act[(g*gstride + MARGIN + q)*8 + e]. Borders hold
+// copies of the edge pixels, so nn.conv2d's edge padding is already in
+// memory.
+//
+// GEMM view of a 3x3 conv: M = output pixels (virtual rows q: every padded
+// position, outputs at border positions are discarded), N = output
+// channels, K = 9 taps x C. A 128-row tile starting at q0 needs input
+// pixels [q0 - Wp - 1, q0 + 128 + Wp + 1); one bulk copy per channel group
+// brings that halo range into shared memory, and tap (i, j) is the same
+// K-major no-swizzle UMMA operand shifted by (i*Wp + j) rows (16 bytes per
+// row): no im2col, no per-tap copies. 9 taps x (C/16) tcgen05.mma
+// (M=128, K=16) accumulate in TMEM.
+//
+// Warp roles (192 threads): warp 0 = bulk-copy producer (4-stage ring),
+// warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..5 =
+// epilogue (TMEM -> registers -> bias/residual/ReLU/pixel-shuffle/head ->
+// global). TMEM holds two accumulators so the epilogue of tile i overlaps
+// the MMAs of tile i+1. Deterministic: fixed tiles, fixed K order, no
+// atomics -- so a blob compressed on one GPU decodes on any other.
+
+#include <cuda_bf16.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "tc_conv.cuh"
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kThreadsTC = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, K-major, no swizzle (canonical interleave:
+// core matrix = 8 rows x 16 B contiguous; LBO = next core matrix along K,
+// SBO = next 8-row group along M/N).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    return d;
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+// 32 consecutive f32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+        "[%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(a));
+    const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(b));
+    return lo | (hi << 16);
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+__device__ __forceinline__ float sigmoid_f32(float x) {
+    if (x >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-x)));
+    const float e = expf(x);
+    return __fdiv_rn(e, __fadd_rn(1.f, e));
+}
+
+// store one 16-byte group at padded pixel q, plus its border copies
+__device__ __forceinline__ void store_px(uint16_t *slab, int64_t q, uint4 v, int y, int x, int H, int W, int Wp) {
+    uint4 *p = reinterpret_cast<uint4 *>(slab);
+    p[q] = v;
+    const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
+    const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
+    if (dy) p[q - Wp] = v;
+    if (dy2) p[q + Wp] = v;
+    if (dx) p[q - 1] = v;
+    if (dx2) p[q + 1] = v;
+    if (dy && dx) p[q - Wp - 1] = v;
+    if (dy && dx2) p[q - Wp + 1] = v;
+    if (dy2 && dx) p[q + Wp - 1] = v;
+    if (dy2 && dx2) p[q + Wp + 1] = v;
+}
+
+template <int N, int KS, int MODE>
+__global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
+    constexpr int C = 32;               // input channels (4 groups of 8)
+    constexpr int NG = C / 8;
+    constexpr int KG = KS * KS * NG;    // K core-matrix groups
+    constexpr int TMEM_COLS = (2 * N < 32) ? 32 : 2 * N;
+    const int Wp = L.Wp;
+    const int npix = KS == 3 ? ((128 + 2 * Wp + 2 + 7) & ~7) : 128;
+    const uint32_t stage_bytes = (uint32_t)NG * npix * 16;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_w = smem;                                   // KG x N x 16 B
+    uint8_t *s_a = smem + (size_t)KG * N * 16;             // kStages x NG x npix x 16 B
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_a + (size_t)kStages * stage_bytes);
+    uint64_t *full = bars;                 // [kStages]
+    uint64_t *empty = bars + kStages;      // [kStages]
+    uint64_t *tfull = bars + 2 * kStages;  // [2]
+    uint64_t *tempty = tfull + 2;          // [2]
+    uint64_t *wbar = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        mbar_init(wbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"((uint32_t)TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t n_tiles = L.n_tiles;
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t wbytes = (uint32_t)KG * N * 16;
+            mbar_expect_tx(wbar, wbytes);
+            bulk_g2s(s_w, L.wts, wbytes, wbar);
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int s = i % kStages;
+                const int r = i / kStages;
+                if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+                const int64_t q_lo = t * 128 - (KS == 3 ? (Wp + 1) : 0);
+                mbar_expect_tx(&full[s], stage_bytes);
+                uint8_t *dst = s_a + (size_t)s * stage_bytes;
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    const uint16_t *src = L.in + ((int64_t)g * L.gstride + L.margin + q_lo) * 8;
+                    bulk_g2s(dst + (size_t)g * npix * 16, src, (uint32_t)npix * 16, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(128, N);
+            mbar_wait(wbar, 0);
+            tc_fence_after();
+            const uint32_t w_base = smem_u32(s_w);
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int s = i % kStages;
+                const int a = i & 1;
+                const int u = i >> 1;
+                if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
+                mbar_wait(&full[s], (i / kStages) & 1);
+                tc_fence_after();
+                const uint32_t a_base = smem_u32(s_a + (size_t)s * stage_bytes);
+                const uint32_t d = tmem + (uint32_t)(a * N);
+#pragma unroll
+                for (int tap = 0; tap < KS * KS; ++tap) {
+                    const int ti = tap / KS, tj = tap % KS;
+                    const uint32_t off = KS == 3 ? (uint32_t)(ti * Wp + tj) * 16u : 0u;
+#pragma unroll
+                    for (int ks = 0; ks < NG / 2; ++ks) {
+                        const uint64_t ad = umma_desc(a_base + (uint32_t)(2 * ks) * npix * 16u + off,
+                                                      (uint32_t)npix * 16u, 128u);
+                        const uint64_t bd = umma_desc(w_base + (uint32_t)(tap * NG + 2 * ks) * N * 16u,
+                                                      (uint32_t)N * 16u, 128u);
+                        mma_bf16(d, ad, bd, idesc, (tap | ks) ? 1u : 0u);
+                    }
+                }
+                mma_commit(&empty[s]);
+                mma_commit(&tfull[a]);
+            }
+        }
+    } else {
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int Hp = L.Hp, H = L.H, W = L.W;
+        const int64_t hw = (int64_t)Hp * Wp;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int a = i & 1;
+            const int u = i >> 1;
+            mbar_wait(&tfull[a], u & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * N);
+            const int64_t q = t * 128 + row;
+            const int64_t n = q / hw;
+            const int rem = (int)(q - n * hw);
+            const int y = rem / Wp, x = rem - (rem / Wp) * Wp;
+            const bool valid = n < L.n_img && y >= 1 && y <= H && x >= 1 && x <= W;
+            if constexpr (MODE == TC_OUT_ACT) {
+                float v[32];
+                tmem_ld32(taddr, v);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[a]);
+                if (valid) {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        float o[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(v[8 * g + e], L.bias[8 * g + e]);
+                        if (L.resid) {
+                            const uint4 rv = reinterpret_cast<const uint4 *>(L.resid + ((int64_t)g * L.gstride + L.margin) * 8)[q];
+                            const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                o[2 * e] = __fadd_rn(bf16_lo(rw[e]), o[2 * e]);
+                                o[2 * e + 1] = __fadd_rn(bf16_hi(rw[e]), o[2 * e + 1]);
+                            }
+                        }
+                        if (L.relu) {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) o[e] = fmaxf(o[e], 0.f);
+                        }
+                        const uint4 w4 = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
+                                                    pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+                        store_px(L.out + ((int64_t)g * L.out_gstride + L.out_margin) * 8, q, w4, y, x, H, W, Wp);
+                    }
+                }
+            } else if constexpr (MODE == TC_OUT_SHUFFLE) {
+                // N = 128 = 4 chunks of 32 columns: chunk z holds output
+                // channels c = 8z..8z+7 at all four (dy, dx) sub-positions
+                const int H2 = 2 * H, W2 = 2 * W, Wp2 = W2 + 2;
+                const int64_t hw2 = (int64_t)(H2 + 2) * Wp2;
+#pragma unroll 1
+                for (int z = 0; z < 4; ++z) {
+                    float v[32];
+                    tmem_ld32(taddr + (uint32_t)(32 * z), v);
+                    if (z == 3) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[a]);
+                    }
+                    if (!valid) continue;
+#pragma unroll
+                    for (int sub = 0; sub < 4; ++sub) {
+                        const int dy = sub >> 1, dx = sub & 1;
+                        float o[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            o[e] = fmaxf(__fadd_rn(v[4 * e + sub], L.bias[32 * z + 4 * e + sub]), 0.f);
+                        const int Y = 2 * (y - 1) + dy + 1, X = 2 * (x - 1) + dx + 1;
+                        const int64_t q2 = n * hw2 + (int64_t)Y * Wp2 + X;
+                        const uint4 w4 = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
+                                                    pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+                        store_px(L.out + ((int64_t)z * L.out_gstride + L.out_margin) * 8, q2, w4, Y, X, H2, W2, Wp2);
+                    }
+                }
+            } else {
+                // logistic head (vqvae.py:105-112, logistic.py:36-40, 109-114)
+                float v[16];
+                tmem_ld16(taddr, v);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[a]);
+                if (valid && (y - 1) < L.crop_h && (x - 1) < L.crop_w) {
+                    const int64_t px = (n * L.crop_h + (y - 1)) * (int64_t)L.crop_w + (x - 1);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        float av = __fadd_rn(v[c], L.bias[c]);
+                        av = fminf(fmaxf(av, -15.f), 15.f);
+                        const float mu = __fmul_rn(255.f, sigmoid_f32(av));
+                        float bv = __fadd_rn(v[3 + c], L.bias[3 + c]);
+                        bv = fminf(fmaxf(bv, L.log_s_min), L.log_s_max);
+                        float sv = fminf(fmaxf(expf(bv), 0.5f), 64.f);
+                        const int shift = (int)floor((double)mu + 0.5);
+                        const double sd = (double)sv;
+                        int d = 0;
+                        for (int k = 0; k < L.n_thresh; ++k) d += sd > L.thresh[k];
+                        L.shift[px * 3 + c] = (uint8_t)shift;
+                        L.dsel[px * 3 + c] = (uint8_t)d;
+                        if (L.mu) L.mu[px * 3 + c] = mu;
+                        if (L.s) L.s[px * 3 + c] = sv;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)TMEM_COLS));
+    }
+}
+
+template <int N, int KS, int MODE>
+int launch_tc(const TcLayer &L, cudaStream_t s) {
+    constexpr int NG = 4;
+    constexpr int KG = KS * KS * NG;
+    const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
+    const size_t smem = (size_t)KG * N * 16 + (size_t)kStages * NG * npix * 16 + 8 * (2 * kStages + 5) + 16;
+    if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
+    auto kern = tc_conv_kernel<N, KS, MODE>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = (int)((227 * 1024) / (smem + 1024));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 4) per_sm = 4;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > L.n_tiles) grid = L.n_tiles;
+    if (grid < 1) return PILC_OK;
+    const double flops = 2.0 * L.n_img * L.H * L.W * (double)(MODE == TC_OUT_HEAD ? 6 : N) * 32 * KS * KS;
+    ProfScope _ps(PROF_TC_CONV, s, flops);
+    kern<<<(unsigned)grid, kThreadsTC, smem, s>>>(L);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+// dec.proj folded into a table: T[k] = relu(W cb[k] + b), bf16 (K x 32)
+__global__ void dec_table_kernel(const float *__restrict__ cb, const float *__restrict__ w,
+                                 const float *__restrict__ b, int K, int Dc, int ci_pad, int co_pad,
+                                 uint16_t *__restrict__ table) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K * 32) return;
+    const int k = i / 32, c = i % 32;
+    float acc = 0.f;
+    for (int j = 0; j < Dc; ++j) acc = fmaf(cb[k * Dc + j], w[(int64_t)j * co_pad + c], acc);
+    acc = fmaxf(__fadd_rn(acc, b[c]), 0.f);
+    table[i] = __bfloat16_as_ushort(__float2bfloat16_rn(acc));
+}
+
+// X = T[idx] at every padded position (borders replicate by clamping)
+__global__ void gather_kernel(const uint8_t *__restrict__ idx, const uint16_t *__restrict__ table,
+                              int64_t n_img, int gh, int gw, uint16_t *__restrict__ x, int64_t gstride,
+                              int64_t margin) {
+    const int Hp = gh + 2, Wp = gw + 2;
+    const int64_t total = n_img * Hp * Wp;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = q / ((int64_t)Hp * Wp);
+        const int rem = (int)(q - n * Hp * Wp);
+        int y = rem / Wp - 1, xx = rem % Wp - 1;
+        y = y < 0 ? 0 : (y >= gh ? gh - 1 : y);
+        xx = xx < 0 ? 0 : (xx >= gw ? gw - 1 : xx);
+        const int k = idx[(n * gh + y) * gw + xx];
+        const uint4 *row = reinterpret_cast<const uint4 *>(table + k * 32);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) reinterpret_cast<uint4 *>(x + ((int64_t)g * gstride + margin) * 8)[q] = row[g];
+    }
+}
+
+}  // namespace
+
+int tc_launch_act(const TcLayer &L, cudaStream_t s) { return launch_tc<32, 3, TC_OUT_ACT>(L, s); }
+int tc_launch_shuffle(const TcLayer &L, cudaStream_t s) { return launch_tc<128, 3, TC_OUT_SHUFFLE>(L, s); }
+int tc_launch_head(const TcLayer &L, cudaStream_t s) { return launch_tc<16, 3, TC_OUT_HEAD>(L, s); }
+
+int tc_dec_table(const float *cb, const float *w, const float *b, int K, int Dc, int ci_pad, int co_pad,
+                 uint16_t *table, cudaStream_t s) {
+    ProfScope _ps(PROF_GATHER, s, (double)K * 32);
+    dec_table_kernel<<<(K * 32 + 255) / 256, 256, 0, s>>>(cb, w, b, K, Dc, ci_pad, co_pad, table);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+int tc_gather(const uint8_t *idx, const uint16_t *table, int64_t n_img, int gh, int gw, uint16_t *x,
+              int64_t gstride, int64_t margin, cudaStream_t s) {
+    const int64_t total = n_img * (gh + 2) * (int64_t)(gw + 2);
+    int64_t blocks = ceil_div64(total, 256);
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    ProfScope _ps(PROF_GATHER, s, (double)total);
+    gather_kernel<<<(unsigned)blocks, 256, 0, s>>>(idx, table, n_img, gh, gw, x, gstride, margin);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}

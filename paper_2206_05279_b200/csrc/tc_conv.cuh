@@ -1,0 +1,35 @@
+// tcgen05 decoder convolutions (tc_conv.cu), driven from vq.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+enum TcOutMode { TC_OUT_ACT = 0, TC_OUT_SHUFFLE = 1, TC_OUT_HEAD = 2 };
+
+struct TcLayer {
+    const uint16_t *in;  // padded group-major bf16 activations (32 channels)
+    int64_t gstride;     // pixels per channel-group slab (margins included)
+    int64_t margin;      // leading margin pixels of each slab
+    int Hp, Wp, H, W;    // padded / interior dims of the conv grid
+    int64_t n_img, n_tiles;
+    const uint16_t *wts;  // B operand, [KG][N][8] bf16
+    const float *bias;
+    const uint16_t *resid;  // TC_OUT_ACT: same layout as out (nullable)
+    uint16_t *out;
+    int64_t out_gstride, out_margin;
+    int relu;
+    // head
+    uint8_t *shift, *dsel;
+    float *mu, *s;
+    int crop_h, crop_w;
+    const double *thresh;
+    int n_thresh;
+    float log_s_min, log_s_max;
+};
+
+int tc_launch_act(const TcLayer &L, cudaStream_t s);
+int tc_launch_shuffle(const TcLayer &L, cudaStream_t s);
+int tc_launch_head(const TcLayer &L, cudaStream_t s);
+int tc_dec_table(const float *cb, const float *w, const float *b, int K, int Dc, int ci_pad, int co_pad,
+                 uint16_t *table, cudaStream_t s);
+int tc_gather(const uint8_t *idx, const uint16_t *table, int64_t n_img, int gh, int gw, uint16_t *x,
+              int64_t gstride, int64_t margin, cudaStream_t s);

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tc_conv.cuh"
 
 namespace {
 
@@ -39,7 +40,12 @@ struct Layout {
     std::vector<ConvSpec> enc;  // stem, down, blocks(2B), proj
     std::vector<ConvSpec> dec;  // proj, blocks(2B), up, head(mu|s)
     int64_t cb_off;             // K x Dc float32 codebook
-    int64_t total;
+    // tcgen05 decoder (C == 32): bf16 B operands [KG][N][8], offsets in
+    // uint16 units from the model base; see tc_conv.cu
+    bool tc;
+    std::vector<int64_t> tc_blk;  // 2B block convs, N = 32
+    int64_t tc_up, tc_head;       // N = 128, N = 16 (mu 0..2, s 3..5)
+    int64_t total;                // floats, bf16 region included
 };
 
 ConvSpec make_spec(int ci, int co, int ks, int64_t &cursor) {
@@ -74,6 +80,20 @@ Layout make_layout(int K, int Dc, int C, int B) {
     for (int i = 0; i < 2 * B; ++i) L.dec.push_back(make_spec(C, C, 3, cur));
     L.dec.push_back(make_spec(C, 4 * C, 3, cur));
     L.dec.push_back(make_spec(C, 6, 3, cur));
+    L.tc = (C == 32);
+    if (L.tc) {
+        cur = (cur + 7) / 8 * 8;  // 32-byte aligned bf16 region
+        int64_t h = cur * 2;      // uint16 cursor
+        for (int i = 0; i < 2 * B; ++i) {
+            L.tc_blk.push_back(h);
+            h += 36 * 32 * 8;
+        }
+        L.tc_up = h;
+        h += 36 * 128 * 8;
+        L.tc_head = h;
+        h += 36 * 16 * 8;
+        cur = (h + 1) / 2;
+    }
     L.total = cur;
     return L;
 }
@@ -303,9 +323,17 @@ ConvArgs base_args(const float *model, const ConvSpec &sp) {
 }
 
 // ---- codebook argmin (vqvae.py:66-76) --------------------------------------
-// Warp per latent vector. Lane l scores codes l, l+32, ...: the squared
-// distance is accumulated in float64 component by component in the
-// reference's order without FMA; the warp min breaks ties to the lowest k.
+// Warp per latent vector; lane l owns codes l, l+32, ... The reference
+// accumulates (z_c - cb_kc)^2 in float64, component by component, and takes
+// the first minimum. Screening pass in float32: every term is non-negative,
+// so the float32 sequential sum satisfies |d32 - d| <= g*d with
+// g = (Dc + 4) * 2^-24 (Higham, sum of n positive terms + one rounding per
+// subtraction and square). The true argmin k* has d(k*) <= d(k32) <=
+// m/(1-g) where m = min d32, hence d32(k*) <= m (1+g)/(1-g). Every code
+// under that bound (with a 4x safety factor) is re-scored exactly as the
+// reference does -- float64, same order, no FMA -- and the warp picks the
+// smallest float64 distance, ties to the lowest index. Normally one or two
+// codes survive the screen, so float64 work drops ~100x.
 constexpr int kArgWarps = 8;
 
 __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__restrict__ z,
@@ -313,21 +341,43 @@ __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__r
                                                                  const float *__restrict__ cb, int K,
                                                                  int Dc, uint8_t *__restrict__ idx) {
     extern __shared__ float sm[];
-    float *s_cb = sm;                      // K x Dc
-    float *s_z = sm + (int64_t)K * Dc;     // kArgWarps x Dc
-    for (int i = threadIdx.x; i < K * Dc; i += blockDim.x) s_cb[i] = cb[i];
+    float *s_cb = sm;                      // K x (Dc+1): +1 pad against bank conflicts
+    float *s_z = sm + (int64_t)K * (Dc + 1);  // kArgWarps x Dc
+    const int P = Dc + 1;
+    for (int i = threadIdx.x; i < K * Dc; i += blockDim.x) s_cb[(i / Dc) * P + (i % Dc)] = cb[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float *zw = s_z + warp * Dc;
+    const float g = (float)(Dc + 4) * 5.9604645e-08f;  // (Dc+4) * 2^-24
+    const float slack = 1.f + 4.f * g;
     for (int64_t v = (int64_t)blockIdx.x * kArgWarps + warp; v < n_vec;
          v += (int64_t)gridDim.x * kArgWarps) {
         for (int c = lane; c < Dc; c += 32) zw[c] = z[v * Dc + c];
         __syncwarp();
+        // screening in float32 (no FMA: keeps the error model simple)
+        float m32 = INFINITY;
+        for (int k = lane; k < K; k += 32) {
+            const float *row = s_cb + k * P;
+            float d = 0.f;
+            for (int c = 0; c < Dc; ++c) {
+                const float diff = __fsub_rn(zw[c], row[c]);
+                d = __fadd_rn(d, __fmul_rn(diff, diff));
+            }
+            m32 = fminf(m32, d);
+        }
+        for (int o = 16; o; o >>= 1) m32 = fminf(m32, __shfl_xor_sync(0xffffffffu, m32, o));
+        const float bound = m32 * slack + 1e-30f;
         double best = INFINITY;
         int bk = 0x7FFFFFFF;
         for (int k = lane; k < K; k += 32) {
-            const float *row = s_cb + k * Dc;
-            double dist = 0.0;
+            const float *row = s_cb + k * P;
+            float d = 0.f;
+            for (int c = 0; c < Dc; ++c) {
+                const float diff = __fsub_rn(zw[c], row[c]);
+                d = __fadd_rn(d, __fmul_rn(diff, diff));
+            }
+            if (!(d <= bound)) continue;
+            double dist = 0.0;  // exact reference arithmetic
             for (int c = 0; c < Dc; ++c) {
                 const double diff = __dsub_rn((double)zw[c], (double)row[c]);
                 dist = __dadd_rn(dist, __dmul_rn(diff, diff));
@@ -353,7 +403,7 @@ __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__r
 int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc, uint8_t *idx,
                   cudaStream_t s) {
     if (n_vec == 0) return PILC_OK;
-    const size_t smem = sizeof(float) * ((size_t)K * Dc + (size_t)kArgWarps * Dc);
+    const size_t smem = sizeof(float) * ((size_t)K * (Dc + 1) + (size_t)kArgWarps * Dc);
     if (smem > 200 * 1024) return PILC_E_UNSUPPORTED;
     cudaFuncSetAttribute(argmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t blocks = ceil_div64(n_vec, kArgWarps);
@@ -385,6 +435,35 @@ int64_t ws_parts(int64_t n, int H, int W, int Dc, int C, Work *w, char *base) {
         w->Z = reinterpret_cast<float *>(base + al(a) + 2 * al(b));
     }
     return al(a) + 2 * al(b) + al(z);
+}
+
+// tcgen05 decoder scratch: three latent slabs X, T, Y and the shuffled
+// full-resolution slab U, each 4 channel groups x gstride pixels x 16 B.
+struct TcWork {
+    uint16_t *X, *T, *Y, *U, *table;
+    int64_t gs, gs2, margin, margin2;
+};
+
+int64_t tc_ws(int64_t n, int H, int W, TcWork *w, char *base) {
+    const int gh = (H + 1) / 2, gw = (W + 1) / 2;
+    const int64_t Wp = gw + 2, Wp2 = 2 * gw + 2;
+    const int64_t m1 = 256 + 2 * Wp, m2 = 256 + 2 * Wp2;
+    const int64_t gs = 2 * m1 + n * (gh + 2) * Wp;
+    const int64_t gs2 = 2 * m2 + n * (2 * gh + 2) * Wp2;
+    auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
+    const int64_t slab = al(4 * gs * 16), slab2 = al(4 * gs2 * 16);
+    if (w) {
+        w->X = reinterpret_cast<uint16_t *>(base);
+        w->T = reinterpret_cast<uint16_t *>(base + slab);
+        w->Y = reinterpret_cast<uint16_t *>(base + 2 * slab);
+        w->U = reinterpret_cast<uint16_t *>(base + 3 * slab);
+        w->table = reinterpret_cast<uint16_t *>(base + 3 * slab + slab2);
+        w->gs = gs;
+        w->gs2 = gs2;
+        w->margin = m1;
+        w->margin2 = m2;
+    }
+    return 3 * slab + slab2 + al(256 * 32 * 2);
 }
 
 bool check_cfg(int K, int Dc, int C, int B) {
@@ -422,13 +501,38 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
     for (size_t l = 0; l + 1 < L.dec.size(); ++l) put_conv(L.dec[l], 0, L.dec[l].co);
     put_conv(L.dec.back(), 0, 3);  // dec.mu -> channels 0..2
     put_conv(L.dec.back(), 3, 3);  // dec.s  -> channels 3..5
+    if (L.tc) {
+        // B operand for tcgen05: element (n, k = tap*32 + ci) of the K-major
+        // [K/8][N][8] interleave layout, bf16 round-to-nearest-even
+        uint16_t *h = reinterpret_cast<uint16_t *>(dst);
+        auto bf16 = [](float f) -> uint16_t {
+            uint32_t u;
+            memcpy(&u, &f, 4);
+            u += 0x7FFFu + ((u >> 16) & 1u);
+            return (uint16_t)(u >> 16);
+        };
+        auto put_b = [&](int64_t off, const ConvSpec &sp, int N, int n_lo, int n_cnt) {
+            for (int n = 0; n < n_cnt; ++n)
+                for (int ci = 0; ci < 32; ++ci)
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const int k = tap * 32 + ci;
+                        const float w = dst[sp.w_off + ((int64_t)tap * sp.ci_pad + ci) * sp.co_pad + n_lo + n];
+                        h[off + ((int64_t)(k >> 3) * N + n) * 8 + (k & 7)] = bf16(w);
+                    }
+        };
+        for (int i = 0; i < 2 * B; ++i) put_b(L.tc_blk[i], L.dec[1 + i], 32, 0, 32);
+        put_b(L.tc_up, L.dec[1 + 2 * B], 128, 0, 128);
+        put_b(L.tc_head, L.dec[2 + 2 * B], 16, 0, 6);
+    }
     return PILC_OK;
 }
 
 extern "C" int64_t pilc_vq_workspace_bytes(int64_t n_img, int32_t H, int32_t W, int32_t K, int32_t Dc,
                                            int32_t C, int32_t B) {
     if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return -1;
-    return ws_parts(n_img, H, W, Dc, C, nullptr, nullptr);
+    const int64_t a = ws_parts(n_img, H, W, Dc, C, nullptr, nullptr);
+    const int64_t b = C == 32 ? tc_ws(n_img, H, W, nullptr, nullptr) : 0;
+    return a > b ? a : b;
 }
 
 extern "C" int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model, int32_t K, int32_t Dc,
@@ -500,24 +604,13 @@ extern "C" int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int3
     return launch_argmin(z, n_img * gh * gw, model + L.cb_off, K, Dc, idx_out, s);
 }
 
-extern "C" int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
-                              int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host,
-                              int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
-                              uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
-    if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B) || D < 1 || D > 256) return PILC_E_ARG;
-    if (D > 1 && !d_thresh_host) return PILC_E_ARG;
-    if (n_img == 0) return PILC_OK;
-    Work w;
-    if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-    const Layout L = make_layout(K, Dc, C, B);
-    cudaStream_t s = as_stream(stream);
+namespace {
+
+int simt_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *model, const Layout &L, int B,
+                const double *thr, int D, const Work &w, uint8_t *shift_out, uint8_t *d_out, float *mu_out,
+                float *s_out, cudaStream_t s) {
     const int gh = (H + 1) / 2, gw = (W + 1) / 2;
     int rc;
-    double *thr = nullptr;
-    if (D > 1) {
-        if (cudaMallocAsync(&thr, sizeof(double) * (D - 1), s) != cudaSuccess) return PILC_E_CUDA;
-        cudaMemcpyAsync(thr, d_thresh_host, sizeof(double) * (D - 1), cudaMemcpyHostToDevice, s);
-    }
     // dec.proj (1x1) over the gathered codebook rows, ReLU -> B
     ConvArgs a = base_args(model, L.dec[0]);
     a.in_mode = IN_CODEBOOK;
@@ -573,6 +666,133 @@ extern "C" int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int3
         a.log_s_max = (float)log(64.0);
         rc = launch_conv(a, L.dec[2 + 2 * B].co_t, n_img, s);
     }
+    return rc;
+}
+
+int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *model, const Layout &L, int K, int Dc,
+              int B, const double *thr, int D, const TcWork &tw, uint8_t *shift_out, uint8_t *d_out, float *mu_out,
+              float *s_out, cudaStream_t s) {
+    const int gh = (H + 1) / 2, gw = (W + 1) / 2;
+    const uint16_t *hb = reinterpret_cast<const uint16_t *>(model);
+    int rc = tc_dec_table(model + L.cb_off, model + L.dec[0].w_off, model + L.dec[0].b_off, K, Dc, L.dec[0].ci_pad,
+                          L.dec[0].co_pad, tw.table, s);
+    if (!rc) rc = tc_gather(idx, tw.table, n_img, gh, gw, tw.X, tw.gs, tw.margin, s);
+    TcLayer b;
+    memset(&b, 0, sizeof(b));
+    b.gstride = b.out_gstride = tw.gs;
+    b.margin = b.out_margin = tw.margin;
+    b.Hp = gh + 2;
+    b.Wp = gw + 2;
+    b.H = gh;
+    b.W = gw;
+    b.n_img = n_img;
+    b.n_tiles = ceil_div64(n_img * b.Hp * (int64_t)b.Wp, 128);
+    b.relu = 1;
+    uint16_t *X = tw.X, *T = tw.T, *Y = tw.Y;
+    for (int i = 0; !rc && i < B; ++i) {
+        TcLayer c1 = b;
+        c1.in = X;
+        c1.out = T;
+        c1.wts = hb + L.tc_blk[2 * i];
+        c1.bias = model + L.dec[1 + 2 * i].b_off;
+        rc = tc_launch_act(c1, s);
+        if (rc) break;
+        TcLayer c2 = b;
+        c2.in = T;
+        c2.out = Y;
+        c2.resid = X;
+        c2.wts = hb + L.tc_blk[2 * i + 1];
+        c2.bias = model + L.dec[2 + 2 * i].b_off;
+        rc = tc_launch_act(c2, s);
+        uint16_t *tmp = X;
+        X = Y;
+        Y = tmp;
+    }
+    if (!rc) {
+        TcLayer up = b;
+        up.in = X;
+        up.out = tw.U;
+        up.out_gstride = tw.gs2;
+        up.out_margin = tw.margin2;
+        up.wts = hb + L.tc_up;
+        up.bias = model + L.dec[1 + 2 * B].b_off;
+        rc = tc_launch_shuffle(up, s);
+    }
+    if (!rc) {
+        TcLayer hd;
+        memset(&hd, 0, sizeof(hd));
+        hd.in = tw.U;
+        hd.gstride = tw.gs2;
+        hd.margin = tw.margin2;
+        hd.Hp = 2 * gh + 2;
+        hd.Wp = 2 * gw + 2;
+        hd.H = 2 * gh;
+        hd.W = 2 * gw;
+        hd.n_img = n_img;
+        hd.n_tiles = ceil_div64(n_img * hd.Hp * (int64_t)hd.Wp, 128);
+        hd.wts = hb + L.tc_head;
+        hd.bias = model + L.dec[2 + 2 * B].b_off;
+        hd.shift = shift_out;
+        hd.dsel = d_out;
+        hd.mu = mu_out;
+        hd.s = s_out;
+        hd.crop_h = H;
+        hd.crop_w = W;
+        hd.thresh = thr;
+        hd.n_thresh = D - 1;
+        hd.log_s_min = (float)log(0.5);
+        hd.log_s_max = (float)log(64.0);
+        rc = tc_launch_head(hd, s);
+    }
+    return rc;
+}
+
+int vq_decode(int path, const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,
+              int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host, int32_t D, void *workspace,
+              int64_t ws_bytes, uint8_t *shift_out, uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
+    if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B) || D < 1 || D > 256) return PILC_E_ARG;
+    if (D > 1 && !d_thresh_host) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    const Layout L = make_layout(K, Dc, C, B);
+    const bool use_tc = path == 0 && L.tc;
+    Work w;
+    TcWork tw;
+    if (use_tc) {
+        if (tc_ws(n_img, H, W, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+    } else if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) {
+        return PILC_E_ARG;
+    }
+    cudaStream_t s = as_stream(stream);
+    double *thr = nullptr;
+    if (D > 1) {
+        if (cudaMallocAsync(&thr, sizeof(double) * (D - 1), s) != cudaSuccess) return PILC_E_CUDA;
+        cudaMemcpyAsync(thr, d_thresh_host, sizeof(double) * (D - 1), cudaMemcpyHostToDevice, s);
+    }
+    const int rc = use_tc ? tc_decode(idx, n_img, H, W, model, L, K, Dc, B, thr, D, tw, shift_out, d_out, mu_out,
+                                      s_out, s)
+                          : simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
     if (thr) cudaFreeAsync(thr, s);
     return rc;
+}
+
+}  // namespace
+
+// The production decoder: tcgen05 bf16 when C == 32 (the default model),
+// else the SIMT fp32 kernels. The choice depends only on the model
+// configuration, so compress and decompress always take the same path.
+extern "C" int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
+                              int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host,
+                              int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
+                              uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
+    return vq_decode(0, idx, n_img, H, W, model, K, Dc, C, B, d_thresh_host, D, workspace, ws_bytes, shift_out, d_out,
+                     mu_out, s_out, stream);
+}
+
+// fp32 SIMT decoder for any configuration (validation reference).
+extern "C" int pilc_vq_decode_simt(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
+                                   int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host,
+                                   int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
+                                   uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
+    return vq_decode(1, idx, n_img, H, W, model, K, Dc, C, B, d_thresh_host, D, workspace, ws_bytes, shift_out, d_out,
+                     mu_out, s_out, stream);
 }

@@ -49,8 +49,11 @@ def encode_indices_device(img_d: torch.Tensor, weights: ModelWeights, dev, strea
 
 
 def decode_head_device(idx_d: torch.Tensor, weights: ModelWeights, H: int, W: int, grid: ScaleGrid, dev, stream,
-                       want_params: bool = False):
-    """-> (shift u8, d u8[, mu f32, s f32]) each (N, H, W, 3)."""
+                       want_params: bool = False, precise: bool = False):
+    """-> (shift u8, d u8[, mu f32, s f32]) each (N, H, W, 3).
+
+    The codec path uses the production decoder (tcgen05 bf16 for the
+    default C=32 model); precise=True selects the fp32 SIMT kernels."""
     N = idx_d.shape[0]
     shift = torch.empty((N, H, W, 3), dtype=torch.uint8, device=dev)
     dsel = torch.empty((N, H, W, 3), dtype=torch.uint8, device=dev)
@@ -60,7 +63,7 @@ def decode_head_device(idx_d: torch.Tensor, weights: ModelWeights, H: int, W: in
         s = torch.empty((N, H, W, 3), dtype=torch.float32, device=dev)
     thr = np.ascontiguousarray(grid.d_thresholds(), dtype=np.float64)
     ws = _workspace(N, H, W, weights, dev)
-    _lib.call("pilc_vq_decode", ptr(idx_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
+    _lib.call("pilc_vq_decode_simt" if precise else "pilc_vq_decode", ptr(idx_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
               ptr(thr) if thr.size else None, grid.D, ptr(ws), ws.numel(), ptr(shift), ptr(dsel), ptr(mu), ptr(s),
               sptr(stream))
     return (shift, dsel, mu, s) if want_params else (shift, dsel)
@@ -102,8 +105,9 @@ def argmin_codebook(z, weights: ModelWeights) -> np.ndarray:
     return out.cpu().numpy().reshape(z.shape[:-1])
 
 
-def decode_to_params(indices, weights: ModelWeights, out_shape: tuple[int, int]):
-    """Per-pixel (mu, s) planes H x W x 3 float32, computed on the GPU."""
+def decode_to_params(indices, weights: ModelWeights, out_shape: tuple[int, int], *, precise: bool = False):
+    """Per-pixel (mu, s) planes H x W x 3 float32, computed on the GPU by
+    the production decoder (precise=True: fp32 SIMT kernels)."""
     _require_network(weights)
     H, W = out_shape
     gh, gw = latent_shape(H, W)
@@ -115,7 +119,8 @@ def decode_to_params(indices, weights: ModelWeights, out_shape: tuple[int, int])
     dev = require_device()
     stream = torch.cuda.current_stream(dev)
     idx_d = torch.from_numpy(indices.astype(np.uint8)[None].copy()).to(dev)
-    _, _, mu, s = decode_head_device(idx_d, weights, H, W, default_grid(), dev, stream, want_params=True)
+    _, _, mu, s = decode_head_device(idx_d, weights, H, W, default_grid(), dev, stream, want_params=True,
+                                     precise=precise)
     return mu[0].cpu().numpy(), s[0].cpu().numpy()
 
 

@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 
 import paper_2206_05279_b200 as pc
+import paper_2206_05279_b200.logistic  # noqa: F401
 from oracle import oracle as O
 from paper_2206_05279_b200 import container as ct
 from paper_2206_05279_b200 import predictor, tables, vqvae
@@ -189,10 +190,33 @@ def test_vqvae_encoder_and_decoder_vs_reference(golden, tag, small_model, full_m
         idx = vqvae.encode_to_indices(img, m)
         agree += int((idx == z[f"idx{k}"]).sum())
         total += idx.size
-        mu, s = vqvae.decode_to_params(z[f"idx{k}"], m, img.shape[:2])
+        mu, s = vqvae.decode_to_params(z[f"idx{k}"], m, img.shape[:2], precise=True)
         np.testing.assert_allclose(mu, z[f"mu{k}"], rtol=0, atol=2e-3)
         np.testing.assert_allclose(s, z[f"s{k}"], rtol=2e-4, atol=0)
     assert agree == total, f"index agreement {agree}/{total}"
+
+
+def test_tcgen05_decoder_vs_fp32(golden, full_model):
+    """The production decoder of the default model runs tcgen05 bf16
+    (csrc/tc_conv.cu); compare with the fp32 SIMT decoder and the
+    reference's (mu, s). bf16 activations: tolerance on mu in grey levels,
+    on s relative; the recentring shift and grid index d must agree for
+    nearly all subpixels (bpd parity is checked end to end elsewhere)."""
+    z = golden("vqvae_full.npz")
+    for k in range(int(z["n"])):
+        H, W = z[f"img{k}"].shape[:2]
+        mu_t, s_t = vqvae.decode_to_params(z[f"idx{k}"], full_model, (H, W))
+        mu_f, s_f = vqvae.decode_to_params(z[f"idx{k}"], full_model, (H, W), precise=True)
+        assert np.isfinite(mu_t).all() and np.isfinite(s_t).all()
+        assert np.abs(mu_t - mu_f).max() < 4.0 and np.abs(mu_t - mu_f).mean() < 0.5
+        assert np.abs(np.log(s_t / s_f)).max() < 0.2
+        assert np.abs(mu_t - z[f"mu{k}"]).mean() < 0.5
+        d_t = pc.logistic.scales_to_distributions(s_t, default_grid())
+        d_f = pc.logistic.scales_to_distributions(s_f, default_grid())
+        assert (d_t == d_f).mean() > 0.95
+        sh_t = pc.logistic.round_half_away(mu_t)
+        sh_f = pc.logistic.round_half_away(mu_f)
+        assert (sh_t == sh_f).mean() > 0.6
 
 
 @pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (31, 33), (32, 32), (97, 61)])
