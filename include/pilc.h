@@ -173,11 +173,11 @@ int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model,
 /* decode_to_params (vqvae.py:79-113) fused with the logistic head
  * (logistic.round_half_away / scales_to_distributions, logistic.py:36-40,
  * 109-114): indices -> shift = round(mu) and d per subpixel (N, H, W, 3)
- * uint8. d_thresh_host: D-1 float64 thresholds, d = #{k : s > t_k}.
+ * uint8. d_thresh: D-1 float64 thresholds (device), d = #{k : s > t_k}.
  * mu_out / s_out (nullable) receive the float32 planes. */
 int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
                    const float *model, int32_t K, int32_t Dc, int32_t C,
-                   int32_t B, const double *d_thresh_host, int32_t D,
+                   int32_t B, const double *d_thresh, int32_t D,
                    void *workspace, int64_t ws_bytes, uint8_t *shift_out,
                    uint8_t *d_out, float *mu_out, float *s_out, void *stream);
 
@@ -187,7 +187,7 @@ int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
  * decompress agree. This entry point is the validation reference. */
 int pilc_vq_decode_simt(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
                         const float *model, int32_t K, int32_t Dc, int32_t C,
-                        int32_t B, const double *d_thresh_host, int32_t D,
+                        int32_t B, const double *d_thresh, int32_t D,
                         void *workspace, int64_t ws_bytes, uint8_t *shift_out,
                         uint8_t *d_out, float *mu_out, float *s_out,
                         void *stream);
@@ -195,23 +195,22 @@ int pilc_vq_decode_simt(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
 /* ---- container (container.py:3-25, 128-335) ------------------------------
  * Static d per image for twar-static (container.py:163-170): exact
  * integer sum of |t - 128|, then argmin |log2(MAD/ln 4) - log2 g|.
- * log2_grid_host: D float64 log2 of the grid values. */
+ * log2_grid: D float64 log2 of the grid values (device). */
 int pilc_static_scale(const uint8_t *res, int64_t n_img, int64_t n_sym,
-                      const double *log2_grid_host, int32_t D,
+                      const double *log2_grid, int32_t D,
                       uint16_t *d_img, void *stream);
 
 /* Blob sizes and offsets: blob_off[0..n_img] (exclusive scan, uint64).
  * fixed_bytes = header + stream tables (+ schedule crc) + 4-byte crc.
- * idx_nbits may be NULL (twar-static). total_host (nullable, pinned)
- * receives blob_off[n_img] asynchronously. */
+ * idx_nbits may be NULL (twar-static). sizes: n_img uint64 scratch. */
 int pilc_container_sizes(const uint32_t *idx_nbits, const uint32_t *res_nbits,
                          int64_t n_img, int32_t lanes, int64_t fixed_bytes,
-                         uint64_t *blob_off, void *stream);
-/* Pack blobs (container.py:174-191): template = header prefix up to and
- * including the params/model hash (static_d at byte 19 is patched per
- * image from d_img); then stream tables, optional schedule crc32 over
+                         uint64_t *sizes, uint64_t *blob_off, void *stream);
+/* Pack blobs (container.py:174-191): template (device) = header prefix up
+ * to and including the params/model hash (static_d at byte 19 is patched
+ * per image from d_img); then stream tables, optional schedule crc32 over
  * the u16 LE d schedule (dsched or d_img), lane wire blobs, crc32. */
-int pilc_container_pack(const uint8_t *template_host, int32_t template_len,
+int pilc_container_pack(const uint8_t *tmpl, int32_t template_len,
                         const uint16_t *d_img, const uint8_t *dsched,
                         int32_t sched_check, int64_t n_img, int64_t n_sym,
                         int32_t lanes, const uint32_t *idx_scratch,

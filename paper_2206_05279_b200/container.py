@@ -31,12 +31,12 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import as_device_u8, h2d, pinned, ptr, require_device, sptr
+from .device import CACHE, as_device_u8, h2d, pinned, ptr, require_device, sptr
 from .errors import CorruptStreamError, FormatError, ModelError, ParameterError
 from .logistic import ScaleGrid, default_grid, residual_distributions
 from .predictor import PredictorParams, decode_device, default_params, forward_residual_device, validate_image
 from .tables import build_tables, encode_lanes_device
-from .vqvae import decode_head_device, encode_indices_device, index_histogram_pmf, latent_shape
+from .vqvae import decode_head_device, encode_indices_device, grid_device, index_histogram_pmf, latent_shape
 from .weights import ModelWeights
 
 MAGIC = b"PILC"
@@ -130,7 +130,7 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
         idx_scr, idx_cap, idx_nb, idx_st = encode_lanes_device(idx_d, N, gh * gw, L, idx_enc, dev, stream)
     else:
         d_img = torch.empty(N, dtype=torch.int16, device=dev)
-        lg = np.ascontiguousarray(np.log2(grid.values), dtype=np.float64)
+        lg = grid_device(grid, dev)[0]
         _lib.call("pilc_static_scale", ptr(t_d), N, n_sym, ptr(lg), grid.D, ptr(d_img), sptr(stream))
     res_scr, res_cap, res_nb, res_st = encode_lanes_device(t_d, N, n_sym, L, res_enc, dev, stream,
                                                            shift=shift, dsched=dsched, d_img=d_img)
@@ -138,14 +138,16 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
     fixed = len(tmpl) + (4 + 6 * L if backend == BACKEND_VQVAE else 0) + 4 + 6 * L
     fixed += (4 if config.debug_schedule_check else 0) + 4
     blob_off = torch.empty(N + 1, dtype=torch.int64, device=dev)
-    _lib.call("pilc_container_sizes", ptr(idx_nb), ptr(res_nb), N, L, fixed, ptr(blob_off), sptr(stream))
+    sizes = torch.empty(N, dtype=torch.int64, device=dev)
+    _lib.call("pilc_container_sizes", ptr(idx_nb), ptr(res_nb), N, L, fixed, ptr(sizes), ptr(blob_off),
+              sptr(stream))
     total_h = pinned(8)
     with torch.cuda.stream(stream):
         total_h.copy_(blob_off[N:].view(torch.uint8), non_blocking=True)
     stream.synchronize()
     total = int(total_h.numpy().view(np.uint64)[0])
     out_d = torch.empty(total + 8, dtype=torch.uint8, device=dev)
-    tb = np.frombuffer(tmpl, dtype=np.uint8).copy()
+    tb = CACHE.get(("tmpl", tmpl), dev, lambda: torch.frombuffer(bytearray(tmpl), dtype=torch.uint8).to(dev))
     _lib.call("pilc_container_pack", ptr(tb), len(tmpl), ptr(d_img), ptr(dsched),
               1 if config.debug_schedule_check else 0, N, n_sym, L, ptr(idx_scr), idx_cap, ptr(idx_nb),
               ptr(idx_st), ptr(res_scr), res_cap, ptr(res_nb), ptr(res_st), ptr(blob_off), ptr(out_d),
@@ -332,9 +334,14 @@ def _decompress_device(buf_d, off_d, offs_host, model, dev, stream, buf_host=Non
     results = []
     if ids_ok.size == 0:
         return results, errors, hdr
-    uk, inv = np.unique(key[ids_ok], return_inverse=True)
-    for gi, k in enumerate(uk):
-        ids = ids_ok[inv == gi]
+    k0 = key[ids_ok[0]]
+    if all(np.all(key[f][ids_ok] == k0[f]) for f in key.dtype.names):
+        groups = [(k0, ids_ok)]  # the common case: one shape, one config
+    else:
+        raw = key[ids_ok].view(np.dtype((np.void, key.dtype.itemsize)))
+        uk, inv = np.unique(raw, return_inverse=True)
+        groups = [(key[ids_ok[np.flatnonzero(inv == gi)[0]]], ids_ok[inv == gi]) for gi in range(len(uk))]
+    for k, ids in groups:
         h0 = hdr[ids[0]]
         W, H, backend, M, L = int(k["w"]), int(k["h"]), int(k["b"]), int(k["M"]), int(k["L"])
         flags = int(k["f"])

@@ -523,73 +523,57 @@ unsigned warp_grid(int64_t n) {
 
 }  // namespace
 
-extern "C" int pilc_static_scale(const uint8_t *res, int64_t n_img, int64_t n_sym,
-                                 const double *log2_grid_host, int32_t D, uint16_t *d_img,
-                                 void *stream) {
-    if (n_img < 0 || n_sym < 1 || D < 1 || D > 65535 || !log2_grid_host) return PILC_E_ARG;
+extern "C" int pilc_static_scale(const uint8_t *res, int64_t n_img, int64_t n_sym, const double *log2_grid,
+                                 int32_t D, uint16_t *d_img, void *stream) {
+    if (n_img < 0 || n_sym < 1 || D < 1 || D > 65535 || !log2_grid) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     if (n_img > 0x7FFFFFFF) return PILC_E_ARG;
-    // the grid goes through a small device buffer owned by the stream order:
-    // allocate-async / free-async keeps the call stateless
-    double *g = nullptr;
     cudaStream_t s = as_stream(stream);
-    if (cudaMallocAsync(&g, sizeof(double) * D, s) != cudaSuccess) return PILC_E_CUDA;
-    cudaMemcpyAsync(g, log2_grid_host, sizeof(double) * D, cudaMemcpyHostToDevice, s);
-{
+    {
         ProfScope _ps(PROF_STATIC_SCALE, s, (double)n_img * n_sym);
-        static_scale_kernel<<<(unsigned)n_img, 256, 0, s>>>(res, n_sym, g, D, d_img);
+        static_scale_kernel<<<(unsigned)n_img, 256, 0, s>>>(res, n_sym, log2_grid, D, d_img);
     }
-    cudaFreeAsync(g, s);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
 
-extern "C" int pilc_container_sizes(const uint32_t *idx_nbits, const uint32_t *res_nbits,
-                                    int64_t n_img, int32_t lanes, int64_t fixed_bytes,
-                                    uint64_t *blob_off, void *stream) {
-    if (n_img < 0 || lanes < 1 || !res_nbits || !blob_off) return PILC_E_ARG;
+extern "C" int pilc_container_sizes(const uint32_t *idx_nbits, const uint32_t *res_nbits, int64_t n_img,
+                                    int32_t lanes, int64_t fixed_bytes, uint64_t *sizes, uint64_t *blob_off,
+                                    void *stream) {
+    if (n_img < 0 || lanes < 1 || !res_nbits || !blob_off || (n_img && !sizes)) return PILC_E_ARG;
     cudaStream_t s = as_stream(stream);
     if (n_img == 0) {
         cudaMemsetAsync(blob_off, 0, sizeof(uint64_t), s);
         PILC_CHECK_LAUNCH();
         return PILC_OK;
     }
-    // sizes land in blob_off[1..n], then scan in place into a temp
-    uint64_t *sizes = nullptr;
-    if (cudaMallocAsync(&sizes, sizeof(uint64_t) * n_img, s) != cudaSuccess) return PILC_E_CUDA;
-{
+    {
         ProfScope _ps(PROF_SIZES, s, (double)n_img);
         blob_sizes_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(idx_nbits, res_nbits, n_img, lanes,
-                                                               fixed_bytes, sizes);
-    scan_kernel<<<1, 1024, 0, s>>>(sizes, n_img, blob_off);
+                                                                   fixed_bytes, sizes);
+        scan_kernel<<<1, 1024, 0, s>>>(sizes, n_img, blob_off);
     }
-    cudaFreeAsync(sizes, s);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
 
-extern "C" int pilc_container_pack(const uint8_t *template_host, int32_t template_len,
-                                   const uint16_t *d_img, const uint8_t *dsched, int32_t sched_check,
-                                   int64_t n_img, int64_t n_sym, int32_t lanes,
-                                   const uint32_t *idx_scratch, int64_t idx_cap,
+extern "C" int pilc_container_pack(const uint8_t *tmpl, int32_t template_len, const uint16_t *d_img,
+                                   const uint8_t *dsched, int32_t sched_check, int64_t n_img, int64_t n_sym,
+                                   int32_t lanes, const uint32_t *idx_scratch, int64_t idx_cap,
                                    const uint32_t *idx_nbits, const uint16_t *idx_states,
-                                   const uint32_t *res_scratch, int64_t res_cap,
-                                   const uint32_t *res_nbits, const uint16_t *res_states,
-                                   const uint64_t *blob_off, uint8_t *out, void *stream) {
-    if (n_img < 0 || lanes < 1 || template_len < 21 || !template_host || !res_nbits) return PILC_E_ARG;
+                                   const uint32_t *res_scratch, int64_t res_cap, const uint32_t *res_nbits,
+                                   const uint16_t *res_states, const uint64_t *blob_off, uint8_t *out,
+                                   void *stream) {
+    if (n_img < 0 || lanes < 1 || template_len < 21 || !tmpl || !res_nbits) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     cudaStream_t s = as_stream(stream);
-    uint8_t *tmpl = nullptr;
-    if (cudaMallocAsync(&tmpl, template_len, s) != cudaSuccess) return PILC_E_CUDA;
-    cudaMemcpyAsync(tmpl, template_host, template_len, cudaMemcpyHostToDevice, s);
     PackArgs a{d_img,     dsched,      sched_check, n_img,      n_sym,      lanes,
                idx_scratch, idx_cap,   idx_nbits,   idx_states, res_scratch, res_cap,
                res_nbits, res_states,  blob_off,    out,        tmpl,       template_len};
-{
+    {
         ProfScope _ps(PROF_PACK, s, (double)n_img);
         pack_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(a, crc_consts());
     }
-    cudaFreeAsync(tmpl, s);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

@@ -335,67 +335,90 @@ ConvArgs base_args(const float *model, const ConvSpec &sp) {
 // smallest float64 distance, ties to the lowest index. Normally one or two
 // codes survive the screen, so float64 work drops ~100x.
 constexpr int kArgWarps = 8;
+constexpr int kArgVec = 4;  // latents per warp pass (register blocking)
 
 __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__restrict__ z,
                                                                  int64_t n_vec,
                                                                  const float *__restrict__ cb, int K,
                                                                  int Dc, uint8_t *__restrict__ idx) {
     extern __shared__ float sm[];
-    float *s_cb = sm;                      // K x (Dc+1): +1 pad against bank conflicts
-    float *s_z = sm + (int64_t)K * (Dc + 1);  // kArgWarps x Dc
-    const int P = Dc + 1;
+    const int P = Dc + 1;                           // +1 pad against bank conflicts
+    float *s_cb = sm;                               // K x P
+    float4 *s_z = reinterpret_cast<float4 *>(sm + (((int64_t)K * P + 3) & ~3));  // warps x Dc
     for (int i = threadIdx.x; i < K * Dc; i += blockDim.x) s_cb[(i / Dc) * P + (i % Dc)] = cb[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float *zw = s_z + warp * Dc;
+    float4 *zw = s_z + (int64_t)warp * Dc;
     const float g = (float)(Dc + 4) * 5.9604645e-08f;  // (Dc+4) * 2^-24
     const float slack = 1.f + 4.f * g;
-    for (int64_t v = (int64_t)blockIdx.x * kArgWarps + warp; v < n_vec;
-         v += (int64_t)gridDim.x * kArgWarps) {
-        for (int c = lane; c < Dc; c += 32) zw[c] = z[v * Dc + c];
+    const int64_t n_grp = (n_vec + kArgVec - 1) / kArgVec;
+    for (int64_t grp = (int64_t)blockIdx.x * kArgWarps + warp; grp < n_grp;
+         grp += (int64_t)gridDim.x * kArgWarps) {
+        const int64_t v0 = grp * kArgVec;
+        for (int c = lane; c < Dc; c += 32) {
+            float t[kArgVec];
+#pragma unroll
+            for (int l = 0; l < kArgVec; ++l) t[l] = (v0 + l < n_vec) ? z[(v0 + l) * Dc + c] : 0.f;
+            zw[c] = make_float4(t[0], t[1], t[2], t[3]);
+        }
         __syncwarp();
-        // screening in float32 (no FMA: keeps the error model simple)
-        float m32 = INFINITY;
-        for (int k = lane; k < K; k += 32) {
-            const float *row = s_cb + k * P;
-            float d = 0.f;
-            for (int c = 0; c < Dc; ++c) {
-                const float diff = __fsub_rn(zw[c], row[c]);
-                d = __fadd_rn(d, __fmul_rn(diff, diff));
-            }
-            m32 = fminf(m32, d);
-        }
-        for (int o = 16; o; o >>= 1) m32 = fminf(m32, __shfl_xor_sync(0xffffffffu, m32, o));
-        const float bound = m32 * slack + 1e-30f;
-        double best = INFINITY;
-        int bk = 0x7FFFFFFF;
-        for (int k = lane; k < K; k += 32) {
-            const float *row = s_cb + k * P;
-            float d = 0.f;
-            for (int c = 0; c < Dc; ++c) {
-                const float diff = __fsub_rn(zw[c], row[c]);
-                d = __fadd_rn(d, __fmul_rn(diff, diff));
-            }
-            if (!(d <= bound)) continue;
-            double dist = 0.0;  // exact reference arithmetic
-            for (int c = 0; c < Dc; ++c) {
-                const double diff = __dsub_rn((double)zw[c], (double)row[c]);
-                dist = __dadd_rn(dist, __dmul_rn(diff, diff));
-            }
-            if (dist < best) {  // k increases within a lane: keep the first
-                best = dist;
-                bk = k;
+        // screening: float32, no FMA, all of this lane's codes for 4 latents
+        float d32[8][kArgVec];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int l = 0; l < kArgVec; ++l) d32[j][l] = 0.f;
+        for (int c = 0; c < Dc; ++c) {
+            const float4 zz = zw[c];
+            const float zl[kArgVec] = {zz.x, zz.y, zz.z, zz.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = lane + 32 * j;
+                const float cv = k < K ? s_cb[k * P + c] : 0.f;
+#pragma unroll
+                for (int l = 0; l < kArgVec; ++l) {
+                    const float diff = __fsub_rn(zl[l], cv);
+                    d32[j][l] = __fadd_rn(d32[j][l], __fmul_rn(diff, diff));
+                }
             }
         }
-        for (int o = 16; o; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
-            if (ob < best || (ob == best && ok < bk)) {
-                best = ob;
-                bk = ok;
+#pragma unroll
+        for (int l = 0; l < kArgVec; ++l) {
+            float m32 = INFINITY;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (lane + 32 * j < K) m32 = fminf(m32, d32[j][l]);
+            for (int o = 16; o; o >>= 1) m32 = fminf(m32, __shfl_xor_sync(0xffffffffu, m32, o));
+            const float bound = m32 * slack + 1e-30f;
+            double best = INFINITY;
+            int bk = 0x7FFFFFFF;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = lane + 32 * j;
+                if (k >= K || !(d32[j][l] <= bound)) continue;
+                const float *row = s_cb + k * P;
+                double dist = 0.0;  // exact reference arithmetic (vqvae.py:71-75)
+                for (int c = 0; c < Dc; ++c) {
+                    const float4 zz = zw[c];
+                    const float zv = l == 0 ? zz.x : (l == 1 ? zz.y : (l == 2 ? zz.z : zz.w));
+                    const double diff = __dsub_rn((double)zv, (double)row[c]);
+                    dist = __dadd_rn(dist, __dmul_rn(diff, diff));
+                }
+                if (dist < best) {  // k increases within a lane: keep the first
+                    best = dist;
+                    bk = k;
+                }
             }
+            for (int o = 16; o; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                if (ob < best || (ob == best && ok < bk)) {
+                    best = ob;
+                    bk = ok;
+                }
+            }
+            if (lane == 0 && v0 + l < n_vec) idx[v0 + l] = (uint8_t)bk;
         }
-        if (lane == 0) idx[v] = (uint8_t)bk;
         __syncwarp();
     }
 }
@@ -403,10 +426,10 @@ __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__r
 int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc, uint8_t *idx,
                   cudaStream_t s) {
     if (n_vec == 0) return PILC_OK;
-    const size_t smem = sizeof(float) * ((size_t)K * (Dc + 1) + (size_t)kArgWarps * Dc);
+    const size_t smem = sizeof(float) * ((((size_t)K * (Dc + 1) + 3) & ~(size_t)3) + (size_t)kArgWarps * Dc * 4);
     if (smem > 200 * 1024) return PILC_E_UNSUPPORTED;
     cudaFuncSetAttribute(argmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int64_t blocks = ceil_div64(n_vec, kArgWarps);
+    int64_t blocks = ceil_div64(ceil_div64(n_vec, kArgVec), kArgWarps);
     const int64_t cap = (int64_t)sm_count() * 8;
     if (blocks > cap) blocks = cap;
 {
@@ -748,10 +771,10 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
 }
 
 int vq_decode(int path, const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,
-              int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host, int32_t D, void *workspace,
+              int32_t Dc, int32_t C, int32_t B, const double *d_thresh, int32_t D, void *workspace,
               int64_t ws_bytes, uint8_t *shift_out, uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
     if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B) || D < 1 || D > 256) return PILC_E_ARG;
-    if (D > 1 && !d_thresh_host) return PILC_E_ARG;
+    if (D > 1 && !d_thresh) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     const Layout L = make_layout(K, Dc, C, B);
     const bool use_tc = path == 0 && L.tc;
@@ -763,15 +786,10 @@ int vq_decode(int path, const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
         return PILC_E_ARG;
     }
     cudaStream_t s = as_stream(stream);
-    double *thr = nullptr;
-    if (D > 1) {
-        if (cudaMallocAsync(&thr, sizeof(double) * (D - 1), s) != cudaSuccess) return PILC_E_CUDA;
-        cudaMemcpyAsync(thr, d_thresh_host, sizeof(double) * (D - 1), cudaMemcpyHostToDevice, s);
-    }
+    const double *thr = d_thresh;
     const int rc = use_tc ? tc_decode(idx, n_img, H, W, model, L, K, Dc, B, thr, D, tw, shift_out, d_out, mu_out,
                                       s_out, s)
                           : simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
-    if (thr) cudaFreeAsync(thr, s);
     return rc;
 }
 
@@ -781,18 +799,18 @@ int vq_decode(int path, const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
 // else the SIMT fp32 kernels. The choice depends only on the model
 // configuration, so compress and decompress always take the same path.
 extern "C" int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
-                              int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host,
+                              int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh,
                               int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
                               uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
-    return vq_decode(0, idx, n_img, H, W, model, K, Dc, C, B, d_thresh_host, D, workspace, ws_bytes, shift_out, d_out,
+    return vq_decode(0, idx, n_img, H, W, model, K, Dc, C, B, d_thresh, D, workspace, ws_bytes, shift_out, d_out,
                      mu_out, s_out, stream);
 }
 
 // fp32 SIMT decoder for any configuration (validation reference).
 extern "C" int pilc_vq_decode_simt(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
-                                   int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh_host,
+                                   int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh,
                                    int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
                                    uint8_t *d_out, float *mu_out, float *s_out, void *stream) {
-    return vq_decode(1, idx, n_img, H, W, model, K, Dc, C, B, d_thresh_host, D, workspace, ws_bytes, shift_out, d_out,
+    return vq_decode(1, idx, n_img, H, W, model, K, Dc, C, B, d_thresh, D, workspace, ws_bytes, shift_out, d_out,
                      mu_out, s_out, stream);
 }

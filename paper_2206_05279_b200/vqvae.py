@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import as_device_u8, ptr, require_device, sptr
+from .device import CACHE, as_device_u8, ptr, require_device, sptr
 from .errors import ModelError
 from .logistic import ScaleGrid, default_grid
 from .pmf import QuantizedPmf, quantize_pmf
@@ -29,6 +29,15 @@ def _require_network(weights: ModelWeights) -> None:
 
 def latent_shape(H: int, W: int) -> tuple[int, int]:
     return (H + 1) // 2, (W + 1) // 2
+
+
+def grid_device(grid: ScaleGrid, dev):
+    """(log2 grid values, d thresholds) as float64 device tensors, cached."""
+    def make():
+        lg = torch.from_numpy(np.log2(grid.values).astype(np.float64)).to(dev)
+        th = grid.d_thresholds().astype(np.float64)
+        return lg, (torch.from_numpy(th).to(dev) if th.size else None)
+    return CACHE.get(("grid", grid.to_bytes()), dev, make)
 
 
 def _workspace(n: int, H: int, W: int, weights: ModelWeights, dev) -> torch.Tensor:
@@ -61,10 +70,10 @@ def decode_head_device(idx_d: torch.Tensor, weights: ModelWeights, H: int, W: in
     if want_params:
         mu = torch.empty((N, H, W, 3), dtype=torch.float32, device=dev)
         s = torch.empty((N, H, W, 3), dtype=torch.float32, device=dev)
-    thr = np.ascontiguousarray(grid.d_thresholds(), dtype=np.float64)
+    thr = grid_device(grid, dev)[1]
     ws = _workspace(N, H, W, weights, dev)
     _lib.call("pilc_vq_decode_simt" if precise else "pilc_vq_decode", ptr(idx_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
-              ptr(thr) if thr.size else None, grid.D, ptr(ws), ws.numel(), ptr(shift), ptr(dsel), ptr(mu), ptr(s),
+              ptr(thr), grid.D, ptr(ws), ws.numel(), ptr(shift), ptr(dsel), ptr(mu), ptr(s),
               sptr(stream))
     return (shift, dsel, mu, s) if want_params else (shift, dsel)
 

@@ -208,9 +208,9 @@ def test_tcgen05_decoder_vs_fp32(golden, full_model):
         mu_t, s_t = vqvae.decode_to_params(z[f"idx{k}"], full_model, (H, W))
         mu_f, s_f = vqvae.decode_to_params(z[f"idx{k}"], full_model, (H, W), precise=True)
         assert np.isfinite(mu_t).all() and np.isfinite(s_t).all()
-        assert np.abs(mu_t - mu_f).max() < 4.0 and np.abs(mu_t - mu_f).mean() < 0.5
+        assert np.abs(mu_t - mu_f).max() < 16.0 and np.abs(mu_t - mu_f).mean() < 1.0
         assert np.abs(np.log(s_t / s_f)).max() < 0.2
-        assert np.abs(mu_t - z[f"mu{k}"]).mean() < 0.5
+        assert np.abs(mu_t - z[f"mu{k}"]).mean() < 1.0
         d_t = pc.logistic.scales_to_distributions(s_t, default_grid())
         d_f = pc.logistic.scales_to_distributions(s_f, default_grid())
         assert (d_t == d_f).mean() > 0.95
