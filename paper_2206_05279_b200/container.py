@@ -206,13 +206,16 @@ def compress_batch(images, model: ModelWeights | None = None, config: CodecConfi
     out_d, off_d, total = _compress_device(img_d, model, config, dev, stream)
     if return_device:
         return out_d, off_d, total
-    host = pinned(total + 8 * (img_d.shape[0] + 1))
+    # D2H straight into pinned memory; the returned arrays are views of it
+    n = img_d.shape[0]
+    host = pinned(total + 8 * (n + 1) + 8)
     hv = host.numpy()
+    o8 = (total + 7) & ~7
     with torch.cuda.stream(stream):
         host[:total].copy_(out_d[:total], non_blocking=True)
-        host[total:].copy_(off_d.view(torch.uint8), non_blocking=True)
+        host[o8:o8 + 8 * (n + 1)].copy_(off_d.view(torch.uint8), non_blocking=True)
     stream.synchronize()
-    return hv[:total].copy(), hv[total:].view(np.uint64).copy()
+    return hv[:total], hv[o8:o8 + 8 * (n + 1)].view(np.uint64)
 
 
 def compress(image: np.ndarray, model: ModelWeights | None = None, config: CodecConfig = CodecConfig()) -> bytes:
@@ -439,24 +442,27 @@ def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=
     errors = _resolve_errors(results, errors, hdr)
     if errors and raise_on_error:
         raise errors[min(errors)]
-    shapes = {(int(h["height"]), int(h["width"])) for h in hdr[[i for i in range(n) if i not in errors]]} \
-        if len(errors) < n else set()
-    # D2H through pinned memory
+    # D2H through pinned memory. One group covering every blob in order (the
+    # batch case) lands directly in the returned array.
+    if len(results) == 1 and not errors and results[0][0].size == n:
+        img = results[0][1]
+        host = pinned(img.numel())
+        with torch.cuda.stream(stream):
+            host.copy_(img.view(-1), non_blocking=True)
+        stream.synchronize()
+        out = host.numpy().reshape(tuple(img.shape))
+        return (out, errors) if not raise_on_error else out
     imgs: list = [None] * n
     for ids, img, *_ in results:
         host = pinned(img.numel())
         with torch.cuda.stream(stream):
             host.copy_(img.view(-1), non_blocking=True)
         stream.synchronize()
-        arr = host.numpy().reshape(tuple(img.shape)).copy()
+        arr = host.numpy().reshape(tuple(img.shape))
         for j, i in enumerate(ids):
             if int(i) not in errors:
                 imgs[int(i)] = arr[j]
-    if len(shapes) == 1 and not errors:
-        out = np.stack(imgs) if n > 1 else imgs[0][None]
-    else:
-        out = imgs
-    return (out, errors) if not raise_on_error else out
+    return (imgs, errors) if not raise_on_error else imgs
 
 
 def decompress(blob: bytes, model: ModelWeights | None = None, workers: int = 1) -> np.ndarray:

@@ -18,10 +18,38 @@
 namespace {
 
 constexpr int kThreads = 128;
+constexpr int kDecThreads = 64;  // 128 KB table per CTA: more CTAs, fewer idle threads
 constexpr int kSmemTableMax = 160 * 1024;
 
 __device__ __forceinline__ int lane_count(int64_t n_sym, int lanes, int l) {
     return l < n_sym ? (int)((n_sym - l + lanes - 1) / lanes) : 0;
+}
+
+// Byte j of a 16-byte vector.
+__device__ __forceinline__ uint32_t vbyte(const uint4 &v, int j) {
+    const uint32_t w = j < 4 ? v.x : (j < 8 ? v.y : (j < 12 ? v.z : v.w));
+    return (w >> (8 * (j & 3))) & 0xFFu;
+}
+
+struct EncState {
+    uint32_t state;
+    uint64_t acc;
+    int nacc;
+    uint32_t words;
+};
+
+__device__ __forceinline__ void enc_step(EncState &e, const uint32_t *tab, int X, int M, uint32_t d,
+                                         uint32_t x, uint32_t *out) {
+    const uint32_t t = tab[d * X + x];
+    const uint32_t b = ((t & 0xFFFFu) + e.state) >> M;
+    e.acc |= (uint64_t)(e.state & ((1u << b) - 1u)) << e.nacc;
+    e.nacc += b;
+    if (e.nacc >= 32) {
+        out[e.words++] = (uint32_t)e.acc;
+        e.acc >>= 32;
+        e.nacc -= 32;
+    }
+    e.state = (e.state >> b) + (t >> 16);
 }
 
 __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
@@ -47,29 +75,34 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
         const int64_t base = img * n_sym + l;
         const uint32_t dconst = d_img ? d_img[img] : 0u;
         uint32_t *out = scratch + k * lane_cap;
-        uint32_t state = 1u << M;
-        uint64_t acc = 0;
-        int nacc = 0;
-        uint32_t words = 0;
-        for (int i = cnt - 1; i >= 0; --i) {
+        EncState e{1u << M, 0, 0, 0};
+        auto scalar = [&](int i) {
             const int64_t pos = base + (int64_t)i * lanes;
             uint32_t x = syms[pos];
             if (shift) x = (x - shift[pos] + 128u) & 0xFFu;
-            const uint32_t d = dsched ? dsched[pos] : dconst;
-            const uint32_t e = tab[d * X + x];
-            const uint32_t b = ((e & 0xFFFFu) + state) >> M;
-            acc |= (uint64_t)(state & ((1u << b) - 1u)) << nacc;
-            nacc += b;
-            if (nacc >= 32) {
-                out[words++] = (uint32_t)acc;
-                acc >>= 32;
-                nacc -= 32;
+            enc_step(e, tab, X, M, dsched ? dsched[pos] : dconst, x, out);
+        };
+        int i = cnt - 1;
+        if (lanes == 1) {
+            // reverse order; 16-byte vector loads over aligned chunks
+            for (; i >= 0 && ((base + i + 1) & 15); --i) scalar(i);
+            for (; i >= 15; i -= 16) {
+                const int64_t p0 = base + i - 15;  // 16-aligned
+                const uint4 sv = *reinterpret_cast<const uint4 *>(syms + p0);
+                const uint4 hv = shift ? *reinterpret_cast<const uint4 *>(shift + p0) : make_uint4(0, 0, 0, 0);
+                const uint4 dv = dsched ? *reinterpret_cast<const uint4 *>(dsched + p0) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int j = 15; j >= 0; --j) {
+                    uint32_t x = vbyte(sv, j);
+                    if (shift) x = (x - vbyte(hv, j) + 128u) & 0xFFu;
+                    enc_step(e, tab, X, M, dsched ? vbyte(dv, j) : dconst, x, out);
+                }
             }
-            state = (state >> b) + (e >> 16);
         }
-        if (nacc) out[words] = (uint32_t)acc;
-        nbits[k] = words * 32u + (uint32_t)nacc;
-        states[k] = (uint16_t)state;
+        for (; i >= 0; --i) scalar(i);
+        if (e.nacc) out[e.words] = (uint32_t)e.acc;
+        nbits[k] = e.words * 32u + (uint32_t)e.nacc;
+        states[k] = (uint16_t)e.state;
     }
 }
 
@@ -80,7 +113,44 @@ __device__ __forceinline__ uint32_t load_word(const uint32_t *base_w, int64_t w,
     return (w >= lo_w && w <= hi_w) ? __ldg(base_w + w) : 0u;
 }
 
-__global__ void __launch_bounds__(kThreads) rans_decode_kernel(
+// Backward bit reader: a 64-bit window over aligned words plus a 4-deep
+// prefetch of the next lower words, so refills never wait on memory.
+struct BitReader {
+    const uint32_t *words;
+    int64_t lo_w, hi_w, wlo, A, start;
+    uint64_t win;
+    uint32_t pf[4];
+
+    __device__ __forceinline__ void init(const uint32_t *w, int64_t start_bit, uint32_t nb) {
+        words = w;
+        start = start_bit;
+        lo_w = start_bit >> 5;
+        hi_w = (start_bit + (int64_t)nb - 1) >> 5;
+        A = start_bit + nb;
+        wlo = ((A - 1) >> 5) - 1;
+        win = ((uint64_t)load_word(words, wlo + 1, lo_w, hi_w) << 32) | load_word(words, wlo, lo_w, hi_w);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pf[j] = load_word(words, wlo - 1 - j, lo_w, hi_w);
+    }
+    // returns false on underflow
+    __device__ __forceinline__ bool take(uint32_t b, uint32_t &v) {
+        if (A - start < (int64_t)b) return false;
+        const int64_t lo = A - b;
+        if (lo < wlo * 32) {
+            wlo -= 1;
+            win = (win << 32) | pf[0];
+            pf[0] = pf[1];
+            pf[1] = pf[2];
+            pf[2] = pf[3];
+            pf[3] = load_word(words, wlo - 4, lo_w, hi_w);
+        }
+        v = (uint32_t)(win >> (lo - wlo * 32)) & ((1u << b) - 1u);
+        A = lo;
+        return true;
+    }
+};
+
+__global__ void __launch_bounds__(kDecThreads) rans_decode_kernel(
     const uint8_t *__restrict__ buf, const uint64_t *__restrict__ lane_off,
     const uint32_t *__restrict__ nbits_a, const uint16_t *__restrict__ states,
     const uint8_t *__restrict__ dsched, const uint16_t *__restrict__ d_img, int64_t n_img,
@@ -109,39 +179,41 @@ __global__ void __launch_bounds__(kThreads) rans_decode_kernel(
         const int cnt = lane_count(n_sym, lanes, l);
         const int64_t sbase = img * n_sym + l;
         const uint32_t dconst = d_img ? d_img[img] : 0u;
-        const uint32_t nb = nbits_a[k];
-        // absolute bit addresses relative to `words`
-        const int64_t start_bit = (head + (int64_t)lane_off[k]) * 8;
-        const int64_t lo_w = start_bit >> 5;
-        const int64_t hi_w = (start_bit + (int64_t)nb - 1) >> 5;  // word of the last bit
-        int64_t A = start_bit + nb;      // read position (exclusive top)
-        int64_t wlo = ((A - 1) >> 5) - 1;  // window = bits [32*wlo, 32*wlo+64)
-        uint64_t win = ((uint64_t)load_word(words, wlo + 1, lo_w, hi_w) << 32) |
-                       load_word(words, wlo, lo_w, hi_w);
+        BitReader br;
+        br.init(words, (head + (int64_t)lane_off[k]) * 8, nbits_a[k]);
         uint32_t state = states[k];
         uint8_t st = 0;
-        for (int i = 0; i < cnt; ++i) {
-            const int64_t pos = sbase + (int64_t)i * lanes;
-            const uint32_t d = dsched ? dsched[pos] : dconst;
+        // one symbol: returns the decoded (un-recentred) byte; st on underflow
+        auto step = [&](uint32_t d, uint32_t sh) -> uint32_t {
             const uint32_t e = tab[d * T + (state - T)];
             const uint32_t b = (e >> 8) & 0xFFu;
-            uint32_t x = e & 0xFFu;
-            if (unshift) x = (x + unshift[pos] + 128u) & 0xFFu;  // (x + shift - 128) mod 256
-            out[pos] = (uint8_t)x;
-            if (A - start_bit < (int64_t)b) {
-                st = PILC_ST_UNDERFLOW;
-                break;
-            }
-            const int64_t lo = A - b;
-            if (lo < wlo * 32) {  // slide the window down one word
-                wlo -= 1;
-                win = (win << 32) | load_word(words, wlo, lo_w, hi_w);
-            }
-            const uint32_t v = (uint32_t)(win >> (lo - wlo * 32)) & ((1u << b) - 1u);
-            A = lo;
+            uint32_t v = 0;
+            if (!br.take(b, v)) st = PILC_ST_UNDERFLOW;
             state = (e >> 16) + v;
+            return unshift ? ((e + sh + 128u) & 0xFFu) : (e & 0xFFu);  // (x + shift - 128) mod 256
+        };
+        int i = 0;
+        if (lanes == 1) {
+            for (; i < cnt && ((sbase + i) & 15) && !st; ++i) {
+                const int64_t pos = sbase + i;
+                out[pos] = (uint8_t)step(dsched ? dsched[pos] : dconst, unshift ? unshift[pos] : 0u);
+            }
+            for (; i + 16 <= cnt && !st; i += 16) {
+                const int64_t p0 = sbase + i;  // 16-aligned
+                const uint4 dv = dsched ? *reinterpret_cast<const uint4 *>(dsched + p0) : make_uint4(0, 0, 0, 0);
+                const uint4 hv = unshift ? *reinterpret_cast<const uint4 *>(unshift + p0) : make_uint4(0, 0, 0, 0);
+                uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    o[j >> 2] |= step(dsched ? vbyte(dv, j) : dconst, vbyte(hv, j)) << (8 * (j & 3));
+                *reinterpret_cast<uint4 *>(out + p0) = make_uint4(o[0], o[1], o[2], o[3]);
+            }
         }
-        if (!st && (state != T || A != start_bit)) st = PILC_ST_END_STATE;
+        for (; i < cnt && !st; ++i) {
+            const int64_t pos = sbase + (int64_t)i * lanes;
+            out[pos] = (uint8_t)step(dsched ? dsched[pos] : dconst, unshift ? unshift[pos] : 0u);
+        }
+        if (!st && (state != T || br.A != br.start)) st = PILC_ST_END_STATE;
         lane_status[k] = st;
     }
 }
@@ -191,7 +263,7 @@ extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, co
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(rans_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t total = n_img * lanes;
-    int64_t blocks = ceil_div64(total, kThreads);
+    int64_t blocks = ceil_div64(total, kDecThreads);
     // one table copy per block: keep the grid at one resident block per SM
     // when the table is large, several when it is small
     const int64_t per_sm = in_smem ? (tab_bytes > 96 * 1024 ? 1 : (tab_bytes > 48 * 1024 ? 2 : 8)) : 16;
@@ -199,7 +271,7 @@ extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, co
     if (blocks > cap) blocks = cap;
 {
         ProfScope _ps(PROF_RANS_DEC, as_stream(stream), (double)n_img * n_sym);
-        rans_decode_kernel<<<(unsigned)blocks, kThreads, smem, as_stream(stream)>>>(
+        rans_decode_kernel<<<(unsigned)blocks, kDecThreads, smem, as_stream(stream)>>>(
         buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, in_smem,
         unshift, out, lane_status);
     }
