@@ -166,6 +166,14 @@ int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W,
                    const float *model, int32_t K, int32_t Dc, int32_t C,
                    int32_t B, void *workspace, int64_t ws_bytes,
                    uint8_t *idx_out, float *z_out, void *stream);
+/* Same contract, always the fp32 SIMT kernels (validation reference). The
+ * production pilc_vq_encode runs the block convs and the projection as
+ * 3xTF32 tcgen05 GEMMs when C == Dc == 32 (fp32-class z: hi/lo split of
+ * activations and weights, three MMAs per K step). */
+int pilc_vq_encode_simt(const uint8_t *img, int64_t n_img, int32_t H,
+                        int32_t W, const float *model, int32_t K, int32_t Dc,
+                        int32_t C, int32_t B, void *workspace, int64_t ws_bytes,
+                        uint8_t *idx_out, float *z_out, void *stream);
 /* Codebook argmin alone: z (n_vec, Dc) float32 -> u8 (vqvae.py:66-76). */
 int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model,
                    int32_t K, int32_t Dc, int32_t C, int32_t B, uint8_t *idx_out,

@@ -31,6 +31,7 @@ _SIGS = {
     "pilc_model_pack": (ctypes.c_int, [P, I32, I32, I32, I32, P]),
     "pilc_vq_workspace_bytes": (I64, [I64, I32, I32, I32, I32, I32, I32]),
     "pilc_vq_encode": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I64, P, P, P]),
+    "pilc_vq_encode_simt": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I64, P, P, P]),
     "pilc_vq_argmin": (ctypes.c_int, [P, I64, P, I32, I32, I32, I32, P, P]),
     "pilc_vq_decode": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, P]),
     "pilc_vq_decode_simt": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, P]),

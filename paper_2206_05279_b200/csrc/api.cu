@@ -10,7 +10,8 @@ const char *kCatNames[PROF_NCAT] = {"conv_kernel",        "argmin_kernel",  "ran
                                     "rans_decode_kernel", "twar_forward_kernel", "twar_decode_kernel",
                                     "static_scale_kernel", "blob_sizes+scan", "pack_kernel",
                                     "parse_kernel",       "lanes_kernel",   "crc_kernel",
-                                    "sched_crc_kernel",   "tc_conv_kernel", "gather_kernel"};
+                                    "sched_crc_kernel",   "tc_conv_kernel", "gather_kernel",
+                                    "tc3_conv_kernel"};
 struct Rec {
     int cat;
     cudaEvent_t e0, e1;

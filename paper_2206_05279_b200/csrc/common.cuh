@@ -34,6 +34,7 @@ enum ProfCat {
     PROF_SCHED_CRC,
     PROF_TC_CONV,
     PROF_GATHER,
+    PROF_TC3_CONV,
     PROF_NCAT
 };
 void *prof_begin(int cat, cudaStream_t s, double units);

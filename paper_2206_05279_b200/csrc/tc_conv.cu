@@ -146,9 +146,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v) {
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(a));
-    const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(b));
-    return lo | (hi << 16);
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);  // .x = a (low half)
+    return *reinterpret_cast<const uint32_t *>(&v);
 }
 
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
@@ -158,6 +157,18 @@ __device__ __forceinline__ float sigmoid_f32(float x) {
     if (x >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-x)));
     const float e = expf(x);
     return __fdiv_rn(e, __fadd_rn(1.f, e));
+}
+
+// q / d for q < 2^32 without the XU pipe: m = floor(2^32 / d) (host), the
+// high product underestimates by at most one.
+struct FastDiv {
+    uint32_t d, m;
+};
+__host__ inline FastDiv make_fastdiv(uint32_t d) { return FastDiv{d, (uint32_t)(0x100000000ull / d)}; }
+__device__ __forceinline__ uint32_t fdiv(uint32_t q, FastDiv f) {
+    uint32_t n = __umulhi(q, f.m);
+    if (q - n * f.d >= f.d) ++n;
+    return n;
 }
 
 // store one 16-byte group at padded pixel q, plus its border copies
@@ -196,8 +207,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     uint64_t *tempty = tfull + 2;          // [2]
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
+    float *s_bias = reinterpret_cast<float *>(wbar + 2);  // N floats
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = threadIdx.x; c < N; c += blockDim.x) s_bias[c] = c < (MODE == TC_OUT_HEAD ? 6 : N) ? L.bias[c] : 0.f;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
@@ -278,20 +291,36 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
-        const int Hp = L.Hp, H = L.H, W = L.W;
-        const int64_t hw = (int64_t)Hp * Wp;
+        const int H = L.H, W = L.W;
+        const FastDiv div_hw{(uint32_t)(L.Hp * Wp), (uint32_t)(0x100000000ull / (uint32_t)(L.Hp * Wp))};
+        const FastDiv div_w{(uint32_t)Wp, (uint32_t)(0x100000000ull / (uint32_t)Wp)};
+        constexpr int NB = MODE == TC_OUT_HEAD ? 6 : N;
+        float bias[MODE == TC_OUT_ACT ? NB : 1];
+        if constexpr (MODE == TC_OUT_ACT) {
+#pragma unroll
+            for (int c = 0; c < NB; ++c) bias[c] = L.bias[c];
+        }
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
             const int a = i & 1;
             const int u = i >> 1;
+            const uint32_t q = (uint32_t)t * 128u + (uint32_t)row;
+            const uint32_t n = fdiv(q, div_hw);
+            const uint32_t rem = q - n * div_hw.d;
+            const int y = (int)fdiv(rem, div_w), x = (int)(rem - (uint32_t)y * div_w.d);
+            const bool valid = n < (uint64_t)L.n_img && y >= 1 && y <= H && x >= 1 && x <= W;
+            // residual prefetch: independent of the accumulator, issue before the wait
+            uint4 rv[4];
+            if constexpr (MODE == TC_OUT_ACT) {
+                if (L.resid && valid) {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        rv[g] = reinterpret_cast<const uint4 *>(L.resid + ((int64_t)g * L.gstride + L.margin) * 8)[q];
+                }
+            }
             mbar_wait(&tfull[a], u & 1);
             tc_fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * N);
-            const int64_t q = t * 128 + row;
-            const int64_t n = q / hw;
-            const int rem = (int)(q - n * hw);
-            const int y = rem / Wp, x = rem - (rem / Wp) * Wp;
-            const bool valid = n < L.n_img && y >= 1 && y <= H && x >= 1 && x <= W;
             if constexpr (MODE == TC_OUT_ACT) {
                 float v[32];
                 tmem_ld32(taddr, v);
@@ -299,14 +328,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[a]);
                 if (valid) {
+                    uint4 w4[4];
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
                         float o[8];
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(v[8 * g + e], L.bias[8 * g + e]);
+                        for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(v[8 * g + e], bias[8 * g + e]);
                         if (L.resid) {
-                            const uint4 rv = reinterpret_cast<const uint4 *>(L.resid + ((int64_t)g * L.gstride + L.margin) * 8)[q];
-                            const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+                            const uint32_t rw[4] = {rv[g].x, rv[g].y, rv[g].z, rv[g].w};
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 o[2 * e] = __fadd_rn(bf16_lo(rw[e]), o[2 * e]);
@@ -317,10 +346,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
 #pragma unroll
                             for (int e = 0; e < 8; ++e) o[e] = fmaxf(o[e], 0.f);
                         }
-                        const uint4 w4 = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
-                                                    pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
-                        store_px(L.out + ((int64_t)g * L.out_gstride + L.out_margin) * 8, q, w4, y, x, H, W, Wp);
+                        w4[g] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                                           pack_bf16(o[6], o[7]));
                     }
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        store_px(L.out + ((int64_t)g * L.out_gstride + L.out_margin) * 8, q, w4[g], y, x, H, W, Wp);
                 }
             } else if constexpr (MODE == TC_OUT_SHUFFLE) {
                 // N = 128 = 4 chunks of 32 columns: chunk z holds output
@@ -343,9 +374,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                         float o[8];
 #pragma unroll
                         for (int e = 0; e < 8; ++e)
-                            o[e] = fmaxf(__fadd_rn(v[4 * e + sub], L.bias[32 * z + 4 * e + sub]), 0.f);
+                            o[e] = fmaxf(__fadd_rn(v[4 * e + sub], s_bias[32 * z + 4 * e + sub]), 0.f);
                         const int Y = 2 * (y - 1) + dy + 1, X = 2 * (x - 1) + dx + 1;
-                        const int64_t q2 = n * hw2 + (int64_t)Y * Wp2 + X;
+                        const int64_t q2 = (int64_t)n * hw2 + (int64_t)Y * Wp2 + X;
                         const uint4 w4 = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
                                                     pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
                         store_px(L.out + ((int64_t)z * L.out_gstride + L.out_margin) * 8, q2, w4, Y, X, H2, W2, Wp2);
@@ -359,13 +390,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[a]);
                 if (valid && (y - 1) < L.crop_h && (x - 1) < L.crop_w) {
-                    const int64_t px = (n * L.crop_h + (y - 1)) * (int64_t)L.crop_w + (x - 1);
+                    const int64_t px = ((int64_t)n * L.crop_h + (y - 1)) * (int64_t)L.crop_w + (x - 1);
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        float av = __fadd_rn(v[c], L.bias[c]);
+                        float av = __fadd_rn(v[c], s_bias[c]);
                         av = fminf(fmaxf(av, -15.f), 15.f);
                         const float mu = __fmul_rn(255.f, sigmoid_f32(av));
-                        float bv = __fadd_rn(v[3 + c], L.bias[3 + c]);
+                        float bv = __fadd_rn(v[3 + c], s_bias[3 + c]);
                         bv = fminf(fmaxf(bv, L.log_s_min), L.log_s_max);
                         float sv = fminf(fmaxf(expf(bv), 0.5f), 64.f);
                         const int shift = (int)floor((double)mu + 0.5);
@@ -389,12 +420,268 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     }
 }
 
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void store_px4(float *slab, int64_t q, float4 v, int y, int x, int H, int W, int Wp) {
+    float4 *p = reinterpret_cast<float4 *>(slab);
+    p[q] = v;
+    const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
+    const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
+    if (dy) p[q - Wp] = v;
+    if (dy2) p[q + Wp] = v;
+    if (dx) p[q - 1] = v;
+    if (dx2) p[q + 1] = v;
+    if (dy && dx) p[q - Wp - 1] = v;
+    if (dy && dx2) p[q - Wp + 1] = v;
+    if (dy2 && dx) p[q + Wp - 1] = v;
+    if (dy2 && dx2) p[q + Wp + 1] = v;
+}
+
+// 3xTF32 conv, C = 32 in, N = 32 out: D = Ahi*Bhi + Ahi*Blo + Alo*Bhi, all
+// accumulated in fp32 TMEM. Same pipeline as tc_conv_kernel (producer /
+// MMA / 4 epilogue warps, 3-stage ring, double-buffered accumulator).
+constexpr int kStages3 = 3;
+
+template <int KS, int MODE>
+__global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
+    constexpr int N = 32;
+    constexpr int NG = 8;  // 4-channel groups
+    constexpr int KG = KS * KS * NG;
+    constexpr int TMEM_COLS = 2 * N;
+    const int Wp = L.Wp;
+    const int npix = KS == 3 ? ((128 + 2 * Wp + 2 + 7) & ~7) : 128;
+    const uint32_t half_bytes = (uint32_t)NG * npix * 16;  // one of hi / lo
+    const uint32_t stage_bytes = 2 * half_bytes;
+    const uint32_t wbytes = (uint32_t)KG * N * 16;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_whi = smem;
+    uint8_t *s_wlo = smem + wbytes;
+    uint8_t *s_a = smem + 2 * (size_t)wbytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_a + (size_t)kStages3 * stage_bytes);
+    uint64_t *full = bars;
+    uint64_t *empty = bars + kStages3;
+    uint64_t *tfull = bars + 2 * kStages3;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *wbar = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages3; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        mbar_init(wbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"((uint32_t)TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int64_t n_tiles = L.n_tiles;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(wbar, 2 * wbytes);
+            bulk_g2s(s_whi, L.w_hi, wbytes, wbar);
+            bulk_g2s(s_wlo, L.w_lo, wbytes, wbar);
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int s = i % kStages3;
+                const int r = i / kStages3;
+                if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+                const int64_t q_lo = t * 128 - (KS == 3 ? (Wp + 1) : 0);
+                mbar_expect_tx(&full[s], stage_bytes);
+                uint8_t *dst = s_a + (size_t)s * stage_bytes;
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    const int64_t off = ((int64_t)g * L.gstride + L.margin + q_lo) * 4;
+                    bulk_g2s(dst + (size_t)g * npix * 16, L.in_hi + off, (uint32_t)npix * 16, &full[s]);
+                    bulk_g2s(dst + half_bytes + (size_t)g * npix * 16, L.in_lo + off, (uint32_t)npix * 16, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, N);
+            mbar_wait(wbar, 0);
+            tc_fence_after();
+            const uint32_t whi = smem_u32(s_whi), wlo = smem_u32(s_wlo);
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int s = i % kStages3;
+                const int a = i & 1;
+                const int u = i >> 1;
+                if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
+                mbar_wait(&full[s], (i / kStages3) & 1);
+                tc_fence_after();
+                const uint32_t ahi = smem_u32(s_a + (size_t)s * stage_bytes);
+                const uint32_t alo = ahi + half_bytes;
+                const uint32_t d = tmem + (uint32_t)(a * N);
+                uint32_t acc = 0;
+#pragma unroll 1
+                for (int tap = 0; tap < KS * KS; ++tap) {
+                    const int ti = tap / KS, tj = tap % KS;
+                    const uint32_t off = KS == 3 ? (uint32_t)(ti * Wp + tj) * 16u : 0u;
+#pragma unroll
+                    for (int ks = 0; ks < NG / 2; ++ks) {
+                        const uint32_t ao = (uint32_t)(2 * ks) * npix * 16u + off;
+                        const uint32_t bo = (uint32_t)(tap * NG + 2 * ks) * N * 16u;
+                        const uint64_t dah = umma_desc(ahi + ao, (uint32_t)npix * 16u, 128u);
+                        const uint64_t dal = umma_desc(alo + ao, (uint32_t)npix * 16u, 128u);
+                        const uint64_t dbh = umma_desc(whi + bo, (uint32_t)N * 16u, 128u);
+                        const uint64_t dbl = umma_desc(wlo + bo, (uint32_t)N * 16u, 128u);
+                        mma_tf32(d, dal, dbh, idesc, acc);
+                        mma_tf32(d, dah, dbl, idesc, 1u);
+                        mma_tf32(d, dah, dbh, idesc, 1u);
+                        acc = 1u;
+                    }
+                }
+                mma_commit(&empty[s]);
+                mma_commit(&tfull[a]);
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int H = L.H, W = L.W;
+        const FastDiv div_hw{(uint32_t)(L.Hp * Wp), (uint32_t)(0x100000000ull / (uint32_t)(L.Hp * Wp))};
+        const FastDiv div_w{(uint32_t)Wp, (uint32_t)(0x100000000ull / (uint32_t)Wp)};
+        float bias[N];
+#pragma unroll
+        for (int c = 0; c < N; ++c) bias[c] = L.bias[c];
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int a = i & 1;
+            const int u = i >> 1;
+            const uint32_t q = (uint32_t)t * 128u + (uint32_t)row;
+            const uint32_t n = fdiv(q, div_hw);
+            const uint32_t rem = q - n * div_hw.d;
+            const int y = (int)fdiv(rem, div_w), x = (int)(rem - (uint32_t)y * div_w.d);
+            const bool valid = n < (uint64_t)L.n_img && y >= 1 && y <= H && x >= 1 && x <= W;
+            float4 rh[MODE == TC3_ACT ? NG : 1], rl[MODE == TC3_ACT ? NG : 1];
+            if constexpr (MODE == TC3_ACT) {
+                if (L.res_hi && valid) {
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        const int64_t ro = (int64_t)g * L.gstride + L.margin + q;
+                        rh[g] = reinterpret_cast<const float4 *>(L.res_hi)[ro];
+                        rl[g] = reinterpret_cast<const float4 *>(L.res_lo)[ro];
+                    }
+                }
+            }
+            mbar_wait(&tfull[a], u & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * N);
+            float v[32];
+            tmem_ld32(taddr, v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+            if (!valid) continue;
+            if constexpr (MODE == TC3_ACT) {
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    float o[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) o[e] = __fadd_rn(v[4 * g + e], bias[4 * g + e]);
+                    if (L.res_hi) {
+                        o[0] = __fadd_rn(__fadd_rn(rh[g].x, rl[g].x), o[0]);
+                        o[1] = __fadd_rn(__fadd_rn(rh[g].y, rl[g].y), o[1]);
+                        o[2] = __fadd_rn(__fadd_rn(rh[g].z, rl[g].z), o[2]);
+                        o[3] = __fadd_rn(__fadd_rn(rh[g].w, rl[g].w), o[3]);
+                    }
+                    if (L.relu) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
+                    }
+                    float hi[4], lo[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        hi[e] = tf32_rna(o[e]);
+                        lo[e] = __fsub_rn(o[e], hi[e]);
+                    }
+                    // residual already in registers: store as we go
+                    const int64_t so = ((int64_t)g * L.gstride + L.margin) * 4;
+                    store_px4(L.out_hi + so, q, make_float4(hi[0], hi[1], hi[2], hi[3]), y, x, H, W, Wp);
+                    store_px4(L.out_lo + so, q, make_float4(lo[0], lo[1], lo[2], lo[3]), y, x, H, W, Wp);
+                }
+            } else {
+                float4 *zo = reinterpret_cast<float4 *>(L.z + (((int64_t)n * H + (y - 1)) * (int64_t)W + (x - 1)) * 32);
+#pragma unroll
+                for (int g = 0; g < NG; ++g)
+                    zo[g] = make_float4(__fadd_rn(v[4 * g], bias[4 * g]), __fadd_rn(v[4 * g + 1], bias[4 * g + 1]),
+                                        __fadd_rn(v[4 * g + 2], bias[4 * g + 2]),
+                                        __fadd_rn(v[4 * g + 3], bias[4 * g + 3]));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)TMEM_COLS));
+    }
+}
+
+template <int KS, int MODE>
+int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
+    constexpr int NG = 8;
+    constexpr int KG = KS * KS * NG;
+    const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
+    const size_t smem = 2 * (size_t)KG * 32 * 16 + (size_t)kStages3 * 2 * NG * npix * 16 + 8 * (2 * kStages3 + 5) + 16;
+    if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
+    if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
+    auto kern = tc3_conv_kernel<KS, MODE>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = (int)((227 * 1024) / (smem + 1024));
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    if (grid > L.n_tiles) grid = L.n_tiles;
+    if (grid < 1) return PILC_OK;
+    const double flops = 2.0 * L.n_img * L.H * L.W * 32.0 * 32 * KS * KS;
+    ProfScope _ps(PROF_TC3_CONV, s, flops);
+    kern<<<(unsigned)grid, kThreadsTC, smem, s>>>(L);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
 template <int N, int KS, int MODE>
 int launch_tc(const TcLayer &L, cudaStream_t s) {
     constexpr int NG = 4;
     constexpr int KG = KS * KS * NG;
     const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
-    const size_t smem = (size_t)KG * N * 16 + (size_t)kStages * NG * npix * 16 + 8 * (2 * kStages + 5) + 16;
+    const size_t smem = (size_t)KG * N * 16 + (size_t)kStages * NG * npix * 16 + 8 * (2 * kStages + 6) + 4 * N + 16;
+    if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     auto kern = tc_conv_kernel<N, KS, MODE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -447,6 +734,11 @@ __global__ void gather_kernel(const uint8_t *__restrict__ idx, const uint16_t *_
 }  // namespace
 
 int tc_launch_act(const TcLayer &L, cudaStream_t s) { return launch_tc<32, 3, TC_OUT_ACT>(L, s); }
+int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s) {
+    if (ks == 3 && mode == TC3_ACT) return launch_tc3<3, TC3_ACT>(L, s);
+    if (ks == 1 && mode == TC3_Z) return launch_tc3<1, TC3_Z>(L, s);
+    return PILC_E_UNSUPPORTED;
+}
 int tc_launch_shuffle(const TcLayer &L, cudaStream_t s) { return launch_tc<128, 3, TC_OUT_SHUFFLE>(L, s); }
 int tc_launch_head(const TcLayer &L, cudaStream_t s) { return launch_tc<16, 3, TC_OUT_HEAD>(L, s); }
 

@@ -26,6 +26,26 @@ struct TcLayer {
     float log_s_min, log_s_max;
 };
 
+// 3xTF32 encoder layers: activations are fp32 split into a tf32 "hi" slab
+// and an fp32 "lo" residual slab, 4 channels (16 B) per group, same padded
+// group-major pixel indexing as the bf16 path.
+enum Tc3Mode { TC3_ACT = 0, TC3_Z = 1 };
+
+struct Tc3Layer {
+    const float *in_hi, *in_lo;
+    int64_t gstride, margin;
+    int Hp, Wp, H, W;
+    int64_t n_img, n_tiles;
+    const float *w_hi, *w_lo;  // B operand hi/lo, [KG][N][4] fp32
+    const float *bias;
+    const float *res_hi, *res_lo;  // TC3_ACT residual (nullable)
+    float *out_hi, *out_lo;        // TC3_ACT
+    float *z;                      // TC3_Z: (n, H, W, 32) fp32
+    int relu;
+};
+
+int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s);
+
 int tc_launch_act(const TcLayer &L, cudaStream_t s);
 int tc_launch_shuffle(const TcLayer &L, cudaStream_t s);
 int tc_launch_head(const TcLayer &L, cudaStream_t s);

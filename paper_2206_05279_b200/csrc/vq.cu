@@ -45,6 +45,11 @@ struct Layout {
     bool tc;
     std::vector<int64_t> tc_blk;  // 2B block convs, N = 32
     int64_t tc_up, tc_head;       // N = 128, N = 16 (mu 0..2, s 3..5)
+    // 3xTF32 encoder (C == 32, Dc == 32): B operands hi / lo, [KG][32][4]
+    // fp32, float offsets; lo follows hi
+    bool tf;
+    std::vector<int64_t> tf_blk;
+    int64_t tf_proj;
     int64_t total;                // floats, bf16 region included
 };
 
@@ -94,13 +99,23 @@ Layout make_layout(int K, int Dc, int C, int B) {
         h += 36 * 16 * 8;
         cur = (h + 1) / 2;
     }
+    L.tf = (C == 32 && Dc == 32);
+    if (L.tf) {
+        cur = (cur + 7) / 8 * 8;
+        for (int i = 0; i < 2 * B; ++i) {
+            L.tf_blk.push_back(cur);
+            cur += 2 * 72 * 32 * 4;
+        }
+        L.tf_proj = cur;
+        cur += 2 * 8 * 32 * 4;
+    }
     L.total = cur;
     return L;
 }
 
 // ---- conv kernel -----------------------------------------------------------
 enum InMode { IN_F32 = 0, IN_U8 = 1, IN_CODEBOOK = 2 };
-enum OutMode { OUT_F32 = 0, OUT_SHUFFLE = 1, OUT_HEAD = 2 };
+enum OutMode { OUT_F32 = 0, OUT_SHUFFLE = 1, OUT_HEAD = 2, OUT_TFSPLIT = 3 };
 
 struct ConvArgs {
     const float *in;
@@ -125,6 +140,9 @@ struct ConvArgs {
     const double *thresh;
     int n_thresh;
     float log_s_min, log_s_max;
+    // OUT_TFSPLIT: tf32 hi / fp32 lo slabs, padded group-major (tc_conv.cu)
+    float *out_hi, *out_lo;
+    int64_t out_gstride, out_margin;
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -134,6 +152,21 @@ __device__ __forceinline__ float sigmoid_f32(float x) {
     if (x >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-x)));
     const float e = expf(x);
     return __fdiv_rn(e, __fadd_rn(1.f, e));
+}
+
+__device__ __forceinline__ void store_px4s(float *slab, int64_t q, float4 v, int y, int x, int H, int W, int Wp) {
+    float4 *p = reinterpret_cast<float4 *>(slab);
+    p[q] = v;
+    const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
+    const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
+    if (dy) p[q - Wp] = v;
+    if (dy2) p[q + Wp] = v;
+    if (dx) p[q - 1] = v;
+    if (dx2) p[q + 1] = v;
+    if (dy && dx) p[q - Wp - 1] = v;
+    if (dy && dx2) p[q - Wp + 1] = v;
+    if (dy2 && dx) p[q + Wp - 1] = v;
+    if (dy2 && dx2) p[q + Wp + 1] = v;
 }
 
 template <int CO_T>
@@ -248,6 +281,26 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
                 const int cc = co >> 2, dy = (co >> 1) & 1, dx = co & 1;
                 const float v = fmaxf(__fadd_rn(acc[c], a.b[co]), 0.f);
                 a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = v;
+            }
+        } else if (a.out_mode == OUT_TFSPLIT) {
+            // bias + ReLU, then split into the 3xTF32 encoder layout
+            const int Wp = a.Wo + 2;
+            const int64_t q = ((int64_t)n * (a.Ho + 2) + oy + 1) * Wp + ox + 1;
+#pragma unroll
+            for (int g = 0; g < CO_T / 4; ++g) {
+                float hi[4], lo[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    float v = __fadd_rn(acc[4 * g + e], a.b[co0 + 4 * g + e]);
+                    if (a.relu) v = fmaxf(v, 0.f);
+                    uint32_t r;
+                    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+                    hi[e] = __uint_as_float(r);
+                    lo[e] = __fsub_rn(v, hi[e]);
+                }
+                const int64_t so = ((int64_t)((co0 >> 2) + g) * a.out_gstride + a.out_margin) * 4;
+                store_px4s(a.out_hi + so, q, make_float4(hi[0], hi[1], hi[2], hi[3]), oy + 1, ox + 1, a.Ho, a.Wo, Wp);
+                store_px4s(a.out_lo + so, q, make_float4(lo[0], lo[1], lo[2], lo[3]), oy + 1, ox + 1, a.Ho, a.Wo, Wp);
             }
         } else {
             // logistic head (vqvae.py:105-112, logistic.py:36-40, 109-114)
@@ -489,6 +542,31 @@ int64_t tc_ws(int64_t n, int H, int W, TcWork *w, char *base) {
     return 3 * slab + slab2 + al(256 * 32 * 2);
 }
 
+// 3xTF32 encoder scratch: full-res stem output (NHWC fp32), three latent
+// tensors as hi/lo slab pairs (8 groups x gstride x 16 B each), z.
+struct TfWork {
+    float *A, *Xh, *Xl, *Th, *Tl, *Yh, *Yl, *Z;
+    int64_t gs, margin;
+};
+
+int64_t tf_ws(int64_t n, int H, int W, TfWork *w, char *base) {
+    const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
+    const int64_t Wp = gw + 2;
+    const int64_t m1 = 256 + 2 * Wp;
+    const int64_t gs = 2 * m1 + n * (gh + 2) * Wp;
+    auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
+    const int64_t a = al(n * He * We * 32 * 4), slab = al(8 * gs * 16), z = al(n * gh * gw * 32 * 4);
+    if (w) {
+        w->A = reinterpret_cast<float *>(base);
+        float **sl[6] = {&w->Xh, &w->Xl, &w->Th, &w->Tl, &w->Yh, &w->Yl};
+        for (int i = 0; i < 6; ++i) *sl[i] = reinterpret_cast<float *>(base + a + i * slab);
+        w->Z = reinterpret_cast<float *>(base + a + 6 * slab);
+        w->gs = gs;
+        w->margin = m1;
+    }
+    return a + 6 * slab + z;
+}
+
 bool check_cfg(int K, int Dc, int C, int B) {
     return K >= 1 && K <= 256 && Dc >= 1 && C >= 1 && B >= 0 && Dc <= 4096 && C <= 4096;
 }
@@ -547,6 +625,33 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
         put_b(L.tc_up, L.dec[1 + 2 * B], 128, 0, 128);
         put_b(L.tc_head, L.dec[2 + 2 * B], 16, 0, 6);
     }
+    if (L.tf) {
+        // tf32 hi = round-to-nearest (ties away) to 10 mantissa bits, lo = w - hi
+        auto tf32 = [](float f) -> float {
+            uint32_t u;
+            memcpy(&u, &f, 4);
+            if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+            float r;
+            memcpy(&r, &u, 4);
+            return r;
+        };
+        auto put_t = [&](int64_t off, const ConvSpec &sp) {
+            const int taps = sp.ks * sp.ks;
+            const int64_t half = (int64_t)taps * 8 * 32 * 4;
+            for (int n = 0; n < 32; ++n)
+                for (int ci = 0; ci < 32; ++ci)
+                    for (int tap = 0; tap < taps; ++tap) {
+                        const int k = tap * 32 + ci;
+                        const float w = dst[sp.w_off + ((int64_t)tap * sp.ci_pad + ci) * sp.co_pad + n];
+                        const float hi = tf32(w);
+                        const int64_t e = ((int64_t)(k >> 2) * 32 + n) * 4 + (k & 3);
+                        dst[off + e] = hi;
+                        dst[off + half + e] = w - hi;
+                    }
+        };
+        for (int i = 0; i < 2 * B; ++i) put_t(L.tf_blk[i], L.enc[2 + i]);
+        put_t(L.tf_proj, L.enc[2 + 2 * B]);
+    }
     return PILC_OK;
 }
 
@@ -555,7 +660,9 @@ extern "C" int64_t pilc_vq_workspace_bytes(int64_t n_img, int32_t H, int32_t W, 
     if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return -1;
     const int64_t a = ws_parts(n_img, H, W, Dc, C, nullptr, nullptr);
     const int64_t b = C == 32 ? tc_ws(n_img, H, W, nullptr, nullptr) : 0;
-    return a > b ? a : b;
+    const int64_t c = (C == 32 && Dc == 32) ? tf_ws(n_img, H, W, nullptr, nullptr) : 0;
+    const int64_t m = a > b ? a : b;
+    return m > c ? m : c;
 }
 
 extern "C" int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model, int32_t K, int32_t Dc,
@@ -565,15 +672,11 @@ extern "C" int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model,
     return launch_argmin(z, n_vec, model + L.cb_off, K, Dc, idx_out, as_stream(stream));
 }
 
-extern "C" int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model,
-                              int32_t K, int32_t Dc, int32_t C, int32_t B, void *workspace,
-                              int64_t ws_bytes, uint8_t *idx_out, float *z_out, void *stream) {
-    if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return PILC_E_ARG;
-    if (n_img == 0) return PILC_OK;
-    Work w;
-    if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-    const Layout L = make_layout(K, Dc, C, B);
-    cudaStream_t s = as_stream(stream);
+namespace {
+
+int simt_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,
+                int32_t Dc, int32_t B, const Layout &L, const Work &w, uint8_t *idx_out, float *z_out,
+                cudaStream_t s) {
     const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
     int rc;
     // stem (3x3, image -> He x We x C, ReLU); normalisation + even-pad fused
@@ -625,6 +728,123 @@ extern "C" int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int3
     a.out = z;
     if ((rc = launch_conv(a, L.enc[2 + 2 * B].co_t, n_img, s))) return rc;
     return launch_argmin(z, n_img * gh * gw, model + L.cb_off, K, Dc, idx_out, s);
+}
+
+
+int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K, int32_t Dc,
+              int32_t B, const Layout &L, const TfWork &w, uint8_t *idx_out, float *z_out, cudaStream_t s) {
+    const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
+    int rc;
+    ConvArgs a = base_args(model, L.enc[0]);  // stem, SIMT fp32
+    a.in_mode = IN_U8;
+    a.in_u8 = img;
+    a.src_h = H;
+    a.src_w = W;
+    a.Hi = a.Ho = He;
+    a.Wi = a.Wo = We;
+    a.relu = 1;
+    a.out = w.A;
+    if ((rc = launch_conv(a, L.enc[0].co_t, n_img, s))) return rc;
+    a = base_args(model, L.enc[1]);  // down (stride 2), SIMT fp32 -> hi/lo slabs
+    a.in = w.A;
+    a.Hi = He;
+    a.Wi = We;
+    a.stride = 2;
+    a.Ho = gh;
+    a.Wo = gw;
+    a.relu = 1;
+    a.out_mode = OUT_TFSPLIT;
+    a.out_hi = w.Xh;
+    a.out_lo = w.Xl;
+    a.out_gstride = w.gs;
+    a.out_margin = w.margin;
+    if ((rc = launch_conv(a, L.enc[1].co_t, n_img, s))) return rc;
+    Tc3Layer b;
+    memset(&b, 0, sizeof(b));
+    b.gstride = w.gs;
+    b.margin = w.margin;
+    b.Hp = gh + 2;
+    b.Wp = gw + 2;
+    b.H = gh;
+    b.W = gw;
+    b.n_img = n_img;
+    b.n_tiles = ceil_div64(n_img * b.Hp * (int64_t)b.Wp, 128);
+    b.relu = 1;
+    float *Xh = w.Xh, *Xl = w.Xl, *Yh = w.Yh, *Yl = w.Yl;
+    const int64_t half3 = 72 * 32 * 4, half1 = 8 * 32 * 4;
+    for (int i = 0; i < B; ++i) {
+        Tc3Layer c1 = b;
+        c1.in_hi = Xh;
+        c1.in_lo = Xl;
+        c1.out_hi = w.Th;
+        c1.out_lo = w.Tl;
+        c1.w_hi = model + L.tf_blk[2 * i];
+        c1.w_lo = c1.w_hi + half3;
+        c1.bias = model + L.enc[2 + 2 * i].b_off;
+        if ((rc = tc3_launch(c1, 3, TC3_ACT, s))) return rc;
+        Tc3Layer c2 = b;
+        c2.in_hi = w.Th;
+        c2.in_lo = w.Tl;
+        c2.res_hi = Xh;
+        c2.res_lo = Xl;
+        c2.out_hi = Yh;
+        c2.out_lo = Yl;
+        c2.w_hi = model + L.tf_blk[2 * i + 1];
+        c2.w_lo = c2.w_hi + half3;
+        c2.bias = model + L.enc[3 + 2 * i].b_off;
+        if ((rc = tc3_launch(c2, 3, TC3_ACT, s))) return rc;
+        float *th = Xh, *tl = Xl;
+        Xh = Yh;
+        Xl = Yl;
+        Yh = th;
+        Yl = tl;
+    }
+    float *z = z_out ? z_out : w.Z;
+    Tc3Layer pj = b;  // proj 1x1 -> z (fp32, NHWC interior)
+    pj.in_hi = Xh;
+    pj.in_lo = Xl;
+    pj.w_hi = model + L.tf_proj;
+    pj.w_lo = pj.w_hi + half1;
+    pj.bias = model + L.enc[2 + 2 * B].b_off;
+    pj.relu = 0;
+    pj.z = z;
+    if ((rc = tc3_launch(pj, 1, TC3_Z, s))) return rc;
+    return launch_argmin(z, n_img * gh * gw, model + L.cb_off, K, Dc, idx_out, s);
+}
+
+int vq_encode(int path, const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,
+              int32_t Dc, int32_t C, int32_t B, void *workspace, int64_t ws_bytes, uint8_t *idx_out, float *z_out,
+              void *stream) {
+    if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return PILC_E_ARG;
+    if (n_img == 0) return PILC_OK;
+    const Layout L = make_layout(K, Dc, C, B);
+    cudaStream_t s = as_stream(stream);
+    if (path == 0 && L.tf) {
+        TfWork tw;
+        if (tf_ws(n_img, H, W, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+        return tf_encode(img, n_img, H, W, model, K, Dc, B, L, tw, idx_out, z_out, s);
+    }
+    Work w;
+    if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+    return simt_encode(img, n_img, H, W, model, K, Dc, B, L, w, idx_out, z_out, s);
+}
+
+}  // namespace
+
+// Production encoder: 3xTF32 tcgen05 block convs when C == Dc == 32 (the
+// default model), fp32 SIMT otherwise. Index parity needs fp32-class z; the
+// argmin itself is exact given z.
+extern "C" int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model,
+                              int32_t K, int32_t Dc, int32_t C, int32_t B, void *workspace,
+                              int64_t ws_bytes, uint8_t *idx_out, float *z_out, void *stream) {
+    return vq_encode(0, img, n_img, H, W, model, K, Dc, C, B, workspace, ws_bytes, idx_out, z_out, stream);
+}
+
+// fp32 SIMT encoder for any configuration (validation reference).
+extern "C" int pilc_vq_encode_simt(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model,
+                                   int32_t K, int32_t Dc, int32_t C, int32_t B, void *workspace,
+                                   int64_t ws_bytes, uint8_t *idx_out, float *z_out, void *stream) {
+    return vq_encode(1, img, n_img, H, W, model, K, Dc, C, B, workspace, ws_bytes, idx_out, z_out, stream);
 }
 
 namespace {

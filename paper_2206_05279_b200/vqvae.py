@@ -47,12 +47,15 @@ def _workspace(n: int, H: int, W: int, weights: ModelWeights, dev) -> torch.Tens
     return torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
 
 
-def encode_indices_device(img_d: torch.Tensor, weights: ModelWeights, dev, stream, z_out=None) -> torch.Tensor:
+def encode_indices_device(img_d: torch.Tensor, weights: ModelWeights, dev, stream, z_out=None,
+                          precise: bool = False) -> torch.Tensor:
+    """Production encoder (3xTF32 tcgen05 for the default C=Dc=32 model);
+    precise=True selects the fp32 SIMT kernels."""
     N, H, W, _ = img_d.shape
     gh, gw = latent_shape(H, W)
     idx = torch.empty((N, gh, gw), dtype=torch.uint8, device=dev)
     ws = _workspace(N, H, W, weights, dev)
-    _lib.call("pilc_vq_encode", ptr(img_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
+    _lib.call("pilc_vq_encode_simt" if precise else "pilc_vq_encode", ptr(img_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
               ptr(ws), ws.numel(), ptr(idx), ptr(z_out), sptr(stream))
     return idx
 
@@ -78,17 +81,17 @@ def decode_head_device(idx_d: torch.Tensor, weights: ModelWeights, H: int, W: in
     return (shift, dsel, mu, s) if want_params else (shift, dsel)
 
 
-def encode_to_indices(image, weights: ModelWeights) -> np.ndarray:
+def encode_to_indices(image, weights: ModelWeights, *, precise: bool = False) -> np.ndarray:
     """Nearest-codebook index per latent; ties take the smaller index."""
     validate_image(image)
     _require_network(weights)
     dev = require_device()
     stream = torch.cuda.current_stream(dev)
     img_d = as_device_u8(np.asarray(image)[None], dev, stream)
-    return encode_indices_device(img_d, weights, dev, stream)[0].cpu().numpy()
+    return encode_indices_device(img_d, weights, dev, stream, precise=precise)[0].cpu().numpy()
 
 
-def encoder_latents(image, weights: ModelWeights) -> np.ndarray:
+def encoder_latents(image, weights: ModelWeights, *, precise: bool = False) -> np.ndarray:
     """Pre-argmin latents z (gh, gw, Dc) float32 (testing hook)."""
     validate_image(image)
     _require_network(weights)
@@ -98,7 +101,7 @@ def encoder_latents(image, weights: ModelWeights) -> np.ndarray:
     gh, gw = latent_shape(H, W)
     z = torch.empty((1, gh, gw, weights.config.Dc), dtype=torch.float32, device=dev)
     img_d = as_device_u8(np.asarray(image)[None], dev, stream)
-    encode_indices_device(img_d, weights, dev, stream, z_out=z)
+    encode_indices_device(img_d, weights, dev, stream, z_out=z, precise=precise)
     return z[0].cpu().numpy()
 
 

@@ -196,6 +196,26 @@ def test_vqvae_encoder_and_decoder_vs_reference(golden, tag, small_model, full_m
     assert agree == total, f"index agreement {agree}/{total}"
 
 
+def test_tf32x3_encoder_vs_fp32(golden, full_model):
+    """Production encoder of the default model: 3xTF32 tcgen05 block convs
+    (hi/lo split, three MMAs per K step). z must stay fp32-class (compared
+    with the fp32 SIMT kernels and with the reference's numpy/BLAS z) and the
+    codebook indices must equal the reference's."""
+    z = golden("vqvae_full.npz")
+    imgs = list(smooth_images(24, 32, 32, seed=77))
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        zt = vqvae.encoder_latents(img, full_model)
+        zf = vqvae.encoder_latents(img, full_model, precise=True)
+        scale = np.abs(zf).max()
+        assert np.abs(zt - zf).max() <= 2e-5 * scale, np.abs(zt - zf).max() / scale
+        assert np.abs(zt - z[f"z{k}"]).max() <= 2e-5 * scale
+        assert np.array_equal(vqvae.encode_to_indices(img, full_model), z[f"idx{k}"])
+    for img in imgs:  # production and fp32 SIMT encoders pick the same codes
+        assert np.array_equal(vqvae.encode_to_indices(img, full_model),
+                              vqvae.encode_to_indices(img, full_model, precise=True))
+
+
 def test_tcgen05_decoder_vs_fp32(golden, full_model):
     """The production decoder of the default model runs tcgen05 bf16
     (csrc/tc_conv.cu); compare with the fp32 SIMT decoder and the
