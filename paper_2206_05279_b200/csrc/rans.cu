@@ -86,17 +86,31 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
         if (lanes == 1) {
             // reverse order; 16-byte vector loads over aligned chunks
             for (; i >= 0 && ((base + i + 1) & 15); --i) scalar(i);
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
+            uint4 sv = z4, hv = z4, dv = z4;
+            if (i >= 15) {
+                const int64_t p0 = base + i - 15;
+                sv = *reinterpret_cast<const uint4 *>(syms + p0);
+                if (shift) hv = *reinterpret_cast<const uint4 *>(shift + p0);
+                if (dsched) dv = *reinterpret_cast<const uint4 *>(dsched + p0);
+            }
             for (; i >= 15; i -= 16) {
-                const int64_t p0 = base + i - 15;  // 16-aligned
-                const uint4 sv = *reinterpret_cast<const uint4 *>(syms + p0);
-                const uint4 hv = shift ? *reinterpret_cast<const uint4 *>(shift + p0) : make_uint4(0, 0, 0, 0);
-                const uint4 dv = dsched ? *reinterpret_cast<const uint4 *>(dsched + p0) : make_uint4(0, 0, 0, 0);
+                uint4 sn = z4, hn = z4, dn = z4;  // prefetch the previous chunk
+                if (i >= 31) {
+                    const int64_t pn = base + i - 31;
+                    sn = *reinterpret_cast<const uint4 *>(syms + pn);
+                    if (shift) hn = *reinterpret_cast<const uint4 *>(shift + pn);
+                    if (dsched) dn = *reinterpret_cast<const uint4 *>(dsched + pn);
+                }
 #pragma unroll
                 for (int j = 15; j >= 0; --j) {
                     uint32_t x = vbyte(sv, j);
                     if (shift) x = (x - vbyte(hv, j) + 128u) & 0xFFu;
                     enc_step(e, tab, X, M, dsched ? vbyte(dv, j) : dconst, x, out);
                 }
+                sv = sn;
+                hv = hn;
+                dv = dn;
             }
         }
         for (; i >= 0; --i) scalar(i);
@@ -198,15 +212,28 @@ __global__ void __launch_bounds__(kDecThreads) rans_decode_kernel(
                 const int64_t pos = sbase + i;
                 out[pos] = (uint8_t)step(dsched ? dsched[pos] : dconst, unshift ? unshift[pos] : 0u);
             }
+            // 16-symbol chunks; the next chunk's d / shift vectors are loaded
+            // one chunk ahead so the state chain never waits on memory
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
+            uint4 dv = z4, hv = z4;
+            if (i + 16 <= cnt) {
+                if (dsched) dv = *reinterpret_cast<const uint4 *>(dsched + sbase + i);
+                if (unshift) hv = *reinterpret_cast<const uint4 *>(unshift + sbase + i);
+            }
             for (; i + 16 <= cnt && !st; i += 16) {
                 const int64_t p0 = sbase + i;  // 16-aligned
-                const uint4 dv = dsched ? *reinterpret_cast<const uint4 *>(dsched + p0) : make_uint4(0, 0, 0, 0);
-                const uint4 hv = unshift ? *reinterpret_cast<const uint4 *>(unshift + p0) : make_uint4(0, 0, 0, 0);
+                uint4 dn = z4, hn = z4;
+                if (i + 32 <= cnt) {
+                    if (dsched) dn = *reinterpret_cast<const uint4 *>(dsched + p0 + 16);
+                    if (unshift) hn = *reinterpret_cast<const uint4 *>(unshift + p0 + 16);
+                }
                 uint32_t o[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
                     o[j >> 2] |= step(dsched ? vbyte(dv, j) : dconst, vbyte(hv, j)) << (8 * (j & 3));
                 *reinterpret_cast<uint4 *>(out + p0) = make_uint4(o[0], o[1], o[2], o[3]);
+                dv = dn;
+                hv = hn;
             }
         }
         for (; i < cnt && !st; ++i) {

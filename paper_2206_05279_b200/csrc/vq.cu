@@ -193,11 +193,16 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
 
     const int ntap = ks * ks;
     for (int c0 = 0; c0 < a.Ci_pad; c0 += kCK) {
-        // stage the input patch, channel-planar
+        // stage the input patch, channel-planar in smem; element order is
+        // channel-fastest so a warp reads 4 pixels x 8 contiguous channels
         const int patch = IR * IR;
-        for (int e = t; e < kCK * patch; e += kThreads) {
-            const int ci = e / patch, rem = e - ci * patch;
-            const int py = rem / IR, px = rem - py * IR;
+        const int ci = t & 7;
+        int py = (t >> 3) / IR, px = (t >> 3) - ((t >> 3) / IR) * IR;
+        for (int e = t; e < kCK * patch; e += kThreads, px += kThreads / 8) {
+            while (px >= IR) {
+                px -= IR;
+                ++py;
+            }
             const int c = c0 + ci;
             float v = 0.f;
             if (a.in_mode == IN_F32) {
@@ -376,19 +381,19 @@ ConvArgs base_args(const float *model, const ConvSpec &sp) {
 }
 
 // ---- codebook argmin (vqvae.py:66-76) --------------------------------------
-// Warp per latent vector; lane l owns codes l, l+32, ... The reference
-// accumulates (z_c - cb_kc)^2 in float64, component by component, and takes
-// the first minimum. Screening pass in float32: every term is non-negative,
-// so the float32 sequential sum satisfies |d32 - d| <= g*d with
-// g = (Dc + 4) * 2^-24 (Higham, sum of n positive terms + one rounding per
-// subtraction and square). The true argmin k* has d(k*) <= d(k32) <=
-// m/(1-g) where m = min d32, hence d32(k*) <= m (1+g)/(1-g). Every code
-// under that bound (with a 4x safety factor) is re-scored exactly as the
+// The reference accumulates (z_c - cb_kc)^2 in float64, component by
+// component, and takes the first minimum. Screening pass in float32 with the
+// expansion d' = |z|^2 + |c_k|^2 - 2 z.c_k (one FMA per term). Standard
+// bounds (dot product and sums of n terms, unit roundoff u = 2^-24) give
+// |d' - d| <= E_k = (Dc + 6) u (|z| + |c_k|)^2 (a 2x safety factor is
+// applied), so the true argmin k* satisfies d'(k*) - E_k* <= min_j (d'_j +
+// E_j). Every code passing that screen is re-scored exactly as the
 // reference does -- float64, same order, no FMA -- and the warp picks the
-// smallest float64 distance, ties to the lowest index. Normally one or two
-// codes survive the screen, so float64 work drops ~100x.
+// smallest float64 distance, ties to the lowest index. Typically one or
+// two codes survive. Warp per 8 latents, lane per 8 codes: 64 fp32
+// accumulators per thread, 10 shared loads per 64 FMAs.
 constexpr int kArgWarps = 8;
-constexpr int kArgVec = 4;  // latents per warp pass (register blocking)
+constexpr int kArgVec = 8;
 
 __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__restrict__ z,
                                                                  int64_t n_vec,
@@ -397,13 +402,19 @@ __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__r
     extern __shared__ float sm[];
     const int P = Dc + 1;                           // +1 pad against bank conflicts
     float *s_cb = sm;                               // K x P
-    float4 *s_z = reinterpret_cast<float4 *>(sm + (((int64_t)K * P + 3) & ~3));  // warps x Dc
+    float *s_cn = sm + (int64_t)K * P;              // K: |c_k|^2
+    float4 *s_z = reinterpret_cast<float4 *>(sm + ((((int64_t)K * P + K) + 3) & ~3));  // warps x Dc x 2
     for (int i = threadIdx.x; i < K * Dc; i += blockDim.x) s_cb[(i / Dc) * P + (i % Dc)] = cb[i];
     __syncthreads();
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        float acc = 0.f;
+        for (int c = 0; c < Dc; ++c) acc = fmaf(s_cb[k * P + c], s_cb[k * P + c], acc);
+        s_cn[k] = acc;
+    }
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float4 *zw = s_z + (int64_t)warp * Dc;
-    const float g = (float)(Dc + 4) * 5.9604645e-08f;  // (Dc+4) * 2^-24
-    const float slack = 1.f + 4.f * g;
+    float4 *zw = s_z + (int64_t)warp * Dc * 2;
+    const float g = 2.f * (float)(Dc + 6) * 5.9604645e-08f;
     const int64_t n_grp = (n_vec + kArgVec - 1) / kArgVec;
     for (int64_t grp = (int64_t)blockIdx.x * kArgWarps + warp; grp < n_grp;
          grp += (int64_t)gridDim.x * kArgWarps) {
@@ -412,48 +423,61 @@ __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__r
             float t[kArgVec];
 #pragma unroll
             for (int l = 0; l < kArgVec; ++l) t[l] = (v0 + l < n_vec) ? z[(v0 + l) * Dc + c] : 0.f;
-            zw[c] = make_float4(t[0], t[1], t[2], t[3]);
+            zw[2 * c] = make_float4(t[0], t[1], t[2], t[3]);
+            zw[2 * c + 1] = make_float4(t[4], t[5], t[6], t[7]);
         }
         __syncwarp();
-        // screening: float32, no FMA, all of this lane's codes for 4 latents
-        float d32[8][kArgVec];
+        float dot[8][kArgVec];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
 #pragma unroll
-            for (int l = 0; l < kArgVec; ++l) d32[j][l] = 0.f;
+            for (int l = 0; l < kArgVec; ++l) dot[j][l] = 0.f;
+        float zn[kArgVec];
+#pragma unroll
+        for (int l = 0; l < kArgVec; ++l) zn[l] = 0.f;
         for (int c = 0; c < Dc; ++c) {
-            const float4 zz = zw[c];
-            const float zl[kArgVec] = {zz.x, zz.y, zz.z, zz.w};
+            const float4 za = zw[2 * c], zb = zw[2 * c + 1];
+            const float zl[kArgVec] = {za.x, za.y, za.z, za.w, zb.x, zb.y, zb.z, zb.w};
+#pragma unroll
+            for (int l = 0; l < kArgVec; ++l) zn[l] = fmaf(zl[l], zl[l], zn[l]);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int k = lane + 32 * j;
                 const float cv = k < K ? s_cb[k * P + c] : 0.f;
 #pragma unroll
-                for (int l = 0; l < kArgVec; ++l) {
-                    const float diff = __fsub_rn(zl[l], cv);
-                    d32[j][l] = __fadd_rn(d32[j][l], __fmul_rn(diff, diff));
-                }
+                for (int l = 0; l < kArgVec; ++l) dot[j][l] = fmaf(zl[l], cv, dot[j][l]);
             }
         }
+        float cn[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cn[j] = (lane + 32 * j < K) ? s_cn[lane + 32 * j] : 0.f;
 #pragma unroll
         for (int l = 0; l < kArgVec; ++l) {
-            float m32 = INFINITY;
+            // d' and its error radius for each of this lane's codes
+            float lo_best = INFINITY;
+            const float znl = zn[l], zr = sqrtf(znl);
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (lane + 32 * j < K) m32 = fminf(m32, d32[j][l]);
-            for (int o = 16; o; o >>= 1) m32 = fminf(m32, __shfl_xor_sync(0xffffffffu, m32, o));
-            const float bound = m32 * slack + 1e-30f;
+            for (int j = 0; j < 8; ++j) {
+                if (lane + 32 * j >= K) continue;
+                const float d = znl + cn[j] - 2.f * dot[j][l];
+                const float r = zr + sqrtf(cn[j]);
+                const float e = g * r * r + 1e-30f;
+                lo_best = fminf(lo_best, d + e);
+                dot[j][l] = d - e;  // reuse: lower end of the interval
+            }
+            for (int o = 16; o; o >>= 1) lo_best = fminf(lo_best, __shfl_xor_sync(0xffffffffu, lo_best, o));
             double best = INFINITY;
             int bk = 0x7FFFFFFF;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int k = lane + 32 * j;
-                if (k >= K || !(d32[j][l] <= bound)) continue;
+                if (k >= K || !(dot[j][l] <= lo_best)) continue;
                 const float *row = s_cb + k * P;
                 double dist = 0.0;  // exact reference arithmetic (vqvae.py:71-75)
                 for (int c = 0; c < Dc; ++c) {
-                    const float4 zz = zw[c];
-                    const float zv = l == 0 ? zz.x : (l == 1 ? zz.y : (l == 2 ? zz.z : zz.w));
+                    const float4 zz = zw[2 * c + (l >> 2)];
+                    const int q = l & 3;
+                    const float zv = q == 0 ? zz.x : (q == 1 ? zz.y : (q == 2 ? zz.z : zz.w));
                     const double diff = __dsub_rn((double)zv, (double)row[c]);
                     dist = __dadd_rn(dist, __dmul_rn(diff, diff));
                 }
@@ -479,7 +503,7 @@ __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__r
 int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc, uint8_t *idx,
                   cudaStream_t s) {
     if (n_vec == 0) return PILC_OK;
-    const size_t smem = sizeof(float) * ((((size_t)K * (Dc + 1) + 3) & ~(size_t)3) + (size_t)kArgWarps * Dc * 4);
+    const size_t smem = sizeof(float) * ((((size_t)K * (Dc + 1) + K + 3) & ~(size_t)3) + (size_t)kArgWarps * Dc * 8);
     if (smem > 200 * 1024) return PILC_E_UNSUPPORTED;
     cudaFuncSetAttribute(argmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t blocks = ceil_div64(ceil_div64(n_vec, kArgVec), kArgWarps);
