@@ -35,6 +35,14 @@ BATCH = 8192
 H = W = 32
 WORKLOAD = "cifar10-32x32x3-synthetic-smooth, batch 8192/GPU, twar-vqvae full model (K256 Dc32 C32 B4, seed 1), M=12, L=1"
 METRIC = "PILC round-trip (compress+decompress) raw-image MB/s"
+# BASELINE.json configs: [1] is the default line; the others are --workload
+WORKLOADS = {
+    "cifar": dict(H=32, W=32, N=8192, desc=WORKLOAD),
+    "in64": dict(H=64, W=64, N=4096, desc="imagenet64-64x64x3-synthetic-smooth, batch 4096/GPU, twar-vqvae full "
+                                          "model (seed 1), M=12, L=1"),
+    "1080p": dict(H=1080, W=1920, N=8, desc="1920x1080x3 synthetic-smooth frames, 8/GPU, split into 64x64 patch "
+                                           "containers (510/frame), twar-vqvae full model (seed 1), M=12, L=1"),
+}
 
 
 def _dist():
@@ -197,9 +205,19 @@ def run_gpu(args):
     stream = torch.cuda.current_stream(dev)
     model = pc.random_weights(seed=1)
     cfg = pc.CodecConfig(backend="twar-vqvae")
-    imgs = smooth_images(BATCH, H, W, seed=rank)
+    wl = WORKLOADS[args.workload]
+    if args.workload == "1080p":
+        from paper_2206_05279_b200 import patches as pt
+        frames = np.stack([smooth_images(1, wl["H"], wl["W"], seed=1000 * rank + f)[0] for f in range(wl["N"])])
+        plist = [p for f in frames for p in pt.split_frame(f)]
+        shapes = sorted({p.shape for p in plist})
+        groups_h = [np.stack([p for p in plist if p.shape == sh]) for sh in shapes]
+        imgs = frames
+    else:
+        imgs = smooth_images(wl["N"], wl["H"], wl["W"], seed=rank)
+        groups_h = [imgs]
     raw_bytes = imgs.size
-    img_d = torch.from_numpy(imgs).to(dev)
+    groups_d = [torch.from_numpy(g).to(dev) for g in groups_h]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -208,20 +226,25 @@ def run_gpu(args):
         torch.cuda.synchronize(dev)
 
     def step_device():
-        out_d, off_d, total = ct._compress_device(img_d, model, cfg, dev, stream)
-        offs_host = off_d.cpu().numpy().view(np.uint64)
-        results, errors, hdr = ct._decompress_device(out_d, off_d, offs_host, model, dev, stream)
-        return out_d, offs_host, results, errors
+        outs = []
+        for img_d in groups_d:
+            out_d, off_d, total = ct._compress_device(img_d, model, cfg, dev, stream)
+            offs_host = off_d.cpu().numpy().view(np.uint64)
+            results, errors, hdr = ct._decompress_device(out_d, off_d, offs_host, model, dev, stream)
+            outs.append((offs_host, results, errors))
+        return outs
 
     # warm-up (+ correctness of the device path, outside the timed region)
     for _ in range(args.warmup):
-        out_d, offs_host, results, errors = step_device()
+        outs = step_device()
     torch.cuda.synchronize(dev)
-    assert not errors, errors
-    dec = results[0][1].cpu().numpy()
-    lossless = bool(np.array_equal(dec, imgs))
-    blob_sizes = np.diff(offs_host.astype(np.int64))
-    bpd = float(np.mean(8.0 * blob_sizes / (H * W * 3)))
+    lossless = True
+    bits = 0.0
+    for g, (offs_host, results, errors) in zip(groups_h, outs):
+        assert not errors, errors
+        lossless &= bool(np.array_equal(results[0][1].cpu().numpy(), g))
+        bits += 8.0 * float(np.diff(offs_host.astype(np.int64)).sum())
+    bpd = bits / float(sum(g.size for g in groups_h))
 
     # timed region: device-resident inputs
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -233,10 +256,11 @@ def run_gpu(args):
             flush.fill_(k & 0xFF)  # evict L2 between steps (outside the events)
             e0, e1, e2 = ev[k]
             e0.record(stream)
-            out_d, off_d, total = ct._compress_device(img_d, model, cfg, dev, stream)
+            packed = [ct._compress_device(img_d, model, cfg, dev, stream) for img_d in groups_d]
             e1.record(stream)
-            offs_host = off_d.cpu().numpy().view(np.uint64)
-            ct._decompress_device(out_d, off_d, offs_host, model, dev, stream)
+            for out_d, off_d, total in packed:
+                offs_host = off_d.cpu().numpy().view(np.uint64)
+                ct._decompress_device(out_d, off_d, offs_host, model, dev, stream)
             e2.record(stream)
         barrier()
     launches = _lib.prof_launches()
@@ -255,17 +279,35 @@ def run_gpu(args):
     e2e_times = []
     h2d = d2h = 0
     barrier()
+    lat = None
     for k in range(max(1, args.steps)):
         flush.fill_(k & 0xFF)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        buf, off = pc.compress_batch(imgs, model, cfg)
-        out = pc.decompress_batch(buf, off, model)
+        if args.workload == "1080p":
+            buf, off = pt.compress_frames(imgs, model, cfg)
+            out = pt.decompress_frames(buf, off, len(imgs), wl["H"], wl["W"], model)
+        else:
+            buf, off = pc.compress_batch(imgs, model, cfg)
+            out = pc.decompress_batch(buf, off, model)
         torch.cuda.synchronize(dev)
         e2e_times.append(time.perf_counter() - t0)
         h2d = imgs.nbytes + buf.nbytes + off.nbytes
         d2h = buf.nbytes + off.nbytes + out.nbytes
     assert np.array_equal(out, imgs)
+    if args.workload == "1080p":
+        # single-frame decompress latency: blobs in host RAM -> frame in RAM
+        per = len(pt.patch_grid(wl["H"], wl["W"]))
+        fb = buf[: int(off[per])]
+        fo = off[: per + 1]
+        ts = []
+        for _ in range(5):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            fr = pt.decompress_frames(fb, fo, 1, wl["H"], wl["W"], model)
+            ts.append(time.perf_counter() - t0)
+        assert np.array_equal(fr[0], imgs[0])
+        lat = round(1000 * statistics.median(ts), 3)
     te = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -318,8 +360,9 @@ def run_gpu(args):
             "vs_baseline": None,
             "dtype": "f32 (network, SIMT), f64 (argmin), int (coder/predictor/container)",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": BATCH * ws, "image": [H, W, 3],
+            "config": {"workload": wl["desc"], "global_batch": wl["N"] * ws, "image": [wl["H"], wl["W"], 3],
                        "parallelism": f"shard{ws}", "l2": "flushed (256 MiB write) before each step"},
+            "frame_decompress_latency_ms": lat,
             "compress_mb_s": round(raw_bytes * ws / 1e6 / t_cs, 3),
             "decompress_mb_s": round(raw_bytes * ws / 1e6 / t_ds, 3),
             "bpd": round(bpd, 4),
@@ -336,6 +379,87 @@ def run_gpu(args):
     if ws > 1:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
+    return 0
+
+
+def run_coder(args):
+    """configs[4]: coder only. n = 2^26 symbols from the paper's Table-6
+    generator (report._bench_symbols, report.py:34-44: d uniform over the 8
+    default-grid distributions, symbol ~ PMF_d, seed 0); symbol i -> lane
+    i mod L. Encode and decode each timed with CUDA events (device-resident
+    symbols / d / lane payloads); GB/s counts algorithmic bytes (symbol + d +
+    payload), the SURVEY §8d unit."""
+    import numpy as np
+    import torch
+
+    from paper_2206_05279_b200 import _lib, tables
+    from paper_2206_05279_b200.device import ptr, sptr
+    from paper_2206_05279_b200.logistic import default_grid, residual_distributions
+
+    _, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    M, n = 12, 1 << 26
+    pmfs = residual_distributions(default_grid(), M)
+    rng = np.random.default_rng(0)
+    d = rng.integers(0, 8, n).astype(np.uint8)
+    syms = np.empty(n, np.uint8)
+    for i, pmf in enumerate(pmfs):
+        sel = d == i
+        syms[sel] = rng.choice(256, int(sel.sum()), p=pmf.P.astype(np.float64) / (1 << M))
+    enc, dec = tables.build_tables(pmfs, M)
+    s_d = torch.from_numpy(syms).to(dev)
+    d_d = torch.from_numpy(d).to(dev)
+    rows = []
+    for L in [1 << k for k in (10, 12, 14, 16, 18, 20)]:
+        def encode():
+            return tables.encode_lanes_device(s_d, 1, n, L, enc, dev, stream, dsched=d_d)
+        scr, cap, nb, st = encode()
+        lane_off = torch.arange(L, dtype=torch.int64, device=dev) * (cap * 4)
+        out = torch.empty(n, dtype=torch.uint8, device=dev)
+        lstat = torch.zeros(L, dtype=torch.uint8, device=dev)
+
+        def decode():
+            lstat.zero_()
+            _lib.call("pilc_rans_decode", ptr(scr), ptr(lane_off), ptr(nb), ptr(st), ptr(d_d), None, 1, n, L,
+                      ptr(dec.device_words(dev)), dec.D, M, None, ptr(out), ptr(lstat), sptr(stream))
+        decode()
+        torch.cuda.synchronize(dev)
+        assert torch.equal(out, s_d) and int(lstat.max()) == 0
+        payload = float(nb.to(torch.int64).sum().item()) / 8.0
+        te, td = [], []
+        for _ in range(max(args.steps, 1)):
+            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a.record(stream)
+            encode()
+            b.record(stream)
+            decode()
+            c.record(stream)
+            torch.cuda.synchronize(dev)
+            te.append(a.elapsed_time(b) / 1e3)
+            td.append(b.elapsed_time(c) / 1e3)
+        algo = 2.0 * n + payload
+        rows.append({"lanes": L, "bits_per_symbol": round(8 * payload / n, 4),
+                     "encode_gb_s": round(algo / statistics.median(te) / 1e9, 2),
+                     "decode_gb_s": round(algo / statistics.median(td) / 1e9, 2),
+                     "encode_msym_s": round(n / statistics.median(te) / 1e6, 1),
+                     "decode_msym_s": round(n / statistics.median(td) / 1e6, 1)})
+    if rank == 0:
+        peak = None
+        try:
+            with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+                peak = json.load(f).get("hbm_gbs")
+        except OSError:
+            peak = 6650.0
+        best = max(rows, key=lambda r: r["decode_gb_s"])
+        print(json.dumps({"metric": "rANS coder-only decode GB/s (algorithmic bytes)", "value": best["decode_gb_s"],
+                          "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                          "higher_is_better": True, "data": "synthetic",
+                          "config": {"workload": "coder-only sweep, n=2^26 Table-6 symbols, D=8, M=12"},
+                          "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
+                                       "frac": round(best["decode_gb_s"] / (peak / 1.0), 4)},
+                          "sweep": rows}), flush=True)
     return 0
 
 
@@ -356,9 +480,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--workload", default="cifar", choices=sorted(WORKLOADS) + ["coder"],
+                    help="BASELINE config: cifar (configs[1], default), in64 (configs[2]), 1080p (configs[3]), "
+                         "coder (configs[4], coder-only lane sweep)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "coder":
+        return run_coder(args)
     return run_gpu(args)
 
 

@@ -262,6 +262,9 @@ int32_t pilc_prof_categories(void);
 const char *pilc_prof_name(int32_t cat);
 int pilc_prof_read(int32_t cat, int64_t *launches, double *total_ms,
                    double *units);
+/* Per-launch records in launch order (timing enabled only). */
+int64_t pilc_prof_count(void);
+int pilc_prof_record(int64_t i, int32_t *cat, double *ms, double *units);
 
 #ifdef __cplusplus
 }

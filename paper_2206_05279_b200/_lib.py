@@ -47,6 +47,8 @@ _SIGS = {
     "pilc_prof_categories": (I32, []),
     "pilc_prof_name": (ctypes.c_char_p, [I32]),
     "pilc_prof_read": (ctypes.c_int, [I32, P, P, P]),
+    "pilc_prof_count": (I64, []),
+    "pilc_prof_record": (ctypes.c_int, [I64, P, P, P]),
 }
 
 # pilc_header (include/pilc.h), 72 bytes
@@ -122,6 +124,17 @@ def prof_read() -> dict:
         call("pilc_prof_read", c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(u))
         if n.value:
             out[lib.pilc_prof_name(c).decode()] = (n.value, ms.value, u.value)
+    return out
+
+
+def prof_records() -> list:
+    """[(kernel, ms, work_units)] per launch, in launch order."""
+    lib = load()
+    out = []
+    for i in range(lib.pilc_prof_count()):
+        c, ms, u = ctypes.c_int32(), ctypes.c_double(), ctypes.c_double()
+        call("pilc_prof_record", i, ctypes.byref(c), ctypes.byref(ms), ctypes.byref(u))
+        out.append((lib.pilc_prof_name(c.value).decode(), ms.value, u.value))
     return out
 
 

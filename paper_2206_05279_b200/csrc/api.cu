@@ -55,6 +55,24 @@ extern "C" void pilc_prof_reset(int32_t enable_timing) {
 
 extern "C" int64_t pilc_prof_launches(void) { return g_launches.load(); }
 
+extern "C" int64_t pilc_prof_count(void) {
+    std::lock_guard<std::mutex> g(g_mu);
+    return (int64_t)g_recs.size();
+}
+
+extern "C" int pilc_prof_record(int64_t i, int32_t *cat, double *ms, double *units) {
+    std::lock_guard<std::mutex> g(g_mu);
+    if (i < 0 || i >= (int64_t)g_recs.size()) return PILC_E_ARG;
+    const Rec &r = g_recs[(size_t)i];
+    if (cudaEventSynchronize(r.e1) != cudaSuccess) return PILC_E_CUDA;
+    float t = 0;
+    cudaEventElapsedTime(&t, r.e0, r.e1);
+    *cat = r.cat;
+    *ms = t;
+    *units = r.units;
+    return PILC_OK;
+}
+
 extern "C" int32_t pilc_prof_categories(void) { return PROF_NCAT; }
 
 extern "C" const char *pilc_prof_name(int32_t cat) {

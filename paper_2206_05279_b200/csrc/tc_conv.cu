@@ -435,10 +435,10 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// Round to tf32 (10 mantissa bits), nearest with ties away from zero, in
+// integer ops (cvt.rna.tf32 issues on the XU pipe). Finite inputs only.
 __device__ __forceinline__ float tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void store_px4(float *slab, int64_t q, float4 v, int y, int x, int H, int W, int Wp) {

@@ -298,9 +298,7 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
                 for (int e = 0; e < 4; ++e) {
                     float v = __fadd_rn(acc[4 * g + e], a.b[co0 + 4 * g + e]);
                     if (a.relu) v = fmaxf(v, 0.f);
-                    uint32_t r;
-                    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-                    hi[e] = __uint_as_float(r);
+                    hi[e] = __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);  // tf32 rna
                     lo[e] = __fsub_rn(v, hi[e]);
                 }
                 const int64_t so = ((int64_t)((co0 >> 2) + g) * a.out_gstride + a.out_margin) * 4;
@@ -453,19 +451,36 @@ __global__ void __launch_bounds__(32 * kArgWarps) argmin_kernel(const float *__r
         for (int j = 0; j < 8; ++j) cn[j] = (lane + 32 * j < K) ? s_cn[lane + 32 * j] : 0.f;
 #pragma unroll
         for (int l = 0; l < kArgVec; ++l) {
-            // d' and its error radius for each of this lane's codes
+            // d' and its error radius for each of this lane's codes;
+            // (|z| + |c|)^2 <= 2 (|z|^2 + |c|^2) avoids square roots
             float lo_best = INFINITY;
-            const float znl = zn[l], zr = sqrtf(znl);
+            const float znl = zn[l];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (lane + 32 * j >= K) continue;
                 const float d = znl + cn[j] - 2.f * dot[j][l];
-                const float r = zr + sqrtf(cn[j]);
-                const float e = g * r * r + 1e-30f;
+                const float e = 2.f * g * (znl + cn[j]) + 1e-30f;
                 lo_best = fminf(lo_best, d + e);
                 dot[j][l] = d - e;  // reuse: lower end of the interval
             }
             for (int o = 16; o; o >>= 1) lo_best = fminf(lo_best, __shfl_xor_sync(0xffffffffu, lo_best, o));
+            int ncand = 0, kc = 0x7FFFFFFF;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = lane + 32 * j;
+                if (k < K && dot[j][l] <= lo_best) {
+                    ++ncand;
+                    kc = min(kc, k);
+                }
+            }
+            int tot = ncand;
+            for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            if (tot == 1) {
+                // a single code survives: it is the exact argmin, no float64 needed
+                for (int o = 16; o; o >>= 1) kc = min(kc, __shfl_xor_sync(0xffffffffu, kc, o));
+                if (lane == 0 && v0 + l < n_vec) idx[v0 + l] = (uint8_t)kc;
+                continue;
+            }
             double best = INFINITY;
             int bk = 0x7FFFFFFF;
 #pragma unroll

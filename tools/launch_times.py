@@ -1,0 +1,23 @@
+"""Per-launch device times of one compress + decompress step (live, CUDA events)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2206_05279_b200 as pc
+from paper_2206_05279_b200 import _lib, container as ct
+from paper_2206_05279_b200.synth import smooth_images
+H = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+N = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
+dev = torch.device("cuda", 0); stream = torch.cuda.current_stream(dev)
+model = pc.random_weights(seed=1); cfg = pc.CodecConfig(backend="twar-vqvae")
+img_d = torch.from_numpy(smooth_images(N, H, H, seed=0)).to(dev)
+def step():
+    o, off, t = ct._compress_device(img_d, model, cfg, dev, stream)
+    offs = off.cpu().numpy().view(np.uint64)
+    ct._decompress_device(o, off, offs, model, dev, stream)
+for _ in range(3): step()
+torch.cuda.synchronize(); _lib.prof_reset(True); step(); torch.cuda.synchronize()
+tot = 0
+for k, ms, u in _lib.prof_records():
+    tot += ms
+    print(f"{k:22s} {ms*1e3:9.1f} us  units={u:.3g}")
+print("sum", tot)
