@@ -137,7 +137,9 @@ int pilc_rans_encode(const uint8_t *syms, const uint8_t *shift,
  * buf + lane_off[i*lanes + l] and holds nbits bits; initial state
  * states[...]. lane_status (in/out, uint8 per lane): lanes whose status is
  * already non-zero (from pilc_container_lanes) are skipped; otherwise set
- * to PILC_ST_UNDERFLOW / PILC_ST_END_STATE / 0. Symbols are written to
+ * to PILC_ST_UNDERFLOW / PILC_ST_END_STATE / 0. `buf` must stay readable
+ * 16 bytes past the last lane payload (16-byte chunked backward reads).
+ * Symbols are written to
  * out + i*n_sym + j; if unshift != NULL they are un-recentred on the way
  * out, out = (x + unshift - 128) & 255. */
 int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off,

@@ -146,7 +146,7 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
         total_h.copy_(blob_off[N:].view(torch.uint8), non_blocking=True)
     stream.synchronize()
     total = int(total_h.numpy().view(np.uint64)[0])
-    out_d = torch.empty(total + 8, dtype=torch.uint8, device=dev)
+    out_d = torch.empty(total + 16, dtype=torch.uint8, device=dev)
     tb = CACHE.get(("tmpl", tmpl), dev, lambda: torch.frombuffer(bytearray(tmpl), dtype=torch.uint8).to(dev))
     _lib.call("pilc_container_pack", ptr(tb), len(tmpl), ptr(d_img), ptr(dsched),
               1 if config.debug_schedule_check else 0, N, n_sym, L, ptr(idx_scr), idx_cap, ptr(idx_nb),
@@ -436,7 +436,7 @@ def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=
     if base or int(offs[-1]) > buf_host.size:
         if int(offs[-1]) > buf_host.size:
             raise FormatError("container truncated")
-    buf_d = h2d(buf_host[: int(offs[-1])], dev, stream, pad=8)
+    buf_d = h2d(buf_host[: int(offs[-1])], dev, stream, pad=16)
     off_d = h2d(offs.view(np.uint8), dev, stream).view(torch.int64)
     results, errors, hdr = _decompress_device(buf_d, off_d, offs, model, dev, stream, buf_host)
     errors = _resolve_errors(results, errors, hdr)

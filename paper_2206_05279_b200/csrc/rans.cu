@@ -18,7 +18,6 @@
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kDecThreads = 64;  // 128 KB table per CTA: more CTAs, fewer idle threads
 constexpr int kSmemTableMax = 160 * 1024;
 
 __device__ __forceinline__ int lane_count(int64_t n_sym, int lanes, int l) {
@@ -127,24 +126,44 @@ __device__ __forceinline__ uint32_t load_word(const uint32_t *base_w, int64_t w,
     return (w >= lo_w && w <= hi_w) ? __ldg(base_w + w) : 0u;
 }
 
-// Backward bit reader: a 64-bit window over aligned words plus a 4-deep
-// prefetch of the next lower words, so refills never wait on memory.
+// Backward bit reader. A 64-bit window over aligned 32-bit words is refilled
+// one word at a time from 16-byte chunks held in registers: `cur` holds the
+// chunk being consumed, `nxt` the one below it, loaded a whole chunk (128
+// bits, ~10 symbols) before it is needed, so the state chain never waits on
+// memory. Chunks never straddle the lane's first or last word by more than
+// 12 bytes; buffers are padded by 16 bytes (pilc.h).
 struct BitReader {
-    const uint32_t *words;
-    int64_t lo_w, hi_w, wlo, A, start;
+    const uint4 *base4;
+    int64_t A, start, wlo, cq;
     uint64_t win;
-    uint32_t pf[4];
+    uint4 cur, nxt;
 
-    __device__ __forceinline__ void init(const uint32_t *w, int64_t start_bit, uint32_t nb) {
-        words = w;
+    __device__ __forceinline__ uint4 chunk(int64_t c, int64_t lo_c, int64_t hi_c) const {
+        return (c >= lo_c && c <= hi_c) ? __ldg(base4 + c) : make_uint4(0, 0, 0, 0);
+    }
+    __device__ __forceinline__ static uint32_t pick(const uint4 &v, int k) {
+        return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+    }
+    int64_t lo_c, hi_c;
+
+    __device__ __forceinline__ void init(const uint32_t *words, int64_t start_bit, uint32_t nb) {
+        base4 = reinterpret_cast<const uint4 *>(words);
         start = start_bit;
-        lo_w = start_bit >> 5;
-        hi_w = (start_bit + (int64_t)nb - 1) >> 5;
+        const int64_t lo_w = start_bit >> 5;
+        const int64_t hi_w = (start_bit + (int64_t)nb - 1) >> 5;
+        lo_c = lo_w >> 2;
+        hi_c = nb ? (hi_w >> 2) : lo_c - 1;
         A = start_bit + nb;
-        wlo = ((A - 1) >> 5) - 1;
-        win = ((uint64_t)load_word(words, wlo + 1, lo_w, hi_w) << 32) | load_word(words, wlo, lo_w, hi_w);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) pf[j] = load_word(words, wlo - 1 - j, lo_w, hi_w);
+        wlo = ((A - 1) >> 5) - 1;  // window = bits [32*wlo, 32*wlo + 64)
+        const int64_t c_top = (wlo + 1) >> 2, c_lo = wlo >> 2;
+        const uint4 a = chunk(c_top, lo_c, hi_c);
+        const uint4 b = c_lo == c_top ? a : chunk(c_lo, lo_c, hi_c);
+        const uint64_t w1 = pick(a, (int)((wlo + 1) & 3));
+        const uint64_t w0 = pick(b, (int)(wlo & 3));
+        win = (w1 << 32) | w0;
+        cq = (wlo - 1) >> 2;  // chunk of the next word to bring in
+        cur = chunk(cq, lo_c, hi_c);
+        nxt = chunk(cq - 1, lo_c, hi_c);
     }
     // returns false on underflow
     __device__ __forceinline__ bool take(uint32_t b, uint32_t &v) {
@@ -152,11 +171,12 @@ struct BitReader {
         const int64_t lo = A - b;
         if (lo < wlo * 32) {
             wlo -= 1;
-            win = (win << 32) | pf[0];
-            pf[0] = pf[1];
-            pf[1] = pf[2];
-            pf[2] = pf[3];
-            pf[3] = load_word(words, wlo - 4, lo_w, hi_w);
+            if ((wlo >> 2) != cq) {  // move down one chunk, prefetch the next
+                cur = nxt;
+                cq -= 1;
+                nxt = chunk(cq - 1, lo_c, hi_c);
+            }
+            win = (win << 32) | pick(cur, (int)(wlo & 3));
         }
         v = (uint32_t)(win >> (lo - wlo * 32)) & ((1u << b) - 1u);
         A = lo;
@@ -164,25 +184,43 @@ struct BitReader {
     }
 };
 
-__global__ void __launch_bounds__(kDecThreads) rans_decode_kernel(
+__global__ void __launch_bounds__(512) rans_decode_kernel(
     const uint8_t *__restrict__ buf, const uint64_t *__restrict__ lane_off,
     const uint32_t *__restrict__ nbits_a, const uint16_t *__restrict__ states,
     const uint8_t *__restrict__ dsched, const uint16_t *__restrict__ d_img, int64_t n_img,
     int64_t n_sym, int lanes, const uint32_t *__restrict__ dec_tab_g, int D, int M,
     int tab_in_smem, const uint8_t *__restrict__ unshift, uint8_t *__restrict__ out,
     uint8_t *__restrict__ lane_status) {
-    extern __shared__ uint32_t s_tab[];
+    extern __shared__ __align__(16) uint32_t s_tab[];
+    __shared__ __align__(8) uint64_t tbar;
     const uint32_t *tab = dec_tab_g;
     if (tab_in_smem) {
-        const int n = D << M;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) s_tab[i] = dec_tab_g[i];
+        // one bulk copy of the whole table (up to 160 KB) instead of a
+        // per-thread load/store loop
+        const uint32_t bytes = (uint32_t)(D << M) * 4u;
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&tbar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    (uint32_t)__cvta_generic_to_shared(s_tab)),
+                "l"(dec_tab_g), "r"(bytes), "r"(bar)
+                : "memory");
+        }
         __syncthreads();
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+            "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(bar)
+            : "memory");
         tab = s_tab;
     }
-    // word-aligned view of the buffer (buffer base is at least 4-aligned)
-    const uintptr_t base_addr = reinterpret_cast<uintptr_t>(buf) & ~(uintptr_t)3;
+    // 16-byte aligned view of the buffer
+    const uintptr_t base_addr = reinterpret_cast<uintptr_t>(buf) & ~(uintptr_t)15;
     const uint32_t *words = reinterpret_cast<const uint32_t *>(base_addr);
-    const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(buf) - base_addr);  // 0..3
+    const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(buf) - base_addr);  // 0..15
     const int64_t total = n_img * lanes;
     const uint32_t T = 1u << M;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
@@ -290,15 +328,18 @@ extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, co
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(rans_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t total = n_img * lanes;
-    int64_t blocks = ceil_div64(total, kDecThreads);
-    // one table copy per block: keep the grid at one resident block per SM
-    // when the table is large, several when it is small
+    // one table copy per block; per_sm resident blocks fit in shared memory.
+    // Spread the lanes over every SM: threads per block = lanes / (SMs x
+    // per_sm), rounded to warps, in [32, 512].
     const int64_t per_sm = in_smem ? (tab_bytes > 96 * 1024 ? 1 : (tab_bytes > 48 * 1024 ? 2 : 8)) : 16;
-    const int64_t cap = (int64_t)sm_count() * per_sm;
-    if (blocks > cap) blocks = cap;
+    const int64_t slots = (int64_t)sm_count() * per_sm;
+    int64_t threads = ceil_div64(ceil_div64(total, slots), 32) * 32;
+    threads = threads < 32 ? 32 : (threads > 512 ? 512 : threads);
+    int64_t blocks = ceil_div64(total, threads);
+    if (blocks > slots) blocks = slots;
 {
         ProfScope _ps(PROF_RANS_DEC, as_stream(stream), (double)n_img * n_sym);
-        rans_decode_kernel<<<(unsigned)blocks, kDecThreads, smem, as_stream(stream)>>>(
+        rans_decode_kernel<<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
         buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, in_smem,
         unshift, out, lane_status);
     }

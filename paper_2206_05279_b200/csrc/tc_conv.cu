@@ -208,9 +208,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
     float *s_bias = reinterpret_cast<float *>(wbar + 2);  // N floats
+    float *s_thr = s_bias + N;                            // head: n_thresh floats
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int c = threadIdx.x; c < N; c += blockDim.x) s_bias[c] = c < (MODE == TC_OUT_HEAD ? 6 : N) ? L.bias[c] : 0.f;
+    if constexpr (MODE == TC_OUT_HEAD) {
+        for (int k = threadIdx.x; k < L.n_thresh; k += blockDim.x) s_thr[k] = __double2float_rd(L.thresh[k]);
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
@@ -399,10 +403,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                         float bv = __fadd_rn(v[3 + c], s_bias[3 + c]);
                         bv = fminf(fmaxf(bv, L.log_s_min), L.log_s_max);
                         float sv = fminf(fmaxf(expf(bv), 0.5f), 64.f);
-                        const int shift = (int)floor((double)mu + 0.5);
-                        const double sd = (double)sv;
+                        // round_half_away(mu), mu >= 0, exact in f32: frac is exact
+                        const float fl = floorf(mu);
+                        const int shift = (int)fl + (__fsub_rn(mu, fl) >= 0.5f ? 1 : 0);
+                        // s > t_k (f64)  <=>  s > rd32(t_k): no float lies in (rd32, t_k]
                         int d = 0;
-                        for (int k = 0; k < L.n_thresh; ++k) d += sd > L.thresh[k];
+                        for (int k = 0; k < L.n_thresh; ++k) d += sv > s_thr[k];
                         L.shift[px * 3 + c] = (uint8_t)shift;
                         L.dsel[px * 3 + c] = (uint8_t)d;
                         if (L.mu) L.mu[px * 3 + c] = mu;
@@ -680,7 +686,8 @@ int launch_tc(const TcLayer &L, cudaStream_t s) {
     constexpr int NG = 4;
     constexpr int KG = KS * KS * NG;
     const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
-    const size_t smem = (size_t)KG * N * 16 + (size_t)kStages * NG * npix * 16 + 8 * (2 * kStages + 6) + 4 * N + 16;
+    const size_t smem = (size_t)KG * N * 16 + (size_t)kStages * NG * npix * 16 + 8 * (2 * kStages + 6) + 4 * N +
+                        4 * (MODE == TC_OUT_HEAD ? 256 : 0) + 16;
     if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     auto kern = tc_conv_kernel<N, KS, MODE>;

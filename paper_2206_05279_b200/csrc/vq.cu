@@ -318,10 +318,10 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
                 bv = fminf(fmaxf(bv, a.log_s_min), a.log_s_max);
                 float sv = expf(bv);
                 sv = fminf(fmaxf(sv, 0.5f), 64.f);
-                const int shift = (int)floor((double)mu + 0.5);
-                const double sd = (double)sv;
-                int d = 0;
-                for (int k = 0; k < a.n_thresh; ++k) d += sd > a.thresh[k];
+                const float fl = floorf(mu);  // round_half_away(mu), exact in f32
+                const int shift = (int)fl + (__fsub_rn(mu, fl) >= 0.5f ? 1 : 0);
+                int d = 0;  // s > t_k  <=>  s > rd32(t_k)
+                for (int k = 0; k < a.n_thresh; ++k) d += sv > __double2float_rd(a.thresh[k]);
                 a.shift[px * 3 + c] = (uint8_t)shift;
                 a.dsel[px * 3 + c] = (uint8_t)d;
                 if (a.mu) a.mu[px * 3 + c] = mu;

@@ -202,7 +202,7 @@ def encode_lanes_device(syms: torch.Tensor, n_img: int, n_sym: int, lanes: int, 
                         dev, stream, shift=None, dsched=None, d_img=None):
     """GPU lanes for a batch: returns (scratch, cap, nbits, states) tensors."""
     cap = lane_cap_words(n_sym, lanes, tables.M)
-    scratch = torch.empty(max(n_img * lanes * cap, 1), dtype=torch.int32, device=dev)
+    scratch = torch.empty(n_img * lanes * cap + 4, dtype=torch.int32, device=dev)  # +16 B read slack
     nbits = torch.empty(max(n_img * lanes, 1), dtype=torch.int32, device=dev)
     states = torch.empty(max(n_img * lanes, 1), dtype=torch.int16, device=dev)
     _lib.call("pilc_rans_encode", ptr(syms), ptr(shift), ptr(dsched), ptr(d_img), n_img, n_sym, lanes,
@@ -260,7 +260,7 @@ def interleaved_decode(lane_set: LaneSet, count: int, d_schedule, tables: Decode
     for l, p in enumerate(payloads):
         offs[l] = pos
         pos += len(p)
-    buf = np.zeros(pos + 8, np.uint8)
+    buf = np.zeros(pos + 16, np.uint8)
     buf[:pos] = np.frombuffer(b"".join(payloads), np.uint8)
     buf_d = torch.from_numpy(buf).to(dev)
     out = torch.zeros(max(count, 1), dtype=torch.uint8, device=dev)
