@@ -18,7 +18,7 @@
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kSmemTableMax = 160 * 1024;
+constexpr int kSmemTableMax = 160 * 1024;  // + 32 KB cp.async ring at 512 threads
 
 __device__ __forceinline__ int lane_count(int64_t n_sym, int lanes, int l) {
     return l < n_sym ? (int)((n_sym - l + lanes - 1) / lanes) : 0;
@@ -112,91 +112,109 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
                 dv = dn;
             }
         }
-        for (; i >= 0; --i) scalar(i);
+        // strided lanes: the next (lower) symbol's inputs are fetched one ahead
+        if (i >= 0) {
+            int64_t pos = base + (int64_t)i * lanes;
+            uint32_t xn = syms[pos], hn = shift ? shift[pos] : 0u, dn = dsched ? dsched[pos] : dconst;
+            for (; i >= 0; --i, pos -= lanes) {
+                const uint32_t xc = xn, hc = hn, dc = dn;
+                if (i > 0) {
+                    xn = syms[pos - lanes];
+                    if (shift) hn = shift[pos - lanes];
+                    if (dsched) dn = dsched[pos - lanes];
+                }
+                enc_step(e, tab, X, M, dc, shift ? ((xc - hc + 128u) & 0xFFu) : xc, out);
+            }
+        }
         if (e.nacc) out[e.words] = (uint32_t)e.acc;
         nbits[k] = e.words * 32u + (uint32_t)e.nacc;
         states[k] = (uint16_t)e.state;
     }
 }
 
-// Aligned 32-bit word holding absolute byte address 4*w; reads outside
-// [lo_w, hi_w] return 0 (never used by a valid stream).
-__device__ __forceinline__ uint32_t load_word(const uint32_t *base_w, int64_t w, int64_t lo_w,
-                                              int64_t hi_w) {
-    return (w >= lo_w && w <= hi_w) ? __ldg(base_w + w) : 0u;
-}
+// Backward bit reader, 32-bit arithmetic relative to the lane's first
+// 16-byte chunk. A 64-bit window over aligned words is refilled one word at a
+// time from the current 16-byte chunk `cur` (registers). Chunks arrive
+// through a per-thread ring of kRing slots in shared memory filled with
+// cp.async three chunks (~30 symbols) ahead: unlike a register prefetch, a
+// pending cp.async never stalls an instruction until cp.async.wait_group
+// asks for that very chunk, so the state chain does not wait on memory.
+// Chunks stay inside [first chunk, last chunk] of the lane; buffers are padded
+// by 16 bytes (pilc.h) so the last chunk is always readable.
+constexpr int kRing = 4;
 
-// Backward bit reader. A 64-bit window over aligned 32-bit words is refilled
-// one word at a time from 16-byte chunks held in registers: `cur` holds the
-// chunk being consumed, `nxt` the one below it, loaded a whole chunk (128
-// bits, ~10 symbols) before it is needed, so the state chain never waits on
-// memory. Chunks never straddle the lane's first or last word by more than
-// 12 bytes; buffers are padded by 16 bytes (pilc.h).
 struct BitReader {
-    const uint4 *base4;
-    int64_t A, start, wlo, cq;
+    const uint4 *base4;  // chunk 0 = the lane's first chunk
+    uint4 *ring;         // this thread's kRing slots (stride = blockDim.x)
+    int stride;
+    int A, start, wl, cq, hi_c;
     uint64_t win;
-    uint4 cur, nxt;
+    uint4 cur;
 
-    __device__ __forceinline__ uint4 chunk(int64_t c, int64_t lo_c, int64_t hi_c) const {
-        return (c >= lo_c && c <= hi_c) ? __ldg(base4 + c) : make_uint4(0, 0, 0, 0);
+    __device__ __forceinline__ void issue(int c) {
+        if (c >= 0 && c <= hi_c) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + (c & (kRing - 1)) * stride);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(base4 + c) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     __device__ __forceinline__ static uint32_t pick(const uint4 &v, int k) {
         return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
     }
-    int64_t lo_c, hi_c;
-
-    __device__ __forceinline__ void init(const uint32_t *words, int64_t start_bit, uint32_t nb) {
-        base4 = reinterpret_cast<const uint4 *>(words);
-        start = start_bit;
-        const int64_t lo_w = start_bit >> 5;
-        const int64_t hi_w = (start_bit + (int64_t)nb - 1) >> 5;
-        lo_c = lo_w >> 2;
-        hi_c = nb ? (hi_w >> 2) : lo_c - 1;
-        A = start_bit + nb;
-        wlo = ((A - 1) >> 5) - 1;  // window = bits [32*wlo, 32*wlo + 64)
-        const int64_t c_top = (wlo + 1) >> 2, c_lo = wlo >> 2;
-        const uint4 a = chunk(c_top, lo_c, hi_c);
-        const uint4 b = c_lo == c_top ? a : chunk(c_lo, lo_c, hi_c);
-        const uint64_t w1 = pick(a, (int)((wlo + 1) & 3));
-        const uint64_t w0 = pick(b, (int)(wlo & 3));
-        win = (w1 << 32) | w0;
-        cq = (wlo - 1) >> 2;  // chunk of the next word to bring in
-        cur = chunk(cq, lo_c, hi_c);
-        nxt = chunk(cq - 1, lo_c, hi_c);
+    __device__ __forceinline__ uint4 direct(int c) const {
+        return (c >= 0 && c <= hi_c) ? __ldg(base4 + c) : make_uint4(0, 0, 0, 0);
     }
-    // returns false on underflow
+    __device__ __forceinline__ void init(const uint4 *lane_base4, uint4 *my_ring, int ring_stride, int start_bit,
+                                         uint32_t nb) {
+        base4 = lane_base4;
+        ring = my_ring;
+        stride = ring_stride;
+        start = start_bit;                               // 0..127
+        hi_c = nb ? (int)((start_bit + nb - 1) >> 7) : -1;
+        A = start_bit + (int)nb;
+        wl = ((A - 1) >> 5) - 1;                         // window = bits [32 wl, 32 wl + 64)
+        const int c_top = (wl + 1) >> 2, c_lo = wl >> 2;
+        const uint4 a = direct(c_top);
+        const uint4 b = c_lo == c_top ? a : direct(c_lo);
+        win = ((uint64_t)pick(a, (wl + 1) & 3) << 32) | pick(b, wl & 3);
+        cq = (wl - 1) >> 2;                              // chunk of the next word to bring in
+        cur = direct(cq);
+        issue(cq - 1);
+        issue(cq - 2);
+        issue(cq - 3);
+    }
+    // false on underflow
     __device__ __forceinline__ bool take(uint32_t b, uint32_t &v) {
-        if (A - start < (int64_t)b) return false;
-        const int64_t lo = A - b;
-        if (lo < wlo * 32) {
-            wlo -= 1;
-            if ((wlo >> 2) != cq) {  // move down one chunk, prefetch the next
-                cur = nxt;
-                cq -= 1;
-                nxt = chunk(cq - 1, lo_c, hi_c);
+        const int lo = A - (int)b;
+        if (lo < start) return false;
+        if (lo < (wl << 5)) {
+            --wl;
+            if ((wl >> 2) != cq) {
+                --cq;
+                asm volatile("cp.async.wait_group 2;" ::: "memory");
+                cur = (cq >= 0 && cq <= hi_c) ? ring[(cq & (kRing - 1)) * stride] : make_uint4(0, 0, 0, 0);
+                issue(cq - 3);
             }
-            win = (win << 32) | pick(cur, (int)(wlo & 3));
+            win = (win << 32) | pick(cur, wl & 3);
         }
-        v = (uint32_t)(win >> (lo - wlo * 32)) & ((1u << b) - 1u);
+        v = (uint32_t)(win >> (lo - (wl << 5))) & ((1u << b) - 1u);
         A = lo;
         return true;
     }
 };
 
+template <bool SMEM>
 __global__ void __launch_bounds__(512) rans_decode_kernel(
     const uint8_t *__restrict__ buf, const uint64_t *__restrict__ lane_off,
     const uint32_t *__restrict__ nbits_a, const uint16_t *__restrict__ states,
     const uint8_t *__restrict__ dsched, const uint16_t *__restrict__ d_img, int64_t n_img,
     int64_t n_sym, int lanes, const uint32_t *__restrict__ dec_tab_g, int D, int M,
-    int tab_in_smem, const uint8_t *__restrict__ unshift, uint8_t *__restrict__ out,
+    const uint8_t *__restrict__ unshift, uint8_t *__restrict__ out,
     uint8_t *__restrict__ lane_status) {
     extern __shared__ __align__(16) uint32_t s_tab[];
     __shared__ __align__(8) uint64_t tbar;
-    const uint32_t *tab = dec_tab_g;
-    if (tab_in_smem) {
-        // one bulk copy of the whole table (up to 160 KB) instead of a
-        // per-thread load/store loop
+    if constexpr (SMEM) {
+        // one bulk copy of the whole table (up to 160 KB)
         const uint32_t bytes = (uint32_t)(D << M) * 4u;
         const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&tbar);
         if (threadIdx.x == 0) {
@@ -215,32 +233,35 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
             "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
             "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(bar)
             : "memory");
-        tab = s_tab;
     }
-    // 16-byte aligned view of the buffer
-    const uintptr_t base_addr = reinterpret_cast<uintptr_t>(buf) & ~(uintptr_t)15;
-    const uint32_t *words = reinterpret_cast<const uint32_t *>(base_addr);
-    const int64_t head = (int64_t)(reinterpret_cast<uintptr_t>(buf) - base_addr);  // 0..15
-    const int64_t total = n_img * lanes;
+    uint4 *ring_base = reinterpret_cast<uint4 *>(s_tab + (SMEM ? (D << M) : 0));
+    uint4 *my_ring = ring_base + threadIdx.x;
     const uint32_t T = 1u << M;
+    auto lookup = [&](uint32_t d, uint32_t st) -> uint32_t {
+        const uint32_t i = d * T + (st - T);
+        if constexpr (SMEM) return s_tab[i];
+        else return __ldg(dec_tab_g + i);
+    };
+    const int64_t total = n_img * lanes;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
         if (lane_status[k]) continue;
-        const int64_t img = k / lanes;
+        const int64_t img = lanes == 1 ? k : k / lanes;
         const int l = (int)(k - img * lanes);
         const int cnt = lane_count(n_sym, lanes, l);
         const int64_t sbase = img * n_sym + l;
         const uint32_t dconst = d_img ? d_img[img] : 0u;
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(buf) + lane_off[k];
         BitReader br;
-        br.init(words, (head + (int64_t)lane_off[k]) * 8, nbits_a[k]);
+        br.init(reinterpret_cast<const uint4 *>(a0 & ~(uintptr_t)15), my_ring, (int)blockDim.x, (int)(a0 & 15) * 8,
+                nbits_a[k]);
         uint32_t state = states[k];
         uint8_t st = 0;
-        // one symbol: returns the decoded (un-recentred) byte; st on underflow
+        // one symbol: the decoded (optionally un-recentred) byte
         auto step = [&](uint32_t d, uint32_t sh) -> uint32_t {
-            const uint32_t e = tab[d * T + (state - T)];
-            const uint32_t b = (e >> 8) & 0xFFu;
+            const uint32_t e = lookup(d, state);
             uint32_t v = 0;
-            if (!br.take(b, v)) st = PILC_ST_UNDERFLOW;
+            if (!br.take((e >> 8) & 0xFFu, v)) st = PILC_ST_UNDERFLOW;
             state = (e >> 16) + v;
             return unshift ? ((e + sh + 128u) & 0xFFu) : (e & 0xFFu);  // (x + shift - 128) mod 256
         };
@@ -251,7 +272,7 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
                 out[pos] = (uint8_t)step(dsched ? dsched[pos] : dconst, unshift ? unshift[pos] : 0u);
             }
             // 16-symbol chunks; the next chunk's d / shift vectors are loaded
-            // one chunk ahead so the state chain never waits on memory
+            // one chunk ahead
             const uint4 z4 = make_uint4(0, 0, 0, 0);
             uint4 dv = z4, hv = z4;
             if (i + 16 <= cnt) {
@@ -274,12 +295,25 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
                 hv = hn;
             }
         }
+        // strided lanes: the next symbol's d / shift are fetched one ahead
+        uint32_t dn = 0, hn = 0;
+        if (i < cnt) {
+            const int64_t pos = sbase + (int64_t)i * lanes;
+            dn = dsched ? dsched[pos] : dconst;
+            hn = unshift ? unshift[pos] : 0u;
+        }
         for (; i < cnt && !st; ++i) {
             const int64_t pos = sbase + (int64_t)i * lanes;
-            out[pos] = (uint8_t)step(dsched ? dsched[pos] : dconst, unshift ? unshift[pos] : 0u);
+            const uint32_t dc = dn, hc = hn;
+            if (i + 1 < cnt) {
+                dn = dsched ? dsched[pos + lanes] : dconst;
+                hn = unshift ? unshift[pos + lanes] : 0u;
+            }
+            out[pos] = (uint8_t)step(dc, hc);
         }
         if (!st && (state != T || br.A != br.start)) st = PILC_ST_END_STATE;
         lane_status[k] = st;
+        asm volatile("cp.async.wait_all;" ::: "memory");  // ring slots are reused by the next lane
     }
 }
 
@@ -315,18 +349,14 @@ extern "C" int pilc_rans_encode(const uint8_t *syms, const uint8_t *shift, const
 }
 
 extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, const uint32_t *nbits,
-                                const uint16_t *states, const uint8_t *dsched,
-                                const uint16_t *d_img, int64_t n_img, int64_t n_sym,
-                                int32_t lanes, const uint32_t *dec_tab, int32_t D, int32_t M,
-                                const uint8_t *unshift, uint8_t *out, uint8_t *lane_status,
+                                const uint16_t *states, const uint8_t *dsched, const uint16_t *d_img,
+                                int64_t n_img, int64_t n_sym, int32_t lanes, const uint32_t *dec_tab, int32_t D,
+                                int32_t M, const uint8_t *unshift, uint8_t *out, uint8_t *lane_status,
                                 void *stream) {
     if (n_img < 0 || n_sym < 0 || lanes < 1 || M < 2 || M > 12 || D < 1) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     const int64_t tab_bytes = ((int64_t)D << M) * 4;
     const int in_smem = tab_bytes <= kSmemTableMax;
-    const size_t smem = in_smem ? (size_t)tab_bytes : 0;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(rans_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t total = n_img * lanes;
     // one table copy per block; per_sm resident blocks fit in shared memory.
     // Spread the lanes over every SM: threads per block = lanes / (SMs x
@@ -337,11 +367,22 @@ extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, co
     threads = threads < 32 ? 32 : (threads > 512 ? 512 : threads);
     int64_t blocks = ceil_div64(total, threads);
     if (blocks > slots) blocks = slots;
-{
+    const size_t smem = (in_smem ? (size_t)tab_bytes : 0) + (size_t)kRing * 16 * (size_t)threads;
+    {
         ProfScope _ps(PROF_RANS_DEC, as_stream(stream), (double)n_img * n_sym);
-        rans_decode_kernel<<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
-        buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, in_smem,
-        unshift, out, lane_status);
+        if (in_smem) {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(rans_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rans_decode_kernel<true><<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
+                buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, unshift, out,
+                lane_status);
+        } else {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(rans_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rans_decode_kernel<false><<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
+                buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, unshift, out,
+                lane_status);
+        }
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;

@@ -470,19 +470,19 @@ constexpr int kStages3 = 3;
 template <int KS, int MODE>
 __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
     constexpr int N = 32;
-    constexpr int NG = 8;  // 4-channel groups
+    constexpr int N2 = 64;  // B' = [B_hi | B_lo] along N
+    constexpr int NG = 8;   // 4-channel groups
     constexpr int KG = KS * KS * NG;
-    constexpr int TMEM_COLS = 2 * N;
+    constexpr int TMEM_COLS = 2 * N2;
     const int Wp = L.Wp;
     const int npix = KS == 3 ? ((128 + 2 * Wp + 2 + 7) & ~7) : 128;
     const uint32_t half_bytes = (uint32_t)NG * npix * 16;  // one of hi / lo
     const uint32_t stage_bytes = 2 * half_bytes;
-    const uint32_t wbytes = (uint32_t)KG * N * 16;
+    const uint32_t wbytes = (uint32_t)KG * N2 * 16;
 
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t *s_whi = smem;
-    uint8_t *s_wlo = smem + wbytes;
-    uint8_t *s_a = smem + 2 * (size_t)wbytes;
+    uint8_t *s_w = smem;
+    uint8_t *s_a = smem + (size_t)wbytes;
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_a + (size_t)kStages3 * stage_bytes);
     uint64_t *full = bars;
     uint64_t *empty = bars + kStages3;
@@ -517,9 +517,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(wbar, 2 * wbytes);
-            bulk_g2s(s_whi, L.w_hi, wbytes, wbar);
-            bulk_g2s(s_wlo, L.w_lo, wbytes, wbar);
+            mbar_expect_tx(wbar, wbytes);
+            bulk_g2s(s_w, L.w_hi, wbytes, wbar);
             int i = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const int s = i % kStages3;
@@ -538,10 +537,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_tf32(128, N);
+            // per K step: D[0:64] += A_hi x [B_hi | B_lo]; D[0:32] += A_lo x B_hi.
+            // The epilogue adds D[0:32] + D[32:64]: A_hi B_hi + A_lo B_hi + A_hi B_lo.
+            constexpr uint32_t idesc64 = idesc_tf32(128, N2);
+            constexpr uint32_t idesc32 = idesc_tf32(128, N);
             mbar_wait(wbar, 0);
             tc_fence_after();
-            const uint32_t whi = smem_u32(s_whi), wlo = smem_u32(s_wlo);
+            const uint32_t wb = smem_u32(s_w);
             int i = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const int s = i % kStages3;
@@ -552,7 +554,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
                 tc_fence_after();
                 const uint32_t ahi = smem_u32(s_a + (size_t)s * stage_bytes);
                 const uint32_t alo = ahi + half_bytes;
-                const uint32_t d = tmem + (uint32_t)(a * N);
+                const uint32_t d = tmem + (uint32_t)(a * N2);
                 uint32_t acc = 0;
 #pragma unroll 1
                 for (int tap = 0; tap < KS * KS; ++tap) {
@@ -561,14 +563,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
 #pragma unroll
                     for (int ks = 0; ks < NG / 2; ++ks) {
                         const uint32_t ao = (uint32_t)(2 * ks) * npix * 16u + off;
-                        const uint32_t bo = (uint32_t)(tap * NG + 2 * ks) * N * 16u;
+                        const uint32_t bo = (uint32_t)(tap * NG + 2 * ks) * N2 * 16u;
                         const uint64_t dah = umma_desc(ahi + ao, (uint32_t)npix * 16u, 128u);
                         const uint64_t dal = umma_desc(alo + ao, (uint32_t)npix * 16u, 128u);
-                        const uint64_t dbh = umma_desc(whi + bo, (uint32_t)N * 16u, 128u);
-                        const uint64_t dbl = umma_desc(wlo + bo, (uint32_t)N * 16u, 128u);
-                        mma_tf32(d, dal, dbh, idesc, acc);
-                        mma_tf32(d, dah, dbl, idesc, 1u);
-                        mma_tf32(d, dah, dbh, idesc, 1u);
+                        const uint64_t db = umma_desc(wb + bo, (uint32_t)N2 * 16u, 128u);
+                        mma_tf32(d, dah, db, idesc64, acc);
+                        mma_tf32(d, dal, db, idesc32, 1u);
                         acc = 1u;
                     }
                 }
@@ -607,9 +607,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
             }
             mbar_wait(&tfull[a], u & 1);
             tc_fence_after();
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * N);
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * N2);
             float v[32];
-            tmem_ld32(taddr, v);
+            {
+                float w[32];
+                tmem_ld32(taddr, v);
+                tmem_ld32(taddr + 32, w);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) v[c] = __fadd_rn(v[c], w[c]);
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[a]);
@@ -664,7 +670,7 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
     constexpr int NG = 8;
     constexpr int KG = KS * KS * NG;
     const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
-    const size_t smem = 2 * (size_t)KG * 32 * 16 + (size_t)kStages3 * 2 * NG * npix * 16 + 8 * (2 * kStages3 + 5) + 16;
+    const size_t smem = (size_t)KG * 64 * 16 + (size_t)kStages3 * 2 * NG * npix * 16 + 8 * (2 * kStages3 + 5) + 16;
     if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     auto kern = tc3_conv_kernel<KS, MODE>;

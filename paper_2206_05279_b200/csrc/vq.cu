@@ -194,36 +194,51 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
     const int ntap = ks * ks;
     for (int c0 = 0; c0 < a.Ci_pad; c0 += kCK) {
         // stage the input patch, channel-planar in smem; element order is
-        // channel-fastest so a warp reads 4 pixels x 8 contiguous channels
+        // channel-fastest so a warp reads 4 pixels x 8 contiguous channels.
+        // Four elements per thread per round: all loads first, then the
+        // shared stores, so four global loads are in flight per thread.
         const int patch = IR * IR;
         const int ci = t & 7;
-        int py = (t >> 3) / IR, px = (t >> 3) - ((t >> 3) / IR) * IR;
-        for (int e = t; e < kCK * patch; e += kThreads, px += kThreads / 8) {
-            while (px >= IR) {
-                px -= IR;
-                ++py;
+        const int c = c0 + ci;
+        const uint32_t m_ir = 0xFFFFFFFFu / (uint32_t)IR + 1u;  // ceil(2^32 / IR)
+        for (int base = t; base < kCK * patch; base += 4 * kThreads) {
+            float v[4];
+            int sidx[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = base + u * kThreads;
+                v[u] = 0.f;
+                sidx[u] = -1;
+                if (e < kCK * patch) {
+                    const uint32_t pix = (uint32_t)e >> 3;
+                    const int py = (int)__umulhi(pix, m_ir), px = (int)pix - py * IR;  // pix / IR, exact for pix < 2^16
+                    sidx[u] = (ci * IR + py) * IC + px;
+                    if (a.in_mode == IN_F32) {
+                        if (c < a.Ci) {
+                            const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
+                            v[u] = __ldg(a.in + (((int64_t)n * a.Hi + y) * a.Wi + x) * a.Ci + c);
+                        }
+                    } else if (a.in_mode == IN_U8) {
+                        if (c < 3) {
+                            const int y = clampi(iy0 + py, 0, a.src_h - 1), x = clampi(ix0 + px, 0, a.src_w - 1);
+                            v[u] = (float)__ldg(a.in_u8 + (((int64_t)n * a.src_h + y) * a.src_w + x) * 3 + c);
+                        }
+                    } else {
+                        if (c < a.Ci) {
+                            const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
+                            const int k = a.in_u8[((int64_t)n * a.Hi + y) * a.Wi + x];
+                            v[u] = a.codebook[(int64_t)k * a.Ci + c];
+                        }
+                    }
+                }
             }
-            const int c = c0 + ci;
-            float v = 0.f;
-            if (a.in_mode == IN_F32) {
-                if (c < a.Ci) {
-                    const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
-                    v = a.in[(((int64_t)n * a.Hi + y) * a.Wi + x) * a.Ci + c];
-                }
-            } else if (a.in_mode == IN_U8) {
-                if (c < 3) {
-                    const int y = clampi(iy0 + py, 0, a.src_h - 1), x = clampi(ix0 + px, 0, a.src_w - 1);
-                    const float raw = a.in_u8[(((int64_t)n * a.src_h + y) * a.src_w + x) * 3 + c];
-                    v = __fsub_rn(__fdiv_rn(raw, 127.5f), 1.f);  // vqvae.py:41-43
-                }
-            } else {
-                if (c < a.Ci) {
-                    const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
-                    const int k = a.in_u8[((int64_t)n * a.Hi + y) * a.Wi + x];
-                    v = a.codebook[(int64_t)k * a.Ci + c];
-                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (sidx[u] < 0) continue;
+                float x = v[u];
+                if (a.in_mode == IN_U8 && c < 3) x = __fsub_rn(__fdiv_rn(x, 127.5f), 1.f);  // vqvae.py:41-43
+                s_in[sidx[u]] = x;
             }
-            s_in[(ci * IR + py) * IC + px] = v;
         }
         // stage weights [tap][ci][co0 .. co0+CO_T)
         for (int e = t; e < ntap * kCK * CO_T; e += kThreads) {
@@ -674,18 +689,17 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
             memcpy(&r, &u, 4);
             return r;
         };
+        // B' layout [K/4][64][4]: rows 0..31 = tf32 hi, rows 32..63 = lo
         auto put_t = [&](int64_t off, const ConvSpec &sp) {
             const int taps = sp.ks * sp.ks;
-            const int64_t half = (int64_t)taps * 8 * 32 * 4;
             for (int n = 0; n < 32; ++n)
                 for (int ci = 0; ci < 32; ++ci)
                     for (int tap = 0; tap < taps; ++tap) {
                         const int k = tap * 32 + ci;
                         const float w = dst[sp.w_off + ((int64_t)tap * sp.ci_pad + ci) * sp.co_pad + n];
                         const float hi = tf32(w);
-                        const int64_t e = ((int64_t)(k >> 2) * 32 + n) * 4 + (k & 3);
-                        dst[off + e] = hi;
-                        dst[off + half + e] = w - hi;
+                        dst[off + ((int64_t)(k >> 2) * 64 + n) * 4 + (k & 3)] = hi;
+                        dst[off + ((int64_t)(k >> 2) * 64 + 32 + n) * 4 + (k & 3)] = w - hi;
                     }
         };
         for (int i = 0; i < 2 * B; ++i) put_t(L.tf_blk[i], L.enc[2 + i]);
