@@ -11,7 +11,7 @@ const char *kCatNames[PROF_NCAT] = {"conv_kernel",        "argmin_kernel",  "ran
                                     "static_scale_kernel", "blob_sizes+scan", "pack_kernel",
                                     "parse_kernel",       "lanes_kernel",   "crc_kernel",
                                     "sched_crc_kernel",   "tc_conv_kernel", "gather_kernel",
-                                    "tc3_conv_kernel"};
+                                    "tc3_conv_kernel", "enc_front_kernel"};
 struct Rec {
     int cat;
     cudaEvent_t e0, e1;

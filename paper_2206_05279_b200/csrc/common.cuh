@@ -35,6 +35,7 @@ enum ProfCat {
     PROF_TC_CONV,
     PROF_GATHER,
     PROF_TC3_CONV,
+    PROF_ENC_FRONT,
     PROF_NCAT
 };
 void *prof_begin(int cat, cudaStream_t s, double units);

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "tc_conv.cuh"
+#include "enc_front.cuh"
 
 namespace {
 
@@ -788,30 +789,27 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
               int32_t B, const Layout &L, const TfWork &w, uint8_t *idx_out, float *z_out, cudaStream_t s) {
     const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
     int rc;
-    ConvArgs a = base_args(model, L.enc[0]);  // stem, SIMT fp32
-    a.in_mode = IN_U8;
-    a.in_u8 = img;
-    a.src_h = H;
-    a.src_w = W;
-    a.Hi = a.Ho = He;
-    a.Wi = a.Wo = We;
-    a.relu = 1;
-    a.out = w.A;
-    if ((rc = launch_conv(a, L.enc[0].co_t, n_img, s))) return rc;
-    a = base_args(model, L.enc[1]);  // down (stride 2), SIMT fp32 -> hi/lo slabs
-    a.in = w.A;
-    a.Hi = He;
-    a.Wi = We;
-    a.stride = 2;
-    a.Ho = gh;
-    a.Wo = gw;
-    a.relu = 1;
-    a.out_mode = OUT_TFSPLIT;
-    a.out_hi = w.Xh;
-    a.out_lo = w.Xl;
-    a.out_gstride = w.gs;
-    a.out_margin = w.margin;
-    if ((rc = launch_conv(a, L.enc[1].co_t, n_img, s))) return rc;
+    // stem + down fused (enc_front.cu) -> hi / lo slabs of the latent grid
+    EncFront f;
+    f.img = img;
+    f.n_img = n_img;
+    f.H = H;
+    f.W = W;
+    f.gh = gh;
+    f.gw = gw;
+    f.w_stem = model + L.enc[0].w_off;
+    f.b_stem = model + L.enc[0].b_off;
+    f.stem_ci_pad = L.enc[0].ci_pad;
+    f.stem_co_pad = L.enc[0].co_pad;
+    f.w_down = model + L.enc[1].w_off;
+    f.b_down = model + L.enc[1].b_off;
+    f.down_ci_pad = L.enc[1].ci_pad;
+    f.down_co_pad = L.enc[1].co_pad;
+    f.out_hi = w.Xh;
+    f.out_lo = w.Xl;
+    f.gstride = w.gs;
+    f.margin = w.margin;
+    if ((rc = enc_front_launch(f, s))) return rc;
     Tc3Layer b;
     memset(&b, 0, sizeof(b));
     b.gstride = w.gs;

@@ -45,20 +45,52 @@ def sptr(stream: torch.cuda.Stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+_PINNED: "weakref.WeakValueDictionary" = None
+
+
 def pinned(nbytes: int) -> torch.Tensor:
-    return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    """Page-locked host buffer (torch's caching host allocator). Buffers the
+    batch API returns (blob buffers, decoded images) live here, so feeding
+    them back (decompress_batch(compress_batch(...))) DMAs with no staging."""
+    global _PINNED
+    import weakref
+
+    if _PINNED is None:
+        _PINNED = weakref.WeakValueDictionary()
+    t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    _PINNED[t.data_ptr()] = t
+    return t
+
+
+def _pinned_owner(arr: np.ndarray):
+    if _PINNED is None:
+        return None
+    p = arr.ctypes.data
+    for base, t in list(_PINNED.items()):
+        if base <= p and p + arr.nbytes <= base + t.numel():
+            return t
+    return None
 
 
 def h2d(arr: np.ndarray, dev: torch.device, stream: torch.cuda.Stream, pad: int = 0) -> torch.Tensor:
-    """Host numpy -> device tensor through a pinned staging copy."""
+    """Host numpy -> device tensor. Page-locked sources (buffers this package
+    returned) DMA directly; pageable ones go through a pinned staging copy."""
     a = np.ascontiguousarray(arr)
     flat = a.view(np.uint8).reshape(-1)
+    out = torch.empty(flat.size + pad, dtype=torch.uint8, device=dev)
+    owner = _pinned_owner(flat) if flat.size else None
+    with torch.cuda.stream(stream):
+        if owner is not None:
+            out[: flat.size].copy_(torch.from_numpy(flat), non_blocking=True)
+            if pad:
+                out[flat.size:].zero_()
+            out._pilc_host = owner  # type: ignore[attr-defined]
+            return out
     host = pinned(flat.size + pad)
     hv = host.numpy()
     hv[: flat.size] = flat
     if pad:
         hv[flat.size:] = 0
-    out = torch.empty(flat.size + pad, dtype=torch.uint8, device=dev)
     with torch.cuda.stream(stream):
         out.copy_(host, non_blocking=True)
     # keep the staging buffer alive until the copy has run
