@@ -29,6 +29,7 @@ constexpr int SCP = SC + 1;              // pitch
 constexpr int IR = SR + 2, IC = SC + 2;  // image patch 19 x 35
 constexpr int kThreads = 256;
 constexpr int C = 32;
+constexpr int kImgF = (3 * IR * IC + 3) & ~3;  // image patch floats, rounded for float4 alignment
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -50,7 +51,7 @@ __device__ __forceinline__ void store4(float *slab, int64_t q, float4 v, int y, 
 __global__ void __launch_bounds__(kThreads) enc_front_kernel(EncFront a) {
     extern __shared__ __align__(16) float sm[];
     float *s_img = sm;                      // [3][IR][IC]
-    float *s_ws = s_img + 3 * IR * IC;      // stem weights [27][32] (k = c*9 + i*3 + j)
+    float *s_ws = s_img + kImgF;            // stem weights [27][32] (k = c*9 + i*3 + j), 16-B aligned
     float *s_bs = s_ws + 27 * C;            // [32]
     float *s_wd = s_bs + C;                 // down weights [9][32 ci][32 co]
     float *s_bd = s_wd + 9 * C * C;         // [32]
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kThreads) enc_front_kernel(EncFront a) {
 }  // namespace
 
 size_t enc_front_smem() {
-    return sizeof(float) * (3 * IR * IC + 27 * C + C + 9 * C * C + C + C * SR * SCP);
+    return sizeof(float) * (kImgF + 27 * C + C + 9 * C * C + C + C * SR * SCP);
 }
 
 int enc_front_launch(const EncFront &a, cudaStream_t s) {
