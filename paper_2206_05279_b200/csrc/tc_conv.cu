@@ -648,12 +648,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
                     store_px4(L.out_lo + so, q, make_float4(lo[0], lo[1], lo[2], lo[3]), y, x, H, W, Wp);
                 }
             } else {
-                float4 *zo = reinterpret_cast<float4 *>(L.z + (((int64_t)n * H + (y - 1)) * (int64_t)W + (x - 1)) * 32);
+                // z = acc + bias, written as tf32 hi / fp32 lo into 128-latent
+                // tiles in the UMMA K-major layout the argmin GEMM reads
+                const int64_t vix = ((int64_t)n * H + (y - 1)) * (int64_t)W + (x - 1);
+                float4 *zo = L.z ? reinterpret_cast<float4 *>(L.z + vix * 32) : nullptr;
+                float4 *zt = reinterpret_cast<float4 *>(L.zt) + (vix >> 7) * (2 * NG * 128) + (vix & 127);
 #pragma unroll
-                for (int g = 0; g < NG; ++g)
-                    zo[g] = make_float4(__fadd_rn(v[4 * g], bias[4 * g]), __fadd_rn(v[4 * g + 1], bias[4 * g + 1]),
-                                        __fadd_rn(v[4 * g + 2], bias[4 * g + 2]),
-                                        __fadd_rn(v[4 * g + 3], bias[4 * g + 3]));
+                for (int g = 0; g < NG; ++g) {
+                    float zz[4], hi[4], lo[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        zz[e] = __fadd_rn(v[4 * g + e], bias[4 * g + e]);
+                        hi[e] = tf32_rna(zz[e]);
+                        lo[e] = __fsub_rn(zz[e], hi[e]);
+                    }
+                    if (zo) zo[g] = make_float4(zz[0], zz[1], zz[2], zz[3]);
+                    zt[g * 128] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                    zt[(NG + g) * 128] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                }
             }
         }
     }
@@ -685,6 +697,245 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
     kern<<<(unsigned)grid, kThreadsTC, smem, s>>>(L);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
+}
+
+// ---- codebook argmin on tcgen05 (vqvae.py:66-76) ---------------------------
+// Per 128-latent tile: dot[r][k] = z_r . c_k for all 256 codes as a 3xTF32
+// GEMM (z_hi c_hi + z_hi c_lo + z_lo c_hi, fp32 TMEM accumulators, M=128,
+// N=256, K=32). The epilogue forms d'_k = |c_k|^2 - 2 dot_k (+|z|^2) and an
+// error radius E_k = g (|z|^2 + |c_k|^2) with g = 1e-4, ten times the
+// worst case of the split products, tf32 truncation of the lo parts and
+// fp32 accumulation of 96 terms (~1e-5). The reference's argmin (float64,
+// component order, first minimum) must satisfy d'_k - E_k <= min_j (d'_j +
+// E_j); if exactly one code passes it is the answer, otherwise the
+// survivors are re-scored exactly as the reference does (float64, same
+// order, no FMA) and the smallest wins, ties to the lowest index.
+// Warps: 0 producer (bulk copies of the z tile), 1 TMEM + MMA, 2..9
+// epilogue (two warps per TMEM lane quarter, 128 codes each).
+constexpr int kAmThreads = 320;
+constexpr int kAmStages = 3;
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
+    constexpr int NC = 256;           // codes (N)
+    constexpr uint32_t ZB = 2 * 8 * 128 * 16;  // z tile bytes (hi + lo)
+    constexpr uint32_t CB = 2 * 8 * NC * 16;   // codebook operand bytes
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_cb = smem;                                  // [hi|lo][8][256][16 B]
+    uint8_t *s_z = smem + CB;                              // kAmStages x ZB
+    float *s_cn = reinterpret_cast<float *>(s_z + kAmStages * ZB);  // |c_k|^2
+    float *s_m = s_cn + NC;                                // [2][128] exchange
+    int *s_i = reinterpret_cast<int *>(s_m + 256);         // [2][128] counts / codes, [2][128] first
+    double *s_d = reinterpret_cast<double *>(s_i + 512);   // [2][128]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_d + 256);
+    uint64_t *full = bars, *empty = bars + kAmStages, *tfull = bars + 2 * kAmStages, *tempty = tfull + 2;
+    uint64_t *wbar = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kAmStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 8);
+        }
+        mbar_init(wbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(wbar, CB);
+        bulk_g2s(s_cb, a.cbt, CB, wbar);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    // |c_k|^2 from hi + lo (exact fp32 codebook), after the codebook landed
+    mbar_wait(wbar, 0);
+    for (int k = threadIdx.x; k < NC; k += blockDim.x) {
+        const float *hi = reinterpret_cast<const float *>(s_cb);
+        const float *lo = hi + 8 * NC * 4;
+        float acc = 0.f;
+        for (int c = 0; c < 32; ++c) {
+            const int e = ((c >> 2) * NC + k) * 4 + (c & 3);
+            const float v = __fadd_rn(hi[e], lo[e]);
+            acc = fmaf(v, v, acc);
+        }
+        s_cn[k] = acc;
+    }
+    __syncthreads();
+
+    const int64_t n_tiles = a.n_tiles;
+    if (warp == 0) {
+        if (lane == 0) {
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int s = i % kAmStages, r = i / kAmStages;
+                if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+                mbar_expect_tx(&full[s], ZB);
+                bulk_g2s(s_z + (size_t)s * ZB, a.zt + t * (ZB / 4), ZB, &full[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, NC);
+            tc_fence_after();
+            const uint32_t bhi = smem_u32(s_cb), blo = bhi + CB / 2;
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int s = i % kAmStages, b = i & 1, u = i >> 1;
+                if (u > 0) mbar_wait(&tempty[b], (u - 1) & 1);
+                mbar_wait(&full[s], (i / kAmStages) & 1);
+                tc_fence_after();
+                const uint32_t ahi = smem_u32(s_z + (size_t)s * ZB), alo = ahi + ZB / 2;
+                const uint32_t d = tmem + (uint32_t)(b * NC);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const uint32_t ao = (uint32_t)(2 * ks) * 128 * 16, bo = (uint32_t)(2 * ks) * NC * 16;
+                    const uint64_t dah = umma_desc(ahi + ao, 128 * 16, 128), dal = umma_desc(alo + ao, 128 * 16, 128);
+                    const uint64_t dbh = umma_desc(bhi + bo, NC * 16, 128), dbl = umma_desc(blo + bo, NC * 16, 128);
+                    mma_tf32(d, dah, dbh, idesc, ks ? 1u : 0u);
+                    mma_tf32(d, dah, dbl, idesc, 1u);
+                    mma_tf32(d, dal, dbh, idesc, 1u);
+                }
+                mma_commit(&empty[s]);
+                mma_commit(&tfull[b]);
+            }
+        }
+    } else {
+        const int ew = warp - 2;              // 0..7
+        const int quarter = warp & 3;         // TMEM lane quarter (hardware rule: warp % 4)
+        const int half = ew >> 2;             // codes 128*half .. +127
+        const int row = quarter * 32 + lane;
+        const float g = 1e-4f;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int b = i & 1, u = i >> 1;
+            const int64_t v = t * 128 + row;
+            const bool live = v < a.n_vec;
+            // |z|^2 from the tile in global memory (L2): z = hi + lo exactly
+            float zv[32];
+            float zn = 0.f;
+            {
+                const float4 *zt = reinterpret_cast<const float4 *>(a.zt) + t * (2 * 8 * 128) + row;
+#pragma unroll
+                for (int gq = 0; gq < 8; ++gq) {
+                    const float4 h = live ? zt[gq * 128] : make_float4(0, 0, 0, 0);
+                    const float4 l = live ? zt[(8 + gq) * 128] : make_float4(0, 0, 0, 0);
+                    zv[4 * gq + 0] = __fadd_rn(h.x, l.x);
+                    zv[4 * gq + 1] = __fadd_rn(h.y, l.y);
+                    zv[4 * gq + 2] = __fadd_rn(h.z, l.z);
+                    zv[4 * gq + 3] = __fadd_rn(h.w, l.w);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; ++c) zn = fmaf(zv[c], zv[c], zn);
+            }
+            mbar_wait(&tfull[b], u & 1);
+            tc_fence_after();
+            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * NC + half * 128);
+            const float gzn = g * zn;
+            // pass 1: smallest upper end  d'_k + E_k
+            float m = INFINITY;
+#pragma unroll 1
+            for (int ch = 0; ch < 4; ++ch) {
+                float dv[32];
+                tmem_ld32(tbase + 32 * ch, dv);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int k = half * 128 + 32 * ch + j;
+                    const float cn = s_cn[k];
+                    const float dp = fmaf(-2.f, dv[j], cn);
+                    if (k < a.K) m = fminf(m, dp + fmaf(g, cn, gzn));
+                }
+            }
+            s_m[half * 128 + row] = m;
+            named_bar(1, 256);
+            m = fminf(s_m[row], s_m[128 + row]);
+            // pass 2: survivors  d'_k - E_k <= m
+            int cnt = 0, first = 0x7FFFFFFF;
+#pragma unroll 1
+            for (int ch = 0; ch < 4; ++ch) {
+                float dv[32];
+                tmem_ld32(tbase + 32 * ch, dv);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int k = half * 128 + 32 * ch + j;
+                    const float cn = s_cn[k];
+                    const float dp = fmaf(-2.f, dv[j], cn);
+                    if (k < a.K && dp - fmaf(g, cn, gzn) <= m) {
+                        ++cnt;
+                        first = min(first, k);
+                    }
+                }
+            }
+            s_i[half * 128 + row] = cnt;
+            s_i[256 + half * 128 + row] = first;
+            named_bar(1, 256);
+            const int tot = s_i[row] + s_i[128 + row];
+            const int kfirst = min(s_i[256 + row], s_i[256 + 128 + row]);
+            named_bar(1, 256);
+            // pass 3 (rare): exact float64 re-score of the survivors
+            double best = INFINITY;
+            int bk = 0x7FFFFFFF;
+            if (__any_sync(0xffffffffu, tot > 1)) {
+#pragma unroll 1
+                for (int ch = 0; ch < 4; ++ch) {
+                    float dv[32];
+                    tmem_ld32(tbase + 32 * ch, dv);
+                    if (tot <= 1) continue;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int k = half * 128 + 32 * ch + j;
+                        const float cn = s_cn[k];
+                        const float dp = fmaf(-2.f, dv[j], cn);
+                        if (!(k < a.K && dp - fmaf(g, cn, gzn) <= m)) continue;
+                        const float *hi = reinterpret_cast<const float *>(s_cb);
+                        const float *lo = hi + 8 * NC * 4;
+                        double dist = 0.0;
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            const int e = ((c >> 2) * NC + k) * 4 + (c & 3);
+                            const double diff = __dsub_rn((double)zv[c], (double)__fadd_rn(hi[e], lo[e]));
+                            dist = __dadd_rn(dist, __dmul_rn(diff, diff));
+                        }
+                        if (dist < best) {
+                            best = dist;
+                            bk = k;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[b]);
+            s_d[half * 128 + row] = best;
+            s_i[half * 128 + row] = bk;
+            named_bar(1, 256);
+            if (half == 0 && live) {
+                int out = kfirst;
+                if (tot > 1) {
+                    const double b0 = s_d[row], b1 = s_d[128 + row];
+                    const int k0 = s_i[row], k1 = s_i[128 + row];
+                    out = (b1 < b0) ? k1 : k0;  // equal distances: the lower half holds the lower k
+                }
+                a.idx[v] = (uint8_t)out;
+            }
+            named_bar(1, 256);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
 }
 
 template <int N, int KS, int MODE>
@@ -747,6 +998,20 @@ __global__ void gather_kernel(const uint8_t *__restrict__ idx, const uint16_t *_
 }  // namespace
 
 int tc_launch_act(const TcLayer &L, cudaStream_t s) { return launch_tc<32, 3, TC_OUT_ACT>(L, s); }
+int argmin_tc_launch(const ArgminTc &a, cudaStream_t s) {
+    if (a.n_tiles <= 0) return PILC_OK;
+    if (a.K < 1 || a.K > 256) return PILC_E_ARG;
+    const size_t smem = 2 * 8 * 256 * 16 + (size_t)kAmStages * 2 * 8 * 128 * 16 + 4 * 256 + 4 * 256 + 4 * 512 +
+                        8 * 256 + 8 * (2 * kAmStages + 5) + 16;
+    cudaFuncSetAttribute(argmin_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t grid = sm_count();
+    if (grid > a.n_tiles) grid = a.n_tiles;
+    ProfScope _ps(PROF_ARGMIN, s, 3.0 * a.n_vec * a.K * 32);
+    argmin_tc_kernel<<<(unsigned)grid, kAmThreads, smem, s>>>(a);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
 int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s) {
     if (ks == 3 && mode == TC3_ACT) return launch_tc3<3, TC3_ACT>(L, s);
     if (ks == 1 && mode == TC3_Z) return launch_tc3<1, TC3_Z>(L, s);

@@ -40,9 +40,20 @@ struct Tc3Layer {
     const float *bias;
     const float *res_hi, *res_lo;  // TC3_ACT residual (nullable)
     float *out_hi, *out_lo;        // TC3_ACT
-    float *z;                      // TC3_Z: (n, H, W, 32) fp32
+    float *z;                      // TC3_Z: (n, H, W, 32) fp32 (nullable)
+    float *zt;                     // TC3_Z: 128-latent tiles [tile][hi|lo][8][128][4]
     int relu;
 };
+
+// Codebook argmin on tcgen05 (3xTF32 distance GEMM + exact float64 rescore).
+struct ArgminTc {
+    const float *zt;       // z tiles from the projection epilogue
+    int64_t n_vec, n_tiles;
+    const float *cbt;      // codebook B operand: [hi|lo][8][256][4]
+    int K;
+    uint8_t *idx;
+};
+int argmin_tc_launch(const ArgminTc &a, cudaStream_t s);
 
 int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s);
 

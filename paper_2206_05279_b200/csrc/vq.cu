@@ -51,6 +51,7 @@ struct Layout {
     bool tf;
     std::vector<int64_t> tf_blk;
     int64_t tf_proj;
+    int64_t tf_cb;  // argmin GEMM B operand [hi|lo][8][256][4] fp32 (codes >= K zero)
     int64_t total;                // floats, bf16 region included
 };
 
@@ -109,6 +110,8 @@ Layout make_layout(int K, int Dc, int C, int B) {
         }
         L.tf_proj = cur;
         cur += 2 * 8 * 32 * 4;
+        L.tf_cb = cur;
+        cur += 2 * 8 * 256 * 4;
     }
     L.total = cur;
     return L;
@@ -600,7 +603,7 @@ int64_t tc_ws(int64_t n, int H, int W, TcWork *w, char *base) {
 // 3xTF32 encoder scratch: full-res stem output (NHWC fp32), three latent
 // tensors as hi/lo slab pairs (8 groups x gstride x 16 B each), z.
 struct TfWork {
-    float *A, *Xh, *Xl, *Th, *Tl, *Yh, *Yl, *Z;
+    float *A, *Xh, *Xl, *Th, *Tl, *Yh, *Yl, *Z, *ZT;
     int64_t gs, margin;
 };
 
@@ -610,16 +613,18 @@ int64_t tf_ws(int64_t n, int H, int W, TfWork *w, char *base) {
     const int64_t m1 = 256 + 2 * Wp;
     const int64_t gs = 2 * m1 + n * (gh + 2) * Wp;
     auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
-    const int64_t a = al(n * He * We * 32 * 4), slab = al(8 * gs * 16), z = al(n * gh * gw * 32 * 4);
+    const int64_t a = 256, slab = al(8 * gs * 16), z = al(n * gh * gw * 32 * 4);
+    const int64_t zt = al(((n * gh * gw + 127) / 128) * 128 * 32 * 4 * 2);
     if (w) {
         w->A = reinterpret_cast<float *>(base);
         float **sl[6] = {&w->Xh, &w->Xl, &w->Th, &w->Tl, &w->Yh, &w->Yl};
         for (int i = 0; i < 6; ++i) *sl[i] = reinterpret_cast<float *>(base + a + i * slab);
         w->Z = reinterpret_cast<float *>(base + a + 6 * slab);
+        w->ZT = reinterpret_cast<float *>(base + a + 6 * slab + z);
         w->gs = gs;
         w->margin = m1;
     }
-    return a + 6 * slab + z;
+    return a + 6 * slab + z + zt;
 }
 
 bool check_cfg(int K, int Dc, int C, int B) {
@@ -705,6 +710,13 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
         };
         for (int i = 0; i < 2 * B; ++i) put_t(L.tf_blk[i], L.enc[2 + i]);
         put_t(L.tf_proj, L.enc[2 + 2 * B]);
+        for (int k = 0; k < K; ++k)
+            for (int c = 0; c < 32; ++c) {
+                const float w = dst[L.cb_off + (int64_t)k * 32 + c];
+                const float hi = tf32(w);
+                dst[L.tf_cb + ((int64_t)(c >> 2) * 256 + k) * 4 + (c & 3)] = hi;
+                dst[L.tf_cb + 8 * 256 * 4 + ((int64_t)(c >> 2) * 256 + k) * 4 + (c & 3)] = w - hi;
+            }
     }
     return PILC_OK;
 }
@@ -850,17 +862,24 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
         Yh = th;
         Yl = tl;
     }
-    float *z = z_out ? z_out : w.Z;
-    Tc3Layer pj = b;  // proj 1x1 -> z (fp32, NHWC interior)
+    Tc3Layer pj = b;  // proj 1x1 -> z tiles (+ plain z when asked)
     pj.in_hi = Xh;
     pj.in_lo = Xl;
     pj.w_hi = model + L.tf_proj;
     pj.w_lo = pj.w_hi + half1;
     pj.bias = model + L.enc[2 + 2 * B].b_off;
     pj.relu = 0;
-    pj.z = z;
+    pj.z = z_out;
+    pj.zt = w.ZT;
     if ((rc = tc3_launch(pj, 1, TC3_Z, s))) return rc;
-    return launch_argmin(z, n_img * gh * gw, model + L.cb_off, K, Dc, idx_out, s);
+    ArgminTc am;
+    am.zt = w.ZT;
+    am.n_vec = n_img * gh * gw;
+    am.n_tiles = ceil_div64(am.n_vec, 128);
+    am.cbt = model + L.tf_cb;
+    am.K = K;
+    am.idx = idx_out;
+    return argmin_tc_launch(am, s);
 }
 
 int vq_encode(int path, const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,
