@@ -712,26 +712,29 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
 // order, no FMA) and the smallest wins, ties to the lowest index.
 // Warps: 0 producer (bulk copies of the z tile), 1 TMEM + MMA, 2..9
 // epilogue (two warps per TMEM lane quarter, 128 codes each).
-constexpr int kAmThreads = 320;
+constexpr int kAmThreads = 576;  // 2 + 16 warps
 constexpr int kAmStages = 3;
+constexpr int kAmParts = 4;      // epilogue warps per TMEM lane quarter (64 codes each)
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
     constexpr int NC = 256;           // codes (N)
+    constexpr int NE = 32 * 4 * kAmParts;      // epilogue threads (512)
     constexpr uint32_t ZB = 2 * 8 * 128 * 16;  // z tile bytes (hi + lo)
     constexpr uint32_t CB = 2 * 8 * NC * 16;   // codebook operand bytes
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *s_cb = smem;                                  // [hi|lo][8][256][16 B]
     uint8_t *s_z = smem + CB;                              // kAmStages x ZB
-    float *s_cn = reinterpret_cast<float *>(s_z + kAmStages * ZB);  // |c_k|^2
-    float *s_m = s_cn + NC;                                // [2][128] exchange
-    int *s_i = reinterpret_cast<int *>(s_m + 256);         // [2][128] counts / codes, [2][128] first
-    double *s_d = reinterpret_cast<double *>(s_i + 512);   // [2][128]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_d + 256);
+    float2 *s_cn = reinterpret_cast<float2 *>(s_z + kAmStages * ZB);  // (|c_k|^2, g |c_k|^2)
+    float4 *s_x = reinterpret_cast<float4 *>(s_cn + NC);   // [parts][128] (m, lo1, lo2, k1)
+    double *s_d = reinterpret_cast<double *>(s_x + kAmParts * 128);  // [parts][128]
+    int *s_k = reinterpret_cast<int *>(s_d + kAmParts * 128);        // [parts][128]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_k + kAmParts * 128);
     uint64_t *full = bars, *empty = bars + kAmStages, *tfull = bars + 2 * kAmStages, *tempty = tfull + 2;
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
+    const float g = 1e-4f;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -741,7 +744,7 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 8);
+            mbar_init(&tempty[b], 4 * kAmParts);
         }
         mbar_init(wbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -757,7 +760,6 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    // |c_k|^2 from hi + lo (exact fp32 codebook), after the codebook landed
     mbar_wait(wbar, 0);
     for (int k = threadIdx.x; k < NC; k += blockDim.x) {
         const float *hi = reinterpret_cast<const float *>(s_cb);
@@ -768,7 +770,8 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
             const float v = __fadd_rn(hi[e], lo[e]);
             acc = fmaf(v, v, acc);
         }
-        s_cn[k] = acc;
+        // codes >= K can never win: +inf distance
+        s_cn[k] = k < a.K ? make_float2(acc, g * acc) : make_float2(INFINITY, 0.f);
     }
     __syncthreads();
 
@@ -810,99 +813,107 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
             }
         }
     } else {
-        const int ew = warp - 2;              // 0..7
-        const int quarter = warp & 3;         // TMEM lane quarter (hardware rule: warp % 4)
-        const int half = ew >> 2;             // codes 128*half .. +127
+        const int ew = warp - 2;              // 0..15
+        const int quarter = warp & 3;         // TMEM lane quarter (warp % 4)
+        const int part = ew >> 2;             // codes 64*part .. +63
         const int row = quarter * 32 + lane;
-        const float g = 1e-4f;
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
             const int b = i & 1, u = i >> 1;
             const int64_t v = t * 128 + row;
             const bool live = v < a.n_vec;
-            // |z|^2 from the tile in global memory (L2): z = hi + lo exactly
-            float zv[32];
+            // |z|^2 (z = hi + lo exactly), from the tile in L2
+            const float4 *zt = reinterpret_cast<const float4 *>(a.zt) + t * (2 * 8 * 128) + row;
             float zn = 0.f;
-            {
-                const float4 *zt = reinterpret_cast<const float4 *>(a.zt) + t * (2 * 8 * 128) + row;
+#pragma unroll
+            for (int gq = 0; gq < 8; ++gq) {
+                const float4 h = zt[gq * 128], l = zt[(8 + gq) * 128];
+                const float z0 = __fadd_rn(h.x, l.x), z1 = __fadd_rn(h.y, l.y);
+                const float z2 = __fadd_rn(h.z, l.z), z3 = __fadd_rn(h.w, l.w);
+                zn = fmaf(z0, z0, zn);
+                zn = fmaf(z1, z1, zn);
+                zn = fmaf(z2, z2, zn);
+                zn = fmaf(z3, z3, zn);
+            }
+            const float gzn = g * zn;
+            mbar_wait(&tfull[b], u & 1);
+            tc_fence_after();
+            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * NC + part * 64);
+            // one pass: m = min upper end, lo1 < lo2 the two smallest lower ends
+            float m = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
+            int k1 = 0x7FFFFFFF;
+#pragma unroll
+            for (int ch = 0; ch < 2; ++ch) {
+                float dv[32];
+                tmem_ld32(tbase + 32 * ch, dv);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int k = part * 64 + 32 * ch + j;
+                    const float2 c = s_cn[k];
+                    const float dp = fmaf(-2.f, dv[j], c.x);
+                    const float e = c.y + gzn;
+                    m = fminf(m, dp + e);
+                    const float lo = dp - e;
+                    if (lo < lo2) {
+                        if (lo < lo1) {
+                            lo2 = lo1;
+                            lo1 = lo;
+                            k1 = k;
+                        } else {
+                            lo2 = lo;
+                        }
+                    }
+                }
+            }
+            s_x[part * 128 + row] = make_float4(m, lo1, lo2, __int_as_float(k1));
+            named_bar(1, NE);
+            // merge the parts in code order (ties keep the lower part / code)
+            float M = INFINITY, L1 = INFINITY, L2 = INFINITY;
+            int K1 = 0x7FFFFFFF;
+#pragma unroll
+            for (int p = 0; p < kAmParts; ++p) {
+                const float4 x = s_x[p * 128 + row];
+                M = fminf(M, x.x);
+                if (x.y < L1) {
+                    L2 = fminf(L1, x.z);
+                    L1 = x.y;
+                    K1 = __float_as_int(x.w);
+                } else {
+                    L2 = fminf(L2, x.y);
+                }
+            }
+            const bool single = L2 > M;
+            // rare: more than one survivor -> exact float64 re-score
+            double best = INFINITY;
+            int bk = 0x7FFFFFFF;
+            if (__any_sync(0xffffffffu, !single && live)) {
+                float zv[32];
 #pragma unroll
                 for (int gq = 0; gq < 8; ++gq) {
-                    const float4 h = live ? zt[gq * 128] : make_float4(0, 0, 0, 0);
-                    const float4 l = live ? zt[(8 + gq) * 128] : make_float4(0, 0, 0, 0);
+                    const float4 h = zt[gq * 128], l = zt[(8 + gq) * 128];
                     zv[4 * gq + 0] = __fadd_rn(h.x, l.x);
                     zv[4 * gq + 1] = __fadd_rn(h.y, l.y);
                     zv[4 * gq + 2] = __fadd_rn(h.z, l.z);
                     zv[4 * gq + 3] = __fadd_rn(h.w, l.w);
                 }
+                const float *hi = reinterpret_cast<const float *>(s_cb);
+                const float *lo = hi + 8 * NC * 4;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) zn = fmaf(zv[c], zv[c], zn);
-            }
-            mbar_wait(&tfull[b], u & 1);
-            tc_fence_after();
-            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * NC + half * 128);
-            const float gzn = g * zn;
-            // pass 1: smallest upper end  d'_k + E_k
-            float m = INFINITY;
-#pragma unroll 1
-            for (int ch = 0; ch < 4; ++ch) {
-                float dv[32];
-                tmem_ld32(tbase + 32 * ch, dv);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int k = half * 128 + 32 * ch + j;
-                    const float cn = s_cn[k];
-                    const float dp = fmaf(-2.f, dv[j], cn);
-                    if (k < a.K) m = fminf(m, dp + fmaf(g, cn, gzn));
-                }
-            }
-            s_m[half * 128 + row] = m;
-            named_bar(1, 256);
-            m = fminf(s_m[row], s_m[128 + row]);
-            // pass 2: survivors  d'_k - E_k <= m
-            int cnt = 0, first = 0x7FFFFFFF;
-#pragma unroll 1
-            for (int ch = 0; ch < 4; ++ch) {
-                float dv[32];
-                tmem_ld32(tbase + 32 * ch, dv);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int k = half * 128 + 32 * ch + j;
-                    const float cn = s_cn[k];
-                    const float dp = fmaf(-2.f, dv[j], cn);
-                    if (k < a.K && dp - fmaf(g, cn, gzn) <= m) {
-                        ++cnt;
-                        first = min(first, k);
-                    }
-                }
-            }
-            s_i[half * 128 + row] = cnt;
-            s_i[256 + half * 128 + row] = first;
-            named_bar(1, 256);
-            const int tot = s_i[row] + s_i[128 + row];
-            const int kfirst = min(s_i[256 + row], s_i[256 + 128 + row]);
-            named_bar(1, 256);
-            // pass 3 (rare): exact float64 re-score of the survivors
-            double best = INFINITY;
-            int bk = 0x7FFFFFFF;
-            if (__any_sync(0xffffffffu, tot > 1)) {
-#pragma unroll 1
-                for (int ch = 0; ch < 4; ++ch) {
+                for (int ch = 0; ch < 2; ++ch) {
                     float dv[32];
                     tmem_ld32(tbase + 32 * ch, dv);
-                    if (tot <= 1) continue;
+                    if (single || !live) continue;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const int k = half * 128 + 32 * ch + j;
-                        const float cn = s_cn[k];
-                        const float dp = fmaf(-2.f, dv[j], cn);
-                        if (!(k < a.K && dp - fmaf(g, cn, gzn) <= m)) continue;
-                        const float *hi = reinterpret_cast<const float *>(s_cb);
-                        const float *lo = hi + 8 * NC * 4;
-                        double dist = 0.0;
+                        const int k = part * 64 + 32 * ch + j;
+                        const float2 c = s_cn[k];
+                        const float dp = fmaf(-2.f, dv[j], c.x);
+                        if (!(dp - (c.y + gzn) <= M)) continue;
+                        double dist = 0.0;  // vqvae.py:71-75 arithmetic
 #pragma unroll
-                        for (int c = 0; c < 32; ++c) {
-                            const int e = ((c >> 2) * NC + k) * 4 + (c & 3);
-                            const double diff = __dsub_rn((double)zv[c], (double)__fadd_rn(hi[e], lo[e]));
+                        for (int cc = 0; cc < 32; ++cc) {
+                            const int e = ((cc >> 2) * NC + k) * 4 + (cc & 3);
+                            const double diff = __dsub_rn((double)zv[cc], (double)__fadd_rn(hi[e], lo[e]));
                             dist = __dadd_rn(dist, __dmul_rn(diff, diff));
                         }
                         if (dist < best) {
@@ -915,19 +926,26 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[b]);
-            s_d[half * 128 + row] = best;
-            s_i[half * 128 + row] = bk;
-            named_bar(1, 256);
-            if (half == 0 && live) {
-                int out = kfirst;
-                if (tot > 1) {
-                    const double b0 = s_d[row], b1 = s_d[128 + row];
-                    const int k0 = s_i[row], k1 = s_i[128 + row];
-                    out = (b1 < b0) ? k1 : k0;  // equal distances: the lower half holds the lower k
+            s_d[part * 128 + row] = best;
+            s_k[part * 128 + row] = bk;
+            named_bar(1, NE);
+            if (part == 0 && live) {
+                int out = K1;
+                if (!single) {
+                    double bb = INFINITY;
+                    out = 0x7FFFFFFF;
+#pragma unroll
+                    for (int p = 0; p < kAmParts; ++p) {
+                        const double dd = s_d[p * 128 + row];
+                        if (dd < bb) {  // parts in code order: equal distances keep the lower code
+                            bb = dd;
+                            out = s_k[p * 128 + row];
+                        }
+                    }
                 }
                 a.idx[v] = (uint8_t)out;
             }
-            named_bar(1, 256);
+            named_bar(1, NE);
         }
     }
     tc_fence_before();
@@ -1001,8 +1019,8 @@ int tc_launch_act(const TcLayer &L, cudaStream_t s) { return launch_tc<32, 3, TC
 int argmin_tc_launch(const ArgminTc &a, cudaStream_t s) {
     if (a.n_tiles <= 0) return PILC_OK;
     if (a.K < 1 || a.K > 256) return PILC_E_ARG;
-    const size_t smem = 2 * 8 * 256 * 16 + (size_t)kAmStages * 2 * 8 * 128 * 16 + 4 * 256 + 4 * 256 + 4 * 512 +
-                        8 * 256 + 8 * (2 * kAmStages + 5) + 16;
+    const size_t smem = 2 * 8 * 256 * 16 + (size_t)kAmStages * 2 * 8 * 128 * 16 + 8 * 256 + 16 * kAmParts * 128 +
+                        8 * kAmParts * 128 + 4 * kAmParts * 128 + 8 * (2 * kAmStages + 5) + 16;
     cudaFuncSetAttribute(argmin_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t grid = sm_count();
     if (grid > a.n_tiles) grid = a.n_tiles;
