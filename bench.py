@@ -96,15 +96,22 @@ def cpu_oracle_run(per_proc: int, procs: int, seed0: int = 1000):
     return nbytes / 1e6 / wall, nbytes, wall
 
 
+def cpu_sample_size(procs: int, target_s: float) -> int:
+    """Images per process so one oracle run lasts about target_s seconds."""
+    _, _, wall = cpu_oracle_run(2, procs)
+    return max(2, int(round(2 * target_s / max(wall, 1e-3))))
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
     procs = len(os.sched_getaffinity(0))
-    per_proc = 2
+    # each step is a bounded sample; the whole run stays within ~3 minutes
+    per_proc = cpu_sample_size(procs, max(1.0, min(10.0, 150.0 / (args.steps + args.warmup))))
     vals = []
     for _ in range(args.warmup):
-        cpu_oracle_run(1, procs)
+        cpu_oracle_run(2, procs)
     t_all = 0.0
     for _ in range(args.steps):
         v, nbytes, wall = cpu_oracle_run(per_proc, procs)
@@ -153,6 +160,22 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:  # NVML polls in microseconds; nvidia-smi takes ~0.1 s per sample
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = (pynvml.nvmlClocksThrottleReasonHwSlowdown, pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksThrottleReasonSwThermalSlowdown, pynvml.nvmlClocksThrottleReasonSwPowerCap)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append([str(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), str(mx)]
+                                    + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.01)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -235,7 +258,7 @@ def run_gpu(args):
         return outs
 
     # warm-up (+ correctness of the device path, outside the timed region)
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):
         outs = step_device()
     torch.cuda.synchronize(dev)
     lossless = True
@@ -325,7 +348,7 @@ def run_gpu(args):
         dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
         roofline = None
         notes = {
-            "tc3_conv_kernel": "3xTF32 tcgen05 (kind::tf32, 3 MMAs per K step) encoder block convs; "
+            "tc3_conv_kernel": "3xTF32 tcgen05 (kind::tf32, 2 MMAs per K step: A_hi x [B_hi|B_lo] and A_lo x B_hi) encoder block convs; "
                                "algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch",
             "tc_conv_kernel": "bf16 tcgen05 decoder convs; algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch",
             "conv_kernel": "fp32 SIMT convs (stem/down); algorithmic FLOPs = 2*N*Ho*Wo*Cout*Cin*k^2 per launch",
@@ -354,9 +377,10 @@ def run_gpu(args):
         cpu = None
         if ws == 1 and not args.no_cpu:
             procs = len(os.sched_getaffinity(0))
-            v, nbytes, wall = cpu_oracle_run(2, procs)
+            per_proc = cpu_sample_size(procs, 10.0)
+            v, nbytes, wall = cpu_oracle_run(per_proc, procs)
             cpu = {"value": round(v, 4), "unit": "MB/s", "cores": procs, "kind": "port",
-                   "sample": f"{2 * procs} CIFAR images ({nbytes} B) compress+decompress, oracle/ numpy+C, "
+                   "sample": f"{per_proc * procs} CIFAR images ({nbytes} B) compress+decompress, oracle/ numpy+C, "
                              f"{procs} processes x 1 thread, {wall:.1f} s"}
         line = {
             "metric": METRIC,

@@ -702,51 +702,76 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
 // ---- codebook argmin on tcgen05 (vqvae.py:66-76) ---------------------------
 // Per 128-latent tile: dot[r][k] = z_r . c_k for all 256 codes as a 3xTF32
 // GEMM (z_hi c_hi + z_hi c_lo + z_lo c_hi, fp32 TMEM accumulators, M=128,
-// N=256, K=32). The epilogue forms d'_k = |c_k|^2 - 2 dot_k (+|z|^2) and an
-// error radius E_k = g (|z|^2 + |c_k|^2) with g = 1e-4, ten times the
-// worst case of the split products, tf32 truncation of the lo parts and
-// fp32 accumulation of 96 terms (~1e-5). The reference's argmin (float64,
-// component order, first minimum) must satisfy d'_k - E_k <= min_j (d'_j +
-// E_j); if exactly one code passes it is the answer, otherwise the
-// survivors are re-scored exactly as the reference does (float64, same
-// order, no FMA) and the smallest wins, ties to the lowest index.
-// Warps: 0 producer (bulk copies of the z tile), 1 TMEM + MMA, 2..9
-// epilogue (two warps per TMEM lane quarter, 128 codes each).
-constexpr int kAmThreads = 576;  // 2 + 16 warps
+// N=256, K=32). The epilogue ranks codes by f_k = |c_k|^2 - 2 dot_k (|z|^2 is
+// common to the row and cannot change the order). f_k is within
+// e_k = a1 |z| |c_k| + a2 |c_k|^2 of the exact value: the dot product of the
+// split operands is off by at most eps |z||c_k| (Cauchy-Schwarz) with
+// eps = 2^-21 + 2^-21 + 2^-22 (tf32-truncated lo parts, dropped lo x lo) +
+// 96 x 2^-23 (fp32 accumulation of 96 products, even with truncating adds)
+// ~ 1.3e-5, |c_k|^2 in fp32 is within 32 x 2^-24, plus one rounding of f_k;
+// a1 = 5.3e-5 and a2 = 4e-6 are twice those worst cases (the reference's own
+// float64 rounding, ~1e-13 relative, is far inside the margin). With
+// E = max_k e_k (a row constant), d1 < d2 the two smallest f and k1 the
+// code of d1: if d2 - d1 > 2E every other code is strictly farther than k1
+// under the reference's arithmetic, so k1 is its answer. Otherwise (~0.3% of
+// rows) every code with f_k <= d1 + 2E -- a superset of the reference's
+// possible winners -- is re-scored exactly as the reference does (float64,
+// component order, no FMA) and the first minimum wins.
+// Warps: 0 producer (bulk copies of z tiles), 1 TMEM + MMA, 2..9 epilogue
+// in two groups of four (one per TMEM lane quarter); group g owns the tiles
+// with i % 2 == g and TMEM buffer g, so a group re-scoring a rare ambiguous
+// row never stalls the other, and no barrier spans the groups.
+constexpr int kAmThreads = 320;
 constexpr int kAmStages = 3;
-constexpr int kAmParts = 4;      // epilogue warps per TMEM lane quarter (64 codes each)
 
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float *v) {
+    uint32_t r[64];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[32 * h + 0]), "=r"(r[32 * h + 1]), "=r"(r[32 * h + 2]), "=r"(r[32 * h + 3]),
+              "=r"(r[32 * h + 4]), "=r"(r[32 * h + 5]), "=r"(r[32 * h + 6]), "=r"(r[32 * h + 7]),
+              "=r"(r[32 * h + 8]), "=r"(r[32 * h + 9]), "=r"(r[32 * h + 10]), "=r"(r[32 * h + 11]),
+              "=r"(r[32 * h + 12]), "=r"(r[32 * h + 13]), "=r"(r[32 * h + 14]), "=r"(r[32 * h + 15]),
+              "=r"(r[32 * h + 16]), "=r"(r[32 * h + 17]), "=r"(r[32 * h + 18]), "=r"(r[32 * h + 19]),
+              "=r"(r[32 * h + 20]), "=r"(r[32 * h + 21]), "=r"(r[32 * h + 22]), "=r"(r[32 * h + 23]),
+              "=r"(r[32 * h + 24]), "=r"(r[32 * h + 25]), "=r"(r[32 * h + 26]), "=r"(r[32 * h + 27]),
+              "=r"(r[32 * h + 28]), "=r"(r[32 * h + 29]), "=r"(r[32 * h + 30]), "=r"(r[32 * h + 31])
+            : "r"(taddr + 32u * h));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
 
 __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
-    constexpr int NC = 256;           // codes (N)
-    constexpr int NE = 32 * 4 * kAmParts;      // epilogue threads (512)
+    constexpr int NC = 256;                    // codes (N)
     constexpr uint32_t ZB = 2 * 8 * 128 * 16;  // z tile bytes (hi + lo)
     constexpr uint32_t CB = 2 * 8 * NC * 16;   // codebook operand bytes
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t *s_cb = smem;                                  // [hi|lo][8][256][16 B]
-    uint8_t *s_z = smem + CB;                              // kAmStages x ZB
-    float2 *s_cn = reinterpret_cast<float2 *>(s_z + kAmStages * ZB);  // (|c_k|^2, g |c_k|^2)
-    float4 *s_x = reinterpret_cast<float4 *>(s_cn + NC);   // [parts][128] (m, lo1, lo2, k1)
-    double *s_d = reinterpret_cast<double *>(s_x + kAmParts * 128);  // [parts][128]
-    int *s_k = reinterpret_cast<int *>(s_d + kAmParts * 128);        // [parts][128]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_k + kAmParts * 128);
+    uint8_t *s_cb = smem;                                            // [hi|lo][8][256][16 B]
+    uint8_t *s_z = smem + CB;                                        // kAmStages x ZB
+    float *s_cn = reinterpret_cast<float *>(s_z + kAmStages * ZB);   // |c_k|^2, +inf for k >= K
+    uint32_t *s_max = reinterpret_cast<uint32_t *>(s_cn + NC);       // max |c_k|, max |c_k|^2 (f32 bits)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_max + 4);
     uint64_t *full = bars, *empty = bars + kAmStages, *tfull = bars + 2 * kAmStages, *tempty = tfull + 2;
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
-    const float g = 1e-4f;
+    const float a1 = 5.3e-5f, a2 = 4e-6f;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kAmStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], 1 + 4);  // MMA commit + the epilogue warps reading |z|^2
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4 * kAmParts);
+            mbar_init(&tempty[b], 4);
         }
         mbar_init(wbar, 1);
+        s_max[0] = s_max[1] = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         mbar_expect_tx(wbar, CB);
         bulk_g2s(s_cb, a.cbt, CB, wbar);
@@ -761,17 +786,20 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     mbar_wait(wbar, 0);
+    const float *cb_hi = reinterpret_cast<const float *>(s_cb);
+    const float *cb_lo = cb_hi + 8 * NC * 4;
     for (int k = threadIdx.x; k < NC; k += blockDim.x) {
-        const float *hi = reinterpret_cast<const float *>(s_cb);
-        const float *lo = hi + 8 * NC * 4;
         float acc = 0.f;
         for (int c = 0; c < 32; ++c) {
             const int e = ((c >> 2) * NC + k) * 4 + (c & 3);
-            const float v = __fadd_rn(hi[e], lo[e]);
+            const float v = __fadd_rn(cb_hi[e], cb_lo[e]);
             acc = fmaf(v, v, acc);
         }
-        // codes >= K can never win: +inf distance
-        s_cn[k] = k < a.K ? make_float2(acc, g * acc) : make_float2(INFINITY, 0.f);
+        s_cn[k] = k < a.K ? acc : INFINITY;  // codes >= K can never win
+        if (k < a.K) {  // non-negative floats order as their bit patterns
+            atomicMax(&s_max[0], __float_as_uint(sqrtf(acc) * 1.000001f));
+            atomicMax(&s_max[1], __float_as_uint(acc));
+        }
     }
     __syncthreads();
 
@@ -813,139 +841,119 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
             }
         }
     } else {
-        const int ew = warp - 2;              // 0..15
-        const int quarter = warp & 3;         // TMEM lane quarter (warp % 4)
-        const int part = ew >> 2;             // codes 64*part .. +63
+        const int grp = (warp - 2) >> 2;  // tiles i with i % 2 == grp, TMEM buffer grp
+        const int quarter = warp & 3;     // TMEM lane quarter (warp % 4)
         const int row = quarter * 32 + lane;
-        int i = 0;
-        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int b = i & 1, u = i >> 1;
+        const float cmax = __uint_as_float(s_max[0]), cnmax = __uint_as_float(s_max[1]);
+        const float4 *cn4 = reinterpret_cast<const float4 *>(s_cn);
+        const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(grp * NC);
+        int i = grp;
+        for (int64_t t = blockIdx.x + (int64_t)grp * gridDim.x; t < n_tiles; t += 2 * (int64_t)gridDim.x, i += 2) {
+            const int s = i % kAmStages, u = i >> 1;
             const int64_t v = t * 128 + row;
             const bool live = v < a.n_vec;
-            // |z|^2 (z = hi + lo exactly), from the tile in L2
-            const float4 *zt = reinterpret_cast<const float4 *>(a.zt) + t * (2 * 8 * 128) + row;
+            // |z|^2 from the staged tile (z = hi + lo exactly)
+            mbar_wait(&full[s], (i / kAmStages) & 1);
+            const float4 *zs = reinterpret_cast<const float4 *>(s_z + (size_t)s * ZB) + row;
             float zn = 0.f;
 #pragma unroll
             for (int gq = 0; gq < 8; ++gq) {
-                const float4 h = zt[gq * 128], l = zt[(8 + gq) * 128];
-                const float z0 = __fadd_rn(h.x, l.x), z1 = __fadd_rn(h.y, l.y);
-                const float z2 = __fadd_rn(h.z, l.z), z3 = __fadd_rn(h.w, l.w);
-                zn = fmaf(z0, z0, zn);
-                zn = fmaf(z1, z1, zn);
-                zn = fmaf(z2, z2, zn);
-                zn = fmaf(z3, z3, zn);
+                const float4 h = zs[gq * 128], l = zs[(8 + gq) * 128];
+                zn = fmaf(__fadd_rn(h.x, l.x), __fadd_rn(h.x, l.x), zn);
+                zn = fmaf(__fadd_rn(h.y, l.y), __fadd_rn(h.y, l.y), zn);
+                zn = fmaf(__fadd_rn(h.z, l.z), __fadd_rn(h.z, l.z), zn);
+                zn = fmaf(__fadd_rn(h.w, l.w), __fadd_rn(h.w, l.w), zn);
             }
-            const float gzn = g * zn;
-            mbar_wait(&tfull[b], u & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            // 2E, E = max_k e_k; the 1.000001 covers the roundings of |z|^2, sqrt and the products
+            const float e2 = 2.f * fmaf(a1 * sqrtf(zn) * 1.000001f, cmax, a2 * cnmax) * 1.000001f;
+
+            mbar_wait(&tfull[grp], u & 1);
             tc_fence_after();
-            const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * NC + part * 64);
-            // one pass: m = min upper end, lo1 < lo2 the two smallest lower ends
-            float m = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
-            int k1 = 0x7FFFFFFF;
+            // two interleaved chains of (smallest, its code, second smallest)
+            float d1a = INFINITY, d2a = INFINITY, d1b = INFINITY, d2b = INFINITY;
+            int k1a = 0, k1b = 0;
+#pragma unroll 1
+            for (int c = 0; c < NC / 64; ++c) {
+                float dv[64];
+                tmem_ld64(tbase + 64 * c, dv);
 #pragma unroll
-            for (int ch = 0; ch < 2; ++ch) {
-                float dv[32];
-                tmem_ld32(tbase + 32 * ch, dv);
+                for (int j = 0; j < 64; j += 4) {
+                    const float4 cn = cn4[(64 * c + j) >> 2];
+                    const int k = 64 * c + j;
+                    float f = fmaf(-2.f, dv[j], cn.x);
+                    d2a = fminf(d2a, fmaxf(d1a, f));
+                    k1a = f < d1a ? k : k1a;
+                    d1a = fminf(d1a, f);
+                    f = fmaf(-2.f, dv[j + 1], cn.y);
+                    d2b = fminf(d2b, fmaxf(d1b, f));
+                    k1b = f < d1b ? k + 1 : k1b;
+                    d1b = fminf(d1b, f);
+                    f = fmaf(-2.f, dv[j + 2], cn.z);
+                    d2a = fminf(d2a, fmaxf(d1a, f));
+                    k1a = f < d1a ? k + 2 : k1a;
+                    d1a = fminf(d1a, f);
+                    f = fmaf(-2.f, dv[j + 3], cn.w);
+                    d2b = fminf(d2b, fmaxf(d1b, f));
+                    k1b = f < d1b ? k + 3 : k1b;
+                    d1b = fminf(d1b, f);
+                }
+            }
+            float d1, d2;
+            int k1;
+            if (d1b < d1a) {
+                d1 = d1b, k1 = k1b, d2 = fminf(d1a, d2b);
+            } else {
+                d1 = d1a, k1 = k1a, d2 = fminf(d2a, d1b);
+            }
+            const bool amb = live && !(d2 - d1 > e2);
+            if (__any_sync(0xffffffffu, amb)) {
+                // rare: re-score every code with f_k <= d1 + 2E exactly as vqvae.py:71-75
+                float zv[32];
+                if (amb) {
+                    const float4 *zt = reinterpret_cast<const float4 *>(a.zt) + t * (2 * 8 * 128) + row;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int k = part * 64 + 32 * ch + j;
-                    const float2 c = s_cn[k];
-                    const float dp = fmaf(-2.f, dv[j], c.x);
-                    const float e = c.y + gzn;
-                    m = fminf(m, dp + e);
-                    const float lo = dp - e;
-                    if (lo < lo2) {
-                        if (lo < lo1) {
-                            lo2 = lo1;
-                            lo1 = lo;
-                            k1 = k;
-                        } else {
-                            lo2 = lo;
-                        }
+                    for (int gq = 0; gq < 8; ++gq) {
+                        const float4 h = zt[gq * 128], l = zt[(8 + gq) * 128];
+                        zv[4 * gq + 0] = __fadd_rn(h.x, l.x);
+                        zv[4 * gq + 1] = __fadd_rn(h.y, l.y);
+                        zv[4 * gq + 2] = __fadd_rn(h.z, l.z);
+                        zv[4 * gq + 3] = __fadd_rn(h.w, l.w);
                     }
                 }
-            }
-            s_x[part * 128 + row] = make_float4(m, lo1, lo2, __int_as_float(k1));
-            named_bar(1, NE);
-            // merge the parts in code order (ties keep the lower part / code)
-            float M = INFINITY, L1 = INFINITY, L2 = INFINITY;
-            int K1 = 0x7FFFFFFF;
+                const float thr = d1 + e2;
+                double best = INFINITY;
+#pragma unroll 1
+                for (int c = 0; c < NC / 64; ++c) {
+                    float dv[64];
+                    tmem_ld64(tbase + 64 * c, dv);
+                    if (!amb) continue;
+                    uint64_t cand = 0;
 #pragma unroll
-            for (int p = 0; p < kAmParts; ++p) {
-                const float4 x = s_x[p * 128 + row];
-                M = fminf(M, x.x);
-                if (x.y < L1) {
-                    L2 = fminf(L1, x.z);
-                    L1 = x.y;
-                    K1 = __float_as_int(x.w);
-                } else {
-                    L2 = fminf(L2, x.y);
-                }
-            }
-            const bool single = L2 > M;
-            // rare: more than one survivor -> exact float64 re-score
-            double best = INFINITY;
-            int bk = 0x7FFFFFFF;
-            if (__any_sync(0xffffffffu, !single && live)) {
-                float zv[32];
-#pragma unroll
-                for (int gq = 0; gq < 8; ++gq) {
-                    const float4 h = zt[gq * 128], l = zt[(8 + gq) * 128];
-                    zv[4 * gq + 0] = __fadd_rn(h.x, l.x);
-                    zv[4 * gq + 1] = __fadd_rn(h.y, l.y);
-                    zv[4 * gq + 2] = __fadd_rn(h.z, l.z);
-                    zv[4 * gq + 3] = __fadd_rn(h.w, l.w);
-                }
-                const float *hi = reinterpret_cast<const float *>(s_cb);
-                const float *lo = hi + 8 * NC * 4;
-#pragma unroll
-                for (int ch = 0; ch < 2; ++ch) {
-                    float dv[32];
-                    tmem_ld32(tbase + 32 * ch, dv);
-                    if (single || !live) continue;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int k = part * 64 + 32 * ch + j;
-                        const float2 c = s_cn[k];
-                        const float dp = fmaf(-2.f, dv[j], c.x);
-                        if (!(dp - (c.y + gzn) <= M)) continue;
-                        double dist = 0.0;  // vqvae.py:71-75 arithmetic
+                    for (int j = 0; j < 64; ++j)
+                        cand |= (uint64_t)(fmaf(-2.f, dv[j], s_cn[64 * c + j]) <= thr) << j;
+#pragma unroll 1
+                    for (; cand; cand &= cand - 1) {  // codes in increasing order
+                        const int k = 64 * c + __ffsll((long long)cand) - 1;
+                        double dist = 0.0;
 #pragma unroll
                         for (int cc = 0; cc < 32; ++cc) {
                             const int e = ((cc >> 2) * NC + k) * 4 + (cc & 3);
-                            const double diff = __dsub_rn((double)zv[cc], (double)__fadd_rn(hi[e], lo[e]));
+                            const double diff = __dsub_rn((double)zv[cc], (double)__fadd_rn(cb_hi[e], cb_lo[e]));
                             dist = __dadd_rn(dist, __dmul_rn(diff, diff));
                         }
-                        if (dist < best) {
+                        if (dist < best) {  // equal distances keep the lower code
                             best = dist;
-                            bk = k;
+                            k1 = k;
                         }
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[b]);
-            s_d[part * 128 + row] = best;
-            s_k[part * 128 + row] = bk;
-            named_bar(1, NE);
-            if (part == 0 && live) {
-                int out = K1;
-                if (!single) {
-                    double bb = INFINITY;
-                    out = 0x7FFFFFFF;
-#pragma unroll
-                    for (int p = 0; p < kAmParts; ++p) {
-                        const double dd = s_d[p * 128 + row];
-                        if (dd < bb) {  // parts in code order: equal distances keep the lower code
-                            bb = dd;
-                            out = s_k[p * 128 + row];
-                        }
-                    }
-                }
-                a.idx[v] = (uint8_t)out;
-            }
-            named_bar(1, NE);
+            if (lane == 0) mbar_arrive(&tempty[grp]);
+            if (live) a.idx[v] = (uint8_t)k1;
         }
     }
     tc_fence_before();
@@ -1019,8 +1027,8 @@ int tc_launch_act(const TcLayer &L, cudaStream_t s) { return launch_tc<32, 3, TC
 int argmin_tc_launch(const ArgminTc &a, cudaStream_t s) {
     if (a.n_tiles <= 0) return PILC_OK;
     if (a.K < 1 || a.K > 256) return PILC_E_ARG;
-    const size_t smem = 2 * 8 * 256 * 16 + (size_t)kAmStages * 2 * 8 * 128 * 16 + 8 * 256 + 16 * kAmParts * 128 +
-                        8 * kAmParts * 128 + 4 * kAmParts * 128 + 8 * (2 * kAmStages + 5) + 16;
+    const size_t smem = 2 * 8 * 256 * 16 + (size_t)kAmStages * 2 * 8 * 128 * 16 + 4 * 256 + 16 +
+                        8 * (2 * kAmStages + 5) + 16;
     cudaFuncSetAttribute(argmin_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t grid = sm_count();
     if (grid > a.n_tiles) grid = a.n_tiles;

@@ -72,6 +72,24 @@ def _pinned_owner(arr: np.ndarray):
     return None
 
 
+_POOL = None
+
+
+def _par_copy(dst: np.ndarray, src: np.ndarray, chunk: int = 4 << 20) -> None:
+    """memcpy into pinned staging with a few threads (numpy drops the GIL)."""
+    n = src.size
+    if n < 4 * chunk:
+        dst[...] = src
+        return
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="pilc-copy")
+    step = -(-n // 8)
+    list(_POOL.map(lambda i: np.copyto(dst[i:i + step], src[i:i + step]), range(0, n, step)))
+
+
 def h2d(arr: np.ndarray, dev: torch.device, stream: torch.cuda.Stream, pad: int = 0) -> torch.Tensor:
     """Host numpy -> device tensor. Page-locked sources (buffers this package
     returned) DMA directly; pageable ones go through a pinned staging copy."""
@@ -88,7 +106,7 @@ def h2d(arr: np.ndarray, dev: torch.device, stream: torch.cuda.Stream, pad: int 
             return out
     host = pinned(flat.size + pad)
     hv = host.numpy()
-    hv[: flat.size] = flat
+    _par_copy(hv[: flat.size], flat)
     if pad:
         hv[flat.size:] = 0
     with torch.cuda.stream(stream):
