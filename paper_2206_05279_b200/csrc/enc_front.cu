@@ -1,7 +1,7 @@
 // Fused encoder front for the 3xTF32 encoder: stem (3x3, 3 -> 32, ReLU) and
 // down (3x3 stride 2, 32 -> 32, ReLU) in one kernel, stem tile kept in
-// shared memory, output written straight into the tf32 hi / fp32 lo slabs
-// the tcgen05 block convs read (tc_conv.cu).
+// shared memory, output written straight into the fp32 slab the tcgen05
+// block convs read (tc_conv.cu).
 //
 // Reference: vqvae.encode_to_indices (vqvae.py:55-57) with _even_pad,
 // _normalize (vqvae.py:33-43) and nn.conv2d's edge-replicate padding
@@ -14,12 +14,14 @@
 //   2. stem at the 33 x 33 clamped positions the tile needs, one position
 //      x 32 channels per thread per round -> smem (channel-planar)
 //   3. down conv: 4 outputs x 8 channels per thread
-//   4. bias + ReLU + tf32 split -> hi / lo slabs (+ border copies)
+//   4. bias + ReLU -> the fp32 slab set and the scaled fp16 hi / lo operand
+//      slabs of the first block conv (+ border copies)
 #include <math.h>
 #include <stdint.h>
 
 #include "common.cuh"
 #include "enc_front.cuh"
+#include <cuda_fp16.h>
 
 namespace {
 
@@ -35,6 +37,21 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 
 __device__ __forceinline__ void store4(float *slab, int64_t q, float4 v, int y, int x, int H, int W, int Wp) {
     float4 *p = reinterpret_cast<float4 *>(slab);
+    p[q] = v;
+    const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
+    const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
+    if (dy) p[q - Wp] = v;
+    if (dy2) p[q + Wp] = v;
+    if (dx) p[q - 1] = v;
+    if (dx2) p[q + 1] = v;
+    if (dy && dx) p[q - Wp - 1] = v;
+    if (dy && dx2) p[q - Wp + 1] = v;
+    if (dy2 && dx) p[q + Wp - 1] = v;
+    if (dy2 && dx2) p[q + Wp + 1] = v;
+}
+
+__device__ __forceinline__ void store16(uint16_t *slab, int64_t q, uint4 v, int y, int x, int H, int W, int Wp) {
+    uint4 *p = reinterpret_cast<uint4 *>(slab);
     p[q] = v;
     const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
     const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
@@ -149,27 +166,48 @@ __global__ void __launch_bounds__(kThreads) enc_front_kernel(EncFront a) {
                 }
             }
     }
-    // 4. bias + ReLU + tf32 split into the padded group-major slabs
+    // 4. bias + ReLU -> the fp32 slab set and the scaled fp16 hi / lo operands
     const int Wp = a.gw + 2;
+    const int k0 = *a.k0;
+    const float sc = __int_as_float((127 + k0) << 23);
+    float mx = 0.f;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         const int oy = oy0 + ry + 4 * u, ox = ox0 + cx;
         if (oy >= a.gh || ox >= a.gw) continue;
         const int64_t q = (n * (a.gh + 2) + oy + 1) * (int64_t)Wp + ox + 1;
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            v[e] = fmaxf(__fadd_rn(acc[u][e], s_bd[8 * cgrp + e]), 0.f);
+            mx = fmaxf(mx, v[e]);
+        }
 #pragma unroll
         for (int g2 = 0; g2 < 2; ++g2) {
-            float hi[4], lo[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float v = fmaxf(__fadd_rn(acc[u][4 * g2 + e], s_bd[8 * cgrp + 4 * g2 + e]), 0.f);
-                hi[e] = __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);  // tf32 rna
-                lo[e] = __fsub_rn(v, hi[e]);
-            }
             const int64_t so = ((int64_t)(2 * cgrp + g2) * a.gstride + a.margin) * 4;
-            store4(a.out_hi + so, q, make_float4(hi[0], hi[1], hi[2], hi[3]), oy + 1, ox + 1, a.gh, a.gw, Wp);
-            store4(a.out_lo + so, q, make_float4(lo[0], lo[1], lo[2], lo[3]), oy + 1, ox + 1, a.gh, a.gw, Wp);
+            store4(a.out32 + so, q, make_float4(v[4 * g2], v[4 * g2 + 1], v[4 * g2 + 2], v[4 * g2 + 3]), oy + 1,
+                   ox + 1, a.gh, a.gw, Wp);
         }
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float x0 = __fmul_rn(v[2 * e], sc), x1 = __fmul_rn(v[2 * e + 1], sc);
+            const __half2 hh = __floats2half2_rn(x0, x1);
+            const float2 hf = __half22float2(hh);
+            const __half2 ll = __floats2half2_rn(__fmul_rn(__fsub_rn(x0, hf.x), 2048.f),
+                                                 __fmul_rn(__fsub_rn(x1, hf.y), 2048.f));
+            h[e] = *reinterpret_cast<const uint32_t *>(&hh);
+            l[e] = *reinterpret_cast<const uint32_t *>(&ll);
+        }
+        store16(a.out + ((int64_t)cgrp * a.gstride + a.margin) * 8, q, make_uint4(h[0], h[1], h[2], h[3]), oy + 1,
+                ox + 1, a.gh, a.gw, Wp);
+        store16(a.out + ((int64_t)(4 + cgrp) * a.gstride + a.margin) * 8, q, make_uint4(l[0], l[1], l[2], l[3]),
+                oy + 1, ox + 1, a.gh, a.gw, Wp);
     }
+    // per-image max (bound input of the first block conv) and the scale
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(mx));
+    if ((t & 31) == 0 && m != 0u) atomicMax(a.out_max + n, m);
+    if (t == 0) a.kx_out[n] = k0;
 }
 
 }  // namespace

@@ -11,7 +11,11 @@ struct EncFront {
     int stem_ci_pad, stem_co_pad;
     const float *w_down, *b_down;
     int down_ci_pad, down_co_pad;
-    float *out_hi, *out_lo;  // padded group-major tf32 hi / fp32 lo slabs
+    float *out32;       // padded group-major fp32 slab set (tc_conv.cu encoder layout)
+    uint16_t *out;      // scaled fp16 hi / lo slab set (scale 2^k0)
+    uint32_t *out_max;  // per-image max |out| (float bits, atomicMax)
+    int32_t *kx_out;    // per-image scale exponent (= k0)
+    const int32_t *k0;  // device: static scale exponent of this output
     int64_t gstride, margin;
 };
 

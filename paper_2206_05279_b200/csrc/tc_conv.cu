@@ -28,6 +28,7 @@
 // atomics -- so a blob compressed on one GPU decodes on any other.
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
@@ -107,6 +108,22 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
         "}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+
+// issued by one elected lane of a converged warp: the issue loop stays
+// warp-uniform, so descriptors live in uniform registers and no per-MMA
+// single-lane branch is needed
+__device__ __forceinline__ void mma_bf16_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar);
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -259,37 +276,33 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(128, N);
-            mbar_wait(wbar, 0);
+        // warp-uniform issue loop, one elected lane per MMA (see tc3)
+        constexpr uint32_t idesc = idesc_bf16(128, N);
+        mbar_wait(wbar, 0);
+        tc_fence_after();
+        const uint64_t dA0 = umma_desc(smem_u32(s_a), (uint32_t)npix * 16u, 128u);
+        const uint64_t dB0 = umma_desc(smem_u32(s_w), (uint32_t)N * 16u, 128u);
+        const uint32_t npx = (uint32_t)npix;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int s = i % kStages;
+            const int a = i & 1;
+            const int u = i >> 1;
+            if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
+            mbar_wait(&full[s], (i / kStages) & 1);
             tc_fence_after();
-            const uint32_t w_base = smem_u32(s_w);
-            int i = 0;
-            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-                const int s = i % kStages;
-                const int a = i & 1;
-                const int u = i >> 1;
-                if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
-                mbar_wait(&full[s], (i / kStages) & 1);
-                tc_fence_after();
-                const uint32_t a_base = smem_u32(s_a + (size_t)s * stage_bytes);
-                const uint32_t d = tmem + (uint32_t)(a * N);
+            const uint64_t dA = dA0 + (uint64_t)((uint32_t)s * (stage_bytes >> 4));
+            const uint32_t d = tmem + (uint32_t)(a * N);
 #pragma unroll
-                for (int tap = 0; tap < KS * KS; ++tap) {
-                    const int ti = tap / KS, tj = tap % KS;
-                    const uint32_t off = KS == 3 ? (uint32_t)(ti * Wp + tj) * 16u : 0u;
+            for (int tap = 0; tap < KS * KS; ++tap) {
+                const uint32_t off = KS == 3 ? (uint32_t)((tap / KS) * Wp + tap % KS) : 0u;
 #pragma unroll
-                    for (int ks = 0; ks < NG / 2; ++ks) {
-                        const uint64_t ad = umma_desc(a_base + (uint32_t)(2 * ks) * npix * 16u + off,
-                                                      (uint32_t)npix * 16u, 128u);
-                        const uint64_t bd = umma_desc(w_base + (uint32_t)(tap * NG + 2 * ks) * N * 16u,
-                                                      (uint32_t)N * 16u, 128u);
-                        mma_bf16(d, ad, bd, idesc, (tap | ks) ? 1u : 0u);
-                    }
-                }
-                mma_commit(&empty[s]);
-                mma_commit(&tfull[a]);
+                for (int ks = 0; ks < NG / 2; ++ks)
+                    mma_bf16_elect(d, dA + (uint64_t)(2u * ks * npx + off), dB0 + (uint64_t)((tap * NG + 2 * ks) * N),
+                                   idesc, (tap | ks) ? 1u : 0u);
             }
+            mma_commit_elect(&empty[s]);
+            mma_commit_elect(&tfull[a]);
         }
     } else {
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
@@ -462,33 +475,118 @@ __device__ __forceinline__ void store_px4(float *slab, int64_t q, float4 v, int 
     if (dy2 && dx2) p[q + Wp + 1] = v;
 }
 
-// 3xTF32 conv, C = 32 in, N = 32 out: D = Ahi*Bhi + Ahi*Blo + Alo*Bhi, all
-// accumulated in fp32 TMEM. Same pipeline as tc_conv_kernel (producer /
-// MMA / 4 epilogue warps, 3-stage ring, double-buffered accumulator).
-constexpr int kStages3 = 3;
+// Encoder conv, C = 32 in, N = 32 out, as a 3-product fp16 split on
+// tcgen05 kind::f16: fp32-class accuracy at twice the tf32 MMA rate (an
+// SS-mode MMA with N <= 64 is bound by reading its operands from shared
+// memory, and an fp16 K=16 step reads as many bytes as a tf32 K=8 step).
+//
+// Operands. Each activation tensor A_j is stored as two fp16 slab sets per
+// image scale 2^k (k = kx[j][n] for image n): x 2^k = h + l 2^-11 with
+// h = fp16(x 2^k), l = fp16((x 2^k - h) 2^11) (error <= 2^-22 |x 2^k|; tiny
+// values stay exact to 2^-36 absolute); weights likewise with 2^kw. Then
+//   conv = [sum h hw + 2^-11 sum (h lw + l hw)] 2^-(k + kw),
+// the dropped l lw term being <= 2^-22 |x||w|. D[0:32] = sum h hw and
+// D[32:64] = sum (h lw + l hw) accumulate in fp32 TMEM: per K=16 step one MMA
+// A_hi x [W_hi | W_lo] (N=64) and one A_lo x W_hi (N=32) into D[32:64].
+//
+// Scales. The epilogue writing A_j must pick k before A_j is complete, so it
+// uses a rigorous per-image bound: |out| <= max|in| L1 + max|b| (+ max|res|),
+// L1 = max_co sum |w|, from the exact per-image maxima of its inputs (which
+// earlier kernels recorded with atomicMax: order-independent, so nothing
+// depends on the batch or the tiling); k puts the bound below 2^15 < 65504.
+// It also records the exact max of its own output for the next layer.
+// Block outputs are kept in fp32 as well: the residual add is exact.
+//
+// Warps: 0 bulk-copy producer (hi / lo slabs, ring of kStages3), 1 TMEM +
+// MMA issuer (warp-uniform loop, elected lane), 2..9 epilogue in two groups
+// of four (one per accumulator buffer, so one group's epilogue overlaps the
+// other's), 10 residual producer (bulk copies of the fp32 block input).
+constexpr int kStages3 = 6;
+constexpr int kThreadsTC3 = 352;
+
+// kind::f16 instruction descriptor: D f32, A/B fp16, both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// issued by one elected lane of a converged warp (keeps the issue loop
+// warp-uniform: descriptors stay in uniform registers)
+__device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float exp2i(int k) { return __int_as_float((127 + k) << 23); }
+
+// scale exponent k for a per-image bound with float bits `mb`: |x 2^k| < 2^15.
+// k in [-90, 90] and kw in [-30, 30] keep 2^k and 2^-(k + kw) normal.
+__device__ __forceinline__ int act_exp(uint32_t mb) {
+    int k = 0;
+    if (mb != 0u && mb < 0x7F800000u) k = 14 - ((int)(mb >> 23) - 127);
+    return min(max(k, -90), 90);
+}
+
+// fp16 pair (h, l) of two scaled values, packed two per 32-bit word
+__device__ __forceinline__ void split2(float a, float b, uint32_t &h, uint32_t &l) {
+    const __half2 hh = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(__fmul_rn(__fsub_rn(a, hf.x), 2048.f), __fmul_rn(__fsub_rn(b, hf.y), 2048.f));
+    h = *reinterpret_cast<const uint32_t *>(&hh);
+    l = *reinterpret_cast<const uint32_t *>(&ll);
+}
 
 template <int KS, int MODE>
-__global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
+__global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
     constexpr int N = 32;
-    constexpr int N2 = 64;  // B' = [B_hi | B_lo] along N
-    constexpr int NG = 8;   // 4-channel groups
-    constexpr int KG = KS * KS * NG;
+    constexpr int N2 = 64;  // B' = [W_hi | W_lo] along N
+    constexpr int NH = 4;   // 8-channel fp16 groups
+    constexpr int KG = KS * KS * NH;
     constexpr int TMEM_COLS = 2 * N2;
     const int Wp = L.Wp;
     const int npix = KS == 3 ? ((128 + 2 * Wp + 2 + 7) & ~7) : 128;
-    const uint32_t half_bytes = (uint32_t)NG * npix * 16;  // one of hi / lo
-    const uint32_t stage_bytes = 2 * half_bytes;
+    const uint32_t h_bytes = (uint32_t)NH * npix * 16;
+    const uint32_t stage_bytes = 2 * h_bytes;
     const uint32_t wbytes = (uint32_t)KG * N2 * 16;
 
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *s_w = smem;
     uint8_t *s_a = smem + (size_t)wbytes;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_a + (size_t)kStages3 * stage_bytes);
+    const bool has_res = MODE == TC3_ACT && L.res != nullptr;
+    float4 *s_res = reinterpret_cast<float4 *>(s_a + (size_t)kStages3 * stage_bytes);  // [2][8][128]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(s_res) + (has_res ? 2 * 8 * 128 * 16 : 0));
     uint64_t *full = bars;
     uint64_t *empty = bars + kStages3;
     uint64_t *tfull = bars + 2 * kStages3;
     uint64_t *tempty = tfull + 2;
-    uint64_t *wbar = tempty + 2;
+    uint64_t *rfull = tempty + 2;
+    uint64_t *rempty = rfull + 2;
+    uint64_t *wbar = rempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -500,6 +598,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4);
+            mbar_init(&rfull[a], 1);
+            mbar_init(&rempty[a], 4);
         }
         mbar_init(wbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -518,7 +618,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
     if (warp == 0) {
         if (lane == 0) {
             mbar_expect_tx(wbar, wbytes);
-            bulk_g2s(s_w, L.w_hi, wbytes, wbar);
+            bulk_g2s(s_w, L.w, wbytes, wbar);
             int i = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const int s = i % kStages3;
@@ -528,81 +628,117 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
                 mbar_expect_tx(&full[s], stage_bytes);
                 uint8_t *dst = s_a + (size_t)s * stage_bytes;
 #pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    const int64_t off = ((int64_t)g * L.gstride + L.margin + q_lo) * 4;
-                    bulk_g2s(dst + (size_t)g * npix * 16, L.in_hi + off, (uint32_t)npix * 16, &full[s]);
-                    bulk_g2s(dst + half_bytes + (size_t)g * npix * 16, L.in_lo + off, (uint32_t)npix * 16, &full[s]);
+                for (int g = 0; g < 2 * NH; ++g) {  // hi groups 0..3, lo groups 4..7
+                    const int64_t off = ((int64_t)g * L.gstride + L.margin + q_lo) * 8;
+                    bulk_g2s(dst + (size_t)g * npix * 16, L.in + off, (uint32_t)npix * 16, &full[s]);
                 }
+            }
+        }
+    } else if (warp == 10) {
+        // residual producer: the block input rows of tile i (8 fp32 groups x
+        // 128 rows) into buffer i % 2 for the epilogue group that owns it
+        if (has_res && lane == 0) {
+            int i = 0;
+            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const int a = i & 1;
+                const int u = i >> 1;
+                if (u > 0) mbar_wait(&rempty[a], (u - 1) & 1);
+                mbar_expect_tx(&rfull[a], 8 * 128 * 16);
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                    bulk_g2s(s_res + (a * 8 + g) * 128, L.res + ((int64_t)g * L.gstride + L.margin + t * 128) * 4,
+                             128 * 16, &rfull[a]);
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // per K step: D[0:64] += A_hi x [B_hi | B_lo]; D[0:32] += A_lo x B_hi.
-            // The epilogue adds D[0:32] + D[32:64]: A_hi B_hi + A_lo B_hi + A_hi B_lo.
-            constexpr uint32_t idesc64 = idesc_tf32(128, N2);
-            constexpr uint32_t idesc32 = idesc_tf32(128, N);
-            mbar_wait(wbar, 0);
+        // the whole warp runs the (warp-uniform) issue loop; one elected lane
+        // issues each MMA. Descriptors: base + offsets in 16-byte units (the
+        // address field cannot carry: smem addresses are < 2^18).
+        constexpr uint32_t idesc64 = idesc_f16(128, N2);
+        constexpr uint32_t idesc32 = idesc_f16(128, N);
+        mbar_wait(wbar, 0);
+        tc_fence_after();
+        const uint64_t dA0 = umma_desc(smem_u32(s_a), (uint32_t)npix * 16u, 128u);
+        const uint64_t dB0 = umma_desc(smem_u32(s_w), (uint32_t)N2 * 16u, 128u);
+        const uint32_t npx = (uint32_t)npix;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int s = i % kStages3;
+            const int a = i & 1;
+            const int u = i >> 1;
+            if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
+            mbar_wait(&full[s], (i / kStages3) & 1);
             tc_fence_after();
-            const uint32_t wb = smem_u32(s_w);
-            int i = 0;
-            for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-                const int s = i % kStages3;
-                const int a = i & 1;
-                const int u = i >> 1;
-                if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
-                mbar_wait(&full[s], (i / kStages3) & 1);
-                tc_fence_after();
-                const uint32_t ahi = smem_u32(s_a + (size_t)s * stage_bytes);
-                const uint32_t alo = ahi + half_bytes;
-                const uint32_t d = tmem + (uint32_t)(a * N2);
-                uint32_t acc = 0;
-#pragma unroll 1
-                for (int tap = 0; tap < KS * KS; ++tap) {
-                    const int ti = tap / KS, tj = tap % KS;
-                    const uint32_t off = KS == 3 ? (uint32_t)(ti * Wp + tj) * 16u : 0u;
+            const uint64_t dAh = dA0 + (uint64_t)((uint32_t)s * (stage_bytes >> 4));
+            const uint64_t dAl = dAh + (uint64_t)(h_bytes >> 4);
+            const uint32_t d = tmem + (uint32_t)(a * N2);
 #pragma unroll
-                    for (int ks = 0; ks < NG / 2; ++ks) {
-                        const uint32_t ao = (uint32_t)(2 * ks) * npix * 16u + off;
-                        const uint32_t bo = (uint32_t)(tap * NG + 2 * ks) * N2 * 16u;
-                        const uint64_t dah = umma_desc(ahi + ao, (uint32_t)npix * 16u, 128u);
-                        const uint64_t dal = umma_desc(alo + ao, (uint32_t)npix * 16u, 128u);
-                        const uint64_t db = umma_desc(wb + bo, (uint32_t)N2 * 16u, 128u);
-                        mma_tf32(d, dah, db, idesc64, acc);
-                        mma_tf32(d, dal, db, idesc32, 1u);
-                        acc = 1u;
-                    }
+            for (int tap = 0; tap < KS * KS; ++tap) {
+                const uint32_t off = KS == 3 ? (uint32_t)((tap / KS) * Wp + tap % KS) : 0u;
+#pragma unroll
+                for (int ks = 0; ks < NH / 2; ++ks) {
+                    const uint64_t ao = (uint64_t)(2u * ks * npx + off);
+                    const uint64_t bo = (uint64_t)((tap * NH + 2 * ks) * N2);
+                    mma_f16_elect(d, dAh + ao, dB0 + bo, idesc64, (tap | ks) ? 1u : 0u);  // D[0:32] += h hw, D[32:64] += h lw
+                    mma_f16_elect(d + N, dAl + ao, dB0 + bo, idesc32, 1u);                // D[32:64] += l hw
                 }
-                mma_commit(&empty[s]);
-                mma_commit(&tfull[a]);
             }
+            mma_commit_elect(&empty[s]);
+            mma_commit_elect(&tfull[a]);
         }
     } else {
+        // two epilogue groups of four warps (one per TMEM lane quarter);
+        // group g owns the tiles with i % 2 == g and accumulator buffer g
+        const int grp = (warp - 2) >> 2;
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int H = L.H, W = L.W;
-        const FastDiv div_hw{(uint32_t)(L.Hp * Wp), (uint32_t)(0x100000000ull / (uint32_t)(L.Hp * Wp))};
+        const uint32_t img_px = (uint32_t)(L.Hp * Wp);
+        const FastDiv div_hw{img_px, (uint32_t)(0x100000000ull / img_px)};
         const FastDiv div_w{(uint32_t)Wp, (uint32_t)(0x100000000ull / (uint32_t)Wp)};
+        const int kw = __float_as_int(L.meta[0]);
+        const float l1 = L.meta[1], bmax = L.meta[2];
         float bias[N];
 #pragma unroll
         for (int c = 0; c < N; ++c) bias[c] = L.bias[c];
-        int i = 0;
-        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int a = i & 1;
+        // per-row image scalars are fetched one tile ahead
+        int kx_n = 0;
+        uint32_t mx_n = 0, mr_n = 0;
+        auto fetch = [&](int64_t t) {
+            const uint32_t q = (uint32_t)t * 128u + (uint32_t)row;
+            const uint32_t n = fdiv(q, div_hw);
+            if (t < n_tiles && n < (uint64_t)L.n_img) {
+                kx_n = L.kx_in[n];
+                if constexpr (MODE == TC3_ACT) {
+                    mx_n = L.mx_in[n];
+                    if (L.res) mr_n = L.mx_res[n];
+                }
+            }
+        };
+        int i = grp;
+        int64_t t = blockIdx.x + (int64_t)grp * gridDim.x;
+        fetch(t);
+        for (; t < n_tiles; t += 2 * (int64_t)gridDim.x, i += 2) {
+            const int a = grp;
             const int u = i >> 1;
             const uint32_t q = (uint32_t)t * 128u + (uint32_t)row;
             const uint32_t n = fdiv(q, div_hw);
             const uint32_t rem = q - n * div_hw.d;
             const int y = (int)fdiv(rem, div_w), x = (int)(rem - (uint32_t)y * div_w.d);
             const bool valid = n < (uint64_t)L.n_img && y >= 1 && y <= H && x >= 1 && x <= W;
-            float4 rh[MODE == TC3_ACT ? NG : 1], rl[MODE == TC3_ACT ? NG : 1];
-            if constexpr (MODE == TC3_ACT) {
-                if (L.res_hi && valid) {
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        const int64_t ro = (int64_t)g * L.gstride + L.margin + q;
-                        rh[g] = reinterpret_cast<const float4 *>(L.res_hi)[ro];
-                        rl[g] = reinterpret_cast<const float4 *>(L.res_lo)[ro];
-                    }
+            const int kxi = kx_n;
+            const uint32_t mxi = mx_n, mri = mr_n;
+            fetch(t + 2 * (int64_t)gridDim.x);
+            float inv = 1.f, osc = 1.f;
+            int ko = 0;
+            if (valid) {
+                inv = exp2i(-kxi - kw);
+                if constexpr (MODE == TC3_ACT) {
+                    // rigorous bound on |out| for this image -> output scale 2^ko
+                    float bound = __fadd_rn(__fmul_rn(__uint_as_float(mxi), l1), bmax);
+                    if (L.res) bound = __fadd_rn(bound, __uint_as_float(mri));
+                    ko = act_exp(__float_as_uint(bound));
+                    osc = exp2i(ko);
                 }
             }
             mbar_wait(&tfull[a], u & 1);
@@ -614,57 +750,83 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
                 tmem_ld32(taddr, v);
                 tmem_ld32(taddr + 32, w);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) v[c] = __fadd_rn(v[c], w[c]);
+                for (int c = 0; c < 32; ++c)  // products by powers of two are exact: 2 roundings, as unfused
+                    v[c] = __fmaf_rn(__fmaf_rn(w[c], 0.00048828125f, v[c]), inv, bias[c]);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[a]);
-            if (!valid) continue;
             if constexpr (MODE == TC3_ACT) {
+                float mx = 0.f;
+                if (has_res) mbar_wait(&rfull[a], u & 1);
+                if (valid) {
 #pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    float o[4];
+                    for (int g = 0; g < 8; ++g) {
+                        if (has_res) {
+                            const float4 r = s_res[(a * 8 + g) * 128 + row];
+                            v[4 * g + 0] = __fadd_rn(r.x, v[4 * g + 0]);
+                            v[4 * g + 1] = __fadd_rn(r.y, v[4 * g + 1]);
+                            v[4 * g + 2] = __fadd_rn(r.z, v[4 * g + 2]);
+                            v[4 * g + 3] = __fadd_rn(r.w, v[4 * g + 3]);
+                        }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) o[e] = __fadd_rn(v[4 * g + e], bias[4 * g + e]);
-                    if (L.res_hi) {
-                        o[0] = __fadd_rn(__fadd_rn(rh[g].x, rl[g].x), o[0]);
-                        o[1] = __fadd_rn(__fadd_rn(rh[g].y, rl[g].y), o[1]);
-                        o[2] = __fadd_rn(__fadd_rn(rh[g].z, rl[g].z), o[2]);
-                        o[3] = __fadd_rn(__fadd_rn(rh[g].w, rl[g].w), o[3]);
+                        for (int e = 0; e < 4; ++e) {
+                            if (L.relu) v[4 * g + e] = fmaxf(v[4 * g + e], 0.f);
+                            mx = fmaxf(mx, fabsf(v[4 * g + e]));
+                        }
+                        if (L.out32) {
+                            const int64_t so = ((int64_t)g * L.gstride + L.margin) * 4;
+                            store_px4(L.out32 + so, q, make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]),
+                                      y, x, H, W, Wp);
+                        }
                     }
-                    if (L.relu) {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) o[e] = fmaxf(o[e], 0.f);
+                    for (int j = 0; j < NH; ++j) {
+                        uint4 h, l;
+                        split2(__fmul_rn(v[8 * j + 0], osc), __fmul_rn(v[8 * j + 1], osc), h.x, l.x);
+                        split2(__fmul_rn(v[8 * j + 2], osc), __fmul_rn(v[8 * j + 3], osc), h.y, l.y);
+                        split2(__fmul_rn(v[8 * j + 4], osc), __fmul_rn(v[8 * j + 5], osc), h.z, l.z);
+                        split2(__fmul_rn(v[8 * j + 6], osc), __fmul_rn(v[8 * j + 7], osc), h.w, l.w);
+                        store_px(L.out + ((int64_t)j * L.gstride + L.margin) * 8, q, h, y, x, H, W, Wp);
+                        store_px(L.out + ((int64_t)(NH + j) * L.gstride + L.margin) * 8, q, l, y, x, H, W, Wp);
                     }
-                    float hi[4], lo[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        hi[e] = tf32_rna(o[e]);
-                        lo[e] = __fsub_rn(o[e], hi[e]);
+                }
+                if (has_res) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&rempty[a]);
+                }
+                // per-image exact max |out| and the output scale: one write
+                // per warp when the warp's rows share an image
+                const uint32_t n_ref = __shfl_sync(0xFFFFFFFFu, n, 0);
+                const bool same = __all_sync(0xFFFFFFFFu, n == n_ref && valid);
+                if (same) {
+                    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(mx));
+                    if (lane == 0) {
+                        if (m != 0u) atomicMax(L.mx_out + n_ref, m);
+                        L.kx_out[n_ref] = ko;
                     }
-                    // residual already in registers: store as we go
-                    const int64_t so = ((int64_t)g * L.gstride + L.margin) * 4;
-                    store_px4(L.out_hi + so, q, make_float4(hi[0], hi[1], hi[2], hi[3]), y, x, H, W, Wp);
-                    store_px4(L.out_lo + so, q, make_float4(lo[0], lo[1], lo[2], lo[3]), y, x, H, W, Wp);
+                } else if (valid) {
+                    if (mx != 0.f) atomicMax(L.mx_out + n, __float_as_uint(mx));
+                    L.kx_out[n] = ko;
                 }
             } else {
+                if (!valid) continue;
                 // z = acc + bias, written as tf32 hi / fp32 lo into 128-latent
                 // tiles in the UMMA K-major layout the argmin GEMM reads
                 const int64_t vix = ((int64_t)n * H + (y - 1)) * (int64_t)W + (x - 1);
                 float4 *zo = L.z ? reinterpret_cast<float4 *>(L.z + vix * 32) : nullptr;
-                float4 *zt = reinterpret_cast<float4 *>(L.zt) + (vix >> 7) * (2 * NG * 128) + (vix & 127);
+                float4 *zt = reinterpret_cast<float4 *>(L.zt) + (vix >> 7) * (2 * 8 * 128) + (vix & 127);
 #pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    float zz[4], hi[4], lo[4];
+                for (int g = 0; g < 8; ++g) {
+                    float hi[4], lo[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        zz[e] = __fadd_rn(v[4 * g + e], bias[4 * g + e]);
-                        hi[e] = tf32_rna(zz[e]);
-                        lo[e] = __fsub_rn(zz[e], hi[e]);
+                        hi[e] = tf32_rna(v[4 * g + e]);
+                        lo[e] = __fsub_rn(v[4 * g + e], hi[e]);
                     }
-                    if (zo) zo[g] = make_float4(zz[0], zz[1], zz[2], zz[3]);
+                    if (zo) zo[g] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
                     zt[g * 128] = make_float4(hi[0], hi[1], hi[2], hi[3]);
-                    zt[(NG + g) * 128] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                    zt[(8 + g) * 128] = make_float4(lo[0], lo[1], lo[2], lo[3]);
                 }
             }
         }
@@ -679,10 +841,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc3_conv_kernel(Tc3Layer L) {
 
 template <int KS, int MODE>
 int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
-    constexpr int NG = 8;
-    constexpr int KG = KS * KS * NG;
+    constexpr int KG = KS * KS * 4;
     const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
-    const size_t smem = (size_t)KG * 64 * 16 + (size_t)kStages3 * 2 * NG * npix * 16 + 8 * (2 * kStages3 + 5) + 16;
+    const size_t smem = (size_t)KG * 64 * 16 + (size_t)kStages3 * 8 * npix * 16 + (L.res ? 2 * 8 * 128 * 16 : 0) +
+                        8 * (2 * kStages3 + 9) + 16;
     if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     auto kern = tc3_conv_kernel<KS, MODE>;
@@ -694,7 +856,7 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
     if (grid < 1) return PILC_OK;
     const double flops = 2.0 * L.n_img * L.H * L.W * 32.0 * 32 * KS * KS;
     ProfScope _ps(PROF_TC3_CONV, s, flops);
-    kern<<<(unsigned)grid, kThreadsTC, smem, s>>>(L);
+    kern<<<(unsigned)grid, kThreadsTC3, smem, s>>>(L);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

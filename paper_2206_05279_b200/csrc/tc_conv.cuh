@@ -26,22 +26,31 @@ struct TcLayer {
     float log_s_min, log_s_max;
 };
 
-// 3xTF32 encoder layers: activations are fp32 split into a tf32 "hi" slab
-// and an fp32 "lo" residual slab, 4 channels (16 B) per group, same padded
-// group-major pixel indexing as the bf16 path.
+// Encoder layers (3-product fp16 split, tc_conv.cu). Operands: the scaled
+// fp16 hi / lo slab sets of a tensor (8-channel groups, 16 B per pixel: hi
+// groups 0..3 then lo groups 4..7), padded group-major like the bf16 path;
+// block outputs also as an fp32 slab set (4-channel groups) for the exact
+// residual. kx / mx: per-image scale exponent and exact max |x| (float bits).
 enum Tc3Mode { TC3_ACT = 0, TC3_Z = 1 };
 
 struct Tc3Layer {
-    const float *in_hi, *in_lo;
+    const uint16_t *in;  // hi / lo slabs of the input
     int64_t gstride, margin;
     int Hp, Wp, H, W;
     int64_t n_img, n_tiles;
-    const float *w_hi, *w_lo;  // B operand hi/lo, [KG][N][4] fp32
+    const uint16_t *w;   // B operand [KG][64][8] fp16: rows 0..31 = hi(w 2^kw), 32..63 = lo
+    const float *meta;   // {kw (int bits), L1 = max_co sum|w|, max|b|}
+    const int32_t *kx_in;
+    const uint32_t *mx_in;
     const float *bias;
-    const float *res_hi, *res_lo;  // TC3_ACT residual (nullable)
-    float *out_hi, *out_lo;        // TC3_ACT
-    float *z;                      // TC3_Z: (n, H, W, 32) fp32 (nullable)
-    float *zt;                     // TC3_Z: 128-latent tiles [tile][hi|lo][8][128][4]
+    const float *res;         // TC3_ACT residual fp32 slab (nullable)
+    const uint32_t *mx_res;   // with res
+    uint16_t *out;            // TC3_ACT hi / lo slabs of the output
+    float *out32;             // TC3_ACT fp32 copy (nullable)
+    int32_t *kx_out;
+    uint32_t *mx_out;         // atomicMax; zeroed by the caller
+    float *z;                 // TC3_Z: (n, H, W, 32) fp32 (nullable)
+    float *zt;                // TC3_Z: 128-latent tiles [tile][hi|lo][8][128][4]
     int relu;
 };
 

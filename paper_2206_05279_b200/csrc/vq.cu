@@ -20,6 +20,8 @@
 #include "common.cuh"
 #include "tc_conv.cuh"
 #include "enc_front.cuh"
+#include <cuda_fp16.h>
+#include <cmath>
 
 namespace {
 
@@ -46,11 +48,13 @@ struct Layout {
     bool tc;
     std::vector<int64_t> tc_blk;  // 2B block convs, N = 32
     int64_t tc_up, tc_head;       // N = 128, N = 16 (mu 0..2, s 3..5)
-    // 3xTF32 encoder (C == 32, Dc == 32): B operands hi / lo, [KG][32][4]
-    // fp32, float offsets; lo follows hi
+    // tcgen05 encoder (C == 32, Dc == 32): fp16-split B operands
+    // [KG][64][8] (rows 0..31 hi, 32..63 lo of w 2^kw), float offsets;
+    // tf_meta: per block conv / proj {kw (int), L1, max|b|, 0}, then
+    // {k0 (int): scale exponent of the encoder front's output, 0, 0, 0}
     bool tf;
     std::vector<int64_t> tf_blk;
-    int64_t tf_proj;
+    int64_t tf_proj, tf_meta;
     int64_t tf_cb;  // argmin GEMM B operand [hi|lo][8][256][4] fp32 (codes >= K zero)
     int64_t total;                // floats, bf16 region included
 };
@@ -106,10 +110,12 @@ Layout make_layout(int K, int Dc, int C, int B) {
         cur = (cur + 7) / 8 * 8;
         for (int i = 0; i < 2 * B; ++i) {
             L.tf_blk.push_back(cur);
-            cur += 2 * 72 * 32 * 4;
+            cur += 36 * 64 * 8 / 2;
         }
         L.tf_proj = cur;
-        cur += 2 * 8 * 32 * 4;
+        cur += 4 * 64 * 8 / 2;
+        L.tf_meta = cur;
+        cur += 4 * (2 * B + 2);
         L.tf_cb = cur;
         cur += 2 * 8 * 256 * 4;
     }
@@ -119,7 +125,7 @@ Layout make_layout(int K, int Dc, int C, int B) {
 
 // ---- conv kernel -----------------------------------------------------------
 enum InMode { IN_F32 = 0, IN_U8 = 1, IN_CODEBOOK = 2 };
-enum OutMode { OUT_F32 = 0, OUT_SHUFFLE = 1, OUT_HEAD = 2, OUT_TFSPLIT = 3 };
+enum OutMode { OUT_F32 = 0, OUT_SHUFFLE = 1, OUT_HEAD = 2 };
 
 struct ConvArgs {
     const float *in;
@@ -144,9 +150,6 @@ struct ConvArgs {
     const double *thresh;
     int n_thresh;
     float log_s_min, log_s_max;
-    // OUT_TFSPLIT: tf32 hi / fp32 lo slabs, padded group-major (tc_conv.cu)
-    float *out_hi, *out_lo;
-    int64_t out_gstride, out_margin;
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -158,20 +161,6 @@ __device__ __forceinline__ float sigmoid_f32(float x) {
     return __fdiv_rn(e, __fadd_rn(1.f, e));
 }
 
-__device__ __forceinline__ void store_px4s(float *slab, int64_t q, float4 v, int y, int x, int H, int W, int Wp) {
-    float4 *p = reinterpret_cast<float4 *>(slab);
-    p[q] = v;
-    const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
-    const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
-    if (dy) p[q - Wp] = v;
-    if (dy2) p[q + Wp] = v;
-    if (dx) p[q - 1] = v;
-    if (dx2) p[q + 1] = v;
-    if (dy && dx) p[q - Wp - 1] = v;
-    if (dy && dx2) p[q - Wp + 1] = v;
-    if (dy2 && dx) p[q + Wp - 1] = v;
-    if (dy2 && dx2) p[q + Wp + 1] = v;
-}
 
 template <int CO_T>
 __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
@@ -305,24 +294,6 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
                 const int cc = co >> 2, dy = (co >> 1) & 1, dx = co & 1;
                 const float v = fmaxf(__fadd_rn(acc[c], a.b[co]), 0.f);
                 a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = v;
-            }
-        } else if (a.out_mode == OUT_TFSPLIT) {
-            // bias + ReLU, then split into the 3xTF32 encoder layout
-            const int Wp = a.Wo + 2;
-            const int64_t q = ((int64_t)n * (a.Ho + 2) + oy + 1) * Wp + ox + 1;
-#pragma unroll
-            for (int g = 0; g < CO_T / 4; ++g) {
-                float hi[4], lo[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float v = __fadd_rn(acc[4 * g + e], a.b[co0 + 4 * g + e]);
-                    if (a.relu) v = fmaxf(v, 0.f);
-                    hi[e] = __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);  // tf32 rna
-                    lo[e] = __fsub_rn(v, hi[e]);
-                }
-                const int64_t so = ((int64_t)((co0 >> 2) + g) * a.out_gstride + a.out_margin) * 4;
-                store_px4s(a.out_hi + so, q, make_float4(hi[0], hi[1], hi[2], hi[3]), oy + 1, ox + 1, a.Ho, a.Wo, Wp);
-                store_px4s(a.out_lo + so, q, make_float4(lo[0], lo[1], lo[2], lo[3]), oy + 1, ox + 1, a.Ho, a.Wo, Wp);
             }
         } else {
             // logistic head (vqvae.py:105-112, logistic.py:36-40, 109-114)
@@ -600,31 +571,41 @@ int64_t tc_ws(int64_t n, int H, int W, TcWork *w, char *base) {
     return 3 * slab + slab2 + al(256 * 32 * 2);
 }
 
-// 3xTF32 encoder scratch: full-res stem output (NHWC fp32), three latent
-// tensors as hi/lo slab pairs (8 groups x gstride x 16 B each), z.
+// tcgen05 encoder scratch: two fp32 slab sets (block outputs, 8 groups x
+// gstride x 16 B), three fp16 hi / lo slab sets (same size), z, z tiles,
+// per-image max |x| and scale exponent of the 2B+1 conv inputs.
 struct TfWork {
-    float *A, *Xh, *Xl, *Th, *Tl, *Yh, *Yl, *Z, *ZT;
+    float *X32, *Y32;
+    uint16_t *XH, *YH, *TH;
+    float *Z, *ZT;
+    uint32_t *mx;
+    int32_t *kx;
     int64_t gs, margin;
 };
 
-int64_t tf_ws(int64_t n, int H, int W, TfWork *w, char *base) {
+int64_t tf_ws(int64_t n, int H, int W, int B, TfWork *w, char *base) {
     const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
     const int64_t Wp = gw + 2;
     const int64_t m1 = 256 + 2 * Wp;
     const int64_t gs = 2 * m1 + n * (gh + 2) * Wp;
     auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
-    const int64_t a = 256, slab = al(8 * gs * 16), z = al(n * gh * gw * 32 * 4);
+    const int64_t slab = al(8 * gs * 16), z = al(n * gh * gw * 32 * 4);
     const int64_t zt = al(((n * gh * gw + 127) / 128) * 128 * 32 * 4 * 2);
+    const int64_t mx = al((2 * B + 1) * n * 4);
     if (w) {
-        w->A = reinterpret_cast<float *>(base);
-        float **sl[6] = {&w->Xh, &w->Xl, &w->Th, &w->Tl, &w->Yh, &w->Yl};
-        for (int i = 0; i < 6; ++i) *sl[i] = reinterpret_cast<float *>(base + a + i * slab);
-        w->Z = reinterpret_cast<float *>(base + a + 6 * slab);
-        w->ZT = reinterpret_cast<float *>(base + a + 6 * slab + z);
+        w->X32 = reinterpret_cast<float *>(base);
+        w->Y32 = reinterpret_cast<float *>(base + slab);
+        w->XH = reinterpret_cast<uint16_t *>(base + 2 * slab);
+        w->YH = reinterpret_cast<uint16_t *>(base + 3 * slab);
+        w->TH = reinterpret_cast<uint16_t *>(base + 4 * slab);
+        w->Z = reinterpret_cast<float *>(base + 5 * slab);
+        w->ZT = reinterpret_cast<float *>(base + 5 * slab + z);
+        w->mx = reinterpret_cast<uint32_t *>(base + 5 * slab + z + zt);
+        w->kx = reinterpret_cast<int32_t *>(base + 5 * slab + z + zt + mx);
         w->gs = gs;
         w->margin = m1;
     }
-    return a + 6 * slab + z + zt;
+    return 5 * slab + z + zt + 2 * mx;
 }
 
 bool check_cfg(int K, int Dc, int C, int B) {
@@ -695,21 +676,68 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
             memcpy(&r, &u, 4);
             return r;
         };
-        // B' layout [K/4][64][4]: rows 0..31 = tf32 hi, rows 32..63 = lo
+        // B' layout [K/8][64][8] fp16: rows 0..31 = h = fp16(w 2^kw), rows
+        // 32..63 = l = fp16((w 2^kw - h) 2^11); kw puts max |w 2^kw| below 2^15
+        float *meta = dst + L.tf_meta;
+        int n_kw = 0;
+        // L1 = max over output channels of sum |w| (rounded up), max |b|
+        auto l1_of = [&](const ConvSpec &sp, float &l1, float &bm) {
+            double best = 0.0;
+            bm = 0.f;
+            for (int n = 0; n < sp.co; ++n) {
+                double acc = 0.0;
+                for (int ci = 0; ci < sp.ci; ++ci)
+                    for (int tap = 0; tap < sp.ks * sp.ks; ++tap)
+                        acc += std::fabs((double)dst[sp.w_off + ((int64_t)tap * sp.ci_pad + ci) * sp.co_pad + n]);
+                best = acc > best ? acc : best;
+                bm = fmaxf(bm, fabsf(dst[sp.b_off + n]));
+            }
+            l1 = (float)(best * (1.0 + 1e-6));
+        };
         auto put_t = [&](int64_t off, const ConvSpec &sp) {
             const int taps = sp.ks * sp.ks;
+            float mx = 0.f;
+            for (int n = 0; n < 32; ++n)
+                for (int ci = 0; ci < 32; ++ci)
+                    for (int tap = 0; tap < taps; ++tap)
+                        mx = fmaxf(mx, fabsf(dst[sp.w_off + ((int64_t)tap * sp.ci_pad + ci) * sp.co_pad + n]));
+            int kw = 0;
+            if (mx > 0.f && std::isfinite(mx)) kw = 14 - std::ilogb(mx);
+            kw = kw < -30 ? -30 : (kw > 30 ? 30 : kw);
+            float l1, bm;
+            l1_of(sp, l1, bm);
+            int32_t kwi = kw;
+            memcpy(meta + 4 * n_kw, &kwi, 4);
+            meta[4 * n_kw + 1] = l1;
+            meta[4 * n_kw + 2] = bm;
+            ++n_kw;
+            const float sc = std::ldexp(1.f, kw);
+            uint16_t *h = reinterpret_cast<uint16_t *>(dst + off);
             for (int n = 0; n < 32; ++n)
                 for (int ci = 0; ci < 32; ++ci)
                     for (int tap = 0; tap < taps; ++tap) {
                         const int k = tap * 32 + ci;
-                        const float w = dst[sp.w_off + ((int64_t)tap * sp.ci_pad + ci) * sp.co_pad + n];
-                        const float hi = tf32(w);
-                        dst[off + ((int64_t)(k >> 2) * 64 + n) * 4 + (k & 3)] = hi;
-                        dst[off + ((int64_t)(k >> 2) * 64 + 32 + n) * 4 + (k & 3)] = w - hi;
+                        const float w = dst[sp.w_off + ((int64_t)tap * sp.ci_pad + ci) * sp.co_pad + n] * sc;
+                        const __half wh = __float2half_rn(w);
+                        const __half wl = __float2half_rn((w - __half2float(wh)) * 2048.f);
+                        h[((int64_t)(k >> 3) * 64 + n) * 8 + (k & 7)] = __half_as_ushort(wh);
+                        h[((int64_t)(k >> 3) * 64 + 32 + n) * 8 + (k & 7)] = __half_as_ushort(wl);
                     }
         };
         for (int i = 0; i < 2 * B; ++i) put_t(L.tf_blk[i], L.enc[2 + i]);
         put_t(L.tf_proj, L.enc[2 + 2 * B]);
+        {
+            // static bound of the encoder front's output (input in [-1, 1])
+            float l1s, bms, l1d, bmd;
+            l1_of(L.enc[0], l1s, bms);
+            l1_of(L.enc[1], l1d, bmd);
+            const double bound = (double)l1d * ((double)l1s + bms) + bmd;
+            int k0 = 0;
+            if (bound > 0.0 && std::isfinite(bound)) k0 = 14 - std::ilogb(bound * (1.0 + 1e-6));
+            k0 = k0 < -90 ? -90 : (k0 > 90 ? 90 : k0);
+            int32_t k0i = k0;
+            memcpy(meta + 4 * (2 * B + 1), &k0i, 4);
+        }
         for (int k = 0; k < K; ++k)
             for (int c = 0; c < 32; ++c) {
                 const float w = dst[L.cb_off + (int64_t)k * 32 + c];
@@ -726,7 +754,7 @@ extern "C" int64_t pilc_vq_workspace_bytes(int64_t n_img, int32_t H, int32_t W, 
     if (n_img < 0 || H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return -1;
     const int64_t a = ws_parts(n_img, H, W, Dc, C, nullptr, nullptr);
     const int64_t b = C == 32 ? tc_ws(n_img, H, W, nullptr, nullptr) : 0;
-    const int64_t c = (C == 32 && Dc == 32) ? tf_ws(n_img, H, W, nullptr, nullptr) : 0;
+    const int64_t c = (C == 32 && Dc == 32) ? tf_ws(n_img, H, W, B, nullptr, nullptr) : 0;
     const int64_t m = a > b ? a : b;
     return m > c ? m : c;
 }
@@ -817,10 +845,14 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
     f.b_down = model + L.enc[1].b_off;
     f.down_ci_pad = L.enc[1].ci_pad;
     f.down_co_pad = L.enc[1].co_pad;
-    f.out_hi = w.Xh;
-    f.out_lo = w.Xl;
+    f.out32 = w.X32;
+    f.out = w.XH;
+    f.out_max = w.mx;
+    f.kx_out = w.kx;
+    f.k0 = reinterpret_cast<const int32_t *>(model + L.tf_meta + 4 * (2 * B + 1));
     f.gstride = w.gs;
     f.margin = w.margin;
+    if (cudaMemsetAsync(w.mx, 0, (size_t)(2 * B + 1) * n_img * 4, s) != cudaSuccess) return PILC_E_CUDA;
     if ((rc = enc_front_launch(f, s))) return rc;
     Tc3Layer b;
     memset(&b, 0, sizeof(b));
@@ -833,40 +865,48 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
     b.n_img = n_img;
     b.n_tiles = ceil_div64(n_img * b.Hp * (int64_t)b.Wp, 128);
     b.relu = 1;
-    float *Xh = w.Xh, *Xl = w.Xl, *Yh = w.Yh, *Yl = w.Yl;
-    const int64_t half3 = 72 * 32 * 4, half1 = 8 * 32 * 4;
+    float *X32 = w.X32, *Y32 = w.Y32;
+    uint16_t *XH = w.XH, *YH = w.YH;
+    const float *meta = model + L.tf_meta;
     for (int i = 0; i < B; ++i) {
-        Tc3Layer c1 = b;
-        c1.in_hi = Xh;
-        c1.in_lo = Xl;
-        c1.out_hi = w.Th;
-        c1.out_lo = w.Tl;
-        c1.w_hi = model + L.tf_blk[2 * i];
-        c1.w_lo = c1.w_hi + half3;
+        Tc3Layer c1 = b;  // T = relu(conv1(X))
+        c1.in = XH;
+        c1.kx_in = w.kx + (2 * i) * n_img;
+        c1.mx_in = w.mx + (2 * i) * n_img;
+        c1.out = w.TH;
+        c1.kx_out = w.kx + (2 * i + 1) * n_img;
+        c1.mx_out = w.mx + (2 * i + 1) * n_img;
+        c1.w = reinterpret_cast<const uint16_t *>(model + L.tf_blk[2 * i]);
+        c1.meta = meta + 4 * (2 * i);
         c1.bias = model + L.enc[2 + 2 * i].b_off;
         if ((rc = tc3_launch(c1, 3, TC3_ACT, s))) return rc;
-        Tc3Layer c2 = b;
-        c2.in_hi = w.Th;
-        c2.in_lo = w.Tl;
-        c2.res_hi = Xh;
-        c2.res_lo = Xl;
-        c2.out_hi = Yh;
-        c2.out_lo = Yl;
-        c2.w_hi = model + L.tf_blk[2 * i + 1];
-        c2.w_lo = c2.w_hi + half3;
+        Tc3Layer c2 = b;  // X' = relu(X + conv2(T))
+        c2.in = w.TH;
+        c2.kx_in = c1.kx_out;
+        c2.mx_in = c1.mx_out;
+        c2.res = X32;
+        c2.mx_res = c1.mx_in;
+        c2.out = YH;
+        c2.out32 = i + 1 < B ? Y32 : nullptr;
+        c2.kx_out = w.kx + (2 * i + 2) * n_img;
+        c2.mx_out = w.mx + (2 * i + 2) * n_img;
+        c2.w = reinterpret_cast<const uint16_t *>(model + L.tf_blk[2 * i + 1]);
+        c2.meta = meta + 4 * (2 * i + 1);
         c2.bias = model + L.enc[3 + 2 * i].b_off;
         if ((rc = tc3_launch(c2, 3, TC3_ACT, s))) return rc;
-        float *th = Xh, *tl = Xl;
-        Xh = Yh;
-        Xl = Yl;
-        Yh = th;
-        Yl = tl;
+        float *t32 = X32;
+        X32 = Y32;
+        Y32 = t32;
+        uint16_t *th = XH;
+        XH = YH;
+        YH = th;
     }
     Tc3Layer pj = b;  // proj 1x1 -> z tiles (+ plain z when asked)
-    pj.in_hi = Xh;
-    pj.in_lo = Xl;
-    pj.w_hi = model + L.tf_proj;
-    pj.w_lo = pj.w_hi + half1;
+    pj.in = XH;
+    pj.kx_in = w.kx + (2 * B) * n_img;
+    pj.mx_in = w.mx + (2 * B) * n_img;
+    pj.w = reinterpret_cast<const uint16_t *>(model + L.tf_proj);
+    pj.meta = meta + 4 * (2 * B);
     pj.bias = model + L.enc[2 + 2 * B].b_off;
     pj.relu = 0;
     pj.z = z_out;
@@ -891,7 +931,7 @@ int vq_encode(int path, const uint8_t *img, int64_t n_img, int32_t H, int32_t W,
     cudaStream_t s = as_stream(stream);
     if (path == 0 && L.tf) {
         TfWork tw;
-        if (tf_ws(n_img, H, W, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+        if (tf_ws(n_img, H, W, B, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
         return tf_encode(img, n_img, H, W, model, K, Dc, B, L, tw, idx_out, z_out, s);
     }
     Work w;

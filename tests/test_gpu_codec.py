@@ -196,11 +196,12 @@ def test_vqvae_encoder_and_decoder_vs_reference(golden, tag, small_model, full_m
     assert agree == total, f"index agreement {agree}/{total}"
 
 
-def test_tf32x3_encoder_vs_fp32(golden, full_model):
-    """Production encoder of the default model: 3xTF32 tcgen05 block convs
-    (hi/lo split, three MMAs per K step). z must stay fp32-class (compared
-    with the fp32 SIMT kernels and with the reference's numpy/BLAS z) and the
-    codebook indices must equal the reference's."""
+def test_fp16x3_encoder_vs_fp32(golden, full_model):
+    """Production encoder of the default model: tcgen05 block convs as a
+    3-product fp16 split with per-image power-of-two scales (csrc/tc_conv.cu).
+    z must stay fp32-class (compared with the fp32 SIMT kernels and with the
+    reference's numpy/BLAS z) and the codebook indices must equal the
+    reference's."""
     z = golden("vqvae_full.npz")
     imgs = list(smooth_images(24, 32, 32, seed=77))
     for k in range(int(z["n"])):
