@@ -30,25 +30,28 @@ __device__ __forceinline__ uint32_t vbyte(const uint4 &v, int j) {
     return (w >> (8 * (j & 3))) & 0xFFu;
 }
 
+// ---- encoder --------------------------------------------------------------
+// The state chain per symbol is four integer ops (b = (delta + S) >> M;
+// S = (S >> b) + phi); the table word of every symbol depends only on (d, x)
+// and is fetched ahead of the chain. The bit output is branch-free: a 64-bit
+// accumulator, one predicated 32-bit store when 32 bits are complete.
 struct EncState {
-    uint32_t state;
+    uint32_t S;
     uint64_t acc;
-    int nacc;
+    uint32_t nacc;
     uint32_t words;
 };
 
-__device__ __forceinline__ void enc_step(EncState &e, const uint32_t *tab, int X, int M, uint32_t d,
-                                         uint32_t x, uint32_t *out) {
-    const uint32_t t = tab[d * X + x];
-    const uint32_t b = ((t & 0xFFFFu) + e.state) >> M;
-    e.acc |= (uint64_t)(e.state & ((1u << b) - 1u)) << e.nacc;
+__device__ __forceinline__ void enc_push(EncState &e, uint32_t t, int M, uint32_t *out) {
+    const uint32_t b = ((t & 0xFFFFu) + e.S) >> M;
+    e.acc |= (uint64_t)(e.S & ((1u << b) - 1u)) << e.nacc;
     e.nacc += b;
-    if (e.nacc >= 32) {
-        out[e.words++] = (uint32_t)e.acc;
-        e.acc >>= 32;
-        e.nacc -= 32;
-    }
-    e.state = (e.state >> b) + (t >> 16);
+    e.S = (e.S >> b) + (t >> 16);
+    const bool f = e.nacc >= 32u;
+    if (f) out[e.words] = (uint32_t)e.acc;
+    e.words += f ? 1u : 0u;
+    e.acc = f ? (e.acc >> 32) : e.acc;
+    e.nacc -= f ? 32u : 0u;
 }
 
 __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
@@ -75,131 +78,196 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
         const uint32_t dconst = d_img ? d_img[img] : 0u;
         uint32_t *out = scratch + k * lane_cap;
         EncState e{1u << M, 0, 0, 0};
-        auto scalar = [&](int i) {
-            const int64_t pos = base + (int64_t)i * lanes;
-            uint32_t x = syms[pos];
-            if (shift) x = (x - shift[pos] + 128u) & 0xFFu;
-            enc_step(e, tab, X, M, dsched ? dsched[pos] : dconst, x, out);
+        auto word = [&](uint32_t x, uint32_t h, uint32_t d) -> uint32_t {
+            if (shift) x = (x - h + 128u) & 0xFFu;
+            return tab[d * X + x];
         };
         int i = cnt - 1;
         if (lanes == 1) {
-            // reverse order; 16-byte vector loads over aligned chunks
-            for (; i >= 0 && ((base + i + 1) & 15); --i) scalar(i);
-            const uint4 z4 = make_uint4(0, 0, 0, 0);
-            uint4 sv = z4, hv = z4, dv = z4;
-            if (i >= 15) {
-                const int64_t p0 = base + i - 15;
-                sv = *reinterpret_cast<const uint4 *>(syms + p0);
-                if (shift) hv = *reinterpret_cast<const uint4 *>(shift + p0);
-                if (dsched) dv = *reinterpret_cast<const uint4 *>(dsched + p0);
+            // reverse order; 16-byte vector loads over aligned chunks, the
+            // previous chunk prefetched while this one is coded
+            for (; i >= 0 && ((base + i + 1) & 15); --i) {
+                const int64_t pos = base + i;
+                enc_push(e, word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst), M, out);
             }
-            for (; i >= 15; i -= 16) {
-                uint4 sn = z4, hn = z4, dn = z4;  // prefetch the previous chunk
-                if (i >= 31) {
-                    const int64_t pn = base + i - 31;
-                    sn = *reinterpret_cast<const uint4 *>(syms + pn);
-                    if (shift) hn = *reinterpret_cast<const uint4 *>(shift + pn);
-                    if (dsched) dn = *reinterpret_cast<const uint4 *>(dsched + pn);
+            // 16-symbol blocks, a register ring of four blocks: the inputs of
+            // block j + 4 are requested as soon as block j is coded (~64
+            // symbols ahead, longer than a DRAM round trip at this chain length)
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
+            auto ld = [&](int ii, uint4 &sv, uint4 &hv, uint4 &dv) {  // block with top symbol ii
+                if (ii >= 15) {
+                    const int64_t p0 = base + ii - 15;
+                    sv = *reinterpret_cast<const uint4 *>(syms + p0);
+                    if (shift) hv = *reinterpret_cast<const uint4 *>(shift + p0);
+                    if (dsched) dv = *reinterpret_cast<const uint4 *>(dsched + p0);
                 }
+            };
+            auto blk = [&](const uint4 &sv, const uint4 &hv, const uint4 &dv) {
+                uint32_t t[16];
 #pragma unroll
-                for (int j = 15; j >= 0; --j) {
-                    uint32_t x = vbyte(sv, j);
-                    if (shift) x = (x - vbyte(hv, j) + 128u) & 0xFFu;
-                    enc_step(e, tab, X, M, dsched ? vbyte(dv, j) : dconst, x, out);
+                for (int j = 0; j < 16; ++j)
+                    t[j] = word(vbyte(sv, j), vbyte(hv, j), dsched ? vbyte(dv, j) : dconst);
+#pragma unroll
+                for (int j = 15; j >= 0; --j) enc_push(e, t[j], M, out);
+            };
+            uint4 s0 = z4, s1 = z4, s2 = z4, s3 = z4, h0 = z4, h1 = z4, h2 = z4, h3 = z4;
+            uint4 d0 = z4, d1 = z4, d2 = z4, d3 = z4;
+            ld(i, s0, h0, d0);
+            ld(i - 16, s1, h1, d1);
+            ld(i - 32, s2, h2, d2);
+            ld(i - 48, s3, h3, d3);
+            for (; i >= 63; i -= 64) {
+                blk(s0, h0, d0);
+                ld(i - 64, s0, h0, d0);
+                blk(s1, h1, d1);
+                ld(i - 80, s1, h1, d1);
+                blk(s2, h2, d2);
+                ld(i - 96, s2, h2, d2);
+                blk(s3, h3, d3);
+                ld(i - 112, s3, h3, d3);
+            }
+            if (i >= 15) {
+                blk(s0, h0, d0);
+                i -= 16;
+                if (i >= 15) {
+                    blk(s1, h1, d1);
+                    i -= 16;
+                    if (i >= 15) {
+                        blk(s2, h2, d2);
+                        i -= 16;
+                    }
                 }
-                sv = sn;
-                hv = hn;
-                dv = dn;
             }
         }
-        // strided lanes: the next (lower) symbol's inputs are fetched one ahead
+        // strided lanes: inputs of the next (lower) symbols fetched 4 ahead
         if (i >= 0) {
-            int64_t pos = base + (int64_t)i * lanes;
-            uint32_t xn = syms[pos], hn = shift ? shift[pos] : 0u, dn = dsched ? dsched[pos] : dconst;
-            for (; i >= 0; --i, pos -= lanes) {
-                const uint32_t xc = xn, hc = hn, dc = dn;
-                if (i > 0) {
-                    xn = syms[pos - lanes];
-                    if (shift) hn = shift[pos - lanes];
-                    if (dsched) dn = dsched[pos - lanes];
-                }
-                enc_step(e, tab, X, M, dc, shift ? ((xc - hc + 128u) & 0xFFu) : xc, out);
+            constexpr int P = 4;
+            uint32_t tq[P];
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const int ii = i - j;
+                const int64_t pos = base + (int64_t)ii * lanes;
+                tq[j] = ii >= 0 ? word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst) : 0u;
+            }
+            for (; i >= 0; --i) {
+                const uint32_t tc = tq[0];
+#pragma unroll
+                for (int j = 0; j + 1 < P; ++j) tq[j] = tq[j + 1];
+                const int ii = i - P;
+                const int64_t pos = base + (int64_t)ii * lanes;
+                tq[P - 1] = ii >= 0 ? word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst) : 0u;
+                enc_push(e, tc, M, out);
             }
         }
         if (e.nacc) out[e.words] = (uint32_t)e.acc;
-        nbits[k] = e.words * 32u + (uint32_t)e.nacc;
-        states[k] = (uint16_t)e.state;
+        nbits[k] = e.words * 32u + e.nacc;
+        states[k] = (uint16_t)e.S;
     }
 }
 
-// Backward bit reader, 32-bit arithmetic relative to the lane's first
-// 16-byte chunk. A 64-bit window over aligned words is refilled one word at a
-// time from the current 16-byte chunk `cur` (registers). Chunks arrive
-// through a per-thread ring of kRing slots in shared memory filled with
-// cp.async three chunks (~30 symbols) ahead: unlike a register prefetch, a
-// pending cp.async never stalls an instruction until cp.async.wait_group
-// asks for that very chunk, so the state chain does not wait on memory.
-// Chunks stay inside [first chunk, last chunk] of the lane; buffers are padded
-// by 16 bytes (pilc.h) so the last chunk is always readable.
-constexpr int kRing = 4;
+// ---- decoder --------------------------------------------------------------
+// Backward bit reader, branch-free. Positions are bit indices relative to
+// the lane's first 16-byte chunk. `win` holds bits [L, L + 64) (L a multiple
+// of 32); before every pop at least 32 bits lie in [L, A), so a field of
+// b <= 12 bits is one 64-bit funnel shift. A pop that leaves fewer than 32
+// shifts in the next lower word from the register queue q (words consumed
+// w, z, y, x; k = words left); an empty queue reloads from a per-thread ring
+// of kRing shared-memory chunks that cp.async fills kAhead chunks ahead.
+// Lanes of a warp refill at different symbols, so everything here is
+// predicated rather than branched: a warp would otherwise run the refill
+// path at almost every symbol anyway. cp.async.wait_group runs once per
+// 16-symbol block (sync()): a block pops at most 192 bits = 1.5 chunks, and
+// the chunks it can need were committed at least kAhead - 2 groups ago.
+constexpr int kRing = 8;
+constexpr int kAhead = 4;
 
 struct BitReader {
     const uint4 *base4;  // chunk 0 = the lane's first chunk
-    uint4 *ring;         // this thread's kRing slots (stride = blockDim.x)
-    int stride;
-    int A, start, wl, cq, hi_c;
-    uint64_t win;
-    uint4 cur;
+    uint32_t ring_s;     // shared address of this thread's slot 0 (stride = blockDim.x * 16)
+    uint32_t ring_stride;
+    int hi_c;            // last chunk holding payload bits
+    int A, L, start, k, c;
+    uint32_t wlo, whi;   // window: bits [L, L + 32) and [L + 32, L + 64)
+    uint4 q;
 
-    __device__ __forceinline__ void issue(int c) {
-        if (c >= 0 && c <= hi_c) {
-            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + (c & (kRing - 1)) * stride);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(base4 + c) : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+    __device__ __forceinline__ uint4 direct(int ci) const {
+        return (ci >= 0 && ci <= hi_c) ? __ldg(base4 + ci) : make_uint4(0, 0, 0, 0);
     }
-    __device__ __forceinline__ static uint32_t pick(const uint4 &v, int k) {
-        return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+    __device__ __forceinline__ static uint32_t pick(const uint4 &v, int j) {
+        return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
     }
-    __device__ __forceinline__ uint4 direct(int c) const {
-        return (c >= 0 && c <= hi_c) ? __ldg(base4 + c) : make_uint4(0, 0, 0, 0);
+    // cp.async chunk ci into its slot when `on` and ci is inside the lane;
+    // a group is committed either way
+    __device__ __forceinline__ void issue(int ci, bool on) {
+        const uint32_t pr = (on && ci >= 0 && ci <= hi_c) ? 1u : 0u;
+        const uint32_t dst = ring_s + (uint32_t)(ci & (kRing - 1)) * ring_stride;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+            "@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}\n" ::"r"(dst),
+            "l"(base4 + ci), "r"(pr)
+            : "memory");
+        if (on) asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    __device__ __forceinline__ void init(const uint4 *lane_base4, uint4 *my_ring, int ring_stride, int start_bit,
-                                         uint32_t nb) {
+    __device__ __forceinline__ void init(const uint4 *lane_base4, uint32_t my_ring_s, uint32_t stride_bytes,
+                                         int start_bit, uint32_t nb) {
         base4 = lane_base4;
-        ring = my_ring;
-        stride = ring_stride;
-        start = start_bit;                               // 0..127
+        ring_s = my_ring_s;
+        ring_stride = stride_bytes;
+        start = start_bit;  // 0..127
         hi_c = nb ? (int)((start_bit + nb - 1) >> 7) : -1;
         A = start_bit + (int)nb;
-        wl = ((A - 1) >> 5) - 1;                         // window = bits [32 wl, 32 wl + 64)
-        const int c_top = (wl + 1) >> 2, c_lo = wl >> 2;
-        const uint4 a = direct(c_top);
-        const uint4 b = c_lo == c_top ? a : direct(c_lo);
-        win = ((uint64_t)pick(a, (wl + 1) & 3) << 32) | pick(b, wl & 3);
-        cq = (wl - 1) >> 2;                              // chunk of the next word to bring in
-        cur = direct(cq);
-        issue(cq - 1);
-        issue(cq - 2);
-        issue(cq - 3);
+        const int wl = ((A - 1) >> 5) - 1;  // window = words wl, wl + 1 (wl may be -1)
+        L = wl * 32;
+        const int wt = wl + 1;
+        whi = pick(direct(wt >> 2), wt & 3);
+        wlo = wl >= 0 ? pick(direct(wl >> 2), wl & 3) : 0u;
+        const int wn = wl - 1;  // next word to bring in
+        c = wn >> 2;            // arithmetic: -1 for wn in [-4, -1]
+        const uint4 q0 = direct(c);
+        // queue holds words (wn & 3) .. 0 of chunk c, top word in q.w
+        k = (wn & 3) + 1;
+        q.w = pick(q0, k - 1);
+        q.z = k >= 2 ? pick(q0, k - 2) : 0u;
+        q.y = k >= 3 ? pick(q0, k - 3) : 0u;
+        q.x = k >= 4 ? q0.x : 0u;
+#pragma unroll
+        for (int j = 1; j <= kAhead; ++j) issue(c - j, true);
     }
-    // false on underflow
-    __device__ __forceinline__ bool take(uint32_t b, uint32_t &v) {
-        const int lo = A - (int)b;
-        if (lo < start) return false;
-        if (lo < (wl << 5)) {
-            --wl;
-            if ((wl >> 2) != cq) {
-                --cq;
-                asm volatile("cp.async.wait_group 2;" ::: "memory");
-                cur = (cq >= 0 && cq <= hi_c) ? ring[(cq & (kRing - 1)) * stride] : make_uint4(0, 0, 0, 0);
-                issue(cq - 3);
-            }
-            win = (win << 32) | pick(cur, wl & 3);
-        }
-        v = (uint32_t)(win >> (lo - (wl << 5))) & ((1u << b) - 1u);
-        A = lo;
-        return true;
+    __device__ __forceinline__ void sync() const { asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 2) : "memory"); }
+    // pop b bits (b <= 12); underflow shows as A < start at the end
+    __device__ __forceinline__ uint32_t take(uint32_t b) {
+        A -= (int)b;
+        const uint32_t sh = (uint32_t)(A - L);
+        const uint32_t v = (uint32_t)((((uint64_t)whi << 32) | wlo) >> sh) & ((1u << b) - 1u);  // 20 <= sh < 64
+        const bool p = sh < 32u;
+        // refill: window down one word, queue shifts
+        whi = p ? wlo : whi;
+        wlo = p ? q.w : wlo;
+        L = p ? L - 32 : L;
+        q.w = p ? q.z : q.w;
+        q.z = p ? q.y : q.z;
+        q.y = p ? q.x : q.y;
+        k = p ? k - 1 : k;
+        // empty queue: next chunk from the ring, one more cp.async
+        const bool r = p && k == 0;
+        const int cn = c - 1;
+        const uint32_t src = ring_s + (uint32_t)(cn & (kRing - 1)) * ring_stride;
+        uint4 nq = q;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
+            "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
+            : "+r"(nq.x), "+r"(nq.y), "+r"(nq.z), "+r"(nq.w)
+            : "r"(src), "r"(r ? 1u : 0u)
+            : "memory");
+        const bool inl = cn >= 0 && cn <= hi_c;
+        q.x = r ? (inl ? nq.x : 0u) : q.x;
+        q.y = r ? (inl ? nq.y : 0u) : q.y;
+        q.z = r ? (inl ? nq.z : 0u) : q.z;
+        q.w = r ? (inl ? nq.w : 0u) : q.w;
+        k = r ? 4 : k;
+        c = r ? cn : c;
+        issue(cn - kAhead, r);
+        return v;
     }
 };
 
@@ -234,13 +302,14 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
             "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(bar)
             : "memory");
     }
-    uint4 *ring_base = reinterpret_cast<uint4 *>(s_tab + (SMEM ? (D << M) : 0));
-    uint4 *my_ring = ring_base + threadIdx.x;
+    const uint32_t my_ring =
+        (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4 *>(s_tab + (SMEM ? (D << M) : 0)) + threadIdx.x);
     const uint32_t T = 1u << M;
-    auto lookup = [&](uint32_t d, uint32_t st) -> uint32_t {
-        const uint32_t i = d * T + (st - T);
-        if constexpr (SMEM) return s_tab[i];
-        else return __ldg(dec_tab_g + i);
+    // table row of distribution d, pre-offset by -T so the index is the state
+    const uint32_t *tabT = (SMEM ? s_tab : dec_tab_g) - T;
+    auto lookup = [&](uint32_t dT, uint32_t st) -> uint32_t {
+        if constexpr (SMEM) return tabT[dT + st];
+        else return __ldg(tabT + dT + st);
     };
     const int64_t total = n_img * lanes;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
@@ -250,68 +319,100 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
         const int l = (int)(k - img * lanes);
         const int cnt = lane_count(n_sym, lanes, l);
         const int64_t sbase = img * n_sym + l;
-        const uint32_t dconst = d_img ? d_img[img] : 0u;
+        const uint32_t dconstT = (d_img ? (uint32_t)d_img[img] : 0u) << M;
         const uintptr_t a0 = reinterpret_cast<uintptr_t>(buf) + lane_off[k];
         BitReader br;
-        br.init(reinterpret_cast<const uint4 *>(a0 & ~(uintptr_t)15), my_ring, (int)blockDim.x, (int)(a0 & 15) * 8,
+        br.init(reinterpret_cast<const uint4 *>(a0 & ~(uintptr_t)15), my_ring, blockDim.x * 16u, (int)(a0 & 15) * 8,
                 nbits_a[k]);
         uint32_t state = states[k];
-        uint8_t st = 0;
         // one symbol: the decoded (optionally un-recentred) byte
-        auto step = [&](uint32_t d, uint32_t sh) -> uint32_t {
-            const uint32_t e = lookup(d, state);
-            uint32_t v = 0;
-            if (!br.take((e >> 8) & 0xFFu, v)) st = PILC_ST_UNDERFLOW;
-            state = (e >> 16) + v;
+        auto step = [&](uint32_t dT, uint32_t sh) -> uint32_t {
+            const uint32_t e = lookup(dT, state);
+            state = (e >> 16) + br.take((e >> 8) & 0xFFu);
             return unshift ? ((e + sh + 128u) & 0xFFu) : (e & 0xFFu);  // (x + shift - 128) mod 256
         };
         int i = 0;
         if (lanes == 1) {
-            for (; i < cnt && ((sbase + i) & 15) && !st; ++i) {
+            for (; i < cnt && ((sbase + i) & 15); ++i) {
                 const int64_t pos = sbase + i;
-                out[pos] = (uint8_t)step(dsched ? dsched[pos] : dconst, unshift ? unshift[pos] : 0u);
+                br.sync();
+                out[pos] = (uint8_t)step(dsched ? ((uint32_t)dsched[pos] << M) : dconstT, unshift ? unshift[pos] : 0u);
             }
-            // 16-symbol chunks; the next chunk's d / shift vectors are loaded
-            // one chunk ahead
+            // 16-symbol blocks, a register ring of four blocks for d / shift:
+            // block j + 4 is requested as soon as block j is decoded
             const uint4 z4 = make_uint4(0, 0, 0, 0);
-            uint4 dv = z4, hv = z4;
-            if (i + 16 <= cnt) {
-                if (dsched) dv = *reinterpret_cast<const uint4 *>(dsched + sbase + i);
-                if (unshift) hv = *reinterpret_cast<const uint4 *>(unshift + sbase + i);
-            }
-            for (; i + 16 <= cnt && !st; i += 16) {
-                const int64_t p0 = sbase + i;  // 16-aligned
-                uint4 dn = z4, hn = z4;
-                if (i + 32 <= cnt) {
-                    if (dsched) dn = *reinterpret_cast<const uint4 *>(dsched + p0 + 16);
-                    if (unshift) hn = *reinterpret_cast<const uint4 *>(unshift + p0 + 16);
+            auto ld = [&](int ii, uint4 &dv, uint4 &hv) {
+                if (ii + 16 <= cnt) {
+                    if (dsched) dv = *reinterpret_cast<const uint4 *>(dsched + sbase + ii);
+                    if (unshift) hv = *reinterpret_cast<const uint4 *>(unshift + sbase + ii);
                 }
+            };
+            auto blk = [&](const uint4 &dv, const uint4 &hv, int64_t p0) {
+                br.sync();
                 uint32_t o[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
-                    o[j >> 2] |= step(dsched ? vbyte(dv, j) : dconst, vbyte(hv, j)) << (8 * (j & 3));
+                    o[j >> 2] |= step(dsched ? (vbyte(dv, j) << M) : dconstT, vbyte(hv, j)) << (8 * (j & 3));
                 *reinterpret_cast<uint4 *>(out + p0) = make_uint4(o[0], o[1], o[2], o[3]);
-                dv = dn;
-                hv = hn;
+            };
+            uint4 d0 = z4, d1 = z4, d2 = z4, d3 = z4, h0 = z4, h1 = z4, h2 = z4, h3 = z4;
+            ld(i, d0, h0);
+            ld(i + 16, d1, h1);
+            ld(i + 32, d2, h2);
+            ld(i + 48, d3, h3);
+            for (; i + 64 <= cnt; i += 64) {
+                blk(d0, h0, sbase + i);
+                ld(i + 64, d0, h0);
+                blk(d1, h1, sbase + i + 16);
+                ld(i + 80, d1, h1);
+                blk(d2, h2, sbase + i + 32);
+                ld(i + 96, d2, h2);
+                blk(d3, h3, sbase + i + 48);
+                ld(i + 112, d3, h3);
+            }
+            if (i + 16 <= cnt) {
+                blk(d0, h0, sbase + i);
+                i += 16;
+                if (i + 16 <= cnt) {
+                    blk(d1, h1, sbase + i);
+                    i += 16;
+                    if (i + 16 <= cnt) {
+                        blk(d2, h2, sbase + i);
+                        i += 16;
+                    }
+                }
             }
         }
-        // strided lanes: the next symbol's d / shift are fetched one ahead
-        uint32_t dn = 0, hn = 0;
+        // strided lanes: d / shift of the next symbols fetched 4 ahead
         if (i < cnt) {
-            const int64_t pos = sbase + (int64_t)i * lanes;
-            dn = dsched ? dsched[pos] : dconst;
-            hn = unshift ? unshift[pos] : 0u;
-        }
-        for (; i < cnt && !st; ++i) {
-            const int64_t pos = sbase + (int64_t)i * lanes;
-            const uint32_t dc = dn, hc = hn;
-            if (i + 1 < cnt) {
-                dn = dsched ? dsched[pos + lanes] : dconst;
-                hn = unshift ? unshift[pos + lanes] : 0u;
+            constexpr int P = 4;
+            uint32_t dq[P], hq[P];
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const int ii = i + j;
+                const int64_t pos = sbase + (int64_t)ii * lanes;
+                dq[j] = ii < cnt ? (dsched ? ((uint32_t)dsched[pos] << M) : dconstT) : 0u;
+                hq[j] = (ii < cnt && unshift) ? unshift[pos] : 0u;
             }
-            out[pos] = (uint8_t)step(dc, hc);
+            for (; i < cnt; ++i) {
+                const int64_t pos = sbase + (int64_t)i * lanes;
+                const uint32_t dc = dq[0], hc = hq[0];
+#pragma unroll
+                for (int j = 0; j + 1 < P; ++j) {
+                    dq[j] = dq[j + 1];
+                    hq[j] = hq[j + 1];
+                }
+                const int ii = i + P;
+                const int64_t pn = sbase + (int64_t)ii * lanes;
+                dq[P - 1] = ii < cnt ? (dsched ? ((uint32_t)dsched[pn] << M) : dconstT) : 0u;
+                hq[P - 1] = (ii < cnt && unshift) ? unshift[pn] : 0u;
+                br.sync();
+                out[pos] = (uint8_t)step(dc, hc);
+            }
         }
-        if (!st && (state != T || br.A != br.start)) st = PILC_ST_END_STATE;
+        uint8_t st = 0;
+        if (br.A < br.start) st = PILC_ST_UNDERFLOW;
+        else if (state != T || br.A != br.start) st = PILC_ST_END_STATE;
         lane_status[k] = st;
         asm volatile("cp.async.wait_all;" ::: "memory");  // ring slots are reused by the next lane
     }
