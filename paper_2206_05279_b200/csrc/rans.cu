@@ -39,35 +39,45 @@ struct EncState {
     uint32_t S;
     uint64_t acc;
     uint32_t nacc;
-    uint32_t words;
+    uint32_t *wp;  // next output word
 };
 
-__device__ __forceinline__ void enc_push(EncState &e, uint32_t t, int M, uint32_t *out) {
+__device__ __forceinline__ void st_if(uint32_t *p, uint32_t v, bool on) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.u32 [%0], %1;\n\t}\n" ::"l"(p), "r"(v),
+        "r"(on ? 1u : 0u)
+        : "memory");
+}
+
+__device__ __forceinline__ void enc_push(EncState &e, uint32_t t, int M) {
     const uint32_t b = ((t & 0xFFFFu) + e.S) >> M;
     e.acc |= (uint64_t)(e.S & ((1u << b) - 1u)) << e.nacc;
     e.nacc += b;
     e.S = (e.S >> b) + (t >> 16);
     const bool f = e.nacc >= 32u;
-    if (f) out[e.words] = (uint32_t)e.acc;
-    e.words += f ? 1u : 0u;
+    st_if(e.wp, (uint32_t)e.acc, f);
+    e.wp += f ? 1 : 0;
     e.acc = f ? (e.acc >> 32) : e.acc;
     e.nacc -= f ? 32u : 0u;
 }
 
+template <bool SMEM>
 __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
     const uint8_t *__restrict__ syms, const uint8_t *__restrict__ shift,
     const uint8_t *__restrict__ dsched, const uint16_t *__restrict__ d_img,
     int64_t n_img, int64_t n_sym, int lanes, const uint32_t *__restrict__ enc_tab_g,
-    int D, int X, int M, int tab_in_smem, uint32_t *__restrict__ scratch,
+    int D, int X, int M, uint32_t *__restrict__ scratch,
     int64_t lane_cap, uint32_t *__restrict__ nbits, uint16_t *__restrict__ states) {
     extern __shared__ uint32_t s_tab[];
-    const uint32_t *tab = enc_tab_g;
-    if (tab_in_smem) {
+    if constexpr (SMEM) {
         const int n = D * X;
         for (int i = threadIdx.x; i < n; i += blockDim.x) s_tab[i] = enc_tab_g[i];
         __syncthreads();
-        tab = s_tab;
     }
+    auto tab = [&](uint32_t i) -> uint32_t {
+        if constexpr (SMEM) return s_tab[i];
+        else return __ldg(enc_tab_g + i);
+    };
     const int64_t total = n_img * lanes;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
@@ -77,10 +87,10 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
         const int64_t base = img * n_sym + l;
         const uint32_t dconst = d_img ? d_img[img] : 0u;
         uint32_t *out = scratch + k * lane_cap;
-        EncState e{1u << M, 0, 0, 0};
+        EncState e{1u << M, 0, 0, out};
         auto word = [&](uint32_t x, uint32_t h, uint32_t d) -> uint32_t {
             if (shift) x = (x - h + 128u) & 0xFFu;
-            return tab[d * X + x];
+            return tab(d * X + x);
         };
         int i = cnt - 1;
         if (lanes == 1) {
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
             // previous chunk prefetched while this one is coded
             for (; i >= 0 && ((base + i + 1) & 15); --i) {
                 const int64_t pos = base + i;
-                enc_push(e, word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst), M, out);
+                enc_push(e, word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst), M);
             }
             // 16-symbol blocks, a register ring of four blocks: the inputs of
             // block j + 4 are requested as soon as block j is coded (~64
@@ -108,7 +118,7 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
                 for (int j = 0; j < 16; ++j)
                     t[j] = word(vbyte(sv, j), vbyte(hv, j), dsched ? vbyte(dv, j) : dconst);
 #pragma unroll
-                for (int j = 15; j >= 0; --j) enc_push(e, t[j], M, out);
+                for (int j = 15; j >= 0; --j) enc_push(e, t[j], M);
             };
             uint4 s0 = z4, s1 = z4, s2 = z4, s3 = z4, h0 = z4, h1 = z4, h2 = z4, h3 = z4;
             uint4 d0 = z4, d1 = z4, d2 = z4, d3 = z4;
@@ -156,11 +166,11 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
                 const int ii = i - P;
                 const int64_t pos = base + (int64_t)ii * lanes;
                 tq[P - 1] = ii >= 0 ? word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst) : 0u;
-                enc_push(e, tc, M, out);
+                enc_push(e, tc, M);
             }
         }
-        if (e.nacc) out[e.words] = (uint32_t)e.acc;
-        nbits[k] = e.words * 32u + e.nacc;
+        if (e.nacc) *e.wp = (uint32_t)e.acc;
+        nbits[k] = (uint32_t)(e.wp - out) * 32u + e.nacc;
         states[k] = (uint16_t)e.S;
     }
 }
@@ -433,17 +443,25 @@ extern "C" int pilc_rans_encode(const uint8_t *syms, const uint8_t *shift, const
     const int64_t tab_bytes = (int64_t)D * X * 4;
     const int in_smem = tab_bytes <= kSmemTableMax;
     const size_t smem = in_smem ? (size_t)tab_bytes : 0;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(rans_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t total = n_img * lanes;
-    int64_t blocks = ceil_div64(total, kThreads);
+    // spread the lanes over every SM: threads per block = lanes / SMs,
+    // rounded to warps, in [32, kThreads]
+    int64_t threads = ceil_div64(ceil_div64(total, sm_count()), 32) * 32;
+    threads = threads < 32 ? 32 : (threads > kThreads ? kThreads : threads);
+    int64_t blocks = ceil_div64(total, threads);
     const int64_t cap = (int64_t)sm_count() * 16;
     if (blocks > cap) blocks = cap;
-{
+    {
         ProfScope _ps(PROF_RANS_ENC, as_stream(stream), (double)n_img * n_sym);
-        rans_encode_kernel<<<(unsigned)blocks, kThreads, smem, as_stream(stream)>>>(
-        syms, shift, dsched, d_img, n_img, n_sym, lanes, enc_tab, D, X, M, in_smem, scratch,
-        lane_cap, nbits, states);
+        if (in_smem) {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(rans_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            rans_encode_kernel<true><<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
+                syms, shift, dsched, d_img, n_img, n_sym, lanes, enc_tab, D, X, M, scratch, lane_cap, nbits, states);
+        } else {
+            rans_encode_kernel<false><<<(unsigned)blocks, (unsigned)threads, 0, as_stream(stream)>>>(
+                syms, shift, dsched, d_img, n_img, n_sym, lanes, enc_tab, D, X, M, scratch, lane_cap, nbits, states);
+        }
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
