@@ -54,6 +54,26 @@ struct Tc3Layer {
     int relu;
 };
 
+// Encoder front (stem SIMT + stride-2 down as a 3-product fp16 MMA over the
+// space-to-depth stem, tc_conv.cu); outputs like the block convs.
+struct EncFrontTc {
+    const uint8_t *img;  // (n, H, W, 3)
+    int64_t n_img, n_tiles;
+    int H, W, gh, gw;
+    const float *w_stem, *b_stem;  // packed model layout [tap][ci_pad][co_pad]
+    int stem_ci_pad, stem_co_pad;
+    const uint16_t *w_down;        // [36][64][8] fp16 hi / lo of w 2^kw_down
+    const float *b_down;
+    const float *meta_down;        // {kw_down (int), L1, max|b|, k_stem (int)}: weight / stem-output scales
+    const int32_t *k0;             // output scale exponent
+    float *out32;                  // fp32 slab set
+    uint16_t *out;                 // hi / lo slab set (scale 2^k0)
+    int64_t gstride, margin;
+    uint32_t *out_max;
+    int32_t *kx_out;
+};
+int enc_front_tc_launch(const EncFrontTc &a, cudaStream_t s);
+
 // Codebook argmin on tcgen05 (3xTF32 distance GEMM + exact float64 rescore).
 struct ArgminTc {
     const float *zt;       // z tiles from the projection epilogue

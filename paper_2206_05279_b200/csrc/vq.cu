@@ -19,7 +19,6 @@
 
 #include "common.cuh"
 #include "tc_conv.cuh"
-#include "enc_front.cuh"
 #include <cuda_fp16.h>
 #include <cmath>
 
@@ -51,10 +50,11 @@ struct Layout {
     // tcgen05 encoder (C == 32, Dc == 32): fp16-split B operands
     // [KG][64][8] (rows 0..31 hi, 32..63 lo of w 2^kw), float offsets;
     // tf_meta: per block conv / proj {kw (int), L1, max|b|, 0}, then
-    // {k0 (int): scale exponent of the encoder front's output, 0, 0, 0}
+    // {k0 (int): scale exponent of the encoder front's output, 0, 0, 0},
+    // then the down conv {kw, L1, max|b|, k_stem (int): stem output scale}
     bool tf;
     std::vector<int64_t> tf_blk;
-    int64_t tf_proj, tf_meta;
+    int64_t tf_proj, tf_down, tf_meta;
     int64_t tf_cb;  // argmin GEMM B operand [hi|lo][8][256][4] fp32 (codes >= K zero)
     int64_t total;                // floats, bf16 region included
 };
@@ -114,8 +114,10 @@ Layout make_layout(int K, int Dc, int C, int B) {
         }
         L.tf_proj = cur;
         cur += 4 * 64 * 8 / 2;
+        L.tf_down = cur;
+        cur += 36 * 64 * 8 / 2;
         L.tf_meta = cur;
-        cur += 4 * (2 * B + 2);
+        cur += 4 * (2 * B + 3);
         L.tf_cb = cur;
         cur += 2 * 8 * 256 * 4;
     }
@@ -679,7 +681,6 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
         // B' layout [K/8][64][8] fp16: rows 0..31 = h = fp16(w 2^kw), rows
         // 32..63 = l = fp16((w 2^kw - h) 2^11); kw puts max |w 2^kw| below 2^15
         float *meta = dst + L.tf_meta;
-        int n_kw = 0;
         // L1 = max over output channels of sum |w| (rounded up), max |b|
         auto l1_of = [&](const ConvSpec &sp, float &l1, float &bm) {
             double best = 0.0;
@@ -694,7 +695,7 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
             }
             l1 = (float)(best * (1.0 + 1e-6));
         };
-        auto put_t = [&](int64_t off, const ConvSpec &sp) {
+        auto put_t = [&](int64_t off, const ConvSpec &sp, int mi) {
             const int taps = sp.ks * sp.ks;
             float mx = 0.f;
             for (int n = 0; n < 32; ++n)
@@ -707,10 +708,9 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
             float l1, bm;
             l1_of(sp, l1, bm);
             int32_t kwi = kw;
-            memcpy(meta + 4 * n_kw, &kwi, 4);
-            meta[4 * n_kw + 1] = l1;
-            meta[4 * n_kw + 2] = bm;
-            ++n_kw;
+            memcpy(meta + 4 * mi, &kwi, 4);
+            meta[4 * mi + 1] = l1;
+            meta[4 * mi + 2] = bm;
             const float sc = std::ldexp(1.f, kw);
             uint16_t *h = reinterpret_cast<uint16_t *>(dst + off);
             for (int n = 0; n < 32; ++n)
@@ -724,8 +724,9 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
                         h[((int64_t)(k >> 3) * 64 + 32 + n) * 8 + (k & 7)] = __half_as_ushort(wl);
                     }
         };
-        for (int i = 0; i < 2 * B; ++i) put_t(L.tf_blk[i], L.enc[2 + i]);
-        put_t(L.tf_proj, L.enc[2 + 2 * B]);
+        for (int i = 0; i < 2 * B; ++i) put_t(L.tf_blk[i], L.enc[2 + i], i);
+        put_t(L.tf_proj, L.enc[2 + 2 * B], 2 * B);
+        put_t(L.tf_down, L.enc[1], 2 * B + 2);
         {
             // static bound of the encoder front's output (input in [-1, 1])
             float l1s, bms, l1d, bmd;
@@ -737,6 +738,13 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
             k0 = k0 < -90 ? -90 : (k0 > 90 ? 90 : k0);
             int32_t k0i = k0;
             memcpy(meta + 4 * (2 * B + 1), &k0i, 4);
+            // stem output bound (input in [-1, 1]) -> its operand scale
+            const double bs = (double)l1s + bms;
+            int ks = 0;
+            if (bs > 0.0 && std::isfinite(bs)) ks = 14 - std::ilogb(bs * (1.0 + 1e-6));
+            ks = ks < -90 ? -90 : (ks > 90 ? 90 : ks);
+            int32_t ksi = ks;
+            memcpy(meta + 4 * (2 * B + 2) + 3, &ksi, 4);
         }
         for (int k = 0; k < K; ++k)
             for (int c = 0; c < 32; ++c) {
@@ -829,10 +837,11 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
               int32_t B, const Layout &L, const TfWork &w, uint8_t *idx_out, float *z_out, cudaStream_t s) {
     const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
     int rc;
-    // stem + down fused (enc_front.cu) -> hi / lo slabs of the latent grid
-    EncFront f;
+    // stem + down fused on tcgen05 (tc_conv.cu) -> fp32 + hi / lo slabs of the latent grid
+    EncFrontTc f;
     f.img = img;
     f.n_img = n_img;
+    f.n_tiles = ceil_div64(n_img * (int64_t)(gh + 2) * (gw + 2), 128);
     f.H = H;
     f.W = W;
     f.gh = gh;
@@ -841,19 +850,18 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
     f.b_stem = model + L.enc[0].b_off;
     f.stem_ci_pad = L.enc[0].ci_pad;
     f.stem_co_pad = L.enc[0].co_pad;
-    f.w_down = model + L.enc[1].w_off;
+    f.w_down = reinterpret_cast<const uint16_t *>(model + L.tf_down);
     f.b_down = model + L.enc[1].b_off;
-    f.down_ci_pad = L.enc[1].ci_pad;
-    f.down_co_pad = L.enc[1].co_pad;
+    f.meta_down = model + L.tf_meta + 4 * (2 * B + 2);
+    f.k0 = reinterpret_cast<const int32_t *>(model + L.tf_meta + 4 * (2 * B + 1));
     f.out32 = w.X32;
     f.out = w.XH;
     f.out_max = w.mx;
     f.kx_out = w.kx;
-    f.k0 = reinterpret_cast<const int32_t *>(model + L.tf_meta + 4 * (2 * B + 1));
     f.gstride = w.gs;
     f.margin = w.margin;
     if (cudaMemsetAsync(w.mx, 0, (size_t)(2 * B + 1) * n_img * 4, s) != cudaSuccess) return PILC_E_CUDA;
-    if ((rc = enc_front_launch(f, s))) return rc;
+    if ((rc = enc_front_tc_launch(f, s))) return rc;
     Tc3Layer b;
     memset(&b, 0, sizeof(b));
     b.gstride = w.gs;
