@@ -862,10 +862,10 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
 }
 
 // ---- encoder front on tcgen05 (vqvae.py:55-57) -----------------------------
-// stem (3x3, 3 -> 32, ReLU, SIMT fp32) feeding down (3x3 stride 2, 32 -> 32,
-// ReLU) as a 3-product fp16 MMA, in one kernel: the stem never leaves the SM.
+// stem (3x3, 3 -> 32, ReLU) and down (3x3 stride 2, 32 -> 32, ReLU), both as
+// 3-product fp16 MMAs, in one kernel: the stem never leaves the SM.
 //
-// The stride-2 conv becomes a stride-1 implicit GEMM over the space-to-depth
+// Down. The stride-2 conv is a stride-1 implicit GEMM over the space-to-depth
 // view of the stem output: s2d cell (a, b) of the latent grid holds stem
 // pixels (2a + pi, 2b + pj), four phases x 32 channels. Down output (u, v)
 // tap (i, j) reads stem (2u + i - 1, 2v + j - 1) = s2d cell (u + di, v + dj)
@@ -873,56 +873,68 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
 // (likewise j). With s2d cells on the padded latent indexing (borders
 // included) each tap is the stage's K-major operand shifted by
 // (di + 1) Wp + (dj + 1) rows and offset to the phase's channel groups --
-// the same tap-shift trick as the block convs. Clamping (nn.conv2d edge
-// padding, _even_pad) is exact: every s2d cell, border cells included, is
-// the stem at clamp(2a + pi) x clamp(2b + pj), which is what the reference's
-// padded down conv reads.
+// the tap-shift trick of the block convs. Clamping (nn.conv2d edge padding,
+// _even_pad) is exact: every s2d cell, border cells included, is the stem at
+// clamp(2a + pi) x clamp(2b + pj), which is what the reference's padded down
+// conv reads. Cells no valid output reads stay zero.
 //
-// Warps: 0 weight copy, 1 MMA issuer, 2..5 epilogue, 6..15 stem producers
-// (two s2d cells x one phase per thread per round, fp32 FMA in the
-// reference's channel-tap order, scaled fp16 hi / lo into the stage).
-constexpr int kEfStages = 2;
-constexpr int kEfThreads = 512;
-constexpr int kEfProd = 320;
+// Stem. Per down tile the needed stem pixels m = phase * npix + s2d row are
+// cut into 128-pixel chunks: an im2col row per pixel (27 normalised inputs
+// in the reference's channel-tap order, padded to K = 32, scaled by 2^14 and
+// split into fp16 hi / lo), one 128 x 32 x 32 3-product MMA per chunk, and an
+// epilogue (bias, ReLU, 2^k_stem scale, split) that writes the chunk into
+// the down stage.
+//
+// Warps: 0 weight copies, 1 MMA issuer (stem chunks of tile i + 1 are issued
+// before the down GEMM of tile i), 2..5 down epilogue, 6..9 stem epilogue,
+// 10..13 im2col producers.
+constexpr int kEfThreads = 448;
+constexpr int kEfRing = 3;     // im2col chunk buffers
+constexpr int kEfSlots = 6;    // stem accumulators in TMEM (>= chunks per tile)
+constexpr int kEfChunkBytes = 2 * 4 * 128 * 16;  // hi + lo, 4 K groups, 128 rows
 
 __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc a) {
     constexpr int N = 32, N2 = 64;
-    constexpr int NHG = 16;  // 8-channel fp16 groups per operand: 4 phases x 4
     const int Wp = a.gw + 2, Hp = a.gh + 2;
     const int npix = (128 + Wp + 1 + 7) & ~7;
-    const uint32_t h_bytes = (uint32_t)NHG * npix * 16;
+    const int nch = (4 * npix + 127) >> 7;  // stem chunks per down tile
+    const uint32_t h_bytes = 16u * npix * 16u;  // 4 phases x 4 channel groups
     const uint32_t stage_bytes = 2 * h_bytes;
-    constexpr uint32_t wbytes = 36 * N2 * 16;
+    constexpr uint32_t wd_bytes = 36 * N2 * 16, ws_bytes = 4 * N2 * 16;
 
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t *s_w = smem;
-    float *s_ws = reinterpret_cast<float *>(smem + wbytes);  // stem weights [27][32] (k = c*9 + i*3 + j)
-    float *s_bs = s_ws + 27 * N;
+    uint8_t *s_wd = smem;
+    uint8_t *s_wsb = smem + wd_bytes;
+    uint8_t *s_a = s_wsb + ws_bytes;                             // down stage
+    uint8_t *s_c = s_a + stage_bytes;                            // im2col ring
+    float *s_bs = reinterpret_cast<float *>(s_c + kEfRing * kEfChunkBytes);
     float *s_bd = s_bs + N;
     float *s_norm = s_bd + N;  // x / 127.5 - 1 for every byte value (vqvae.py:41-43)
-    uint8_t *s_a = reinterpret_cast<uint8_t *>(s_norm + 256);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_a + (size_t)kEfStages * stage_bytes);
-    uint64_t *full = bars;
-    uint64_t *empty = bars + kEfStages;
-    uint64_t *tfull = bars + 2 * kEfStages;
-    uint64_t *tempty = tfull + 2;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_norm + 256);
+    uint64_t *afull = bars, *aempty = afull + kEfRing;
+    uint64_t *sfull = aempty + kEfRing, *sempty = sfull + kEfSlots;
+    uint64_t *dfull = sempty + kEfSlots, *dempty = dfull + 1;
+    uint64_t *tfull = dempty + 1, *tempty = tfull + 2;
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int e = threadIdx.x; e < 27 * N; e += blockDim.x) {
-        const int k = e / N, co = e % N;  // k = c*9 + tap
-        const int c = k / 9, tap = k % 9;
-        s_ws[e] = a.w_stem[((int64_t)tap * a.stem_ci_pad + c) * a.stem_co_pad + co];
+    if (threadIdx.x < N) {
+        s_bs[threadIdx.x] = a.b_stem[threadIdx.x];
+        s_bd[threadIdx.x] = a.b_down[threadIdx.x];
     }
-    if (threadIdx.x < N) s_bs[threadIdx.x] = a.b_stem[threadIdx.x];
-    if (threadIdx.x < N) s_bd[threadIdx.x] = a.b_down[threadIdx.x];
     for (int e = threadIdx.x; e < 256; e += blockDim.x) s_norm[e] = __fsub_rn(__fdiv_rn((float)e, 127.5f), 1.f);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kEfStages; ++s) {
-            mbar_init(&full[s], kEfProd / 32);
-            mbar_init(&empty[s], 1);
+        for (int r = 0; r < kEfRing; ++r) {
+            mbar_init(&afull[r], 4);
+            mbar_init(&aempty[r], 1);
         }
+        for (int r = 0; r < kEfSlots; ++r) {
+            mbar_init(&sfull[r], 1);
+            mbar_init(&sempty[r], 4);
+        }
+        mbar_init(dfull, 4);
+        mbar_init(dempty, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4);
@@ -932,124 +944,88 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(128u));
+                     "r"(512u));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem_down = tmem + 64u * kEfSlots;
     const int64_t n_tiles = a.n_tiles;
     const uint32_t img_px = (uint32_t)(Hp * Wp);
     const FastDiv div_hw{img_px, (uint32_t)(0x100000000ull / img_px)};
     const FastDiv div_w{(uint32_t)Wp, (uint32_t)(0x100000000ull / (uint32_t)Wp)};
+    const FastDiv div_np{(uint32_t)npix, (uint32_t)(0x100000000ull / (uint32_t)npix)};
+    const int He = 2 * a.gh, We = 2 * a.gw;
+    // stem pixel m of tile t: s2d row p = m % npix, phase ph = m / npix;
+    // live when some valid down output reads it
+    auto stem_px = [&](int64_t t, int m, int &ph, int &p, uint32_t &n, int &sy, int &sx) -> bool {
+        ph = (int)fdiv((uint32_t)m, div_np);
+        p = m - ph * npix;
+        if (ph > 3) return false;
+        const int64_t q = t * 128 - (Wp + 1) + p;
+        if (q < 0) return false;
+        n = fdiv((uint32_t)q, div_hw);
+        const uint32_t rem = (uint32_t)q - n * img_px;
+        const int yy = (int)fdiv(rem, div_w), xx = (int)(rem - (uint32_t)yy * div_w.d);
+        // latent rows -1 .. gh-1 (row -1 only in phase pi = 1), likewise columns
+        if (n >= (uint64_t)a.n_img || yy > a.gh || xx > a.gw || (yy < 1 && !(ph >> 1)) || (xx < 1 && !(ph & 1)))
+            return false;
+        sy = min(max(2 * (yy - 1) + (ph >> 1), 0), He - 1);
+        sx = min(max(2 * (xx - 1) + (ph & 1), 0), We - 1);
+        return true;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(wbar, wbytes);
-            bulk_g2s(s_w, a.w_down, wbytes, wbar);
+            mbar_expect_tx(wbar, wd_bytes + ws_bytes);
+            bulk_g2s(s_wd, a.w_down, wd_bytes, wbar);
+            bulk_g2s(s_wsb, a.w_stem16, ws_bytes, wbar);
         }
-    } else if (warp >= 6) {
-        // stem producers: unit = (s2d rows p, p + 1; phase ph), all 32
-        // channels in two passes of 16: every broadcast weight load feeds 8
-        // FMAs of each row. Rows are padded latent cells q_lo + p,
-        // q_lo = 128 t - (Wp + 1). Image bytes come through L1, normalised by
-        // a 256-entry table.
-        const int pt = threadIdx.x - 6 * 32;
-        const int He = 2 * a.gh, We = 2 * a.gw;
-        const float sc = exp2i(__float_as_int(a.meta_down[3]));
-        const int npairs = npix >> 1;
-        const int rowf = a.W * 3;
-        int i = 0;
-        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int s = i % kEfStages;
-            if (i >= kEfStages) mbar_wait(&empty[s], ((i / kEfStages) - 1) & 1);
-            uint4 *hs = reinterpret_cast<uint4 *>(s_a + (size_t)s * stage_bytes);
-            uint4 *ls = hs + NHG * npix;
-            const int64_t q_lo = t * 128 - (Wp + 1);
-            for (int it = pt; it < 4 * npairs; it += kEfProd) {
-                const int ph = it & 3, p0 = (it >> 2) * 2;
-                // per row: image base and the 3 clamped row / column offsets
-                const uint8_t *rb[2][3];
-                int cx[2][3];
-                bool live[2];
+    } else if (warp >= 10) {
+        // im2col producers: one stem pixel (row of the chunk) per thread
+        const int row = threadIdx.x - 10 * 32;
+        int64_t g = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            for (int c = 0; c < nch; ++c, ++g) {
+                const int slot = (int)(g % kEfRing);
+                if (g >= kEfRing) mbar_wait(&aempty[slot], (uint32_t)((g / kEfRing) - 1) & 1);
+                uint4 *hs = reinterpret_cast<uint4 *>(s_c + (size_t)slot * kEfChunkBytes);
+                uint4 *ls = hs + 4 * 128;
+                int ph, p, sy = 0, sx = 0;
+                uint32_t n = 0;
+                const bool live = stem_px(t, c * 128 + row, ph, p, n, sy, sx);
+                uint32_t hw[16], lw[16];
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int64_t q = q_lo + p0 + r;
-                    live[r] = false;
-                    int sy = 0, sx = 0;
-                    const uint8_t *img = a.img;
-                    if (q >= 0) {
-                        const uint32_t n = fdiv((uint32_t)q, div_hw);
-                        const uint32_t rem = (uint32_t)q - n * img_px;
-                        const int yy = (int)fdiv(rem, div_w), xx = (int)(rem - (uint32_t)yy * div_w.d);
-                        // cells / phases some valid output reads: rows -1 .. gh-1
-                        // of the latent grid, row -1 only in phase 1 (likewise columns)
-                        const bool need = yy <= a.gh && xx <= a.gw && (yy >= 1 || (ph >> 1)) && (xx >= 1 || (ph & 1));
-                        if (n < (uint64_t)a.n_img && need) {
-                            live[r] = true;
-                            sy = min(max(2 * (yy - 1) + (ph >> 1), 0), He - 1);
-                            sx = min(max(2 * (xx - 1) + (ph & 1), 0), We - 1);
-                            img = a.img + (int64_t)n * a.H * rowf;
+                for (int e = 0; e < 16; ++e) hw[e] = lw[e] = 0u;
+                if (live) {
+                    const uint8_t *img = a.img + (int64_t)n * a.H * a.W * 3;
+                    float xv[28];
+#pragma unroll
+                    for (int ki = 0; ki < 3; ++ki) {
+                        const uint8_t *rp = img + (int64_t)min(max(sy + ki - 1, 0), a.H - 1) * a.W * 3;
+#pragma unroll
+                        for (int kj = 0; kj < 3; ++kj) {
+                            const uint8_t *px = rp + min(max(sx + kj - 1, 0), a.W - 1) * 3;
+#pragma unroll
+                            for (int ch = 0; ch < 3; ++ch) xv[ch * 9 + ki * 3 + kj] = s_norm[__ldg(px + ch)];
                         }
                     }
+                    xv[27] = 0.f;
 #pragma unroll
-                    for (int k3 = 0; k3 < 3; ++k3) {
-                        rb[r][k3] = img + (int64_t)min(max(sy + k3 - 1, 0), a.H - 1) * rowf;
-                        cx[r][k3] = min(max(sx + k3 - 1, 0), a.W - 1) * 3;
-                    }
+                    for (int e = 0; e < 14; ++e)  // k = 2e, 2e + 1; |x 2^14| <= 2^14
+                        split2(__fmul_rn(xv[2 * e], 16384.f), __fmul_rn(xv[2 * e + 1], 16384.f), hw[e], lw[e]);
                 }
-                // two passes of 16 output channels (register budget)
-#pragma unroll 1
-                for (int hf = 0; hf < 2; ++hf) {
-                    float acc0[16], acc1[16];
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        acc0[c] = s_bs[16 * hf + c];
-                        acc1[c] = s_bs[16 * hf + c];
-                    }
-                    if (live[0] || live[1]) {
-#pragma unroll
-                        for (int k = 0; k < 27; ++k) {  // k = c*9 + ki*3 + kj (reference channel-tap order)
-                            const int c = k / 9, ki = (k % 9) / 3, kj = k % 3;
-                            const float x0 = s_norm[__ldg(rb[0][ki] + cx[0][kj] + c)];
-                            const float x1 = s_norm[__ldg(rb[1][ki] + cx[1][kj] + c)];
-                            const float4 *w4 = reinterpret_cast<const float4 *>(s_ws + k * N + 16 * hf);
-#pragma unroll
-                            for (int g = 0; g < 4; ++g) {
-                                const float4 w = w4[g];
-                                acc0[4 * g + 0] = fmaf(x0, w.x, acc0[4 * g + 0]);
-                                acc0[4 * g + 1] = fmaf(x0, w.y, acc0[4 * g + 1]);
-                                acc0[4 * g + 2] = fmaf(x0, w.z, acc0[4 * g + 2]);
-                                acc0[4 * g + 3] = fmaf(x0, w.w, acc0[4 * g + 3]);
-                                acc1[4 * g + 0] = fmaf(x1, w.x, acc1[4 * g + 0]);
-                                acc1[4 * g + 1] = fmaf(x1, w.y, acc1[4 * g + 1]);
-                                acc1[4 * g + 2] = fmaf(x1, w.z, acc1[4 * g + 2]);
-                                acc1[4 * g + 3] = fmaf(x1, w.w, acc1[4 * g + 3]);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int r = 0; r < 2; ++r) {
-                        const float *acc = r ? acc1 : acc0;
-                        const float m = live[r] ? sc : 0.f;  // dead cells store zeros
-#pragma unroll
-                        for (int jj = 0; jj < 2; ++jj) {
-                            const int j = 2 * hf + jj;
-                            uint4 h, l;
-                            split2(__fmul_rn(fmaxf(acc[8 * jj + 0], 0.f), m), __fmul_rn(fmaxf(acc[8 * jj + 1], 0.f), m), h.x, l.x);
-                            split2(__fmul_rn(fmaxf(acc[8 * jj + 2], 0.f), m), __fmul_rn(fmaxf(acc[8 * jj + 3], 0.f), m), h.y, l.y);
-                            split2(__fmul_rn(fmaxf(acc[8 * jj + 4], 0.f), m), __fmul_rn(fmaxf(acc[8 * jj + 5], 0.f), m), h.z, l.z);
-                            split2(__fmul_rn(fmaxf(acc[8 * jj + 6], 0.f), m), __fmul_rn(fmaxf(acc[8 * jj + 7], 0.f), m), h.w, l.w);
-                            hs[(ph * 4 + j) * npix + p0 + r] = h;
-                            ls[(ph * 4 + j) * npix + p0 + r] = l;
-                        }
-                    }
+                for (int kg = 0; kg < 4; ++kg) {
+                    hs[kg * 128 + row] = make_uint4(hw[4 * kg], hw[4 * kg + 1], hw[4 * kg + 2], hw[4 * kg + 3]);
+                    ls[kg * 128 + row] = make_uint4(lw[4 * kg], lw[4 * kg + 1], lw[4 * kg + 2], lw[4 * kg + 3]);
                 }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afull[slot]);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
         }
     } else if (warp == 1) {
         constexpr uint32_t idesc64 = idesc_f16(128, N2);
@@ -1057,19 +1033,43 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
         mbar_wait(wbar, 0);
         tc_fence_after();
         const uint64_t dA0 = umma_desc(smem_u32(s_a), (uint32_t)npix * 16u, 128u);
-        const uint64_t dB0 = umma_desc(smem_u32(s_w), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dB0 = umma_desc(smem_u32(s_wd), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dC0 = umma_desc(smem_u32(s_c), 128u * 16u, 128u);
+        const uint64_t dS0 = umma_desc(smem_u32(s_wsb), (uint32_t)N2 * 16u, 128u);
         const uint32_t npx = (uint32_t)npix;
+        int64_t gi = 0;  // next stem chunk to issue (global index)
+        // stem chunks of one tile: A (im2col) x [Ws_hi | Ws_lo] and A_lo x Ws_hi
+        auto issue_stem = [&]() {
+            for (int c = 0; c < nch; ++c, ++gi) {
+                const int r = (int)(gi % kEfRing), sl = (int)(gi % kEfSlots);
+                mbar_wait(&afull[r], (uint32_t)(gi / kEfRing) & 1);
+                if (gi >= kEfSlots) mbar_wait(&sempty[sl], (uint32_t)((gi / kEfSlots) - 1) & 1);
+                tc_fence_after();
+                const uint64_t dh = dC0 + (uint64_t)((uint32_t)r * (kEfChunkBytes >> 4));
+                const uint64_t dl = dh + (uint64_t)(4 * 128);
+                const uint32_t d = tmem + 64u * sl;
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const uint64_t ao = (uint64_t)(2 * ks * 128);
+                    const uint64_t bo = (uint64_t)(2 * ks * N2);
+                    mma_f16_elect(d, dh + ao, dS0 + bo, idesc64, ks ? 1u : 0u);
+                    mma_f16_elect(d + N, dl + ao, dS0 + bo, idesc32, 1u);
+                }
+                mma_commit_elect(&aempty[r]);
+                mma_commit_elect(&sfull[sl]);
+            }
+        };
+        if (blockIdx.x < n_tiles) issue_stem();
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int s = i % kEfStages;
+            if (t + gridDim.x < n_tiles) issue_stem();  // next tile's stem overlaps this tile's down GEMM
             const int b = i & 1;
             const int u = i >> 1;
             if (u > 0) mbar_wait(&tempty[b], (u - 1) & 1);
-            mbar_wait(&full[s], (i / kEfStages) & 1);
+            mbar_wait(dfull, (uint32_t)i & 1);
             tc_fence_after();
-            const uint64_t dAh = dA0 + (uint64_t)((uint32_t)s * (stage_bytes >> 4));
-            const uint64_t dAl = dAh + (uint64_t)(h_bytes >> 4);
-            const uint32_t d = tmem + (uint32_t)(b * N2);
+            const uint64_t dAl = dA0 + (uint64_t)(h_bytes >> 4);
+            const uint32_t d = tmem_down + (uint32_t)(b * N2);
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
                 const int ti = tap / 3, tj = tap % 3;
@@ -1079,21 +1079,73 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
                 for (int ks = 0; ks < 2; ++ks) {
                     const uint64_t ao = (uint64_t)((ph * 4u + 2u * ks) * npx + rows);
                     const uint64_t bo = (uint64_t)((tap * 4 + 2 * ks) * N2);
-                    mma_f16_elect(d, dAh + ao, dB0 + bo, idesc64, (tap | ks) ? 1u : 0u);
+                    mma_f16_elect(d, dA0 + ao, dB0 + bo, idesc64, (tap | ks) ? 1u : 0u);
                     mma_f16_elect(d + N, dAl + ao, dB0 + bo, idesc32, 1u);
                 }
             }
-            mma_commit_elect(&empty[s]);
+            mma_commit_elect(dempty);
             mma_commit_elect(&tfull[b]);
         }
-    } else if (warp >= 2) {
+    } else if (warp >= 6) {
+        // stem epilogue: chunk row -> stem pixel; bias, ReLU, 2^k_stem, split
+        // into the down stage (phase ph's 4 hi / 4 lo channel groups, row p)
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int kws = __float_as_int(a.meta_stem[0]);
+        const float inv = exp2i(-14 - kws);
+        const float sc = exp2i(__float_as_int(a.meta_down[3]));
+        uint4 *hs = reinterpret_cast<uint4 *>(s_a);
+        uint4 *ls = hs + 16 * npix;
+        int64_t g = 0;
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            if (i > 0) mbar_wait(dempty, (uint32_t)(i - 1) & 1);  // the down GEMM of the previous tile is done
+            for (int c = 0; c < nch; ++c, ++g) {
+                const int sl = (int)(g % kEfSlots);
+                int ph, p, sy, sx;
+                uint32_t n;
+                const bool live = stem_px(t, c * 128 + row, ph, p, n, sy, sx);
+                mbar_wait(&sfull[sl], (uint32_t)(g / kEfSlots) & 1);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + 64u * sl;
+                float v[32];
+                {
+                    float w[32];
+                    tmem_ld32(taddr, v);
+                    tmem_ld32(taddr + 32, w);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        v[k] = __fmul_rn(fmaxf(__fmaf_rn(__fmaf_rn(w[k], 0.00048828125f, v[k]), inv, s_bs[k]), 0.f),
+                                         live ? sc : 0.f);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sempty[sl]);
+                if (ph < 4) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint4 h, l;
+                        split2(v[8 * j + 0], v[8 * j + 1], h.x, l.x);
+                        split2(v[8 * j + 2], v[8 * j + 3], h.y, l.y);
+                        split2(v[8 * j + 4], v[8 * j + 5], h.z, l.z);
+                        split2(v[8 * j + 6], v[8 * j + 7], h.w, l.w);
+                        hs[(ph * 4 + j) * npix + p] = h;
+                        ls[(ph * 4 + j) * npix + p] = l;
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dfull);
+        }
+    } else {
+        // down epilogue
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int H = a.gh, W = a.gw;
         const float inv = exp2i(-__float_as_int(a.meta_down[3]) - __float_as_int(a.meta_down[0]));
         const int ko = *a.k0;
         const float osc = exp2i(ko);
-        const float *bias = s_bd;
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
             const int b = i & 1;
@@ -1105,7 +1157,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
             const bool valid = n < (uint64_t)a.n_img && y >= 1 && y <= H && x >= 1 && x <= W;
             mbar_wait(&tfull[b], u & 1);
             tc_fence_after();
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * N2);
+            const uint32_t taddr = tmem_down + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * N2);
             float v[32];
             {
                 float w[32];
@@ -1113,7 +1165,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
                 tmem_ld32(taddr + 32, w);
 #pragma unroll
                 for (int c = 0; c < 32; ++c)
-                    v[c] = fmaxf(__fmaf_rn(__fmaf_rn(w[c], 0.00048828125f, v[c]), inv, bias[c]), 0.f);
+                    v[c] = fmaxf(__fmaf_rn(__fmaf_rn(w[c], 0.00048828125f, v[c]), inv, s_bd[c]), 0.f);
             }
             tc_fence_before();
             __syncwarp();
@@ -1157,7 +1209,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
     }
 }
 
@@ -1503,7 +1555,9 @@ int argmin_tc_launch(const ArgminTc &a, cudaStream_t s) {
 int enc_front_tc_launch(const EncFrontTc &a, cudaStream_t s) {
     const int Wp = a.gw + 2;
     const int npix = (128 + Wp + 1 + 7) & ~7;
-    const size_t smem = 36 * 64 * 16 + (27 * 32 + 32 + 32 + 256) * 4 + (size_t)kEfStages * 2 * 16 * npix * 16 + 8 * (2 * kEfStages + 5) + 16;
+    if ((4 * npix + 127) / 128 > kEfSlots) return PILC_E_UNSUPPORTED;
+    const size_t smem = 36 * 64 * 16 + 4 * 64 * 16 + (size_t)2 * 16 * npix * 16 + (size_t)kEfRing * kEfChunkBytes +
+                        (32 + 32 + 256) * 4 + 8 * (2 * kEfRing + 2 * kEfSlots + 7) + 16;
     if ((uint64_t)a.n_img * (a.gh + 2) * Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     cudaFuncSetAttribute(enc_front_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

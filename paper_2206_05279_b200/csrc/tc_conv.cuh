@@ -54,14 +54,16 @@ struct Tc3Layer {
     int relu;
 };
 
-// Encoder front (stem SIMT + stride-2 down as a 3-product fp16 MMA over the
-// space-to-depth stem, tc_conv.cu); outputs like the block convs.
+// Encoder front (stem and the stride-2 down conv as 3-product fp16 MMAs, the
+// down GEMM over the space-to-depth stem, tc_conv.cu); outputs like the
+// block convs.
 struct EncFrontTc {
     const uint8_t *img;  // (n, H, W, 3)
     int64_t n_img, n_tiles;
     int H, W, gh, gw;
-    const float *w_stem, *b_stem;  // packed model layout [tap][ci_pad][co_pad]
-    int stem_ci_pad, stem_co_pad;
+    const uint16_t *w_stem16;      // [4][64][8] fp16 hi / lo of w_stem 2^kw_stem, K = c*9 + tap (27 -> 32)
+    const float *meta_stem;        // {kw_stem (int), ...}
+    const float *b_stem;
     const uint16_t *w_down;        // [36][64][8] fp16 hi / lo of w 2^kw_down
     const float *b_down;
     const float *meta_down;        // {kw_down (int), L1, max|b|, k_stem (int)}: weight / stem-output scales

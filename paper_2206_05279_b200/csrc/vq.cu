@@ -51,10 +51,11 @@ struct Layout {
     // [KG][64][8] (rows 0..31 hi, 32..63 lo of w 2^kw), float offsets;
     // tf_meta: per block conv / proj {kw (int), L1, max|b|, 0}, then
     // {k0 (int): scale exponent of the encoder front's output, 0, 0, 0},
-    // then the down conv {kw, L1, max|b|, k_stem (int): stem output scale}
+    // then the down conv {kw, L1, max|b|, k_stem (int): stem output scale},
+    // then the stem {kw, 0, 0, 0} (stem B operand [4][64][8], K = c*9 + tap)
     bool tf;
     std::vector<int64_t> tf_blk;
-    int64_t tf_proj, tf_down, tf_meta;
+    int64_t tf_proj, tf_down, tf_stem, tf_meta;
     int64_t tf_cb;  // argmin GEMM B operand [hi|lo][8][256][4] fp32 (codes >= K zero)
     int64_t total;                // floats, bf16 region included
 };
@@ -116,8 +117,10 @@ Layout make_layout(int K, int Dc, int C, int B) {
         cur += 4 * 64 * 8 / 2;
         L.tf_down = cur;
         cur += 36 * 64 * 8 / 2;
+        L.tf_stem = cur;
+        cur += 4 * 64 * 8 / 2;
         L.tf_meta = cur;
-        cur += 4 * (2 * B + 3);
+        cur += 4 * (2 * B + 4);
         L.tf_cb = cur;
         cur += 2 * 8 * 256 * 4;
     }
@@ -728,6 +731,32 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
         put_t(L.tf_proj, L.enc[2 + 2 * B], 2 * B);
         put_t(L.tf_down, L.enc[1], 2 * B + 2);
         {
+            // stem: K = c*9 + i*3 + j (the reference's im2col order), 27 -> 32
+            const ConvSpec &sp = L.enc[0];
+            float mx = 0.f;
+            for (int n = 0; n < 32; ++n)
+                for (int c = 0; c < 3; ++c)
+                    for (int tap = 0; tap < 9; ++tap)
+                        mx = fmaxf(mx, fabsf(dst[sp.w_off + ((int64_t)tap * sp.ci_pad + c) * sp.co_pad + n]));
+            int kw = 0;
+            if (mx > 0.f && std::isfinite(mx)) kw = 14 - std::ilogb(mx);
+            kw = kw < -30 ? -30 : (kw > 30 ? 30 : kw);
+            int32_t kwi = kw;
+            memcpy(meta + 4 * (2 * B + 3), &kwi, 4);
+            const float sc = std::ldexp(1.f, kw);
+            uint16_t *h = reinterpret_cast<uint16_t *>(dst + L.tf_stem);
+            for (int n = 0; n < 32; ++n)
+                for (int c = 0; c < 3; ++c)
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const int k = c * 9 + tap;
+                        const float w = dst[sp.w_off + ((int64_t)tap * sp.ci_pad + c) * sp.co_pad + n] * sc;
+                        const __half wh = __float2half_rn(w);
+                        const __half wl = __float2half_rn((w - __half2float(wh)) * 2048.f);
+                        h[((int64_t)(k >> 3) * 64 + n) * 8 + (k & 7)] = __half_as_ushort(wh);
+                        h[((int64_t)(k >> 3) * 64 + 32 + n) * 8 + (k & 7)] = __half_as_ushort(wl);
+                    }
+        }
+        {
             // static bound of the encoder front's output (input in [-1, 1])
             float l1s, bms, l1d, bmd;
             l1_of(L.enc[0], l1s, bms);
@@ -846,10 +875,9 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
     f.W = W;
     f.gh = gh;
     f.gw = gw;
-    f.w_stem = model + L.enc[0].w_off;
+    f.w_stem16 = reinterpret_cast<const uint16_t *>(model + L.tf_stem);
+    f.meta_stem = model + L.tf_meta + 4 * (2 * B + 3);
     f.b_stem = model + L.enc[0].b_off;
-    f.stem_ci_pad = L.enc[0].ci_pad;
-    f.stem_co_pad = L.enc[0].co_pad;
     f.w_down = reinterpret_cast<const uint16_t *>(model + L.tf_down);
     f.b_down = model + L.enc[1].b_off;
     f.meta_down = model + L.tf_meta + 4 * (2 * B + 2);
