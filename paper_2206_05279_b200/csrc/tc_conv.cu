@@ -20,11 +20,11 @@
 // row): no im2col, no per-tap copies. 9 taps x (C/16) tcgen05.mma
 // (M=128, K=16) accumulate in TMEM.
 //
-// Warp roles (192 threads): warp 0 = bulk-copy producer (4-stage ring),
-// warp 1 = TMEM allocator + single-thread MMA issuer, warps 2..5 =
-// epilogue (TMEM -> registers -> bias/residual/ReLU/pixel-shuffle/head ->
-// global). TMEM holds two accumulators so the epilogue of tile i overlaps
-// the MMAs of tile i+1. Deterministic: fixed tiles, fixed K order, no
+// Warp roles (320 threads): warp 0 = bulk-copy producer (8-stage ring),
+// warp 1 = TMEM allocator + MMA issuer (warp-uniform loop, elected lane),
+// warps 2..9 = epilogue in two groups of four, one per TMEM accumulator
+// (TMEM -> registers -> bias/residual/ReLU/pixel-shuffle/head -> global), so
+// the epilogues of tiles i and i+1 overlap each other and the MMAs of i+2. Deterministic: fixed tiles, fixed K order, no
 // atomics -- so a blob compressed on one GPU decodes on any other.
 
 #include <cuda_bf16.h>
@@ -38,8 +38,8 @@
 
 namespace {
 
-constexpr int kStages = 4;
-constexpr int kThreadsTC = 192;
+constexpr int kStages = 8;
+constexpr int kThreadsTC = 320;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -305,7 +305,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
             mma_commit_elect(&tfull[a]);
         }
     } else {
-        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31
+        // epilogue: two groups of four warps (2..5, 6..9), group g owns the
+        // tiles with i % 2 == g and accumulator buffer g, so one group's
+        // epilogue overlaps the other's; warp w reads TMEM lanes 32*(w%4) .. +31
+        const int grp = (warp - 2) >> 2;
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int H = L.H, W = L.W;
@@ -317,9 +320,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
 #pragma unroll
             for (int c = 0; c < NB; ++c) bias[c] = L.bias[c];
         }
-        int i = 0;
-        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int a = i & 1;
+        int i = grp;
+        for (int64_t t = blockIdx.x + (int64_t)grp * gridDim.x; t < n_tiles; t += 2 * (int64_t)gridDim.x, i += 2) {
+            const int a = grp;
             const int u = i >> 1;
             const uint32_t q = (uint32_t)t * 128u + (uint32_t)row;
             const uint32_t n = fdiv(q, div_hw);
@@ -1489,10 +1492,9 @@ int launch_tc(const TcLayer &L, cudaStream_t s) {
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     auto kern = tc_conv_kernel<N, KS, MODE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = (int)((227 * 1024) / (smem + 1024));
-    if (per_sm < 1) per_sm = 1;
-    if (per_sm > 4) per_sm = 4;
-    int64_t grid = (int64_t)sm_count() * per_sm;
+    // one persistent CTA per SM (two epilogue groups, an 8-deep copy ring);
+    // the head's math-heavy epilogue (few registers) runs two CTAs per SM
+    int64_t grid = (int64_t)sm_count() * (MODE == TC_OUT_HEAD ? 2 : 1);
     if (grid > L.n_tiles) grid = L.n_tiles;
     if (grid < 1) return PILC_OK;
     const double flops = 2.0 * L.n_img * L.H * L.W * (double)(MODE == TC_OUT_HEAD ? 6 : N) * 32 * KS * KS;
