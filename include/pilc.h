@@ -237,6 +237,21 @@ int pilc_container_parse(const uint8_t *buf, const uint64_t *blob_off,
                          int64_t n_blob, uint64_t params_hash,
                          uint64_t model_hash, int32_t has_model,
                          pilc_header *hdr, void *stream);
+/* Batch summary of parsed headers (one small record the host can read in a
+ * single transfer): number of headers with a nonzero status, whether all
+ * share blob 0's grouping key (width, height, backend, M, lanes, flags, D,
+ * grid crc), blob 0's header and its grid bytes (u16 D + D f64, when blob 0
+ * parsed OK). Replaces the reference's per-blob parse_header on the hot path
+ * (container.py:195-258) for the common one-shape batch. */
+typedef struct pilc_summary {
+    int32_t n_bad, uniform;
+    pilc_header h0;
+    uint8_t grid[2 + 8 * 256];
+    uint8_t pad[6];
+} pilc_summary;
+int pilc_container_summary(const uint8_t *buf, const uint64_t *blob_off,
+                           const pilc_header *hdr, int64_t n_blob,
+                           pilc_summary *out, void *stream);
 /* Per-lane extraction for a group of blobs sharing (lanes, backend):
  * blob_idx[g] selects the blob; for stream 0 (index) / 1 (residual) the
  * lane payload offset (absolute, into buf), bit count and state are

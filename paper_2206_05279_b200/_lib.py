@@ -40,6 +40,7 @@ _SIGS = {
     "pilc_container_pack": (ctypes.c_int, [P, I32, P, P, I32, I64, I64, I32, P, I64, P, P, P, I64, P, P, P, P, P]),
     "pilc_container_parse": (ctypes.c_int, [P, P, I64, ctypes.c_uint64, ctypes.c_uint64, I32, P, P]),
     "pilc_container_lanes": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
+    "pilc_container_summary": (ctypes.c_int, [P, P, P, I64, P, P]),
     "pilc_crc32": (ctypes.c_int, [P, P, P, I64, P, P]),
     "pilc_sched_crc": (ctypes.c_int, [P, P, I64, I64, P, P]),
     "pilc_prof_reset": (None, [I32]),
@@ -66,6 +67,11 @@ HEADER_DTYPE = np.dtype(
     align=True,
 )
 assert HEADER_DTYPE.itemsize == 72
+
+# pilc_summary (include/pilc.h)
+SUMMARY_DTYPE = np.dtype([("n_bad", "<i4"), ("uniform", "<i4"), ("h0", HEADER_DTYPE), ("grid", "u1", 2 + 8 * 256),
+                          ("pad", "u1", 6)], align=True)
+assert SUMMARY_DTYPE.itemsize == 2136
 
 ST_NAMES = {
     0: "OK", 1: "TRUNCATED", 2: "BAD_MAGIC", 3: "BAD_VERSION", 4: "CRC", 5: "BAD_BACKEND",

@@ -105,7 +105,9 @@ def _template(backend: int, cfg: CodecConfig, W: int, H: int, params: PredictorP
 
 
 def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, stream):
-    """One (H, W) group, all on `stream`. Returns (out_d, blob_off_d, total)."""
+    """One (H, W) group, all on `stream`, with no host synchronisation.
+    Returns (out_d, blob_off_d): blob i is out_d[blob_off_d[i]:blob_off_d[i+1]]
+    (out_d is sized for the worst case)."""
     N, H, W, _ = img_d.shape
     if W >= (1 << 32) or H >= (1 << 32):
         raise ParameterError("image dimensions do not fit 32 bits")
@@ -141,18 +143,16 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
     sizes = torch.empty(N, dtype=torch.int64, device=dev)
     _lib.call("pilc_container_sizes", ptr(idx_nb), ptr(res_nb), N, L, fixed, ptr(sizes), ptr(blob_off),
               sptr(stream))
-    total_h = pinned(8)
-    with torch.cuda.stream(stream):
-        total_h.copy_(blob_off[N:].view(torch.uint8), non_blocking=True)
-    stream.synchronize()
-    total = int(total_h.numpy().view(np.uint64)[0])
-    out_d = torch.empty(total + 16, dtype=torch.uint8, device=dev)
+    # worst-case output size (every lane at its word capacity): no host read
+    # of the exact total is needed before packing, so the stream never stalls
+    per = fixed + L * (8 + 4 * res_cap) + (L * (8 + 4 * idx_cap) if backend == BACKEND_VQVAE else 0)
+    out_d = torch.empty(N * per + 16, dtype=torch.uint8, device=dev)
     tb = CACHE.get(("tmpl", tmpl), dev, lambda: torch.frombuffer(bytearray(tmpl), dtype=torch.uint8).to(dev))
     _lib.call("pilc_container_pack", ptr(tb), len(tmpl), ptr(d_img), ptr(dsched),
               1 if config.debug_schedule_check else 0, N, n_sym, L, ptr(idx_scr), idx_cap, ptr(idx_nb),
               ptr(idx_st), ptr(res_scr), res_cap, ptr(res_nb), ptr(res_st), ptr(blob_off), ptr(out_d),
               sptr(stream))
-    return out_d, blob_off, total
+    return out_d, blob_off
 
 
 def _groups_by_shape(shapes):
@@ -203,19 +203,22 @@ def compress_batch(images, model: ModelWeights | None = None, config: CodecConfi
         img_d = as_device_u8(arr, dev, stream)
     if img_d.shape[0] == 0:
         return np.zeros(0, np.uint8), np.zeros(1, np.uint64)
-    out_d, off_d, total = _compress_device(img_d, model, config, dev, stream)
+    out_d, off_d = _compress_device(img_d, model, config, dev, stream)
+    n = img_d.shape[0]
+    offs = pinned(8 * (n + 1))
+    with torch.cuda.stream(stream):
+        offs.copy_(off_d.view(torch.uint8), non_blocking=True)
+    stream.synchronize()
+    ov = offs.numpy().view(np.uint64)
+    total = int(ov[n])
     if return_device:
         return out_d, off_d, total
     # D2H straight into pinned memory; the returned arrays are views of it
-    n = img_d.shape[0]
-    host = pinned(total + 8 * (n + 1) + 8)
-    hv = host.numpy()
-    o8 = (total + 7) & ~7
+    host = pinned(total + 8)
     with torch.cuda.stream(stream):
         host[:total].copy_(out_d[:total], non_blocking=True)
-        host[o8:o8 + 8 * (n + 1)].copy_(off_d.view(torch.uint8), non_blocking=True)
     stream.synchronize()
-    return hv[:total], hv[o8:o8 + 8 * (n + 1)].view(np.uint64)
+    return host.numpy()[:total], ov
 
 
 def compress(image: np.ndarray, model: ModelWeights | None = None, config: CodecConfig = CodecConfig()) -> bytes:
@@ -290,6 +293,9 @@ def _lane_error(status_row: np.ndarray) -> Exception | None:
 
 
 def _parse_device(buf_d, off_d, n, model, dev, stream):
+    """Parse every header on the device; returns the device header array and
+    the batch summary (one small pinned read: status count, one-group flag,
+    blob 0's header and grid bytes)."""
     params = _params_of(model)
     ph = int(np.frombuffer(params.hash8(), "<u8")[0])
     has_model = model is not None and model.has_network
@@ -297,11 +303,21 @@ def _parse_device(buf_d, off_d, n, model, dev, stream):
     hdr_d = torch.empty(n * _lib.HEADER_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     _lib.call("pilc_container_parse", ptr(buf_d), ptr(off_d), n, ph, mh, 1 if has_model else 0, ptr(hdr_d),
               sptr(stream))
+    summ_d = torch.empty(_lib.SUMMARY_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    _lib.call("pilc_container_summary", ptr(buf_d), ptr(off_d), ptr(hdr_d), n, ptr(summ_d), sptr(stream))
+    host = pinned(summ_d.numel())
+    with torch.cuda.stream(stream):
+        host.copy_(summ_d, non_blocking=True)
+    stream.synchronize()
+    return hdr_d, host.numpy().view(_lib.SUMMARY_DTYPE)[0].copy()
+
+
+def _headers_host(hdr_d, stream):
     host = pinned(hdr_d.numel())
     with torch.cuda.stream(stream):
         host.copy_(hdr_d, non_blocking=True)
     stream.synchronize()
-    return host.numpy().view(_lib.HEADER_DTYPE).copy(), hdr_d
+    return host.numpy().view(_lib.HEADER_DTYPE).copy()
 
 
 def _grid_of(buf_host, buf_d, off, h) -> ScaleGrid:
@@ -313,48 +329,63 @@ def _grid_of(buf_host, buf_d, off, h) -> ScaleGrid:
     return ScaleGrid.from_bytes(raw)[0]
 
 
-def _decompress_device(buf_d, off_d, offs_host, model, dev, stream, buf_host=None):
-    """Decode all blobs. Returns (images: list of (ids, device tensor),
-    errors: dict blob -> Exception)."""
-    n = len(offs_host) - 1
-    hdr, hdr_d = _parse_device(buf_d, off_d, n, model, dev, stream)
+def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_host=None):
+    """Decode all n blobs. Returns (images: list of (ids, device tensor,
+    lane statuses, schedule crcs, L), errors: dict blob -> Exception, host
+    headers or None). One small host read (the batch summary) when every
+    blob parses and shares one shape / config; otherwise every header is read
+    and the blobs are grouped on the host."""
+    hdr_d, summ = _parse_device(buf_d, off_d, n, model, dev, stream)
     has_model = model is not None and model.has_network
+    h0 = summ["h0"]
     errors: dict = {}
-    st = hdr["status"]
-    for i in np.flatnonzero(st != 0):
-        errors[int(i)] = _header_error(hdr[i], model is not None)
-    ok = st == 0
-    need_model = ok & (hdr["backend"] == BACKEND_VQVAE)
-    if not has_model and need_model.any():
-        for i in np.flatnonzero(need_model):
-            errors[int(i)] = ModelError("container needs model weights to decode")
-        ok &= ~need_model
-    key = np.zeros(n, dtype=[("w", "<u4"), ("h", "<u4"), ("b", "u1"), ("M", "u1"), ("L", "<u2"),
-                             ("f", "u1"), ("D", "<u2"), ("g", "<u4")])
-    key["w"], key["h"], key["b"], key["M"] = hdr["width"], hdr["height"], hdr["backend"], hdr["M"]
-    key["L"], key["f"], key["D"], key["g"] = hdr["lanes"], hdr["flags"], hdr["D"], hdr["grid_crc"]
-    ids_ok = np.flatnonzero(ok)
-    results = []
-    if ids_ok.size == 0:
-        return results, errors, hdr
-    k0 = key[ids_ok[0]]
-    if all(np.all(key[f][ids_ok] == k0[f]) for f in key.dtype.names):
-        groups = [(k0, ids_ok)]  # the common case: one shape, one config
+    fast = (int(summ["n_bad"]) == 0 and int(summ["uniform"]) == 1 and not (int(h0["flags"]) & FLAG_SCHEDULE_CHECKSUM)
+            and (int(h0["backend"]) != BACKEND_VQVAE or has_model))
+    hdr = None
+    if fast:
+        grid = ScaleGrid.from_bytes(bytes(summ["grid"][: 2 + 8 * int(h0["D"])]))[0]
+        groups = [(h0, None, grid)]
     else:
-        raw = key[ids_ok].view(np.dtype((np.void, key.dtype.itemsize)))
-        uk, inv = np.unique(raw, return_inverse=True)
-        groups = [(key[ids_ok[np.flatnonzero(inv == gi)[0]]], ids_ok[inv == gi]) for gi in range(len(uk))]
-    for k, ids in groups:
-        h0 = hdr[ids[0]]
-        W, H, backend, M, L = int(k["w"]), int(k["h"]), int(k["b"]), int(k["M"]), int(k["L"])
-        flags = int(k["f"])
-        grid = _grid_of(buf_host, buf_d, int(offs_host[ids[0]]), h0)
+        hdr = _headers_host(hdr_d, stream)
+        st = hdr["status"]
+        for i in np.flatnonzero(st != 0):
+            errors[int(i)] = _header_error(hdr[i], model is not None)
+        ok = st == 0
+        need_model = ok & (hdr["backend"] == BACKEND_VQVAE)
+        if not has_model and need_model.any():
+            for i in np.flatnonzero(need_model):
+                errors[int(i)] = ModelError("container needs model weights to decode")
+            ok &= ~need_model
+        key = np.zeros(n, dtype=[("w", "<u4"), ("h", "<u4"), ("b", "u1"), ("M", "u1"), ("L", "<u2"),
+                                 ("f", "u1"), ("D", "<u2"), ("g", "<u4")])
+        key["w"], key["h"], key["b"], key["M"] = hdr["width"], hdr["height"], hdr["backend"], hdr["M"]
+        key["L"], key["f"], key["D"], key["g"] = hdr["lanes"], hdr["flags"], hdr["D"], hdr["grid_crc"]
+        ids_ok = np.flatnonzero(ok)
+        groups = []
+        if ids_ok.size:
+            raw = key[ids_ok].view(np.dtype((np.void, key.dtype.itemsize)))
+            uk, inv = np.unique(raw, return_inverse=True)
+            for gi in range(len(uk)):
+                ids = ids_ok[inv.reshape(-1) == gi]
+                off0 = int(offs_host[ids[0]]) if offs_host is not None else int(off_d[ids[0]].item())
+                groups.append((hdr[ids[0]], ids, _grid_of(buf_host, buf_d, off0, hdr[ids[0]])))
+    results = []
+    hdr16 = hdr_d.view(torch.int16).view(n, _lib.HEADER_DTYPE.itemsize // 2)
+    sd_col = _lib.HEADER_DTYPE.fields["static_d"][1] // 2
+    for h0, ids, grid in groups:
+        W, H, backend, M, L = int(h0["width"]), int(h0["height"]), int(h0["backend"]), int(h0["M"]), int(h0["lanes"])
+        flags = int(h0["flags"])
         if grid.D > 256:
-            for i in ids:
+            for i in (range(n) if ids is None else ids):
                 errors[int(i)] = ParameterError("the GPU path carries distribution indices as uint8 (grid D <= 256)")
             continue
-        ng = ids.size
-        ids_d = torch.from_numpy(ids.astype(np.int64)).to(dev)
+        if ids is None:
+            ng = n
+            ids_d = torch.arange(n, dtype=torch.int64, device=dev)
+            ids = _ArangeIds(n)
+        else:
+            ng = ids.size
+            ids_d = torch.from_numpy(ids.astype(np.int64)).to(dev)
         _, res_dec = build_tables(residual_distributions(grid, M), M)
         n_sym = H * W * 3
         shift = dsel = d_img = None
@@ -374,7 +405,8 @@ def _decompress_device(buf_d, off_d, offs_host, model, dev, stream, buf_host=Non
             lane_st["idx"] = ls
             shift, dsel = decode_head_device(idx, model, H, W, grid, dev, stream)
         else:
-            d_img = torch.from_numpy(hdr["static_d"][ids].astype(np.int16)).to(dev)
+            # static_d straight from the device headers (no host round trip)
+            d_img = hdr16[:, sd_col].index_select(0, ids_d).contiguous()
         sched = None
         if flags & FLAG_SCHEDULE_CHECKSUM:
             sched = torch.empty(ng, dtype=torch.int32, device=dev)
@@ -395,12 +427,29 @@ def _decompress_device(buf_d, off_d, offs_host, model, dev, stream, buf_host=Non
     return results, errors, hdr
 
 
+class _ArangeIds:
+    """ids of a one-group batch: 0 .. n-1 (numpy-like for the error paths)."""
+
+    def __init__(self, n: int):
+        self.size = n
+
+    def __iter__(self):
+        return iter(range(self.size))
+
+    def __getitem__(self, j):
+        return j
+
+    def __array__(self, dtype=None, copy=None):
+        return np.arange(self.size, dtype=dtype)
+
+
 def _resolve_errors(results, errors, hdr):
     """Per-blob errors of the decode stages, in the reference's order."""
     for ids, _img, lane_st, sched, L in results:
         st_idx = lane_st["idx"].cpu().numpy().reshape(-1, L) if "idx" in lane_st else None
         st_res = lane_st["res"].cpu().numpy().reshape(-1, L)
         crc = sched.cpu().numpy().view(np.uint32) if sched is not None else None
+        ids = np.asarray(ids)
         bad = np.zeros(ids.size, bool)
         if st_idx is not None:
             bad |= st_idx.any(axis=1)
@@ -438,13 +487,13 @@ def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=
             raise FormatError("container truncated")
     buf_d = h2d(buf_host[: int(offs[-1])], dev, stream, pad=16)
     off_d = h2d(offs.view(np.uint8), dev, stream).view(torch.int64)
-    results, errors, hdr = _decompress_device(buf_d, off_d, offs, model, dev, stream, buf_host)
+    results, errors, hdr = _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host, offs)
     errors = _resolve_errors(results, errors, hdr)
     if errors and raise_on_error:
         raise errors[min(errors)]
     # D2H through pinned memory. One group covering every blob in order (the
     # batch case) lands directly in the returned array.
-    if len(results) == 1 and not errors and results[0][0].size == n:
+    if len(results) == 1 and not errors and np.asarray(results[0][0]).size == n:
         img = results[0][1]
         host = pinned(img.numel())
         with torch.cuda.stream(stream):
@@ -459,7 +508,7 @@ def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=
             host.copy_(img.view(-1), non_blocking=True)
         stream.synchronize()
         arr = host.numpy().reshape(tuple(img.shape))
-        for j, i in enumerate(ids):
+        for j, i in enumerate(np.asarray(ids)):
             if int(i) not in errors:
                 imgs[int(i)] = arr[j]
     return (imgs, errors) if not raise_on_error else imgs

@@ -521,6 +521,47 @@ unsigned warp_grid(int64_t n) {
     return (unsigned)(blocks > cap ? cap : (blocks < 1 ? 1 : blocks));
 }
 
+// ---- batch summary --------------------------------------------------------
+// One block: counts headers with a nonzero status, checks that every header
+// shares blob 0's grouping key (dims, backend, M, lanes, flags, D, grid crc)
+// and copies blob 0's header and grid bytes, so the host decides the common
+// one-group case from one small read instead of every header.
+__global__ void summary_kernel(const uint8_t *__restrict__ buf, const uint64_t *__restrict__ blob_off,
+                               const pilc_header *__restrict__ hdr, int64_t n, pilc_summary *__restrict__ out) {
+    __shared__ int s_bad[32], s_diff[32];
+    const pilc_header h0 = hdr[0];
+    int bad = 0, diff = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const pilc_header h = hdr[i];
+        bad += h.status != 0;
+        diff |= h.width != h0.width || h.height != h0.height || h.backend != h0.backend || h.M != h0.M ||
+                h.lanes != h0.lanes || h.flags != h0.flags || h.D != h0.D || h.grid_crc != h0.grid_crc;
+    }
+    for (int o = 16; o; o >>= 1) {
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+        diff |= __shfl_xor_sync(0xffffffffu, diff, o);
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        s_bad[w] = bad;
+        s_diff[w] = diff;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int b = 0, d = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            b += s_bad[k];
+            d |= s_diff[k];
+        }
+        out->n_bad = b;
+        out->uniform = !d;
+        out->h0 = h0;
+    }
+    // grid bytes of blob 0: u16 D + D f64 at offset 21 (valid when its status is OK)
+    const int nb = h0.status == 0 ? 2 + 8 * (int)h0.D : 0;
+    for (int k = threadIdx.x; k < nb && k < (int)sizeof(out->grid); k += blockDim.x) out->grid[k] = buf[blob_off[0] + 21 + k];
+}
+
 }  // namespace
 
 extern "C" int pilc_static_scale(const uint8_t *res, int64_t n_img, int64_t n_sym, const double *log2_grid,
@@ -587,6 +628,17 @@ extern "C" int pilc_container_parse(const uint8_t *buf, const uint64_t *blob_off
         ProfScope _ps(PROF_PARSE, as_stream(stream), (double)n_blob);
         parse_kernel<<<warp_grid(n_blob), 32 * kWarps, 0, as_stream(stream)>>>(
         buf, blob_off, n_blob, params_hash, model_hash, has_model, hdr, crc_consts());
+    }
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+extern "C" int pilc_container_summary(const uint8_t *buf, const uint64_t *blob_off, const pilc_header *hdr,
+                                      int64_t n_blob, pilc_summary *out, void *stream) {
+    if (n_blob < 1 || !buf || !blob_off || !hdr || !out) return PILC_E_ARG;
+    {
+        ProfScope _ps(PROF_PARSE, as_stream(stream), (double)n_blob);
+        summary_kernel<<<1, 1024, 0, as_stream(stream)>>>(buf, blob_off, hdr, n_blob, out);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;

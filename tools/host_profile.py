@@ -12,9 +12,8 @@ cfg = pc.CodecConfig(backend="twar-vqvae")
 imgs = smooth_images(8192, 32, 32, seed=0)
 img_d = torch.from_numpy(imgs).to(dev)
 def step():
-    out_d, off_d, total = ct._compress_device(img_d, model, cfg, dev, stream)
-    offs = off_d.cpu().numpy().view(np.uint64)
-    r = ct._decompress_device(out_d, off_d, offs, model, dev, stream)
+    out_d, off_d = ct._compress_device(img_d, model, cfg, dev, stream)
+    r = ct._decompress_device(out_d, off_d, img_d.shape[0], model, dev, stream)
     torch.cuda.synchronize()
     return r
 for _ in range(3):
