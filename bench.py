@@ -355,11 +355,14 @@ def run_gpu(args):
         dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
         roofline = None
         notes = {
-            "tc3_conv_kernel": "3xTF32 tcgen05 (kind::tf32, 2 MMAs per K step: A_hi x [B_hi|B_lo] and A_lo x B_hi) encoder block convs; "
-                               "algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch",
+            "tc3_conv_kernel": "encoder block convs, 3-product fp16 split on tcgen05 kind::f16 (per K=16 step A_hi x [W_hi|W_lo] "
+                               "N=64 + A_lo x W_hi N=32, fp32 TMEM); algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch "
+                               "(MMA FLOPs issued = 3x that)",
             "tc_conv_kernel": "bf16 tcgen05 decoder convs; algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch",
-            "conv_kernel": "fp32 SIMT convs (stem/down); algorithmic FLOPs = 2*N*Ho*Wo*Cout*Cin*k^2 per launch",
-            "argmin_kernel": "fp32 SIMT codebook distances (3*n*K*Dc FLOPs)",
+            "enc_front_kernel": "encoder stem + stride-2 down, both 3-product fp16 MMAs (down over the space-to-depth stem); "
+                                "algorithmic FLOPs = 2*N*(4*gh*gw*32*27 + gh*gw*32*32*9)",
+            "conv_kernel": "fp32 SIMT convs (non-default model shapes); algorithmic FLOPs = 2*N*Ho*Wo*Cout*Cin*k^2 per launch",
+            "argmin_kernel": "codebook distance GEMM (3xTF32 tcgen05) + proven-margin screen + exact f64 rescore (3*n*K*Dc FLOPs)",
         }
         if dom:
             name, (n, ms, units) = dom
@@ -369,7 +372,7 @@ def run_gpu(args):
                 roofline = {"kernel": name, "bound": "tensor", "achieved": round(ach, 3), "peak": peak,
                             "unit": "TFLOP/s", "frac": round(ach / peak, 5), "traffic": None,
                             "launches_per_step": n / args.steps, "ms_per_launch": round(ms / n, 4),
-                            "peak_source": f"{src} bf16 dense, sustained (a tf32 MMA runs at half that rate)",
+                            "peak_source": f"{src} bf16 dense, sustained (kind::f16 fp16/bf16 MMAs run at this rate)",
                             "note": notes[name]}
             else:
                 gbs = units / (ms / 1e3) / 1e9
@@ -400,7 +403,8 @@ def run_gpu(args):
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
-            "dtype": "bf16 tcgen05 decoder, 3xTF32 tcgen05 + f32 SIMT encoder, f32/f64 argmin, int coder/predictor/container",
+            "dtype": "bf16 tcgen05 decoder, fp32-class encoder (3-product fp16 split on tcgen05), 3xTF32 + f64 argmin, "
+                     "int coder/predictor/container",
             "data": "synthetic",
             "config": {"workload": wl["desc"], "global_batch": wl["N"] * ws, "image": [wl["H"], wl["W"], 3],
                        "parallelism": f"shard{ws}", "l2": "flushed (256 MiB write) before each step"},

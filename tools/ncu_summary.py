@@ -44,62 +44,54 @@ def launches(path, out):
     print("\n".join(lines))
 
 
-WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "L1/TEX Cache Throughput",
-        "L2 Cache Throughput", "Achieved Occupancy", "Registers Per Thread", "Dynamic Shared Memory Per Block",
-        "Grid Size", "Block Size", "Executed Ipc Active", "Issue Slots Busy"]
+RAW = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe (TC) % active"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor math % active"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem operand reads (TC) % of peak"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def full(path, out, js=None):
-    txt = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(txt)))
-    h = rows[0]
-    idx = {k: i for i, k in enumerate(h)}
-    per = collections.OrderedDict()
-    for r in rows[1:]:
-        key = (r[idx["ID"]], kname(r[idx["Kernel Name"]]))
-        if r[idx["Metric Name"]] in WANT:
-            per.setdefault(key, {})[r[idx["Metric Name"]]] = f"{r[idx['Metric Value']]} {r[idx['Metric Unit']]}".strip()
+    """One row per profiled launch (raw page), with dram bytes per launch."""
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     hdr, units = rr[0], rr[1]
     cols = {k: i for i, k in enumerate(hdr)}
-    dram = {}
-    tensor = {}
+    lines = ["| id | kernel | " + " | ".join(lab for _, lab in RAW) + " | dram bytes (r+w) |",
+             "|---|---|" + "---:|" * (len(RAW) + 1)]
+    dram = collections.defaultdict(list)
     for r in rr[2:]:
         name = kname(r[cols["Kernel Name"]])
         b = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             if m in cols:
-                v = float(r[cols[m]].replace(",", "") or 0)
-                u = units[cols[m]]
-                v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-                b += v
-        dram.setdefault(name, []).append(b)
-        for m in cols:
-            if m.startswith("sm__pipe_tensor") and "pct_of_peak_sustained_active" in m:
-                tensor.setdefault(name, {})[m] = r[cols[m]]
-    lines = []
-    for (i, k), d in per.items():
-        lines.append(f"### launch {i}: `{k}`")
-        for m in WANT:
-            if m in d:
-                lines.append(f"- {m}: {d[m]}")
-        if k in dram:
-            lines.append(f"- dram bytes (read+write): {dram[k][0]:.0f}")
-        for m, v in tensor.get(k, {}).items():
-            lines.append(f"- {m}: {v}")
-        lines.append("")
-    open(out, "w").write("\n".join(lines))
+                b += float(r[cols[m]].replace(",", "") or 0) * SCALE.get(units[cols[m]], 1)
+        dram[name.split("<")[0]].append(b)
+        vals = []
+        for m, _ in RAW:
+            if m in cols:
+                v, u = r[cols[m]], units[cols[m]]
+                vals.append(f"{v} {u}".strip() if u not in ("%", "") else v)
+            else:
+                vals.append("")
+        lines.append(f"| {r[cols['ID']]} | `{name}` | " + " | ".join(vals) + f" | {b:.3e} |")
+    open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if js:
         try:
             cur = json.load(open(js))
-        except OSError:
+        except (OSError, ValueError):
             cur = {}
-        cur.setdefault("dram_bytes_per_launch", {})
-        for k, v in dram.items():
-            base = k.split("<")[0]
-            cur["dram_bytes_per_launch"][base] = sum(v) / len(v)
+        cur["dram_bytes_per_launch"] = {k: sum(v) / len(v) for k, v in dram.items()}
+        cur["source"] = path
         json.dump(cur, open(js, "w"), indent=1, sort_keys=True)
 
 
