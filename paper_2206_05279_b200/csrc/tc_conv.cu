@@ -889,10 +889,11 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
 // the down stage.
 //
 // Warps: 0 weight copies, 1 MMA issuer (stem chunks of tile i + 1 are issued
-// before the down GEMM of tile i), 2..5 down epilogue, 6..9 stem epilogue,
-// 10..13 im2col producers.
-constexpr int kEfThreads = 448;
-constexpr int kEfRing = 3;     // im2col chunk buffers
+// before the down GEMM of tile i), 2..5 down epilogue, 6..9 and 14..17 stem
+// epilogue, 10..13 and 18..21 im2col producers (pairs of groups take
+// alternate chunks).
+constexpr int kEfThreads = 704;
+constexpr int kEfRing = 4;     // im2col chunk buffers
 constexpr int kEfSlots = 6;    // stem accumulators in TMEM (>= chunks per tile)
 constexpr int kEfChunkBytes = 2 * 4 * 128 * 16;  // hi + lo, 4 K groups, 128 rows
 
@@ -936,7 +937,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
             mbar_init(&sfull[r], 1);
             mbar_init(&sempty[r], 4);
         }
-        mbar_init(dfull, 4);
+        mbar_init(dfull, 8);
         mbar_init(dempty, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
@@ -986,12 +987,15 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
             bulk_g2s(s_wd, a.w_down, wd_bytes, wbar);
             bulk_g2s(s_wsb, a.w_stem16, ws_bytes, wbar);
         }
-    } else if (warp >= 10) {
-        // im2col producers: one stem pixel (row of the chunk) per thread
-        const int row = threadIdx.x - 10 * 32;
+    } else if ((warp >= 10 && warp < 14) || warp >= 18) {
+        // im2col producers, two groups of four warps (10..13, 18..21) taking
+        // alternate chunks; one stem pixel (row of the chunk) per thread
+        const int pg = warp >= 18 ? 1 : 0;
+        const int row = threadIdx.x - (pg ? 18 : 10) * 32;
         int64_t g = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
             for (int c = 0; c < nch; ++c, ++g) {
+                if ((int)(g & 1) != pg) continue;
                 const int slot = (int)(g % kEfRing);
                 if (g >= kEfRing) mbar_wait(&aempty[slot], (uint32_t)((g / kEfRing) - 1) & 1);
                 uint4 *hs = reinterpret_cast<uint4 *>(s_c + (size_t)slot * kEfChunkBytes);
@@ -1090,8 +1094,10 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
             mma_commit_elect(&tfull[b]);
         }
     } else if (warp >= 6) {
-        // stem epilogue: chunk row -> stem pixel; bias, ReLU, 2^k_stem, split
-        // into the down stage (phase ph's 4 hi / 4 lo channel groups, row p)
+        // stem epilogue, two groups of four warps (6..9, 14..17) taking
+        // alternate chunks: chunk row -> stem pixel; bias, ReLU, 2^k_stem,
+        // split into the down stage (phase ph's 4 hi / 4 lo groups, row p)
+        const int grp = warp >= 14 ? 1 : 0;
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int kws = __float_as_int(a.meta_stem[0]);
@@ -1104,6 +1110,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
             if (i > 0) mbar_wait(dempty, (uint32_t)(i - 1) & 1);  // the down GEMM of the previous tile is done
             for (int c = 0; c < nch; ++c, ++g) {
+                if ((int)(g & 1) != grp) continue;
                 const int sl = (int)(g % kEfSlots);
                 int ph, p, sy, sx;
                 uint32_t n;
