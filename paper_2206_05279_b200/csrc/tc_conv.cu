@@ -794,7 +794,8 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
                         store_px(L.out + ((int64_t)(NH + j) * L.gstride + L.margin) * 8, q, l, y, x, H, W, Wp);
                     }
                 }
-                if (has_res) {
+                if (has_res) {  // loads consumed above; the next fill is an async-proxy write
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&rempty[a]);
                 }

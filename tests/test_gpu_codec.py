@@ -12,6 +12,7 @@ import struct
 import zlib
 
 import numpy as np
+import torch
 import pytest
 
 import paper_2206_05279_b200 as pc
@@ -363,3 +364,25 @@ def test_large_batch_round_trip(full_model):
     assert np.array_equal(pc.decompress_batch(buf, off, full_model), imgs)
     bufs, offs = pc.compress_batch(imgs)
     assert np.array_equal(pc.decompress_batch(bufs, offs), imgs)
+
+
+def test_tcgen05_decoder_deterministic(full_model):
+    """Compress and decompress each run the decoder: its (shift, d) planes
+    must be bit-identical across calls and batch sizes, or blobs
+    would not decode. Batches large enough for every CTA to cycle its
+    shared-memory rings several times."""
+    from paper_2206_05279_b200.logistic import default_grid
+
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.current_stream(dev)
+    rng = np.random.default_rng(3)
+    idx = rng.integers(0, 256, (1024, 16, 16), dtype=np.uint8)
+    ref = [t.cpu().numpy() for t in vqvae.decode_head_device(torch.from_numpy(idx).to(dev), full_model, 32, 32,
+                                                             default_grid(), dev, s)]
+    for _ in range(2):
+        out = [t.cpu().numpy() for t in vqvae.decode_head_device(torch.from_numpy(idx).to(dev), full_model, 32, 32,
+                                                                 default_grid(), dev, s)]
+        assert all(np.array_equal(a, b) for a, b in zip(ref, out))
+    sub = [t.cpu().numpy() for t in vqvae.decode_head_device(torch.from_numpy(idx[:3]).to(dev), full_model, 32, 32,
+                                                             default_grid(), dev, s)]
+    assert all(np.array_equal(a[:3], b) for a, b in zip(ref, sub))
