@@ -11,8 +11,10 @@ exchange.
 from __future__ import annotations
 
 import numpy as np
+import torch
 
-from .container import CodecConfig, compress_batch, decompress_batch
+from .container import CodecConfig, _decompress_device, _resolve_errors, compress_batch
+from .device import h2d, pinned, require_device
 
 
 def patch_grid(H: int, W: int, ph: int = 64, pw: int = 64):
@@ -32,15 +34,136 @@ def assemble(patches: list, H: int, W: int, ph: int = 64, pw: int = 64) -> np.nd
     return out
 
 
-def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph: int = 64, pw: int = 64):
-    """Frames (list or (F, H, W, 3)) -> (buffer, offsets) of F * n_patches blobs."""
-    patches = [p for f in frames for p in split_frame(np.asarray(f), ph, pw)]
-    return compress_batch(patches, model, config)
+def _groups(H: int, W: int, ph: int, pw: int):
+    """Shape groups of the patch grid: (row slice, col slice, n_rows, n_cols,
+    patch h, patch w) for the full patches and the ragged bottom row / right
+    column / corner (those that exist)."""
+    fh, fw = H // ph, W // pw
+    hr, wr = H - fh * ph, W - fw * pw
+    out = []
+    for rows, nr, h in ((slice(0, fh * ph), fh, ph), (slice(fh * ph, H), 1 if hr else 0, hr)):
+        for cols, nc, w in ((slice(0, fw * pw), fw, pw), (slice(fw * pw, W), 1 if wr else 0, wr)):
+            if nr and nc:
+                out.append((rows, cols, nr, nc, h, w))
+    return out
 
 
-def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None, ph: int = 64, pw: int = 64):
-    out = decompress_batch(buffer, offsets, model)
-    per = len(patch_grid(H, W, ph, pw))
-    if isinstance(out, np.ndarray):
-        out = list(out)
-    return np.stack([assemble(out[f * per:(f + 1) * per], H, W, ph, pw) for f in range(n_frames)])
+def _raster_index(H: int, W: int, ph: int, pw: int):
+    """For each group, the raster positions (within a frame) of its patches."""
+    fh, fw = H // ph, W // pw
+    ncols = fw + (1 if W - fw * pw else 0)
+    idx = []
+    for rows, cols, nr, nc, h, w in _groups(H, W, ph, pw):
+        r0 = 0 if rows.start == 0 else fh
+        c0 = 0 if cols.start == 0 else fw
+        rr, cc = np.meshgrid(np.arange(r0, r0 + nr), np.arange(c0, c0 + nc), indexing="ij")
+        idx.append((rr * ncols + cc).reshape(-1))
+    return idx
+
+
+def _group_patches(frames, g):
+    """(F*nr*nc, h, w, 3) patches of one shape group, raster order within it
+    (numpy array or device tensor)."""
+    rows, cols, nr, nc, h, w = g
+    F = frames.shape[0]
+    v = frames[:, rows, cols].reshape(F, nr, h, nc, w, 3)
+    if isinstance(v, torch.Tensor):
+        return v.permute(0, 1, 3, 2, 4, 5).contiguous().reshape(F * nr * nc, h, w, 3)
+    return np.ascontiguousarray(v.transpose(0, 1, 3, 2, 4, 5)).reshape(F * nr * nc, h, w, 3)
+
+
+def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph: int = 64, pw: int = 64,
+                    device=None):
+    """Frames (F, H, W, 3) -> (buffer, offsets) of F * n_patches blobs, frame
+    by frame, raster order within a frame. The frames go to the GPU once; each
+    shape group of the patch grid is cut there and compressed as one batch;
+    each (frame, group) run of blobs is copied from the device straight to its
+    place in the page-locked result (no host-side shuffling)."""
+    dev = require_device(device)
+    stream = torch.cuda.current_stream(dev)
+    frames_d = frames if isinstance(frames, torch.Tensor) else torch.from_numpy(np.asarray(frames, dtype=np.uint8))
+    frames_d = frames_d.to(dev)
+    F, H, W = frames_d.shape[:3]
+    groups = _groups(H, W, ph, pw)
+    ridx = _raster_index(H, W, ph, pw)
+    per = sum(len(r) for r in ridx)
+    parts = []
+    for g in groups:
+        out_d, off_d, _ = compress_batch(_group_patches(frames_d, g), model, config, device=dev, return_device=True)
+        parts.append((out_d, off_d))
+    offs_h = []
+    for out_d, off_d in parts:
+        h = pinned(off_d.numel() * 8)
+        with torch.cuda.stream(stream):
+            h.copy_(off_d.view(torch.uint8), non_blocking=True)
+        offs_h.append(h)
+    stream.synchronize()
+    goffs = [h.numpy().view(np.uint64) for h in offs_h]
+    sizes = np.zeros((F, per), np.uint64)
+    for off, r in zip(goffs, ridx):
+        sizes[:, r] = np.diff(off).reshape(F, -1)
+    offsets = np.zeros(F * per + 1, np.uint64)
+    np.cumsum(sizes.reshape(-1), out=offsets[1:])
+    host = pinned(int(offsets[-1]) + 8)
+    with torch.cuda.stream(stream):
+        for (out_d, _), off, r in zip(parts, goffs, ridx):
+            k = len(r)
+            for f in range(F):
+                if bool(np.all(np.diff(r) == 1)):  # one run per frame
+                    runs = [(0, k)]
+                else:
+                    runs = [(j, j + 1) for j in range(k)]
+                for j0, j1 in runs:
+                    s0, s1 = int(off[f * k + j0]), int(off[f * k + j1])
+                    d0 = int(offsets[f * per + r[j0]])
+                    host[d0:d0 + s1 - s0].copy_(out_d[s0:s1], non_blocking=True)
+    stream.synchronize()
+    return host.numpy()[: int(offsets[-1])], offsets
+
+
+def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None, ph: int = 64, pw: int = 64,
+                      device=None):
+    """Inverse of compress_frames: the blob buffer goes to the GPU once, each
+    shape group is gathered there (device copies of its (frame, group) runs),
+    decoded as one batch, written into device frames, and the frames come
+    back in one copy."""
+    dev = require_device(device)
+    stream = torch.cuda.current_stream(dev)
+    buffer = np.asarray(buffer, dtype=np.uint8)
+    offsets = np.asarray(offsets, dtype=np.uint64)
+    groups = _groups(H, W, ph, pw)
+    ridx = _raster_index(H, W, ph, pw)
+    per = sum(len(r) for r in ridx)
+    F = n_frames
+    buf_d = h2d(buffer[: int(offsets[F * per])], dev, stream)
+    frames_d = torch.empty((F, H, W, 3), dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(stream):
+        for g, r in zip(groups, ridx):
+            rows, cols, nr, nc, h, w = g
+            k = len(r)
+            pos = (np.arange(F)[:, None] * per + r[None, :]).reshape(-1)
+            lens = offsets[pos + 1] - offsets[pos]
+            goff = np.zeros(F * k + 1, np.uint64)
+            np.cumsum(lens, out=goff[1:])
+            gbuf = torch.empty(int(goff[-1]) + 16, dtype=torch.uint8, device=dev)
+            gbuf[int(goff[-1]):].zero_()
+            contiguous = bool(np.all(np.diff(r) == 1))
+            for f in range(F):
+                runs = [(0, k)] if contiguous else [(j, j + 1) for j in range(k)]
+                for j0, j1 in runs:
+                    s0, s1 = int(offsets[f * per + r[j0]]), int(offsets[f * per + r[j1 - 1] + 1])
+                    d0 = int(goff[f * k + j0])
+                    gbuf[d0:d0 + s1 - s0].copy_(buf_d[s0:s1], non_blocking=True)
+            goff_d = torch.from_numpy(goff.view(np.int64)).to(dev, non_blocking=False)
+            results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, stream)
+            errors = _resolve_errors(results, errors, hdr)
+            if errors:
+                raise errors[min(errors)]
+            img = results[0][1]
+            frames_d[:, rows, cols] = img.reshape(F, nr, nc, h, w, 3).permute(0, 1, 3, 2, 4, 5).reshape(
+                F, nr * h, nc * w, 3)
+    host = pinned(frames_d.numel())
+    with torch.cuda.stream(stream):
+        host.copy_(frames_d.view(-1), non_blocking=True)
+    stream.synchronize()
+    return host.numpy().reshape(F, H, W, 3)

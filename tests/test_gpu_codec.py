@@ -386,3 +386,20 @@ def test_tcgen05_decoder_deterministic(full_model):
     sub = [t.cpu().numpy() for t in vqvae.decode_head_device(torch.from_numpy(idx[:3]).to(dev), full_model, 32, 32,
                                                              default_grid(), dev, s)]
     assert all(np.array_equal(a[:3], b) for a, b in zip(ref, sub))
+
+
+def test_frames_as_patch_containers(small_model):
+    """BASELINE config 4: frames split into patch containers. Blobs come out
+    frame by frame in raster order, byte-identical to compressing the patch
+    list, for grids with ragged bottom rows and right columns."""
+    from paper_2206_05279_b200 import patches as pt
+
+    cfg = pc.CodecConfig(backend="twar-vqvae")
+    for (H, W), (ph, pw) in (((100, 70), (32, 32)), ((64, 128), (64, 64))):
+        frames = smooth_images(2, H, W, seed=H + W)
+        buf, off = pt.compress_frames(frames, small_model, cfg, ph, pw)
+        plist = [p for f in frames for p in pt.split_frame(f, ph, pw)]
+        rbuf, roff = pc.compress_batch(plist, small_model, cfg)
+        assert np.array_equal(off, roff) and np.array_equal(buf, rbuf)
+        out = pt.decompress_frames(buf, off, 2, H, W, small_model, ph, pw)
+        assert np.array_equal(out, frames)
