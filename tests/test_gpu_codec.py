@@ -403,3 +403,15 @@ def test_frames_as_patch_containers(small_model):
         assert np.array_equal(off, roff) and np.array_equal(buf, rbuf)
         out = pt.decompress_frames(buf, off, 2, H, W, small_model, ph, pw)
         assert np.array_equal(out, frames)
+
+
+def test_indices_equal_reference_on_sample(full_model):
+    """Codebook indices of the production (tcgen05) encoder equal the
+    reference's -- the oracle's numpy/BLAS restatement, bit-identical to
+    pixelcodec on the same BLAS -- on 192 synthetic images (49152 latents);
+    tools/index_parity.py runs larger samples."""
+    om = O.Model.from_bytes(full_model.to_bytes())
+    imgs = smooth_images(192, 32, 32, seed=123)
+    gpu = np.stack([vqvae.encode_to_indices(im, full_model) for im in imgs])
+    ref = np.stack([O.encode_indices(im, om) for im in imgs])
+    assert int((gpu != ref).sum()) == 0
