@@ -177,17 +177,16 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
 
 // ---- decoder --------------------------------------------------------------
 // Backward bit reader, branch-free. Positions are bit indices relative to
-// the lane's first 16-byte chunk. `win` holds bits [L, L + 64) (L a multiple
-// of 32); before every pop at least 32 bits lie in [L, A), so a field of
-// b <= 12 bits is one 64-bit funnel shift. A pop that leaves fewer than 32
-// shifts in the next lower word from the register queue q (words consumed
-// w, z, y, x; k = words left); an empty queue reloads from a per-thread ring
-// of kRing shared-memory chunks that cp.async fills kAhead chunks ahead.
-// Lanes of a warp refill at different symbols, so everything here is
-// predicated rather than branched: a warp would otherwise run the refill
-// path at almost every symbol anyway. cp.async.wait_group runs once per
-// 16-symbol block (sync()): a block pops at most 192 bits = 1.5 chunks, and
-// the chunks it can need were committed at least kAhead - 2 groups ago.
+// the lane's first 16-byte chunk. The window (hi:lo) holds the cnt >= 32
+// unread bits just below position A, left-aligned, so a field of b <= 12
+// bits is `hi >> (32 - b)`: the state chain pays one 32-bit shift. A pop
+// that leaves fewer than 32 bits ORs in the next lower word (index wn),
+// read from a per-thread ring of kRing 16-byte chunk slots in shared memory
+// (one predicated 32-bit load). cp.async keeps the ring kAhead chunks ahead;
+// issuing and waiting happen once per 16-symbol block (sync()): a block pops
+// at most 192 bits = 6 words, so it touches at most two chunks, both issued
+// at least kAhead - 2 groups earlier. Lanes of a warp refill at different
+// symbols, so the per-symbol path is predicated rather than branched.
 constexpr int kRing = 8;
 constexpr int kAhead = 4;
 
@@ -196,27 +195,22 @@ struct BitReader {
     uint32_t ring_s;     // shared address of this thread's slot 0 (stride = blockDim.x * 16)
     uint32_t ring_stride;
     int hi_c;            // last chunk holding payload bits
-    int A, L, start, k, c;
-    uint32_t wlo, whi;   // window: bits [L, L + 32) and [L + 32, L + 64)
-    uint4 q;
+    int A, cnt, start, wn, ci;  // ci: lowest chunk issued to the ring
+    uint32_t hi, lo;     // window: bits [A - cnt, A), left-aligned (bit A-1 at bit 63 of hi:lo)
 
-    __device__ __forceinline__ uint4 direct(int ci) const {
-        return (ci >= 0 && ci <= hi_c) ? __ldg(base4 + ci) : make_uint4(0, 0, 0, 0);
+    __device__ __forceinline__ uint4 direct(int c) const {
+        return (c >= 0 && c <= hi_c) ? __ldg(base4 + c) : make_uint4(0, 0, 0, 0);
     }
     __device__ __forceinline__ static uint32_t pick(const uint4 &v, int j) {
         return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
     }
-    // cp.async chunk ci into its slot when `on` and ci is inside the lane;
-    // a group is committed either way
-    __device__ __forceinline__ void issue(int ci, bool on) {
-        const uint32_t pr = (on && ci >= 0 && ci <= hi_c) ? 1u : 0u;
-        const uint32_t dst = ring_s + (uint32_t)(ci & (kRing - 1)) * ring_stride;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
-            "@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}\n" ::"r"(dst),
-            "l"(base4 + ci), "r"(pr)
-            : "memory");
-        if (on) asm volatile("cp.async.commit_group;" ::: "memory");
+    __device__ __forceinline__ uint32_t word(int wi) const { return wi >= 0 ? pick(direct(wi >> 2), wi & 3) : 0u; }
+    __device__ __forceinline__ void issue(int c) {
+        if (c >= 0 && c <= hi_c) {
+            const uint32_t dst = ring_s + (uint32_t)(c & (kRing - 1)) * ring_stride;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(base4 + c) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     __device__ __forceinline__ void init(const uint4 *lane_base4, uint32_t my_ring_s, uint32_t stride_bytes,
                                          int start_bit, uint32_t nb) {
@@ -226,57 +220,46 @@ struct BitReader {
         start = start_bit;  // 0..127
         hi_c = nb ? (int)((start_bit + nb - 1) >> 7) : -1;
         A = start_bit + (int)nb;
-        const int wl = ((A - 1) >> 5) - 1;  // window = words wl, wl + 1 (wl may be -1)
-        L = wl * 32;
-        const int wt = wl + 1;
-        whi = pick(direct(wt >> 2), wt & 3);
-        wlo = wl >= 0 ? pick(direct(wl >> 2), wl & 3) : 0u;
-        const int wn = wl - 1;  // next word to bring in
-        c = wn >> 2;            // arithmetic: -1 for wn in [-4, -1]
-        const uint4 q0 = direct(c);
-        // queue holds words (wn & 3) .. 0 of chunk c, top word in q.w
-        k = (wn & 3) + 1;
-        q.w = pick(q0, k - 1);
-        q.z = k >= 2 ? pick(q0, k - 2) : 0u;
-        q.y = k >= 3 ? pick(q0, k - 3) : 0u;
-        q.x = k >= 4 ? q0.x : 0u;
-#pragma unroll
-        for (int j = 1; j <= kAhead; ++j) issue(c - j, true);
+        const int wt = (A - 1) >> 5;  // word holding bit A-1 (arithmetic: -1 when A == 0)
+        const int nt = A - 32 * wt;   // its valid bits, 1..32
+        const uint32_t w2 = word(wt - 1);
+        hi = (word(wt) << (32 - nt)) | (nt < 32 ? w2 >> nt : 0u);
+        lo = w2 << (32 - nt);
+        cnt = nt + 32;
+        wn = wt - 2;  // next word to bring in
+        ci = (wn >> 2) + 1;
+        sync();
     }
-    __device__ __forceinline__ void sync() const { asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 2) : "memory"); }
-    // pop b bits (b <= 12); underflow shows as A < start at the end
+    // once per 16-symbol block: keep the ring kAhead chunks below the
+    // current one, then wait for the chunks this block can touch
+    __device__ __forceinline__ void sync() {
+        const int target = (wn >> 2) - kAhead;
+#pragma unroll
+        for (int j = 0; j < kAhead + 1; ++j)
+            if (ci > target) issue(--ci);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 2) : "memory");
+    }
+    // pop b bits (1 <= b <= 12); underflow shows as A < start at the end
     __device__ __forceinline__ uint32_t take(uint32_t b) {
+        const uint32_t v = hi >> (32u - b);
+        hi = __funnelshift_l(lo, hi, b);
+        lo <<= b;
+        cnt -= (int)b;
         A -= (int)b;
-        const uint32_t sh = (uint32_t)(A - L);
-        const uint32_t v = (uint32_t)((((uint64_t)whi << 32) | wlo) >> sh) & ((1u << b) - 1u);  // 20 <= sh < 64
-        const bool p = sh < 32u;
-        // refill: window down one word, queue shifts
-        whi = p ? wlo : whi;
-        wlo = p ? q.w : wlo;
-        L = p ? L - 32 : L;
-        q.w = p ? q.z : q.w;
-        q.z = p ? q.y : q.z;
-        q.y = p ? q.x : q.y;
-        k = p ? k - 1 : k;
-        // empty queue: next chunk from the ring, one more cp.async
-        const bool r = p && k == 0;
-        const int cn = c - 1;
-        const uint32_t src = ring_s + (uint32_t)(cn & (kRing - 1)) * ring_stride;
-        uint4 nq = q;
+        // refill below the valid bits (lo is zero here) with word wn
+        const bool p = cnt < 32;
+        const uint32_t src = ring_s + (uint32_t)((wn >> 2) & (kRing - 1)) * ring_stride + (uint32_t)(wn & 3) * 4u;
+        uint32_t w = 0;
         asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
-            "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}\n"
-            : "+r"(nq.x), "+r"(nq.y), "+r"(nq.z), "+r"(nq.w)
-            : "r"(src), "r"(r ? 1u : 0u)
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}\n"
+            : "+r"(w)
+            : "r"(src), "r"(p ? 1u : 0u)
             : "memory");
-        const bool inl = cn >= 0 && cn <= hi_c;
-        q.x = r ? (inl ? nq.x : 0u) : q.x;
-        q.y = r ? (inl ? nq.y : 0u) : q.y;
-        q.z = r ? (inl ? nq.z : 0u) : q.z;
-        q.w = r ? (inl ? nq.w : 0u) : q.w;
-        k = r ? 4 : k;
-        c = r ? cn : c;
-        issue(cn - kAhead, r);
+        const uint32_t sh = (uint32_t)cnt & 31u;
+        hi = p ? (hi | (w >> sh)) : hi;
+        lo = p ? (w << (32u - sh)) : lo;
+        cnt = p ? cnt + 32 : cnt;
+        wn = p ? wn - 1 : wn;
         return v;
     }
 };
