@@ -149,6 +149,9 @@ def run_reference(args):
 
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled on a thread while the timed
+    region runs (NVML, ~5 ms period; nvidia-smi as fallback). One sample is
+    taken on entry and one on exit, so even a short region has samples."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -158,40 +161,49 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
+        self._nv = None
         try:  # NVML polls in microseconds; nvidia-smi takes ~0.1 s per sample
             import pynvml
 
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
             bits = (pynvml.nvmlClocksThrottleReasonHwSlowdown, pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
                     pynvml.nvmlClocksThrottleReasonSwThermalSlowdown, pynvml.nvmlClocksThrottleReasonSwPowerCap)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            while not self._stop.is_set():
+            self._nv = (pynvml, h, bits, pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nv = None
+
+    def _sample(self):
+        if self._nv is not None:
+            pynvml, h, bits, mx = self._nv
+            try:
                 r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 self.samples.append([str(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), str(mx)]
                                     + ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.01)
-            return
-        except Exception:
-            pass
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                return
             except Exception:
                 pass
-            self._stop.wait(0.2)
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            if out:
+                self.samples.append([x.strip() for x in out.split(",")])
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            self._stop.wait(0.005 if self._nv is not None else 0.2)
 
     def __enter__(self):
+        self._sample()
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        self._sample()
         self._stop.set()
         self._t.join(timeout=10)
 
