@@ -90,7 +90,32 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
         const uint8_t *cd = coded + n * hw3;
         const uint8_t *sh = shift ? shift + n * hw3 : nullptr;
         uint8_t *o_g = out + n * hw3;
-        uint8_t *o = stage_in_smem ? s_img + (int64_t)warp * hw3 : o_g;
+        uint8_t *o = stage_in_smem ? s_img + (int64_t)warp * 2 * hw3 : o_g;
+        const bool vec = stage_in_smem && ((hw3 | reinterpret_cast<uintptr_t>(cd) | reinterpret_cast<uintptr_t>(o_g) |
+                                            (sh ? reinterpret_cast<uintptr_t>(sh) : 0)) & 15) == 0;
+        if (stage_in_smem) {
+            // stage the un-recentred residual t in shared memory (coalesced
+            // 16-byte loads): the wavefront below reads it at smem latency
+            uint8_t *tb = o + hw3;
+            if (vec) {
+                for (int64_t i = 16 * lane; i < hw3; i += 512) {
+                    uint4 c4 = *reinterpret_cast<const uint4 *>(cd + i);
+                    if (sh) {
+                        const uint4 s4 = *reinterpret_cast<const uint4 *>(sh + i);
+                        uint32_t *cw = reinterpret_cast<uint32_t *>(&c4);
+                        const uint32_t *sw = reinterpret_cast<const uint32_t *>(&s4);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) cw[e] = __vadd4(__vadd4(cw[e], sw[e]), 0x80808080u);  // bytewise mod 256
+                    }
+                    *reinterpret_cast<uint4 *>(tb + i) = c4;
+                }
+            } else {
+                for (int64_t i = lane; i < hw3; i += 32) tb[i] = (uint8_t)unrec(cd, sh, i);
+            }
+            __syncwarp();
+            cd = tb;
+            sh = nullptr;
+        }
         // ---- red: skewed wavefront per strip of 32 rows
         for (int u0 = 0; u0 < H; u0 += 32) {
             const int u = u0 + lane;
@@ -149,8 +174,13 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
             __syncwarp();
         }
         if (stage_in_smem) {
-            // coalesced copy-out, 4 bytes per lane when aligned
-            for (int64_t i = lane; i < hw3; i += 32) o_g[i] = o[i];
+            // coalesced copy-out, 16 bytes per lane when aligned
+            if (vec) {
+                for (int64_t i = 16 * lane; i < hw3; i += 512)
+                    *reinterpret_cast<uint4 *>(o_g + i) = *reinterpret_cast<const uint4 *>(o + i);
+            } else {
+                for (int64_t i = lane; i < hw3; i += 32) o_g[i] = o[i];
+            }
             __syncwarp();
         }
     }
@@ -191,8 +221,8 @@ extern "C" int pilc_twar_decode(const uint8_t *coded, const uint8_t *shift, uint
     if (n_img < 0 || H < 1 || W < 1 || !params12_host) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     const int64_t hw3 = (int64_t)H * W * 3;
-    const int stage = hw3 * kDecWarps <= 200 * 1024;
-    const size_t smem = stage ? (size_t)(hw3 * kDecWarps) : 0;
+    const int stage = 2 * hw3 * kDecWarps <= 200 * 1024;  // output + staged residual per warp
+    const size_t smem = stage ? (size_t)(2 * hw3 * kDecWarps) : 0;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(twar_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t blocks = ceil_div64(n_img, kDecWarps);
