@@ -230,7 +230,8 @@ int pilc_container_pack(const uint8_t *tmpl, int32_t template_len,
                         const uint16_t *res_states, const uint64_t *blob_off,
                         uint8_t *out, void *stream);
 /* Parse + validate n_blob blobs laid end to end in buf (blob i spans
- * [blob_off[i], blob_off[i+1])), including the crc32 trailer. params_hash
+ * [blob_off[i], blob_off[i+1])), including the crc32 trailer; buf must be
+ * readable 16 bytes past the last blob (vector reads). params_hash
  * and model_hash are the expected 8-byte digests read as little-endian
  * uint64. Writes hdr[i]. */
 int pilc_container_parse(const uint8_t *buf, const uint64_t *blob_off,

@@ -119,22 +119,81 @@ __device__ inline uint32_t warp_xor(uint32_t v) {
     return v;
 }
 
-// Whole-warp crc32 of [p, p+n). stage: 32*64 + 64 bytes of this warp's smem.
-__device__ inline uint32_t warp_crc32(const CrcConsts *cc, const uint8_t *p, uint64_t n,
-                                      uint8_t *stage) {
+// Slice-by-4 tables T1..T3 (T0 = CrcConsts::tab), built in shared memory.
+struct CrcSlices {
+    uint32_t t[3][256];
+};
+
+__device__ inline void build_crc_slices(CrcSlices *sl, const uint32_t *t0) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t c = t0[i];
+        c = (c >> 8) ^ t0[c & 0xFF];
+        sl->t[0][i] = c;
+        c = (c >> 8) ^ t0[c & 0xFF];
+        sl->t[1][i] = c;
+        c = (c >> 8) ^ t0[c & 0xFF];
+        sl->t[2][i] = c;
+    }
+}
+
+// crc32 of n <= 64 bytes at a 4-byte aligned smem address, slice-by-4
+__device__ inline uint32_t crc_chunk4(const uint32_t *t0, const CrcSlices *sl, const uint8_t *p, int n) {
+    uint32_t c = 0xFFFFFFFFu;
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(p);
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {
+        c ^= w[j >> 2];
+        c = sl->t[2][c & 0xFF] ^ sl->t[1][(c >> 8) & 0xFF] ^ sl->t[0][(c >> 16) & 0xFF] ^ t0[c >> 24];
+    }
+    for (; j < n; ++j) c = t0[(c ^ p[j]) & 0xFF] ^ (c >> 8);
+    return c ^ 0xFFFFFFFFu;
+}
+
+// Whole-warp crc32 of [p, p+n). stage: 32*68 + 64 bytes of this warp's smem.
+// VEC: the bytes are fetched with 16-byte loads from the enclosing aligned
+// vectors, so the source must be readable up to 15 bytes past p+n (the
+// container buffers carry a 16-byte pad); chunks then use slice-by-4 (sl).
+template <bool VEC = false>
+__device__ inline uint32_t warp_crc32(const CrcConsts *cc, const uint8_t *p, uint64_t n, uint8_t *stage,
+                                      const CrcSlices *sl = nullptr) {
     const int lane = threadIdx.x & 31;
     uint32_t crc = 0;  // crc32 of the empty string
     uint64_t done = 0;
     while (done < n) {
         const uint64_t rem = n - done;
         const int rb = rem >= 2048 ? 2048 : (int)rem;
-        // coalesced byte loads into smem, chunk i at stage + i*68 (padded)
-        for (int j = lane; j < rb; j += 32) stage[(j >> 6) * 68 + (j & 63)] = p[done + j];
+        // chunk i of the round at stage + i*68 (padded: conflict-free per-lane reads)
+        if constexpr (VEC) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(p + done);
+            const uint4 *a0 = reinterpret_cast<const uint4 *>(a & ~(uintptr_t)15);
+            const int lead = (int)(a & 15);
+            const int nv = (lead + rb + 15) >> 4;
+            uint4 v[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const int vi = lane + 32 * k;
+                v[k] = vi < nv ? a0[vi] : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const int vi = lane + 32 * k;
+                const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int idx = 16 * vi + e - lead;
+                    if (idx >= 0 && idx < rb) stage[(idx >> 6) * 68 + (idx & 63)] = (uint8_t)(w4[e >> 2] >> (8 * (e & 3)));
+                }
+            }
+        } else {
+            for (int j = lane; j < rb; j += 32) stage[(j >> 6) * 68 + (j & 63)] = p[done + j];
+        }
         __syncwarp();
         const int beg = lane * 64;
         int len = rb - beg;
         len = len < 0 ? 0 : (len > 64 ? 64 : len);
-        uint32_t c = crc_bytes(cc->tab, stage + lane * 68, len);
+        uint32_t c;
+        if constexpr (VEC) c = crc_chunk4(cc->tab, sl, stage + lane * 68, len);
+        else c = crc_bytes(cc->tab, stage + lane * 68, len);
         uint32_t term;
         if (rb == 2048) {
             term = crc_multmodp(cc->qpow[31 - lane], c);

@@ -231,8 +231,11 @@ __device__ uint32_t sched_crc_warp(const CrcConsts *cc, const uint8_t *dsched, u
 
 __global__ void __launch_bounds__(32 * kWarps) pack_kernel(PackArgs a, CrcConsts ccv) {
     __shared__ CrcConsts cc;
-    __shared__ uint8_t stage[kWarps][kStage];
+    __shared__ CrcSlices sl;
+    __shared__ __align__(16) uint8_t stage[kWarps][kStage];
     load_crc_consts(&cc, ccv);
+    __syncthreads();
+    build_crc_slices(&sl, cc.tab);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = a.lanes;
@@ -268,7 +271,8 @@ __global__ void __launch_bounds__(32 * kWarps) pack_kernel(PackArgs a, CrcConsts
         }
         __syncwarp();
         __threadfence_block();
-        const uint32_t crc = warp_crc32(&cc, blob, size - 4, stage[warp]);
+        // the output buffer carries 16 bytes of slack (pilc.h): vector reads
+        const uint32_t crc = warp_crc32<true>(&cc, blob, size - 4, stage[warp], &sl);
         if (lane == 0) wr_u32(blob + size - 4, crc);
     }
 }
@@ -280,8 +284,11 @@ __global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__res
                                                             uint64_t model_hash, int has_model,
                                                             pilc_header *hdr, CrcConsts ccv) {
     __shared__ CrcConsts cc;
-    __shared__ uint8_t stage[kWarps][kStage];
+    __shared__ CrcSlices sl;
+    __shared__ __align__(16) uint8_t stage[kWarps][kStage];
     load_crc_consts(&cc, ccv);
+    __syncthreads();
+    build_crc_slices(&sl, cc.tab);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < n_blob;
@@ -298,7 +305,8 @@ __global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__res
             h.aux = b[4];
         }
         if (!st) {
-            const uint32_t crc = warp_crc32(&cc, b, n - 4, stage[warp]);
+            // blob buffers are padded by 16 bytes (pilc.h): vector reads
+            const uint32_t crc = warp_crc32<true>(&cc, b, n - 4, stage[warp], &sl);
             if (crc != rd_u32(b + n - 4)) st = PILC_ST_CRC;
         }
         // sequential structure walk (lane 0), mirroring _Reader.take
