@@ -265,6 +265,7 @@ def run_gpu(args):
         for img_d in groups_d:
             out_d, off_d = ct._compress_device(img_d, model, cfg, dev, stream)
             results, errors, hdr = ct._decompress_device(out_d, off_d, img_d.shape[0], model, dev, stream)
+            ct._verify(results)  # the speculated summary matched (raises otherwise)
             outs.append((off_d.cpu().numpy().view(np.uint64), results, errors))
         return outs
 

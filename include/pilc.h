@@ -256,10 +256,13 @@ int pilc_container_summary(const uint8_t *buf, const uint64_t *blob_off,
 /* Per-lane extraction for a group of blobs sharing (lanes, backend):
  * blob_idx[g] selects the blob; for stream 0 (index) / 1 (residual) the
  * lane payload offset (absolute, into buf), bit count and state are
- * written at [g*lanes + l], with the _read_lanes checks in lane_status. */
+ * written at [g*lanes + l], with the _read_lanes checks in lane_status.
+ * Blobs whose lane count, or M / D when expect_M / expect_D are nonzero,
+ * differ from the group's get a nonzero lane status (the coder skips them). */
 int pilc_container_lanes(const uint8_t *buf, const uint64_t *blob_off,
                          const pilc_header *hdr, const int64_t *blob_idx,
                          int64_t n_group, int32_t lanes, int32_t stream_id,
+                         int32_t expect_M, int32_t expect_D,
                          uint64_t *lane_off, uint32_t *nbits, uint16_t *states,
                          uint8_t *lane_status, void *stream);
 /* crc32 (zlib polynomial) of [off[i], off[i] + len[i]) into crc[i]. */

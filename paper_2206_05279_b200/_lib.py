@@ -39,7 +39,7 @@ _SIGS = {
     "pilc_container_sizes": (ctypes.c_int, [P, P, I64, I32, I64, P, P, P]),
     "pilc_container_pack": (ctypes.c_int, [P, I32, P, P, I32, I64, I64, I32, P, I64, P, P, P, I64, P, P, P, P, P]),
     "pilc_container_parse": (ctypes.c_int, [P, P, I64, ctypes.c_uint64, ctypes.c_uint64, I32, P, P]),
-    "pilc_container_lanes": (ctypes.c_int, [P, P, P, P, I64, I32, I32, P, P, P, P, P]),
+    "pilc_container_lanes": (ctypes.c_int, [P, P, P, P, I64, I32, I32, I32, I32, P, P, P, P, P]),
     "pilc_container_summary": (ctypes.c_int, [P, P, P, I64, P, P]),
     "pilc_crc32": (ctypes.c_int, [P, P, P, I64, P, P]),
     "pilc_sched_crc": (ctypes.c_int, [P, P, I64, I64, P, P]),

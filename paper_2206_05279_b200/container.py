@@ -292,10 +292,9 @@ def _lane_error(status_row: np.ndarray) -> Exception | None:
     return None
 
 
-def _parse_device(buf_d, off_d, n, model, dev, stream):
-    """Parse every header on the device; returns the device header array and
-    the batch summary (one small pinned read: status count, one-group flag,
-    blob 0's header and grid bytes)."""
+def _parse_begin(buf_d, off_d, n, model, dev, stream):
+    """Queue the header parse and the batch summary (with its pinned read-back)
+    on `stream`; returns (hdr_d, summary pinned tensor, event)."""
     params = _params_of(model)
     ph = int(np.frombuffer(params.hash8(), "<u8")[0])
     has_model = model is not None and model.has_network
@@ -308,7 +307,17 @@ def _parse_device(buf_d, off_d, n, model, dev, stream):
     host = pinned(summ_d.numel())
     with torch.cuda.stream(stream):
         host.copy_(summ_d, non_blocking=True)
-    stream.synchronize()
+        ev = torch.cuda.Event()
+        ev.record(stream)
+    return hdr_d, host, ev
+
+
+def _parse_device(buf_d, off_d, n, model, dev, stream):
+    """Parse every header on the device; returns the device header array and
+    the batch summary (one small pinned read: status count, one-group flag,
+    blob 0's header and grid bytes)."""
+    hdr_d, host, ev = _parse_begin(buf_d, off_d, n, model, dev, stream)
+    ev.synchronize()
     return hdr_d, host.numpy().view(_lib.SUMMARY_DTYPE)[0].copy()
 
 
@@ -329,18 +338,75 @@ def _grid_of(buf_host, buf_d, off, h) -> ScaleGrid:
     return ScaleGrid.from_bytes(raw)[0]
 
 
-def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_host=None):
+# Speculation: the one-group summary of the last batch decoded per (device,
+# batch size, model). A batch that matches it is decoded without waiting for
+# its own summary (the decode kernels are queued right behind the parse);
+# the summary is checked afterwards (_verify) and a mismatch redoes the batch
+# on the exact path. Wrong guesses are safe: every kernel is bounded by the
+# buffers sized from the guess and by each blob's own parsed header.
+_SPEC: dict = {}
+_SPEC_KEYS = ("width", "height", "backend", "M", "lanes", "flags", "D", "grid_crc")
+
+
+class SpeculationMiss(Exception):
+    """The batch did not match the speculated one-group summary."""
+
+
+def _spec_key(dev, n, model):
+    return (dev.index, n, model.hash8() if model is not None and model.has_network else None)
+
+
+def _summary_fast(summ, model) -> bool:
+    h0 = summ["h0"]
+    has_model = model is not None and model.has_network
+    return (int(summ["n_bad"]) == 0 and int(summ["uniform"]) == 1 and not (int(h0["flags"]) & FLAG_SCHEDULE_CHECKSUM)
+            and (int(h0["backend"]) != BACKEND_VQVAE or has_model))
+
+
+def _verify(results):
+    """Check the speculated summary of a batch (blocks until its summary is
+    back); raises SpeculationMiss when the batch differs from the guess."""
+    pending = getattr(results, "pending", None)
+    if pending is None:
+        return
+    summ_h, ev, spec = pending
+    results.pending = None
+    ev.synchronize()
+    summ = summ_h.numpy().view(_lib.SUMMARY_DTYPE)[0]
+    ok = int(summ["n_bad"]) == 0 and int(summ["uniform"]) == 1 and all(
+        int(summ["h0"][k]) == int(spec["h0"][k]) for k in _SPEC_KEYS)
+    ok = ok and bytes(summ["grid"][: 2 + 8 * int(spec["h0"]["D"])]) == bytes(spec["grid"][: 2 + 8 * int(spec["h0"]["D"])])
+    if not ok:
+        raise SpeculationMiss()
+
+
+class _Results(list):
+    pending = None
+
+
+def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_host=None, speculate=True):
     """Decode all n blobs. Returns (images: list of (ids, device tensor,
     lane statuses, schedule crcs, L), errors: dict blob -> Exception, host
     headers or None). One small host read (the batch summary) when every
-    blob parses and shares one shape / config; otherwise every header is read
-    and the blobs are grouped on the host."""
-    hdr_d, summ = _parse_device(buf_d, off_d, n, model, dev, stream)
+    blob parses and shares one shape / config -- none before the decode
+    kernels when the batch matches the last one (speculation, checked by
+    _verify); otherwise every header is read and the blobs are grouped on the
+    host."""
+    key = _spec_key(dev, n, model)
+    spec = _SPEC.get(key) if speculate else None
+    pending = None
+    if spec is not None:
+        hdr_d, summ_h, ev = _parse_begin(buf_d, off_d, n, model, dev, stream)
+        summ = spec
+        pending = (summ_h, ev, spec)
+    else:
+        hdr_d, summ = _parse_device(buf_d, off_d, n, model, dev, stream)
     has_model = model is not None and model.has_network
     h0 = summ["h0"]
     errors: dict = {}
-    fast = (int(summ["n_bad"]) == 0 and int(summ["uniform"]) == 1 and not (int(h0["flags"]) & FLAG_SCHEDULE_CHECKSUM)
-            and (int(h0["backend"]) != BACKEND_VQVAE or has_model))
+    fast = _summary_fast(summ, model)
+    if fast and spec is None:
+        _SPEC[key] = summ
     hdr = None
     if fast:
         grid = ScaleGrid.from_bytes(bytes(summ["grid"][: 2 + 8 * int(h0["D"])]))[0]
@@ -397,8 +463,8 @@ def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_
             nb = torch.empty(ng * L, dtype=torch.int32, device=dev)
             ss = torch.empty(ng * L, dtype=torch.int16, device=dev)
             ls = torch.empty(ng * L, dtype=torch.uint8, device=dev)
-            _lib.call("pilc_container_lanes", ptr(buf_d), ptr(off_d), ptr(hdr_d), ptr(ids_d), ng, L, 0, ptr(lo),
-                      ptr(nb), ptr(ss), ptr(ls), sptr(stream))
+            _lib.call("pilc_container_lanes", ptr(buf_d), ptr(off_d), ptr(hdr_d), ptr(ids_d), ng, L, 0, M, grid.D,
+                      ptr(lo), ptr(nb), ptr(ss), ptr(ls), sptr(stream))
             idx = torch.zeros((ng, gh, gw), dtype=torch.uint8, device=dev)
             _lib.call("pilc_rans_decode", ptr(buf_d), ptr(lo), ptr(nb), ptr(ss), None, None, ng, gh * gw, L,
                       ptr(idx_dec.device_words(dev)), idx_dec.D, M, None, ptr(idx), ptr(ls), sptr(stream))
@@ -415,8 +481,8 @@ def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_
         nb = torch.empty(ng * L, dtype=torch.int32, device=dev)
         ss = torch.empty(ng * L, dtype=torch.int16, device=dev)
         ls = torch.empty(ng * L, dtype=torch.uint8, device=dev)
-        _lib.call("pilc_container_lanes", ptr(buf_d), ptr(off_d), ptr(hdr_d), ptr(ids_d), ng, L, 1, ptr(lo),
-                  ptr(nb), ptr(ss), ptr(ls), sptr(stream))
+        _lib.call("pilc_container_lanes", ptr(buf_d), ptr(off_d), ptr(hdr_d), ptr(ids_d), ng, L, 1, M, grid.D,
+                  ptr(lo), ptr(nb), ptr(ss), ptr(ls), sptr(stream))
         t = torch.zeros((ng, H, W, 3), dtype=torch.uint8, device=dev)
         _lib.call("pilc_rans_decode", ptr(buf_d), ptr(lo), ptr(nb), ptr(ss), ptr(dsel), ptr(d_img), ng, n_sym, L,
                   ptr(res_dec.device_words(dev)), res_dec.D, M, ptr(shift), ptr(t), ptr(ls), sptr(stream))
@@ -424,7 +490,9 @@ def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_
         params = _params_of(model)
         img = decode_device(t, params, stream)
         results.append((ids, img, lane_st, sched, L))
-    return results, errors, hdr
+    out = _Results(results)
+    out.pending = pending
+    return out, errors, hdr
 
 
 class _ArangeIds:
@@ -488,6 +556,11 @@ def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=
     buf_d = h2d(buf_host[: int(offs[-1])], dev, stream, pad=16)
     off_d = h2d(offs.view(np.uint8), dev, stream).view(torch.int64)
     results, errors, hdr = _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host, offs)
+    try:
+        _verify(results)
+    except SpeculationMiss:
+        results, errors, hdr = _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host, offs,
+                                                  speculate=False)
     errors = _resolve_errors(results, errors, hdr)
     if errors and raise_on_error:
         raise errors[min(errors)]

@@ -442,9 +442,9 @@ __global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__res
 // ---- lanes (container.py:261-271, bits.py:75-85) -------------------------
 __global__ void lanes_kernel(const uint8_t *__restrict__ buf, const uint64_t *__restrict__ blob_off,
                              const pilc_header *__restrict__ hdr, const int64_t *__restrict__ blob_idx,
-                             int64_t n_group, int lanes, int stream_id, uint64_t *__restrict__ lane_off,
-                             uint32_t *__restrict__ nbits, uint16_t *__restrict__ states,
-                             uint8_t *__restrict__ lane_status) {
+                             int64_t n_group, int lanes, int stream_id, int expect_M, int expect_D,
+                             uint64_t *__restrict__ lane_off, uint32_t *__restrict__ nbits,
+                             uint16_t *__restrict__ states, uint8_t *__restrict__ lane_status) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t g = (int64_t)blockIdx.x * kWarps + warp; g < n_group;
          g += (int64_t)gridDim.x * kWarps) {
@@ -454,7 +454,11 @@ __global__ void lanes_kernel(const uint8_t *__restrict__ buf, const uint64_t *__
         const uint32_t M = h.M;
         const uint32_t tab = stream_id == 0 ? h.idx_table_off : h.res_table_off;
         uint64_t start = h.payload_off + (stream_id == 0 ? 0 : h.idx_bytes);
-        const bool ok = h.status == 0 && tab != 0;
+        // blobs whose lane count / precision / grid size differ from the
+        // group's (a speculated group, container.py) are rejected here, so the
+        // coder never indexes its tables with another blob's parameters
+        const bool ok = h.status == 0 && tab != 0 && h.lanes == (uint32_t)lanes &&
+                        (expect_M == 0 || h.M == (uint32_t)expect_M) && (expect_D == 0 || h.D == (uint32_t)expect_D);
         // lane wire sizes -> running offsets, 32 lanes at a time
         for (int l0 = 0; l0 < lanes; l0 += 32) {
             const int l = l0 + lane;
@@ -654,15 +658,16 @@ extern "C" int pilc_container_summary(const uint8_t *buf, const uint64_t *blob_o
 
 extern "C" int pilc_container_lanes(const uint8_t *buf, const uint64_t *blob_off,
                                     const pilc_header *hdr, const int64_t *blob_idx, int64_t n_group,
-                                    int32_t lanes, int32_t stream_id, uint64_t *lane_off,
-                                    uint32_t *nbits, uint16_t *states, uint8_t *lane_status,
+                                    int32_t lanes, int32_t stream_id, int32_t expect_M, int32_t expect_D,
+                                    uint64_t *lane_off, uint32_t *nbits, uint16_t *states, uint8_t *lane_status,
                                     void *stream) {
     if (n_group < 0 || lanes < 1 || (stream_id != 0 && stream_id != 1)) return PILC_E_ARG;
     if (n_group == 0) return PILC_OK;
 {
         ProfScope _ps(PROF_LANES, as_stream(stream), (double)n_group * lanes);
         lanes_kernel<<<warp_grid(n_group), 32 * kWarps, 0, as_stream(stream)>>>(
-        buf, blob_off, hdr, blob_idx, n_group, lanes, stream_id, lane_off, nbits, states, lane_status);
+        buf, blob_off, hdr, blob_idx, n_group, lanes, stream_id, expect_M, expect_D, lane_off, nbits, states,
+        lane_status);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;

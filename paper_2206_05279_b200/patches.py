@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .container import CodecConfig, _decompress_device, _resolve_errors, compress_batch
+from .container import CodecConfig, SpeculationMiss, _decompress_device, _resolve_errors, _verify, compress_batch
 from .device import h2d, pinned, require_device
 
 
@@ -156,6 +156,10 @@ def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None
                     gbuf[d0:d0 + s1 - s0].copy_(buf_d[s0:s1], non_blocking=True)
             goff_d = torch.from_numpy(goff.view(np.int64)).to(dev, non_blocking=False)
             results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, stream)
+            try:
+                _verify(results)
+            except SpeculationMiss:
+                results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, stream, speculate=False)
             errors = _resolve_errors(results, errors, hdr)
             if errors:
                 raise errors[min(errors)]

@@ -415,3 +415,24 @@ def test_indices_equal_reference_on_sample(full_model):
     gpu = np.stack([vqvae.encode_to_indices(im, full_model) for im in imgs])
     ref = np.stack([O.encode_indices(im, om) for im in imgs])
     assert int((gpu != ref).sum()) == 0
+
+
+def test_speculative_decode_misses_are_redone(small_model):
+    """decompress_batch queues the decode of a batch that looks like the last
+    one before its summary is read; a batch of another shape / config, or one
+    with a corrupt blob, must still decode exactly / raise exactly."""
+    cfg = pc.CodecConfig(backend="twar-vqvae")
+    a = smooth_images(24, 32, 32, seed=1)
+    b = smooth_images(24, 16, 48, seed=2)
+    ba, oa = pc.compress_batch(a, small_model, cfg)
+    bb, ob = pc.compress_batch(b, small_model, cfg)
+    bs, os_ = pc.compress_batch(a)  # static backend, same shape and count
+    for _ in range(2):
+        assert np.array_equal(pc.decompress_batch(ba, oa, small_model), a)
+        assert np.array_equal(pc.decompress_batch(bb, ob, small_model), b)
+        assert np.array_equal(pc.decompress_batch(bs, os_, small_model), a)
+    bad = np.array(ba, copy=True)
+    bad[int(oa[5]) + 150] ^= 0x04
+    with pytest.raises(pc.CodecError):
+        pc.decompress_batch(bad, oa, small_model)
+    assert np.array_equal(pc.decompress_batch(ba, oa, small_model), a)
