@@ -76,15 +76,24 @@ def _cpu_worker(args):
     return nbytes, time.perf_counter() - t0
 
 
-def cpu_oracle_run(per_proc: int, procs: int, seed0: int = 1000):
+def bench_model(name: str):
+    """--weights: `random` = random_weights(ModelConfig(), seed=1) (the
+    BASELINE config); `trained` = tests/golden/trained.pilw, the same
+    architecture briefly trained by the trainer port (one-code histogram)."""
+    import paper_2206_05279_b200 as pc
+
+    if name == "trained":
+        return pc.ModelWeights.load(os.path.join(REPO, "tests", "golden", "trained.pilw"))
+    return pc.random_weights(seed=1)
+
+
+def cpu_oracle_run(per_proc: int, procs: int, seed0: int = 1000, weights: str = "random"):
     """Times the oracle port on `procs` processes (one core each)."""
     import multiprocessing as mp
 
-    import paper_2206_05279_b200 as pc
-
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
         os.environ[k] = "1"
-    model_bytes = pc.random_weights(seed=1).to_bytes()
+    model_bytes = bench_model(weights).to_bytes()
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
         pool.map(_cpu_worker, [(seed0 + i, 1, model_bytes) for i in range(procs)])  # spawn + warm-up
@@ -96,9 +105,9 @@ def cpu_oracle_run(per_proc: int, procs: int, seed0: int = 1000):
     return nbytes / 1e6 / wall, nbytes, wall
 
 
-def cpu_sample_size(procs: int, target_s: float) -> int:
+def cpu_sample_size(procs: int, target_s: float, weights: str = "random") -> int:
     """Images per process so one oracle run lasts about target_s seconds."""
-    _, _, wall = cpu_oracle_run(2, procs)
+    _, _, wall = cpu_oracle_run(2, procs, weights=weights)
     return max(2, int(round(2 * target_s / max(wall, 1e-3))))
 
 
@@ -108,13 +117,13 @@ def run_reference(args):
         return 0
     procs = len(os.sched_getaffinity(0))
     # each step is a bounded sample; the whole run stays within ~3 minutes
-    per_proc = cpu_sample_size(procs, max(1.0, min(10.0, 150.0 / (args.steps + args.warmup))))
+    per_proc = cpu_sample_size(procs, max(1.0, min(10.0, 150.0 / (args.steps + args.warmup))), args.weights)
     vals = []
     for _ in range(args.warmup):
-        cpu_oracle_run(2, procs)
+        cpu_oracle_run(2, procs, weights=args.weights)
     t_all = 0.0
     for _ in range(args.steps):
-        v, nbytes, wall = cpu_oracle_run(per_proc, procs)
+        v, nbytes, wall = cpu_oracle_run(per_proc, procs, weights=args.weights)
         vals.append(v)
         t_all += wall
     value = statistics.median(vals)
@@ -132,7 +141,7 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f32/f64 (numpy+BLAS network), int (C coder)",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample_images_per_step": per_proc * procs},
+        "config": {"workload": WORKLOAD, "weights": args.weights, "sample_images_per_step": per_proc * procs},
         "cpu_baseline": {
             "value": round(value, 4), "unit": "MB/s", "cores": procs, "kind": "port",
             "sample": f"{per_proc} images/process x {procs} processes per step, oracle/ "
@@ -238,7 +247,7 @@ def run_gpu(args):
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream(dev)
-    model = pc.random_weights(seed=1)
+    model = bench_model(args.weights)
     cfg = pc.CodecConfig(backend="twar-vqvae")
     wl = WORKLOADS[args.workload]
     if args.workload == "1080p":
@@ -409,8 +418,8 @@ def run_gpu(args):
         cpu = None
         if ws == 1 and not args.no_cpu:
             procs = len(os.sched_getaffinity(0))
-            per_proc = cpu_sample_size(procs, 10.0)
-            v, nbytes, wall = cpu_oracle_run(per_proc, procs)
+            per_proc = cpu_sample_size(procs, 10.0, args.weights)
+            v, nbytes, wall = cpu_oracle_run(per_proc, procs, weights=args.weights)
             cpu = {"value": round(v, 4), "unit": "MB/s", "cores": procs, "kind": "port",
                    "sample": f"{per_proc * procs} CIFAR images ({nbytes} B) compress+decompress, oracle/ numpy+C, "
                              f"{procs} processes x 1 thread, {wall:.1f} s"}
@@ -428,7 +437,7 @@ def run_gpu(args):
             "dtype": "bf16 tcgen05 decoder, fp32-class encoder (3-product fp16 split on tcgen05), 3xTF32 + f64 argmin, "
                      "int coder/predictor/container",
             "data": "synthetic",
-            "config": {"workload": wl["desc"], "global_batch": wl["N"] * ws, "image": [wl["H"], wl["W"], 3],
+            "config": {"workload": wl["desc"], "weights": args.weights, "global_batch": wl["N"] * ws, "image": [wl["H"], wl["W"], 3],
                        "parallelism": f"shard{ws}", "l2": "flushed (256 MiB write) before each step"},
             "frame_decompress_latency_ms": lat,
             "compress_mb_s": round(raw_bytes * ws / 1e6 / t_cs, 3),
@@ -551,6 +560,8 @@ def main():
     ap.add_argument("--workload", default="cifar", choices=sorted(WORKLOADS) + ["coder"],
                     help="BASELINE config: cifar (configs[1], default), in64 (configs[2]), 1080p (configs[3]), "
                          "coder (configs[4], coder-only lane sweep)")
+    ap.add_argument("--weights", default="random", choices=["random", "trained"],
+                    help="random_weights(seed=1) (default) or tests/golden/trained.pilw")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

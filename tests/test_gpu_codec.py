@@ -436,3 +436,24 @@ def test_speculative_decode_misses_are_redone(small_model):
     with pytest.raises(pc.CodecError):
         pc.decompress_batch(bad, oa, small_model)
     assert np.array_equal(pc.decompress_batch(ba, oa, small_model), a)
+
+
+def test_trained_model_round_trip_and_vs_oracle():
+    """tests/golden/trained.pilw (trainer port, one-code index histogram):
+    indices equal the oracle's, containers within 0.5% of the oracle's size,
+    batch and single paths lossless -- including odd shapes."""
+    m = pc.ModelWeights.load(os.path.join(GOLDEN, "trained.pilw"))
+    om = O.Model.from_bytes(m.to_bytes())
+    cfg = pc.CodecConfig(backend="twar-vqvae")
+    imgs = smooth_images(64, 32, 32, seed=321)
+    buf, off = pc.compress_batch(imgs, m, cfg)
+    assert np.array_equal(pc.decompress_batch(buf, off, m), imgs)
+    for k in range(0, 64, 8):
+        assert np.array_equal(vqvae.encode_to_indices(imgs[k], m), O.encode_indices(imgs[k], om))
+        ref = O.compress(imgs[k], om, backend="twar-vqvae")
+        n = int(off[k + 1] - off[k])
+        assert abs(n - len(ref)) / len(ref) <= 0.005, (k, n, len(ref))
+    for shape in ((17, 33), (1, 1), (64, 8)):
+        img = smooth_images(1, *shape, seed=7)[0]
+        blob = pc.compress(img, m, cfg)
+        assert np.array_equal(pc.decompress(blob, m), img)
