@@ -23,6 +23,7 @@ I64 = ctypes.c_int64
 _SIGS = {
     "pilc_version": (ctypes.c_char_p, []),
     "pilc_device_arch": (ctypes.c_int, []),
+    "pilc_set_tuning": (ctypes.c_int, [I32, I32]),
     "pilc_twar_forward": (ctypes.c_int, [P, P, I64, I32, I32, P, P]),
     "pilc_twar_decode": (ctypes.c_int, [P, P, P, I64, I32, I32, P, P]),
     "pilc_rans_encode": (ctypes.c_int, [P, P, P, P, I64, I64, I32, P, I32, I32, I32, P, I64, P, P, P]),
@@ -111,6 +112,17 @@ def call(name: str, *args) -> int:
     if rc != 0:
         raise LibraryError(f"{name} failed with status {rc} ({['OK', 'E_ARG', 'E_CUDA', 'E_UNSUPPORTED'][rc] if rc < 4 else rc})")
     return rc
+
+
+TUNE_BLOCK_FUSION = 0
+
+
+def set_tuning(key: int, value: int) -> int:
+    """pilc_set_tuning: returns the previous value."""
+    prev = load().pilc_set_tuning(key, value)
+    if prev < 0:
+        raise ValueError(f"unknown tuning key {key}")
+    return prev
 
 
 def prof_reset(timing: bool) -> None:

@@ -36,6 +36,7 @@ enum ProfCat {
     PROF_GATHER,
     PROF_TC3_CONV,
     PROF_ENC_FRONT,
+    PROF_TC3_BLOCK,
     PROF_NCAT
 };
 void *prof_begin(int cat, cudaStream_t s, double units);
@@ -46,6 +47,10 @@ struct ProfScope {
     ProfScope(int cat, cudaStream_t st, double units) : s(st) { tok = prof_begin(cat, st, units); }
     ~ProfScope() { prof_end(tok, s); }
 };
+
+// Library tuning switches (pilc_set_tuning); defaults are the production path.
+enum { PILC_TUNE_BLOCK_FUSION = 0, PILC_TUNE_N };
+extern int g_tuning[PILC_TUNE_N];
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 

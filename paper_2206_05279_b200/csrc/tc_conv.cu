@@ -865,6 +865,307 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
     return PILC_OK;
 }
 
+// ---- one encoder residual block per launch (vqvae.py:60-62) -----------------
+// conv1 and conv2 of a block with the intermediate T = relu(conv1(X)) kept in
+// shared memory: per CTA iteration one image's padded X hi / lo rows (tile
+// halo included) come in by bulk copy, conv1's epilogue writes T hi / lo
+// (edge copies included) into shared memory, and conv2 reads it from there.
+// The arithmetic is exactly that of two tc3 ACT launches (same MMAs in the
+// same K order, same epilogue roundings, same per-image scales), so results
+// are bit-identical to the unfused path; what goes away is T's HBM round
+// trip and one launch.
+//
+// Schedule (one image i per iteration, T = ceil(Hp Wp / 128) tiles per
+// conv): MMA issues conv1 tiles of i, commits `xfree` (X(i+1) may load),
+// then conv2 tile j as soon as conv1 tiles j - 1 .. j + 1 are in T
+// (`hrdy[j]`, per tile). Accumulators alternate over a global tile counter
+// as in tc3; conv2 residual rows are loaded by the epilogue threads while
+// the MMAs run. The per-image max of T (the conv2 output bound) is reduced
+// through per-(tile, quarter) slots, double-buffered by image parity, and
+// read after `hready` (all conv1 epilogues of the image done).
+//
+// Measured (B200, 8192 CIFAR images): ~460 us per block vs 525 us for the
+// two tc3 launches. The epilogue (global fp32 + hi / lo stores, residual
+// loads) and the MMA issue loop (~115 cycles per h/l MMA pair against a
+// ~96-cycle operand floor) bound it, not the conv1 -> conv2 dependency.
+constexpr int kThreadsBK = 320;
+constexpr int kBkMaxTiles = 8;
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kThreadsBK, 1) tc3_block_kernel(Tc3Block L) {
+    constexpr int N = 32, N2 = 64, NH = 4, KG = 36;
+    constexpr uint32_t WB = KG * N2 * 16;
+    const int Wp = L.Wp, HW = L.Hp * Wp;
+    const int T = (HW + 127) >> 7;
+    const int M0 = (Wp + 1 + 7) & ~7;
+    const int RX = M0 + T * 128 + M0;
+    const uint32_t slab = (uint32_t)RX * 16u;
+    const int nrows = HW + 2 * (Wp + 1);
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_w1 = smem;
+    uint8_t *s_w2 = smem + WB;
+    uint8_t *s_x = smem + 2 * WB;
+    uint8_t *s_h = s_x + 8 * (size_t)slab;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_h + 8 * (size_t)slab);
+    uint64_t *xfull = bars, *xfree = bars + 1, *hready = bars + 2, *wbar = bars + 3;
+    uint64_t *tfull = bars + 4, *tempty = bars + 6;
+    uint64_t *hrdy = bars + 12;  // [kBkMaxTiles]: conv1 tile j of the image is in T
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 12 + kBkMaxTiles);
+    uint32_t *part = tmem_slot + 4;            // [2][kBkMaxTiles][4] max |T| per tile quarter
+    float *s_b = reinterpret_cast<float *>(part + 2 * kBkMaxTiles * 4);  // bias1 | bias2
+
+    // warp index broadcast from lane 0: ptxas then knows role branches are
+    // warp-uniform and keeps the MMA issue loop on the uniform datapath
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (threadIdx.x < 2 * N) s_b[threadIdx.x] = threadIdx.x < N ? L.bias1[threadIdx.x] : L.bias2[threadIdx.x - N];
+    if (threadIdx.x == 0) {
+        mbar_init(xfull, 1);
+        mbar_init(xfree, 1);
+        mbar_init(hready, 8);
+        mbar_init(wbar, 1);
+        for (int j = 0; j < kBkMaxTiles; ++j) mbar_init(&hrdy[j], 4);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2u * N2));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
+    const int64_t n_img = L.n_img;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(wbar, 2 * WB);
+            bulk_g2s(s_w1, L.w1, WB, wbar);
+            bulk_g2s(s_w2, L.w2, WB, wbar);
+            int it = 0;
+            for (int64_t n = blockIdx.x; n < n_img; n += gridDim.x, ++it) {
+                if (it > 0) mbar_wait(xfree, (it - 1) & 1);
+                mbar_expect_tx(xfull, 8u * (uint32_t)nrows * 16u);
+                const int64_t q_lo = n * HW - (Wp + 1);
+#pragma unroll 1
+                for (int g = 0; g < 2 * NH; ++g)
+                    bulk_g2s(s_x + (size_t)g * slab + (size_t)(M0 - Wp - 1) * 16,
+                             L.in + ((int64_t)g * L.gstride + L.margin + q_lo) * 8, (uint32_t)nrows * 16u, xfull);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc64 = idesc_f16(128, N2);
+        constexpr uint32_t idesc32 = idesc_f16(128, N);
+        mbar_wait(wbar, 0);
+        tc_fence_after();
+        const uint64_t dX = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_x), 0), slab, 128u);
+        const uint64_t dH = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_h), 0), slab, 128u);
+        const uint64_t dW1 = umma_desc(smem_u32(s_w1), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dW2 = umma_desc(smem_u32(s_w2), (uint32_t)N2 * 16u, 128u);
+        const uint32_t rx = (uint32_t)RX;
+        int64_t ti = 0;
+        auto conv = [&](uint64_t dA, uint64_t dB, int it2) {
+            for (int j = 0; j < T; ++j, ++ti) {
+                if (it2 >= 0) {  // conv2 tile j reads T rows of conv1 tiles j - 1 .. j + 1
+                    if (j == 0) mbar_wait(&hrdy[0], it2 & 1);
+                    if (j + 1 < T) mbar_wait(&hrdy[j + 1], it2 & 1);
+                    tc_fence_after();
+                }
+                const int a = (int)(ti & 1);
+                const int64_t u = ti >> 1;
+                if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(a * N2);
+                const uint32_t r0 = (uint32_t)(M0 + 128 * j - Wp - 1);
+#pragma unroll
+                for (int tap = 0; tap < 9; ++tap) {
+                    const uint32_t off = r0 + (uint32_t)((tap / 3) * Wp + tap % 3);
+#pragma unroll
+                    for (int ks = 0; ks < NH / 2; ++ks) {
+                        const uint64_t ao = (uint64_t)(2u * ks * rx + off);
+                        const uint64_t bo = (uint64_t)((tap * NH + 2 * ks) * N2);
+                        mma_f16_elect(d, dA + ao, dB + bo, idesc64, (tap | ks) ? 1u : 0u);
+                        mma_f16_elect(d + N, dA + ao + (uint64_t)(NH * rx), dB + bo, idesc32, 1u);
+                    }
+                }
+                mma_commit_elect(&tfull[a]);
+            }
+        };
+        int it = 0;
+        for (int64_t n = blockIdx.x; n < n_img; n += gridDim.x, ++it) {
+            mbar_wait(xfull, it & 1);
+            tc_fence_after();
+            conv(dX, dW1, -1);
+            mma_commit_elect(xfree);
+            conv(dH, dW2, it);
+        }
+    } else {
+        const int grp = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int H = L.H, W = L.W;
+        const int kw1 = __float_as_int(L.meta1[0]), kw2 = __float_as_int(L.meta2[0]);
+        const float l1a = L.meta1[1], bm1 = L.meta1[2], l1b = L.meta2[1], bm2 = L.meta2[2];
+        int64_t ti = 0;
+        int it = 0;
+        // per-image scalars are fetched one image ahead (a global load per
+        // image would otherwise stall every iteration)
+        int kx_nx = 0;
+        uint32_t mx_nx = 0;
+        if (blockIdx.x < n_img) {
+            kx_nx = L.kx_in[blockIdx.x];
+            mx_nx = L.mx_in[blockIdx.x];
+        }
+        for (int64_t n = blockIdx.x; n < n_img; n += gridDim.x, ++it) {
+            const int kxi = kx_nx;
+            const float mxi = __uint_as_float(mx_nx);
+            if (n + gridDim.x < n_img) {
+                kx_nx = L.kx_in[n + gridDim.x];
+                mx_nx = L.mx_in[n + gridDim.x];
+            }
+            // conv1: T = relu(conv1(X)), scale 2^k1 from the bound on |T|
+            const int k1 = act_exp(__float_as_uint(__fadd_rn(__fmul_rn(mxi, l1a), bm1)));
+            uint32_t *pt = part + (it & 1) * kBkMaxTiles * 4;
+            for (int j = 0; j < T; ++j, ++ti) {
+                if ((int)(ti & 1) != grp) continue;
+                const uint32_t u = (uint32_t)(ti >> 1);
+                const int r = 128 * j + row;
+                const int y = r / Wp, x = r - (r / Wp) * Wp;
+                const bool valid = r < HW && y >= 1 && y <= H && x >= 1 && x <= W;
+                const float inv = exp2i(-kxi - kw1), osc = exp2i(k1);
+                mbar_wait(&tfull[grp], u & 1);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(grp * N2);
+                float v[32];
+                {
+                    float w[32];
+                    tmem_ld32(taddr, v);
+                    tmem_ld32(taddr + 32, w);
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) v[c] = __fmaf_rn(__fmaf_rn(w[c], 0.00048828125f, v[c]), inv, s_b[c]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[grp]);
+                float mx = 0.f;
+                if (valid) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        v[c] = fmaxf(v[c], 0.f);
+                        mx = fmaxf(mx, fabsf(v[c]));
+                    }
+#pragma unroll
+                    for (int g = 0; g < NH; ++g) {
+                        uint4 h, l;
+                        split2(__fmul_rn(v[8 * g + 0], osc), __fmul_rn(v[8 * g + 1], osc), h.x, l.x);
+                        split2(__fmul_rn(v[8 * g + 2], osc), __fmul_rn(v[8 * g + 3], osc), h.y, l.y);
+                        split2(__fmul_rn(v[8 * g + 4], osc), __fmul_rn(v[8 * g + 5], osc), h.z, l.z);
+                        split2(__fmul_rn(v[8 * g + 6], osc), __fmul_rn(v[8 * g + 7], osc), h.w, l.w);
+                        store_px(reinterpret_cast<uint16_t *>(s_h + (size_t)g * slab + (size_t)M0 * 16), r, h, y, x,
+                                 H, W, Wp);
+                        store_px(reinterpret_cast<uint16_t *>(s_h + (size_t)(NH + g) * slab + (size_t)M0 * 16), r, l,
+                                 y, x, H, W, Wp);
+                    }
+                }
+                const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(mx));
+                fence_async_smem();  // T rows -> conv2's MMA operand
+                __syncwarp();
+                if (lane == 0) {
+                    pt[j * 4 + quarter] = m;
+                    mbar_arrive(&hrdy[j]);
+                }
+            }
+            if (lane == 0) mbar_arrive(hready);
+            mbar_wait(hready, it & 1);
+            uint32_t mt = 0;
+            for (int k = 0; k < 4 * T; ++k) mt = max(mt, pt[k]);
+            // conv2: X' = relu(X + conv2(T)), scale from |T| L1 + max|b| + max|X|
+            const float bound = __fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(mt), l1b), bm2), mxi);
+            const int k2 = act_exp(__float_as_uint(bound));
+            for (int j = 0; j < T; ++j, ++ti) {
+                if ((int)(ti & 1) != grp) continue;
+                const uint32_t u = (uint32_t)(ti >> 1);
+                const int r = 128 * j + row;
+                const int y = r / Wp, x = r - (r / Wp) * Wp;
+                const bool valid = r < HW && y >= 1 && y <= H && x >= 1 && x <= W;
+                const float inv = exp2i(-k1 - kw2), osc = exp2i(k2);
+                const int64_t q = n * HW + r;
+                float4 rr[8] = {};  // residual rows, in flight while the MMAs finish
+                if (valid) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        rr[g] = __ldg(reinterpret_cast<const float4 *>(L.res) + (int64_t)g * L.gstride + L.margin + q);
+                }
+                mbar_wait(&tfull[grp], u & 1);
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(grp * N2);
+                float v[32];
+                {
+                    float w[32];
+                    tmem_ld32(taddr, v);
+                    tmem_ld32(taddr + 32, w);
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        v[c] = __fmaf_rn(__fmaf_rn(w[c], 0.00048828125f, v[c]), inv, s_b[N + c]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[grp]);
+                float mx = 0.f;
+                if (valid) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        v[4 * g + 0] = fmaxf(__fadd_rn(rr[g].x, v[4 * g + 0]), 0.f);
+                        v[4 * g + 1] = fmaxf(__fadd_rn(rr[g].y, v[4 * g + 1]), 0.f);
+                        v[4 * g + 2] = fmaxf(__fadd_rn(rr[g].z, v[4 * g + 2]), 0.f);
+                        v[4 * g + 3] = fmaxf(__fadd_rn(rr[g].w, v[4 * g + 3]), 0.f);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) mx = fmaxf(mx, fabsf(v[4 * g + e]));
+                        if (L.out32)
+                            store_px4(L.out32 + ((int64_t)g * L.gstride + L.margin) * 4, q,
+                                      make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]), y, x, H, W, Wp);
+                    }
+#pragma unroll
+                    for (int g = 0; g < NH; ++g) {
+                        uint4 h, l;
+                        split2(__fmul_rn(v[8 * g + 0], osc), __fmul_rn(v[8 * g + 1], osc), h.x, l.x);
+                        split2(__fmul_rn(v[8 * g + 2], osc), __fmul_rn(v[8 * g + 3], osc), h.y, l.y);
+                        split2(__fmul_rn(v[8 * g + 4], osc), __fmul_rn(v[8 * g + 5], osc), h.z, l.z);
+                        split2(__fmul_rn(v[8 * g + 6], osc), __fmul_rn(v[8 * g + 7], osc), h.w, l.w);
+                        store_px(L.out + ((int64_t)g * L.gstride + L.margin) * 8, q, h, y, x, H, W, Wp);
+                        store_px(L.out + ((int64_t)(NH + g) * L.gstride + L.margin) * 8, q, l, y, x, H, W, Wp);
+                    }
+                }
+                const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(mx));
+                if (lane == 0) {
+                    if (m != 0u) atomicMax(L.mx_out + n, m);
+                    L.kx_out[n] = k2;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * N2));
+    }
+}
+
+size_t tc3_block_smem(int Hp, int Wp) {
+    const int T = (Hp * Wp + 127) / 128;
+    const int M0 = (Wp + 1 + 7) & ~7;
+    const size_t RX = (size_t)M0 + (size_t)T * 128 + M0;
+    return 2 * 36 * 64 * 16 + 2 * 8 * RX * 16 + (12 + kBkMaxTiles) * 8 + 16 +
+           2 * kBkMaxTiles * 4 * 4 + 64 * 4;
+}
+
 // ---- encoder front on tcgen05 (vqvae.py:55-57) -----------------------------
 // stem (3x3, 3 -> 32, ReLU) and down (3x3 stride 2, 32 -> 32, ReLU), both as
 // 3-product fp16 MMAs, in one kernel: the stem never leaves the SM.
@@ -1585,6 +1886,20 @@ int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s) {
     if (ks == 3 && mode == TC3_ACT) return launch_tc3<3, TC3_ACT>(L, s);
     if (ks == 1 && mode == TC3_Z) return launch_tc3<1, TC3_Z>(L, s);
     return PILC_E_UNSUPPORTED;
+}
+int tc3_block_launch(const Tc3Block &b, cudaStream_t s) {
+    const size_t smem = tc3_block_smem(b.Hp, b.Wp);
+    if ((b.Hp * b.Wp + 127) / 128 > kBkMaxTiles || smem > 227 * 1024) return PILC_E_UNSUPPORTED;
+    if ((uint64_t)b.n_img * b.Hp * b.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;
+    cudaFuncSetAttribute(tc3_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t grid = sm_count();
+    if (grid > b.n_img) grid = b.n_img;
+    if (grid < 1) return PILC_OK;
+    const double flops = 2.0 * 2.0 * b.n_img * b.H * b.W * 32.0 * 32 * 9;
+    ProfScope _ps(PROF_TC3_BLOCK, s, flops);
+    tc3_block_kernel<<<(unsigned)grid, kThreadsBK, smem, s>>>(b);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
 }
 int tc_launch_shuffle(const TcLayer &L, cudaStream_t s) { return launch_tc<128, 3, TC_OUT_SHUFFLE>(L, s); }
 int tc_launch_head(const TcLayer &L, cudaStream_t s) { return launch_tc<16, 3, TC_OUT_HEAD>(L, s); }

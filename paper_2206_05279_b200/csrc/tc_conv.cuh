@@ -54,6 +54,27 @@ struct Tc3Layer {
     int relu;
 };
 
+// One encoder residual block, X' = relu(X + conv2(relu(conv1(X)))), both
+// convs in one kernel with the intermediate kept in shared memory (one image
+// per CTA iteration); same arithmetic as two tc3 ACT launches.
+struct Tc3Block {
+    const uint16_t *in;   // hi / lo slabs of X
+    const float *res;     // fp32 slabs of X
+    int64_t gstride, margin;
+    int Hp, Wp, H, W;
+    int64_t n_img;
+    const uint16_t *w1, *w2;      // [36][64][8] fp16 B operands
+    const float *meta1, *meta2;   // {kw, L1, max|b|}
+    const float *bias1, *bias2;
+    const int32_t *kx_in;
+    const uint32_t *mx_in;
+    uint16_t *out;
+    float *out32;                 // nullable
+    int32_t *kx_out;
+    uint32_t *mx_out;             // atomicMax; zeroed by the caller
+};
+int tc3_block_launch(const Tc3Block &b, cudaStream_t s);
+
 // Encoder front (stem and the stride-2 down conv as 3-product fp16 MMAs, the
 // down GEMM over the space-to-depth stem, tc_conv.cu); outputs like the
 // block convs.

@@ -15,6 +15,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -905,6 +906,37 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
     uint16_t *XH = w.XH, *YH = w.YH;
     const float *meta = model + L.tf_meta;
     for (int i = 0; i < B; ++i) {
+        if (g_tuning[PILC_TUNE_BLOCK_FUSION]) {  // both convs in one kernel, T stays in shared memory
+            Tc3Block k;
+            k.in = XH;
+            k.res = X32;
+            k.gstride = w.gs;
+            k.margin = w.margin;
+            k.Hp = b.Hp;
+            k.Wp = b.Wp;
+            k.H = gh;
+            k.W = gw;
+            k.n_img = n_img;
+            k.w1 = reinterpret_cast<const uint16_t *>(model + L.tf_blk[2 * i]);
+            k.w2 = reinterpret_cast<const uint16_t *>(model + L.tf_blk[2 * i + 1]);
+            k.meta1 = meta + 4 * (2 * i);
+            k.meta2 = meta + 4 * (2 * i + 1);
+            k.bias1 = model + L.enc[2 + 2 * i].b_off;
+            k.bias2 = model + L.enc[3 + 2 * i].b_off;
+            k.kx_in = w.kx + (2 * i) * n_img;
+            k.mx_in = w.mx + (2 * i) * n_img;
+            k.out = YH;
+            k.out32 = i + 1 < B ? Y32 : nullptr;
+            k.kx_out = w.kx + (2 * i + 2) * n_img;
+            k.mx_out = w.mx + (2 * i + 2) * n_img;
+            rc = tc3_block_launch(k, s);
+            if (rc == PILC_OK) {
+                std::swap(X32, Y32);
+                std::swap(XH, YH);
+                continue;
+            }
+            if (rc != PILC_E_UNSUPPORTED) return rc;
+        }
         Tc3Layer c1 = b;  // T = relu(conv1(X))
         c1.in = XH;
         c1.kx_in = w.kx + (2 * i) * n_img;

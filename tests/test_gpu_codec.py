@@ -457,3 +457,28 @@ def test_trained_model_round_trip_and_vs_oracle():
         img = smooth_images(1, *shape, seed=7)[0]
         blob = pc.compress(img, m, cfg)
         assert np.array_equal(pc.decompress(blob, m), img)
+
+
+@pytest.mark.parametrize("shape,n", [((32, 32), 301), ((30, 18), 7), ((1, 1), 3), ((17, 33), 5), ((64, 64), 2)])
+def test_fused_encoder_blocks_bit_identical(full_model, shape, n):
+    """tc3_block_kernel (conv1 + conv2 of a block, T in shared memory) gives
+    exactly the z and indices of two separate tc3 launches per block."""
+    from paper_2206_05279_b200 import _lib
+    from paper_2206_05279_b200.device import as_device_u8, require_device
+
+    dev = require_device()
+    stream = torch.cuda.current_stream(dev)
+    imgs = smooth_images(n, *shape, seed=606)
+    gh, gw = vqvae.latent_shape(*shape)
+    img_d = as_device_u8(imgs, dev, stream)
+    out = []
+    for fused in (1, 0):
+        prev = _lib.set_tuning(_lib.TUNE_BLOCK_FUSION, fused)
+        try:
+            z = torch.empty((n, gh, gw, 32), dtype=torch.float32, device=dev)
+            idx = vqvae.encode_indices_device(img_d, full_model, dev, stream, z_out=z)
+            out.append((z.cpu().numpy(), idx.cpu().numpy()))
+        finally:
+            _lib.set_tuning(_lib.TUNE_BLOCK_FUSION, prev)
+    assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
+    assert np.array_equal(out[0][1], out[1][1])

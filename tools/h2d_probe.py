@@ -37,3 +37,17 @@ def reg():
     d.copy_(torch.from_numpy(flat), non_blocking=True); torch.cuda.synchronize()
     cr.cudaHostUnregister(flat.ctypes.data)
 t("cudaHostRegister + DMA + unregister", reg)
+import threading
+def threaded(k):
+    def go():
+        step = -(-flat.size // k)
+        streams = [torch.cuda.Stream() for _ in range(k)]
+        def work(i):
+            with torch.cuda.stream(streams[i]):
+                d[i * step:(i + 1) * step].copy_(torch.from_numpy(flat[i * step:(i + 1) * step]))
+        ts = [threading.Thread(target=work, args=(i,)) for i in range(k)]
+        for t_ in ts: t_.start()
+        for t_ in ts: t_.join()
+    return go
+for k in (2, 4, 8):
+    t(f"{k} threads, pageable copy_ per slice", threaded(k))
