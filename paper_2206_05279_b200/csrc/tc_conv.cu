@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     float *s_bias = reinterpret_cast<float *>(wbar + 2);  // N floats
     float *s_thr = s_bias + N;                            // head: n_thresh floats
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     for (int c = threadIdx.x; c < N; c += blockDim.x) s_bias[c] = c < (MODE == TC_OUT_HEAD ? 6 : N) ? L.bias[c] : 0.f;
     if constexpr (MODE == TC_OUT_HEAD) {
         for (int k = threadIdx.x; k < L.n_thresh; k += blockDim.x) s_thr[k] = __double2float_rd(L.thresh[k]);
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
 
     const int64_t n_tiles = L.n_tiles;
     if (warp == 0) {
@@ -280,8 +280,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
         constexpr uint32_t idesc = idesc_bf16(128, N);
         mbar_wait(wbar, 0);
         tc_fence_after();
-        const uint64_t dA0 = umma_desc(smem_u32(s_a), (uint32_t)npix * 16u, 128u);
-        const uint64_t dB0 = umma_desc(smem_u32(s_w), (uint32_t)N * 16u, 128u);
+        const uint64_t dA0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_a), 0), (uint32_t)npix * 16u, 128u);
+        const uint64_t dB0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w), 0), (uint32_t)N * 16u, 128u);
         const uint32_t npx = (uint32_t)npix;
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
     uint64_t *wbar = rempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages3; ++s) {
             mbar_init(&full[s], 1);
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
     const int64_t n_tiles = L.n_tiles;
 
     if (warp == 0) {
@@ -661,8 +661,8 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
         constexpr uint32_t idesc32 = idesc_f16(128, N);
         mbar_wait(wbar, 0);
         tc_fence_after();
-        const uint64_t dA0 = umma_desc(smem_u32(s_a), (uint32_t)npix * 16u, 128u);
-        const uint64_t dB0 = umma_desc(smem_u32(s_w), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dA0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_a), 0), (uint32_t)npix * 16u, 128u);
+        const uint64_t dB0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w), 0), (uint32_t)N2 * 16u, 128u);
         const uint32_t npx = (uint32_t)npix;
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
@@ -966,8 +966,8 @@ __global__ void __launch_bounds__(kThreadsBK, 1) tc3_block_kernel(Tc3Block L) {
         tc_fence_after();
         const uint64_t dX = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_x), 0), slab, 128u);
         const uint64_t dH = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_h), 0), slab, 128u);
-        const uint64_t dW1 = umma_desc(smem_u32(s_w1), (uint32_t)N2 * 16u, 128u);
-        const uint64_t dW2 = umma_desc(smem_u32(s_w2), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dW1 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w1), 0), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dW2 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w2), 0), (uint32_t)N2 * 16u, 128u);
         const uint32_t rx = (uint32_t)RX;
         int64_t ti = 0;
         auto conv = [&](uint64_t dA, uint64_t dB, int it2) {
@@ -1224,7 +1224,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     if (threadIdx.x < N) {
         s_bs[threadIdx.x] = a.b_stem[threadIdx.x];
         s_bd[threadIdx.x] = a.b_down[threadIdx.x];
@@ -1256,7 +1256,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
     const uint32_t tmem_down = tmem + 64u * kEfSlots;
     const int64_t n_tiles = a.n_tiles;
     const uint32_t img_px = (uint32_t)(Hp * Wp);
@@ -1341,10 +1341,10 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
         constexpr uint32_t idesc32 = idesc_f16(128, N);
         mbar_wait(wbar, 0);
         tc_fence_after();
-        const uint64_t dA0 = umma_desc(smem_u32(s_a), (uint32_t)npix * 16u, 128u);
-        const uint64_t dB0 = umma_desc(smem_u32(s_wd), (uint32_t)N2 * 16u, 128u);
-        const uint64_t dC0 = umma_desc(smem_u32(s_c), 128u * 16u, 128u);
-        const uint64_t dS0 = umma_desc(smem_u32(s_wsb), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dA0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_a), 0), (uint32_t)npix * 16u, 128u);
+        const uint64_t dB0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_wd), 0), (uint32_t)N2 * 16u, 128u);
+        const uint64_t dC0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_c), 0), 128u * 16u, 128u);
+        const uint64_t dS0 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_wsb), 0), (uint32_t)N2 * 16u, 128u);
         const uint32_t npx = (uint32_t)npix;
         int64_t gi = 0;  // next stem chunk to issue (global index)
         // stem chunks of one tile: A (im2col) x [Ws_hi | Ws_lo] and A_lo x Ws_hi
@@ -1586,7 +1586,7 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
     const float a1 = 5.3e-5f, a2 = 4e-6f;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kAmStages; ++s) {
             mbar_init(&full[s], 1);
@@ -1610,7 +1610,7 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
     mbar_wait(wbar, 0);
     const float *cb_hi = reinterpret_cast<const float *>(s_cb);
     const float *cb_lo = cb_hi + 8 * NC * 4;
