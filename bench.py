@@ -392,6 +392,11 @@ def run_gpu(args):
             "enc_front_kernel": "encoder stem + stride-2 down, both 3-product fp16 MMAs (down over the space-to-depth stem); "
                                 "algorithmic FLOPs = 2*N*(4*gh*gw*32*27 + gh*gw*32*32*9)",
             "conv_kernel": "fp32 SIMT convs (non-default model shapes); algorithmic FLOPs = 2*N*Ho*Wo*Cout*Cin*k^2 per launch",
+            "tc3_block_kernel": "one encoder residual block per launch (conv1 + conv2, intermediate in shared memory), "
+                                "3-product fp16 split on tcgen05 kind::f16; algorithmic FLOPs = 2 convs x 2*N*H*W*32*32*9 "
+                                "(MMA FLOPs issued = 3x that)",
+            "dec_trunk_kernel": "decoder trunk (gather + all 2B bf16 block convs, activations in shared memory, G images per "
+                                "CTA iteration); algorithmic FLOPs = 2B x 2*N*gh*gw*32*32*9",
             "argmin_kernel": "codebook distance GEMM (3xTF32 tcgen05) + proven-margin screen + exact f64 rescore (3*n*K*Dc FLOPs)",
         }
         if dom:

@@ -96,7 +96,9 @@ typedef struct pilc_header {
 const char *pilc_version(void);
 /* Tuning switches of the production path (no reference counterpart; for
  * A/B checks). key 0: encoder residual blocks as one fused kernel per block
- * (default 1) instead of two conv launches -- bit-identical results.
+ * (default 1) instead of two conv launches; key 1: decoder trunk (gather +
+ * block convs) as one kernel with activations in shared memory (default 1)
+ * instead of per-layer launches. Both bit-identical to the unfused path.
  * Returns the previous value, or -PILC_E_ARG for an unknown key. */
 int pilc_set_tuning(int32_t key, int32_t value);
 /* Device sanity: returns 100 for sm_100 etc., or -1 if no usable device. */

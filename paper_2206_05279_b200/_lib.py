@@ -115,6 +115,7 @@ def call(name: str, *args) -> int:
 
 
 TUNE_BLOCK_FUSION = 0
+TUNE_DEC_TRUNK = 1
 
 
 def set_tuning(key: int, value: int) -> int:

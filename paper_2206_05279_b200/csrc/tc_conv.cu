@@ -1166,6 +1166,242 @@ size_t tc3_block_smem(int Hp, int Wp) {
            2 * kBkMaxTiles * 4 * 4 + 64 * 4;
 }
 
+// ---- decoder trunk in shared memory (vqvae.py:80-100) -----------------------
+// dec.proj (as the gathered table T[idx], see dec_table_kernel) and all 2B
+// residual-block convs of a group of G images in one persistent kernel: the
+// latent activations never leave shared memory. X (block input / output,
+// updated in place by conv2's epilogue) and H (conv1 output) are padded
+// group-major slab sets as in tc_conv_kernel, with the G images' padded
+// grids back to back; taps are shifted descriptors into them. Only the
+// trunk output goes to HBM (for the up conv).
+//
+// Per layer the T = ceil(G Hp Wp / 128) tiles are issued in order; tile j of
+// layer l + 1 waits for tiles j - 1 .. j + 1 of layer l (`hrdy`, one
+// mbarrier per tile position, one phase per layer). MMAs complete in issue
+// order, so an epilogue writing a buffer can never overtake an earlier
+// layer's MMA still reading it. Weights stream through a two-slot ring.
+// Arithmetic (MMA K order, fadd order, bf16 rounding) is that of
+// tc_conv_kernel, so the output is bit-identical to the per-layer path.
+constexpr int kDtGroups = 3;  // epilogue groups of four warps, one TMEM accumulator each
+constexpr int kThreadsDT = 64 + 128 * kDtGroups;
+constexpr int kDtMaxTiles = 16;
+constexpr int kDtMaxConvs = 16;
+
+__global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk_kernel(DecTrunk P) {
+    constexpr int N = 32, NG = 4;
+    constexpr uint32_t WB = 36 * N * 16;
+    const int Wp = P.Wp, HW = P.Hp * Wp, G = P.G;
+    const int rows = G * HW;
+    const int T = (rows + 127) >> 7;
+    const int M0 = Wp + 1;
+    const int RS = M0 + rows + M0;
+    const uint32_t slab = (uint32_t)RS * 16u;
+    const int L = P.n_conv;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_w = smem;                                         // [2][36][32][8] bf16
+    uint8_t *s_tab = s_w + 2 * WB;                               // K x 64 B
+    uint8_t *s_x = s_tab + (size_t)P.K * 64;
+    uint8_t *s_h = s_x + NG * (size_t)slab;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_h + NG * (size_t)slab + P.pad_bytes);
+    uint64_t *wfull = bars, *wempty = bars + 2, *tfull = bars + 4, *tempty = bars + 4 + kDtGroups;
+    uint64_t *xready = bars + 4 + 2 * kDtGroups, *tbar = xready + 1, *hrdy = xready + 2;  // hrdy[kDtMaxTiles]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(hrdy + kDtMaxTiles);
+    float *s_b = reinterpret_cast<float *>(tmem_slot + 4);      // [L][32]
+
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < L * N; i += blockDim.x) s_b[i] = P.bias[i / N][i % N];
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&wfull[a], 1);
+            mbar_init(&wempty[a], 1);
+        }
+        for (int a = 0; a < kDtGroups; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        mbar_init(xready, 4 * kDtGroups);
+        mbar_init(tbar, 1);
+        for (int j = 0; j < kDtMaxTiles; ++j) mbar_init(&hrdy[j], 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(128u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
+    const int64_t n_groups = (P.n_img + G - 1) / G;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(tbar, (uint32_t)P.K * 64u);
+            bulk_g2s(s_tab, P.table, (uint32_t)P.K * 64u, tbar);
+            int lc = 0;
+            for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+                for (int l = 0; l < L; ++l, ++lc) {
+                    const int s = lc & 1;
+                    if (lc >= 2) mbar_wait(&wempty[s], ((lc >> 1) - 1) & 1);
+                    mbar_expect_tx(&wfull[s], WB);
+                    bulk_g2s(s_w + (size_t)s * WB, P.w + (size_t)l * (WB / 2), WB, &wfull[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_bf16(128, N);
+        const uint64_t dX = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_x), 0), slab, 128u);
+        const uint64_t dH = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_h), 0), slab, 128u);
+        const uint64_t dW = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w), 0), N * 16u, 128u);
+        const uint32_t rs = (uint32_t)RS;
+        int64_t ti = 0;
+        int lc = 0, gc = 0;
+        for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x, ++gc) {
+            mbar_wait(xready, gc & 1);
+            tc_fence_after();
+            for (int l = 0; l < L; ++l, ++lc) {
+                const int s = lc & 1;
+                mbar_wait(&wfull[s], (lc >> 1) & 1);
+                tc_fence_after();
+                const uint64_t dA = (l & 1) ? dH : dX;
+                const uint64_t dB = dW + (uint64_t)((uint32_t)s * (WB >> 4));
+                for (int j = 0; j < T; ++j, ++ti) {
+                    if (l > 0) {  // tiles j - 1 .. j + 1 of the previous layer are in place
+                        if (j == 0) mbar_wait(&hrdy[0], (lc - 1) & 1);
+                        if (j + 1 < T) mbar_wait(&hrdy[j + 1], (lc - 1) & 1);
+                        tc_fence_after();
+                    }
+                    const int a = (int)(ti % kDtGroups);
+                    const int64_t u = ti / kDtGroups;
+                    if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
+                    tc_fence_after();
+                    const uint32_t d = tmem + (uint32_t)(a * N);
+                    const uint32_t r0 = (uint32_t)(M0 + 128 * j - Wp - 1);
+#pragma unroll
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const uint32_t off = r0 + (uint32_t)((tap / 3) * Wp + tap % 3);
+#pragma unroll
+                        for (int ks = 0; ks < NG / 2; ++ks)
+                            mma_bf16_elect(d, dA + (uint64_t)(2u * ks * rs + off),
+                                           dB + (uint64_t)((tap * NG + 2 * ks) * N), idesc, (tap | ks) ? 1u : 0u);
+                    }
+                    mma_commit_elect(&tfull[a]);
+                }
+                mma_commit_elect(&wempty[s]);
+            }
+        }
+    } else {
+        const int grp = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0 .. 128 kDtGroups - 1
+        const int gh = P.Hp - 2, gw = Wp - 2;
+        const FastDiv div_hw{(uint32_t)HW, (uint32_t)(0x100000000ull / (uint32_t)HW)};
+        const FastDiv div_w{(uint32_t)Wp, (uint32_t)(0x100000000ull / (uint32_t)Wp)};
+        mbar_wait(tbar, 0);
+        int64_t ti = 0;
+        int lc = 0;
+        for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+            const int64_t n0 = gi * G;
+            const int g_act = (int)min((int64_t)G, P.n_img - n0);
+            // gather: X = T[idx] at every padded position of the group (edges by clamping)
+            for (int p = et; p < g_act * HW; p += 128 * kDtGroups) {
+                const int n = (int)fdiv((uint32_t)p, div_hw), rem = p - n * HW;
+                const int yy = (int)fdiv((uint32_t)rem, div_w);
+                int y = yy - 1, x = rem - yy * Wp - 1;
+                y = y < 0 ? 0 : (y >= gh ? gh - 1 : y);
+                x = x < 0 ? 0 : (x >= gw ? gw - 1 : x);
+                const int k = P.idx[((n0 + n) * gh + y) * gw + x];
+                const uint4 *src = reinterpret_cast<const uint4 *>(s_tab + (size_t)k * 64);
+#pragma unroll
+                for (int g = 0; g < NG; ++g)
+                    reinterpret_cast<uint4 *>(s_x + (size_t)g * slab + (size_t)(M0 + p) * 16)[0] = src[g];
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xready);
+            for (int l = 0; l < L; ++l, ++lc) {
+                const bool conv2 = (l & 1) != 0, last = l == L - 1;
+                const float *bias = s_b + l * N;
+                uint8_t *dst = conv2 ? s_x : s_h;
+                for (int j = 0; j < T; ++j, ++ti) {
+                    if ((int)(ti % kDtGroups) != grp) continue;
+                    const uint32_t u = (uint32_t)(ti / kDtGroups);
+                    const int r = 128 * j + row;
+                    const int n = (int)fdiv((uint32_t)r, div_hw), rem = r - n * HW;
+                    const int y = (int)fdiv((uint32_t)rem, div_w), x = rem - y * Wp;
+                    const bool valid = n < g_act && y >= 1 && y <= gh && x >= 1 && x <= gw;
+                    mbar_wait(&tfull[grp], u & 1);
+                    tc_fence_after();
+                    float v[32];
+                    tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(grp * N), v);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[grp]);
+                    if (valid) {
+                        uint4 w4[NG];
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) {
+                            float o[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(v[8 * g + e], bias[8 * g + e]);
+                            if (conv2) {
+                                const uint4 rv = reinterpret_cast<const uint4 *>(s_x + (size_t)g * slab +
+                                                                                (size_t)(M0 + r) * 16)[0];
+                                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    o[2 * e] = __fadd_rn(bf16_lo(rw[e]), o[2 * e]);
+                                    o[2 * e + 1] = __fadd_rn(bf16_hi(rw[e]), o[2 * e + 1]);
+                                }
+                            }
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) o[e] = fmaxf(o[e], 0.f);
+                            w4[g] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                                               pack_bf16(o[6], o[7]));
+                        }
+                        if (last) {
+                            const int64_t q = (n0 + n) * HW + rem;
+#pragma unroll
+                            for (int g = 0; g < NG; ++g)
+                                store_px(P.out + ((int64_t)g * P.out_gstride + P.out_margin) * 8, q, w4[g], y, x, gh,
+                                         gw, Wp);
+                        } else {
+#pragma unroll
+                            for (int g = 0; g < NG; ++g)
+                                store_px(reinterpret_cast<uint16_t *>(dst + (size_t)g * slab + (size_t)M0 * 16), r,
+                                         w4[g], y, x, gh, gw, Wp);
+                        }
+                    }
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&hrdy[j]);
+                }
+            }
+            // the next group's gather overwrites X: every epilogue warp is past its residual reads
+            asm volatile("bar.sync 1, %0;" ::"n"(128 * kDtGroups) : "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128u));
+    }
+}
+
+size_t dec_trunk_smem(int Hp, int Wp, int G, int K, int n_conv, int *pad) {
+    const int rows = G * Hp * Wp, T = (rows + 127) / 128, M0 = Wp + 1;
+    const size_t RS = (size_t)M0 + rows + M0;
+    // the last slab's MMA reads run past its end by up to (128 T + M0) - (rows + M0) rows
+    const int p = ((128 * T - rows + 16) * 16 + 127) / 128 * 128;
+    if (pad) *pad = p;
+    return 2 * 36 * 32 * 16 + (size_t)K * 64 + 2 * 4 * RS * 16 + p + (6 + 2 * kDtGroups + kDtMaxTiles) * 8 + 16 +
+           (size_t)n_conv * 32 * 4;
+}
+
 // ---- encoder front on tcgen05 (vqvae.py:55-57) -----------------------------
 // stem (3x3, 3 -> 32, ReLU) and down (3x3 stride 2, 32 -> 32, ReLU), both as
 // 3-product fp16 MMAs, in one kernel: the stem never leaves the SM.
@@ -1898,6 +2134,34 @@ int tc3_block_launch(const Tc3Block &b, cudaStream_t s) {
     const double flops = 2.0 * 2.0 * b.n_img * b.H * b.W * 32.0 * 32 * 9;
     ProfScope _ps(PROF_TC3_BLOCK, s, flops);
     tc3_block_kernel<<<(unsigned)grid, kThreadsBK, smem, s>>>(b);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+int dec_trunk_launch(const DecTrunk &p0, cudaStream_t s) {
+    DecTrunk p = p0;
+    if (p.n_conv < 1 || p.n_conv > kDtMaxConvs || p.K < 1 || p.K > 256) return PILC_E_UNSUPPORTED;
+    if ((uint64_t)p.n_img * p.Hp * p.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;
+    int G = 0, pad = 0;
+    size_t smem = 0;
+    for (int g = 1; g <= 64; ++g) {  // images per group: the most that fit
+        int pd;
+        const size_t sm = dec_trunk_smem(p.Hp, p.Wp, g, p.K, p.n_conv, &pd);
+        if (sm > 227 * 1024 || (g * p.Hp * p.Wp + 127) / 128 > kDtMaxTiles) break;
+        G = g;
+        pad = pd;
+        smem = sm;
+    }
+    if (G == 0) return PILC_E_UNSUPPORTED;
+    p.G = G;
+    p.pad_bytes = pad;
+    cudaFuncSetAttribute(dec_trunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t groups = (p.n_img + G - 1) / G;
+    int64_t grid = sm_count();
+    if (grid > groups) grid = groups;
+    if (grid < 1) return PILC_OK;
+    const double flops = 2.0 * p.n_img * (p.Hp - 2) * (p.Wp - 2) * 32.0 * 32 * 9 * p.n_conv;
+    ProfScope _ps(PROF_DEC_TRUNK, s, flops);
+    dec_trunk_kernel<<<(unsigned)grid, kThreadsDT, smem, s>>>(p);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

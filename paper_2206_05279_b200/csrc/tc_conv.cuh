@@ -26,6 +26,23 @@ struct TcLayer {
     float log_s_min, log_s_max;
 };
 
+// Decoder trunk (gather of dec.proj's table + all 2B block convs) with the
+// activations resident in shared memory, G images per CTA iteration.
+struct DecTrunk {
+    const uint8_t *idx;        // (n, gh, gw) codebook indices
+    const uint16_t *table;     // K x 32 bf16: relu(proj(codebook)) (dec_table_kernel)
+    int K;
+    int Hp, Wp;                // padded latent grid
+    int64_t n_img;
+    int n_conv;                // 2B, <= 16
+    const uint16_t *w;         // 2B consecutive [36][32][8] bf16 B operands
+    const float *bias[16];
+    uint16_t *out;             // padded group-major bf16 slabs (the up conv's input)
+    int64_t out_gstride, out_margin;
+    int G, pad_bytes;          // set by the launcher
+};
+int dec_trunk_launch(const DecTrunk &p, cudaStream_t s);
+
 // Encoder layers (3-product fp16 split, tc_conv.cu). Operands: the scaled
 // fp16 hi / lo slab sets of a tensor (8-channel groups, 16 B per pixel: hi
 // groups 0..3 then lo groups 4..7), padded group-major like the bf16 path;

@@ -1097,7 +1097,27 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
     const uint16_t *hb = reinterpret_cast<const uint16_t *>(model);
     int rc = tc_dec_table(model + L.cb_off, model + L.dec[0].w_off, model + L.dec[0].b_off, K, Dc, L.dec[0].ci_pad,
                           L.dec[0].co_pad, tw.table, s);
-    if (!rc) rc = tc_gather(idx, tw.table, n_img, gh, gw, tw.X, tw.gs, tw.margin, s);
+    bool trunk_done = false;
+    if (!rc && g_tuning[PILC_TUNE_DEC_TRUNK] && B >= 1 && 2 * B <= 16) {  // gather + blocks in shared memory
+        DecTrunk p;
+        memset(&p, 0, sizeof(p));
+        p.idx = idx;
+        p.table = tw.table;
+        p.K = K;
+        p.Hp = gh + 2;
+        p.Wp = gw + 2;
+        p.n_img = n_img;
+        p.n_conv = 2 * B;
+        p.w = hb + L.tc_blk[0];
+        for (int i = 0; i < 2 * B; ++i) p.bias[i] = model + L.dec[1 + i].b_off;
+        p.out = tw.X;
+        p.out_gstride = tw.gs;
+        p.out_margin = tw.margin;
+        rc = dec_trunk_launch(p, s);
+        if (rc == PILC_OK) trunk_done = true;
+        else if (rc == PILC_E_UNSUPPORTED) rc = PILC_OK;
+    }
+    if (!rc && !trunk_done) rc = tc_gather(idx, tw.table, n_img, gh, gw, tw.X, tw.gs, tw.margin, s);
     TcLayer b;
     memset(&b, 0, sizeof(b));
     b.gstride = b.out_gstride = tw.gs;
@@ -1110,7 +1130,7 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
     b.n_tiles = ceil_div64(n_img * b.Hp * (int64_t)b.Wp, 128);
     b.relu = 1;
     uint16_t *X = tw.X, *T = tw.T, *Y = tw.Y;
-    for (int i = 0; !rc && i < B; ++i) {
+    for (int i = 0; !rc && !trunk_done && i < B; ++i) {
         TcLayer c1 = b;
         c1.in = X;
         c1.out = T;

@@ -482,3 +482,31 @@ def test_fused_encoder_blocks_bit_identical(full_model, shape, n):
             _lib.set_tuning(_lib.TUNE_BLOCK_FUSION, prev)
     assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
     assert np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("shape,n", [((32, 32), 301), ((30, 18), 7), ((1, 1), 3), ((17, 33), 5), ((64, 64), 3)])
+def test_decoder_trunk_kernel_bit_identical(full_model, shape, n):
+    """dec_trunk_kernel (gather + all block convs with activations in shared
+    memory, G images per CTA iteration) gives exactly the mu / s / shift /
+    scale index of the per-layer tcgen05 decoder -- partial last groups and
+    the G = 1 (64 x 64) case included."""
+    from paper_2206_05279_b200 import _lib
+    from paper_2206_05279_b200.device import require_device
+
+    dev = require_device()
+    stream = torch.cuda.current_stream(dev)
+    H, W = shape
+    gh, gw = vqvae.latent_shape(H, W)
+    rng = np.random.default_rng(5)
+    idx = torch.from_numpy(rng.integers(0, 256, (n, gh, gw), dtype=np.uint8)).to(dev)
+    grid = default_grid()
+    out = []
+    for on in (1, 0):
+        prev = _lib.set_tuning(_lib.TUNE_DEC_TRUNK, on)
+        try:
+            r = vqvae.decode_head_device(idx, full_model, H, W, grid, dev, stream, want_params=True)
+            out.append([t.cpu().numpy() for t in r])
+        finally:
+            _lib.set_tuning(_lib.TUNE_DEC_TRUNK, prev)
+    for a, b in zip(*out):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
