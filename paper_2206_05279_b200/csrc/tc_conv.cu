@@ -206,6 +206,7 @@ __device__ __forceinline__ void store_px(uint16_t *slab, int64_t q, uint4 v, int
 
 template <int N, int KS, int MODE>
 __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
+    const int kS = L.n_stages;  // copy ring depth (launcher: as many as fit, <= kStages)
     constexpr int C = 32;               // input channels (4 groups of 8)
     constexpr int NG = C / 8;
     constexpr int KG = KS * KS * NG;    // K core-matrix groups
@@ -217,10 +218,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *s_w = smem;                                   // KG x N x 16 B
     uint8_t *s_a = smem + (size_t)KG * N * 16;             // kStages x NG x npix x 16 B
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_a + (size_t)kStages * stage_bytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_a + (size_t)kS * stage_bytes);
     uint64_t *full = bars;                 // [kStages]
-    uint64_t *empty = bars + kStages;      // [kStages]
-    uint64_t *tfull = bars + 2 * kStages;  // [2]
+    uint64_t *empty = bars + kS;      // [kStages]
+    uint64_t *tfull = bars + 2 * kS;  // [2]
     uint64_t *tempty = tfull + 2;          // [2]
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
         for (int k = threadIdx.x; k < L.n_thresh; k += blockDim.x) s_thr[k] = __double2float_rd(L.thresh[k]);
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -262,8 +263,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
             bulk_g2s(s_w, L.wts, wbytes, wbar);
             int i = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-                const int s = i % kStages;
-                const int r = i / kStages;
+                const int s = i % kS;
+                const int r = i / kS;
                 if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
                 const int64_t q_lo = t * 128 - (KS == 3 ? (Wp + 1) : 0);
                 mbar_expect_tx(&full[s], stage_bytes);
@@ -285,11 +286,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
         const uint32_t npx = (uint32_t)npix;
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int s = i % kStages;
+            const int s = i % kS;
             const int a = i & 1;
             const int u = i >> 1;
             if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
-            mbar_wait(&full[s], (i / kStages) & 1);
+            mbar_wait(&full[s], (i / kS) & 1);
             tc_fence_after();
             const uint64_t dA = dA0 + (uint64_t)((uint32_t)s * (stage_bytes >> 4));
             const uint32_t d = tmem + (uint32_t)(a * N);
@@ -566,6 +567,7 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t &h, uint32_t &
 
 template <int KS, int MODE>
 __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
+    const int kS = L.n_stages;  // copy ring depth (launcher: as many as fit, <= kStages3)
     constexpr int N = 32;
     constexpr int N2 = 64;  // B' = [W_hi | W_lo] along N
     constexpr int NH = 4;   // 8-channel fp16 groups
@@ -581,11 +583,11 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
     uint8_t *s_w = smem;
     uint8_t *s_a = smem + (size_t)wbytes;
     const bool has_res = MODE == TC3_ACT && L.res != nullptr;
-    float4 *s_res = reinterpret_cast<float4 *>(s_a + (size_t)kStages3 * stage_bytes);  // [2][8][128]
+    float4 *s_res = reinterpret_cast<float4 *>(s_a + (size_t)kS * stage_bytes);  // [2][8][128]
     uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(s_res) + (has_res ? 2 * 8 * 128 * 16 : 0));
     uint64_t *full = bars;
-    uint64_t *empty = bars + kStages3;
-    uint64_t *tfull = bars + 2 * kStages3;
+    uint64_t *empty = bars + kS;
+    uint64_t *tfull = bars + 2 * kS;
     uint64_t *tempty = tfull + 2;
     uint64_t *rfull = tempty + 2;
     uint64_t *rempty = rfull + 2;
@@ -594,7 +596,7 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
 
     const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages3; ++s) {
+        for (int s = 0; s < kS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -624,8 +626,8 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
             bulk_g2s(s_w, L.w, wbytes, wbar);
             int i = 0;
             for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-                const int s = i % kStages3;
-                const int r = i / kStages3;
+                const int s = i % kS;
+                const int r = i / kS;
                 if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
                 const int64_t q_lo = t * 128 - (KS == 3 ? (Wp + 1) : 0);
                 mbar_expect_tx(&full[s], stage_bytes);
@@ -666,11 +668,11 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
         const uint32_t npx = (uint32_t)npix;
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const int s = i % kStages3;
+            const int s = i % kS;
             const int a = i & 1;
             const int u = i >> 1;
             if (u > 0) mbar_wait(&tempty[a], (u - 1) & 1);
-            mbar_wait(&full[s], (i / kStages3) & 1);
+            mbar_wait(&full[s], (i / kS) & 1);
             tc_fence_after();
             const uint64_t dAh = dA0 + (uint64_t)((uint32_t)s * (stage_bytes >> 4));
             const uint64_t dAl = dAh + (uint64_t)(h_bytes >> 4);
@@ -847,10 +849,17 @@ template <int KS, int MODE>
 int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
     constexpr int KG = KS * KS * 4;
     const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
-    const size_t smem = (size_t)KG * 64 * 16 + (size_t)kStages3 * 8 * npix * 16 + (L.res ? 2 * 8 * 128 * 16 : 0) +
-                        8 * (2 * kStages3 + 9) + 16;
+    // ring depth: kStages3, or as many stages as fit for wide images (>= 2)
+    auto smem_of = [&](int k) {
+        return (size_t)KG * 64 * 16 + (size_t)k * 8 * npix * 16 + (L.res ? 2 * 8 * 128 * 16 : 0) + 8 * (2 * k + 9) + 16;
+    };
+    int st = kStages3;
+    while (st > 2 && smem_of(st) > 227 * 1024) --st;
+    const size_t smem = smem_of(st);
     if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
+    Tc3Layer Ls = L;
+    Ls.n_stages = st;
     auto kern = tc3_conv_kernel<KS, MODE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = (int)((227 * 1024) / (smem + 1024));
@@ -860,7 +869,7 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
     if (grid < 1) return PILC_OK;
     const double flops = 2.0 * L.n_img * L.H * L.W * 32.0 * 32 * KS * KS;
     ProfScope _ps(PROF_TC3_CONV, s, flops);
-    kern<<<(unsigned)grid, kThreadsTC3, smem, s>>>(L);
+    kern<<<(unsigned)grid, kThreadsTC3, smem, s>>>(Ls);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
@@ -2031,8 +2040,16 @@ int launch_tc(const TcLayer &L, cudaStream_t s) {
     constexpr int NG = 4;
     constexpr int KG = KS * KS * NG;
     const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
-    const size_t smem = (size_t)KG * N * 16 + (size_t)kStages * NG * npix * 16 + 8 * (2 * kStages + 6) + 4 * N +
-                        4 * (MODE == TC_OUT_HEAD ? 256 : 0) + 16;
+    // ring depth: kStages, or as many stages as fit for wide images (>= 2)
+    auto smem_of = [&](int k) {
+        return (size_t)KG * N * 16 + (size_t)k * NG * npix * 16 + 8 * (2 * k + 6) + 4 * N +
+               4 * (MODE == TC_OUT_HEAD ? 256 : 0) + 16;
+    };
+    int st = kStages;
+    while (st > 2 && smem_of(st) > 227 * 1024) --st;
+    const size_t smem = smem_of(st);
+    TcLayer Ls = L;
+    Ls.n_stages = st;
     if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     auto kern = tc_conv_kernel<N, KS, MODE>;
@@ -2044,7 +2061,7 @@ int launch_tc(const TcLayer &L, cudaStream_t s) {
     if (grid < 1) return PILC_OK;
     const double flops = 2.0 * L.n_img * L.H * L.W * (double)(MODE == TC_OUT_HEAD ? 6 : N) * 32 * KS * KS;
     ProfScope _ps(PROF_TC_CONV, s, flops);
-    kern<<<(unsigned)grid, kThreadsTC, smem, s>>>(L);
+    kern<<<(unsigned)grid, kThreadsTC, smem, s>>>(Ls);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

@@ -24,6 +24,7 @@ struct TcLayer {
     const double *thresh;
     int n_thresh;
     float log_s_min, log_s_max;
+    int n_stages;        // set by the launcher
 };
 
 // Decoder trunk (gather of dec.proj's table + all 2B block convs) with the
@@ -69,6 +70,7 @@ struct Tc3Layer {
     float *z;                 // TC3_Z: (n, H, W, 32) fp32 (nullable)
     float *zt;                // TC3_Z: 128-latent tiles [tile][hi|lo][8][128][4]
     int relu;
+    int n_stages;             // set by the launcher
 };
 
 // One encoder residual block, X' = relu(X + conv2(relu(conv1(X)))), both

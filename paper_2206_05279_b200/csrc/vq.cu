@@ -1000,7 +1000,10 @@ int vq_encode(int path, const uint8_t *img, int64_t n_img, int32_t H, int32_t W,
     if (path == 0 && L.tf) {
         TfWork tw;
         if (tf_ws(n_img, H, W, B, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-        return tf_encode(img, n_img, H, W, model, K, Dc, B, L, tw, idx_out, z_out, s);
+        const int rc = tf_encode(img, n_img, H, W, model, K, Dc, B, L, tw, idx_out, z_out, s);
+        // images too wide for the tcgen05 tiles' shared memory: fp32 SIMT
+        // kernels (the choice depends on the shape only; outputs overwritten)
+        if (rc != PILC_E_UNSUPPORTED) return rc;
     }
     Work w;
     if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
@@ -1205,9 +1208,16 @@ int vq_decode(int path, const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
     }
     cudaStream_t s = as_stream(stream);
     const double *thr = d_thresh;
-    const int rc = use_tc ? tc_decode(idx, n_img, H, W, model, L, K, Dc, B, thr, D, tw, shift_out, d_out, mu_out,
-                                      s_out, s)
-                          : simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
+    int rc = use_tc ? tc_decode(idx, n_img, H, W, model, L, K, Dc, B, thr, D, tw, shift_out, d_out, mu_out, s_out,
+                                s)
+                    : simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
+    if (use_tc && rc == PILC_E_UNSUPPORTED) {
+        // too wide for the tcgen05 tiles: the SIMT decoder. The choice is a
+        // function of (model config, H, W) only, so compress and decompress
+        // always agree.
+        if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+        rc = simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
+    }
     return rc;
 }
 

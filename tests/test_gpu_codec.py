@@ -510,3 +510,31 @@ def test_decoder_trunk_kernel_bit_identical(full_model, shape, n):
             _lib.set_tuning(_lib.TUNE_DEC_TRUNK, prev)
     for a, b in zip(*out):
         assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+def test_report_rows_in_reference_format():
+    """report.run_bench (report.py:47-104 twin): rows carry the reference's
+    keys; the GPU coder rows come from a checked round trip."""
+    from paper_2206_05279_b200 import report
+
+    rows = report.run_bench(lane_counts=(1, 8), n_symbols=1 << 14, image_hw=(24, 40), batch=16, reps=2)
+    assert [r["phase"] for r in rows[:4]] == ["coder-encode-fast", "coder-decode-fast"] * 2
+    assert {r["phase"] for r in rows[4:]} == {"model-inference", "ar-decode-parallel", "roundtrip-batch"}
+    for r in rows:
+        assert set(r) == {"phase", "lanes", "bytes", "seconds", "mb_per_s"} and r["mb_per_s"] > 0
+
+
+@pytest.mark.parametrize("shape", [(96, 96), (150, 200), (2, 300), (40, 520), (300, 7)])
+def test_vqvae_wide_images_round_trip(full_model, shape):
+    """Wide images: tcgen05 kernels shrink their copy rings, and shapes whose
+    tiles cannot fit shared memory at all take the fp32 SIMT kernels (a
+    function of the shape only, so compress and decompress agree). Indices
+    stay equal to the oracle's."""
+    img = smooth_images(1, *shape, seed=17)[0]
+    cfg = pc.CodecConfig(backend="twar-vqvae")
+    blob = pc.compress(img, full_model, cfg)
+    assert np.array_equal(pc.decompress(blob, full_model), img)
+    buf, off = pc.compress_batch(np.stack([img, img[::-1].copy()]), full_model, cfg)
+    assert np.array_equal(pc.decompress_batch(buf, off, full_model)[0], img)
+    om = O.Model.from_bytes(full_model.to_bytes())
+    assert np.array_equal(vqvae.encode_to_indices(img, full_model), O.encode_indices(img, om))
