@@ -414,6 +414,22 @@ def run_gpu(args):
                 gbs = units / (ms / 1e3) / 1e9
                 roofline = {"kernel": name, "bound": "hbm", "achieved": round(gbs, 2), "peak": peaks.get("hbm_gbs"),
                             "unit": "GB/s", "frac": round(gbs / peaks.get("hbm_gbs"), 5), "traffic": None}
+            # attainable rate for these MMA shapes: SS-mode tcgen05 MMAs (M=128,
+            # K=16) cost max(44 cycles, operand bytes / 128 B/cycle) each on this
+            # B200 (tools/micro/mma_rate.cu: N=16/32 44, N=64 48, N=128 64), so
+            # N=32-output convs cannot approach the dense peak. Cycles per
+            # 128-row K=16 step (algorithmic 2*128*32*16 FLOP): bf16 convs 44;
+            # the 3-product fp16 encoder (N=64 + N=32 MMAs) 92.
+            floor_cyc = {"tc_conv_kernel": 44.0, "dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0,
+                         "tc3_conv_kernel": 92.0}.get(name)
+            if floor_cyc and roofline and roofline.get("bound") == "tensor":
+                sm = peaks.get("sm_count", 148)
+                mhz = clk.summary().get("sm_mhz") or 1965.0
+                att = 2.0 * 128 * 32 * 16 / floor_cyc * sm * mhz * 1e6 / 1e12
+                roofline["mma_floor"] = {"peak": round(att, 1), "unit": "TFLOP/s",
+                                         "frac": round(roofline["achieved"] / att, 4),
+                                         "note": f"{floor_cyc:.0f} cycles per 128x32x16 step (measured per-MMA floor), "
+                                                 f"{sm} SMs at the sampled SM clock; ignores the padded border rows"}
             tr = _traffic(name)
             if tr is not None and roofline:
                 roofline["traffic"] = tr
