@@ -1460,8 +1460,10 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
     uint8_t *s_c = s_a + stage_bytes;                            // im2col ring
     float *s_bs = reinterpret_cast<float *>(s_c + kEfRing * kEfChunkBytes);
     float *s_bd = s_bs + N;
-    float *s_norm = s_bd + N;  // x / 127.5 - 1 for every byte value (vqvae.py:41-43)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s_norm + 256);
+    // per byte value: the fp16 hi | lo << 16 split of (x / 127.5 - 1) 2^14
+    // (vqvae.py:41-43): the stem operand is a function of the byte alone
+    uint32_t *s_hl = reinterpret_cast<uint32_t *>(s_bd + N);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_hl + 256);
     uint64_t *afull = bars, *aempty = afull + kEfRing;
     uint64_t *sfull = aempty + kEfRing, *sempty = sfull + kEfSlots;
     uint64_t *dfull = sempty + kEfSlots, *dempty = dfull + 1;
@@ -1474,7 +1476,12 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
         s_bs[threadIdx.x] = a.b_stem[threadIdx.x];
         s_bd[threadIdx.x] = a.b_down[threadIdx.x];
     }
-    for (int e = threadIdx.x; e < 256; e += blockDim.x) s_norm[e] = __fsub_rn(__fdiv_rn((float)e, 127.5f), 1.f);
+    for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+        const float xn = __fmul_rn(__fsub_rn(__fdiv_rn((float)e, 127.5f), 1.f), 16384.f);
+        uint32_t h, l;
+        split2(xn, 0.f, h, l);
+        s_hl[e] = (h & 0xFFFFu) | (l << 16);
+    }
     if (threadIdx.x == 0) {
         for (int r = 0; r < kEfRing; ++r) {
             mbar_init(&afull[r], 4);
@@ -1555,7 +1562,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
                 for (int e = 0; e < 16; ++e) hw[e] = lw[e] = 0u;
                 if (live) {
                     const uint8_t *img = a.img + (int64_t)n * a.H * a.W * 3;
-                    float xv[28];
+                    uint32_t xv[28];  // per tap the byte's hi | lo << 16 (K = c*9 + tap, 27 -> 28)
 #pragma unroll
                     for (int ki = 0; ki < 3; ++ki) {
                         const uint8_t *rp = img + (int64_t)min(max(sy + ki - 1, 0), a.H - 1) * a.W * 3;
@@ -1563,13 +1570,15 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
                         for (int kj = 0; kj < 3; ++kj) {
                             const uint8_t *px = rp + min(max(sx + kj - 1, 0), a.W - 1) * 3;
 #pragma unroll
-                            for (int ch = 0; ch < 3; ++ch) xv[ch * 9 + ki * 3 + kj] = s_norm[__ldg(px + ch)];
+                            for (int ch = 0; ch < 3; ++ch) xv[ch * 9 + ki * 3 + kj] = s_hl[__ldg(px + ch)];
                         }
                     }
-                    xv[27] = 0.f;
+                    xv[27] = 0u;
 #pragma unroll
-                    for (int e = 0; e < 14; ++e)  // k = 2e, 2e + 1; |x 2^14| <= 2^14
-                        split2(__fmul_rn(xv[2 * e], 16384.f), __fmul_rn(xv[2 * e + 1], 16384.f), hw[e], lw[e]);
+                    for (int e = 0; e < 14; ++e) {  // k = 2e, 2e + 1 (the same split2 of x 2^14, by table)
+                        hw[e] = __byte_perm(xv[2 * e], xv[2 * e + 1], 0x5410);
+                        lw[e] = __byte_perm(xv[2 * e], xv[2 * e + 1], 0x7632);
+                    }
                 }
 #pragma unroll
                 for (int kg = 0; kg < 4; ++kg) {
