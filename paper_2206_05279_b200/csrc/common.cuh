@@ -227,6 +227,77 @@ __device__ inline uint32_t warp_crc32(const CrcConsts *cc, const uint8_t *p, uin
     return crc;
 }
 
+// Raw crc32 register (init 0, no final xor) of 64 bytes held as 16
+// little-endian words, slice-by-4.
+__device__ inline uint32_t crc_raw64(const uint32_t *t0, const CrcSlices *sl, const uint32_t *w) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        c ^= w[i];
+        c = sl->t[2][c & 0xFF] ^ sl->t[1][(c >> 8) & 0xFF] ^ sl->t[0][(c >> 16) & 0xFF] ^ t0[c >> 24];
+    }
+    return c;
+}
+
+// Whole-warp crc32 of [p, p+n), no staging and no ragged rounds. The message
+// is virtually left-padded with zero bytes to a multiple of 2048 (zero bytes
+// leave a raw register at 0), so every round is 32 full 64-byte chunks, one
+// per lane, read straight from global memory (16-byte loads re-aligned with
+// funnel shifts) and merged with the constant powers x^(8*64*j); the
+// standard init / xorout enter once at the end through x^(8n) (a warp
+// product of the x^(2^k) factors of n). The source must be readable up to
+// the 16-byte boundary after p + n (the container buffers' pad).
+__device__ inline uint32_t warp_crc32_fast(const CrcConsts *cc, const CrcSlices *sl, const uint8_t *p, uint64_t n) {
+    const int lane = threadIdx.x & 31;
+    if (n == 0) return 0;
+    const int64_t pad = (int64_t)((2048 - n % 2048) % 2048);
+    uint32_t crc = 0;
+    for (int64_t r0 = -pad; r0 < (int64_t)n; r0 += 2048) {
+        const int64_t s = r0 + 64 * lane;
+        uint32_t c = 0;
+        uint32_t w[16];
+        if (s >= 0) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(p + s);
+            const uint4 *a0 = reinterpret_cast<const uint4 *>(a & ~(uintptr_t)15);
+            const int off = (int)(a & 15), q = off >> 2, sh = 8 * (off & 3);
+            uint32_t W[20];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const uint4 v = a0[k];
+                W[4 * k] = v.x;
+                W[4 * k + 1] = v.y;
+                W[4 * k + 2] = v.z;
+                W[4 * k + 3] = v.w;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t lo = q == 0 ? W[i] : q == 1 ? W[i + 1] : q == 2 ? W[i + 2] : W[i + 3];
+                const uint32_t hi = q == 0 ? W[i + 1] : q == 1 ? W[i + 2] : q == 2 ? W[i + 3] : W[i + 4];
+                w[i] = __funnelshift_r(lo, hi, sh);
+            }
+            c = crc_raw64(cc->tab, sl, w);
+        } else if (s + 64 > 0) {  // the chunk holding the first byte: what precedes p is zero
+#pragma unroll 1
+            for (int i = 0; i < 16; ++i) {
+                uint32_t v = 0;
+                for (int b = 0; b < 4; ++b) {
+                    const int64_t j = s + 4 * i + b;
+                    if (j >= 0) v |= (uint32_t)p[j] << (8 * b);
+                }
+                w[i] = v;
+            }
+            c = crc_raw64(cc->tab, sl, w);
+        }
+        const uint32_t term = c ? crc_multmodp(cc->qpow[31 - lane], c) : 0u;
+        crc = crc_multmodp(cc->qpow[32], crc) ^ warp_xor(term);
+    }
+    // standard crc32 = raw ^ 0xFFFFFFFF x^(8n) ^ 0xFFFFFFFF
+    uint32_t f = ((n >> lane) & 1) ? cc->x2n[(lane + 3) & 31] : (1u << 31);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) f = crc_multmodp(f, __shfl_xor_sync(0xffffffffu, f, o));
+    return crc ^ crc_multmodp(f, 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+}
+
 __device__ inline void load_crc_consts(CrcConsts *dst, const CrcConsts &src) {
     const uint32_t *s = reinterpret_cast<const uint32_t *>(&src);
     uint32_t *d = reinterpret_cast<uint32_t *>(dst);

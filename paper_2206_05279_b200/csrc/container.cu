@@ -165,13 +165,39 @@ struct PackArgs {
 };
 
 // Copy one lane blob (u64 nbits + payload bytes from 32-bit scratch words).
+// The payload lands at an arbitrary byte offset: whole destination-aligned
+// words are assembled from two source words with a funnel shift and stored
+// as 32-bit words; the partial words at either end go byte by byte (the
+// bytes around belong to the header and to the next blob). Tail bits zero.
 __device__ void put_lane(uint8_t *dst, const uint32_t *words, uint32_t nbits, int lane) {
     const uint32_t nbytes = (nbits + 7) >> 3;
     if (lane < 8) dst[lane] = lane < 4 ? (nbits >> (8 * lane)) & 0xFF : 0;
-    for (uint32_t j = lane; j < nbytes; j += 32) {
+    if (nbytes == 0) return;
+    uint8_t *pay = dst + 8;
+    const uint32_t tmask = (nbits & 7) ? (1u << (nbits & 7)) - 1u : 0xFFu;
+    auto src_byte = [&](uint32_t j) -> uint32_t {
         uint32_t v = (words[j >> 2] >> (8 * (j & 3))) & 0xFF;
-        if (j == nbytes - 1 && (nbits & 7)) v &= (1u << (nbits & 7)) - 1;  // tail bits zero
-        dst[8 + j] = (uint8_t)v;
+        return j == nbytes - 1 ? v & tmask : v;
+    };
+    const uint32_t a = (uint32_t)(reinterpret_cast<uintptr_t>(pay) & 3);
+    const uint32_t head = a ? 4 - a : 0;                       // bytes before the first aligned word
+    if (head >= nbytes || nbytes - head < 8) {                 // short: bytes only
+        for (uint32_t j = lane; j < nbytes; j += 32) pay[j] = (uint8_t)src_byte(j);
+        return;
+    }
+    const uint32_t nw = (nbytes - head) >> 2;                  // whole aligned words
+    const uint32_t tail0 = head + 4 * nw;                      // first byte after them
+    if (lane < (int)head) pay[lane] = (uint8_t)src_byte(lane);
+    if (lane < (int)(nbytes - tail0)) pay[tail0 + lane] = (uint8_t)src_byte(tail0 + lane);
+    uint32_t *pw = reinterpret_cast<uint32_t *>(pay + head);
+    // aligned word m holds payload bytes head + 4m .. +3 = source bytes
+    // starting at byte (head & 3) of source word (head >> 2) + m
+    const uint32_t s0 = head >> 2, sh = 8 * (head & 3);
+    for (uint32_t m = lane; m < nw; m += 32) {
+        const uint32_t lo = words[s0 + m];
+        uint32_t v = sh ? __funnelshift_r(lo, words[s0 + m + 1], sh) : lo;
+        if (head + 4 * m + 3 == nbytes - 1) v = (v & 0x00FFFFFFu) | ((v >> 24 & tmask) << 24);
+        pw[m] = v;
     }
 }
 
@@ -272,7 +298,7 @@ __global__ void __launch_bounds__(32 * kWarps) pack_kernel(PackArgs a, CrcConsts
         __syncwarp();
         __threadfence_block();
         // the output buffer carries 16 bytes of slack (pilc.h): vector reads
-        const uint32_t crc = warp_crc32<true>(&cc, blob, size - 4, stage[warp], &sl);
+        const uint32_t crc = warp_crc32_fast(&cc, &sl, blob, size - 4);
         if (lane == 0) wr_u32(blob + size - 4, crc);
     }
 }
@@ -306,7 +332,7 @@ __global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__res
         }
         if (!st) {
             // blob buffers are padded by 16 bytes (pilc.h): vector reads
-            const uint32_t crc = warp_crc32<true>(&cc, b, n - 4, stage[warp], &sl);
+            const uint32_t crc = warp_crc32_fast(&cc, &sl, b, n - 4);
             if (crc != rd_u32(b + n - 4)) st = PILC_ST_CRC;
         }
         // sequential structure walk (lane 0), mirroring _Reader.take
