@@ -104,10 +104,11 @@ def _template(backend: int, cfg: CodecConfig, W: int, H: int, params: PredictorP
     return t
 
 
-def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, stream):
+def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, stream, idx_d=None):
     """One (H, W) group, all on `stream`, with no host synchronisation.
     Returns (out_d, blob_off_d): blob i is out_d[blob_off_d[i]:blob_off_d[i+1]]
-    (out_d is sized for the worst case)."""
+    (out_d is sized for the worst case). `idx_d`: codebook indices already
+    computed on `stream` (the staged host path encodes while it copies)."""
     N, H, W, _ = img_d.shape
     if W >= (1 << 32) or H >= (1 << 32):
         raise ParameterError("image dimensions do not fit 32 bits")
@@ -125,7 +126,8 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
     if backend == BACKEND_VQVAE:
         if model is None or not model.has_network:
             raise ModelError("vqvae backend needs model weights")
-        idx_d = encode_indices_device(img_d, model, dev, stream)
+        if idx_d is None:
+            idx_d = encode_indices_device(img_d, model, dev, stream)
         shift, dsched = decode_head_device(idx_d, model, H, W, grid, dev, stream)
         idx_enc, _ = build_tables([index_histogram_pmf(model, M)], M, verify=config.verify_tables)
         gh, gw = latent_shape(H, W)
@@ -153,6 +155,40 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
               ptr(idx_st), ptr(res_scr), res_cap, ptr(res_nb), ptr(res_st), ptr(blob_off), ptr(out_d),
               sptr(stream))
     return out_d, blob_off
+
+
+_STAGE_MIN = 1024  # images; smaller batches are copied in one piece
+
+
+def _staged_encode(arr: np.ndarray, model, config: CodecConfig, dev, stream):
+    """Host batch -> device in 2 or 4 pieces on a copy stream while the
+    encoder (the longest stage, and the only one that needs nothing but the
+    images) runs on the pieces already there: only the first piece's copy is
+    exposed. Returns
+    (img_d, idx_d) or None when not worth it (static backend, small batch).
+    Per-image results do not depend on the split."""
+    N = arr.shape[0]
+    if config.backend != "twar-vqvae" or N < _STAGE_MIN or model is None or not model.has_network:
+        return None
+    copy = CACHE.get(("copy-stream",), dev, lambda: torch.cuda.Stream(dev))
+    img_d = torch.empty(arr.shape, dtype=torch.uint8, device=dev)
+    img_d.record_stream(copy)
+    k = 4 if N >= 4 * _STAGE_MIN else 2  # pieces: only the first one's copy is exposed
+    cuts = [N * i // k for i in range(k + 1)]
+    parts = []
+    copy.wait_stream(stream)  # img_d's allocation is ordered on `stream`
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        src = np.ascontiguousarray(arr[a:b])
+        h = torch.from_numpy(src) if src.flags.writeable else torch.from_numpy(src.copy())
+        with torch.cuda.stream(copy):
+            img_d[a:b].copy_(h, non_blocking=h.is_pinned())
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        stream.wait_event(ev)
+        parts.append(encode_indices_device(img_d[a:b], model, dev, stream))
+    with torch.cuda.stream(stream):
+        idx_d = torch.cat(parts)
+    return img_d, idx_d
 
 
 def _groups_by_shape(shapes):
@@ -200,10 +236,15 @@ def compress_batch(images, model: ModelWeights | None = None, config: CodecConfi
             raise ParameterError("expected a uint8 (N, H, W, 3) array")
         if arr.shape[1] < 1 or arr.shape[2] < 1:
             raise ParameterError("image dimensions must be >= 1")
-        img_d = as_device_u8(arr, dev, stream)
+        if img_d_staged := _staged_encode(arr, model, config, dev, stream):
+            img_d, idx_d = img_d_staged
+        else:
+            img_d, idx_d = as_device_u8(arr, dev, stream), None
     if img_d.shape[0] == 0:
         return np.zeros(0, np.uint8), np.zeros(1, np.uint64)
-    out_d, off_d = _compress_device(img_d, model, config, dev, stream)
+    if isinstance(images, torch.Tensor):
+        idx_d = None
+    out_d, off_d = _compress_device(img_d, model, config, dev, stream, idx_d=idx_d)
     n = img_d.shape[0]
     offs = pinned(8 * (n + 1))
     with torch.cuda.stream(stream):
