@@ -243,13 +243,25 @@ __device__ inline uint32_t crc_raw64(const uint32_t *t0, const CrcSlices *sl, co
 // is virtually left-padded with zero bytes to a multiple of 2048 (zero bytes
 // leave a raw register at 0), so every round is 32 full 64-byte chunks, one
 // per lane, read straight from global memory (16-byte loads re-aligned with
-// funnel shifts) and merged with the constant powers x^(8*64*j); the
-// standard init / xorout enter once at the end through x^(8n) (a warp
-// product of the x^(2^k) factors of n). The source must be readable up to
+// funnel shifts) and merged pairwise with table multiplications by the
+// constants x^(8*64*2^k); the standard init enters as 0xFF XORed into the
+// first four bytes and the xorout at the end. The source must be readable up to
 // the 16-byte boundary after p + n (the container buffers' pad).
-__device__ inline uint32_t warp_crc32_fast(const CrcConsts *cc, const CrcSlices *sl, const uint8_t *p, uint64_t n) {
+// Multiplication by the constants x^(8*64*s), s = 1, 2, 4, 8, 16, 32, as
+// byte-sliced tables (the map c -> c x^k mod P is linear): [6][4][256]
+// words, built once on the host (crc_mul_tables, container.cu), read
+// through the read-only cache.
+constexpr int kCrcMulTables = 6 * 4 * 256;
+__device__ inline uint32_t crc_mulk(const uint32_t *__restrict__ mt, int k, uint32_t c) {
+    const uint32_t *t = mt + k * 1024;
+    return __ldg(t + (c & 0xFF)) ^ __ldg(t + 256 + ((c >> 8) & 0xFF)) ^ __ldg(t + 512 + ((c >> 16) & 0xFF)) ^
+           __ldg(t + 768 + (c >> 24));
+}
+
+__device__ inline uint32_t warp_crc32_fast(const CrcConsts *cc, const CrcSlices *sl, const uint32_t *__restrict__ mt,
+                                           const uint8_t *p, uint64_t n) {
     const int lane = threadIdx.x & 31;
-    if (n == 0) return 0;
+    if (n < 4) return __shfl_sync(0xffffffffu, crc_bytes(cc->tab, p, (int)n), 0);  // tiny messages
     const int64_t pad = (int64_t)((2048 - n % 2048) % 2048);
     uint32_t crc = 0;
     for (int64_t r0 = -pad; r0 < (int64_t)n; r0 += 2048) {
@@ -275,6 +287,7 @@ __device__ inline uint32_t warp_crc32_fast(const CrcConsts *cc, const CrcSlices 
                 const uint32_t hi = q == 0 ? W[i + 1] : q == 1 ? W[i + 2] : q == 2 ? W[i + 3] : W[i + 4];
                 w[i] = __funnelshift_r(lo, hi, sh);
             }
+            if (s < 4) w[0] ^= 0xFFFFFFFFu >> (8 * s);  // the init register, folded into bytes 0..3
             c = crc_raw64(cc->tab, sl, w);
         } else if (s + 64 > 0) {  // the chunk holding the first byte: what precedes p is zero
 #pragma unroll 1
@@ -282,20 +295,24 @@ __device__ inline uint32_t warp_crc32_fast(const CrcConsts *cc, const CrcSlices 
                 uint32_t v = 0;
                 for (int b = 0; b < 4; ++b) {
                     const int64_t j = s + 4 * i + b;
-                    if (j >= 0) v |= (uint32_t)p[j] << (8 * b);
+                    if (j >= 0) v |= (uint32_t)(p[j] ^ (j < 4 ? 0xFF : 0)) << (8 * b);
                 }
                 w[i] = v;
             }
             c = crc_raw64(cc->tab, sl, w);
         }
-        const uint32_t term = c ? crc_multmodp(cc->qpow[31 - lane], c) : 0u;
-        crc = crc_multmodp(cc->qpow[32], crc) ^ warp_xor(term);
-    }
-    // standard crc32 = raw ^ 0xFFFFFFFF x^(8n) ^ 0xFFFFFFFF
-    uint32_t f = ((n >> lane) & 1) ? cc->x2n[(lane + 3) & 31] : (1u << 31);
+        // merge the 32 chunk registers pairwise: level k joins 64*2^k-byte
+        // neighbours, the left one times x^(8*64*2^k); lane 0 ends with the round
 #pragma unroll
-    for (int o = 16; o; o >>= 1) f = crc_multmodp(f, __shfl_xor_sync(0xffffffffu, f, o));
-    return crc ^ crc_multmodp(f, 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+        for (int k = 0; k < 5; ++k) {
+            const uint32_t w = __shfl_down_sync(0xffffffffu, c, 1 << k);
+            if ((lane & ((2 << k) - 1)) == 0) c = crc_mulk(mt, k, c) ^ w;
+        }
+        crc = crc_mulk(mt, 5, crc) ^ __shfl_sync(0xffffffffu, c, 0);
+    }
+    // the standard crc's init register entered as 0xFF XORed into bytes 0..3
+    // (crc_I(M) = crc_0(M ^ I) for |M| >= 4); its final xor:
+    return crc ^ 0xFFFFFFFFu;
 }
 
 __device__ inline void load_crc_consts(CrcConsts *dst, const CrcConsts &src) {

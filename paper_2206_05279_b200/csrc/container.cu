@@ -14,6 +14,9 @@
 #include <math.h>
 #include <string.h>
 
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 
 // ---------------------------------------------------------------------------
@@ -37,6 +40,29 @@ const CrcConsts &crc_consts() {
         init = true;
     }
     return cc;
+}
+
+// Device copy of the constant-multiplication tables (common.cuh), per device.
+const uint32_t *crc_mul_tables() {
+    static const uint32_t *dev_tab[64] = {};
+    static std::mutex mu;
+    int d = 0;
+    cudaGetDevice(&d);
+    std::lock_guard<std::mutex> g(mu);
+    if (d < 0 || d >= 64) return nullptr;
+    if (!dev_tab[d]) {
+        const CrcConsts &cc = crc_consts();
+        std::vector<uint32_t> h(kCrcMulTables);
+        const int pw[6] = {1, 2, 4, 8, 16, 32};
+        for (int k = 0; k < 6; ++k)
+            for (int j = 0; j < 4; ++j)
+                for (uint32_t v = 0; v < 256; ++v) h[k * 1024 + j * 256 + v] = crc_multmodp(cc.qpow[pw[k]], v << (8 * j));
+        void *p = nullptr;
+        if (cudaMalloc(&p, h.size() * 4) != cudaSuccess) return nullptr;
+        cudaMemcpy(p, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+        dev_tab[d] = static_cast<const uint32_t *>(p);
+    }
+    return dev_tab[d];
 }
 
 namespace {
@@ -255,7 +281,7 @@ __device__ uint32_t sched_crc_warp(const CrcConsts *cc, const uint8_t *dsched, u
     return crc;
 }
 
-__global__ void __launch_bounds__(32 * kWarps) pack_kernel(PackArgs a, CrcConsts ccv) {
+__global__ void __launch_bounds__(32 * kWarps) pack_kernel(PackArgs a, CrcConsts ccv, const uint32_t *__restrict__ mt) {
     __shared__ CrcConsts cc;
     __shared__ CrcSlices sl;
     __shared__ __align__(16) uint8_t stage[kWarps][kStage];
@@ -298,7 +324,7 @@ __global__ void __launch_bounds__(32 * kWarps) pack_kernel(PackArgs a, CrcConsts
         __syncwarp();
         __threadfence_block();
         // the output buffer carries 16 bytes of slack (pilc.h): vector reads
-        const uint32_t crc = warp_crc32_fast(&cc, &sl, blob, size - 4);
+        const uint32_t crc = warp_crc32_fast(&cc, &sl, mt, blob, size - 4);
         if (lane == 0) wr_u32(blob + size - 4, crc);
     }
 }
@@ -308,7 +334,8 @@ __global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__res
                                                             const uint64_t *__restrict__ blob_off,
                                                             int64_t n_blob, uint64_t params_hash,
                                                             uint64_t model_hash, int has_model,
-                                                            pilc_header *hdr, CrcConsts ccv) {
+                                                            pilc_header *hdr, CrcConsts ccv,
+                                                            const uint32_t *__restrict__ mt) {
     __shared__ CrcConsts cc;
     __shared__ CrcSlices sl;
     __shared__ __align__(16) uint8_t stage[kWarps][kStage];
@@ -332,7 +359,7 @@ __global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__res
         }
         if (!st) {
             // blob buffers are padded by 16 bytes (pilc.h): vector reads
-            const uint32_t crc = warp_crc32_fast(&cc, &sl, b, n - 4);
+            const uint32_t crc = warp_crc32_fast(&cc, &sl, mt, b, n - 4);
             if (crc != rd_u32(b + n - 4)) st = PILC_ST_CRC;
         }
         // sequential structure walk (lane 0), mirroring _Reader.take
@@ -651,7 +678,9 @@ extern "C" int pilc_container_pack(const uint8_t *tmpl, int32_t template_len, co
                res_nbits, res_states,  blob_off,    out,        tmpl,       template_len};
     {
         ProfScope _ps(PROF_PACK, s, (double)n_img);
-        pack_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(a, crc_consts());
+        const uint32_t *mt = crc_mul_tables();
+        if (!mt) return PILC_E_CUDA;
+        pack_kernel<<<warp_grid(n_img), 32 * kWarps, 0, s>>>(a, crc_consts(), mt);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
@@ -662,10 +691,12 @@ extern "C" int pilc_container_parse(const uint8_t *buf, const uint64_t *blob_off
                                     pilc_header *hdr, void *stream) {
     if (n_blob < 0 || !blob_off || !hdr) return PILC_E_ARG;
     if (n_blob == 0) return PILC_OK;
-{
+    const uint32_t *mt = crc_mul_tables();
+    if (!mt) return PILC_E_CUDA;
+    {
         ProfScope _ps(PROF_PARSE, as_stream(stream), (double)n_blob);
         parse_kernel<<<warp_grid(n_blob), 32 * kWarps, 0, as_stream(stream)>>>(
-        buf, blob_off, n_blob, params_hash, model_hash, has_model, hdr, crc_consts());
+            buf, blob_off, n_blob, params_hash, model_hash, has_model, hdr, crc_consts(), mt);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
