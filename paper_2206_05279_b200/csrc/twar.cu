@@ -17,6 +17,12 @@ struct Params {
 };
 
 __device__ __forceinline__ uint32_t round_mod256(float acc) {
+    // |acc| < 2^22: acc +- 0.5 is exact in float32, so floor / ceil there
+    // equal the float64 ones (the common case: unit weights, byte contexts)
+    if (fabsf(acc) < 4194304.f) {
+        const float r = acc >= 0.f ? floorf(__fadd_rn(acc, 0.5f)) : ceilf(__fsub_rn(acc, 0.5f));
+        return (uint32_t)((int)r & 255);
+    }
     const double p = (double)acc;
     const double r = p >= 0.0 ? floor(p + 0.5) : ceil(p - 0.5);
     if (fabs(r) < 4.0e18) return (uint32_t)((long long)r & 255LL);
@@ -36,12 +42,22 @@ __device__ __forceinline__ uint32_t predict(float c0, float c1, float c2, const 
 // One thread per pixel, all three channels (predictor.py:173-195).
 __global__ void twar_forward_kernel(const uint8_t *__restrict__ img, uint8_t *__restrict__ res,
                                     int64_t n_px, int H, int W, Params p) {
+    const int64_t hw = (int64_t)H * W;
+    const bool small = n_px < (1ll << 32) && hw < (1ll << 32);
+    const uint32_t hw32 = (uint32_t)hw, w32 = (uint32_t)W;
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_px;
          g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t hw = (int64_t)H * W;
-        const int64_t n = g / hw;
-        const int rem = (int)(g - n * hw);
-        const int u = rem / W, v = rem - (rem / W) * W;
+        int64_t n;
+        int rem;
+        if (small) {  // 32-bit divisions (the 64-bit ones are a long software sequence)
+            const uint32_t n32 = (uint32_t)g / hw32;
+            n = n32;
+            rem = (int)((uint32_t)g - n32 * hw32);
+        } else {
+            n = g / hw;
+            rem = (int)(g - n * hw);
+        }
+        const int u = (int)((uint32_t)rem / w32), v = rem - u * W;
         const uint8_t *x = img + n * hw * 3;
         const int64_t o = (int64_t)rem * 3;
         const float r = x[o], gg = x[o + 1], bb = x[o + 2];

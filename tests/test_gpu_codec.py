@@ -69,6 +69,20 @@ def test_twar_random_params_vs_oracle(shape):
     assert np.array_equal(predictor.decode_parallel_batch(res, p), imgs)
 
 
+@pytest.mark.parametrize("bias", [4194303.5, 4194304.0, -4194304.5, 1.5e7, 3.0e9, -2.5e10])
+def test_twar_large_accumulators_vs_oracle(bias):
+    """round_mod256 takes a float32 path below |acc| = 2^22 and the float64
+    one above; both must agree with the reference rounding at the switch."""
+    rng = np.random.default_rng(7)
+    imgs = rng.integers(0, 256, (4, 9, 11, 3), dtype=np.uint8)
+    w = np.array([[0.5, -1, 1], [1, -1, 0.25], [1, -0.5, 1]], np.float32)
+    b = np.array([bias, -bias, bias / 3], np.float32)
+    p = predictor.PredictorParams(w, b)
+    res = predictor.forward_residual_batch(imgs, p)
+    assert np.array_equal(res, O.twar_forward(imgs, w, b))
+    assert np.array_equal(predictor.decode_parallel_batch(res, p), imgs)
+
+
 def test_twar_exhaustive_2x2_sample():
     # acceptance 6 style: many 2x2 images with 4-value alphabets
     rng = np.random.default_rng(7)
