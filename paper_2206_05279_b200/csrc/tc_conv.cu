@@ -464,21 +464,6 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-__device__ __forceinline__ void store_px4(float *slab, int64_t q, float4 v, int y, int x, int H, int W, int Wp) {
-    float4 *p = reinterpret_cast<float4 *>(slab);
-    p[q] = v;
-    const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
-    const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
-    if (dy) p[q - Wp] = v;
-    if (dy2) p[q + Wp] = v;
-    if (dx) p[q - 1] = v;
-    if (dx2) p[q + 1] = v;
-    if (dy && dx) p[q - Wp - 1] = v;
-    if (dy && dx2) p[q - Wp + 1] = v;
-    if (dy2 && dx) p[q + Wp - 1] = v;
-    if (dy2 && dx2) p[q + Wp + 1] = v;
-}
-
 // Encoder conv, C = 32 in, N = 32 out, as a 3-product fp16 split on
 // tcgen05 kind::f16: fp32-class accuracy at twice the tf32 MMA rate (an
 // SS-mode MMA with N <= 64 is bound by reading its operands from shared
@@ -781,8 +766,9 @@ __global__ void __launch_bounds__(kThreadsTC3, 1) tc3_conv_kernel(Tc3Layer L) {
                         }
                         if (L.out32) {
                             const int64_t so = ((int64_t)g * L.gstride + L.margin) * 4;
-                            store_px4(L.out32 + so, q, make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]),
-                                      y, x, H, W, Wp);
+                            // fp32 copy: valid pixels only (no reader uses its edge copies)
+                            reinterpret_cast<float4 *>(L.out32 + so)[q] =
+                                make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
                         }
                     }
 #pragma unroll
@@ -1137,8 +1123,9 @@ __global__ void __launch_bounds__(kThreadsBK, 1) tc3_block_kernel(Tc3Block L) {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) mx = fmaxf(mx, fabsf(v[4 * g + e]));
                         if (L.out32)
-                            store_px4(L.out32 + ((int64_t)g * L.gstride + L.margin) * 4, q,
-                                      make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]), y, x, H, W, Wp);
+                            // fp32 copy: valid pixels only (no reader uses its edge copies)
+                            reinterpret_cast<float4 *>(L.out32 + ((int64_t)g * L.gstride + L.margin) * 4)[q] =
+                                make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
                     }
 #pragma unroll
                     for (int g = 0; g < NH; ++g) {
@@ -1743,8 +1730,9 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
 #pragma unroll
                     for (int e = 0; e < 4; ++e) mx = fmaxf(mx, v[4 * g + e]);
                     const int64_t so = ((int64_t)g * a.gstride + a.margin) * 4;
-                    store_px4(a.out32 + so, q, make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]), y, x,
-                              H, W, Wp);
+                    // fp32 copy: valid pixels only (no reader uses its edge copies)
+                    reinterpret_cast<float4 *>(a.out32 + so)[q] =
+                        make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
