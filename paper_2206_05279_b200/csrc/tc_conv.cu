@@ -965,40 +965,46 @@ __global__ void __launch_bounds__(kThreadsBK, 1) tc3_block_kernel(Tc3Block L) {
         const uint64_t dW2 = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w2), 0), (uint32_t)N2 * 16u, 128u);
         const uint32_t rx = (uint32_t)RX;
         int64_t ti = 0;
-        auto conv = [&](uint64_t dA, uint64_t dB, int it2) {
-            for (int j = 0; j < T; ++j, ++ti) {
-                if (it2 >= 0) {  // conv2 tile j reads T rows of conv1 tiles j - 1 .. j + 1
-                    if (j == 0) mbar_wait(&hrdy[0], it2 & 1);
-                    if (j + 1 < T) mbar_wait(&hrdy[j + 1], it2 & 1);
-                    tc_fence_after();
-                }
-                const int a = (int)(ti & 1);
-                const int64_t u = ti >> 1;
-                if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
-                tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(a * N2);
-                const uint32_t r0 = (uint32_t)(M0 + 128 * j - Wp - 1);
-#pragma unroll
-                for (int tap = 0; tap < 9; ++tap) {
-                    const uint32_t off = r0 + (uint32_t)((tap / 3) * Wp + tap % 3);
-#pragma unroll
-                    for (int ks = 0; ks < NH / 2; ++ks) {
-                        const uint64_t ao = (uint64_t)(2u * ks * rx + off);
-                        const uint64_t bo = (uint64_t)((tap * NH + 2 * ks) * N2);
-                        mma_f16_elect(d, dA + ao, dB + bo, idesc64, (tap | ks) ? 1u : 0u);
-                        mma_f16_elect(d + N, dA + ao + (uint64_t)(NH * rx), dB + bo, idesc32, 1u);
-                    }
-                }
-                mma_commit_elect(&tfull[a]);
-            }
-        };
         int it = 0;
         for (int64_t n = blockIdx.x; n < n_img; n += gridDim.x, ++it) {
-            mbar_wait(xfull, it & 1);
-            tc_fence_after();
-            conv(dX, dW1, -1);
-            mma_commit_elect(xfree);
-            conv(dH, dW2, it);
+            // two passes per image: conv1 over X, then conv2 over T; inline
+            // (no lambda) so the descriptors stay in uniform registers
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+                if (pass == 0) {
+                    mbar_wait(xfull, it & 1);
+                    tc_fence_after();
+                }
+                const uint64_t dA = pass ? dH : dX;
+                const uint64_t dB = pass ? dW2 : dW1;
+#pragma unroll 1
+                for (int j = 0; j < T; ++j, ++ti) {
+                    if (pass) {  // conv2 tile j reads T rows of conv1 tiles j - 1 .. j + 1
+                        if (j == 0) mbar_wait(&hrdy[0], it & 1);
+                        if (j + 1 < T) mbar_wait(&hrdy[j + 1], it & 1);
+                        tc_fence_after();
+                    }
+                    const int a = (int)(ti & 1);
+                    const int64_t u = ti >> 1;
+                    if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
+                    tc_fence_after();
+                    const uint32_t d = tmem + (uint32_t)(a * N2);
+                    const uint64_t dAt = dA + (uint64_t)(uint32_t)(M0 + 128 * j - Wp - 1);
+#pragma unroll
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const uint32_t off = (uint32_t)((tap / 3) * Wp + tap % 3);
+#pragma unroll
+                        for (int ks = 0; ks < NH / 2; ++ks) {
+                            const uint64_t ao = (uint64_t)(2u * ks * rx + off);
+                            const uint64_t bo = (uint64_t)((tap * NH + 2 * ks) * N2);
+                            mma_f16_elect(d, dAt + ao, dB + bo, idesc64, (tap | ks) ? 1u : 0u);
+                            mma_f16_elect(d + N, dAt + ao + (uint64_t)(NH * rx), dB + bo, idesc32, 1u);
+                        }
+                    }
+                    mma_commit_elect(&tfull[a]);
+                }
+                if (pass == 0) mma_commit_elect(xfree);
+            }
         }
     } else {
         const int grp = (warp - 2) >> 2;
