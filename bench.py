@@ -329,7 +329,7 @@ def run_gpu(args):
     # end to end through the public API with host buffers (after the same
     # number of untimed warm-up calls as the device loop: the first calls
     # page-lock their host buffers)
-    e2e_times = []
+    e2e_times, e2e_c, e2e_d = [], [], []
     h2d = d2h = 0
     lat = None
     for _ in range(max(1, args.warmup)):
@@ -346,12 +346,19 @@ def run_gpu(args):
         t0 = time.perf_counter()
         if args.workload == "1080p":
             buf, off = pt.compress_frames(imgs, model, cfg)
+            torch.cuda.synchronize(dev)
+            t1 = time.perf_counter()
             out = pt.decompress_frames(buf, off, len(imgs), wl["H"], wl["W"], model)
         else:
             buf, off = pc.compress_batch(imgs, model, cfg)
+            torch.cuda.synchronize(dev)
+            t1 = time.perf_counter()
             out = pc.decompress_batch(buf, off, model)
         torch.cuda.synchronize(dev)
-        e2e_times.append(time.perf_counter() - t0)
+        t2 = time.perf_counter()
+        e2e_times.append(t2 - t0)
+        e2e_c.append(t1 - t0)
+        e2e_d.append(t2 - t1)
         h2d = imgs.nbytes + buf.nbytes + off.nbytes
         d2h = buf.nbytes + off.nbytes + out.nbytes
     assert np.array_equal(out, imgs)
@@ -435,7 +442,32 @@ def run_gpu(args):
                 roofline["traffic"] = tr
                 roofline["traffic_gbs"] = round(tr / (ms / n / 1e3) / 1e9, 1)
                 roofline["traffic_frac_of_hbm"] = round(tr / (ms / n / 1e3) / 1e9 / peaks.get("hbm_gbs"), 4)
-        stages = {k: {"launches": v[0], "ms_per_step": round(v[1] / args.steps, 4)} for k, v in prof.items()}
+        # per-stage rooflines: tensor kernels against the dense bf16 peak (and
+        # the per-MMA floor), every kernel's DRAM bytes (committed ncu capture,
+        # per launch) against the measured HBM bandwidth
+        ncu_name = {"enc_front_kernel": "enc_front_tc_kernel", "argmin_kernel": "argmin_tc_kernel",
+                    "gather_kernel": "dec_table_kernel", "blob_sizes+scan": "blob_sizes_kernel"}
+        hbm_peak = peaks.get("hbm_gbs")
+        tpeak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        # (up conv and head share tc_conv_kernel with different N: no single floor)
+        floor = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0}
+        mhz = clk.summary().get("sm_mhz") or 1965.0
+        stages = {}
+        for k, (n, ms, units) in prof.items():
+            e = {"launches": n, "ms_per_step": round(ms / args.steps, 4)}
+            tr = _traffic(ncu_name.get(k, k))
+            if tr is not None and ms > 0:
+                gbs = tr * n / (ms / 1e3) / 1e9
+                e["hbm_gbs"] = round(gbs, 1)
+                e["hbm_frac"] = round(gbs / hbm_peak, 4)
+            if k in notes and ms > 0:
+                tf = units / (ms / 1e3) / 1e12
+                e["tflops"] = round(tf, 2)
+                e["tensor_frac"] = round(tf / tpeak, 4)
+                if k in floor:
+                    att = 2.0 * 128 * 32 * 16 / floor[k] * peaks.get("sm_count", 148) * mhz * 1e6 / 1e12
+                    e["mma_floor_frac"] = round(tf / att, 4)
+            stages[k] = e
         cpu = None
         if ws == 1 and not args.no_cpu:
             procs = len(os.sched_getaffinity(0))
@@ -466,7 +498,9 @@ def run_gpu(args):
             "bpd": round(bpd, 4),
             "lossless": lossless,
             "e2e": {"value": round(e2e_value, 3), "unit": "MB/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
+                    "d2h_bytes_per_step": int(d2h),
+                    "compress_mb_s": round(raw_bytes / 1e6 / statistics.median(e2e_c), 3),
+                    "decompress_mb_s": round(raw_bytes / 1e6 / statistics.median(e2e_d), 3)},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "stages": stages,
