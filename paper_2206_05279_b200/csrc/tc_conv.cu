@@ -1435,6 +1435,7 @@ size_t dec_trunk_smem(int Hp, int Wp, int G, int K, int n_conv, int *pad) {
 constexpr int kEfThreads = 704;
 constexpr int kEfRing = 4;     // im2col chunk buffers
 constexpr int kEfSlots = 6;    // stem accumulators in TMEM (>= chunks per tile)
+constexpr int kEfMaxQ = 8;     // down-stage phase quarters, at most
 constexpr int kEfChunkBytes = 2 * 4 * 128 * 16;  // hi + lo, 4 K groups, 128 rows
 
 __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc a) {
@@ -1442,15 +1443,19 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
     const int Wp = a.gw + 2, Hp = a.gh + 2;
     const int npix = (128 + Wp + 1 + 7) & ~7;
     const int nch = (4 * npix + 127) >> 7;  // stem chunks per down tile
-    const uint32_t h_bytes = 16u * npix * 16u;  // 4 phases x 4 channel groups
-    const uint32_t stage_bytes = 2 * h_bytes;
+    // the down stage is a ring of nq phase quarters (one phase's 4 hi + 4 lo
+    // channel groups, npix rows each): tile i phase ph lives in quarter
+    // (4 i + ph) % nq, so the stem epilogue of the next tile writes a phase
+    // as soon as the down GEMM's last tap reading that quarter is done
+    const int nq = a.n_quarters;
+    const uint32_t q_bytes = 8u * npix * 16u;
     constexpr uint32_t wd_bytes = 36 * N2 * 16, ws_bytes = 4 * N2 * 16;
 
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *s_wd = smem;
     uint8_t *s_wsb = smem + wd_bytes;
-    uint8_t *s_a = s_wsb + ws_bytes;                             // down stage
-    uint8_t *s_c = s_a + stage_bytes;                            // im2col ring
+    uint8_t *s_a = s_wsb + ws_bytes;                             // down stage quarters [nq]
+    uint8_t *s_c = s_a + (size_t)nq * q_bytes;                   // im2col ring
     float *s_bs = reinterpret_cast<float *>(s_c + kEfRing * kEfChunkBytes);
     float *s_bd = s_bs + N;
     // per byte value: the fp16 hi | lo << 16 split of (x / 127.5 - 1) 2^14
@@ -1459,8 +1464,8 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_hl + 256);
     uint64_t *afull = bars, *aempty = afull + kEfRing;
     uint64_t *sfull = aempty + kEfRing, *sempty = sfull + kEfSlots;
-    uint64_t *dfull = sempty + kEfSlots, *dempty = dfull + 1;
-    uint64_t *tfull = dempty + 1, *tempty = tfull + 2;
+    uint64_t *dfull = sempty + kEfSlots, *qempty = dfull + 1;  // qempty[kEfMaxQ]
+    uint64_t *tfull = qempty + kEfMaxQ, *tempty = tfull + 2;
     uint64_t *wbar = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wbar + 1);
 
@@ -1485,7 +1490,7 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
             mbar_init(&sempty[r], 4);
         }
         mbar_init(dfull, 8);
-        mbar_init(dempty, 1);
+        for (int q = 0; q < kEfMaxQ; ++q) mbar_init(&qempty[q], 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4);
@@ -1624,7 +1629,6 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
             if (u > 0) mbar_wait(&tempty[b], (u - 1) & 1);
             mbar_wait(dfull, (uint32_t)i & 1);
             tc_fence_after();
-            const uint64_t dAl = dA0 + (uint64_t)(h_bytes >> 4);
             const uint32_t d = tmem_down + (uint32_t)(b * N2);
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
@@ -1632,14 +1636,18 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
                 const uint32_t rows = (uint32_t)((ti == 0 ? 0 : Wp) + (tj == 0 ? 0 : 1));  // (di + 1) Wp + (dj + 1)
                 const uint32_t ph = (uint32_t)((ti == 1 ? 0 : 2) + (tj == 1 ? 0 : 1));     // pi * 2 + pj
 #pragma unroll
+                const uint32_t qs = (uint32_t)((4 * i + (int)ph) % nq);
+                const uint64_t dq = dA0 + (uint64_t)(qs * (q_bytes >> 4));
+#pragma unroll
                 for (int ks = 0; ks < 2; ++ks) {
-                    const uint64_t ao = (uint64_t)((ph * 4u + 2u * ks) * npx + rows);
+                    const uint64_t ao = (uint64_t)(2u * ks * npx + rows);
                     const uint64_t bo = (uint64_t)((tap * 4 + 2 * ks) * N2);
-                    mma_f16_elect(d, dA0 + ao, dB0 + bo, idesc64, (tap | ks) ? 1u : 0u);
-                    mma_f16_elect(d + N, dAl + ao, dB0 + bo, idesc32, 1u);
+                    mma_f16_elect(d, dq + ao, dB0 + bo, idesc64, (tap | ks) ? 1u : 0u);
+                    mma_f16_elect(d + N, dq + ao + (uint64_t)(4u * npx), dB0 + bo, idesc32, 1u);
                 }
+                // taps 4, 5, 7, 8 are the last readers of phases 0, 1, 2, 3
+                if (tap == 4 || tap == 5 || tap == 7 || tap == 8) mma_commit_elect(&qempty[qs]);
             }
-            mma_commit_elect(dempty);
             mma_commit_elect(&tfull[b]);
         }
     } else if (warp >= 6) {
@@ -1652,14 +1660,19 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
         const int kws = __float_as_int(a.meta_stem[0]);
         const float inv = exp2i(-14 - kws);
         const float sc = exp2i(__float_as_int(a.meta_down[3]));
-        uint4 *hs = reinterpret_cast<uint4 *>(s_a);
-        uint4 *ls = hs + 16 * npix;
+        uint4 *hs0 = reinterpret_cast<uint4 *>(s_a);
         int64_t g = 0;
         int i = 0;
         for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            if (i > 0) mbar_wait(dempty, (uint32_t)(i - 1) & 1);  // the down GEMM of the previous tile is done
             for (int c = 0; c < nch; ++c, ++g) {
                 if ((int)(g & 1) != grp) continue;
+                // the quarters this chunk writes must be free: their previous
+                // tile's last reading tap has completed
+                const int ph_lo = min(3, (128 * c) / npix), ph_hi = min(3, (128 * c + 127) / npix);
+                for (int q = ph_lo; q <= ph_hi; ++q) {
+                    const int qg = 4 * i + q;
+                    if (qg >= nq) mbar_wait(&qempty[qg % nq], (uint32_t)((qg / nq) - 1) & 1);
+                }
                 const int sl = (int)(g % kEfSlots);
                 int ph, p, sy, sx;
                 uint32_t n;
@@ -1688,8 +1701,9 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
                         split2(v[8 * j + 2], v[8 * j + 3], h.y, l.y);
                         split2(v[8 * j + 4], v[8 * j + 5], h.z, l.z);
                         split2(v[8 * j + 6], v[8 * j + 7], h.w, l.w);
-                        hs[(ph * 4 + j) * npix + p] = h;
-                        ls[(ph * 4 + j) * npix + p] = l;
+                        uint4 *hq = hs0 + (size_t)((4 * i + ph) % nq) * (q_bytes / 16);
+                        hq[j * npix + p] = h;
+                        hq[(4 + j) * npix + p] = l;
                     }
                 }
             }
@@ -2123,8 +2137,15 @@ int enc_front_tc_launch(const EncFrontTc &a, cudaStream_t s) {
     const int Wp = a.gw + 2;
     const int npix = (128 + Wp + 1 + 7) & ~7;
     if ((4 * npix + 127) / 128 > kEfSlots) return PILC_E_UNSUPPORTED;
-    const size_t smem = 36 * 64 * 16 + 4 * 64 * 16 + (size_t)2 * 16 * npix * 16 + (size_t)kEfRing * kEfChunkBytes +
-                        (32 + 32 + 256) * 4 + 8 * (2 * kEfRing + 2 * kEfSlots + 7) + 16;
+    // as many down-stage phase quarters (>= 4, one full stage) as fit
+    auto smem_of = [&](int nq) {
+        return 36 * 64 * 16 + 4 * 64 * 16 + (size_t)nq * 8 * npix * 16 + (size_t)kEfRing * kEfChunkBytes +
+               (32 + 32 + 256) * 4 + 8 * (2 * kEfRing + 2 * kEfSlots + kEfMaxQ + 6) + 16;
+    };
+    EncFrontTc b = a;
+    b.n_quarters = kEfMaxQ;
+    while (b.n_quarters > 4 && smem_of(b.n_quarters) > 227 * 1024) --b.n_quarters;
+    const size_t smem = smem_of(b.n_quarters);
     if ((uint64_t)a.n_img * (a.gh + 2) * Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     cudaFuncSetAttribute(enc_front_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2133,7 +2154,7 @@ int enc_front_tc_launch(const EncFrontTc &a, cudaStream_t s) {
     if (grid < 1) return PILC_OK;
     const double flops = 2.0 * a.n_img * (4.0 * a.gh * a.gw * 32 * 27 + (double)a.gh * a.gw * 32 * 32 * 9);
     ProfScope _ps(PROF_ENC_FRONT, s, flops);
-    enc_front_tc_kernel<<<(unsigned)grid, kEfThreads, smem, s>>>(a);
+    enc_front_tc_kernel<<<(unsigned)grid, kEfThreads, smem, s>>>(b);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

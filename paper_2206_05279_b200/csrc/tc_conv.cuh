@@ -113,6 +113,7 @@ struct EncFrontTc {
     int64_t gstride, margin;
     uint32_t *out_max;
     int32_t *kx_out;
+    int n_quarters;                // set by the launcher
 };
 int enc_front_tc_launch(const EncFrontTc &a, cudaStream_t s);
 
