@@ -1635,7 +1635,6 @@ __global__ void __launch_bounds__(kEfThreads, 1) enc_front_tc_kernel(EncFrontTc 
                 const int ti = tap / 3, tj = tap % 3;
                 const uint32_t rows = (uint32_t)((ti == 0 ? 0 : Wp) + (tj == 0 ? 0 : 1));  // (di + 1) Wp + (dj + 1)
                 const uint32_t ph = (uint32_t)((ti == 1 ? 0 : 2) + (tj == 1 ? 0 : 1));     // pi * 2 + pj
-#pragma unroll
                 const uint32_t qs = (uint32_t)((4 * i + (int)ph) % nq);
                 const uint64_t dq = dA0 + (uint64_t)(qs * (q_bytes >> 4));
 #pragma unroll
