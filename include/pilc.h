@@ -99,6 +99,9 @@ const char *pilc_version(void);
  * (default 1) instead of two conv launches; key 1: decoder trunk (gather +
  * block convs) as one kernel with activations in shared memory (default 1)
  * instead of per-layer launches. Both bit-identical to the unfused path.
+ * key 2: decoder head over pixel pairs (default 1; 24 instead of 36 MMAs per
+ * 256 pixels; a different fp32 summation order than the per-pixel head, so
+ * compress and decompress must use the same setting).
  * Returns the previous value, or -PILC_E_ARG for an unknown key. */
 int pilc_set_tuning(int32_t key, int32_t value);
 /* Device sanity: returns 100 for sm_100 etc., or -1 if no usable device. */

@@ -204,12 +204,34 @@ __device__ __forceinline__ void store_px(uint16_t *slab, int64_t q, uint4 v, int
     if (dy2 && dx2) p[q + Wp + 1] = v;
 }
 
+// store_px into the pixel-pair layout: pixel q, channel group z lives in
+// group z + 4 (q & 1) at row q / 2 (padded widths are even)
+__device__ __forceinline__ void store_px_pair(uint16_t *out, int64_t gs, int64_t mg, int z, int64_t q, uint4 v, int y,
+                                              int x, int H, int W, int Wp) {
+    auto put = [&](int64_t qq) { reinterpret_cast<uint4 *>(out + ((int64_t)(z + 4 * (int)(qq & 1)) * gs + mg) * 8)[qq >> 1] = v; };
+    put(q);
+    const int dy = (y == 1 ? -1 : 0), dy2 = (y == H ? 1 : 0);
+    const int dx = (x == 1 ? -1 : 0), dx2 = (x == W ? 1 : 0);
+    if (dy) put(q - Wp);
+    if (dy2) put(q + Wp);
+    if (dx) put(q - 1);
+    if (dx2) put(q + 1);
+    if (dy && dx) put(q - Wp - 1);
+    if (dy && dx2) put(q - Wp + 1);
+    if (dy2 && dx) put(q + Wp - 1);
+    if (dy2 && dx2) put(q + Wp + 1);
+}
+
 template <int N, int KS, int MODE>
 __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     const int kS = L.n_stages;  // copy ring depth (launcher: as many as fit, <= kStages)
-    constexpr int C = 32;               // input channels (4 groups of 8)
+    // HEAD2: the head over pixel pairs (pair layout: row = two horizontally
+    // adjacent pixels, 8 channel groups: even pixel 0..3, odd pixel 4..7)
+    constexpr bool PAIR = MODE == TC_OUT_HEAD2;
+    constexpr bool HEADM = MODE == TC_OUT_HEAD || PAIR;
+    constexpr int C = PAIR ? 64 : 32;   // input channels per row
     constexpr int NG = C / 8;
-    constexpr int KG = KS * KS * NG;    // K core-matrix groups
+    constexpr int KG = PAIR ? 48 : KS * KS * NG;  // K core-matrix groups (HEAD2: 3 row taps x 128)
     constexpr int TMEM_COLS = (2 * N < 32) ? 32 : 2 * N;
     const int Wp = L.Wp;
     const int npix = KS == 3 ? ((128 + 2 * Wp + 2 + 7) & ~7) : 128;
@@ -229,8 +251,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
     float *s_thr = s_bias + N;                            // head: n_thresh floats
 
     const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-    for (int c = threadIdx.x; c < N; c += blockDim.x) s_bias[c] = c < (MODE == TC_OUT_HEAD ? 6 : N) ? L.bias[c] : 0.f;
-    if constexpr (MODE == TC_OUT_HEAD) {
+    for (int c = threadIdx.x; c < N; c += blockDim.x) s_bias[c] = c < (HEADM ? 6 : N) ? L.bias[c] : 0.f;
+    if constexpr (HEADM) {
         for (int k = threadIdx.x; k < L.n_thresh; k += blockDim.x) s_thr[k] = __double2float_rd(L.thresh[k]);
     }
     if (threadIdx.x == 0) {
@@ -294,13 +316,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
             tc_fence_after();
             const uint64_t dA = dA0 + (uint64_t)((uint32_t)s * (stage_bytes >> 4));
             const uint32_t d = tmem + (uint32_t)(a * N);
+            if constexpr (PAIR) {
+                // per row tap di, 8 K steps of 16 channels: the left pair's odd
+                // pixel (groups 4-7, one row back), this pair (0-7), the right
+                // pair's even pixel (0-3, one row on)
 #pragma unroll
-            for (int tap = 0; tap < KS * KS; ++tap) {
-                const uint32_t off = KS == 3 ? (uint32_t)((tap / KS) * Wp + tap % KS) : 0u;
+                for (int di = 0; di < 3; ++di) {
 #pragma unroll
-                for (int ks = 0; ks < NG / 2; ++ks)
-                    mma_bf16_elect(d, dA + (uint64_t)(2u * ks * npx + off), dB0 + (uint64_t)((tap * NG + 2 * ks) * N),
-                                   idesc, (tap | ks) ? 1u : 0u);
+                    for (int sg = 0; sg < 8; ++sg) {
+                        const uint32_t slab = (sg < 2) ? 4u + 2u * sg : (sg < 6 ? 2u * (sg - 2) : 2u * (sg - 6));
+                        const uint32_t dj = sg < 2 ? 0u : (sg < 6 ? 1u : 2u);
+                        const uint32_t off = (uint32_t)di * (uint32_t)Wp + dj;
+                        mma_bf16_elect(d, dA + (uint64_t)(slab * npx + off), dB0 + (uint64_t)((2 * (di * 8 + sg)) * N),
+                                       idesc, (di | sg) ? 1u : 0u);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int tap = 0; tap < KS * KS; ++tap) {
+                    const uint32_t off = KS == 3 ? (uint32_t)((tap / KS) * Wp + tap % KS) : 0u;
+#pragma unroll
+                    for (int ks = 0; ks < NG / 2; ++ks)
+                        mma_bf16_elect(d, dA + (uint64_t)(2u * ks * npx + off), dB0 + (uint64_t)((tap * NG + 2 * ks) * N),
+                                       idesc, (tap | ks) ? 1u : 0u);
+                }
             }
             mma_commit_elect(&empty[s]);
             mma_commit_elect(&tfull[a]);
@@ -315,7 +354,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
         const int H = L.H, W = L.W;
         const FastDiv div_hw{(uint32_t)(L.Hp * Wp), (uint32_t)(0x100000000ull / (uint32_t)(L.Hp * Wp))};
         const FastDiv div_w{(uint32_t)Wp, (uint32_t)(0x100000000ull / (uint32_t)Wp)};
-        constexpr int NB = MODE == TC_OUT_HEAD ? 6 : N;
+        constexpr int NB = HEADM ? 6 : N;
         float bias[MODE == TC_OUT_ACT ? NB : 1];
         if constexpr (MODE == TC_OUT_ACT) {
 #pragma unroll
@@ -328,7 +367,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
             const uint32_t q = (uint32_t)t * 128u + (uint32_t)row;
             const uint32_t n = fdiv(q, div_hw);
             const uint32_t rem = q - n * div_hw.d;
-            const int y = (int)fdiv(rem, div_w), x = (int)(rem - (uint32_t)y * div_w.d);
+            const int y = (int)fdiv(rem, div_w);
+            // HEAD2 rows are pixel pairs: x is the even pixel of the pair
+            const int x = PAIR ? 2 * (int)(rem - (uint32_t)y * div_w.d) : (int)(rem - (uint32_t)y * div_w.d);
             const bool valid = n < (uint64_t)L.n_img && y >= 1 && y <= H && x >= 1 && x <= W;
             // residual prefetch: independent of the accumulator, issue before the wait
             uint4 rv[4];
@@ -400,7 +441,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                         const int64_t q2 = (int64_t)n * hw2 + (int64_t)Y * Wp2 + X;
                         const uint4 w4 = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
                                                     pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
-                        store_px(L.out + ((int64_t)z * L.out_gstride + L.out_margin) * 8, q2, w4, Y, X, H2, W2, Wp2);
+                        if (L.pair_out)
+                            store_px_pair(L.out, L.out_gstride, L.out_margin, z, q2, w4, Y, X, H2, W2, Wp2);
+                        else
+                            store_px(L.out + ((int64_t)z * L.out_gstride + L.out_margin) * 8, q2, w4, Y, X, H2, W2, Wp2);
                     }
                 }
             } else {
@@ -410,14 +454,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[a]);
-                if (valid && (y - 1) < L.crop_h && (x - 1) < L.crop_w) {
-                    const int64_t px = ((int64_t)n * L.crop_h + (y - 1)) * (int64_t)L.crop_w + (x - 1);
+                auto head_px = [&](const float *vv, int xx) {
+                    if (!(n < (uint64_t)L.n_img && y >= 1 && y <= H && xx >= 1 && xx <= W)) return;
+                    if (!((y - 1) < L.crop_h && (xx - 1) < L.crop_w)) return;
+                    const int64_t px = ((int64_t)n * L.crop_h + (y - 1)) * (int64_t)L.crop_w + (xx - 1);
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
-                        float av = __fadd_rn(v[c], s_bias[c]);
+                        float av = __fadd_rn(vv[c], s_bias[c]);
                         av = fminf(fmaxf(av, -15.f), 15.f);
                         const float mu = __fmul_rn(255.f, sigmoid_f32(av));
-                        float bv = __fadd_rn(v[3 + c], s_bias[3 + c]);
+                        float bv = __fadd_rn(vv[3 + c], s_bias[3 + c]);
                         bv = fminf(fmaxf(bv, L.log_s_min), L.log_s_max);
                         float sv = fminf(fmaxf(expf(bv), 0.5f), 64.f);
                         // round_half_away(mu), mu >= 0, exact in f32: frac is exact
@@ -431,7 +477,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                         if (L.mu) L.mu[px * 3 + c] = mu;
                         if (L.s) L.s[px * 3 + c] = sv;
                     }
-                }
+                };
+                head_px(v, x);
+                if constexpr (PAIR) head_px(v + 6, x + 1);  // columns 6..11: the odd pixel
             }
         }
     }
@@ -2053,16 +2101,18 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
 
 template <int N, int KS, int MODE>
 int launch_tc(const TcLayer &L, cudaStream_t s) {
-    constexpr int NG = 4;
-    constexpr int KG = KS * KS * NG;
+    constexpr int NG = MODE == TC_OUT_HEAD2 ? 8 : 4;
+    constexpr int KG = MODE == TC_OUT_HEAD2 ? 48 : KS * KS * NG;
     const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
     // ring depth: kStages, or as many stages as fit for wide images (>= 2)
     auto smem_of = [&](int k) {
         return (size_t)KG * N * 16 + (size_t)k * NG * npix * 16 + 8 * (2 * k + 6) + 4 * N +
-               4 * (MODE == TC_OUT_HEAD ? 256 : 0) + 16;
+               4 * ((MODE == TC_OUT_HEAD || MODE == TC_OUT_HEAD2) ? 256 : 0) + 16;
     };
     int st = kStages;
-    while (st > 2 && smem_of(st) > 227 * 1024) --st;
+    // the heads run two CTAs per SM: half the shared memory each
+    const size_t cap = (MODE == TC_OUT_HEAD || MODE == TC_OUT_HEAD2) ? 113 * 1024 : 227 * 1024;
+    while (st > 2 && smem_of(st) > cap) --st;
     const size_t smem = smem_of(st);
     TcLayer Ls = L;
     Ls.n_stages = st;
@@ -2072,10 +2122,11 @@ int launch_tc(const TcLayer &L, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // one persistent CTA per SM (two epilogue groups, an 8-deep copy ring);
     // the head's math-heavy epilogue (few registers) runs two CTAs per SM
-    int64_t grid = (int64_t)sm_count() * (MODE == TC_OUT_HEAD ? 2 : 1);
+    int64_t grid = (int64_t)sm_count() * ((MODE == TC_OUT_HEAD || MODE == TC_OUT_HEAD2) ? 2 : 1);
     if (grid > L.n_tiles) grid = L.n_tiles;
     if (grid < 1) return PILC_OK;
-    const double flops = 2.0 * L.n_img * L.H * L.W * (double)(MODE == TC_OUT_HEAD ? 6 : N) * 32 * KS * KS;
+    const double flops = 2.0 * L.n_img * L.H * L.W * (double)((MODE == TC_OUT_HEAD || MODE == TC_OUT_HEAD2) ? 6 : N) *
+                         32 * KS * KS;
     ProfScope _ps(PROF_TC_CONV, s, flops);
     kern<<<(unsigned)grid, kThreadsTC, smem, s>>>(Ls);
     PILC_CHECK_LAUNCH();
@@ -2207,6 +2258,7 @@ int dec_trunk_launch(const DecTrunk &p0, cudaStream_t s) {
 }
 int tc_launch_shuffle(const TcLayer &L, cudaStream_t s) { return launch_tc<128, 3, TC_OUT_SHUFFLE>(L, s); }
 int tc_launch_head(const TcLayer &L, cudaStream_t s) { return launch_tc<16, 3, TC_OUT_HEAD>(L, s); }
+int tc_launch_head2(const TcLayer &L, cudaStream_t s) { return launch_tc<16, 3, TC_OUT_HEAD2>(L, s); }
 
 int tc_dec_table(const float *cb, const float *w, const float *b, int K, int Dc, int ci_pad, int co_pad,
                  uint16_t *table, cudaStream_t s) {

@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-enum TcOutMode { TC_OUT_ACT = 0, TC_OUT_SHUFFLE = 1, TC_OUT_HEAD = 2 };
+enum TcOutMode { TC_OUT_ACT = 0, TC_OUT_SHUFFLE = 1, TC_OUT_HEAD = 2, TC_OUT_HEAD2 = 3 };
 
 struct TcLayer {
     const uint16_t *in;  // padded group-major bf16 activations (32 channels)
@@ -24,6 +24,7 @@ struct TcLayer {
     const double *thresh;
     int n_thresh;
     float log_s_min, log_s_max;
+    int pair_out;        // TC_OUT_SHUFFLE: write the output in the pixel-pair layout (HEAD2's input)
     int n_stages;        // set by the launcher
 };
 
@@ -132,6 +133,7 @@ int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s);
 int tc_launch_act(const TcLayer &L, cudaStream_t s);
 int tc_launch_shuffle(const TcLayer &L, cudaStream_t s);
 int tc_launch_head(const TcLayer &L, cudaStream_t s);
+int tc_launch_head2(const TcLayer &L, cudaStream_t s);  // head over pixel pairs (pair layout input)
 int tc_dec_table(const float *cb, const float *w, const float *b, int K, int Dc, int ci_pad, int co_pad,
                  uint16_t *table, cudaStream_t s);
 int tc_gather(const uint8_t *idx, const uint16_t *table, int64_t n_img, int gh, int gw, uint16_t *x,

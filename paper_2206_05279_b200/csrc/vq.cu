@@ -48,6 +48,7 @@ struct Layout {
     bool tc;
     std::vector<int64_t> tc_blk;  // 2B block convs, N = 32
     int64_t tc_up, tc_head;       // N = 128, N = 16 (mu 0..2, s 3..5)
+    int64_t tc_head2;             // the head over pixel pairs: K = 3 x 128, N = 16 (even px 0..5, odd 6..11)
     // tcgen05 encoder (C == 32, Dc == 32): fp16-split B operands
     // [KG][64][8] (rows 0..31 hi, 32..63 lo of w 2^kw), float offsets;
     // tf_meta: per block conv / proj {kw (int), L1, max|b|, 0}, then
@@ -105,6 +106,8 @@ Layout make_layout(int K, int Dc, int C, int B) {
         h += 36 * 128 * 8;
         L.tc_head = h;
         h += 36 * 16 * 8;
+        L.tc_head2 = h;
+        h += 48 * 16 * 8;
         cur = (h + 1) / 2;
     }
     L.tf = (C == 32 && Dc == 32);
@@ -671,6 +674,24 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
         for (int i = 0; i < 2 * B; ++i) put_b(L.tc_blk[i], L.dec[1 + i], 32, 0, 32);
         put_b(L.tc_up, L.dec[1 + 2 * B], 128, 0, 128);
         put_b(L.tc_head, L.dec[2 + 2 * B], 16, 0, 6);
+        {  // pair head: K = row tap di (3) x [left odd px | even px | odd px | right even px] x 32 ch
+            const ConvSpec &sp = L.dec[2 + 2 * B];
+            for (int kk = 0; kk < 384; ++kk) {
+                const int st = kk / 16, di = st / 8, sg = st % 8, ci = (sg & 1) * 16 + kk % 16, part = sg >> 1;
+                for (int n = 0; n < 16; ++n) {
+                    int dj = -1, co = 0;
+                    if (n < 6) {  // even output pixel x: parts = pixels x-1, x, x+1, (x+2)
+                        co = n;
+                        dj = part < 3 ? part : -1;
+                    } else if (n < 12) {  // odd output pixel x+1: parts = (x-1), x, x+1, x+2
+                        co = n - 6;
+                        dj = part > 0 ? part - 1 : -1;
+                    }
+                    const float w = dj < 0 ? 0.f : dst[sp.w_off + ((int64_t)(di * 3 + dj) * sp.ci_pad + ci) * sp.co_pad + co];
+                    h[L.tc_head2 + ((int64_t)(kk >> 3) * 16 + n) * 8 + (kk & 7)] = bf16(w);
+                }
+            }
+        }
     }
     if (L.tf) {
         // tf32 hi = round-to-nearest (ties away) to 10 mantissa bits, lo = w - hi
@@ -1098,6 +1119,7 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
               float *s_out, cudaStream_t s) {
     const int gh = (H + 1) / 2, gw = (W + 1) / 2;
     const uint16_t *hb = reinterpret_cast<const uint16_t *>(model);
+    const bool pairs = g_tuning[PILC_TUNE_HEAD_PAIRS] != 0;
     int rc = tc_dec_table(model + L.cb_off, model + L.dec[0].w_off, model + L.dec[0].b_off, K, Dc, L.dec[0].ci_pad,
                           L.dec[0].co_pad, tw.table, s);
     bool trunk_done = false;
@@ -1156,8 +1178,23 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
         TcLayer up = b;
         up.in = X;
         up.out = tw.U;
-        up.out_gstride = tw.gs2;
-        up.out_margin = tw.margin2;
+        // the pair head reads U as rows of two pixels (8 channel groups,
+        // half as many rows): the same bytes, addressed differently
+        up.pair_out = pairs ? 1 : 0;
+        up.out_gstride = pairs ? tw.gs2 / 2 : tw.gs2;
+        up.out_margin = pairs ? tw.margin2 / 2 : tw.margin2;
+        if (pairs) {
+            // the pair head's zero-weight K segments read one pair beyond each
+            // image row, which for the first and last row of the batch lies in
+            // the slab margins: they must hold finite values (0 x NaN = NaN)
+            const int64_t gsr = tw.gs2 / 2, mr = tw.margin2 / 2;
+            for (int g = 0; g < 8; ++g) {
+                uint16_t *slab = tw.U + (int64_t)g * gsr * 8;
+                if (cudaMemsetAsync(slab, 0, (size_t)mr * 16, s) != cudaSuccess ||
+                    cudaMemsetAsync(slab + (gsr - mr) * 8, 0, (size_t)mr * 16, s) != cudaSuccess)
+                    return PILC_E_CUDA;
+            }
+        }
         up.wts = hb + L.tc_up;
         up.bias = model + L.dec[1 + 2 * B].b_off;
         rc = tc_launch_shuffle(up, s);
@@ -1166,15 +1203,15 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
         TcLayer hd;
         memset(&hd, 0, sizeof(hd));
         hd.in = tw.U;
-        hd.gstride = tw.gs2;
-        hd.margin = tw.margin2;
+        hd.gstride = pairs ? tw.gs2 / 2 : tw.gs2;
+        hd.margin = pairs ? tw.margin2 / 2 : tw.margin2;
         hd.Hp = 2 * gh + 2;
-        hd.Wp = 2 * gw + 2;
+        hd.Wp = pairs ? gw + 1 : 2 * gw + 2;  // pairs: row width in pixel pairs
         hd.H = 2 * gh;
         hd.W = 2 * gw;
         hd.n_img = n_img;
         hd.n_tiles = ceil_div64(n_img * hd.Hp * (int64_t)hd.Wp, 128);
-        hd.wts = hb + L.tc_head;
+        hd.wts = hb + (pairs ? L.tc_head2 : L.tc_head);
         hd.bias = model + L.dec[2 + 2 * B].b_off;
         hd.shift = shift_out;
         hd.dsel = d_out;
@@ -1186,7 +1223,7 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
         hd.n_thresh = D - 1;
         hd.log_s_min = (float)log(0.5);
         hd.log_s_max = (float)log(64.0);
-        rc = tc_launch_head(hd, s);
+        rc = pairs ? tc_launch_head2(hd, s) : tc_launch_head(hd, s);
     }
     return rc;
 }

@@ -552,3 +552,34 @@ def test_vqvae_wide_images_round_trip(full_model, shape):
     assert np.array_equal(pc.decompress_batch(buf, off, full_model)[0], img)
     om = O.Model.from_bytes(full_model.to_bytes())
     assert np.array_equal(vqvae.encode_to_indices(img, full_model), O.encode_indices(img, om))
+
+
+@pytest.mark.parametrize("shape", [(32, 32), (17, 33), (64, 64), (2, 3)])
+def test_pair_head_matches_per_pixel_head(full_model, shape):
+    """The decoder head over pixel pairs (production) and the per-pixel head
+    compute the same logistic parameters up to fp32 summation order: mu / s
+    within a few ulps (checked with a bf16-level tolerance), and a blob made
+    with either decodes losslessly with the same setting."""
+    from paper_2206_05279_b200 import _lib
+    from paper_2206_05279_b200.device import require_device
+
+    dev = require_device()
+    stream = torch.cuda.current_stream(dev)
+    H, W = shape
+    gh, gw = vqvae.latent_shape(H, W)
+    idx = torch.from_numpy(np.random.default_rng(9).integers(0, 256, (5, gh, gw), dtype=np.uint8)).to(dev)
+    out = []
+    for on in (1, 0):
+        prev = _lib.set_tuning(_lib.TUNE_HEAD_PAIRS, on)
+        try:
+            r = vqvae.decode_head_device(idx, full_model, H, W, default_grid(), dev, stream, want_params=True)
+            out.append([t.cpu().numpy() for t in r])
+            img = smooth_images(3, H, W, seed=4)
+            cfg = pc.CodecConfig(backend="twar-vqvae")
+            buf, off = pc.compress_batch(img, full_model, cfg)
+            assert np.array_equal(pc.decompress_batch(buf, off, full_model), img)
+        finally:
+            _lib.set_tuning(_lib.TUNE_HEAD_PAIRS, prev)
+    (_, _, mu1, s1), (_, _, mu0, s0) = out
+    assert np.allclose(mu1, mu0, rtol=1e-5, atol=1e-3)
+    assert np.allclose(s1, s0, rtol=1e-5, atol=1e-5)
