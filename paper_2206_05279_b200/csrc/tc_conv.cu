@@ -430,13 +430,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) tc_conv_kernel(TcLayer L) {
                         if (lane == 0) mbar_arrive(&tempty[a]);
                     }
                     if (!valid) continue;
+                    float bz[32];  // this chunk's 32 biases: 8 vector loads instead of 32 scalar ones
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float4 b4 = reinterpret_cast<const float4 *>(s_bias + 32 * z)[e];
+                        bz[4 * e] = b4.x;
+                        bz[4 * e + 1] = b4.y;
+                        bz[4 * e + 2] = b4.z;
+                        bz[4 * e + 3] = b4.w;
+                    }
 #pragma unroll
                     for (int sub = 0; sub < 4; ++sub) {
                         const int dy = sub >> 1, dx = sub & 1;
                         float o[8];
 #pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            o[e] = fmaxf(__fadd_rn(v[4 * e + sub], s_bias[32 * z + 4 * e + sub]), 0.f);
+                        for (int e = 0; e < 8; ++e) o[e] = fmaxf(__fadd_rn(v[4 * e + sub], bz[4 * e + sub]), 0.f);
                         const int Y = 2 * (y - 1) + dy + 1, X = 2 * (x - 1) + dx + 1;
                         const int64_t q2 = (int64_t)n * hw2 + (int64_t)Y * Wp2 + X;
                         const uint4 w4 = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
