@@ -121,12 +121,24 @@ def _build_cached(P_rows: tuple, M: int):
     return _build(P_rows, M)
 
 
+_BY_BYTES: dict = {}
+
+
 def build_tables(dists: Sequence[QuantizedPmf], M: int, verify: bool = False):
     """(EncodeTables, DecodeTables) for a distribution set; cached by content."""
     if M > 12:
         raise TableError(f"M={M}: delta is only guaranteed to fit unsigned 16 bits for M <= 12")
     if not dists:
         raise TableError("need at least one distribution")
+    # cache hit: the masses' bytes (and M) name the tables; a hit was
+    # validated when it was built (hashing bytes keeps per-call host time
+    # in the microseconds, this runs on every compress / decompress)
+    key = (M, tuple((p.M, p.P.dtype.str, p.P.tobytes()) for p in dists))
+    hit = _BY_BYTES.get(key)
+    if hit is not None:
+        if verify:
+            verify_encode_tables(hit[0], dists)
+        return hit
     X = dists[0].X
     if X > 256:
         raise TableError("symbol table is uint8; alphabet must be <= 256")
@@ -140,6 +152,8 @@ def build_tables(dists: Sequence[QuantizedPmf], M: int, verify: bool = False):
             raise CoderContractError(f"distribution {d} has masses outside [1, {cap}]")
     rows = tuple(tuple(int(v) for v in p.P) for p in dists)
     enc, dec = _build_cached(rows, M)
+    if len(_BY_BYTES) < 256:
+        _BY_BYTES[key] = (enc, dec)
     if verify:
         verify_encode_tables(enc, dists)
     return enc, dec

@@ -61,14 +61,20 @@ def encode_indices_device(img_d: torch.Tensor, weights: ModelWeights, dev, strea
 
 
 def decode_head_device(idx_d: torch.Tensor, weights: ModelWeights, H: int, W: int, grid: ScaleGrid, dev, stream,
-                       want_params: bool = False, precise: bool = False):
+                       want_params: bool = False, precise: bool = False, out=None):
     """-> (shift u8, d u8[, mu f32, s f32]) each (N, H, W, 3).
 
     The codec path uses the production decoder (tcgen05 bf16 for the
-    default C=32 model); precise=True selects the fp32 SIMT kernels."""
+    default C=32 model); precise=True selects the fp32 SIMT kernels.
+    out=(shift, dsel): contiguous (N, H, W, 3) uint8 tensors to fill (e.g.
+    row slices of a batch-sized pair)."""
     N = idx_d.shape[0]
-    shift = torch.empty((N, H, W, 3), dtype=torch.uint8, device=dev)
-    dsel = torch.empty((N, H, W, 3), dtype=torch.uint8, device=dev)
+    if out is not None:
+        shift, dsel = out
+        assert shift.is_contiguous() and dsel.is_contiguous() and shift.shape == dsel.shape == (N, H, W, 3)
+    else:
+        shift = torch.empty((N, H, W, 3), dtype=torch.uint8, device=dev)
+        dsel = torch.empty((N, H, W, 3), dtype=torch.uint8, device=dev)
     mu = s = None
     if want_params:
         mu = torch.empty((N, H, W, 3), dtype=torch.float32, device=dev)
@@ -137,5 +143,11 @@ def decode_to_params(indices, weights: ModelWeights, out_shape: tuple[int, int],
 
 
 def index_histogram_pmf(weights: ModelWeights, M: int) -> QuantizedPmf:
-    """Index-stream distribution: stored usage counts + 1 (vqvae.py:116-119)."""
-    return quantize_pmf(weights.histogram.astype(np.float64) + 1.0, M)
+    """Index-stream distribution: stored usage counts + 1 (vqvae.py:116-119).
+    Memoised per (histogram bytes, M) on the weights object."""
+    memo = weights.__dict__.setdefault("_index_pmf_memo", {})
+    key = (weights.histogram.tobytes(), M)
+    pmf = memo.get(key)
+    if pmf is None:
+        pmf = memo[key] = quantize_pmf(weights.histogram.astype(np.float64) + 1.0, M)
+    return pmf

@@ -51,6 +51,22 @@ def test_golden_delta_phi():
     assert int(enc.delta[0, 0]) == 4096 and int(enc.phi[0, 0]) == 3072
 
 
+def test_table_cache_by_content():
+    """build_tables is memoised by the masses' bytes: equal content -> the
+    same tables (per-call host time), rejections are never cached."""
+    pmfs = logistic.residual_distributions(logistic.default_grid(), 12)
+    a = tables.build_tables(pmfs, 12)
+    copies = [pc.QuantizedPmf(12, p.P.copy()) for p in pmfs]
+    b = tables.build_tables(copies, 12, verify=True)
+    assert a[0] is b[0] and a[1] is b[1]
+    bad = pc.QuantizedPmf(12, np.array([2047, 2049]))  # inadmissible: P > 2^(M-1) - 1
+    for _ in range(2):
+        with pytest.raises(pc.CodecError):
+            tables.build_tables([bad], 12)
+    with pytest.raises(pc.CodecError):
+        tables.build_tables(pmfs, 11)  # quantized at M=12
+
+
 def test_quantizer_known_answers():
     assert np.all(pc.quantize_pmf(np.ones(256), 12).P == 16)
     q = pc.quantize_pmf(np.array([3.0, 1.0]), 12)  # test_pmf.py:58-62
