@@ -181,8 +181,11 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
 // unread bits just below position A, left-aligned, so a field of b <= 12
 // bits is `hi >> (32 - b)`: the state chain pays one 32-bit shift. A pop
 // that leaves fewer than 32 bits ORs in the next lower word (index wn),
-// read from a per-thread ring of kRing 16-byte chunk slots in shared memory
-// (one predicated 32-bit load). cp.async keeps the ring kAhead chunks ahead;
+// read from a per-thread ring of kRing 16-byte chunks (4 kRing words) in
+// shared memory, one predicated 32-bit load. Ring word q of thread t sits at
+// (q * blockDim + t) * 4, so the address is one multiply-add of wn and a
+// warp's loads never share a bank; chunks land as four 4-byte cp.async.
+// cp.async keeps the ring kAhead chunks ahead;
 // issuing and waiting happen once per 16-symbol block (sync()): a block pops
 // at most 192 bits = 6 words, so it touches at most two chunks, both issued
 // at least kAhead - 2 groups earlier. Lanes of a warp refill at different
@@ -192,8 +195,9 @@ constexpr int kAhead = 4;
 
 struct BitReader {
     const uint4 *base4;  // chunk 0 = the lane's first chunk
-    uint32_t ring_s;     // shared address of this thread's slot 0 (stride = blockDim.x * 16)
-    uint32_t ring_stride;
+    uint32_t ring_s;     // shared address of this thread's ring word 0
+    uint32_t ring_stride;  // bytes between ring words q and q + 1 (blockDim.x * 4): word-interleaved
+                           // across the block's threads, so same-q reads of a warp hit 32 banks
     int hi_c;            // last chunk holding payload bits
     int A, cnt, start, wn, ci;  // ci: lowest chunk issued to the ring
     uint32_t hi, lo;     // window: bits [A - cnt, A), left-aligned (bit A-1 at bit 63 of hi:lo)
@@ -207,8 +211,13 @@ struct BitReader {
     __device__ __forceinline__ uint32_t word(int wi) const { return wi >= 0 ? pick(direct(wi >> 2), wi & 3) : 0u; }
     __device__ __forceinline__ void issue(int c) {
         if (c >= 0 && c <= hi_c) {
-            const uint32_t dst = ring_s + (uint32_t)(c & (kRing - 1)) * ring_stride;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(base4 + c) : "memory");
+            // chunk c = ring words 4c .. 4c + 3 (mod 4 kRing)
+            const uint32_t dst = ring_s + (uint32_t)((4 * c) & (4 * kRing - 1)) * ring_stride;
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(base4 + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + j * ring_stride), "l"(src + j)
+                             : "memory");
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
@@ -239,16 +248,20 @@ struct BitReader {
             if (ci > target) issue(--ci);
         asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 2) : "memory");
     }
-    // pop b bits (1 <= b <= 12); underflow shows as A < start at the end
-    __device__ __forceinline__ uint32_t take(uint32_t b) {
-        const uint32_t v = hi >> (32u - b);
-        hi = __funnelshift_l(lo, hi, b);
+    // pop b bits (1 <= b <= 12); underflow shows as A < start at the end.
+    // `e8` = table entry >> 8: b in bits 0..7, anything above. The funnel
+    // shifts use the shift amount mod 32 (= b), so the state chain pays
+    // entry >> 8 and one funnel shift here (no mask, no 32 - b).
+    __device__ __forceinline__ uint32_t take(uint32_t e8) {
+        const uint32_t b = e8 & 0xFFu;
+        const uint32_t v = __funnelshift_l(hi, 0u, e8);  // top b bits of the window
+        hi = __funnelshift_l(lo, hi, e8);
         lo <<= b;
         cnt -= (int)b;
         A -= (int)b;
         // refill below the valid bits (lo is zero here) with word wn
         const bool p = cnt < 32;
-        const uint32_t src = ring_s + (uint32_t)((wn >> 2) & (kRing - 1)) * ring_stride + (uint32_t)(wn & 3) * 4u;
+        const uint32_t src = ring_s + (uint32_t)(wn & (4 * kRing - 1)) * ring_stride;
         uint32_t w = 0;
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.u32 %0, [%1];\n\t}\n"
@@ -296,13 +309,24 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
             : "memory");
     }
     const uint32_t my_ring =
-        (uint32_t)__cvta_generic_to_shared(reinterpret_cast<uint4 *>(s_tab + (SMEM ? (D << M) : 0)) + threadIdx.x);
+        (uint32_t)__cvta_generic_to_shared(s_tab + (SMEM ? (D << M) : 0) + threadIdx.x);
     const uint32_t T = 1u << M;
     // table row of distribution d, pre-offset by -T so the index is the state
     const uint32_t *tabT = (SMEM ? s_tab : dec_tab_g) - T;
+    // shared address of row -T: the row base (tabs0 + 4 dT) is formed off
+    // the state chain, the state then adds with one multiply-add (the table
+    // is read-only once the bulk copy above has landed)
+    const uint32_t tabs0 = (uint32_t)__cvta_generic_to_shared(s_tab) - 4u * T;
     auto lookup = [&](uint32_t dT, uint32_t st) -> uint32_t {
-        if constexpr (SMEM) return tabT[dT + st];
-        else return __ldg(tabT + dT + st);
+        if constexpr (SMEM) {
+            const uint32_t rowb = tabs0 + (dT << 2);
+            uint32_t a, e;
+            asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a) : "r"(st), "r"(rowb));
+            asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(a));
+            return e;
+        } else {
+            return __ldg(tabT + dT + st);
+        }
     };
     const int64_t total = n_img * lanes;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
@@ -315,13 +339,13 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
         const uint32_t dconstT = (d_img ? (uint32_t)d_img[img] : 0u) << M;
         const uintptr_t a0 = reinterpret_cast<uintptr_t>(buf) + lane_off[k];
         BitReader br;
-        br.init(reinterpret_cast<const uint4 *>(a0 & ~(uintptr_t)15), my_ring, blockDim.x * 16u, (int)(a0 & 15) * 8,
+        br.init(reinterpret_cast<const uint4 *>(a0 & ~(uintptr_t)15), my_ring, blockDim.x * 4u, (int)(a0 & 15) * 8,
                 nbits_a[k]);
         uint32_t state = states[k];
         // one symbol: the decoded (optionally un-recentred) byte
         auto step = [&](uint32_t dT, uint32_t sh) -> uint32_t {
             const uint32_t e = lookup(dT, state);
-            state = (e >> 16) + br.take((e >> 8) & 0xFFu);
+            state = (e >> 16) + br.take(e >> 8);
             return unshift ? ((e + sh + 128u) & 0xFFu) : (e & 0xFFu);  // (x + shift - 128) mod 256
         };
         int i = 0;
