@@ -83,10 +83,12 @@ __global__ void twar_forward_kernel(const uint8_t *__restrict__ img, uint8_t *__
 
 // Inverse (_kernels.py:146-170 wavefront schedule). One warp per image;
 // the image is staged in shared memory when it fits, else decoded in place
-// in the output buffer. Red: lanes take rows 32s..32s+31 of strip s and
-// march a skewed wavefront (lane u handles column step - u), receiving the
-// up / up-left values from lane u-1 by shuffle. Green, blue: rows are
-// independent; each lane owns rows lane, lane+32, ... and walks columns.
+// in the output buffer. Red: lanes take rows of two 32-row strips at a time
+// and march a skewed wavefront (lane u handles columns step - u and
+// step - u - 32), receiving the up / up-left values from lane u-1 by
+// shuffle. Green, blue: rows are independent; one sweep per row decodes
+// both channels, each lane walking two rows. Every pixel's arithmetic is the
+// reference's; only the order across independent pixels changes.
 constexpr int kDecWarps = 4;
 
 __device__ __forceinline__ uint32_t unrec(const uint8_t *coded, const uint8_t *shift, int64_t i) {
@@ -132,63 +134,98 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
             cd = tb;
             sh = nullptr;
         }
-        // ---- red: skewed wavefront per strip of 32 rows
-        for (int u0 = 0; u0 < H; u0 += 32) {
-            const int u = u0 + lane;
-            const bool row_ok = u < H;
-            float left = 0.f;      // out[u][v-1][0]
-            float up_prev = 0.f;   // value lane-1 produced one step ago (= out[u-1][v])
-            float up_prev2 = 0.f;  // two steps ago (= out[u-1][v-1])
-            float mine_prev = 0.f; // what this lane produced last step
-            float mine_prev2 = 0.f;
-            const int steps = W + 31;
+        // ---- red: skewed wavefront over pairs of 32-row strips. At step s
+        // lane u decodes (u0 + u, s - u) in strip a and (u0 + 32 + u, s - u - 32)
+        // in strip b; up / up-left come from lane u - 1's outputs one / two
+        // steps earlier (strip b's lane 0 takes strip a's lane 31), so the two
+        // strips' chains overlap and a pair costs W + 63 steps, not 2 (W + 31).
+        for (int u0 = 0; u0 < H; u0 += 64) {
+            const bool two = u0 + 32 < H;  // warp-uniform
+            const int ua = u0 + lane, ub = u0 + 32 + lane;
+            const bool ok_a = ua < H, ok_b = two && ub < H;
+            float left_a = 0.f, left_b = 0.f;
+            float ma1 = 0.f, ma2 = 0.f, mb1 = 0.f, mb2 = 0.f;  // this lane's outputs 1 / 2 steps ago
+            const int steps = W + (two ? 63 : 31);
             for (int s = 0; s < steps; ++s) {
-                // neighbours from lane-1: its outputs at steps s-1 and s-2
-                const float nb1 = __shfl_up_sync(0xffffffffu, mine_prev, 1);
-                const float nb2 = __shfl_up_sync(0xffffffffu, mine_prev2, 1);
+                const float na1 = __shfl_up_sync(0xffffffffu, ma1, 1);
+                const float na2 = __shfl_up_sync(0xffffffffu, ma2, 1);
+                float nb1 = 0.f, nb2 = 0.f;
+                if (two) {
+                    const int src = (lane + 31) & 31;
+                    const float x1 = __shfl_sync(0xffffffffu, mb1, src);
+                    const float x2 = __shfl_sync(0xffffffffu, mb2, src);
+                    const float y1 = __shfl_sync(0xffffffffu, ma1, 31);
+                    const float y2 = __shfl_sync(0xffffffffu, ma2, 31);
+                    nb1 = lane == 0 ? y1 : x1;
+                    nb2 = lane == 0 ? y2 : x2;
+                }
                 const int v = s - lane;
-                float val = 0.f;
-                if (row_ok && v >= 0 && v < W) {
+                float va = 0.f, vb = 0.f;
+                if (ok_a && v >= 0 && v < W) {
                     float up, ul;
-                    if (lane == 0) {
-                        up = u > 0 ? (float)o[((int64_t)(u - 1) * W + v) * 3] : 0.f;
-                        ul = (u > 0 && v > 0) ? (float)o[((int64_t)(u - 1) * W + v - 1) * 3] : 0.f;
+                    if (lane == 0) {  // row above the pair: decoded by the previous pair
+                        up = ua > 0 ? (float)o[((int64_t)(ua - 1) * W + v) * 3] : 0.f;
+                        ul = (ua > 0 && v > 0) ? (float)o[((int64_t)(ua - 1) * W + v - 1) * 3] : 0.f;
                     } else {
-                        up = nb1;
-                        ul = v > 0 ? nb2 : 0.f;
+                        up = na1;
+                        ul = v > 0 ? na2 : 0.f;
                     }
-                    const float lf = v > 0 ? left : 0.f;
+                    const float lf = v > 0 ? left_a : 0.f;
                     const uint32_t pr = predict(ul, up, lf, p.w, p.b[0]);
-                    const int64_t i = ((int64_t)u * W + v) * 3;
+                    const int64_t i = ((int64_t)ua * W + v) * 3;
                     const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;  // t - 128 + pred
                     o[i] = (uint8_t)x;
-                    val = (float)x;
-                    left = val;
+                    va = (float)x;
+                    left_a = va;
                 }
-                up_prev2 = up_prev;
-                up_prev = nb1;
-                mine_prev2 = mine_prev;
-                mine_prev = val;
-            }
-            __syncwarp();
-        }
-        // ---- green then blue: rows independent
-        for (int c = 1; c < 3; ++c) {
-            for (int u = lane; u < H; u += 32) {
-                float left = 0.f, pleft = 0.f;
-                const int64_t row = (int64_t)u * W * 3;
-                for (int v = 0; v < W; ++v) {
-                    const int64_t i = row + (int64_t)v * 3 + c;
-                    const float here = o[i - 1];
-                    const uint32_t pr = predict(left, pleft, here, p.w + 3 * c, p.b[c]);
+                const int w2 = v - 32;
+                if (ok_b && w2 >= 0 && w2 < W) {
+                    const float ul = w2 > 0 ? nb2 : 0.f;
+                    const float lf = w2 > 0 ? left_b : 0.f;
+                    const uint32_t pr = predict(ul, nb1, lf, p.w, p.b[0]);
+                    const int64_t i = ((int64_t)ub * W + w2) * 3;
                     const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;
                     o[i] = (uint8_t)x;
-                    left = (float)x;
-                    pleft = here;
+                    vb = (float)x;
+                    left_b = vb;
                 }
+                ma2 = ma1;
+                ma1 = va;
+                mb2 = mb1;
+                mb1 = vb;
             }
             __syncwarp();
         }
+        // ---- green and blue in one column sweep (blue at (u, v) needs green
+        // at (u, v) and (u, v - 1) only); rows are independent, each lane
+        // walks two of them (lane + 64k and lane + 32 + 64k) side by side
+        auto gb = [&](int u, int v, float &rL, float &gL, float &bL) {
+            const int64_t i0 = ((int64_t)u * W + v) * 3;
+            const float r = o[i0];
+            const uint32_t pg = predict(gL, rL, r, p.w + 3, p.b[1]);
+            const uint32_t g = (unrec(cd, sh, i0 + 1) + pg + 128u) & 0xFFu;
+            o[i0 + 1] = (uint8_t)g;
+            const float gf = (float)g;
+            const uint32_t pb = predict(bL, gL, gf, p.w + 6, p.b[2]);
+            const uint32_t bb = (unrec(cd, sh, i0 + 2) + pb + 128u) & 0xFFu;
+            o[i0 + 2] = (uint8_t)bb;
+            rL = r;
+            gL = gf;
+            bL = (float)bb;
+        };
+        for (int u = lane; u < H; u += 64) {
+            const int u2 = u + 32;
+            float rL = 0.f, gL = 0.f, bL = 0.f, rL2 = 0.f, gL2 = 0.f, bL2 = 0.f;
+            if (u2 < H) {
+                for (int v = 0; v < W; ++v) {
+                    gb(u, v, rL, gL, bL);
+                    gb(u2, v, rL2, gL2, bL2);
+                }
+            } else {
+                for (int v = 0; v < W; ++v) gb(u, v, rL, gL, bL);
+            }
+        }
+        __syncwarp();
         if (stage_in_smem) {
             // coalesced copy-out, 16 bytes per lane when aligned
             if (vec) {
