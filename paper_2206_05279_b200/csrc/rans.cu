@@ -173,10 +173,11 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
 // (q * blockDim + t) * 4, so the address is one multiply-add of wn and a
 // warp's loads never share a bank; chunks land as four 4-byte cp.async.
 // cp.async keeps the ring kAhead chunks ahead;
-// issuing and waiting happen once per 16-symbol block (sync()): a block pops
-// at most 192 bits = 6 words, so it touches at most two chunks, both issued
-// at least kAhead - 2 groups earlier. Lanes of a warp refill at different
-// symbols, so the per-symbol path is predicated rather than branched.
+// issuing (predicated, branch-free: at most two chunks, one commit group)
+// and waiting happen once per 16-symbol block (sync()): a block pops at
+// most 192 bits = 6 words, so it touches at most two chunks, both issued at
+// least one block earlier. Lanes of a warp refill at different symbols, so
+// the per-symbol path is predicated rather than branched.
 constexpr int kRing = 8;
 constexpr int kAhead = 4;
 
@@ -196,17 +197,18 @@ struct BitReader {
         return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
     }
     __device__ __forceinline__ uint32_t word(int wi) const { return wi >= 0 ? pick(direct(wi >> 2), wi & 3) : 0u; }
-    __device__ __forceinline__ void issue(int c) {
-        if (c >= 0 && c <= hi_c) {
-            // chunk c = ring words 4c .. 4c + 3 (mod 4 kRing)
-            const uint32_t dst = ring_s + (uint32_t)((4 * c) & (4 * kRing - 1)) * ring_stride;
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(base4 + c);
+    // chunk c = ring words 4c .. 4c + 3 (mod 4 kRing), four predicated
+    // 4-byte cp.async (no branch: lanes of a warp refill at different blocks)
+    __device__ __forceinline__ void issue(int c, bool on) {
+        const uint32_t dst = ring_s + (uint32_t)((4 * c) & (4 * kRing - 1)) * ring_stride;
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(base4 + c);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + j * ring_stride), "l"(src + j)
-                             : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        for (int j = 0; j < 4; ++j)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 4;\n\t}\n" ::"r"(
+                    dst + j * ring_stride),
+                "l"(src + j), "r"(on ? 1u : 0u)
+                : "memory");
     }
     __device__ __forceinline__ void init(const uint4 *lane_base4, uint32_t my_ring_s, uint32_t stride_bytes,
                                          int start_bit, uint32_t nb) {
@@ -224,16 +226,31 @@ struct BitReader {
         cnt = nt + 32;
         wn = wt - 2;  // next word to bring in
         ci = (wn >> 2) + 1;
-        sync();
+        // prime the ring kAhead chunks deep and wait for it (once per lane)
+        const int target = (wn >> 2) - kAhead;
+        for (int j = 0; j < kAhead + 1; ++j) {
+            const int c = ci - 1;
+            const bool on = c >= target;
+            issue(c, on && c >= 0 && c <= hi_c);
+            ci = on ? c : ci;
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     }
     // once per 16-symbol block: keep the ring kAhead chunks below the
-    // current one, then wait for the chunks this block can touch
+    // current one (a block pops <= 192 bits, so the target moves <= 2 chunks)
+    // as one commit group, then wait for every group but this one: the
+    // chunks this block reads (the current one and the one below) were
+    // issued at least one block earlier
     __device__ __forceinline__ void sync() {
         const int target = (wn >> 2) - kAhead;
 #pragma unroll
-        for (int j = 0; j < kAhead + 1; ++j)
-            if (ci > target) issue(--ci);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 2) : "memory");
+        for (int j = 0; j < 2; ++j) {
+            const int c = ci - 1;
+            const bool on = c >= target;
+            issue(c, on && c >= 0 && c <= hi_c);
+            ci = on ? c : ci;
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 1;" ::: "memory");
     }
     // pop b bits (1 <= b <= 12); underflow shows as A < start at the end.
     // `e8` = table entry >> 8: b in bits 0..7, anything above. The funnel
