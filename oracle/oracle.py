@@ -61,6 +61,11 @@ def lib():
         L.oracle_twar_decode.argtypes = [P, P, I64, ctypes.c_int, ctypes.c_int, P, P, P]
         L.oracle_encode_batch.restype = None
         L.oracle_encode_batch.argtypes = [P, P, I64, I64, I64, P, P, I64, ctypes.c_int, P, I64, P, P]
+        C = ctypes.c_int
+        L.oracle_conv_fma.restype = ctypes.c_int
+        L.oracle_conv_fma.argtypes = [P, C, C, C, P, P, C, C, C, P]
+        L.oracle_expf_np_array.restype = None
+        L.oracle_expf_np_array.argtypes = [P, P, I64]
         _lib = L
     return _lib
 
@@ -480,6 +485,75 @@ def decode_params(idx: np.ndarray, m: Model, H: int, W: int):
     a = np.clip(conv2d(u, t["dec.mu.w"], t["dec.mu.b"]), np.float32(-15), np.float32(15))
     mu = np.float32(255.0) * sigmoid32(a)
     s = np.exp(np.clip(conv2d(u, t["dec.s.w"], t["dec.s.b"]), LOG_S_MIN, LOG_S_MAX))
+    s = np.clip(s, np.float32(0.5), np.float32(64.0))
+    return (np.ascontiguousarray(mu[:, :H, :W].transpose(1, 2, 0)),
+            np.ascontiguousarray(s[:, :H, :W].transpose(1, 2, 0)))
+
+
+# --------------------------------------------------------------------------
+# The same network with every float operation spelled out (pilc_oracle.c
+# oracle_conv_fma / oracle_expf_np): the statement of the reference's
+# arithmetic that the GPU "exact" network follows. Pinned bit for bit against
+# the reference's own z, mu, s by tests/test_oracle.py.
+
+
+def conv2d_fma(x, w, b, stride=1):
+    x = np.ascontiguousarray(x, np.float32)
+    w = np.ascontiguousarray(w, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    ci, H, W = x.shape
+    co, _, k, _ = w.shape
+    p = k // 2
+    Ho, Wo = (H + 2 * p - k) // stride + 1, (W + 2 * p - k) // stride + 1
+    out = np.empty((co, Ho, Wo), np.float32)
+    if lib().oracle_conv_fma(_p(x), ci, H, W, _p(w), _p(b), co, k, stride, _p(out)):
+        raise NotImplementedError("no modelled BLAS order for this shape")
+    return out
+
+
+def exp_np(x):
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.empty_like(x)
+    lib().oracle_expf_np_array(_p(x), _p(y), x.size)
+    return y
+
+
+def sigmoid_exact(x):
+    x = np.asarray(x, np.float32)
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = np.float32(1.0) / (np.float32(1.0) + exp_np(-x[pos]))
+    e = exp_np(x[~pos])
+    out[~pos] = e / (np.float32(1.0) + e)
+    return out
+
+
+def encoder_latents_exact(img: np.ndarray, m: Model) -> np.ndarray:
+    t = m.t
+    ph, pw = img.shape[0] & 1, img.shape[1] & 1
+    if ph or pw:
+        img = np.pad(img, ((0, ph), (0, pw), (0, 0)), mode="edge")
+    x = np.ascontiguousarray((img.astype(np.float32) / np.float32(127.5) - np.float32(1.0)).transpose(2, 0, 1))
+    h = relu(conv2d_fma(x, t["enc.stem.w"], t["enc.stem.b"]))
+    h = relu(conv2d_fma(h, t["enc.down.w"], t["enc.down.b"], 2))
+    for i in range(m.B):
+        r = relu(conv2d_fma(h, t[f"enc.block{i}.conv1.w"], t[f"enc.block{i}.conv1.b"]))
+        h = relu(h + conv2d_fma(r, t[f"enc.block{i}.conv2.w"], t[f"enc.block{i}.conv2.b"]))
+    z = conv2d_fma(h, t["enc.proj.w"], t["enc.proj.b"])
+    return np.ascontiguousarray(z.transpose(1, 2, 0))
+
+
+def decode_params_exact(idx: np.ndarray, m: Model, H: int, W: int):
+    t = m.t
+    h = np.ascontiguousarray(t["codebook"][idx.astype(np.int64)].transpose(2, 0, 1))
+    h = relu(conv2d_fma(h, t["dec.proj.w"], t["dec.proj.b"]))
+    for i in range(m.B):
+        r = relu(conv2d_fma(h, t[f"dec.block{i}.conv1.w"], t[f"dec.block{i}.conv1.b"]))
+        h = relu(h + conv2d_fma(r, t[f"dec.block{i}.conv2.w"], t[f"dec.block{i}.conv2.b"]))
+    u = relu(pixel_shuffle(conv2d_fma(h, t["dec.up.w"], t["dec.up.b"])))
+    a = np.clip(conv2d_fma(u, t["dec.mu.w"], t["dec.mu.b"]), np.float32(-15), np.float32(15))
+    mu = np.float32(255.0) * sigmoid_exact(a)
+    s = exp_np(np.clip(conv2d_fma(u, t["dec.s.w"], t["dec.s.b"]), LOG_S_MIN, LOG_S_MAX))
     s = np.clip(s, np.float32(0.5), np.float32(64.0))
     return (np.ascontiguousarray(mu[:, :H, :W].transpose(1, 2, 0)),
             np.ascontiguousarray(s[:, :H, :W].transpose(1, 2, 0)))

@@ -171,3 +171,121 @@ void oracle_encode_batch(const uint8_t *syms, const uint16_t *ds, int64_t N,
                                        cnt, L, delta, phi, X, M, buf, &nbits[k]);
     }
 }
+
+/* ---------------------------------------------------------------------------
+ * The reference network's float arithmetic, stated as explicit operations.
+ *
+ * nn.py:15-34 computes each conv as `out += np.tensordot(w[:, :, i, j], tap)`
+ * tap by tap (i outer, j inner), then `out + b`. The tensordot is an f32
+ * GEMM through numpy's OpenBLAS (scipy-openblas 0.3.30 here), whose sgemm
+ * microkernels keep one accumulator per output element and walk the
+ * contraction index in order with fused multiply-adds, starting from zero
+ * (K <= 32 here, so there is a single K block). So, for most pixels:
+ *   t_ij[co,p] = fmaf(w[co,ci=K-1], x[K-1,p], ... fmaf(w[co,0], x[0,p], 0))
+ *   out = ((0 + t_00) + t_01) + ... + t_22 ;  out = out + b[co]
+ * with edge-replicate padding and stride 1 or 2; tap_dot() states the two
+ * places where OpenBLAS walks k differently (single-pixel outputs go to
+ * sgemv; with K >= 32 the last 1..8 pixels of an image go to a k-vectorised
+ * tail kernel). Returns -1 where no order is modelled. tests/test_oracle.py checks
+ * this statement bit for bit against the reference's own z, mu and s
+ * (tests/golden/vqvae_*.npz), which is what pins the GPU "exact" network.
+ * x: [cin][H][W] f32, w: [cout][cin][k][k], out: [cout][Ho][Wo]. */
+/* One tap's contraction over the input channels, in the order OpenBLAS
+ * evaluates it for an output pixel at position p of an n_px-pixel conv
+ * output (n_px = Ho*Wo of one image). -1 = order not modelled. */
+static int tap_dot(const float *w, int wstride, const float *x, int xstride, int K, int64_t p, int64_t n_px,
+                   int cout, float *res) {
+    if (n_px == 1) {
+        if (cout < 4) return -1;
+        /* numpy hands a single-column product to sgemv (sgemv_t): 8 lanes
+         * of fused multiply-adds over k = l (mod 8) then a fixed reduction;
+         * K = 8 reduces adjacent pairs first. */
+        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (K == 8) {
+            for (int l = 0; l < 8; ++l) a[l] = w[l * wstride] * x[l * xstride];
+            *res = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+            return 0;
+        }
+        if (K < 16 || K % 8) return -1;
+        for (int k = 0; k < K; ++k) a[k & 7] = fmaf(w[k * wstride], x[k * xstride], a[k & 7]);
+        *res = ((a[0] + a[4]) + (a[1] + a[5])) + ((a[2] + a[6]) + (a[3] + a[7]));
+        return 0;
+    }
+    const int64_t r = n_px % 16;
+    if (K >= 32 && r >= 1 && r <= 8 && p >= n_px - r) {
+        if (cout < 4 && r != 4 && r != 8) return -1;
+        /* sgemm's narrow m-tail (1..8 leftover pixels) vectorises over k:
+         * 16 lanes k = l (mod 16), then an adjacent-pair tree */
+        float a[16];
+        for (int l = 0; l < 16; ++l) a[l] = 0.0f;
+        for (int k = 0; k < K; ++k) a[k & 15] = fmaf(w[k * wstride], x[k * xstride], a[k & 15]);
+        for (int n = 16; n > 1; n >>= 1)
+            for (int l = 0; l < n / 2; ++l) a[l] = a[2 * l] + a[2 * l + 1];
+        *res = a[0];
+        return 0;
+    }
+    float t = 0.0f;
+    for (int k = 0; k < K; ++k) t = fmaf(w[k * wstride], x[k * xstride], t);
+    *res = t;
+    return 0;
+}
+
+int oracle_conv_fma(const float *x, int cin, int H, int W, const float *w,
+                    const float *b, int cout, int k, int stride, float *out) {
+    int p = k / 2;
+    int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
+    const int64_t n_px = (int64_t)Ho * Wo;
+    float col[4096];
+    if (cin > 4096) return -1;
+    for (int co = 0; co < cout; ++co)
+        for (int y = 0; y < Ho; ++y)
+            for (int xo = 0; xo < Wo; ++xo) {
+                float o = 0.0f;
+                for (int i = 0; i < k; ++i)
+                    for (int j = 0; j < k; ++j) {
+                        int yy = y * stride + i - p, xx = xo * stride + j - p;
+                        yy = yy < 0 ? 0 : (yy >= H ? H - 1 : yy);
+                        xx = xx < 0 ? 0 : (xx >= W ? W - 1 : xx);
+                        for (int ci = 0; ci < cin; ++ci) col[ci] = x[(ci * H + yy) * W + xx];
+                        float t;
+                        if (tap_dot(w + (co * cin * k + i) * k + j, k * k, col, 1, cin, (int64_t)y * Wo + xo, n_px, cout, &t))
+                            return -1;
+                        o = o + t;
+                    }
+                out[(co * Ho + y) * Wo + xo] = o + b[co];
+            }
+    return 0;
+}
+
+/* numpy's float32 exp (the SIMD loop numpy 2.x dispatches to on AVX2/AVX512F
+ * hosts, numpy/_core/src/umath/loops_exponent_log.dispatch.c.src
+ * simd_exp_f32): Cody-Waite reduction by ln 2 in two parts, a [5/2] rational
+ * approximation evaluated with fused multiply-adds, an IEEE division and a
+ * scale by 2^q. The reference's sigmoid and s = exp(.) (nn.py:41-48,
+ * vqvae.py:108) go through it; tests/test_oracle.py compares this statement
+ * with np.exp over every float32 in the head's input ranges. */
+float oracle_expf_np(float x) {
+    const float log2e = 1.44269504088896341f, magic = 0x1.800000p+23f;
+    const float c1 = -6.93145752e-1f, c2 = -1.42860677e-6f;
+    const float p0 = 9.999999999980870924916e-01f, p1 = 7.257664613233124478488e-01f,
+                p2 = 2.473615434895520810817e-01f, p3 = 5.114512081637298353406e-02f,
+                p4 = 6.757896990527504603057e-03f, p5 = 5.082762527590693718096e-04f;
+    const float q1 = -2.742335390411667452936e-01f, q2 = 2.159509375685829852307e-02f;
+    float q = x * log2e;
+    q = q + magic;
+    q = q - magic;
+    float r = fmaf(q, c1, x);
+    r = fmaf(q, c2, r);
+    float n = fmaf(p5, r, p4);
+    n = fmaf(n, r, p3);
+    n = fmaf(n, r, p2);
+    n = fmaf(n, r, p1);
+    n = fmaf(n, r, p0);
+    float d = fmaf(q2, r, q1);
+    d = fmaf(d, r, 1.0f);
+    return ldexpf(n / d, (int)q);
+}
+
+void oracle_expf_np_array(const float *x, float *y, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) y[i] = oracle_expf_np(x[i]);
+}
