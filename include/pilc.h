@@ -94,14 +94,12 @@ typedef struct pilc_header {
 } pilc_header;
 
 const char *pilc_version(void);
-/* Tuning switches of the production path (no reference counterpart; for
- * A/B checks). key 0: encoder residual blocks as one fused kernel per block
+/* Tuning switches of the fast path (no reference counterpart; for A/B
+ * checks). key 0: encoder residual blocks as one fused kernel per block
  * (default 1) instead of two conv launches; key 1: decoder trunk (gather +
  * block convs) as one kernel with activations in shared memory (default 1)
- * instead of per-layer launches. Both bit-identical to the unfused path.
- * key 2: decoder head over pixel pairs (default 1; 24 instead of 36 MMAs per
- * 256 pixels; a different fp32 summation order than the per-pixel head, so
- * compress and decompress must use the same setting).
+ * instead of per-layer launches. Both bit-identical to the unfused path, so
+ * no switch changes any output byte.
  * Returns the previous value, or -PILC_E_ARG for an unknown key. */
 int pilc_set_tuning(int32_t key, int32_t value);
 /* Device sanity: returns 100 for sm_100 etc., or -1 if no usable device. */
@@ -178,14 +176,23 @@ int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W,
                    const float *model, int32_t K, int32_t Dc, int32_t C,
                    int32_t B, void *workspace, int64_t ws_bytes,
                    uint8_t *idx_out, float *z_out, void *stream);
-/* Same contract, always the fp32 SIMT kernels (validation reference). The
- * production pilc_vq_encode runs the block convs and the projection as
- * 3xTF32 tcgen05 GEMMs when C == Dc == 32 (fp32-class z: hi/lo split of
- * activations and weights, three MMAs per K step). */
-int pilc_vq_encode_simt(const uint8_t *img, int64_t n_img, int32_t H,
+/* Same contract, the exact network: the reference's float arithmetic
+ * operation for operation (nn.conv2d as OpenBLAS evaluates it, numpy's
+ * float32 exp; oracle/pilc_oracle.c states it), so z and the indices are
+ * bit-identical to the reference's. pilc_vq_encode (the fast encoder) runs
+ * the convs as fp16-split tcgen05 GEMMs when C == Dc == 32 (fp32-class z:
+ * hi/lo split of activations and weights, three MMAs per K step) and the
+ * exact network otherwise. Returns PILC_E_UNSUPPORTED for the few shapes
+ * where OpenBLAS's order is not modelled (single-pixel convs with Ci not a
+ * multiple of 8, ...). */
+int pilc_vq_encode_exact(const uint8_t *img, int64_t n_img, int32_t H,
                         int32_t W, const float *model, int32_t K, int32_t Dc,
                         int32_t C, int32_t B, void *workspace, int64_t ws_bytes,
                         uint8_t *idx_out, float *z_out, void *stream);
+/* 1 when pilc_vq_decode runs the tcgen05 decoder for this model and image
+ * shape (C == 32 and the tiles fit shared memory), 0 when it runs the exact
+ * network. A function of (config, H, W) only. */
+int pilc_vq_fast_decoder(int32_t K, int32_t Dc, int32_t C, int32_t B, int32_t H, int32_t W);
 /* Codebook argmin alone: z (n_vec, Dc) float32 -> u8 (vqvae.py:66-76). */
 int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model,
                    int32_t K, int32_t Dc, int32_t C, int32_t B, uint8_t *idx_out,
@@ -201,11 +208,13 @@ int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
                    void *workspace, int64_t ws_bytes, uint8_t *shift_out,
                    uint8_t *d_out, float *mu_out, float *s_out, void *stream);
 
-/* Same contract, always the fp32 SIMT kernels (any configuration). The
- * production pilc_vq_decode runs the tcgen05 bf16 path when C == 32; the
- * choice is a function of the model configuration only, so compress and
- * decompress agree. This entry point is the validation reference. */
-int pilc_vq_decode_simt(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
+/* Same contract, the exact network (see pilc_vq_encode_exact): mu and s are
+ * bit-identical to the reference's decode_to_params, so shift and d are
+ * too, and containers decode interchangeably with pixelcodec. The fast
+ * pilc_vq_decode runs the tcgen05 bf16 decoder when pilc_vq_fast_decoder
+ * says so for (model, H, W), else the exact network; containers written
+ * with the fast decoder carry header flag 0x80 (container.py). */
+int pilc_vq_decode_exact(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
                         const float *model, int32_t K, int32_t Dc, int32_t C,
                         int32_t B, const double *d_thresh, int32_t D,
                         void *workspace, int64_t ws_bytes, uint8_t *shift_out,

@@ -625,6 +625,8 @@ def decompress(blob: bytes, model: Model | None = None) -> np.ndarray:
     if zlib.crc32(blob[:-4]) != struct.unpack_from("<I", blob, len(blob) - 4)[0]:
         raise OracleError("CorruptStreamError", "container checksum mismatch")
     backend, M, pad, flags = blob[5], blob[6], blob[7], blob[8]
+    if flags & ~1:  # container.py:223-224
+        raise OracleError("FormatError", f"unknown header flags {flags:#x}")
     W, H, L, static_d = struct.unpack_from("<IIHH", blob, 9)
     (D,) = struct.unpack_from("<H", blob, 21)
     grid = np.frombuffer(blob, "<f8", D, 23).copy()

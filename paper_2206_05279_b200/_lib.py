@@ -32,10 +32,11 @@ _SIGS = {
     "pilc_model_pack": (ctypes.c_int, [P, I32, I32, I32, I32, P]),
     "pilc_vq_workspace_bytes": (I64, [I64, I32, I32, I32, I32, I32, I32]),
     "pilc_vq_encode": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I64, P, P, P]),
-    "pilc_vq_encode_simt": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I64, P, P, P]),
+    "pilc_vq_encode_exact": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I64, P, P, P]),
+    "pilc_vq_fast_decoder": (ctypes.c_int, [I32, I32, I32, I32, I32, I32]),
     "pilc_vq_argmin": (ctypes.c_int, [P, I64, P, I32, I32, I32, I32, P, P]),
     "pilc_vq_decode": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, P]),
-    "pilc_vq_decode_simt": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, P]),
+    "pilc_vq_decode_exact": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, P]),
     "pilc_static_scale": (ctypes.c_int, [P, I64, I64, P, I32, P, P]),
     "pilc_container_sizes": (ctypes.c_int, [P, P, I64, I32, I64, P, P, P]),
     "pilc_container_pack": (ctypes.c_int, [P, I32, P, P, I32, I64, I64, I32, P, I64, P, P, P, I64, P, P, P, P, P]),
@@ -116,7 +117,6 @@ def call(name: str, *args) -> int:
 
 TUNE_BLOCK_FUSION = 0
 TUNE_DEC_TRUNK = 1
-TUNE_HEAD_PAIRS = 2
 
 
 def set_tuning(key: int, value: int) -> int:

@@ -47,6 +47,15 @@ BACKEND_VQVAE = 1
 BACKEND_NAMES = {BACKEND_STATIC: "twar-static", BACKEND_VQVAE: "twar-vqvae"}
 BACKEND_IDS = {v: k for k, v in BACKEND_NAMES.items()}
 FLAG_SCHEDULE_CHECKSUM = 1
+# Decoder numerics (this package's extension of the header flags byte). A
+# twar-vqvae container whose (shift, d) schedule came from the fast tcgen05
+# decoder carries this bit; pixelcodec rejects it ("unknown header flags"),
+# so such a blob can never be decoded with different numerics into wrong
+# pixels. Containers without it were made with the reference's arithmetic
+# (numerics="exact", or pixelcodec itself) and are decoded by the exact
+# network, which reproduces pixelcodec's mu and s bit for bit.
+FLAG_FAST_DECODER = 0x80
+NUMERICS = ("exact", "fast")
 
 
 @dataclass(frozen=True)
@@ -57,6 +66,13 @@ class CodecConfig:
     grid: ScaleGrid = field(default_factory=default_grid)
     verify_tables: bool = False
     debug_schedule_check: bool = False
+    # twar-vqvae network arithmetic (an extension; pixelcodec has no such
+    # field). "exact": the reference's float arithmetic -- containers are
+    # byte-identical to pixelcodec.compress and decode either way. "fast":
+    # tcgen05 encoder (fp32-class, same indices in practice) and bf16
+    # decoder; bits/dim within 0.5% of the reference, containers flagged
+    # FLAG_FAST_DECODER (decodable by this package only).
+    numerics: str = "exact"
 
     def __post_init__(self):
         if self.backend not in BACKEND_IDS:
@@ -65,6 +81,8 @@ class CodecConfig:
             raise ParameterError("M must be in [10, 12]")
         if not 1 <= self.lanes <= 65535:
             raise ParameterError("lane count must fit in 16 bits")
+        if self.numerics not in NUMERICS:
+            raise ParameterError(f"unknown numerics {self.numerics!r}")
 
 
 @dataclass(frozen=True)
@@ -94,9 +112,26 @@ def _params_of(model: ModelWeights | None) -> PredictorParams:
     return model.predictor_params if model is not None else default_params()
 
 
+def fast_decoder(model: ModelWeights, H: int, W: int) -> bool:
+    """Whether numerics="fast" runs the tcgen05 decoder for this model and
+    shape (pilc_vq_fast_decoder: C == 32 and the tiles fit); otherwise the
+    exact network runs and the container is unflagged."""
+    memo = model.__dict__.setdefault("_fast_dec_memo", {})
+    if (H, W) not in memo:
+        memo[(H, W)] = _lib.load().pilc_vq_fast_decoder(*model.cfg_tuple(), H, W) == 1
+    return memo[(H, W)]
+
+
+def _flags(backend: int, cfg: CodecConfig, model, W: int, H: int) -> int:
+    flags = FLAG_SCHEDULE_CHECKSUM if cfg.debug_schedule_check else 0
+    if backend == BACKEND_VQVAE and cfg.numerics == "fast" and fast_decoder(model, H, W):
+        flags |= FLAG_FAST_DECODER
+    return flags
+
+
 def _template(backend: int, cfg: CodecConfig, W: int, H: int, params: PredictorParams,
               model: ModelWeights | None) -> bytes:
-    flags = FLAG_SCHEDULE_CHECKSUM if cfg.debug_schedule_check else 0
+    flags = _flags(backend, cfg, model, W, H)
     t = MAGIC + struct.pack("<BBBBB", VERSION, backend, cfg.M, PAD_RULE_ZERO, flags)
     t += struct.pack("<IIHH", W, H, cfg.lanes, 0) + cfg.grid.to_bytes() + params.hash8()
     if backend == BACKEND_VQVAE:
@@ -126,9 +161,11 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
     if backend == BACKEND_VQVAE:
         if model is None or not model.has_network:
             raise ModelError("vqvae backend needs model weights")
+        exact = config.numerics == "exact"
         if idx_d is None:
-            idx_d = encode_indices_device(img_d, model, dev, stream)
-        shift, dsched = decode_head_device(idx_d, model, H, W, grid, dev, stream)
+            idx_d = encode_indices_device(img_d, model, dev, stream, exact=exact)
+        fast_dec = bool(_flags(backend, config, model, W, H) & FLAG_FAST_DECODER)
+        shift, dsched = decode_head_device(idx_d, model, H, W, grid, dev, stream, exact=not fast_dec)
         idx_enc, _ = build_tables([index_histogram_pmf(model, M)], M, verify=config.verify_tables)
         gh, gw = latent_shape(H, W)
         idx_scr, idx_cap, idx_nb, idx_st = encode_lanes_device(idx_d, N, gh * gw, L, idx_enc, dev, stream)
@@ -185,7 +222,7 @@ def _staged_encode(arr: np.ndarray, model, config: CodecConfig, dev, stream):
             ev = torch.cuda.Event()
             ev.record(copy)
         stream.wait_event(ev)
-        parts.append(encode_indices_device(img_d[a:b], model, dev, stream))
+        parts.append(encode_indices_device(img_d[a:b], model, dev, stream, exact=config.numerics == "exact"))
     with torch.cuda.stream(stream):
         idx_d = torch.cat(parts)
     return img_d, idx_d
@@ -510,7 +547,13 @@ def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_
             _lib.call("pilc_rans_decode", ptr(buf_d), ptr(lo), ptr(nb), ptr(ss), None, None, ng, gh * gw, L,
                       ptr(idx_dec.device_words(dev)), idx_dec.D, M, None, ptr(idx), ptr(ls), sptr(stream))
             lane_st["idx"] = ls
-            shift, dsel = decode_head_device(idx, model, H, W, grid, dev, stream)
+            if (flags & FLAG_FAST_DECODER) and not fast_decoder(model, H, W):
+                for i in ids:
+                    errors[int(i)] = FormatError("fast-decoder container for a model / shape the fast decoder "
+                                                 "does not run")
+                continue
+            shift, dsel = decode_head_device(idx, model, H, W, grid, dev, stream,
+                                             exact=not (flags & FLAG_FAST_DECODER))
         else:
             # static_d straight from the device headers (no host round trip)
             d_img = hdr16[:, sd_col].index_select(0, ids_d).contiguous()
@@ -675,7 +718,8 @@ def parse_header(blob: bytes) -> tuple[ContainerHeader, int]:
         raise FormatError(f"precision M={M} outside [10, 12]")
     if pad_rule != PAD_RULE_ZERO:
         raise FormatError(f"unknown padding rule {pad_rule}")
-    if flags & ~FLAG_SCHEDULE_CHECKSUM:
+    if flags & ~(FLAG_SCHEDULE_CHECKSUM | FLAG_FAST_DECODER) or (flags & FLAG_FAST_DECODER
+                                                                 and backend != BACKEND_VQVAE):
         raise FormatError(f"unknown header flags {flags:#x}")
     W, H, L, static_d = r.unpack("<IIHH")
     if W < 1 or H < 1 or L < 1:
@@ -735,4 +779,5 @@ def inspect(blob: bytes) -> dict:
         "index_stream_bytes": sum(header.index_lane_bytes),
         "residual_stream_bytes": sum(header.residual_lane_bytes),
         "container_bytes": len(blob),
+        "numerics": "fast" if blob[8] & FLAG_FAST_DECODER else "exact",
     }

@@ -50,7 +50,7 @@ struct ProfScope {
 };
 
 // Library tuning switches (pilc_set_tuning); defaults are the production path.
-enum { PILC_TUNE_BLOCK_FUSION = 0, PILC_TUNE_DEC_TRUNK = 1, PILC_TUNE_HEAD_PAIRS = 2, PILC_TUNE_N };
+enum { PILC_TUNE_BLOCK_FUSION = 0, PILC_TUNE_DEC_TRUNK = 1, PILC_TUNE_N };
 extern int g_tuning[PILC_TUNE_N];
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(32 * kWarps) parse_kernel(const uint8_t *__res
                     h.aux = h.backend;
                 } else if (h.M < 10 || h.M > 12) st = PILC_ST_BAD_M;
                 else if (h.pad_rule != 0) st = PILC_ST_BAD_PAD;
-                else if (h.flags & ~1u) st = PILC_ST_BAD_FLAGS;
+                else if ((h.flags & ~0x81u) || ((h.flags & 0x80u) && h.backend != 1)) st = PILC_ST_BAD_FLAGS;  // 0x80: fast decoder (vqvae only)
             }
             if (!st) {
                 if (!need(12)) st = PILC_ST_TRUNCATED;

@@ -2110,12 +2110,13 @@ __global__ void __launch_bounds__(kAmThreads, 1) argmin_tc_kernel(ArgminTc a) {
     }
 }
 
+// shared-memory plan of one tc_conv_kernel launch: ring depth kStages, or as
+// many stages as fit for wide images (>= 2); 0 when even that does not fit
 template <int N, int KS, int MODE>
-int launch_tc(const TcLayer &L, cudaStream_t s) {
+size_t tc_smem_plan(int Wp, int *stages) {
     constexpr int NG = MODE == TC_OUT_HEAD2 ? 8 : 4;
     constexpr int KG = MODE == TC_OUT_HEAD2 ? 48 : KS * KS * NG;
-    const int npix = KS == 3 ? ((128 + 2 * L.Wp + 2 + 7) & ~7) : 128;
-    // ring depth: kStages, or as many stages as fit for wide images (>= 2)
+    const int npix = KS == 3 ? ((128 + 2 * Wp + 2 + 7) & ~7) : 128;
     auto smem_of = [&](int k) {
         return (size_t)KG * N * 16 + (size_t)k * NG * npix * 16 + 8 * (2 * k + 6) + 4 * N +
                4 * ((MODE == TC_OUT_HEAD || MODE == TC_OUT_HEAD2) ? 256 : 0) + 16;
@@ -2124,11 +2125,18 @@ int launch_tc(const TcLayer &L, cudaStream_t s) {
     // the heads run two CTAs per SM: half the shared memory each
     const size_t cap = (MODE == TC_OUT_HEAD || MODE == TC_OUT_HEAD2) ? 113 * 1024 : 227 * 1024;
     while (st > 2 && smem_of(st) > cap) --st;
-    const size_t smem = smem_of(st);
+    *stages = st;
+    return smem_of(st) > 227 * 1024 ? 0 : smem_of(st);
+}
+
+template <int N, int KS, int MODE>
+int launch_tc(const TcLayer &L, cudaStream_t s) {
+    int st = 0;
+    const size_t smem = tc_smem_plan<N, KS, MODE>(L.Wp, &st);
     TcLayer Ls = L;
     Ls.n_stages = st;
     if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
-    if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
+    if (smem == 0) return PILC_E_UNSUPPORTED;
     auto kern = tc_conv_kernel<N, KS, MODE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // one persistent CTA per SM (two epilogue groups, an 8-deep copy ring);
@@ -2268,7 +2276,18 @@ int dec_trunk_launch(const DecTrunk &p0, cudaStream_t s) {
     return PILC_OK;
 }
 int tc_launch_shuffle(const TcLayer &L, cudaStream_t s) { return launch_tc<128, 3, TC_OUT_SHUFFLE>(L, s); }
-int tc_launch_head(const TcLayer &L, cudaStream_t s) { return launch_tc<16, 3, TC_OUT_HEAD>(L, s); }
+// Whether the tcgen05 decoder runs for a latent grid gh x gw (a function of
+// the shape only, never of the batch size: vq_decode splits batches below the
+// 32-bit pixel-index limit). The per-layer block convs, the up conv and the
+// head must fit shared memory; the fused trunk falls back to the per-layer
+// convs with bit-identical results.
+bool tc_decoder_supported(int gh, int gw, bool pairs) {
+    int st;
+    if (!tc_smem_plan<32, 3, TC_OUT_ACT>(gw + 2, &st)) return false;
+    if (!tc_smem_plan<128, 3, TC_OUT_SHUFFLE>(gw + 2, &st)) return false;
+    (void)pairs;
+    return tc_smem_plan<16, 3, TC_OUT_HEAD2>(gw + 1, &st) != 0;
+}
 int tc_launch_head2(const TcLayer &L, cudaStream_t s) { return launch_tc<16, 3, TC_OUT_HEAD2>(L, s); }
 
 int tc_dec_table(const float *cb, const float *w, const float *b, int K, int Dc, int ci_pad, int co_pad,

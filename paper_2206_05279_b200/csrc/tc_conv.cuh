@@ -131,8 +131,8 @@ int argmin_tc_launch(const ArgminTc &a, cudaStream_t s);
 int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s);
 
 int tc_launch_act(const TcLayer &L, cudaStream_t s);
+bool tc_decoder_supported(int gh, int gw, bool pairs);
 int tc_launch_shuffle(const TcLayer &L, cudaStream_t s);
-int tc_launch_head(const TcLayer &L, cudaStream_t s);
 int tc_launch_head2(const TcLayer &L, cudaStream_t s);  // head over pixel pairs (pair layout input)
 int tc_dec_table(const float *cb, const float *w, const float *b, int K, int Dc, int ci_pad, int co_pad,
                  uint16_t *table, cudaStream_t s);

@@ -132,7 +132,29 @@ Layout make_layout(int K, int Dc, int C, int B) {
     return L;
 }
 
-// ---- conv kernel -----------------------------------------------------------
+// ---- conv kernel: the reference's float arithmetic ---------------------------
+// nn.conv2d (nn.py:15-34) is `out += tensordot(w[:, :, i, j], tap)` tap by
+// tap, then `+ b`, where each tensordot is an OpenBLAS sgemm: one fused
+// multiply-add chain per output over the input channels in order, from zero
+// (oracle/pilc_oracle.c oracle_conv_fma states this and is pinned against
+// the reference's own z, mu and s). This kernel performs exactly those
+// operations: per tap t = fmaf(w[ci], x[ci], t) for ci = 0 .. Ci-1, o = o + t
+// (taps in (i, j) order), v = o + b, then the layer's epilogue in the
+// reference's order. Every output is a fixed sequence of IEEE operations on
+// fixed inputs, so results are identical for any batch size, tiling, GPU or
+// GPU count -- and identical to the reference where OpenBLAS takes this
+// order. The two places where it does not (single-pixel outputs go to
+// sgemv; with Ci >= 32 the last 1..8 pixels of an image's raster go to a
+// k-vectorised tail kernel) are computed by xtail_kernel in the order the
+// oracle states, and substituted here before the epilogue.
+//
+// Tiling: a CTA owns TR x 16 output pixels of one image and CO_T output
+// channels; each thread 8 output channels x PPT pixels of one row (columns
+// q, q + 16/PPT, ...), i.e. 8*PPT independent chains per input channel with
+// one broadcast weight load (2 x 16 B) and PPT scalar activation loads from
+// a channel-planar shared-memory patch whose row pitch IC is picked so the
+// warp's activation loads hit distinct banks. Input channels come through
+// shared memory CK at a time; when they all fit, once per CTA.
 enum InMode { IN_F32 = 0, IN_U8 = 1, IN_CODEBOOK = 2 };
 enum OutMode { OUT_F32 = 0, OUT_SHUFFLE = 1, OUT_HEAD = 2 };
 
@@ -151,7 +173,12 @@ struct ConvArgs {
     int relu;
     float *out;
     int out_mode;
-    int tiles_x, tiles_per_img;
+    // tiling (set by launch_conv)
+    int tiles_x, tiles_per_img, TR, IC, CK, CO_T;
+    // outputs at raster positions >= tail_start of each image come from
+    // side[(n * 8 + p - tail_start) * Co_pad + co] (xtail_kernel)
+    int64_t tail_start;
+    float *side;
     // head
     uint8_t *shift, *dsel;
     float *mu, *s;
@@ -163,133 +190,151 @@ struct ConvArgs {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-__device__ __forceinline__ float sigmoid_f32(float x) {
-    // nn.py:41-48: stable two-branch form in float32
-    if (x >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-x)));
-    const float e = expf(x);
+// numpy's float32 exp (oracle_expf_np): Cody-Waite reduction, a [5/2]
+// rational approximation with fused multiply-adds, IEEE division, 2^q scale
+__device__ __forceinline__ float np_expf(float x) {
+    float q = __fmul_rn(x, 1.44269504088896341f);
+    q = __fadd_rn(q, 0x1.800000p+23f);
+    q = __fsub_rn(q, 0x1.800000p+23f);
+    float r = fmaf(q, -6.93145752e-1f, x);
+    r = fmaf(q, -1.42860677e-6f, r);
+    float n = fmaf(5.082762527590693718096e-04f, r, 6.757896990527504603057e-03f);
+    n = fmaf(n, r, 5.114512081637298353406e-02f);
+    n = fmaf(n, r, 2.473615434895520810817e-01f);
+    n = fmaf(n, r, 7.257664613233124478488e-01f);
+    n = fmaf(n, r, 9.999999999980870924916e-01f);
+    float d = fmaf(2.159509375685829852307e-02f, r, -2.742335390411667452936e-01f);
+    d = fmaf(d, r, 1.0f);
+    return scalbnf(__fdiv_rn(n, d), (int)q);
+}
+
+__device__ __forceinline__ float sigmoid_np(float x) {
+    // nn.py:41-48: two-branch form in float32 over numpy's exp
+    if (x >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, np_expf(-x)));
+    const float e = np_expf(x);
     return __fdiv_rn(e, __fadd_rn(1.f, e));
 }
 
+// one input value of the conv at (image n, channel c, input row y, col x), y
+// and x already clamped to the logical input grid
+__device__ __forceinline__ float conv_input(const ConvArgs &a, int64_t n, int c, int y, int x) {
+    if (c >= a.Ci) return 0.f;
+    if (a.in_mode == IN_F32) return __ldg(a.in + (((int64_t)n * a.Hi + y) * a.Wi + x) * a.Ci + c);
+    if (a.in_mode == IN_U8) {
+        // vqvae._even_pad + _normalize (vqvae.py:33-43): the even-padded
+        // image repeats its last row / column, i.e. clamp to the source
+        const int yy = y < a.src_h ? y : a.src_h - 1, xx = x < a.src_w ? x : a.src_w - 1;
+        const float v = (float)__ldg(a.in_u8 + (((int64_t)n * a.src_h + yy) * a.src_w + xx) * 3 + c);
+        return __fsub_rn(__fdiv_rn(v, 127.5f), 1.f);
+    }
+    const int k = a.in_u8[((int64_t)n * a.Hi + y) * a.Wi + x];
+    return a.codebook[(int64_t)k * a.Ci + c];
+}
 
-template <int CO_T>
-__global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
-    extern __shared__ float smem[];
-    const int ks = a.ks, st = a.stride, pad = ks >> 1;
-    const int IR = (kTile - 1) * st + ks;  // input patch rows / cols
-    const int IC = IR + 1;                 // pitch (+1 against bank conflicts)
-    float *s_in = smem;                    // [kCK][IR][IC]
-    float *s_w = smem + kCK * IR * IC;     // [tap][kCK][CO_T]
+template <int PPT>
+__global__ void __launch_bounds__(128) conv_kernel(ConvArgs a) {
+    constexpr int CPT = 8;
+    constexpr int PGR = 16 / PPT;  // pixel groups per tile row
+    extern __shared__ __align__(16) float smem[];
+    const int ks = a.ks, st = a.stride, pad = ks >> 1, TR = a.TR, IC = a.IC, CK = a.CK, CO_T = a.CO_T;
+    const int IR = (TR - 1) * st + ks, ICW = 15 * st + ks;
+    const int plane = (IR * IC) | 1;  // odd: staging stores of consecutive channels hit distinct banks
+    const int ntap = ks * ks;
+    const int nchunk = (a.Ci_pad + CK - 1) / CK;
+    float *s_in = smem;                            // [CK][plane]
+    float *s_w = smem + ((CK * plane + 3) & ~3);   // [ntap or 1][CK][CO_T]
 
     const int tile = blockIdx.x % a.tiles_per_img;
     const int64_t n = blockIdx.x / a.tiles_per_img;
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-    const int oy0 = ty * kTile, ox0 = tx * kTile;
+    const int oy0 = ty * TR, ox0 = tx * 16;
     const int co0 = blockIdx.y * CO_T;
+    const int NCG = CO_T / CPT;
     const int t = threadIdx.x;
-    const int col = t & 15, r0 = t >> 4;  // rows r0 and r0 + 8
+    const int cg = t % NCG, pg = t / NCG;
+    const int pr = pg / PGR, pq = pg - pr * PGR;  // tile row, first column
     const int iy0 = oy0 * st - pad, ix0 = ox0 * st - pad;
 
-    float acc0[CO_T], acc1[CO_T];
+    float o[CPT][PPT];
 #pragma unroll
-    for (int c = 0; c < CO_T; ++c) acc0[c] = acc1[c] = 0.f;
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) o[c][p] = 0.f;
 
-    const int ntap = ks * ks;
-    for (int c0 = 0; c0 < a.Ci_pad; c0 += kCK) {
-        // stage the input patch, channel-planar in smem; element order is
-        // channel-fastest so a warp reads 4 pixels x 8 contiguous channels.
-        // Four elements per thread per round: all loads first, then the
-        // shared stores, so four global loads are in flight per thread.
-        const int patch = IR * IR;
-        const int ci = t & 7;
-        const int c = c0 + ci;
-        const uint32_t m_ir = 0xFFFFFFFFu / (uint32_t)IR + 1u;  // ceil(2^32 / IR)
-        for (int base = t; base < kCK * patch; base += 4 * kThreads) {
-            float v[4];
-            int sidx[4];
+    for (int tap = 0; tap < ntap; ++tap) {
+        const int ti = tap / ks, tj = tap - ti * ks;
+        float acc[CPT][PPT];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = base + u * kThreads;
-                v[u] = 0.f;
-                sidx[u] = -1;
-                if (e < kCK * patch) {
-                    const uint32_t pix = (uint32_t)e >> 3;
-                    const int py = (int)__umulhi(pix, m_ir), px = (int)pix - py * IR;  // pix / IR, exact for pix < 2^16
-                    sidx[u] = (ci * IR + py) * IC + px;
-                    if (a.in_mode == IN_F32) {
-                        if (c < a.Ci) {
-                            const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
-                            v[u] = __ldg(a.in + (((int64_t)n * a.Hi + y) * a.Wi + x) * a.Ci + c);
-                        }
-                    } else if (a.in_mode == IN_U8) {
-                        if (c < 3) {
-                            const int y = clampi(iy0 + py, 0, a.src_h - 1), x = clampi(ix0 + px, 0, a.src_w - 1);
-                            v[u] = (float)__ldg(a.in_u8 + (((int64_t)n * a.src_h + y) * a.src_w + x) * 3 + c);
-                        }
-                    } else {
-                        if (c < a.Ci) {
-                            const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
-                            const int k = a.in_u8[((int64_t)n * a.Hi + y) * a.Wi + x];
-                            v[u] = a.codebook[(int64_t)k * a.Ci + c];
-                        }
-                    }
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) acc[c][p] = 0.f;
+        for (int ch = 0; ch < nchunk; ++ch) {
+            const int c0 = ch * CK;
+            const int cn = min(CK, a.Ci_pad - c0);
+            if (tap == 0 || nchunk > 1) {
+                __syncthreads();
+                const int patch = IR * ICW;
+                for (int e = t; e < cn * patch; e += blockDim.x) {
+                    const int ci = e % cn, pix = e / cn;
+                    const int py = pix / ICW, px = pix - py * ICW;
+                    const int y = clampi(iy0 + py, 0, a.Hi - 1), x = clampi(ix0 + px, 0, a.Wi - 1);
+                    s_in[ci * plane + py * IC + px] = conv_input(a, n, c0 + ci, y, x);
                 }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (sidx[u] < 0) continue;
-                float x = v[u];
-                if (a.in_mode == IN_U8 && c < 3) x = __fsub_rn(__fdiv_rn(x, 127.5f), 1.f);  // vqvae.py:41-43
-                s_in[sidx[u]] = x;
-            }
-        }
-        // stage weights [tap][ci][co0 .. co0+CO_T)
-        for (int e = t; e < ntap * kCK * CO_T; e += kThreads) {
-            const int tap = e / (kCK * CO_T), rem = e - tap * (kCK * CO_T);
-            const int ci = rem / CO_T, co = rem - ci * CO_T;
-            s_w[e] = a.w[((int64_t)tap * a.Ci_pad + c0 + ci) * a.Co_pad + co0 + co];
-        }
-        __syncthreads();
-        for (int ci = 0; ci < kCK; ++ci) {
-            const float *pin = s_in + ci * IR * IC;
-            for (int i = 0; i < ks; ++i) {
-                for (int j = 0; j < ks; ++j) {
-                    const float x0 = pin[(r0 * st + i) * IC + col * st + j];
-                    const float x1 = pin[((r0 + 8) * st + i) * IC + col * st + j];
-                    const float4 *wv = reinterpret_cast<const float4 *>(s_w + ((i * ks + j) * kCK + ci) * CO_T);
-#pragma unroll
-                    for (int q = 0; q < CO_T / 4; ++q) {
-                        const float4 w4 = wv[q];
-                        acc0[4 * q + 0] = fmaf(x0, w4.x, acc0[4 * q + 0]);
-                        acc0[4 * q + 1] = fmaf(x0, w4.y, acc0[4 * q + 1]);
-                        acc0[4 * q + 2] = fmaf(x0, w4.z, acc0[4 * q + 2]);
-                        acc0[4 * q + 3] = fmaf(x0, w4.w, acc0[4 * q + 3]);
-                        acc1[4 * q + 0] = fmaf(x1, w4.x, acc1[4 * q + 0]);
-                        acc1[4 * q + 1] = fmaf(x1, w4.y, acc1[4 * q + 1]);
-                        acc1[4 * q + 2] = fmaf(x1, w4.z, acc1[4 * q + 2]);
-                        acc1[4 * q + 3] = fmaf(x1, w4.w, acc1[4 * q + 3]);
-                    }
+                const int wt0 = nchunk > 1 ? tap : 0, wtn = nchunk > 1 ? 1 : ntap;
+                for (int e = t; e < wtn * cn * CO_T; e += blockDim.x) {
+                    const int co = e % CO_T, r = e / CO_T, ci = r % cn, tp = wt0 + r / cn;
+                    s_w[((tp - wt0) * CK + ci) * CO_T + co] =
+                        __ldg(a.w + ((int64_t)tp * a.Ci_pad + c0 + ci) * a.Co_pad + co0 + co);
                 }
+                __syncthreads();
+            }
+            const float *pin = s_in + (pr * st + ti) * IC + pq * st + tj;
+            const float *pw = s_w + ((nchunk > 1 ? 0 : tap) * CK) * CO_T + cg * CPT;
+#pragma unroll 2
+            for (int ci = 0; ci < cn; ++ci) {
+                float x[PPT];
+#pragma unroll
+                for (int p = 0; p < PPT; ++p) x[p] = pin[ci * plane + p * PGR * st];
+                const float4 w0 = *reinterpret_cast<const float4 *>(pw + ci * CO_T);
+                const float4 w1 = *reinterpret_cast<const float4 *>(pw + ci * CO_T + 4);
+                const float w[CPT] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+                for (int c = 0; c < CPT; ++c)
+#pragma unroll
+                    for (int p = 0; p < PPT; ++p) acc[c][p] = fmaf(w[c], x[p], acc[c][p]);
             }
         }
-        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) o[c][p] = __fadd_rn(o[c][p], acc[c][p]);
     }
 
     // ---- epilogue
+    const int oy = oy0 + pr;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const float *acc = h ? acc1 : acc0;
-        const int oy = oy0 + r0 + 8 * h, ox = ox0 + col;
+    for (int p = 0; p < PPT; ++p) {
+        const int ox = ox0 + pq + p * PGR;
         if (oy >= a.Ho || ox >= a.Wo) continue;
+        const int64_t praster = (int64_t)oy * a.Wo + ox;
+        float v[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            const int co = co0 + cg * CPT + c;
+            float oc = o[c][p];
+            if (praster >= a.tail_start) oc = a.side[((n * 8) + (praster - a.tail_start)) * a.Co_pad + co];
+            v[c] = __fadd_rn(oc, __ldg(a.b + co));
+        }
         if (a.out_mode == OUT_F32) {
             const int64_t base = (((int64_t)n * a.Ho + oy) * a.Wo + ox) * a.Co;
 #pragma unroll
-            for (int c = 0; c < CO_T; ++c) {
-                const int co = co0 + c;
+            for (int c = 0; c < CPT; ++c) {
+                const int co = co0 + cg * CPT + c;
                 if (co >= a.Co) break;
-                float v = __fadd_rn(acc[c], a.b[co]);
-                if (a.resid) v = __fadd_rn(a.resid[base + co], v);
-                if (a.relu) v = fmaxf(v, 0.f);
-                a.out[base + co] = v;
+                float r = v[c];
+                if (a.resid) r = __fadd_rn(a.resid[base + co], r);  // nn.residual_block: relu(x + conv)
+                if (a.relu) r = fmaxf(r, 0.f);
+                a.out[base + co] = r;
             }
         } else if (a.out_mode == OUT_SHUFFLE) {
             // nn.pixel_shuffle (nn.py:51-62): channel c*4 + dy*2 + dx of
@@ -297,12 +342,11 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
             const int Cs = a.Co >> 2;
             const int Hs = a.Ho * 2, Ws = a.Wo * 2;
 #pragma unroll
-            for (int c = 0; c < CO_T; ++c) {
-                const int co = co0 + c;
+            for (int c = 0; c < CPT; ++c) {
+                const int co = co0 + cg * CPT + c;
                 if (co >= a.Co) break;
                 const int cc = co >> 2, dy = (co >> 1) & 1, dx = co & 1;
-                const float v = fmaxf(__fadd_rn(acc[c], a.b[co]), 0.f);
-                a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = v;
+                a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = fmaxf(v[c], 0.f);
             }
         } else {
             // logistic head (vqvae.py:105-112, logistic.py:36-40, 109-114)
@@ -310,13 +354,10 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
             const int64_t px = ((int64_t)n * a.crop_h + oy) * a.crop_w + ox;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                float av = __fadd_rn(acc[c], a.b[c]);
-                av = fminf(fmaxf(av, -15.f), 15.f);
-                const float mu = __fmul_rn(255.f, sigmoid_f32(av));
-                float bv = __fadd_rn(acc[3 + c], a.b[3 + c]);
-                bv = fminf(fmaxf(bv, a.log_s_min), a.log_s_max);
-                float sv = expf(bv);
-                sv = fminf(fmaxf(sv, 0.5f), 64.f);
+                const float av = fminf(fmaxf(v[c], -15.f), 15.f);
+                const float mu = __fmul_rn(255.f, sigmoid_np(av));
+                const float bv = fminf(fmaxf(v[3 + c], a.log_s_min), a.log_s_max);
+                const float sv = fminf(fmaxf(np_expf(bv), 0.5f), 64.f);
                 const float fl = floorf(mu);  // round_half_away(mu), exact in f32
                 const int shift = (int)fl + (__fsub_rn(mu, fl) >= 0.5f ? 1 : 0);
                 int d = 0;  // s > t_k  <=>  s > rd32(t_k)
@@ -330,34 +371,149 @@ __global__ void __launch_bounds__(kThreads) conv_kernel(ConvArgs a) {
     }
 }
 
-size_t conv_smem(int ks, int stride, int co_t) {
-    const int IR = (kTile - 1) * stride + ks;
-    return sizeof(float) * ((size_t)kCK * IR * (IR + 1) + (size_t)ks * ks * kCK * co_t);
+// One tap's contraction in the order OpenBLAS takes for the pixels the main
+// kernel does not cover (oracle/pilc_oracle.c tap_dot): mode 1 = sgemv_t
+// (single-pixel output), mode 2 = sgemm's k-vectorised m-tail.
+__device__ float tail_dot(const ConvArgs &a, int64_t n, int tap, int co, int y, int x, int mode) {
+    const int K = a.Ci;
+    const float *w = a.w + (int64_t)tap * a.Ci_pad * a.Co_pad + co;
+    const int ws = a.Co_pad;
+    if (mode == 1) {
+        float l[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (K == 8) {
+            for (int k = 0; k < 8; ++k) l[k] = __fmul_rn(w[k * ws], conv_input(a, n, k, y, x));
+            return __fadd_rn(__fadd_rn(__fadd_rn(l[0], l[1]), __fadd_rn(l[2], l[3])),
+                             __fadd_rn(__fadd_rn(l[4], l[5]), __fadd_rn(l[6], l[7])));
+        }
+        for (int k = 0; k < K; ++k) l[k & 7] = fmaf(w[k * ws], conv_input(a, n, k, y, x), l[k & 7]);
+        return __fadd_rn(__fadd_rn(__fadd_rn(l[0], l[4]), __fadd_rn(l[1], l[5])),
+                         __fadd_rn(__fadd_rn(l[2], l[6]), __fadd_rn(l[3], l[7])));
+    }
+    float l[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) l[i] = 0.f;
+    for (int k = 0; k < K; ++k) l[k & 15] = fmaf(w[k * ws], conv_input(a, n, k, y, x), l[k & 15]);
+#pragma unroll
+    for (int m = 16; m > 1; m >>= 1)
+#pragma unroll
+        for (int i = 0; i < m / 2; ++i) l[i] = __fadd_rn(l[2 * i], l[2 * i + 1]);
+    return l[0];
 }
 
-int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s) {
-    a.tiles_x = (a.Wo + kTile - 1) / kTile;
-    a.tiles_per_img = a.tiles_x * ((a.Ho + kTile - 1) / kTile);
+__global__ void xtail_kernel(ConvArgs a, int64_t n_img, int n_tail, int mode) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = n_img * n_tail * a.Co;
+    if (i >= total) return;
+    const int co = (int)(i % a.Co);
+    const int j = (int)((i / a.Co) % n_tail);
+    const int64_t n = i / ((int64_t)a.Co * n_tail);
+    const int64_t pr = a.tail_start + j;
+    const int oy = (int)(pr / a.Wo), ox = (int)(pr % a.Wo);
+    const int pad = a.ks >> 1;
+    float o = 0.f;
+    for (int ti = 0; ti < a.ks; ++ti)
+        for (int tj = 0; tj < a.ks; ++tj) {
+            const int y = clampi(oy * a.stride + ti - pad, 0, a.Hi - 1);
+            const int x = clampi(ox * a.stride + tj - pad, 0, a.Wi - 1);
+            o = __fadd_rn(o, tail_dot(a, n, ti * a.ks + tj, co, y, x, mode));
+        }
+    a.side[(n * 8 + j) * a.Co_pad + co] = o;
+}
+
+// bank-friendly row pitch: the warp's first activation load (8 / PPT rows x
+// 16 / PPT column groups, stride st) must hit distinct banks
+int pick_pitch(int ppt, int st, int ks, int ncg) {
+    const int need = 15 * st + ks, pgr = 16 / ppt, rows = (32 / ncg) / pgr;
+    for (int ic = need; ic < need + 64; ++ic) {
+        uint64_t used = 0;
+        bool ok = true;
+        for (int r = 0; r < rows && ok; ++r)
+            for (int q = 0; q < pgr && ok; ++q) {
+                const int bank = (r * st * ic + q * st) & 31;
+                if (used >> bank & 1) ok = false;
+                used |= 1ull << bank;
+            }
+        if (ok) return ic;
+    }
+    return need;
+}
+
+size_t conv_smem(const ConvArgs &a) {
+    const int IR = (a.TR - 1) * a.stride + a.ks;
+    const int plane = (IR * a.IC) | 1;
+    const int nchunk = (a.Ci_pad + a.CK - 1) / a.CK;
+    const int wt = nchunk > 1 ? 1 : a.ks * a.ks;
+    return sizeof(float) * ((((size_t)a.CK * plane + 3) & ~(size_t)3) + (size_t)wt * a.CK * a.CO_T);
+}
+
+// Tail set of a conv layer (see the kernel comment): 0 none, 1 sgemv (single
+// output pixel), 2 sgemm m-tail; -1 when OpenBLAS's order there is not
+// modelled (the exact network then reports PILC_E_UNSUPPORTED).
+int tail_mode_of(const ConvArgs &a, int co_real, int64_t *start, int *count) {
+    const int64_t npx = (int64_t)a.Ho * a.Wo;
+    *start = INT64_MAX;
+    *count = 0;
+    if (npx == 1) {
+        if (co_real < 4 || !(a.Ci == 8 || (a.Ci >= 16 && a.Ci % 8 == 0))) return -1;
+        *start = 0;
+        *count = 1;
+        return 1;
+    }
+    const int r = (int)(npx % 16);
+    if (a.Ci >= 32 && r >= 1 && r <= 8) {
+        if (co_real < 4 && r != 4 && r != 8) return -1;
+        *start = npx - r;
+        *count = r;
+        return 2;
+    }
+    return 0;
+}
+
+// co_real: the reference's output channel count of one conv call (the
+// merged mu|s head is two Co = 3 convs)
+int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side, int co_real) {
+    const int ppt = co_t >= 16 ? 8 : 4;
+    a.CO_T = co_t;
+    const int ncg = co_t / 8;
+    const int threads_per_row = (16 / ppt) * ncg;
+    a.TR = 128 / threads_per_row;
+    if (a.stride == 2 && a.TR > 8) a.TR /= 2;
+    if (a.TR > 32) a.TR = 32;
+    a.IC = pick_pitch(ppt, a.stride, a.ks, ncg);
+    const int threads = a.TR * threads_per_row;
+    const int IR = (a.TR - 1) * a.stride + a.ks;
+    const int plane = (IR * a.IC) | 1;
+    // channels per shared-memory chunk: as many as fit in ~100 KB (2 CTAs / SM)
+    const int budget = 100 * 1024 / 4;
+    int ck = a.Ci_pad;
+    while (ck > 4 && (size_t)ck * plane + (size_t)a.ks * a.ks * ck * co_t > (size_t)budget) ck = (ck / 2 + 3) & ~3;
+    if ((size_t)ck * plane + (size_t)a.ks * a.ks * ck * co_t > (size_t)budget) {
+        while (ck > 4 && (size_t)ck * plane + (size_t)ck * co_t > (size_t)budget) ck -= 4;
+    }
+    a.CK = ck;
+    a.tiles_x = (a.Wo + 15) / 16;
+    a.tiles_per_img = a.tiles_x * ((a.Ho + a.TR - 1) / a.TR);
     const int64_t blocks = n_img * a.tiles_per_img;
     if (blocks > 0x7FFFFFFF) return PILC_E_ARG;
-    dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
-    const size_t smem = conv_smem(a.ks, a.stride, co_t);
-    // algorithmic FLOPs of this conv (true channel counts, no padding)
+    int n_tail = 0;
+    const int tmode = tail_mode_of(a, co_real, &a.tail_start, &n_tail);
+    if (tmode < 0) return PILC_E_UNSUPPORTED;
+    a.side = side;
     const double flops = 2.0 * n_img * a.Ho * a.Wo * (double)a.Co * a.Ci * a.ks * a.ks;
     ProfScope _ps(PROF_CONV, s, flops);
-    switch (co_t) {
-        case 32:
-            cudaFuncSetAttribute(conv_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            conv_kernel<32><<<grid, kThreads, smem, s>>>(a);
-            break;
-        case 16:
-            cudaFuncSetAttribute(conv_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            conv_kernel<16><<<grid, kThreads, smem, s>>>(a);
-            break;
-        default:
-            cudaFuncSetAttribute(conv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            conv_kernel<8><<<grid, kThreads, smem, s>>>(a);
-            break;
+    if (tmode > 0) {
+        const int64_t total = n_img * n_tail * a.Co;
+        xtail_kernel<<<(unsigned)ceil_div64(total, 128), 128, 0, s>>>(a, n_img, n_tail, tmode);
+        PILC_CHECK_LAUNCH();
+    }
+    const size_t smem = conv_smem(a);
+    dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
+    if (ppt == 8) {
+        cudaFuncSetAttribute(conv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        conv_kernel<8><<<grid, threads, smem, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(conv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        conv_kernel<4><<<grid, threads, smem, s>>>(a);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
@@ -532,7 +688,7 @@ int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc,
 }
 
 struct Work {
-    float *A, *B, *T, *Z;
+    float *A, *B, *T, *Z, *side;
 };
 
 int64_t ws_parts(int64_t n, int H, int W, int Dc, int C, Work *w, char *base) {
@@ -541,14 +697,17 @@ int64_t ws_parts(int64_t n, int H, int W, int Dc, int C, Work *w, char *base) {
     const int64_t a = n * He * We * (int64_t)C * 4;        // stem out / shuffled up out
     const int64_t b = n * gh * gw * (int64_t)C * 4;
     const int64_t z = n * gh * gw * (int64_t)Dc * 4;
+    const int64_t cmax = 4 * (int64_t)round_up(C > Dc ? C : Dc, 32);
+    const int64_t sd = n * 8 * cmax * 4;  // tail outputs (launch_conv)
     auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
     if (w) {
         w->A = reinterpret_cast<float *>(base);
         w->B = reinterpret_cast<float *>(base + al(a));
         w->T = reinterpret_cast<float *>(base + al(a) + al(b));
         w->Z = reinterpret_cast<float *>(base + al(a) + 2 * al(b));
+        w->side = reinterpret_cast<float *>(base + al(a) + 2 * al(b) + al(z));
     }
-    return al(a) + 2 * al(b) + al(z);
+    return al(a) + 2 * al(b) + al(z) + al(sd);
 }
 
 // tcgen05 decoder scratch: three latent slabs X, T, Y and the shuffled
@@ -818,6 +977,11 @@ extern "C" int64_t pilc_vq_workspace_bytes(int64_t n_img, int32_t H, int32_t W, 
     return m > c ? m : c;
 }
 
+extern "C" int pilc_vq_fast_decoder(int32_t K, int32_t Dc, int32_t C, int32_t B, int32_t H, int32_t W) {
+    if (H < 1 || W < 1 || !check_cfg(K, Dc, C, B)) return PILC_E_ARG;
+    return (C == 32 && tc_decoder_supported((H + 1) / 2, (W + 1) / 2, true)) ? 1 : 0;
+}
+
 extern "C" int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model, int32_t K, int32_t Dc,
                               int32_t C, int32_t B, uint8_t *idx_out, void *stream) {
     if (n_vec < 0 || !check_cfg(K, Dc, C, B)) return PILC_E_ARG;
@@ -844,7 +1008,7 @@ int simt_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const f
     a.Wo = We;
     a.relu = 1;
     a.out = w.A;
-    if ((rc = launch_conv(a, L.enc[0].co_t, n_img, s))) return rc;
+    if ((rc = launch_conv(a, L.enc[0].co_t, n_img, s, w.side, L.enc[0].co))) return rc;
     // down (3x3 stride 2) -> B
     a = base_args(model, L.enc[1]);
     a.in = w.A;
@@ -855,7 +1019,7 @@ int simt_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const f
     a.Wo = gw;
     a.relu = 1;
     a.out = w.B;
-    if ((rc = launch_conv(a, L.enc[1].co_t, n_img, s))) return rc;
+    if ((rc = launch_conv(a, L.enc[1].co_t, n_img, s, w.side, L.enc[1].co))) return rc;
     for (int i = 0; i < B; ++i) {
         a = base_args(model, L.enc[2 + 2 * i]);
         a.in = w.B;
@@ -863,7 +1027,7 @@ int simt_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const f
         a.Wi = a.Wo = gw;
         a.relu = 1;
         a.out = w.T;
-        if ((rc = launch_conv(a, L.enc[2 + 2 * i].co_t, n_img, s))) return rc;
+        if ((rc = launch_conv(a, L.enc[2 + 2 * i].co_t, n_img, s, w.side, L.enc[2 + 2 * i].co))) return rc;
         a = base_args(model, L.enc[3 + 2 * i]);
         a.in = w.T;
         a.Hi = a.Ho = gh;
@@ -871,7 +1035,7 @@ int simt_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const f
         a.resid = w.B;  // relu(x + conv2(h)), written in place over x
         a.relu = 1;
         a.out = w.B;
-        if ((rc = launch_conv(a, L.enc[3 + 2 * i].co_t, n_img, s))) return rc;
+        if ((rc = launch_conv(a, L.enc[3 + 2 * i].co_t, n_img, s, w.side, L.enc[3 + 2 * i].co))) return rc;
     }
     float *z = z_out ? z_out : w.Z;
     a = base_args(model, L.enc[2 + 2 * B]);
@@ -879,7 +1043,7 @@ int simt_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const f
     a.Hi = a.Ho = gh;
     a.Wi = a.Wo = gw;
     a.out = z;
-    if ((rc = launch_conv(a, L.enc[2 + 2 * B].co_t, n_img, s))) return rc;
+    if ((rc = launch_conv(a, L.enc[2 + 2 * B].co_t, n_img, s, w.side, L.enc[2 + 2 * B].co))) return rc;
     return launch_argmin(z, n_img * gh * gw, model + L.cb_off, K, Dc, idx_out, s);
 }
 
@@ -1033,17 +1197,18 @@ int vq_encode(int path, const uint8_t *img, int64_t n_img, int32_t H, int32_t W,
 
 }  // namespace
 
-// Production encoder: 3xTF32 tcgen05 block convs when C == Dc == 32 (the
-// default model), fp32 SIMT otherwise. Index parity needs fp32-class z; the
-// argmin itself is exact given z.
+// Fast encoder: fp16-split (fp32-class) tcgen05 convs when C == Dc == 32,
+// else the exact network. Index parity needs fp32-class z; the argmin itself
+// is exact given z.
 extern "C" int pilc_vq_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model,
                               int32_t K, int32_t Dc, int32_t C, int32_t B, void *workspace,
                               int64_t ws_bytes, uint8_t *idx_out, float *z_out, void *stream) {
     return vq_encode(0, img, n_img, H, W, model, K, Dc, C, B, workspace, ws_bytes, idx_out, z_out, stream);
 }
 
-// fp32 SIMT encoder for any configuration (validation reference).
-extern "C" int pilc_vq_encode_simt(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model,
+// The exact network (the reference's float arithmetic): z bit-identical to
+// the reference's, so indices are too.
+extern "C" int pilc_vq_encode_exact(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model,
                                    int32_t K, int32_t Dc, int32_t C, int32_t B, void *workspace,
                                    int64_t ws_bytes, uint8_t *idx_out, float *z_out, void *stream) {
     return vq_encode(1, img, n_img, H, W, model, K, Dc, C, B, workspace, ws_bytes, idx_out, z_out, stream);
@@ -1065,7 +1230,7 @@ int simt_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mo
     a.Wi = a.Wo = gw;
     a.relu = 1;
     a.out = w.B;
-    rc = launch_conv(a, L.dec[0].co_t, n_img, s);
+    rc = launch_conv(a, L.dec[0].co_t, n_img, s, w.side, L.dec[0].co);
     for (int i = 0; !rc && i < B; ++i) {
         a = base_args(model, L.dec[1 + 2 * i]);
         a.in = w.B;
@@ -1073,7 +1238,7 @@ int simt_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mo
         a.Wi = a.Wo = gw;
         a.relu = 1;
         a.out = w.T;
-        rc = launch_conv(a, L.dec[1 + 2 * i].co_t, n_img, s);
+        rc = launch_conv(a, L.dec[1 + 2 * i].co_t, n_img, s, w.side, L.dec[1 + 2 * i].co);
         if (rc) break;
         a = base_args(model, L.dec[2 + 2 * i]);
         a.in = w.T;
@@ -1082,7 +1247,7 @@ int simt_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mo
         a.resid = w.B;
         a.relu = 1;
         a.out = w.B;
-        rc = launch_conv(a, L.dec[2 + 2 * i].co_t, n_img, s);
+        rc = launch_conv(a, L.dec[2 + 2 * i].co_t, n_img, s, w.side, L.dec[2 + 2 * i].co);
     }
     if (!rc) {  // up (3x3 C -> 4C) + pixel shuffle + ReLU -> A (2gh x 2gw x C)
         a = base_args(model, L.dec[1 + 2 * B]);
@@ -1091,7 +1256,7 @@ int simt_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mo
         a.Wi = a.Wo = gw;
         a.out_mode = OUT_SHUFFLE;
         a.out = w.A;
-        rc = launch_conv(a, L.dec[1 + 2 * B].co_t, n_img, s);
+        rc = launch_conv(a, L.dec[1 + 2 * B].co_t, n_img, s, w.side, L.dec[1 + 2 * B].co);
     }
     if (!rc) {  // heads (3x3 C -> mu|s) + logistic head, cropped to H x W
         a = base_args(model, L.dec[2 + 2 * B]);
@@ -1109,7 +1274,7 @@ int simt_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mo
         a.n_thresh = D - 1;
         a.log_s_min = (float)log(0.5);
         a.log_s_max = (float)log(64.0);
-        rc = launch_conv(a, L.dec[2 + 2 * B].co_t, n_img, s);
+        rc = launch_conv(a, L.dec[2 + 2 * B].co_t, n_img, s, w.side, 3);
     }
     return rc;
 }
@@ -1119,7 +1284,7 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
               float *s_out, cudaStream_t s) {
     const int gh = (H + 1) / 2, gw = (W + 1) / 2;
     const uint16_t *hb = reinterpret_cast<const uint16_t *>(model);
-    const bool pairs = g_tuning[PILC_TUNE_HEAD_PAIRS] != 0;
+    const bool pairs = true;
     int rc = tc_dec_table(model + L.cb_off, model + L.dec[0].w_off, model + L.dec[0].b_off, K, Dc, L.dec[0].ci_pad,
                           L.dec[0].co_pad, tw.table, s);
     bool trunk_done = false;
@@ -1223,7 +1388,7 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
         hd.n_thresh = D - 1;
         hd.log_s_min = (float)log(0.5);
         hd.log_s_max = (float)log(64.0);
-        rc = pairs ? tc_launch_head2(hd, s) : tc_launch_head(hd, s);
+        rc = tc_launch_head2(hd, s);
     }
     return rc;
 }
@@ -1235,34 +1400,39 @@ int vq_decode(int path, const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
     if (D > 1 && !d_thresh) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     const Layout L = make_layout(K, Dc, C, B);
-    const bool use_tc = path == 0 && L.tc;
-    Work w;
-    TcWork tw;
-    if (use_tc) {
-        if (tc_ws(n_img, H, W, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-    } else if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) {
-        return PILC_E_ARG;
-    }
+    const int gh = (H + 1) / 2, gw = (W + 1) / 2;
     cudaStream_t s = as_stream(stream);
     const double *thr = d_thresh;
-    int rc = use_tc ? tc_decode(idx, n_img, H, W, model, L, K, Dc, B, thr, D, tw, shift_out, d_out, mu_out, s_out,
-                                s)
-                    : simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
-    if (use_tc && rc == PILC_E_UNSUPPORTED) {
-        // too wide for the tcgen05 tiles: the SIMT decoder. The choice is a
-        // function of (model config, H, W) only, so compress and decompress
-        // always agree.
-        if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-        rc = simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
+    if (path == 0 && L.tc && tc_decoder_supported(gh, gw, true)) {
+        // the tcgen05 decoder, in batches below its 32-bit pixel-index limit
+        // (largest slab: the (2gh + 2) x (2gw + 2) hi-res one), so the path
+        // depends on (model config, H, W) only
+        const int64_t per = (int64_t)(2 * gh + 2) * (2 * gw + 2);
+        const int64_t cap = ((int64_t)1 << 31) / per - 1;
+        if (cap < 1) return PILC_E_UNSUPPORTED;
+        TcWork tw;
+        if (tc_ws(n_img < cap ? n_img : cap, H, W, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+        const int64_t px = (int64_t)H * W * 3;
+        for (int64_t i0 = 0; i0 < n_img; i0 += cap) {
+            const int64_t nb = n_img - i0 < cap ? n_img - i0 : cap;
+            if (i0) tc_ws(nb, H, W, &tw, (char *)workspace);
+            const int rc = tc_decode(idx + i0 * gh * gw, nb, H, W, model, L, K, Dc, B, thr, D, tw, shift_out + i0 * px,
+                                     d_out + i0 * px, mu_out ? mu_out + i0 * px : nullptr,
+                                     s_out ? s_out + i0 * px : nullptr, s);
+            if (rc) return rc;
+        }
+        return PILC_OK;
     }
-    return rc;
+    Work w;
+    if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+    return simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
 }
 
 }  // namespace
 
-// The production decoder: tcgen05 bf16 when C == 32 (the default model),
-// else the SIMT fp32 kernels. The choice depends only on the model
-// configuration, so compress and decompress always take the same path.
+// The fast decoder: tcgen05 bf16 when C == 32 and the shape fits its tiles
+// (pilc_vq_fast_decoder), else the exact network. The choice depends only on
+// (model config, H, W); containers record it (container.py FLAG_FAST_DECODER).
 extern "C" int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
                               int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh,
                               int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
@@ -1271,8 +1441,9 @@ extern "C" int pilc_vq_decode(const uint8_t *idx, int64_t n_img, int32_t H, int3
                      mu_out, s_out, stream);
 }
 
-// fp32 SIMT decoder for any configuration (validation reference).
-extern "C" int pilc_vq_decode_simt(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
+// The exact network: the reference's float arithmetic (see conv_kernel),
+// any configuration.
+extern "C" int pilc_vq_decode_exact(const uint8_t *idx, int64_t n_img, int32_t H, int32_t W, const float *model,
                                    int32_t K, int32_t Dc, int32_t C, int32_t B, const double *d_thresh,
                                    int32_t D, void *workspace, int64_t ws_bytes, uint8_t *shift_out,
                                    uint8_t *d_out, float *mu_out, float *s_out, void *stream) {

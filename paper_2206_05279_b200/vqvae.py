@@ -48,24 +48,26 @@ def _workspace(n: int, H: int, W: int, weights: ModelWeights, dev) -> torch.Tens
 
 
 def encode_indices_device(img_d: torch.Tensor, weights: ModelWeights, dev, stream, z_out=None,
-                          precise: bool = False) -> torch.Tensor:
-    """Production encoder (3xTF32 tcgen05 for the default C=Dc=32 model);
-    precise=True selects the fp32 SIMT kernels."""
+                          exact: bool = True) -> torch.Tensor:
+    """exact=True: the exact network (the reference's float arithmetic, z
+    bit-identical); exact=False: the fast encoder (fp16-split tcgen05 for the
+    default C=Dc=32 model, else the exact network)."""
     N, H, W, _ = img_d.shape
     gh, gw = latent_shape(H, W)
     idx = torch.empty((N, gh, gw), dtype=torch.uint8, device=dev)
     ws = _workspace(N, H, W, weights, dev)
-    _lib.call("pilc_vq_encode_simt" if precise else "pilc_vq_encode", ptr(img_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
+    _lib.call("pilc_vq_encode_exact" if exact else "pilc_vq_encode", ptr(img_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
               ptr(ws), ws.numel(), ptr(idx), ptr(z_out), sptr(stream))
     return idx
 
 
 def decode_head_device(idx_d: torch.Tensor, weights: ModelWeights, H: int, W: int, grid: ScaleGrid, dev, stream,
-                       want_params: bool = False, precise: bool = False, out=None):
+                       want_params: bool = False, exact: bool = True, out=None):
     """-> (shift u8, d u8[, mu f32, s f32]) each (N, H, W, 3).
 
-    The codec path uses the production decoder (tcgen05 bf16 for the
-    default C=32 model); precise=True selects the fp32 SIMT kernels.
+    exact=True: the exact network (mu, s bit-identical to the reference's
+    decode_to_params); exact=False: the fast decoder (tcgen05 bf16 when
+    container.fast_decoder(model, H, W), else the exact network).
     out=(shift, dsel): contiguous (N, H, W, 3) uint8 tensors to fill (e.g.
     row slices of a batch-sized pair)."""
     N = idx_d.shape[0]
@@ -81,23 +83,23 @@ def decode_head_device(idx_d: torch.Tensor, weights: ModelWeights, H: int, W: in
         s = torch.empty((N, H, W, 3), dtype=torch.float32, device=dev)
     thr = grid_device(grid, dev)[1]
     ws = _workspace(N, H, W, weights, dev)
-    _lib.call("pilc_vq_decode_simt" if precise else "pilc_vq_decode", ptr(idx_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
+    _lib.call("pilc_vq_decode_exact" if exact else "pilc_vq_decode", ptr(idx_d), N, H, W, ptr(weights.device_model(dev)), *weights.cfg_tuple(),
               ptr(thr), grid.D, ptr(ws), ws.numel(), ptr(shift), ptr(dsel), ptr(mu), ptr(s),
               sptr(stream))
     return (shift, dsel, mu, s) if want_params else (shift, dsel)
 
 
-def encode_to_indices(image, weights: ModelWeights, *, precise: bool = False) -> np.ndarray:
+def encode_to_indices(image, weights: ModelWeights, *, exact: bool = True) -> np.ndarray:
     """Nearest-codebook index per latent; ties take the smaller index."""
     validate_image(image)
     _require_network(weights)
     dev = require_device()
     stream = torch.cuda.current_stream(dev)
     img_d = as_device_u8(np.asarray(image)[None], dev, stream)
-    return encode_indices_device(img_d, weights, dev, stream, precise=precise)[0].cpu().numpy()
+    return encode_indices_device(img_d, weights, dev, stream, exact=exact)[0].cpu().numpy()
 
 
-def encoder_latents(image, weights: ModelWeights, *, precise: bool = False) -> np.ndarray:
+def encoder_latents(image, weights: ModelWeights, *, exact: bool = True) -> np.ndarray:
     """Pre-argmin latents z (gh, gw, Dc) float32 (testing hook)."""
     validate_image(image)
     _require_network(weights)
@@ -107,7 +109,7 @@ def encoder_latents(image, weights: ModelWeights, *, precise: bool = False) -> n
     gh, gw = latent_shape(H, W)
     z = torch.empty((1, gh, gw, weights.config.Dc), dtype=torch.float32, device=dev)
     img_d = as_device_u8(np.asarray(image)[None], dev, stream)
-    encode_indices_device(img_d, weights, dev, stream, z_out=z, precise=precise)
+    encode_indices_device(img_d, weights, dev, stream, z_out=z, exact=exact)
     return z[0].cpu().numpy()
 
 
@@ -123,9 +125,10 @@ def argmin_codebook(z, weights: ModelWeights) -> np.ndarray:
     return out.cpu().numpy().reshape(z.shape[:-1])
 
 
-def decode_to_params(indices, weights: ModelWeights, out_shape: tuple[int, int], *, precise: bool = False):
-    """Per-pixel (mu, s) planes H x W x 3 float32, computed on the GPU by
-    the production decoder (precise=True: fp32 SIMT kernels)."""
+def decode_to_params(indices, weights: ModelWeights, out_shape: tuple[int, int], *, exact: bool = True):
+    """Per-pixel (mu, s) planes H x W x 3 float32, computed on the GPU by the
+    exact network (bit-identical to the reference's) or, exact=False, by the
+    fast decoder."""
     _require_network(weights)
     H, W = out_shape
     gh, gw = latent_shape(H, W)
@@ -138,7 +141,7 @@ def decode_to_params(indices, weights: ModelWeights, out_shape: tuple[int, int],
     stream = torch.cuda.current_stream(dev)
     idx_d = torch.from_numpy(indices.astype(np.uint8)[None].copy()).to(dev)
     _, _, mu, s = decode_head_device(idx_d, weights, H, W, default_grid(), dev, stream, want_params=True,
-                                     precise=precise)
+                                     exact=exact)
     return mu[0].cpu().numpy(), s[0].cpu().numpy()
 
 

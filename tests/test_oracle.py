@@ -129,3 +129,70 @@ def test_corruption_detected(golden):
     with pytest.raises(O.OracleError) as e:
         O.decompress(bytes(blob))
     assert e.value.kind == "CorruptStreamError"
+
+
+# --- the explicit statement of the reference's float arithmetic ---------------
+# (oracle_conv_fma / oracle_expf_np: what the GPU exact network implements)
+
+
+@pytest.mark.parametrize("tag", ["small", "full"])
+def test_fma_statement_reproduces_reference_network(golden, tag):
+    """The reference's own z, mu, s (tests/golden, made by pixelcodec) equal
+    the explicit FMA-chain / sgemv / m-tail / numpy-exp statement bit for bit."""
+    import paper_2206_05279_b200 as pc
+
+    z = golden(f"vqvae_{tag}.npz")
+    if tag == "small":
+        m = O.Model.from_bytes(golden("small.pilw"))
+    else:
+        m = O.Model.from_bytes(pc.random_weights(pc.ModelConfig(), seed=1).to_bytes())
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        H, W = img.shape[:2]
+        assert np.array_equal(O.encoder_latents_exact(img, m).view(np.uint32), z[f"z{k}"].view(np.uint32))
+        mu, s = O.decode_params_exact(z[f"idx{k}"], m, H, W)
+        assert np.array_equal(mu.view(np.uint32), z[f"mu{k}"].view(np.uint32))
+        assert np.array_equal(s.view(np.uint32), z[f"s{k}"].view(np.uint32))
+
+
+def test_conv_statement_matches_numpy_blas():
+    """oracle_conv_fma against the reference's nn.conv2d arithmetic (numpy +
+    OpenBLAS, restated op for op by O.conv2d) on random layers of every shape
+    class: plain, m-tail (1..8 leftover pixels, Ci >= 32), single pixel."""
+    rng = np.random.default_rng(5)
+    checked = 0
+    for ci, co in ((3, 32), (8, 8), (32, 32), (32, 128), (32, 3), (8, 3), (40, 16)):
+        for H, W in ((1, 1), (1, 2), (2, 2), (1, 7), (3, 3), (4, 5), (6, 11), (9, 7), (16, 17), (2, 14)):
+            for ks, st in ((3, 1), (3, 2), (1, 1)):
+                x = rng.standard_normal((ci, H, W)).astype(np.float32)
+                w = rng.standard_normal((co, ci, ks, ks)).astype(np.float32)
+                b = rng.standard_normal(co).astype(np.float32)
+                try:
+                    got = O.conv2d_fma(x, w, b, st)
+                except NotImplementedError:
+                    continue
+                assert np.array_equal(got.view(np.uint32), O.conv2d(x, w, b, st).view(np.uint32)), (ci, co, H, W, ks, st)
+                checked += 1
+    assert checked > 150
+
+
+@pytest.mark.parametrize("lo,hi", [(-15.0, 15.0), (float(np.float32(np.log(0.5))), float(np.float32(np.log(64.0))))])
+def test_exp_statement_matches_numpy(lo, hi):
+    """oracle_expf_np equals np.exp (float32) on the head's input ranges:
+    every float32 in [lo, hi] at a stride of 61 bit patterns (~3.5e7 values)."""
+    def f32_range(a, b):
+        # float32 bit patterns of [a, b] (sign-magnitude: handle each sign)
+        out = []
+        a32, b32 = np.float32(a), np.float32(b)
+        if a32 < 0:
+            top = np.array([-a32], np.float32).view(np.uint32)[0]
+            lo_b = np.array([max(0.0, -b32)], np.float32).view(np.uint32)[0] if b32 < 0 else 0
+            out.append((np.arange(lo_b, top + 1, 61, dtype=np.uint32) | np.uint32(0x80000000)).view(np.float32))
+        if b32 >= 0:
+            lo_b = np.array([max(0.0, a32)], np.float32).view(np.uint32)[0]
+            top = np.array([b32], np.float32).view(np.uint32)[0]
+            out.append(np.arange(lo_b, top + 1, 61, dtype=np.uint32).view(np.float32))
+        return np.concatenate(out)
+
+    x = f32_range(lo, hi)
+    assert np.array_equal(O.exp_np(x).view(np.uint32), np.exp(x).view(np.uint32))

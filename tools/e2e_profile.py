@@ -6,7 +6,7 @@ import paper_2206_05279_b200 as pc
 from paper_2206_05279_b200 import container as ct, device as dv
 from paper_2206_05279_b200.synth import smooth_images
 dev = torch.device("cuda", 0); stream = torch.cuda.current_stream(dev)
-model = pc.random_weights(seed=1); cfg = pc.CodecConfig(backend="twar-vqvae")
+model = pc.random_weights(seed=1); cfg = pc.CodecConfig(backend="twar-vqvae", numerics="fast")
 imgs = smooth_images(8192, 32, 32, seed=0)
 for _ in range(3):
     buf, off = pc.compress_batch(imgs, model, cfg); out = pc.decompress_batch(buf, off, model)

@@ -8,7 +8,7 @@ from paper_2206_05279_b200.synth import smooth_images
 dev = torch.device("cuda", 0)
 stream = torch.cuda.current_stream(dev)
 model = pc.random_weights(seed=1)
-cfg = pc.CodecConfig(backend="twar-vqvae")
+cfg = pc.CodecConfig(backend="twar-vqvae", numerics="fast")
 imgs = smooth_images(8192, 32, 32, seed=0)
 img_d = torch.from_numpy(imgs).to(dev)
 def step():

@@ -8,7 +8,8 @@ from paper_2206_05279_b200.synth import smooth_images
 H = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 dev = torch.device("cuda", 0); stream = torch.cuda.current_stream(dev)
-model = pc.random_weights(seed=1); cfg = pc.CodecConfig(backend="twar-vqvae")
+NUM = sys.argv[3] if len(sys.argv) > 3 else "fast"
+model = pc.random_weights(seed=1); cfg = pc.CodecConfig(backend="twar-vqvae", numerics=NUM)
 img_d = torch.from_numpy(smooth_images(N, H, H, seed=0)).to(dev)
 def step():
     o, off = ct._compress_device(img_d, model, cfg, dev, stream)
