@@ -129,6 +129,14 @@ def _flags(backend: int, cfg: CodecConfig, model, W: int, H: int) -> int:
     return flags
 
 
+def _check_lane_size(n_sym: int, L: int, M: int) -> None:
+    """The GPU coder keeps lane bit positions in 32 bits: a lane of
+    ceil(n_sym / L) symbols at up to M bits each must stay below 2^31 bits."""
+    if -(-n_sym // L) * M >= 1 << 31:
+        raise ParameterError(f"{n_sym} symbols in {L} lane(s) exceed the GPU coder's 2^31-bit lane limit; "
+                             "use more lanes")
+
+
 def _template(backend: int, cfg: CodecConfig, W: int, H: int, params: PredictorParams,
               model: ModelWeights | None) -> bytes:
     flags = _flags(backend, cfg, model, W, H)
@@ -151,6 +159,7 @@ def _compress_device(img_d: torch.Tensor, model, config: CodecConfig, dev, strea
     M, L, grid = config.M, config.lanes, config.grid
     if grid.D > 256:
         raise ParameterError("the GPU path carries distribution indices as uint8 (grid D <= 256)")
+    _check_lane_size(H * W * 3, L, M)
     params = _params_of(model)
     t_d = forward_residual_device(img_d, params, stream)
     res_enc, _ = build_tables(residual_distributions(grid, M), M, verify=config.verify_tables)
@@ -530,8 +539,14 @@ def _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host=None, offs_
         else:
             ng = ids.size
             ids_d = torch.from_numpy(ids.astype(np.int64)).to(dev)
-        _, res_dec = build_tables(residual_distributions(grid, M), M)
         n_sym = H * W * 3
+        try:
+            _check_lane_size(n_sym, L, M)
+        except ParameterError as e:
+            for i in (range(n) if ids is None else ids):
+                errors[int(i)] = e
+            continue
+        _, res_dec = build_tables(residual_distributions(grid, M), M)
         shift = dsel = d_img = None
         lane_st = {}
         if backend == BACKEND_VQVAE:
@@ -620,6 +635,20 @@ def _resolve_errors(results, errors, hdr):
     return errors
 
 
+def check_offsets(offsets) -> np.ndarray:
+    """Blob offsets as uint64[N+1]: one-dimensional and non-decreasing (the
+    parse kernel trusts them for its bounds), else FormatError."""
+    offs = np.asarray(offsets)
+    if offs.ndim != 1 or offs.size < 1:
+        raise FormatError("blob offsets must be a one-dimensional array of N+1 positions")
+    if offs.dtype.kind == "i" and (offs < 0).any():
+        raise FormatError("blob offsets must be non-negative")
+    offs = np.ascontiguousarray(offs, dtype=np.uint64)
+    if offs.size > 1 and (offs[1:] < offs[:-1]).any():
+        raise FormatError("blob offsets must be non-decreasing")
+    return offs
+
+
 def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=None,
                      raise_on_error: bool = True):
     """Decode blobs buffer[offsets[i]:offsets[i+1]]. Returns an
@@ -627,16 +656,14 @@ def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=
     raise_on_error=False returns (images, {blob index: exception})."""
     dev = require_device(device)
     stream = torch.cuda.current_stream(dev)
-    offs = np.ascontiguousarray(offsets, dtype=np.uint64)
+    offs = check_offsets(offsets)
     n = offs.size - 1
     buf_host = np.frombuffer(buffer, np.uint8) if isinstance(buffer, (bytes, bytearray, memoryview)) \
         else np.ascontiguousarray(buffer, dtype=np.uint8)
     if n <= 0:
         return (np.zeros((0, 1, 1, 3), np.uint8), {}) if not raise_on_error else np.zeros((0, 1, 1, 3), np.uint8)
-    base = int(offs[0])
-    if base or int(offs[-1]) > buf_host.size:
-        if int(offs[-1]) > buf_host.size:
-            raise FormatError("container truncated")
+    if int(offs[-1]) > buf_host.size:
+        raise FormatError("container truncated")
     buf_d = h2d(buf_host[: int(offs[-1])], dev, stream, pad=16)
     off_d = h2d(offs.view(np.uint8), dev, stream).view(torch.int64)
     results, errors, hdr = _decompress_device(buf_d, off_d, n, model, dev, stream, buf_host, offs)

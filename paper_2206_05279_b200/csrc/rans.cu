@@ -438,6 +438,8 @@ extern "C" int pilc_rans_encode(const uint8_t *syms, const uint8_t *shift, const
     if (n_img < 0 || n_sym < 0 || lanes < 1 || M < 2 || M > 12 || D < 1 || X < 1 || X > 256)
         return PILC_E_ARG;
     const int64_t per_lane = ceil_div64(n_sym, lanes);
+    // lane bit positions and counts are 32-bit (< 2^31 bits per lane)
+    if (per_lane * M >= ((int64_t)1 << 31)) return PILC_E_ARG;
     if (lane_cap < (per_lane * M + 31) / 32 + 1) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     const int64_t tab_bytes = (int64_t)D * X * 4;
@@ -473,6 +475,8 @@ extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, co
                                 int32_t M, const uint8_t *unshift, uint8_t *out, uint8_t *lane_status,
                                 void *stream) {
     if (n_img < 0 || n_sym < 0 || lanes < 1 || M < 2 || M > 12 || D < 1) return PILC_E_ARG;
+    // lane bit positions are 32-bit: a valid lane holds <= M bits per symbol
+    if (ceil_div64(n_sym, lanes) * M >= ((int64_t)1 << 31)) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     const int64_t tab_bytes = ((int64_t)D << M) * 4;
     const int in_smem = tab_bytes <= kSmemTableMax;

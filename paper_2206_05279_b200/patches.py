@@ -13,7 +13,9 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .container import CodecConfig, SpeculationMiss, _decompress_device, _resolve_errors, _verify, compress_batch
+from .container import (CodecConfig, SpeculationMiss, _decompress_device, _resolve_errors, _verify, check_offsets,
+                        compress_batch)
+from .errors import FormatError
 from .device import h2d, pinned, require_device
 
 
@@ -130,11 +132,14 @@ def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None
     dev = require_device(device)
     stream = torch.cuda.current_stream(dev)
     buffer = np.asarray(buffer, dtype=np.uint8)
-    offsets = np.asarray(offsets, dtype=np.uint64)
+    offsets = check_offsets(offsets)
     groups = _groups(H, W, ph, pw)
     ridx = _raster_index(H, W, ph, pw)
     per = sum(len(r) for r in ridx)
     F = n_frames
+    if offsets.size != F * per + 1 or int(offsets[-1]) > buffer.size:
+        raise FormatError(f"expected {F * per + 1} blob offsets within the buffer for {F} frame(s) of "
+                          f"{per} patches")
     buf_d = h2d(buffer[: int(offsets[F * per])], dev, stream)
     frames_d = torch.empty((F, H, W, 3), dtype=torch.uint8, device=dev)
     with torch.cuda.stream(stream):

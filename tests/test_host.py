@@ -187,3 +187,28 @@ def test_synth_mulberry32_matches_reference_generator():
     assert np.allclose(mulberry32(7, 0, 50), scalar(7, 50), rtol=0, atol=0)
     imgs = smooth_images(2, 8, 12, seed=3)
     assert imgs.shape == (2, 8, 12, 3) and imgs.dtype == np.uint8
+
+
+def test_offsets_validation():
+    """decompress_batch / decompress_frames validate blob offsets before any
+    device work (the parse kernel trusts them): one-dimensional,
+    non-negative, non-decreasing."""
+    from paper_2206_05279_b200.container import check_offsets
+    from paper_2206_05279_b200.errors import FormatError
+
+    assert check_offsets([0, 5, 5, 9]).dtype == np.uint64
+    for bad in ([[0, 1], [1, 2]], [0, 7, 3], [-1, 4], []):
+        with pytest.raises(FormatError):
+            check_offsets(np.array(bad))
+
+
+def test_lane_size_limit():
+    """The GPU coder's lane bit positions are 32-bit: compress refuses lanes
+    that could exceed 2^31 bits (and tells the caller to use more lanes)."""
+    from paper_2206_05279_b200.container import _check_lane_size
+    from paper_2206_05279_b200.errors import ParameterError
+
+    _check_lane_size(3 * 4096 * 4096, 1, 12)
+    with pytest.raises(ParameterError, match="more lanes"):
+        _check_lane_size(3 * 8192 * 8192, 1, 12)
+    _check_lane_size(3 * 8192 * 8192, 2, 12)
