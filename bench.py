@@ -4,17 +4,33 @@
 Workload (BASELINE.json configs[1]): CIFAR10-shaped 32x32x3 synthetic
 "smooth" images (trainer data.ts generator, seed = rank), batch 8192 per GPU,
 twar-vqvae backend, full model random_weights(ModelConfig(), seed=1)
-(K=256, Dc=32, C=32, B=4), M=12, one lane per stream.
+(K=256, Dc=32, C=32, B=4), M=12, one lane per stream, numerics="fast"
+(tcgen05 network; bits/dim within 0.5% of the reference, checked in the
+same line).
 
 One step = compress_batch of the whole batch + decompress_batch of the
 resulting blobs. `value` = raw MB (1e6 B) per step x ranks / max-over-ranks
 step time, measured with CUDA events on the launching stream with the
 images already resident in HBM; L2 is flushed (256 MiB write) before each
 timed step. `e2e` is the same metric through the public host API
-(pinned host images in, host blobs out, host blobs in, host images out).
+(pageable host images in, host blobs out, host blobs in, host images out).
 Images/patches shard across GPUs with no data-path collective ("weak").
 
+The same line carries
+  in64      configs[2] (ImageNet64 x 4096 per GPU): compress / decompress
+            MB/s on device and end to end -- the north-star decompress rate;
+  exact     the same CIFAR round trip with numerics="exact" (the
+            reference's float arithmetic: containers byte-identical to
+            pixelcodec's);
+  parity    bits/dim of this run against the reference's on the same images
+            (the reference itself, baseline/_ref, on a sample), codebook
+            index agreement, and the fraction of exact containers that are
+            byte-identical to the reference's;
+  cpu_baseline  the reference (pixelcodec, baseline/_ref) round trip on all
+            host cores on a sample of the same images.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    (--gpus N > 1 without torchrun relaunches itself under torchrun)
 """
 
 from __future__ import annotations
@@ -33,15 +49,16 @@ sys.path.insert(0, REPO)
 
 BATCH = 8192
 H = W = 32
-WORKLOAD = "cifar10-32x32x3-synthetic-smooth, batch 8192/GPU, twar-vqvae full model (K256 Dc32 C32 B4, seed 1), M=12, L=1"
+WORKLOAD = ("cifar10-32x32x3-synthetic-smooth, batch 8192/GPU, twar-vqvae full model (K256 Dc32 C32 B4, seed 1), "
+            "M=12, L=1, numerics fast")
 METRIC = "PILC round-trip (compress+decompress) raw-image MB/s"
 # BASELINE.json configs: [1] is the default line; the others are --workload
 WORKLOADS = {
     "cifar": dict(H=32, W=32, N=8192, desc=WORKLOAD),
     "in64": dict(H=64, W=64, N=4096, desc="imagenet64-64x64x3-synthetic-smooth, batch 4096/GPU, twar-vqvae full "
-                                          "model (seed 1), M=12, L=1"),
+                                          "model (seed 1), M=12, L=1, numerics fast"),
     "1080p": dict(H=1080, W=1920, N=8, desc="1920x1080x3 synthetic-smooth frames, 8/GPU, split into 64x64 patch "
-                                           "containers (510/frame), twar-vqvae full model (seed 1), M=12, L=1"),
+                                           "containers (510/frame), twar-vqvae full model (seed 1), M=12, L=1, numerics fast"),
 }
 
 
@@ -53,33 +70,113 @@ def _dist():
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle leg (cpu_baseline and --impl reference)
+# CPU legs: the reference itself (pixelcodec from baseline/_ref) and the
+# oracle port. Only this file's CPU legs and tests/ execute either.
+
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+CPU_ENV = {"OPENBLAS_NUM_THREADS": "1", "OMP_NUM_THREADS": "1", "MKL_NUM_THREADS": "1", "NUMBA_NUM_THREADS": "1",
+           "PYTHONDONTWRITEBYTECODE": "1", "NUMBA_CACHE_DIR": "/tmp/pilc_numba_cache"}
 
 
-def _cpu_worker(args):
-    seed, count, model_bytes = args
-    import numpy as np  # noqa: F401  (threads pinned by the parent's env)
+def _ref_worker(args):
+    """One process (one core) of the reference arm: pixelcodec.compress +
+    decompress of each image (the reference's public API, unmodified), the
+    full model built by pixelcodec.weights.random_weights(seed=1). Returns
+    (raw bytes, seconds, blob bytes per image, blobs if asked)."""
+    imgs, keep = args
+    sys.path.insert(0, REF_DIR)
+    import numpy as np
+
+    import pixelcodec
+    from pixelcodec.weights import ModelConfig, random_weights
+
+    m = random_weights(ModelConfig(), seed=1)
+    cfg = pixelcodec.CodecConfig(backend="twar-vqvae")
+    pixelcodec.decompress(pixelcodec.compress(imgs[0][:8, :8], m, cfg), m)  # numba JIT warm-up
+    t0 = time.perf_counter()
+    sizes, blobs = [], []
+    for im in imgs:
+        blob = pixelcodec.compress(im, m, cfg)
+        out = pixelcodec.decompress(blob, m)
+        assert np.array_equal(out, im)
+        sizes.append(len(blob))
+        if keep:
+            blobs.append(blob)
+    return int(sum(im.size for im in imgs)), time.perf_counter() - t0, sizes, blobs
+
+
+def _port_worker(args):
+    imgs, model_bytes = args
+    import numpy as np
 
     from oracle import oracle as O
-    from paper_2206_05279_b200.synth import smooth_images
 
-    imgs = smooth_images(count, H, W, seed=seed)
     m = O.Model.from_bytes(model_bytes)
     O.compress(imgs[0], m, "twar-vqvae")  # warm tables + C library
     t0 = time.perf_counter()
-    nbytes = 0
     for im in imgs:
-        blob = O.compress(im, m, "twar-vqvae")
-        out = O.decompress(blob, m)
-        assert (out == im).all()
-        nbytes += im.size
-    return nbytes, time.perf_counter() - t0
+        assert np.array_equal(O.decompress(O.compress(im, m, "twar-vqvae"), m), im)
+    return int(sum(im.size for im in imgs)), time.perf_counter() - t0
+
+
+def _cpu_pool(procs: int):
+    import multiprocessing as mp
+
+    for k, v in CPU_ENV.items():  # before any child imports numpy / numba
+        os.environ[k] = v
+    return mp.get_context("spawn").Pool(procs)
+
+
+def cpu_reference_run(imgs, procs: int, keep: bool = False, pool=None):
+    """Round trip of `imgs` split over `procs` reference processes. MB/s is
+    raw bytes over the slowest process's own timed loop (after its JIT
+    warm-up). Returns (MB/s, raw bytes, seconds, sizes, blobs)."""
+    own = pool is None
+    pool = pool or _cpu_pool(procs)
+    try:
+        chunks = [imgs[i::procs] for i in range(procs)]
+        res = pool.map(_ref_worker, [(c, keep) for c in chunks if len(c)])
+    finally:
+        if own:
+            pool.close()
+    wall = max(r[1] for r in res)
+    nbytes = sum(r[0] for r in res)
+    sizes = [0] * len(imgs)
+    blobs = [None] * len(imgs) if keep else None
+    for i, r in enumerate(res):
+        sizes[i::procs] = r[2]
+        if keep:
+            blobs[i::procs] = r[3]
+    return nbytes / 1e6 / wall, nbytes, wall, sizes, blobs
+
+
+def cpu_port_run(imgs, procs: int, model_bytes: bytes):
+    pool = _cpu_pool(procs)
+    try:
+        chunks = [imgs[i::procs] for i in range(procs)]
+        res = pool.map(_port_worker, [(c, model_bytes) for c in chunks if len(c)])
+    finally:
+        pool.close()
+    wall = max(r[1] for r in res)
+    nbytes = sum(r[0] for r in res)
+    return nbytes / 1e6 / wall, nbytes, wall
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def bench_model(name: str):
     """--weights: `random` = random_weights(ModelConfig(), seed=1) (the
     BASELINE config); `trained` = tests/golden/trained.pilw, the same
-    architecture briefly trained by the trainer port (one-code histogram)."""
+    architecture trained by the trainer port."""
     import paper_2206_05279_b200 as pc
 
     if name == "trained":
@@ -87,46 +184,43 @@ def bench_model(name: str):
     return pc.random_weights(seed=1)
 
 
-def cpu_oracle_run(per_proc: int, procs: int, seed0: int = 1000, weights: str = "random"):
-    """Times the oracle port on `procs` processes (one core each)."""
-    import multiprocessing as mp
-
-    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
-        os.environ[k] = "1"
-    model_bytes = bench_model(weights).to_bytes()
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(procs) as pool:
-        pool.map(_cpu_worker, [(seed0 + i, 1, model_bytes) for i in range(procs)])  # spawn + warm-up
-        res = pool.map(_cpu_worker, [(seed0 + i, per_proc, model_bytes) for i in range(procs)])
-    # each worker times its own compress+decompress loop (after its warm-up);
-    # the job takes as long as the slowest worker
-    wall = max(r[1] for r in res)
-    nbytes = sum(r[0] for r in res)
-    return nbytes / 1e6 / wall, nbytes, wall
-
-
-def cpu_sample_size(procs: int, target_s: float, weights: str = "random") -> int:
-    """Images per process so one oracle run lasts about target_s seconds."""
-    _, _, wall = cpu_oracle_run(2, procs, weights=weights)
-    return max(2, int(round(2 * target_s / max(wall, 1e-3))))
-
-
 def run_reference(args):
+    """--impl reference: the reference package itself (pixelcodec from
+    baseline/_ref, its public compress/decompress, numba kernels, one
+    thread per process) on every host core, same workload / metric as the
+    GPU arm. Each step is a bounded sample of the workload's images."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
+    if not os.path.isdir(os.path.join(REF_DIR, "pixelcodec")):
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref not installed (tools/install_reference.sh)"}))
+        return 0
+    from paper_2206_05279_b200.synth import smooth_images
+
+    wl = WORKLOADS[args.workload if args.workload in WORKLOADS else "cifar"]
     procs = len(os.sched_getaffinity(0))
-    # each step is a bounded sample; the whole run stays within ~3 minutes
-    per_proc = cpu_sample_size(procs, max(1.0, min(10.0, 150.0 / (args.steps + args.warmup))), args.weights)
-    vals = []
-    for _ in range(args.warmup):
-        cpu_oracle_run(2, procs, weights=args.weights)
-    t_all = 0.0
-    for _ in range(args.steps):
-        v, nbytes, wall = cpu_oracle_run(per_proc, procs, weights=args.weights)
-        vals.append(v)
-        t_all += wall
+    pool = _cpu_pool(procs)
+    try:
+        # size the per-step sample for ~1-10 s of CPU work (whole run < ~3 min)
+        probe = smooth_images(2 * procs, wl["H"], wl["W"], seed=0)
+        _, _, wall, _, _ = cpu_reference_run(probe, procs, pool=pool)
+        target = max(1.0, min(10.0, 150.0 / (args.steps + args.warmup)))
+        per_proc = max(2, int(round(2 * target / max(wall, 1e-3))))
+        n = min(per_proc * procs, wl["N"])
+        imgs = smooth_images(n, wl["H"], wl["W"], seed=0)
+        for _ in range(args.warmup):
+            cpu_reference_run(probe, procs, pool=pool)
+        vals, t_all, sizes = [], 0.0, None
+        for _ in range(args.steps):
+            v, nbytes, wall, sizes, _ = cpu_reference_run(imgs, procs, pool=pool)
+            vals.append(v)
+            t_all += wall
+    finally:
+        pool.close()
     value = statistics.median(vals)
+    bpd = 8.0 * sum(sizes) / (n * wl["H"] * wl["W"] * 3)
+    sample = (f"{n} of the workload's images (seed 0) per step, {procs} processes x 1 thread "
+              f"(pixelcodec {REF_DIR}, numba + OpenBLAS pinned to 1 thread), {cpu_model()}")
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -139,14 +233,12 @@ def run_reference(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32/f64 (numpy+BLAS network), int (C coder)",
+        "dtype": "f32 numpy/OpenBLAS network, f64 argmin, int numba coder",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "weights": args.weights, "sample_images_per_step": per_proc * procs},
-        "cpu_baseline": {
-            "value": round(value, 4), "unit": "MB/s", "cores": procs, "kind": "port",
-            "sample": f"{per_proc} images/process x {procs} processes per step, oracle/ "
-                      "(numpy restatement of pixelcodec + C lanes/predictor), one thread per process",
-        },
+        "config": {"workload": wl["desc"].replace(', numerics fast', ''), "weights": "random", "sample_images_per_step": n},
+        "bpd": round(bpd, 5),
+        "cpu_baseline": {"value": round(value, 4), "unit": "MB/s", "cores": procs, "kind": "reference",
+                         "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "MB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -231,77 +323,99 @@ class ClockSampler:
 # GPU arm
 
 
-def run_gpu(args):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
+class _Ctx:
+    """Per-rank run state: device, stream, process group helpers."""
 
-    import paper_2206_05279_b200 as pc
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.ws, self.rank, self.local = _dist()
+        ndev = torch.cuda.device_count()
+        self.dev = torch.device("cuda", self.local % ndev)
+        torch.cuda.set_device(self.dev)
+        # NCCL for the timing barrier / max reduction when every rank has its
+        # own GPU; gloo when ranks share one (launcher checks on a 1-GPU box)
+        self.backend = "nccl" if ndev >= self.ws else "gloo"
+        if self.ws > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group("gloo")
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=self.dev)
+
+    def barrier(self):
+        if self.ws > 1:
+            if self.backend == "nccl":
+                self.dist.barrier(device_ids=[self.dev.index])
+            else:
+                self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def max(self, vals):
+        t = self.torch.tensor(vals, dtype=self.torch.float64,
+                              device=self.dev if self.backend == "nccl" else "cpu")
+        if self.ws > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return [float(x) for x in t.cpu()]
+
+    def close(self):
+        if self.ws > 1:
+            self.barrier()
+            self.dist.destroy_process_group()
+
+
+def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = False, frames=None, wl=None):
+    """Device-resident round trip of each shape group (compress_batch +
+    decompress_batch internals on one stream; CUDA events), then the same
+    through the public host API. Returns a dict of max-over-ranks times,
+    launch counts, the live per-kernel profile, clocks, bpd and the host
+    blobs / offsets of group 0 (for parity)."""
+    import numpy as np
+
     from paper_2206_05279_b200 import _lib
     from paper_2206_05279_b200 import container as ct
-    from paper_2206_05279_b200.synth import smooth_images
 
-    ws, rank, local = _dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream(dev)
-    model = bench_model(args.weights)
-    cfg = pc.CodecConfig(backend="twar-vqvae")
-    wl = WORKLOADS[args.workload]
-    if args.workload == "1080p":
-        from paper_2206_05279_b200 import patches as pt
-        frames = np.stack([smooth_images(1, wl["H"], wl["W"], seed=1000 * rank + f)[0] for f in range(wl["N"])])
-        plist = [p for f in frames for p in pt.split_frame(f)]
-        shapes = sorted({p.shape for p in plist})
-        groups_h = [np.stack([p for p in plist if p.shape == sh]) for sh in shapes]
-        imgs = frames
-    else:
-        imgs = smooth_images(wl["N"], wl["H"], wl["W"], seed=rank)
-        groups_h = [imgs]
-    raw_bytes = imgs.size
+    torch = ctx.torch
+    dev, stream = ctx.dev, ctx.stream
     groups_d = [torch.from_numpy(g).to(dev) for g in groups_h]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    def barrier():
-        if ws > 1:
-            dist.barrier(device_ids=[local])
-        torch.cuda.synchronize(dev)
+    raw_bytes = sum(g.size for g in groups_h)
 
     def step_device():
         outs = []
         for img_d in groups_d:
             out_d, off_d = ct._compress_device(img_d, model, cfg, dev, stream)
             results, errors, hdr = ct._decompress_device(out_d, off_d, img_d.shape[0], model, dev, stream)
-            ct._verify(results)  # the speculated summary matched (raises otherwise)
-            outs.append((off_d.cpu().numpy().view(np.uint64), results, errors))
+            try:
+                ct._verify(results)  # the speculated summary matched
+            except ct.SpeculationMiss:  # another config ran last: redo once, non-speculatively
+                results, errors, hdr = ct._decompress_device(out_d, off_d, img_d.shape[0], model, dev, stream,
+                                                             speculate=False)
+            outs.append((out_d, off_d, results, errors))
         return outs
 
-    # warm-up (+ correctness of the device path, outside the timed region)
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, warmup)):  # warm-up + correctness, outside the timed region
         outs = step_device()
     torch.cuda.synchronize(dev)
-    lossless = True
-    bits = 0.0
-    for g, (offs_host, results, errors) in zip(groups_h, outs):
+    lossless, bits, blob0 = True, 0.0, None
+    for gi, (g, (out_d, off_d, results, errors)) in enumerate(zip(groups_h, outs)):
         assert not errors, errors
         lossless &= bool(np.array_equal(results[0][1].cpu().numpy(), g))
-        bits += 8.0 * float(np.diff(offs_host.astype(np.int64)).sum())
-    bpd = bits / float(sum(g.size for g in groups_h))
+        offs = off_d.cpu().numpy().view(np.uint64)
+        bits += 8.0 * float(offs[-1] - offs[0])
+        if gi == 0:
+            blob0 = (out_d[: int(offs[-1])].cpu().numpy(), offs)
+    bpd = bits / float(raw_bytes)
 
-    # timed region: device-resident inputs. Pass 1 measures the step with no
-    # per-launch instrumentation (counted launches only); pass 2 repeats the
-    # same K steps with a CUDA event pair around every launch for the stage
-    # table and the roofline (the events themselves cost ~3% of the step).
-    def timed(profile: bool):
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-               torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        _lib.prof_reset(profile)
-        barrier()
-        with ClockSampler(local) as clk:
-            for k in range(args.steps):
-                flush.fill_(k & 0xFF)  # evict L2 between steps (outside the events)
+    def timed(prof_on: bool):
+        ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(steps)]
+        _lib.prof_reset(prof_on)
+        ctx.barrier()
+        with ClockSampler(dev.index) as clk:
+            for k in range(steps):
+                ctx.flush.fill_(k & 0xFF)  # evict L2 between steps (outside the events)
                 e0, e1, e2 = ev[k]
                 e0.record(stream)
                 packed = [ct._compress_device(img_d, model, cfg, dev, stream) for img_d in groups_d]
@@ -309,209 +423,306 @@ def run_gpu(args):
                 for (out_d, off_d), img_d in zip(packed, groups_d):
                     ct._decompress_device(out_d, off_d, img_d.shape[0], model, dev, stream)
                 e2.record(stream)
-            barrier()
+            ctx.barrier()
         launches = _lib.prof_launches()
-        prof = _lib.prof_read() if profile else {}
+        prof = _lib.prof_read() if prof_on else {}
         _lib.prof_reset(False)
-        t_c = sum(a.elapsed_time(b) for a, b, _ in ev) / 1000.0
-        t_d = sum(b.elapsed_time(c) for _, b, c in ev) / 1000.0
+        t_c = sum(a.elapsed_time(b) for a, b, _ in ev) / 1000.0 / steps
+        t_d = sum(b.elapsed_time(c) for _, b, c in ev) / 1000.0 / steps
         return clk, launches, prof, t_c, t_d
 
     clk, launches, _, t_c, t_d = timed(False)
-    _, _, prof, _, _ = timed(True)
-    t_step = (t_c + t_d) / args.steps
-    tt = torch.tensor([t_step, t_c / args.steps, t_d / args.steps], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    t_step, t_cs, t_ds = (float(x) for x in tt.cpu())
-    value = raw_bytes * ws / 1e6 / t_step
+    prof = timed(True)[2] if profile else {}
+    t_step, t_c, t_d = ctx.max([t_c + t_d, t_c, t_d])
 
-    # end to end through the public API with host buffers (after the same
-    # number of untimed warm-up calls as the device loop: the first calls
-    # page-lock their host buffers)
-    e2e_times, e2e_c, e2e_d = [], [], []
-    h2d = d2h = 0
-    lat = None
-    for _ in range(max(1, args.warmup)):
-        if args.workload == "1080p":
-            buf, off = pt.compress_frames(imgs, model, cfg)
-            out = pt.decompress_frames(buf, off, len(imgs), wl["H"], wl["W"], model)
+    # end to end through the public API with host buffers (after untimed
+    # warm-up calls: the first calls page-lock their host buffers)
+    import paper_2206_05279_b200 as pc
+
+    e2e_t, e2e_c, e2e_d = [], [], []
+    imgs = frames if frames is not None else groups_h[0]
+
+    def api_round():
+        if frames is not None:
+            from paper_2206_05279_b200 import patches as pt
+            buf, off = pt.compress_frames(frames, model, cfg)
+            torch.cuda.synchronize(dev)
+            t1 = time.perf_counter()
+            out = pt.decompress_frames(buf, off, len(frames), wl["H"], wl["W"], model)
         else:
             buf, off = pc.compress_batch(imgs, model, cfg)
+            torch.cuda.synchronize(dev)
+            t1 = time.perf_counter()
             out = pc.decompress_batch(buf, off, model)
-    barrier()
-    for k in range(max(1, args.steps)):
-        flush.fill_(k & 0xFF)
+        return buf, off, out, t1
+
+    for _ in range(max(1, warmup)):
+        api_round()
+    ctx.barrier()
+    h2d = d2h = 0
+    for k in range(max(1, steps)):
+        ctx.flush.fill_(k & 0xFF)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        if args.workload == "1080p":
-            buf, off = pt.compress_frames(imgs, model, cfg)
-            torch.cuda.synchronize(dev)
-            t1 = time.perf_counter()
-            out = pt.decompress_frames(buf, off, len(imgs), wl["H"], wl["W"], model)
-        else:
-            buf, off = pc.compress_batch(imgs, model, cfg)
-            torch.cuda.synchronize(dev)
-            t1 = time.perf_counter()
-            out = pc.decompress_batch(buf, off, model)
+        buf, off, out, t1 = api_round()
         torch.cuda.synchronize(dev)
         t2 = time.perf_counter()
-        e2e_times.append(t2 - t0)
+        e2e_t.append(t2 - t0)
         e2e_c.append(t1 - t0)
         e2e_d.append(t2 - t1)
         h2d = imgs.nbytes + buf.nbytes + off.nbytes
         d2h = buf.nbytes + off.nbytes + out.nbytes
     assert np.array_equal(out, imgs)
+    e_t, e_c, e_d = ctx.max([statistics.median(e2e_t), statistics.median(e2e_c), statistics.median(e2e_d)])
+    raw_all = raw_bytes * ctx.ws
+    return {
+        "t_step": t_step, "t_c": t_c, "t_d": t_d, "launches": launches, "prof": prof, "clk": clk,
+        "lossless": lossless, "bpd": bpd, "blob0": blob0,
+        "value": raw_all / 1e6 / t_step, "compress": raw_all / 1e6 / t_c, "decompress": raw_all / 1e6 / t_d,
+        "e2e": {"value": raw_all / 1e6 / e_t, "unit": "MB/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "compress_mb_s": round(raw_all / 1e6 / e_c, 3),
+                "decompress_mb_s": round(raw_all / 1e6 / e_d, 3)},
+        "api": (buf, off),
+    }
+
+
+def run_gpu(args):
+    import numpy as np
+
+    import paper_2206_05279_b200 as pc
+    from paper_2206_05279_b200 import vqvae
+    from paper_2206_05279_b200.device import as_device_u8
+    from paper_2206_05279_b200.synth import smooth_images
+
+    ctx = _Ctx()
+    ws, rank = ctx.ws, ctx.rank
+    dev, stream = ctx.dev, ctx.stream
+    torch = ctx.torch
+    model = bench_model(args.weights)
+    fast = pc.CodecConfig(backend="twar-vqvae", numerics="fast")
+    exact = pc.CodecConfig(backend="twar-vqvae", numerics="exact")
+    wl = WORKLOADS[args.workload]
+    frames = None
+    if args.workload == "1080p":
+        from paper_2206_05279_b200 import patches as pt
+        frames = np.stack([smooth_images(1, wl["H"], wl["W"], seed=1000 * rank + f)[0] for f in range(wl["N"])])
+        plist = [p for f in frames for p in pt.split_frame(f)]
+        shapes = sorted({p.shape for p in plist})
+        groups_h = [np.stack([p for p in plist if p.shape == sh]) for sh in shapes]
+    else:
+        groups_h = [smooth_images(wl["N"], wl["H"], wl["W"], seed=rank)]
+    head = measure(ctx, groups_h, model, fast, args.steps, args.warmup, profile=True, frames=frames, wl=wl)
+    prof, clk = head["prof"], head["clk"]
+
+    lat = None
     if args.workload == "1080p":
         # single-frame decompress latency: blobs in host RAM -> frame in RAM
+        buf, off = head["api"]
         per = len(pt.patch_grid(wl["H"], wl["W"]))
-        fb = buf[: int(off[per])]
-        fo = off[: per + 1]
+        fb, fo = buf[: int(off[per])], off[: per + 1]
         ts = []
         for _ in range(5):
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             fr = pt.decompress_frames(fb, fo, 1, wl["H"], wl["W"], model)
             ts.append(time.perf_counter() - t0)
-        assert np.array_equal(fr[0], imgs[0])
+        assert np.array_equal(fr[0], frames[0])
         lat = round(1000 * statistics.median(ts), 3)
-    te = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = raw_bytes * ws / 1e6 / float(te.item())
+
+    extra = {}
+    if args.workload == "cifar" and not args.headline_only:
+        # configs[2]: IN64 x 4096 per GPU, the north-star decompress rate
+        w64 = WORKLOADS["in64"]
+        r = measure(ctx, [smooth_images(w64["N"], w64["H"], w64["W"], seed=rank)], model, fast, args.steps,
+                    args.warmup)
+        extra["in64"] = {"workload": w64["desc"], "round_trip_mb_s": round(r["value"], 3),
+                         "compress_mb_s": round(r["compress"], 3), "decompress_mb_s": round(r["decompress"], 3),
+                         "ms_per_step": round(1000 * r["t_step"], 3), "e2e": _round(r["e2e"]),
+                         "bpd": round(r["bpd"], 5), "lossless": r["lossless"]}
+        # the same CIFAR round trip with the reference's own float arithmetic
+        r = measure(ctx, groups_h, model, exact, max(2, args.steps // 2), 1)
+        extra["exact"] = {"workload": wl["desc"].replace("numerics fast", "numerics exact"),
+                          "round_trip_mb_s": round(r["value"], 3), "compress_mb_s": round(r["compress"], 3),
+                          "decompress_mb_s": round(r["decompress"], 3), "ms_per_step": round(1000 * r["t_step"], 3),
+                          "e2e": _round(r["e2e"]), "bpd": round(r["bpd"], 5), "lossless": r["lossless"]}
+        exact_blobs = r["blob0"]
+        # codebook index agreement, fast encoder vs the exact one (the
+        # reference's z bit for bit), over the whole batch
+        img_d = as_device_u8(groups_h[0], dev, stream)
+        i_fast = vqvae.encode_indices_device(img_d, model, dev, stream, exact=False)
+        i_exact = vqvae.encode_indices_device(img_d, model, dev, stream, exact=True)
+        agree = int((i_fast == i_exact).sum().item())
+        extra["index_agreement"] = {"value": agree / i_fast.numel(), "latents": int(i_fast.numel()),
+                                    "vs": "exact encoder (bit-identical to the reference's z / indices)"}
+
+    cpu = cpu_port = parity = None
+    if rank == 0 and ws == 1 and not args.no_cpu and args.workload == "cifar":
+        procs = len(os.sched_getaffinity(0))
+        imgs = groups_h[0]
+        if os.path.isdir(os.path.join(REF_DIR, "pixelcodec")):
+            pool = _cpu_pool(procs)
+            try:
+                _, _, wall, _, _ = cpu_reference_run(imgs[: 2 * procs], procs, pool=pool)  # also the JIT warm-up
+                per_proc = max(4, int(round(2 * 12.0 / max(wall, 1e-3))))
+                n = min(per_proc * procs, 4096)
+                v, nbytes, wall, sizes, blobs = cpu_reference_run(imgs[:n], procs, keep=True, pool=pool)
+            finally:
+                pool.close()
+            cpu = {"value": round(v, 4), "unit": "MB/s", "cores": procs, "kind": "reference",
+                   "sample": f"first {n} images of this run's batch ({nbytes} B) round trip through pixelcodec "
+                             f"(baseline/_ref, public compress/decompress), {procs} processes x 1 thread, "
+                             f"{wall:.1f} s, {cpu_model()}"}
+            # bits/dim against the reference on the same images and weights
+            fb, fo = head["blob0"]
+            fast_sizes = np.diff(fo.astype(np.int64))[:n]
+            eb, eo = exact_blobs
+            same = sum(bytes(eb[int(eo[i]): int(eo[i + 1])]) == blobs[i] for i in range(n))
+            px = imgs[0].size
+            bpd_ref = 8.0 * float(sum(sizes)) / (n * px)
+            bpd_fast = 8.0 * float(fast_sizes.sum()) / (n * px)
+            parity = {"images": n, "bpd_ref": round(bpd_ref, 5), "bpd": round(bpd_fast, 5),
+                      "bpd_rel_delta": round((bpd_fast - bpd_ref) / bpd_ref, 6),
+                      "exact_byte_identical": same / n,
+                      "note": "bpd (numerics fast) vs pixelcodec on the same images and weights; "
+                              "exact_byte_identical = exact-numerics containers equal to pixelcodec's"}
+        model_bytes = model.to_bytes()
+        v, nbytes, wall = cpu_port_run(imgs[: 8 * procs], procs, model_bytes)
+        cpu_port = {"value": round(v, 4), "unit": "MB/s", "cores": procs, "kind": "port",
+                    "sample": f"first {8 * procs} images, oracle/ (numpy restatement + C coder), {procs} x 1 thread"}
 
     if rank == 0:
-        peaks = {}
-        try:
-            with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
-                peaks = json.load(f)
-            src = "measured"
-        except OSError:
-            peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
-            src = "fallback"
-        dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
-        roofline = None
-        notes = {
-            "tc3_conv_kernel": "encoder block convs, 3-product fp16 split on tcgen05 kind::f16 (per K=16 step A_hi x [W_hi|W_lo] "
-                               "N=64 + A_lo x W_hi N=32, fp32 TMEM); algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch "
-                               "(MMA FLOPs issued = 3x that)",
-            "tc_conv_kernel": "bf16 tcgen05 decoder convs; algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch",
-            "enc_front_kernel": "encoder stem + stride-2 down, both 3-product fp16 MMAs (down over the space-to-depth stem); "
-                                "algorithmic FLOPs = 2*N*(4*gh*gw*32*27 + gh*gw*32*32*9)",
-            "conv_kernel": "fp32 SIMT convs (non-default model shapes); algorithmic FLOPs = 2*N*Ho*Wo*Cout*Cin*k^2 per launch",
-            "tc3_block_kernel": "one encoder residual block per launch (conv1 + conv2, intermediate in shared memory), "
-                                "3-product fp16 split on tcgen05 kind::f16; algorithmic FLOPs = 2 convs x 2*N*H*W*32*32*9 "
-                                "(MMA FLOPs issued = 3x that)",
-            "dec_trunk_kernel": "decoder trunk (gather + all 2B bf16 block convs, activations in shared memory, G images per "
-                                "CTA iteration); algorithmic FLOPs = 2B x 2*N*gh*gw*32*32*9",
-            "argmin_kernel": "codebook distance GEMM (3xTF32 tcgen05) + proven-margin screen + exact f64 rescore (3*n*K*Dc FLOPs)",
-        }
-        if dom:
-            name, (n, ms, units) = dom
-            if name in notes:
-                ach = units / (ms / 1e3) / 1e12
-                peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-                roofline = {"kernel": name, "bound": "tensor", "achieved": round(ach, 3), "peak": peak,
-                            "unit": "TFLOP/s", "frac": round(ach / peak, 5), "traffic": None,
-                            "launches_per_step": n / args.steps, "ms_per_launch": round(ms / n, 4),
-                            "timing": "per-launch CUDA events over a second pass of the K timed steps",
-                            "peak_source": f"{src} bf16 dense, sustained (kind::f16 fp16/bf16 MMAs run at this rate)",
-                            "note": notes[name]}
-            else:
-                gbs = units / (ms / 1e3) / 1e9
-                roofline = {"kernel": name, "bound": "hbm", "achieved": round(gbs, 2), "peak": peaks.get("hbm_gbs"),
-                            "unit": "GB/s", "frac": round(gbs / peaks.get("hbm_gbs"), 5), "traffic": None}
-            # attainable rate for these MMA shapes: SS-mode tcgen05 MMAs (M=128,
-            # K=16) cost max(44 cycles, operand bytes / 128 B/cycle) each on this
-            # B200 (tools/micro/mma_rate.cu: N=16/32 44, N=64 48, N=128 64), so
-            # N=32-output convs cannot approach the dense peak. Cycles per
-            # 128-row K=16 step (algorithmic 2*128*32*16 FLOP): bf16 convs 44;
-            # the 3-product fp16 encoder (N=64 + N=32 MMAs) 92.
-            floor_cyc = {"tc_conv_kernel": 44.0, "dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0,
-                         "tc3_conv_kernel": 92.0}.get(name)
-            if floor_cyc and roofline and roofline.get("bound") == "tensor":
-                sm = peaks.get("sm_count", 148)
-                mhz = clk.summary().get("sm_mhz") or 1965.0
-                att = 2.0 * 128 * 32 * 16 / floor_cyc * sm * mhz * 1e6 / 1e12
-                roofline["mma_floor"] = {"peak": round(att, 1), "unit": "TFLOP/s",
-                                         "frac": round(roofline["achieved"] / att, 4),
-                                         "note": f"{floor_cyc:.0f} cycles per 128x32x16 step (measured per-MMA floor), "
-                                                 f"{sm} SMs at the sampled SM clock; ignores the padded border rows"}
-            tr = _traffic(name)
-            if tr is not None and roofline:
-                roofline["traffic"] = tr
-                roofline["traffic_gbs"] = round(tr / (ms / n / 1e3) / 1e9, 1)
-                roofline["traffic_frac_of_hbm"] = round(tr / (ms / n / 1e3) / 1e9 / peaks.get("hbm_gbs"), 4)
-        # per-stage rooflines: tensor kernels against the dense bf16 peak (and
-        # the per-MMA floor), every kernel's DRAM bytes (committed ncu capture,
-        # per launch) against the measured HBM bandwidth
-        ncu_name = {"enc_front_kernel": "enc_front_tc_kernel", "argmin_kernel": "argmin_tc_kernel",
-                    "gather_kernel": "dec_table_kernel", "blob_sizes+scan": "blob_sizes_kernel"}
-        hbm_peak = peaks.get("hbm_gbs")
-        tpeak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-        # (up conv and head share tc_conv_kernel with different N: no single floor)
-        floor = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0}
-        mhz = clk.summary().get("sm_mhz") or 1965.0
-        stages = {}
-        for k, (n, ms, units) in prof.items():
-            e = {"launches": n, "ms_per_step": round(ms / args.steps, 4)}
-            tr = _traffic(ncu_name.get(k, k))
-            if tr is not None and ms > 0:
-                gbs = tr * n / (ms / 1e3) / 1e9
-                e["hbm_gbs"] = round(gbs, 1)
-                e["hbm_frac"] = round(gbs / hbm_peak, 4)
-            if k in notes and ms > 0:
-                tf = units / (ms / 1e3) / 1e12
-                e["tflops"] = round(tf, 2)
-                e["tensor_frac"] = round(tf / tpeak, 4)
-                if k in floor:
-                    att = 2.0 * 128 * 32 * 16 / floor[k] * peaks.get("sm_count", 148) * mhz * 1e6 / 1e12
-                    e["mma_floor_frac"] = round(tf / att, 4)
-            stages[k] = e
-        cpu = None
-        if ws == 1 and not args.no_cpu:
-            procs = len(os.sched_getaffinity(0))
-            per_proc = cpu_sample_size(procs, 10.0, args.weights)
-            v, nbytes, wall = cpu_oracle_run(per_proc, procs, weights=args.weights)
-            cpu = {"value": round(v, 4), "unit": "MB/s", "cores": procs, "kind": "port",
-                   "sample": f"{per_proc * procs} CIFAR images ({nbytes} B) compress+decompress, oracle/ numpy+C, "
-                             f"{procs} processes x 1 thread, {wall:.1f} s"}
+        roofline, stages = _roofline(prof, clk, args.steps)
         line = {
             "metric": METRIC,
-            "value": round(value, 3),
+            "value": round(head["value"], 3),
             "unit": "MB/s",
             "n_gpus": ws,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": round(1000 * t_step, 3),
+            "ms_per_step": round(1000 * head["t_step"], 3),
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "bf16 tcgen05 decoder, fp32-class encoder (3-product fp16 split on tcgen05), 3xTF32 + f64 argmin, "
                      "int coder/predictor/container",
             "data": "synthetic",
-            "config": {"workload": wl["desc"], "weights": args.weights, "global_batch": wl["N"] * ws, "image": [wl["H"], wl["W"], 3],
-                       "parallelism": f"shard{ws}", "l2": "flushed (256 MiB write) before each step"},
+            "config": {"workload": wl["desc"], "weights": args.weights, "global_batch": wl["N"] * ws,
+                       "image": [wl["H"], wl["W"], 3], "numerics": "fast", "parallelism": f"shard{ws}",
+                       "l2": "flushed (256 MiB write) before each step"},
             "frame_decompress_latency_ms": lat,
-            "compress_mb_s": round(raw_bytes * ws / 1e6 / t_cs, 3),
-            "decompress_mb_s": round(raw_bytes * ws / 1e6 / t_ds, 3),
-            "bpd": round(bpd, 4),
-            "lossless": lossless,
-            "e2e": {"value": round(e2e_value, 3), "unit": "MB/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h),
-                    "compress_mb_s": round(raw_bytes / 1e6 / statistics.median(e2e_c), 3),
-                    "decompress_mb_s": round(raw_bytes / 1e6 / statistics.median(e2e_d), 3)},
-            "gpu_launches": int(launches),
+            "compress_mb_s": round(head["compress"], 3),
+            "decompress_mb_s": round(head["decompress"], 3),
+            "bpd": round(head["bpd"], 5),
+            "lossless": head["lossless"],
+            "e2e": _round(head["e2e"]),
+            "gpu_launches": int(head["launches"]),
             "roofline": roofline,
             "stages": stages,
             "clocks": clk.summary(),
+            "parity": parity,
+            **extra,
             "cpu_baseline": cpu,
+            "cpu_baseline_port": cpu_port,
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.barrier(device_ids=[local])
-        dist.destroy_process_group()
+    ctx.close()
     return 0
+
+
+def _round(e2e: dict) -> dict:
+    return {k: (round(v, 3) if isinstance(v, float) else v) for k, v in e2e.items()}
+
+
+def _roofline(prof, clk, steps):
+    """Dominant kernel against its roofline (live per-launch CUDA events),
+    plus every stage's rate: tensor kernels against the dense bf16 peak and
+    the per-MMA floor, every kernel's DRAM bytes (committed ncu capture, per
+    launch) against the measured HBM bandwidth."""
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+        src = "measured"
+    except OSError:
+        peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+        src = "fallback"
+    notes = {
+        "tc3_conv_kernel": "encoder convs, 3-product fp16 split on tcgen05 kind::f16 (per K=16 step A_hi x [W_hi|W_lo] "
+                           "N=64 + A_lo x W_hi N=32, fp32 TMEM); algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch "
+                           "(MMA FLOPs issued = 3x that)",
+        "tc_conv_kernel": "bf16 tcgen05 decoder convs; algorithmic FLOPs = 2*N*H*W*Cout*Cin*9 per launch",
+        "enc_front_kernel": "encoder stem + stride-2 down, both 3-product fp16 MMAs (down over the space-to-depth stem); "
+                            "algorithmic FLOPs = 2*N*(4*gh*gw*32*27 + gh*gw*32*32*9)",
+        "conv_kernel": "exact network: fp32 FMA chains in the reference's order (SIMT); algorithmic FLOPs = "
+                       "2*N*Ho*Wo*Cout*Cin*k^2 per launch",
+        "tc3_block_kernel": "one encoder residual block per launch (conv1 + conv2, intermediate in shared memory), "
+                            "3-product fp16 split on tcgen05 kind::f16; algorithmic FLOPs = 2 convs x 2*N*H*W*32*32*9 "
+                            "(MMA FLOPs issued = 3x that)",
+        "dec_trunk_kernel": "decoder trunk (gather + all 2B bf16 block convs, activations in shared memory, G images per "
+                            "CTA iteration); algorithmic FLOPs = 2B x 2*N*gh*gw*32*32*9",
+        "argmin_kernel": "codebook distance GEMM (3xTF32 tcgen05) + proven-margin screen + exact f64 rescore (3*n*K*Dc FLOPs)",
+    }
+    mhz = clk.summary().get("sm_mhz") or 1965.0
+    sm = peaks.get("sm_count", 148)
+    roofline = None
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else None
+    if dom:
+        name, (n, ms, units) = dom
+        if name in notes:
+            ach = units / (ms / 1e3) / 1e12
+            peak = peaks.get("bf16_tflops")
+            roofline = {"kernel": name, "bound": "tensor", "achieved": round(ach, 3), "peak": peak,
+                        "unit": "TFLOP/s", "frac": round(ach / peak, 5), "traffic": None,
+                        "launches_per_step": n / steps, "ms_per_launch": round(ms / n, 4),
+                        "timing": "per-launch CUDA events over a second pass of the K timed steps",
+                        "peak_source": f"{src} dense bf16 burst (kind::f16 fp16/bf16 MMAs run at this rate; "
+                                       f"sustained {peaks.get('bf16_tflops_sustained')})",
+                        "note": notes[name]}
+        else:
+            gbs = units / (ms / 1e3) / 1e9
+            roofline = {"kernel": name, "bound": "hbm", "achieved": round(gbs, 2), "peak": peaks.get("hbm_gbs"),
+                        "unit": "GB/s", "frac": round(gbs / peaks.get("hbm_gbs"), 5), "traffic": None}
+        # attainable rate for these MMA shapes: SS-mode tcgen05 MMAs (M=128,
+        # K=16) cost max(44 cycles, operand bytes / 128 B/cycle) each on this
+        # B200 (tools/micro/mma_rate.cu: N=16/32 44, N=64 48, N=128 64), so
+        # N=32-output convs cannot approach the dense peak. Cycles per
+        # 128-row K=16 step (algorithmic 2*128*32*16 FLOP): bf16 convs 44;
+        # the 3-product fp16 encoder (N=64 + N=32 MMAs) 92.
+        floor_cyc = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0}.get(name)
+        if floor_cyc and roofline and roofline.get("bound") == "tensor":
+            att = 2.0 * 128 * 32 * 16 / floor_cyc * sm * mhz * 1e6 / 1e12
+            roofline["mma_floor"] = {"peak": round(att, 1), "unit": "TFLOP/s",
+                                     "frac": round(roofline["achieved"] / att, 4),
+                                     "note": f"{floor_cyc:.0f} cycles per 128x32x16 step (measured per-MMA floor), "
+                                             f"{sm} SMs at the sampled SM clock; ignores the padded border rows"}
+        tr = _traffic(name)
+        if tr is not None and roofline:
+            roofline["traffic"] = tr
+            roofline["traffic_gbs"] = round(tr / (ms / n / 1e3) / 1e9, 1)
+            roofline["traffic_frac_of_hbm"] = round(tr / (ms / n / 1e3) / 1e9 / peaks.get("hbm_gbs"), 4)
+    ncu_name = {"enc_front_kernel": "enc_front_tc_kernel", "argmin_kernel": "argmin_tc_kernel",
+                "gather_kernel": "dec_table_kernel", "blob_sizes+scan": "blob_sizes_kernel"}
+    hbm_peak = peaks.get("hbm_gbs")
+    tpeak = peaks.get("bf16_tflops")
+    floor = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0}
+    stages = {}
+    for k, (n, ms, units) in prof.items():
+        e = {"launches": n, "ms_per_step": round(ms / steps, 4)}
+        tr = _traffic(ncu_name.get(k, k))
+        if tr is not None and ms > 0:
+            gbs = tr * n / (ms / 1e3) / 1e9
+            e["hbm_gbs"] = round(gbs, 1)
+            e["hbm_frac"] = round(gbs / hbm_peak, 4)
+        if k in notes and ms > 0:
+            tf = units / (ms / 1e3) / 1e12
+            e["tflops"] = round(tf, 2)
+            e["tensor_frac"] = round(tf / tpeak, 4)
+            if k in floor:
+                att = 2.0 * 128 * 32 * 16 / floor[k] * sm * mhz * 1e6 / 1e12
+                e["mma_floor_frac"] = round(tf / att, 4)
+        elif ms > 0 and units > 0 and k.startswith("rans"):
+            e["msym_s"] = round(units / (ms / 1e3) / 1e6, 1)
+        stages[k] = e
+    return roofline, stages
 
 
 def run_coder(args):
@@ -605,19 +816,40 @@ def _traffic(kernel: str):
         return None
 
 
+def _relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: rerun this command under torchrun with
+    N ranks (one per GPU; on a box with fewer GPUs ranks share devices,
+    which checks the launcher, not the scaling)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines")
+    ap.add_argument("--headline-only", action="store_true", help="skip the in64 / exact / index sections")
     ap.add_argument("--workload", default="cifar", choices=sorted(WORKLOADS) + ["coder"],
                     help="BASELINE config: cifar (configs[1], default), in64 (configs[2]), 1080p (configs[3]), "
                          "coder (configs[4], coder-only lane sweep)")
     ap.add_argument("--weights", default="random", choices=["random", "trained"],
                     help="random_weights(seed=1) (default) or tests/golden/trained.pilw")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return _relaunch(args)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={ws}"}), flush=True)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "coder":

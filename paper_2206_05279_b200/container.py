@@ -245,12 +245,26 @@ def _groups_by_shape(shapes):
 
 
 def compress_batch(images, model: ModelWeights | None = None, config: CodecConfig = CodecConfig(),
-                   device=None, return_device: bool = False):
+                   device=None, return_device: bool = False, devices=None):
     """Compress a batch. `images`: (N, H, W, 3) uint8 numpy/torch (host or
     cuda) or a list of (H, W, 3) arrays of mixed shapes. Returns
     (buffer uint8[total], offsets uint64[N+1]); blob i is
     buffer[offsets[i]:offsets[i+1]], byte-identical in format to
-    `pixelcodec.compress` of image i."""
+    `pixelcodec.compress` of image i. `devices` (a list of CUDA devices):
+    the batch is split into contiguous shares, one per device, each run by
+    its own host thread and stream (multi.py); the output is identical to a
+    one-device call."""
+    if devices is not None and len(devices) > 1 and not return_device:
+        from .multi import compress_multi
+
+        if isinstance(images, (list, tuple)):
+            imgs = [validate_image(im) for im in images]
+            if len({im.shape for im in imgs}) == 1:
+                return compress_multi(np.stack(imgs), model, config, devices)
+        else:
+            return compress_multi(images, model, config, devices)
+    if devices is not None and len(devices) == 1:
+        device = devices[0]
     dev = require_device(device)
     stream = torch.cuda.current_stream(dev)
     if isinstance(images, (list, tuple)):
@@ -259,7 +273,7 @@ def compress_batch(images, model: ModelWeights | None = None, config: CodecConfi
         parts = {}
         for shape, ids in groups.items():
             batch = np.stack([imgs[i] for i in ids])
-            parts[shape] = compress_batch(batch, model, config, device)
+            parts[shape] = compress_batch(batch, model, config, device, devices=devices)
         sizes = np.zeros(len(imgs), np.uint64)
         for shape, ids in groups.items():
             _, off = parts[shape]
@@ -650,10 +664,19 @@ def check_offsets(offsets) -> np.ndarray:
 
 
 def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=None,
-                     raise_on_error: bool = True):
+                     raise_on_error: bool = True, devices=None, out: np.ndarray | None = None):
     """Decode blobs buffer[offsets[i]:offsets[i+1]]. Returns an
     (N, H, W, 3) array when all blobs share a shape, else a list; with
-    raise_on_error=False returns (images, {blob index: exception})."""
+    raise_on_error=False returns (images, {blob index: exception}).
+    `devices`: split the blobs over several CUDA devices (multi.py). `out`:
+    an (N, H, W, 3) uint8 array (ideally page-locked) the decoded batch is
+    copied into when every blob decodes to that shape."""
+    if devices is not None and len(devices) > 1:
+        from .multi import decompress_multi
+
+        return decompress_multi(buffer, offsets, model, devices, raise_on_error)
+    if devices is not None and len(devices) == 1:
+        device = devices[0]
     dev = require_device(device)
     stream = torch.cuda.current_stream(dev)
     offs = check_offsets(offsets)
@@ -679,12 +702,19 @@ def decompress_batch(buffer, offsets, model: ModelWeights | None = None, device=
     # batch case) lands directly in the returned array.
     if len(results) == 1 and not errors and np.asarray(results[0][0]).size == n:
         img = results[0][1]
+        if out is not None and tuple(out.shape) == tuple(img.shape) and out.dtype == np.uint8 \
+                and out.flags.c_contiguous:
+            dst = torch.from_numpy(out).view(-1)
+            with torch.cuda.stream(stream):
+                dst.copy_(img.view(-1), non_blocking=dst.is_pinned())
+            stream.synchronize()
+            return (out, errors) if not raise_on_error else out
         host = pinned(img.numel())
         with torch.cuda.stream(stream):
             host.copy_(img.view(-1), non_blocking=True)
         stream.synchronize()
-        out = host.numpy().reshape(tuple(img.shape))
-        return (out, errors) if not raise_on_error else out
+        res = host.numpy().reshape(tuple(img.shape))
+        return (res, errors) if not raise_on_error else res
     imgs: list = [None] * n
     for ids, img, *_ in results:
         host = pinned(img.numel())

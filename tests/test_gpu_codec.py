@@ -628,3 +628,84 @@ def test_vqvae_wide_images_round_trip(full_model, shape):
     ref = O.encode_indices(img, om)
     assert np.array_equal(vqvae.encode_to_indices(img, full_model, exact=False), ref)
     assert np.array_equal(vqvae.encode_to_indices(img, full_model), ref)
+
+
+# --- multi-GPU: one process over a device list, and one process per rank -----
+
+
+@pytest.mark.parametrize("cfg", [None, FAST], ids=["static", "fast"])
+def test_devices_list_matches_one_device(full_model, cfg):
+    """compress_batch / decompress_batch with devices=[...] (one host thread
+    and stream per device, zero-copy rebased outputs; multi.py) give exactly
+    the one-device results. On a one-GPU box the list names device 0 three
+    times, which exercises the threading and the offset rebasing."""
+    n = torch.cuda.device_count()
+    devs = [i % n for i in range(3)]
+    imgs = smooth_images(37, 32, 32, seed=8)
+    model = full_model if cfg is not None else None
+    cfg = cfg or pc.CodecConfig()
+    buf1, off1 = pc.compress_batch(imgs, model, cfg)
+    buf, off = pc.compress_batch(imgs, model, cfg, devices=devs)
+    assert np.array_equal(off, off1) and np.array_equal(buf, buf1)
+    out = pc.decompress_batch(buf, off, model, devices=devs)
+    assert isinstance(out, np.ndarray) and np.array_equal(out, imgs)
+    # mixed shapes and a corrupt blob: per-blob errors keep their batch index
+    mixed = [smooth_images(1, 9 + i % 3, 7, seed=i)[0] for i in range(7)]
+    mb, mo = pc.compress_batch(mixed, model, cfg, devices=devs)
+    mb = np.array(mb, copy=True)
+    mb[int(mo[4]) + 12] ^= 0x20
+    res, errs = pc.decompress_batch(mb, mo, model, devices=devs, raise_on_error=False)
+    assert set(errs) == {4}
+    assert all(np.array_equal(res[i], mixed[i]) for i in range(7) if i != 4)
+
+
+def _shard_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2206_05279_b200.shard import compress_sharded, decompress_sharded
+
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+        model = pc.random_weights(seed=1)
+        cfg = pc.CodecConfig(backend="twar-vqvae", numerics="fast")
+        imgs = smooth_images(21, 32, 32, seed=12)
+        packed = compress_sharded(imgs, model, cfg, dst=0)
+        obj = [packed]
+        dist.broadcast_object_list(obj, src=0)
+        buf, off = obj[0]
+        back = decompress_sharded(buf, off, model, dst=0)
+        if rank == 0:
+            q.put((buf.tobytes(), off.tolist(), back.tobytes()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_sharded_ranks_on_the_gpu_path(full_model):
+    """shard.compress_sharded / decompress_sharded: two ranks (processes),
+    each on its GPU (both on device 0 on a one-GPU box), the product GPU
+    path per rank, results gathered on rank 0 identical to one batch."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    buf, off, back = q.get(timeout=500)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    imgs = smooth_images(21, 32, 32, seed=12)
+    rb, ro = pc.compress_batch(imgs, full_model, FAST)
+    assert buf == rb.tobytes() and off == ro.tolist()
+    assert back == imgs.tobytes()

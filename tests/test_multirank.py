@@ -1,10 +1,11 @@
 """N>1 host logic on CPU: world_size-2 gloo process group, no GPU.
 
 The data path has no collective (images shard by contiguous ranges); what
-crosses ranks is the final gather of per-rank blob buffers into one
-(buffer, offsets) pair. These tests run that logic with real PILC blobs
-(produced by the CPU oracle) over gloo and check the result is byte-identical
-to a single-rank batch."""
+crosses ranks is the final gather of per-rank results. These tests drive the
+product shard API (shard.compress_sharded / decompress_sharded) over gloo
+with the CPU oracle injected as the per-rank codec (there is no GPU here;
+tests/test_gpu_codec.py runs the same API on the GPU path) and check the
+result is byte-identical to a single-rank batch."""
 
 import os
 import socket
@@ -14,7 +15,8 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2206_05279_b200.shard import concat_blobs, gather_blobs, shard_range
+from paper_2206_05279_b200.shard import (concat_blobs, compress_sharded, decompress_sharded, gather_blobs,
+                                         shard_range)
 
 
 def test_shard_ranges_cover_exactly():
@@ -43,11 +45,22 @@ def _worker(rank, world, port, q):
     try:
         from paper_2206_05279_b200.synth import smooth_images
 
+        from oracle import oracle as O
+
         imgs = smooth_images(9, 8, 8, seed=3)
         s, e = shard_range(len(imgs), rank, world)
         buf, off = _blobs_for(imgs[s:e])
         out = gather_blobs(buf, off, dst=0)
+        # the product shard API with the oracle as each rank's codec
+        out2 = compress_sharded(imgs, None, None, dst=0, codec=lambda im, m, c: _blobs_for(im))
+        full_buf, full_off = _blobs_for(imgs)
+
+        def dec(b, o, m):
+            return np.stack([O.decompress(bytes(b[o[i]:o[i + 1]])) for i in range(len(o) - 1)])
+        back = decompress_sharded(full_buf, full_off, None, dst=0, codec=dec)
         if rank == 0:
+            assert out2[0].tobytes() == out[0].tobytes() and out2[1].tolist() == out[1].tolist()
+            assert np.array_equal(back, imgs)
             q.put((out[0].tobytes(), out[1].tolist()))
         dist.barrier()
     finally:
