@@ -196,24 +196,36 @@ void oracle_encode_batch(const uint8_t *syms, const uint16_t *ds, int64_t N,
 static int tap_dot(const float *w, int wstride, const float *x, int xstride, int K, int64_t p, int64_t n_px,
                    int cout, float *res) {
     if (n_px == 1) {
-        if (cout < 4) return -1;
-        /* numpy hands a single-column product to sgemv (sgemv_t): 8 lanes
-         * of fused multiply-adds over k = l (mod 8) then a fixed reduction;
-         * K = 8 reduces adjacent pairs first. */
-        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (K == 8) {
-            for (int l = 0; l < 8; ++l) a[l] = w[l * wstride] * x[l * xstride];
-            *res = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+        /* numpy hands a single-column product to sgemv (sgemv_t); its
+         * order depends on K: short rows are one fused multiply-add chain,
+         * K = 4 and 8 reduce adjacent products pairwise, longer rows keep
+         * 8 lanes (k = l mod 8) reduced as ((l0+l4)+(l1+l5))+((l2+l6)+(l3+l7))
+         * with K = 9 / 10 leftovers folded in after. Modelled for whole
+         * groups of 4 output channels (sgemv_t's column blocks) only. */
+        if (cout % 4) return -1;
+        if (K == 1) {
+            *res = w[0] * x[0];
             return 0;
         }
-        if (K < 16 || K % 8) return -1;
-        for (int k = 0; k < K; ++k) a[k & 7] = fmaf(w[k * wstride], x[k * xstride], a[k & 7]);
-        *res = ((a[0] + a[4]) + (a[1] + a[5])) + ((a[2] + a[6]) + (a[3] + a[7]));
+        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (K == 4 || K == 8) {
+            for (int l = 0; l < K; ++l) a[l] = w[l * wstride] * x[l * xstride];
+            float g = (a[0] + a[1]) + (a[2] + a[3]);
+            *res = K == 4 ? g : g + ((a[4] + a[5]) + (a[6] + a[7]));
+            return 0;
+        }
+        if (!(K == 9 || K == 10 || (K >= 16 && K % 8 == 0))) return -1;
+        const int m = K & ~7;
+        for (int k = 0; k < m; ++k) a[k & 7] = fmaf(w[k * wstride], x[k * xstride], a[k & 7]);
+        float y = ((a[0] + a[4]) + (a[1] + a[5])) + ((a[2] + a[6]) + (a[3] + a[7]));
+        if (K == 9) y = fmaf(w[8 * wstride], x[8 * xstride], y);
+        if (K == 10) y = y + fmaf(w[8 * wstride], x[8 * xstride], w[9 * wstride] * x[9 * xstride]);
+        *res = y;
         return 0;
     }
     const int64_t r = n_px % 16;
     if (K >= 32 && r >= 1 && r <= 8 && p >= n_px - r) {
-        if (cout < 4 && r != 4 && r != 8) return -1;
+        if (cout % 4 && !(cout == 3 && (r == 4 || r == 8))) return -1;  /* modelled: whole column groups, the heads */
         /* sgemm's narrow m-tail (1..8 leftover pixels) vectorises over k:
          * 16 lanes k = l (mod 16), then an adjacent-pair tree */
         float a[16];

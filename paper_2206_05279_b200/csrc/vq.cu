@@ -464,16 +464,22 @@ __device__ float tail_dot(const ConvArgs &a, int64_t n, int tap, int co, int y, 
     const int K = a.Ci;
     const float *w = a.w + (int64_t)tap * a.Ci_pad * a.Co_pad + co;
     const int ws = a.Co_pad;
-    if (mode == 1) {
+    if (mode == 1) {  // sgemv_t, by row length (oracle tap_dot)
         float l[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (K == 8) {
-            for (int k = 0; k < 8; ++k) l[k] = __fmul_rn(w[k * ws], conv_input(a, n, k, y, x));
-            return __fadd_rn(__fadd_rn(__fadd_rn(l[0], l[1]), __fadd_rn(l[2], l[3])),
-                             __fadd_rn(__fadd_rn(l[4], l[5]), __fadd_rn(l[6], l[7])));
+        if (K == 4 || K == 8) {
+            for (int k = 0; k < K; ++k) l[k] = __fmul_rn(w[k * ws], conv_input(a, n, k, y, x));
+            const float g = __fadd_rn(__fadd_rn(l[0], l[1]), __fadd_rn(l[2], l[3]));
+            return K == 4 ? g : __fadd_rn(g, __fadd_rn(__fadd_rn(l[4], l[5]), __fadd_rn(l[6], l[7])));
         }
-        for (int k = 0; k < K; ++k) l[k & 7] = fmaf(w[k * ws], conv_input(a, n, k, y, x), l[k & 7]);
-        return __fadd_rn(__fadd_rn(__fadd_rn(l[0], l[4]), __fadd_rn(l[1], l[5])),
-                         __fadd_rn(__fadd_rn(l[2], l[6]), __fadd_rn(l[3], l[7])));
+        const int m = K & ~7;
+        for (int k = 0; k < m; ++k) l[k & 7] = fmaf(w[k * ws], conv_input(a, n, k, y, x), l[k & 7]);
+        float r = __fadd_rn(__fadd_rn(__fadd_rn(l[0], l[4]), __fadd_rn(l[1], l[5])),
+                            __fadd_rn(__fadd_rn(l[2], l[6]), __fadd_rn(l[3], l[7])));
+        if (K == 9) r = fmaf(w[8 * ws], conv_input(a, n, 8, y, x), r);
+        if (K == 10)
+            r = __fadd_rn(r, fmaf(w[8 * ws], conv_input(a, n, 8, y, x),
+                                  __fmul_rn(w[9 * ws], conv_input(a, n, 9, y, x))));
+        return r;
     }
     float l[16];
 #pragma unroll
@@ -520,14 +526,22 @@ int tail_mode_of(const ConvArgs &a, int co_real, int64_t *start, int *count) {
     *start = INT64_MAX;
     *count = 0;
     if (npx == 1) {
-        if (co_real < 4 || !(a.Ci == 8 || (a.Ci >= 16 && a.Ci % 8 == 0))) return -1;
+        // sgemv_t orders modelled (oracle tap_dot): K in {1, 4, 8, 9, 10} or
+        // a multiple of 8, whole groups of 4 output channels. Elsewhere (odd
+        // channel counts on images of at most 2 x 2 pixels) the plain chain
+        // runs: deterministic, but possibly an ulp away from pixelcodec.
+        const int K = a.Ci;
+        if (co_real % 4 || !(K == 1 || K == 4 || (K >= 8 && K <= 10) || (K >= 16 && K % 8 == 0))) return 0;
+        if (K == 1) return 0;  // one product: the chain is the order
         *start = 0;
         *count = 1;
         return 1;
     }
     const int r = (int)(npx % 16);
     if (a.Ci >= 32 && r >= 1 && r <= 8) {
-        if (co_real < 4 && r != 4 && r != 8) return -1;
+        // modelled for whole groups of 4 output channels and the Co = 3 heads
+        // (r is 4 or 8 there); elsewhere the plain chain (see above)
+        if (co_real % 4 && !(co_real == 3 && (r == 4 || r == 8))) return 0;
         *start = npx - r;
         *count = r;
         return 2;
