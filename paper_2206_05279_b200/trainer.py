@@ -107,13 +107,20 @@ def vq_loss(z: torch.Tensor, zq: torch.Tensor, beta: float) -> torch.Tensor:
 def train(config: ModelConfig = ModelConfig(), steps: int = 200, batch: int = 8, dataset: int = 1000,
           size: int = 32, lr: float = 1e-3, alpha: float = 125.0, beta: float = 0.25, seed: int = 0,
           device=None, log_every: int = 0, residual_fn=None,
-          init_scale: float = 1.0) -> tuple[ModelWeights, list]:
+          init_scale: float = 1.0, restart_every: int = 0, data_init: bool = False) -> tuple[ModelWeights, list]:
     """Train on `dataset` synthetic smooth images of size x size; returns the
     weights (with the index histogram of one full pass) and the loss curve.
 
     `residual_fn(images (N, H, W, 3) uint8) -> (N, H, W, 3) uint8` makes the
     targets; default: the codec's own GPU predictor kernel. `init_scale`
-    multiplies the He-normal std of the convolutions (1.0 = model.ts:75-80)."""
+    multiplies the He-normal std of the convolutions (1.0 = model.ts:75-80).
+
+    Against codebook collapse (the reference trainer's failure mode at these
+    settings: every latent maps to one code) two standard VQ-VAE remedies,
+    off by default so the default run is the reference's: `data_init` sets
+    the codebook to encoder outputs of the first batch, and every
+    `restart_every` steps codes unused since the last restart are moved onto
+    randomly chosen current encoder outputs (dead-code restart)."""
     dev = torch.device(device) if device is not None else (
         torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
     init = random_weights(config, seed=seed, scale=init_scale)
@@ -127,11 +134,31 @@ def train(config: ModelConfig = ModelConfig(), steps: int = 200, batch: int = 8,
     picks = np.floor(mulberry32(seed + 1, 0, steps * batch) * dataset).astype(np.int64).reshape(steps, batch)
     B = config.blocks
     losses = []
+    gen = torch.Generator(device="cpu").manual_seed(seed + 2)
+    used = torch.zeros(config.K, dtype=torch.bool, device=dev)
+
+    def sample_latents(z, k):
+        flat = z.detach().permute(0, 2, 3, 1).reshape(-1, z.shape[1])
+        sel = torch.randint(0, flat.shape[0], (k,), generator=gen).to(dev)
+        return flat[sel]
+
     for step in range(steps):
         pick = torch.from_numpy(picks[step]).to(dev)
         x, t = x_all[pick], t_all[pick]
         z = encode(x, p, B)
-        _, zq, zst = quantize(z, p["codebook"])
+        if data_init and step == 0:
+            with torch.no_grad():
+                p["codebook"].copy_(sample_latents(z, config.K))
+        idx, zq, zst = quantize(z, p["codebook"])
+        if restart_every:
+            used[idx.reshape(-1).unique()] = True
+            if step % restart_every == restart_every - 1:
+                dead = (~used).nonzero().reshape(-1)
+                if dead.numel():
+                    with torch.no_grad():
+                        p["codebook"][dead] = sample_latents(z, dead.numel())
+                    opt.state.pop(p["codebook"], None)  # fresh Adam moments for the moved codes
+                used.zero_()
         mu, s = decode(zst, p, B, size, size)
         loss = nll_bits(t, mu, s) + alpha * vq_loss(z, zq, beta)
         opt.zero_grad(set_to_none=True)
@@ -163,11 +190,15 @@ def main(argv=None) -> int:
     ap.add_argument("--alpha", type=float, default=125.0)
     ap.add_argument("--beta", type=float, default=0.25)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--restart-every", type=int, default=0, help="dead-code restart period (0: off)")
+    ap.add_argument("--data-init", action="store_true", help="codebook from the first batch's latents")
+    ap.add_argument("--init-scale", type=float, default=1.0)
     ap.add_argument("--out", default="model.pilw")
     ap.add_argument("--log-every", type=int, default=50)
     a = ap.parse_args(argv)
     w, losses = train(steps=a.steps, batch=a.batch, dataset=a.dataset, size=a.size, lr=a.lr, alpha=a.alpha,
-                      beta=a.beta, seed=a.seed, log_every=a.log_every)
+                      beta=a.beta, seed=a.seed, log_every=a.log_every, restart_every=a.restart_every,
+                      data_init=a.data_init, init_scale=a.init_scale)
     w.save(a.out)
     print(f"saved {a.out}: final loss {losses[-1]:.4f}, hash8 {w.hash8().hex()}")
     return 0
