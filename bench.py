@@ -176,11 +176,13 @@ def cpu_model() -> str:
 def bench_model(name: str):
     """--weights: `random` = random_weights(ModelConfig(), seed=1) (the
     BASELINE config); `trained` = tests/golden/trained.pilw, the same
-    architecture trained by the trainer port."""
+    architecture trained by the trainer port (reference settings: the
+    codebook collapses onto one code); `sharp` = tests/golden/sharp.pilw,
+    trained longer with the codebook kept alive (bpd ~4.9 on CIFAR)."""
     import paper_2206_05279_b200 as pc
 
-    if name == "trained":
-        return pc.ModelWeights.load(os.path.join(REPO, "tests", "golden", "trained.pilw"))
+    if name in ("trained", "sharp"):
+        return pc.ModelWeights.load(os.path.join(REPO, "tests", "golden", f"{name}.pilw"))
     return pc.random_weights(seed=1)
 
 
@@ -554,6 +556,20 @@ def run_gpu(args):
         agree = int((i_fast == i_exact).sum().item())
         extra["index_agreement"] = {"value": agree / i_fast.numel(), "latents": int(i_fast.numel()),
                                     "vs": "exact encoder (bit-identical to the reference's z / indices)"}
+        # a sharp trained model (bpd ~4.9): the fast decoder's bits/dim where
+        # a wrong recentring shift costs bits, against the exact numerics
+        # (containers identical to pixelcodec's) on the same batch
+        if args.weights == "random":
+            sm = bench_model("sharp")
+            r = measure(ctx, groups_h, sm, fast, max(2, args.steps // 2), 1)
+            eb, eo = pc.compress_batch(groups_h[0], sm, exact)
+            bpd_exact = 8.0 * float(eo[-1]) / groups_h[0].size
+            extra["sharp_model"] = {"weights": "tests/golden/sharp.pilw", "round_trip_mb_s": round(r["value"], 3),
+                                    "compress_mb_s": round(r["compress"], 3),
+                                    "decompress_mb_s": round(r["decompress"], 3), "e2e": _round(r["e2e"]),
+                                    "bpd": round(r["bpd"], 5), "bpd_exact": round(bpd_exact, 5),
+                                    "bpd_rel_delta": round((r["bpd"] - bpd_exact) / bpd_exact, 6),
+                                    "lossless": r["lossless"]}
 
     cpu = cpu_port = parity = None
     if rank == 0 and ws == 1 and not args.no_cpu and args.workload == "cifar":
@@ -841,8 +857,8 @@ def main():
     ap.add_argument("--workload", default="cifar", choices=sorted(WORKLOADS) + ["coder"],
                     help="BASELINE config: cifar (configs[1], default), in64 (configs[2]), 1080p (configs[3]), "
                          "coder (configs[4], coder-only lane sweep)")
-    ap.add_argument("--weights", default="random", choices=["random", "trained"],
-                    help="random_weights(seed=1) (default) or tests/golden/trained.pilw")
+    ap.add_argument("--weights", default="random", choices=["random", "trained", "sharp"],
+                    help="random_weights(seed=1) (default), tests/golden/trained.pilw or tests/golden/sharp.pilw")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return _relaunch(args)

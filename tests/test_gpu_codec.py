@@ -709,3 +709,45 @@ def test_sharded_ranks_on_the_gpu_path(full_model):
     rb, ro = pc.compress_batch(imgs, full_model, FAST)
     assert buf == rb.tobytes() and off == ro.tolist()
     assert back == imgs.tobytes()
+
+
+# --- a sharp trained model (tests/golden/sharp.pilw, make_sharp.py) ----------
+
+
+@pytest.fixture(scope="module")
+def sharp_model():
+    return pc.ModelWeights.load(os.path.join(GOLDEN, "sharp.pilw"))
+
+
+def test_sharp_model_exact_matches_reference(golden, sharp_model):
+    """With a model that predicts sharply (bpd ~4.9 vs 5.8 static), the exact
+    network still reproduces pixelcodec: mu / s bit for bit, containers
+    byte-identical, the reference's containers decode exactly."""
+    z = golden("vqvae_sharp.npz")
+    ref = _blobs(z)
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        mu, s = vqvae.decode_to_params(z[f"idx{k}"], sharp_model, img.shape[:2])
+        assert np.array_equal(mu.view(np.uint32), z[f"mu{k}"].view(np.uint32))
+        assert np.array_equal(s.view(np.uint32), z[f"s{k}"].view(np.uint32))
+        assert pc.compress(img, sharp_model, pc.CodecConfig(backend="twar-vqvae", lanes=1 + (k % 2))) == ref[k]
+        assert np.array_equal(pc.decompress(ref[k], sharp_model), img)
+
+
+@pytest.mark.parametrize("H,n", [(32, 512), (64, 128)])
+def test_sharp_model_fast_bpd_within_half_percent(sharp_model, H, n):
+    """north_star's float contract where it is sensitive: with sharp (mu, s)
+    a wrong recentring shift costs bits, so the bf16 fast decoder's bits/dim
+    is compared with the reference arithmetic's (the exact numerics, whose
+    containers equal pixelcodec's) on n images: |delta| / bpd <= 0.5%
+    (measured: +0.006%)."""
+    imgs = smooth_images(n, H, H, seed=91)
+    sizes = {}
+    for cfg in (EXACT, FAST):
+        buf, off = pc.compress_batch(imgs, sharp_model, cfg)
+        assert np.array_equal(pc.decompress_batch(buf, off, sharp_model), imgs)
+        sizes[cfg.numerics] = float(off[-1])
+    rel = (sizes["fast"] - sizes["exact"]) / sizes["exact"]
+    assert abs(rel) <= 0.005, rel
+    bpd = 8 * sizes["exact"] / imgs.size
+    assert bpd < 5.5  # the model is sharp: well below the static backend (~5.8 / 5.5)

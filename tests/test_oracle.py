@@ -196,3 +196,17 @@ def test_exp_statement_matches_numpy(lo, hi):
 
     x = f32_range(lo, hi)
     assert np.array_equal(O.exp_np(x).view(np.uint32), np.exp(x).view(np.uint32))
+
+
+def test_fma_statement_reproduces_reference_sharp_model(golden):
+    """The same pin on the trained sharp model (tests/golden/sharp.pilw):
+    the reference's mu and s equal the explicit statement bit for bit."""
+    m = O.Model.from_bytes(golden("sharp.pilw"))
+    z = golden("vqvae_sharp.npz")
+    for k in range(int(z["n"])):
+        img = z[f"img{k}"]
+        H, W = img.shape[:2]
+        assert np.array_equal(O.encode_indices(img, m), z[f"idx{k}"])
+        mu, s = O.decode_params_exact(z[f"idx{k}"], m, H, W)
+        assert np.array_equal(mu.view(np.uint32), z[f"mu{k}"].view(np.uint32))
+        assert np.array_equal(s.view(np.uint32), z[f"s{k}"].view(np.uint32))
