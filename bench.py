@@ -741,37 +741,75 @@ def _roofline(prof, clk, steps):
     return roofline, stages
 
 
+def _ref_lanes_worker(args):
+    """pixelcodec.tables.interleaved_encode (the reference coder, baseline/_ref)
+    of the config-5 symbols with L lanes -> (states, nbits, payload bytes)."""
+    L, M, n = args
+    sys.path.insert(0, REF_DIR)
+    import numpy as np
+
+    from pixelcodec import logistic, tables
+
+    syms, d, pmfs = _bench_symbols(M, n)
+    enc, _ = tables.build_tables(pmfs, M)
+    ls = tables.interleaved_encode(syms, d.astype(np.uint16), L, enc)
+    nbits = np.array([len(st) for st in ls.streams], np.uint64)
+    payload = b"".join(st.to_bytes()[8:] for st in ls.streams)
+    del logistic
+    return np.array(ls.states, np.uint16), nbits, payload
+
+
+def _bench_symbols(M: int, n: int, seed: int = 0):
+    """report._bench_symbols (report.py:34-44) restated: d uniform over the
+    default grid's 8 distributions, symbol ~ PMF_d, one generator."""
+    import numpy as np
+
+    from paper_2206_05279_b200.logistic import default_grid, residual_distributions
+
+    rng = np.random.default_rng(seed)
+    pmfs = residual_distributions(default_grid(), M)
+    d = rng.integers(0, 8, n).astype(np.uint16)
+    syms = np.empty(n, np.uint8)
+    for i, pmf in enumerate(pmfs):
+        sel = d == i
+        syms[sel] = rng.choice(256, int(sel.sum()), p=pmf.P.astype(np.float64) / (1 << M))
+    return syms, d, pmfs
+
+
 def run_coder(args):
     """configs[4]: coder only. n = 2^26 symbols from the paper's Table-6
     generator (report._bench_symbols, report.py:34-44: d uniform over the 8
     default-grid distributions, symbol ~ PMF_d, seed 0); symbol i -> lane
     i mod L. Encode and decode each timed with CUDA events (device-resident
     symbols / d / lane payloads); GB/s counts algorithmic bytes (symbol + d +
-    payload), the SURVEY §8d unit."""
+    payload), the SURVEY §8d unit. Every lane set is compared byte for byte
+    with the reference coder's (pixelcodec.tables.interleaved_encode from
+    baseline/_ref, run on the host cores in parallel with the GPU sweep).
+    `lane_ns_per_symbol` = decode time / symbols per lane: the chain latency
+    a lane pays per symbol when the lanes are too few to fill the GPU."""
     import numpy as np
     import torch
 
     from paper_2206_05279_b200 import _lib, tables
     from paper_2206_05279_b200.device import ptr, sptr
-    from paper_2206_05279_b200.logistic import default_grid, residual_distributions
 
     _, rank, local = _dist()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     M, n = 12, 1 << 26
-    pmfs = residual_distributions(default_grid(), M)
-    rng = np.random.default_rng(0)
-    d = rng.integers(0, 8, n).astype(np.uint8)
-    syms = np.empty(n, np.uint8)
-    for i, pmf in enumerate(pmfs):
-        sel = d == i
-        syms[sel] = rng.choice(256, int(sel.sum()), p=pmf.P.astype(np.float64) / (1 << M))
+    Ls = [1 << k for k in (10, 12, 14, 16, 18, 20)]
+    syms, d, pmfs = _bench_symbols(M, n)
+    d = d.astype(np.uint8)
+    pool = refs = None
+    if rank == 0 and not args.no_cpu and os.path.isdir(os.path.join(REF_DIR, "pixelcodec")):
+        pool = _cpu_pool(min(len(Ls), len(os.sched_getaffinity(0))))
+        refs = pool.map_async(_ref_lanes_worker, [(L, M, n) for L in Ls])
     enc, dec = tables.build_tables(pmfs, M)
     s_d = torch.from_numpy(syms).to(dev)
     d_d = torch.from_numpy(d).to(dev)
-    rows = []
-    for L in [1 << k for k in (10, 12, 14, 16, 18, 20)]:
+    rows, gpu_lanes = [], {}
+    for L in Ls:
         def encode():
             return tables.encode_lanes_device(s_d, 1, n, L, enc, dev, stream, dsched=d_d)
         scr, cap, nb, st = encode()
@@ -786,6 +824,8 @@ def run_coder(args):
         decode()
         torch.cuda.synchronize(dev)
         assert torch.equal(out, s_d) and int(lstat.max()) == 0
+        gpu_lanes[L] = (scr.cpu().numpy().view(np.uint8), cap, nb.cpu().numpy().view(np.uint32)[:L].copy(),
+                        st.cpu().numpy().view(np.uint16)[:L].copy())
         payload = float(nb.to(torch.int64).sum().item()) / 8.0
         te, td = [], []
         for _ in range(max(args.steps, 1)):
@@ -799,11 +839,20 @@ def run_coder(args):
             te.append(a.elapsed_time(b) / 1e3)
             td.append(b.elapsed_time(c) / 1e3)
         algo = 2.0 * n + payload
+        tdm, tem = statistics.median(td), statistics.median(te)
         rows.append({"lanes": L, "bits_per_symbol": round(8 * payload / n, 4),
-                     "encode_gb_s": round(algo / statistics.median(te) / 1e9, 2),
-                     "decode_gb_s": round(algo / statistics.median(td) / 1e9, 2),
-                     "encode_msym_s": round(n / statistics.median(te) / 1e6, 1),
-                     "decode_msym_s": round(n / statistics.median(td) / 1e6, 1)})
+                     "encode_gb_s": round(algo / tem / 1e9, 2), "decode_gb_s": round(algo / tdm / 1e9, 2),
+                     "encode_msym_s": round(n / tem / 1e6, 1), "decode_msym_s": round(n / tdm / 1e6, 1),
+                     "lane_ns_per_symbol": round(tdm / (n / L) * 1e9, 2)})
+    if refs is not None:
+        for row, L, (rst, rnb, rpay) in zip(rows, Ls, refs.get()):
+            buf, cap, gnb, gst = gpu_lanes[L]
+            nbytes = (gnb.astype(np.int64) + 7) // 8
+            starts = np.arange(L, dtype=np.int64) * cap * 4
+            idx = np.repeat(starts, nbytes) + (np.arange(int(nbytes.sum())) - np.repeat(np.cumsum(nbytes) - nbytes, nbytes))
+            row["byte_identical_to_reference"] = bool(np.array_equal(gst, rst) and np.array_equal(gnb, rnb)
+                                                      and buf[idx].tobytes() == rpay)
+        pool.close()
     if rank == 0:
         peak = None
         try:
@@ -811,13 +860,17 @@ def run_coder(args):
                 peak = json.load(f).get("hbm_gbs")
         except OSError:
             peak = 6650.0
+        for r in rows:
+            r["decode_hbm_frac"] = round(r["decode_gb_s"] / peak, 4)
+            r["encode_hbm_frac"] = round(r["encode_gb_s"] / peak, 4)
         best = max(rows, key=lambda r: r["decode_gb_s"])
         print(json.dumps({"metric": "rANS coder-only decode GB/s (algorithmic bytes)", "value": best["decode_gb_s"],
                           "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
                           "higher_is_better": True, "data": "synthetic",
-                          "config": {"workload": "coder-only sweep, n=2^26 Table-6 symbols, D=8, M=12"},
-                          "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
-                                       "frac": round(best["decode_gb_s"] / (peak / 1.0), 4)},
+                          "config": {"workload": "coder-only sweep, n=2^26 Table-6 symbols (report._bench_symbols, "
+                                                 "seed 0), D=8, M=12, symbol i -> lane i mod L"},
+                          "roofline": {"bound": "hbm", "achieved": best["decode_gb_s"], "peak": peak, "unit": "GB/s",
+                                       "frac": round(best["decode_gb_s"] / peak, 4)},
                           "sweep": rows}), flush=True)
     return 0
 

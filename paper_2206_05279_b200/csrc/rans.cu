@@ -136,25 +136,53 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
                 i -= 16;
             }
         }
-        // strided lanes: inputs of the next (lower) symbols fetched 4 ahead
-        if (i >= 0) {
-            constexpr int P = 4;
-            uint32_t tq[P];
+        // strided lanes (symbol l + i L): the same two-block register ring as
+        // above with 16 scalar loads per block -- consecutive lanes of a warp
+        // read consecutive bytes, so every load is one coalesced request, and
+        // block j + 2's requests are in flight while block j is coded (~32
+        // symbols, several DRAM round trips of chain work ahead)
+        if (i >= 0 && lanes > 1) {
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
+            auto ld = [&](int ii, uint4 &sv, uint4 &hv, uint4 &dv) {  // block with top symbol ii
+                uint32_t s4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0}, d4[4] = {0, 0, 0, 0};
+                if (ii >= 15) {
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
-                const int ii = i - j;
-                const int64_t pos = base + (int64_t)ii * lanes;
-                tq[j] = ii >= 0 ? word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst) : 0u;
-            }
-            for (; i >= 0; --i) {
-                const uint32_t tc = tq[0];
+                    for (int j = 0; j < 16; ++j) {
+                        const int64_t pos = base + (int64_t)(ii - 15 + j) * lanes;
+                        s4[j >> 2] |= (uint32_t)__ldg(syms + pos) << (8 * (j & 3));
+                        if (shift) h4[j >> 2] |= (uint32_t)__ldg(shift + pos) << (8 * (j & 3));
+                        if (dsched) d4[j >> 2] |= (uint32_t)__ldg(dsched + pos) << (8 * (j & 3));
+                    }
+                }
+                sv = make_uint4(s4[0], s4[1], s4[2], s4[3]);
+                hv = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+                dv = make_uint4(d4[0], d4[1], d4[2], d4[3]);
+            };
+            auto blk = [&](const uint4 &sv, const uint4 &hv, const uint4 &dv) {
+                uint32_t t[16];
 #pragma unroll
-                for (int j = 0; j + 1 < P; ++j) tq[j] = tq[j + 1];
-                const int ii = i - P;
-                const int64_t pos = base + (int64_t)ii * lanes;
-                tq[P - 1] = ii >= 0 ? word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst) : 0u;
-                enc_push(e, tc, M);
+                for (int j = 0; j < 16; ++j)
+                    t[j] = word(vbyte(sv, j), vbyte(hv, j), dsched ? vbyte(dv, j) : dconst);
+#pragma unroll
+                for (int j = 15; j >= 0; --j) enc_push(e, t[j], M);
+            };
+            uint4 s0 = z4, s1 = z4, h0 = z4, h1 = z4, d0 = z4, d1 = z4;
+            ld(i, s0, h0, d0);
+            ld(i - 16, s1, h1, d1);
+            for (; i >= 31; i -= 32) {
+                blk(s0, h0, d0);
+                ld(i - 32, s0, h0, d0);
+                blk(s1, h1, d1);
+                ld(i - 48, s1, h1, d1);
             }
+            if (i >= 15) {
+                blk(s0, h0, d0);
+                i -= 16;
+            }
+        }
+        for (; i >= 0; --i) {  // the last < 16 symbols of a lane (lowest indices)
+            const int64_t pos = base + (int64_t)i * lanes;
+            enc_push(e, word(syms[pos], shift ? shift[pos] : 0u, dsched ? dsched[pos] : dconst), M);
         }
         if (e.nacc) *e.wp = (uint32_t)e.acc;
         nbits[k] = (uint32_t)(e.wp - out) * 32u + e.nacc;
@@ -393,32 +421,48 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
                 i += 16;
             }
         }
-        // strided lanes: d / shift of the next symbols fetched 4 ahead
-        if (i < cnt) {
-            constexpr int P = 4;
-            uint32_t dq[P], hq[P];
+        // strided lanes (symbol l + i L): 16-symbol blocks with a two-block
+        // register ring of d / shift (coalesced across the warp's consecutive
+        // lanes, requested ~32 symbols ahead), as for one lane above
+        if (i < cnt && lanes > 1) {
+            auto ld = [&](int ii, uint4 &dv, uint4 &hv) {
+                uint32_t d4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+                if (ii + 16 <= cnt) {
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
-                const int ii = i + j;
-                const int64_t pos = sbase + (int64_t)ii * lanes;
-                dq[j] = ii < cnt ? (dsched ? ((uint32_t)dsched[pos] << M) : dconstT) : 0u;
-                hq[j] = (ii < cnt && unshift) ? unshift[pos] : 0u;
-            }
-            for (; i < cnt; ++i) {
-                const int64_t pos = sbase + (int64_t)i * lanes;
-                const uint32_t dc = dq[0], hc = hq[0];
-#pragma unroll
-                for (int j = 0; j + 1 < P; ++j) {
-                    dq[j] = dq[j + 1];
-                    hq[j] = hq[j + 1];
+                    for (int j = 0; j < 16; ++j) {
+                        const int64_t pos = sbase + (int64_t)(ii + j) * lanes;
+                        if (dsched) d4[j >> 2] |= (uint32_t)__ldg(dsched + pos) << (8 * (j & 3));
+                        if (unshift) h4[j >> 2] |= (uint32_t)__ldg(unshift + pos) << (8 * (j & 3));
+                    }
                 }
-                const int ii = i + P;
-                const int64_t pn = sbase + (int64_t)ii * lanes;
-                dq[P - 1] = ii < cnt ? (dsched ? ((uint32_t)dsched[pn] << M) : dconstT) : 0u;
-                hq[P - 1] = (ii < cnt && unshift) ? unshift[pn] : 0u;
+                dv = make_uint4(d4[0], d4[1], d4[2], d4[3]);
+                hv = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+            };
+            auto blk = [&](const uint4 &dv, const uint4 &hv, int ii) {
                 br.sync();
-                out[pos] = (uint8_t)step(dc, hc);
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    out[sbase + (int64_t)(ii + j) * lanes] =
+                        (uint8_t)step(dsched ? (vbyte(dv, j) << M) : dconstT, vbyte(hv, j));
+            };
+            uint4 d0, d1, h0, h1;
+            ld(i, d0, h0);
+            ld(i + 16, d1, h1);
+            for (; i + 32 <= cnt; i += 32) {
+                blk(d0, h0, i);
+                ld(i + 32, d0, h0);
+                blk(d1, h1, i + 16);
+                ld(i + 48, d1, h1);
             }
+            if (i + 16 <= cnt) {
+                blk(d0, h0, i);
+                i += 16;
+            }
+        }
+        for (; i < cnt; ++i) {  // the last < 16 symbols of a lane
+            const int64_t pos = sbase + (int64_t)i * lanes;
+            br.sync();
+            out[pos] = (uint8_t)step(dsched ? ((uint32_t)dsched[pos] << M) : dconstT, unshift ? unshift[pos] : 0u);
         }
         uint8_t st = 0;
         if (br.A < br.start) st = PILC_ST_UNDERFLOW;
