@@ -57,8 +57,10 @@ WORKLOADS = {
     "cifar": dict(H=32, W=32, N=8192, desc=WORKLOAD),
     "in64": dict(H=64, W=64, N=4096, desc="imagenet64-64x64x3-synthetic-smooth, batch 4096/GPU, twar-vqvae full "
                                           "model (seed 1), M=12, L=1, numerics fast"),
-    "1080p": dict(H=1080, W=1920, N=8, desc="1920x1080x3 synthetic-smooth frames, 8/GPU, split into 64x64 patch "
-                                           "containers (510/frame), twar-vqvae full model (seed 1), M=12, L=1, numerics fast"),
+    "1080p": dict(H=1080, W=1920, N=8, P=64, desc="1920x1080x3 synthetic-smooth frames, 8/GPU, split into 64x64 "
+                  "patch containers (510/frame), twar-vqvae full model (seed 1), M=12, L=1, numerics fast"),
+    "1080p32": dict(H=1080, W=1920, N=8, P=32, desc="1920x1080x3 synthetic-smooth frames, 8/GPU, split into 32x32 "
+                    "patch containers (2040/frame), twar-vqvae full model (seed 1), M=12, L=1, numerics fast"),
 }
 
 
@@ -447,10 +449,10 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
     def api_round():
         if frames is not None:
             from paper_2206_05279_b200 import patches as pt
-            buf, off = pt.compress_frames(frames, model, cfg)
+            buf, off = pt.compress_frames(frames, model, cfg, wl["P"], wl["P"])
             torch.cuda.synchronize(dev)
             t1 = time.perf_counter()
-            out = pt.decompress_frames(buf, off, len(frames), wl["H"], wl["W"], model)
+            out = pt.decompress_frames(buf, off, len(frames), wl["H"], wl["W"], model, wl["P"], wl["P"])
         else:
             buf, off = pc.compress_batch(imgs, model, cfg)
             torch.cuda.synchronize(dev)
@@ -505,10 +507,10 @@ def run_gpu(args):
     exact = pc.CodecConfig(backend="twar-vqvae", numerics="exact")
     wl = WORKLOADS[args.workload]
     frames = None
-    if args.workload == "1080p":
+    if args.workload.startswith("1080p"):
         from paper_2206_05279_b200 import patches as pt
         frames = np.stack([smooth_images(1, wl["H"], wl["W"], seed=1000 * rank + f)[0] for f in range(wl["N"])])
-        plist = [p for f in frames for p in pt.split_frame(f)]
+        plist = [p for f in frames for p in pt.split_frame(f, wl["P"], wl["P"])]
         shapes = sorted({p.shape for p in plist})
         groups_h = [np.stack([p for p in plist if p.shape == sh]) for sh in shapes]
     else:
@@ -517,16 +519,16 @@ def run_gpu(args):
     prof, clk = head["prof"], head["clk"]
 
     lat = None
-    if args.workload == "1080p":
+    if args.workload.startswith("1080p"):
         # single-frame decompress latency: blobs in host RAM -> frame in RAM
         buf, off = head["api"]
-        per = len(pt.patch_grid(wl["H"], wl["W"]))
+        per = len(pt.patch_grid(wl["H"], wl["W"], wl["P"], wl["P"]))
         fb, fo = buf[: int(off[per])], off[: per + 1]
         ts = []
         for _ in range(5):
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            fr = pt.decompress_frames(fb, fo, 1, wl["H"], wl["W"], model)
+            fr = pt.decompress_frames(fb, fo, 1, wl["H"], wl["W"], model, wl["P"], wl["P"])
             ts.append(time.perf_counter() - t0)
         assert np.array_equal(fr[0], frames[0])
         lat = round(1000 * statistics.median(ts), 3)
@@ -908,8 +910,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines")
     ap.add_argument("--headline-only", action="store_true", help="skip the in64 / exact / index sections")
     ap.add_argument("--workload", default="cifar", choices=sorted(WORKLOADS) + ["coder"],
-                    help="BASELINE config: cifar (configs[1], default), in64 (configs[2]), 1080p (configs[3]), "
-                         "coder (configs[4], coder-only lane sweep)")
+                    help="BASELINE config: cifar (configs[1], default), in64 (configs[2]), 1080p / 1080p32 "
+                         "(configs[3], 64x64 / 32x32 patches), coder (configs[4], coder-only lane sweep)")
     ap.add_argument("--weights", default="random", choices=["random", "trained", "sharp"],
                     help="random_weights(seed=1) (default), tests/golden/trained.pilw or tests/golden/sharp.pilw")
     args = ap.parse_args()
