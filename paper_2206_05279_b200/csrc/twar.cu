@@ -14,6 +14,11 @@ namespace {
 struct Params {
     float w[9];
     float b[3];
+    // every weight an integer with |w| <= 2^13 and every bias an integer
+    // with |b| <= 2^22 (the default predictor): with byte contexts each
+    // float32 product and partial sum is an exact integer below 2^24, so the
+    // round-half-away step is the identity and only the mod 256 remains
+    int integral;
 };
 
 __device__ __forceinline__ uint32_t round_mod256(float acc) {
@@ -31,11 +36,13 @@ __device__ __forceinline__ uint32_t round_mod256(float acc) {
     return (uint32_t)m;
 }
 
-__device__ __forceinline__ uint32_t predict(float c0, float c1, float c2, const float *w, float b) {
+__device__ __forceinline__ uint32_t predict(float c0, float c1, float c2, const float *w, float b,
+                                            int integral = 0) {
     float acc = __fmul_rn(w[0], c0);
     acc = __fadd_rn(acc, __fmul_rn(w[1], c1));
     acc = __fadd_rn(acc, __fmul_rn(w[2], c2));
     acc = __fadd_rn(acc, b);
+    if (integral) return (uint32_t)__float2int_rz(acc) & 255u;  // acc is an exact integer (see Params)
     return round_mod256(acc);
 }
 
@@ -71,9 +78,9 @@ __global__ void twar_forward_kernel(const uint8_t *__restrict__ img, uint8_t *__
             ru = x[o - 3 * W];
             if (v > 0) rul = x[o - 3 * W - 3];
         }
-        const uint32_t pr = predict(rul, ru, rl, p.w, p.b[0]);
-        const uint32_t pg = predict(gl, rl, r, p.w + 3, p.b[1]);
-        const uint32_t pb = predict(bl, gl, gg, p.w + 6, p.b[2]);
+        const uint32_t pr = predict(rul, ru, rl, p.w, p.b[0], p.integral);
+        const uint32_t pg = predict(gl, rl, r, p.w + 3, p.b[1], p.integral);
+        const uint32_t pb = predict(bl, gl, gg, p.w + 6, p.b[2], p.integral);
         uint8_t *t = res + n * hw * 3 + o;
         t[0] = (uint8_t)(((uint32_t)r - pr + 128u) & 0xFFu);
         t[1] = (uint8_t)(((uint32_t)gg - pg + 128u) & 0xFFu);
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
                         ul = v > 0 ? na2 : 0.f;
                     }
                     const float lf = v > 0 ? left_a : 0.f;
-                    const uint32_t pr = predict(ul, up, lf, p.w, p.b[0]);
+                    const uint32_t pr = predict(ul, up, lf, p.w, p.b[0], p.integral);
                     const int64_t i = ((int64_t)ua * W + v) * 3;
                     const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;  // t - 128 + pred
                     o[i] = (uint8_t)x;
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
                 if (ok_b && w2 >= 0 && w2 < W) {
                     const float ul = w2 > 0 ? nb2 : 0.f;
                     const float lf = w2 > 0 ? left_b : 0.f;
-                    const uint32_t pr = predict(ul, nb1, lf, p.w, p.b[0]);
+                    const uint32_t pr = predict(ul, nb1, lf, p.w, p.b[0], p.integral);
                     const int64_t i = ((int64_t)ub * W + w2) * 3;
                     const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;
                     o[i] = (uint8_t)x;
@@ -202,11 +209,11 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
         auto gb = [&](int u, int v, float &rL, float &gL, float &bL) {
             const int64_t i0 = ((int64_t)u * W + v) * 3;
             const float r = o[i0];
-            const uint32_t pg = predict(gL, rL, r, p.w + 3, p.b[1]);
+            const uint32_t pg = predict(gL, rL, r, p.w + 3, p.b[1], p.integral);
             const uint32_t g = (unrec(cd, sh, i0 + 1) + pg + 128u) & 0xFFu;
             o[i0 + 1] = (uint8_t)g;
             const float gf = (float)g;
-            const uint32_t pb = predict(bL, gL, gf, p.w + 6, p.b[2]);
+            const uint32_t pb = predict(bL, gL, gf, p.w + 6, p.b[2], p.integral);
             const uint32_t bb = (unrec(cd, sh, i0 + 2) + pb + 128u) & 0xFFu;
             o[i0 + 2] = (uint8_t)bb;
             rL = r;
@@ -241,9 +248,16 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
 
 Params load_params(const float *p12) {
     Params p;
+    p.integral = 1;
     for (int c = 0; c < 3; ++c) {
-        for (int j = 0; j < 3; ++j) p.w[3 * c + j] = p12[4 * c + j];
-        p.b[c] = p12[4 * c + 3];
+        for (int j = 0; j < 3; ++j) {
+            const float w = p12[4 * c + j];
+            p.w[3 * c + j] = w;
+            p.integral &= (w == floorf(w) && fabsf(w) <= 8192.f) ? 1 : 0;
+        }
+        const float b = p12[4 * c + 3];
+        p.b[c] = b;
+        p.integral &= (b == floorf(b) && fabsf(b) <= 4194304.f) ? 1 : 0;
     }
     return p;
 }
