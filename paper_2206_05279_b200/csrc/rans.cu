@@ -142,41 +142,40 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
         // block j + 2's requests are in flight while block j is coded (~32
         // symbols, several DRAM round trips of chain work ahead)
         if (i >= 0 && lanes > 1) {
-            const uint4 z4 = make_uint4(0, 0, 0, 0);
-            auto ld = [&](int ii, uint4 &sv, uint4 &hv, uint4 &dv) {  // block with top symbol ii
-                uint32_t s4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0}, d4[4] = {0, 0, 0, 0};
+            // the loaded bytes stay unpacked in registers until their block is
+            // coded: packing them at load time would wait for the loads there
+            struct Blk {
+                uint32_t s[16], h[16], d[16];
+            };
+            auto ld = [&](int ii, Blk &b) {  // block with top symbol ii
                 if (ii >= 15) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const int64_t pos = base + (int64_t)(ii - 15 + j) * lanes;
-                        s4[j >> 2] |= (uint32_t)__ldg(syms + pos) << (8 * (j & 3));
-                        if (shift) h4[j >> 2] |= (uint32_t)__ldg(shift + pos) << (8 * (j & 3));
-                        if (dsched) d4[j >> 2] |= (uint32_t)__ldg(dsched + pos) << (8 * (j & 3));
+                        b.s[j] = __ldg(syms + pos);
+                        b.h[j] = shift ? __ldg(shift + pos) : 0u;
+                        b.d[j] = dsched ? __ldg(dsched + pos) : dconst;
                     }
                 }
-                sv = make_uint4(s4[0], s4[1], s4[2], s4[3]);
-                hv = make_uint4(h4[0], h4[1], h4[2], h4[3]);
-                dv = make_uint4(d4[0], d4[1], d4[2], d4[3]);
             };
-            auto blk = [&](const uint4 &sv, const uint4 &hv, const uint4 &dv) {
+            auto blk = [&](const Blk &b) {
                 uint32_t t[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    t[j] = word(vbyte(sv, j), vbyte(hv, j), dsched ? vbyte(dv, j) : dconst);
+                for (int j = 0; j < 16; ++j) t[j] = word(b.s[j], b.h[j], b.d[j]);
 #pragma unroll
                 for (int j = 15; j >= 0; --j) enc_push(e, t[j], M);
             };
-            uint4 s0 = z4, s1 = z4, h0 = z4, h1 = z4, d0 = z4, d1 = z4;
-            ld(i, s0, h0, d0);
-            ld(i - 16, s1, h1, d1);
+            Blk b0, b1;
+            ld(i, b0);
+            ld(i - 16, b1);
             for (; i >= 31; i -= 32) {
-                blk(s0, h0, d0);
-                ld(i - 32, s0, h0, d0);
-                blk(s1, h1, d1);
-                ld(i - 48, s1, h1, d1);
+                blk(b0);
+                ld(i - 32, b0);
+                blk(b1);
+                ld(i - 48, b1);
             }
             if (i >= 15) {
-                blk(s0, h0, d0);
+                blk(b0);
                 i -= 16;
             }
         }
@@ -425,37 +424,35 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
         // register ring of d / shift (coalesced across the warp's consecutive
         // lanes, requested ~32 symbols ahead), as for one lane above
         if (i < cnt && lanes > 1) {
-            auto ld = [&](int ii, uint4 &dv, uint4 &hv) {
-                uint32_t d4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+            struct Blk {
+                uint32_t d[16], h[16];  // unpacked: consumed only when the block is decoded
+            };
+            auto ld = [&](int ii, Blk &b) {
                 if (ii + 16 <= cnt) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const int64_t pos = sbase + (int64_t)(ii + j) * lanes;
-                        if (dsched) d4[j >> 2] |= (uint32_t)__ldg(dsched + pos) << (8 * (j & 3));
-                        if (unshift) h4[j >> 2] |= (uint32_t)__ldg(unshift + pos) << (8 * (j & 3));
+                        b.d[j] = dsched ? ((uint32_t)__ldg(dsched + pos) << M) : dconstT;
+                        b.h[j] = unshift ? (uint32_t)__ldg(unshift + pos) : 0u;
                     }
                 }
-                dv = make_uint4(d4[0], d4[1], d4[2], d4[3]);
-                hv = make_uint4(h4[0], h4[1], h4[2], h4[3]);
             };
-            auto blk = [&](const uint4 &dv, const uint4 &hv, int ii) {
+            auto blk = [&](const Blk &b, int ii) {
                 br.sync();
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    out[sbase + (int64_t)(ii + j) * lanes] =
-                        (uint8_t)step(dsched ? (vbyte(dv, j) << M) : dconstT, vbyte(hv, j));
+                for (int j = 0; j < 16; ++j) out[sbase + (int64_t)(ii + j) * lanes] = (uint8_t)step(b.d[j], b.h[j]);
             };
-            uint4 d0, d1, h0, h1;
-            ld(i, d0, h0);
-            ld(i + 16, d1, h1);
+            Blk b0, b1;
+            ld(i, b0);
+            ld(i + 16, b1);
             for (; i + 32 <= cnt; i += 32) {
-                blk(d0, h0, i);
-                ld(i + 32, d0, h0);
-                blk(d1, h1, i + 16);
-                ld(i + 48, d1, h1);
+                blk(b0, i);
+                ld(i + 32, b0);
+                blk(b1, i + 16);
+                ld(i + 48, b1);
             }
             if (i + 16 <= cnt) {
-                blk(d0, h0, i);
+                blk(b0, i);
                 i += 16;
             }
         }
