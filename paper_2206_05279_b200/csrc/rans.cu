@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const int64_t pos = sbase + (int64_t)(ii + j) * lanes;
-                        b.d[j] = dsched ? ((uint32_t)__ldg(dsched + pos) << M) : dconstT;
+                        b.d[j] = dsched ? (uint32_t)__ldg(dsched + pos) : 0u;  // row shift applied at use
                         b.h[j] = unshift ? (uint32_t)__ldg(unshift + pos) : 0u;
                     }
                 }
@@ -440,7 +440,8 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
             auto blk = [&](const Blk &b, int ii) {
                 br.sync();
 #pragma unroll
-                for (int j = 0; j < 16; ++j) out[sbase + (int64_t)(ii + j) * lanes] = (uint8_t)step(b.d[j], b.h[j]);
+                for (int j = 0; j < 16; ++j)
+                    out[sbase + (int64_t)(ii + j) * lanes] = (uint8_t)step(dsched ? (b.d[j] << M) : dconstT, b.h[j]);
             };
             Blk b0, b1;
             ld(i, b0);
