@@ -751,3 +751,17 @@ def test_sharp_model_fast_bpd_within_half_percent(sharp_model, H, n):
     assert abs(rel) <= 0.005, rel
     bpd = 8 * sizes["exact"] / imgs.size
     assert bpd < 5.5  # the model is sharp: well below the static backend (~5.8 / 5.5)
+
+
+def test_full_hd_frame_as_one_container(full_model):
+    """A 1920x1080 frame as a single container (no patches): both numerics
+    round trip, and the fast container is flagged exactly when the fast
+    decoder takes the shape (its tiles must fit shared memory)."""
+    frame = smooth_images(1, 1080, 1920, seed=44)[0]
+    blobs = {}
+    for cfg in (EXACT, FAST):
+        blob = pc.compress(frame, full_model, cfg)
+        assert np.array_equal(pc.decompress(blob, full_model), frame)
+        blobs[cfg.numerics] = blob
+    assert bool(blobs["fast"][8] & ct.FLAG_FAST_DECODER) == ct.fast_decoder(full_model, 1080, 1920)
+    assert not blobs["exact"][8] & ct.FLAG_FAST_DECODER
