@@ -765,3 +765,31 @@ def test_full_hd_frame_as_one_container(full_model):
         blobs[cfg.numerics] = blob
     assert bool(blobs["fast"][8] & ct.FLAG_FAST_DECODER) == ct.fast_decoder(full_model, 1080, 1920)
     assert not blobs["exact"][8] & ct.FLAG_FAST_DECODER
+
+
+def test_edge_cases_of_the_batch_apis(small_model, full_model):
+    """Device lists longer than the batch (empty shares), patch-frame offsets
+    that do not match the frame count, the reference suite's odd model
+    (C = 6, Dc = 4: single-pixel layers outside the modelled sgemv orders run
+    the plain chain) on tiny images, and fast numerics with the schedule
+    checksum."""
+    from paper_2206_05279_b200 import patches as pt
+
+    n = torch.cuda.device_count()
+    two = smooth_images(2, 16, 16, seed=3)
+    buf, off = pc.compress_batch(two, full_model, FAST, devices=[i % n for i in range(3)])
+    assert np.array_equal(pc.decompress_batch(buf, off, full_model, devices=[i % n for i in range(3)]), two)
+    frames = smooth_images(1, 70, 90, seed=5)
+    fb, fo = pt.compress_frames(frames, small_model, EXACT, 32, 32)
+    with pytest.raises(FormatError):
+        pt.decompress_frames(fb, fo[:-1], 1, 70, 90, small_model, 32, 32)
+    odd = pc.random_weights(pc.ModelConfig(K=16, Dc=4, channels=6, blocks=2), seed=2)
+    for shape in ((1, 1), (2, 2), (1, 5), (3, 2)):
+        img = np.random.default_rng(sum(shape)).integers(0, 256, (*shape, 3), dtype=np.uint8)
+        for cfg in (EXACT, FAST):
+            assert np.array_equal(pc.decompress(pc.compress(img, odd, cfg), odd), img)
+    img = smooth_images(1, 24, 40, seed=6)[0]
+    cfg = pc.CodecConfig(backend="twar-vqvae", numerics="fast", debug_schedule_check=True)
+    blob = pc.compress(img, full_model, cfg)
+    assert blob[8] == (ct.FLAG_FAST_DECODER | ct.FLAG_SCHEDULE_CHECKSUM)
+    assert np.array_equal(pc.decompress(blob, full_model), img)
