@@ -793,3 +793,28 @@ def test_edge_cases_of_the_batch_apis(small_model, full_model):
     blob = pc.compress(img, full_model, cfg)
     assert blob[8] == (ct.FLAG_FAST_DECODER | ct.FLAG_SCHEDULE_CHECKSUM)
     assert np.array_equal(pc.decompress(blob, full_model), img)
+
+
+def test_stream_codec_matches_sync_calls(full_model):
+    """StreamCodec (stream.py): pipelined requests (uploads, kernels and
+    downloads on separate streams, results as futures) return exactly what
+    compress_batch / decompress_batch return, in order, including a corrupt
+    request and a request of another shape in between."""
+    from paper_2206_05279_b200.stream import StreamCodec
+
+    batches = [smooth_images(300, 32, 32, seed=s) for s in range(4)] + [smooth_images(7, 17, 29, seed=9)]
+    with StreamCodec(full_model, FAST) as codec:
+        futs = [codec.compress(b) for b in batches]
+        packed = [f.result() for f in futs]
+        backs = [codec.decompress(buf, off) for buf, off in packed]
+        for b, (buf, off), g in zip(batches, packed, backs):
+            rb, ro = pc.compress_batch(b, full_model, FAST)
+            assert np.array_equal(off, ro) and buf.tobytes() == rb.tobytes()
+            assert np.array_equal(g.result(), b)
+        bad = np.array(packed[1][0], copy=True)
+        bad[int(packed[1][1][3]) + 30] ^= 0x08
+        fbad = codec.decompress(bad, packed[1][1])
+        fok = codec.decompress(*packed[2])
+        with pytest.raises(CorruptStreamError):
+            fbad.result()
+        assert np.array_equal(fok.result(), batches[2])
