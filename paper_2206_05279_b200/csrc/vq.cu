@@ -3,14 +3,19 @@
 //
 // Reference: vqvae.encode_to_indices / decode_to_params (vqvae.py:51-113)
 // over nn.conv2d / residual_block / pixel_shuffle / sigmoid (nn.py:15-67).
-// Activations are NHWC float32 in HBM between layers; every conv is one
-// launch of conv_kernel: a CTA owns a 16x16 output tile of one image and a
-// chunk of output channels; input patches (with edge-replicate clamping,
-// which also realises vqvae._even_pad) and weights are staged through
-// shared memory 8 input channels at a time. Epilogues fuse bias, residual,
-// ReLU, pixel shuffle and the whole logistic head. Fixed per-image tiling
-// and accumulation order: outputs are bit-identical for any batch size,
-// which is what makes GPU-compressed blobs decode on any GPU.
+//
+// Two networks share this file's host side:
+//  - the exact network (numerics="exact", and the fallback of the fast one):
+//    conv_kernel performs the reference's float arithmetic operation for
+//    operation (see the comment above it), activations NHWC float32 in HBM
+//    between layers, epilogues fusing bias, residual, ReLU, pixel shuffle
+//    and the whole logistic head; z, indices, mu and s are bit-identical to
+//    pixelcodec's;
+//  - the fast network (numerics="fast"): the tcgen05 kernels of tc_conv.cu
+//    (fp16-split encoder, bf16 decoder), driven by tf_encode / tc_decode.
+// Both are a fixed sequence of operations per output, independent of batch
+// size, tiling, GPU and GPU count, which is what makes a blob decode on any
+// GPU; the container's header flag 0x80 says which decoder made it.
 
 #include <math.h>
 #include <string.h>
