@@ -106,7 +106,11 @@ __device__ __forceinline__ uint32_t unrec(const uint8_t *coded, const uint8_t *s
 
 __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
     const uint8_t *__restrict__ coded, const uint8_t *__restrict__ shift, uint8_t *__restrict__ out,
-    int64_t n_img, int H, int W, Params p, int stage_in_smem) {
+    int64_t n_img, int H, int W, Params p, int stage_in_smem, int rp) {
+    // rp: row pitch in bytes of the working image (3 W in global memory; in
+    // shared memory padded so the lanes' rows -- and the red wavefront's
+    // skewed diagonals -- fall in different banks: unpadded 64-pixel rows
+    // put all 32 lanes in two banks)
     extern __shared__ uint8_t s_img[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t hw3 = (int64_t)H * W * 3;
@@ -115,15 +119,22 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
         const uint8_t *cd = coded + n * hw3;
         const uint8_t *sh = shift ? shift + n * hw3 : nullptr;
         uint8_t *o_g = out + n * hw3;
-        uint8_t *o = stage_in_smem ? s_img + (int64_t)warp * 2 * hw3 : o_g;
-        const bool vec = stage_in_smem && ((hw3 | reinterpret_cast<uintptr_t>(cd) | reinterpret_cast<uintptr_t>(o_g) |
-                                            (sh ? reinterpret_cast<uintptr_t>(sh) : 0)) & 15) == 0;
+        const int64_t img_b = (int64_t)H * rp;  // bytes of one working image
+        uint8_t *o = stage_in_smem ? s_img + (int64_t)warp * 2 * img_b : o_g;
+        const int w3 = 3 * W;
+        const bool vec = stage_in_smem && (w3 & 15) == 0 && (rp & 3) == 0 &&
+                         ((reinterpret_cast<uintptr_t>(cd) | reinterpret_cast<uintptr_t>(o_g) |
+                           (sh ? reinterpret_cast<uintptr_t>(sh) : 0)) & 15) == 0;
         if (stage_in_smem) {
             // stage the un-recentred residual t in shared memory (coalesced
-            // 16-byte loads): the wavefront below reads it at smem latency
-            uint8_t *tb = o + hw3;
+            // 16-byte loads, rows re-pitched): the wavefront below reads it at
+            // smem latency
+            uint8_t *tb = o + img_b;
             if (vec) {
-                for (int64_t i = 16 * lane; i < hw3; i += 512) {
+                const int cpr = w3 >> 4;  // 16-byte chunks per row
+                for (int64_t c = lane; c < (int64_t)H * cpr; c += 32) {
+                    const int u = (int)(c / cpr), j = (int)(c - (int64_t)u * cpr) * 16;
+                    const int64_t i = (int64_t)u * w3 + j;
                     uint4 c4 = *reinterpret_cast<const uint4 *>(cd + i);
                     if (sh) {
                         const uint4 s4 = *reinterpret_cast<const uint4 *>(sh + i);
@@ -132,10 +143,17 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
 #pragma unroll
                         for (int e = 0; e < 4; ++e) cw[e] = __vadd4(__vadd4(cw[e], sw[e]), 0x80808080u);  // bytewise mod 256
                     }
-                    *reinterpret_cast<uint4 *>(tb + i) = c4;
+                    uint32_t *d = reinterpret_cast<uint32_t *>(tb + (int64_t)u * rp + j);
+                    d[0] = c4.x;
+                    d[1] = c4.y;
+                    d[2] = c4.z;
+                    d[3] = c4.w;
                 }
             } else {
-                for (int64_t i = lane; i < hw3; i += 32) tb[i] = (uint8_t)unrec(cd, sh, i);
+                for (int64_t i = lane; i < hw3; i += 32) {
+                    const int u = (int)(i / w3), j = (int)(i - (int64_t)u * w3);
+                    tb[(int64_t)u * rp + j] = (uint8_t)unrec(cd, sh, i);
+                }
             }
             __syncwarp();
             cd = tb;
@@ -171,15 +189,15 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
                 if (ok_a && v >= 0 && v < W) {
                     float up, ul;
                     if (lane == 0) {  // row above the pair: decoded by the previous pair
-                        up = ua > 0 ? (float)o[((int64_t)(ua - 1) * W + v) * 3] : 0.f;
-                        ul = (ua > 0 && v > 0) ? (float)o[((int64_t)(ua - 1) * W + v - 1) * 3] : 0.f;
+                        up = ua > 0 ? (float)o[(int64_t)(ua - 1) * rp + v * 3] : 0.f;
+                        ul = (ua > 0 && v > 0) ? (float)o[(int64_t)(ua - 1) * rp + (v - 1) * 3] : 0.f;
                     } else {
                         up = na1;
                         ul = v > 0 ? na2 : 0.f;
                     }
                     const float lf = v > 0 ? left_a : 0.f;
                     const uint32_t pr = predict(ul, up, lf, p.w, p.b[0], p.integral);
-                    const int64_t i = ((int64_t)ua * W + v) * 3;
+                    const int64_t i = (int64_t)ua * rp + v * 3;
                     const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;  // t - 128 + pred
                     o[i] = (uint8_t)x;
                     va = (float)x;
@@ -190,7 +208,7 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
                     const float ul = w2 > 0 ? nb2 : 0.f;
                     const float lf = w2 > 0 ? left_b : 0.f;
                     const uint32_t pr = predict(ul, nb1, lf, p.w, p.b[0], p.integral);
-                    const int64_t i = ((int64_t)ub * W + w2) * 3;
+                    const int64_t i = (int64_t)ub * rp + w2 * 3;
                     const uint32_t x = (unrec(cd, sh, i) + pr + 128u) & 0xFFu;
                     o[i] = (uint8_t)x;
                     vb = (float)x;
@@ -207,7 +225,7 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
         // at (u, v) and (u, v - 1) only); rows are independent, each lane
         // walks two of them (lane + 64k and lane + 32 + 64k) side by side
         auto gb = [&](int u, int v, float &rL, float &gL, float &bL) {
-            const int64_t i0 = ((int64_t)u * W + v) * 3;
+            const int64_t i0 = (int64_t)u * rp + v * 3;
             const float r = o[i0];
             const uint32_t pg = predict(gL, rL, r, p.w + 3, p.b[1], p.integral);
             const uint32_t g = (unrec(cd, sh, i0 + 1) + pg + 128u) & 0xFFu;
@@ -236,14 +254,49 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
         if (stage_in_smem) {
             // coalesced copy-out, 16 bytes per lane when aligned
             if (vec) {
-                for (int64_t i = 16 * lane; i < hw3; i += 512)
-                    *reinterpret_cast<uint4 *>(o_g + i) = *reinterpret_cast<const uint4 *>(o + i);
+                const int cpr = w3 >> 4;
+                for (int64_t c = lane; c < (int64_t)H * cpr; c += 32) {
+                    const int u = (int)(c / cpr), j = (int)(c - (int64_t)u * cpr) * 16;
+                    const uint32_t *d = reinterpret_cast<const uint32_t *>(o + (int64_t)u * rp + j);
+                    *reinterpret_cast<uint4 *>(o_g + (int64_t)u * w3 + j) = make_uint4(d[0], d[1], d[2], d[3]);
+                }
             } else {
-                for (int64_t i = lane; i < hw3; i += 32) o_g[i] = o[i];
+                for (int64_t i = lane; i < hw3; i += 32) {
+                    const int u = (int)(i / w3), j = (int)(i - (int64_t)u * w3);
+                    o_g[i] = o[(int64_t)u * rp + j];
+                }
             }
             __syncwarp();
         }
     }
+}
+
+// Shared-memory row pitch for twar_decode_kernel: a multiple of 4 bytes
+// >= 3 W with the fewest bank conflicts for the red wavefront's skewed
+// accesses (lane u at byte 3 s + u (rp - 3)) and the green / blue sweep's
+// (lane u at byte u rp + 3 v), over the four byte phases.
+int decode_pitch(int W) {
+    int best_rp = 3 * W, best = 1 << 30;
+    for (int rp = (3 * W + 3) & ~3; rp < 3 * W + 260; rp += 4) {
+        int worst = 0;
+        for (int pat = 0; pat < 2; ++pat)
+            for (int ph = 0; ph < 4; ++ph) {
+                int words[32][32], cnt[32] = {0};
+                for (int u = 0; u < 32; ++u) {
+                    const long long a = pat == 0 ? 3LL * (ph + 64) + (long long)u * (rp - 3) : (long long)u * rp + ph;
+                    const int wd = (int)(a >> 2), bk = wd & 31;
+                    bool dup = false;
+                    for (int k = 0; k < cnt[bk]; ++k) dup |= words[bk][k] == wd;
+                    if (!dup) words[bk][cnt[bk]++] = wd;
+                }
+                for (int b = 0; b < 32; ++b) worst = worst > cnt[b] ? worst : cnt[b];
+            }
+        if (worst < best) {
+            best = worst;
+            best_rp = rp;
+        }
+    }
+    return best_rp;
 }
 
 Params load_params(const float *p12) {
@@ -288,8 +341,10 @@ extern "C" int pilc_twar_decode(const uint8_t *coded, const uint8_t *shift, uint
     if (n_img < 0 || H < 1 || W < 1 || !params12_host) return PILC_E_ARG;
     if (n_img == 0) return PILC_OK;
     const int64_t hw3 = (int64_t)H * W * 3;
-    const int stage = 2 * hw3 * kDecWarps <= 200 * 1024;  // output + staged residual per warp
-    const size_t smem = stage ? (size_t)(2 * hw3 * kDecWarps) : 0;
+    const int rp_s = decode_pitch(W);
+    const int stage = 2 * (int64_t)H * rp_s * kDecWarps <= 200 * 1024;  // output + staged residual per warp
+    const int rp = stage ? rp_s : 3 * W;
+    const size_t smem = stage ? (size_t)(2 * (int64_t)H * rp * kDecWarps) : 0;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(twar_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t blocks = ceil_div64(n_img, kDecWarps);
@@ -298,7 +353,7 @@ extern "C" int pilc_twar_decode(const uint8_t *coded, const uint8_t *shift, uint
 {
         ProfScope _ps(PROF_TWAR_DEC, as_stream(stream), (double)n_img * hw3);
         twar_decode_kernel<<<(unsigned)blocks, 32 * kDecWarps, smem, as_stream(stream)>>>(
-        coded, shift, img, n_img, H, W, load_params(params12_host), stage);
+        coded, shift, img, n_img, H, W, load_params(params12_host), stage, rp);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
