@@ -120,7 +120,9 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
         const uint8_t *sh = shift ? shift + n * hw3 : nullptr;
         uint8_t *o_g = out + n * hw3;
         const int64_t img_b = (int64_t)H * rp;  // bytes of one working image
-        uint8_t *o = stage_in_smem ? s_img + (int64_t)warp * 2 * img_b : o_g;
+        // staged: one buffer per warp, decoded in place (every residual byte is
+        // read once, just before its pixel's output overwrites it)
+        uint8_t *o = stage_in_smem ? s_img + (int64_t)warp * img_b : o_g;
         const int w3 = 3 * W;
         const bool vec = stage_in_smem && (w3 & 15) == 0 && (rp & 3) == 0 &&
                          ((reinterpret_cast<uintptr_t>(cd) | reinterpret_cast<uintptr_t>(o_g) |
@@ -129,11 +131,11 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
             // stage the un-recentred residual t in shared memory (coalesced
             // 16-byte loads, rows re-pitched): the wavefront below reads it at
             // smem latency
-            uint8_t *tb = o + img_b;
+            uint8_t *tb = o;
             if (vec) {
                 const int cpr = w3 >> 4;  // 16-byte chunks per row
-                for (int64_t c = lane; c < (int64_t)H * cpr; c += 32) {
-                    const int u = (int)(c / cpr), j = (int)(c - (int64_t)u * cpr) * 16;
+                for (int c = lane; c < H * cpr; c += 32) {
+                    const int u = c / cpr, j = (c - u * cpr) * 16;
                     const int64_t i = (int64_t)u * w3 + j;
                     uint4 c4 = *reinterpret_cast<const uint4 *>(cd + i);
                     if (sh) {
@@ -255,8 +257,8 @@ __global__ void __launch_bounds__(32 * kDecWarps) twar_decode_kernel(
             // coalesced copy-out, 16 bytes per lane when aligned
             if (vec) {
                 const int cpr = w3 >> 4;
-                for (int64_t c = lane; c < (int64_t)H * cpr; c += 32) {
-                    const int u = (int)(c / cpr), j = (int)(c - (int64_t)u * cpr) * 16;
+                for (int c = lane; c < H * cpr; c += 32) {
+                    const int u = c / cpr, j = (c - u * cpr) * 16;
                     const uint32_t *d = reinterpret_cast<const uint32_t *>(o + (int64_t)u * rp + j);
                     *reinterpret_cast<uint4 *>(o_g + (int64_t)u * w3 + j) = make_uint4(d[0], d[1], d[2], d[3]);
                 }
@@ -342,9 +344,9 @@ extern "C" int pilc_twar_decode(const uint8_t *coded, const uint8_t *shift, uint
     if (n_img == 0) return PILC_OK;
     const int64_t hw3 = (int64_t)H * W * 3;
     const int rp_s = decode_pitch(W);
-    const int stage = 2 * (int64_t)H * rp_s * kDecWarps <= 200 * 1024;  // output + staged residual per warp
+    const int stage = (int64_t)H * rp_s * kDecWarps <= 200 * 1024;  // one image per warp, decoded in place
     const int rp = stage ? rp_s : 3 * W;
-    const size_t smem = stage ? (size_t)(2 * (int64_t)H * rp * kDecWarps) : 0;
+    const size_t smem = stage ? (size_t)((int64_t)H * rp * kDecWarps) : 0;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(twar_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int64_t blocks = ceil_div64(n_img, kDecWarps);
