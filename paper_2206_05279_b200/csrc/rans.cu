@@ -214,7 +214,10 @@ struct BitReader {
     uint32_t ring_stride;  // bytes between ring words q and q + 1 (blockDim.x * 4): word-interleaved
                            // across the block's threads, so same-q reads of a warp hit 32 banks
     int hi_c;            // last chunk holding payload bits
-    int A, cnt, start, wn, ci;  // ci: lowest chunk issued to the ring
+    int cnt, start, wn, ci;  // ci: lowest chunk issued to the ring
+    // read position A = 32 (wn + 1) + cnt (the window's bottom is word wn's
+    // top); kept implicit so the per-symbol path does not update it
+    __device__ __forceinline__ int A() const { return 32 * (wn + 1) + cnt; }
     uint32_t hi, lo;     // window: bits [A - cnt, A), left-aligned (bit A-1 at bit 63 of hi:lo)
 
     __device__ __forceinline__ uint4 direct(int c) const {
@@ -244,9 +247,9 @@ struct BitReader {
         ring_stride = stride_bytes;
         start = start_bit;  // 0..127
         hi_c = nb ? (int)((start_bit + nb - 1) >> 7) : -1;
-        A = start_bit + (int)nb;
-        const int wt = (A - 1) >> 5;  // word holding bit A-1 (arithmetic: -1 when A == 0)
-        const int nt = A - 32 * wt;   // its valid bits, 1..32
+        const int A0 = start_bit + (int)nb;
+        const int wt = (A0 - 1) >> 5;  // word holding bit A0-1 (arithmetic: -1 when A0 == 0)
+        const int nt = A0 - 32 * wt;   // its valid bits, 1..32
         const uint32_t w2 = word(wt - 1);
         hi = (word(wt) << (32 - nt)) | (nt < 32 ? w2 >> nt : 0u);
         lo = w2 << (32 - nt);
@@ -289,7 +292,6 @@ struct BitReader {
         hi = __funnelshift_l(lo, hi, e8);
         lo <<= b;
         cnt -= (int)b;
-        A -= (int)b;
         // refill below the valid bits (lo is zero here) with word wn
         const bool p = cnt < 32;
         const uint32_t src = ring_s + (uint32_t)(wn & (4 * kRing - 1)) * ring_stride;
@@ -463,8 +465,8 @@ __global__ void __launch_bounds__(512) rans_decode_kernel(
             out[pos] = (uint8_t)step(dsched ? ((uint32_t)dsched[pos] << M) : dconstT, unshift ? unshift[pos] : 0u);
         }
         uint8_t st = 0;
-        if (br.A < br.start) st = PILC_ST_UNDERFLOW;
-        else if (state != T || br.A != br.start) st = PILC_ST_END_STATE;
+        if (br.A() < br.start) st = PILC_ST_UNDERFLOW;
+        else if (state != T || br.A() != br.start) st = PILC_ST_END_STATE;
         lane_status[k] = st;
         asm volatile("cp.async.wait_all;" ::: "memory");  // ring slots are reused by the next lane
     }
