@@ -107,6 +107,17 @@ def _ref_worker(args):
     return int(sum(im.size for im in imgs)), time.perf_counter() - t0, sizes, blobs
 
 
+def _ref_blobs_worker(imgs):
+    """pixelcodec.compress (twar-vqvae, full model, defaults) of each image."""
+    sys.path.insert(0, REF_DIR)
+    import pixelcodec
+    from pixelcodec.weights import ModelConfig, random_weights
+
+    m = random_weights(ModelConfig(), seed=1)
+    cfg = pixelcodec.CodecConfig(backend="twar-vqvae")
+    return [pixelcodec.compress(im, m, cfg) for im in imgs]
+
+
 def _port_worker(args):
     imgs, model_bytes = args
     import numpy as np
@@ -696,6 +707,29 @@ def run_gpu(args):
                       "exact_byte_identical": same / n,
                       "note": "bpd (numerics fast) vs pixelcodec on the same images and weights; "
                               "exact_byte_identical = exact-numerics containers equal to pixelcodec's"}
+            # the same checks on IN64 images and on odd shapes (one container each)
+            extra_imgs = list(smooth_images(256, 64, 64, seed=0))
+            for k, (h, w) in enumerate([(17, 29), (33, 65), (1, 1), (7, 3), (100, 40), (56, 64), (2, 2), (31, 1)]):
+                extra_imgs += list(smooth_images(2, h, w, seed=50 + k))
+            pool = _cpu_pool(procs)
+            try:
+                chunks = [extra_imgs[i::procs] for i in range(procs)]
+                got = pool.map(_ref_blobs_worker, chunks)
+            finally:
+                pool.close()
+            ref_blobs = [None] * len(extra_imgs)
+            for i, g in enumerate(got):
+                ref_blobs[i::procs] = g
+            eb2, eo2 = pc.compress_batch(extra_imgs, model, exact)
+            fb2, fo2 = pc.compress_batch(extra_imgs[:256], model, fast)
+            same2 = sum(bytes(eb2[int(eo2[i]): int(eo2[i + 1])]) == ref_blobs[i] for i in range(len(extra_imgs)))
+            ref64 = 8.0 * sum(len(b) for b in ref_blobs[:256]) / (256 * 64 * 64 * 3)
+            fast64 = 8.0 * float(fo2[-1]) / (256 * 64 * 64 * 3)
+            parity["more_shapes"] = {
+                "images": len(extra_imgs), "exact_byte_identical": same2 / len(extra_imgs),
+                "in64_bpd_ref": round(ref64, 5), "in64_bpd": round(fast64, 5),
+                "in64_bpd_rel_delta": round((fast64 - ref64) / ref64, 6),
+                "note": "256 IN64 images + 16 odd shapes (1x1 .. 100x40) against pixelcodec.compress"}
         model_bytes = model.to_bytes()
         v, nbytes, wall = cpu_port_run(imgs[: 8 * procs], procs, model_bytes)
         cpu_port = {"value": round(v, 4), "unit": "MB/s", "cores": procs, "kind": "port",
