@@ -1112,7 +1112,7 @@ extern "C" int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model,
 
 namespace {
 
-int simt_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,
+int exact_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,
                 int32_t Dc, int32_t B, const Layout &L, const Work &w, uint8_t *idx_out, float *z_out,
                 cudaStream_t s) {
     const int He = H + (H & 1), We = W + (W & 1), gh = He / 2, gw = We / 2;
@@ -1317,16 +1317,27 @@ int vq_encode(int path, const uint8_t *img, int64_t n_img, int32_t H, int32_t W,
     const Layout L = make_layout(K, Dc, C, B);
     cudaStream_t s = as_stream(stream);
     if (path == 0 && L.tf) {
+        // the tcgen05 encoder in batches below its 32-bit pixel-index limit
+        // (padded latent grid), so the path depends on (model config, H, W)
+        // only; images too wide for its tiles' shared memory run the exact
+        // network (any outputs already written are overwritten)
+        const int gh = (H + 1) / 2, gw = (W + 1) / 2;
+        const int64_t per = (int64_t)(gh + 2) * (gw + 2);
+        const int64_t cap = ((int64_t)1 << 31) / per - 1;
+        int rc = cap < 1 ? PILC_E_UNSUPPORTED : PILC_OK;
         TfWork tw;
-        if (tf_ws(n_img, H, W, B, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-        const int rc = tf_encode(img, n_img, H, W, model, K, Dc, B, L, tw, idx_out, z_out, s);
-        // images too wide for the tcgen05 tiles' shared memory: fp32 SIMT
-        // kernels (the choice depends on the shape only; outputs overwritten)
+        if (!rc && tf_ws(n_img < cap ? n_img : cap, H, W, B, &tw, (char *)workspace) > ws_bytes) return PILC_E_ARG;
+        for (int64_t i0 = 0; !rc && i0 < n_img; i0 += cap) {
+            const int64_t nb = n_img - i0 < cap ? n_img - i0 : cap;
+            if (i0) tf_ws(nb, H, W, B, &tw, (char *)workspace);
+            rc = tf_encode(img + i0 * (int64_t)H * W * 3, nb, H, W, model, K, Dc, B, L, tw,
+                           idx_out + i0 * (int64_t)gh * gw, z_out ? z_out + i0 * (int64_t)gh * gw * Dc : nullptr, s);
+        }
         if (rc != PILC_E_UNSUPPORTED) return rc;
     }
     Work w;
     if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-    return simt_encode(img, n_img, H, W, model, K, Dc, B, L, w, idx_out, z_out, s);
+    return exact_encode(img, n_img, H, W, model, K, Dc, B, L, w, idx_out, z_out, s);
 }
 
 }  // namespace
@@ -1350,7 +1361,7 @@ extern "C" int pilc_vq_encode_exact(const uint8_t *img, int64_t n_img, int32_t H
 
 namespace {
 
-int simt_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *model, const Layout &L, int B,
+int exact_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *model, const Layout &L, int B,
                 const double *thr, int D, const Work &w, uint8_t *shift_out, uint8_t *d_out, float *mu_out,
                 float *s_out, cudaStream_t s) {
     const int gh = (H + 1) / 2, gw = (W + 1) / 2;
@@ -1559,7 +1570,7 @@ int vq_decode(int path, const uint8_t *idx, int64_t n_img, int32_t H, int32_t W,
     }
     Work w;
     if (ws_parts(n_img, H, W, Dc, C, &w, (char *)workspace) > ws_bytes) return PILC_E_ARG;
-    return simt_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
+    return exact_decode(idx, n_img, H, W, model, L, B, thr, D, w, shift_out, d_out, mu_out, s_out, s);
 }
 
 }  // namespace
