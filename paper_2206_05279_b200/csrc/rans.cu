@@ -49,16 +49,27 @@ __device__ __forceinline__ void st_if(uint32_t *p, uint32_t v, bool on) {
         : "memory");
 }
 
-__device__ __forceinline__ void enc_push(EncState &e, uint32_t t, int M) {
+// one symbol's bits into the accumulator, no flush (nacc stays < 64 for two
+// symbols after a flush: < 32 + 2 x 12)
+__device__ __forceinline__ void enc_bits(EncState &e, uint32_t t, int M) {
     const uint32_t b = ((t & 0xFFFFu) + e.S) >> M;
     e.acc |= (uint64_t)(e.S & ((1u << b) - 1u)) << e.nacc;
     e.nacc += b;
     e.S = (e.S >> b) + (t >> 16);
+}
+
+// a complete 32-bit word out, branch-free (leaves nacc < 32)
+__device__ __forceinline__ void enc_flush(EncState &e) {
     const bool f = e.nacc >= 32u;
     st_if(e.wp, (uint32_t)e.acc, f);
     e.wp += f ? 1 : 0;
     e.acc = f ? (e.acc >> 32) : e.acc;
     e.nacc -= f ? 32u : 0u;
+}
+
+__device__ __forceinline__ void enc_push(EncState &e, uint32_t t, int M) {
+    enc_bits(e, t, M);
+    enc_flush(e);
 }
 
 template <bool SMEM>
@@ -120,7 +131,11 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
                 for (int j = 0; j < 16; ++j)
                     t[j] = word(vbyte(sv, j), vbyte(hv, j), dsched ? vbyte(dv, j) : dconst);
 #pragma unroll
-                for (int j = 15; j >= 0; --j) enc_push(e, t[j], M);
+                for (int j = 15; j >= 1; j -= 2) {  // one flush per two symbols
+                    enc_bits(e, t[j], M);
+                    enc_bits(e, t[j - 1], M);
+                    enc_flush(e);
+                }
             };
             uint4 s0 = z4, s1 = z4, h0 = z4, h1 = z4, d0 = z4, d1 = z4;
             ld(i, s0, h0, d0);
@@ -163,7 +178,11 @@ __global__ void __launch_bounds__(kThreads) rans_encode_kernel(
 #pragma unroll
                 for (int j = 0; j < 16; ++j) t[j] = word(b.s[j], b.h[j], b.d[j]);
 #pragma unroll
-                for (int j = 15; j >= 0; --j) enc_push(e, t[j], M);
+                for (int j = 15; j >= 1; j -= 2) {  // one flush per two symbols
+                    enc_bits(e, t[j], M);
+                    enc_bits(e, t[j - 1], M);
+                    enc_flush(e);
+                }
             };
             Blk b0, b1;
             ld(i, b0);
@@ -301,7 +320,7 @@ struct BitReader {
             : "+r"(w)
             : "r"(src), "r"(p ? 1u : 0u)
             : "memory");
-        const uint32_t sh = (uint32_t)cnt & 31u;
+        const uint32_t sh = (uint32_t)cnt;  // < 32 when p (the only case whose result is kept)
         hi = p ? (hi | (w >> sh)) : hi;
         lo = p ? (w << (32u - sh)) : lo;
         cnt = p ? cnt + 32 : cnt;
