@@ -805,6 +805,9 @@ def _roofline(prof, clk, steps):
         "tc3_block_kernel": "one encoder residual block per launch (conv1 + conv2, intermediate in shared memory), "
                             "3-product fp16 split on tcgen05 kind::f16; algorithmic FLOPs = 2 convs x 2*N*H*W*32*32*9 "
                             "(MMA FLOPs issued = 3x that)",
+        "enc_trunk_kernel": "encoder trunk (all B residual blocks + the 1x1 projection of one image per CTA iteration, "
+                            "activations in shared memory), 3-product fp16 split on tcgen05 kind::f16; algorithmic "
+                            "FLOPs = (2B x 9 + 1) x 2*N*H*W*32*32 (MMA FLOPs issued = 3x that)",
         "dec_trunk_kernel": "decoder trunk (gather + all 2B bf16 block convs, activations in shared memory, G images per "
                             "CTA iteration); algorithmic FLOPs = 2B x 2*N*gh*gw*32*32*9",
         "argmin_kernel": "codebook distance GEMM (3xTF32 tcgen05) + proven-margin screen + exact f64 rescore (3*n*K*Dc FLOPs)",
@@ -835,7 +838,8 @@ def _roofline(prof, clk, steps):
         # N=32-output convs cannot approach the dense peak. Cycles per
         # 128-row K=16 step (algorithmic 2*128*32*16 FLOP): bf16 convs 44;
         # the 3-product fp16 encoder (N=64 + N=32 MMAs) 92.
-        floor_cyc = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0}.get(name)
+        floor_cyc = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0,
+                     "enc_trunk_kernel": 92.0}.get(name)
         if floor_cyc and roofline and roofline.get("bound") == "tensor":
             att = 2.0 * 128 * 32 * 16 / floor_cyc * sm * mhz * 1e6 / 1e12
             roofline["mma_floor"] = {"peak": round(att, 1), "unit": "TFLOP/s",
@@ -851,7 +855,7 @@ def _roofline(prof, clk, steps):
                 "gather_kernel": "dec_table_kernel", "blob_sizes+scan": "blob_sizes_kernel"}
     hbm_peak = peaks.get("hbm_gbs")
     tpeak = peaks.get("bf16_tflops")
-    floor = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0}
+    floor = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0, "enc_trunk_kernel": 92.0}
     stages = {}
     for k, (n, ms, units) in prof.items():
         e = {"launches": n, "ms_per_step": round(ms / steps, 4)}

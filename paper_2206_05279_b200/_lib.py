@@ -117,6 +117,7 @@ def call(name: str, *args) -> int:
 
 TUNE_BLOCK_FUSION = 0
 TUNE_DEC_TRUNK = 1
+TUNE_ENC_TRUNK = 2
 
 
 def set_tuning(key: int, value: int) -> int:

@@ -38,6 +38,7 @@ enum ProfCat {
     PROF_ENC_FRONT,
     PROF_TC3_BLOCK,
     PROF_DEC_TRUNK,
+    PROF_ENC_TRUNK,
     PROF_NCAT
 };
 void *prof_begin(int cat, cudaStream_t s, double units);
@@ -50,7 +51,7 @@ struct ProfScope {
 };
 
 // Library tuning switches (pilc_set_tuning); defaults are the production path.
-enum { PILC_TUNE_BLOCK_FUSION = 0, PILC_TUNE_DEC_TRUNK = 1, PILC_TUNE_N };
+enum { PILC_TUNE_BLOCK_FUSION = 0, PILC_TUNE_DEC_TRUNK = 1, PILC_TUNE_ENC_TRUNK = 2, PILC_TUNE_N };
 extern int g_tuning[PILC_TUNE_N];
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -580,6 +580,40 @@ __device__ __forceinline__ void mma_f16_elect(uint32_t d_tmem, uint64_t a, uint6
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// as mma_f16_elect with the descriptors as (low, high) words: the address
+// offsets are added to the low word only (shared-memory addresses < 2^18 never
+// carry out of the 14-bit field), one 32-bit add per descriptor
+__device__ __forceinline__ void mma_f16_elect_w(uint32_t d_tmem, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                                uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p, e;\n\t"
+        ".reg .b64 da, db;\n\t"
+        "mov.b64 da, {%1, %2};\n\t"
+        "mov.b64 db, {%3, %4};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc));
+}
+
+// bf16 twin of mma_f16_elect_w
+__device__ __forceinline__ void mma_bf16_elect_w(uint32_t d_tmem, uint32_t alo, uint32_t ahi, uint32_t blo,
+                                                 uint32_t bhi, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p, e;\n\t"
+        ".reg .b64 da, db;\n\t"
+        "mov.b64 da, {%1, %2};\n\t"
+        "mov.b64 db, {%3, %4};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %5, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc));
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
     asm volatile(
         "{\n\t"
@@ -1227,6 +1261,439 @@ size_t tc3_block_smem(int Hp, int Wp) {
            2 * kBkMaxTiles * 4 * 4 + 64 * 4;
 }
 
+// ---- encoder trunk in shared memory (vqvae.py:58-64) ------------------------
+// All B residual blocks and the 1x1 projection of one image per CTA
+// iteration: X (hi / lo operands, updated in place by each conv2 epilogue)
+// and T (conv1 output) stay in shared memory, the fp32 block input (the
+// exact residual) and the biases in tensor memory; only z leaves, as the
+// argmin's 128-latent tiles.
+//
+// Per layer the T = ceil(Hp Wp / 128) tiles are issued in order and tile j of
+// layer l + 1 waits for tiles j - 1 .. j + 1 of layer l (`hrdy`, one phase
+// per layer); MMAs complete in issue order, so no epilogue overwrites a
+// buffer an earlier MMA still reads. Weights stream through a two-slot ring.
+// Two operand buffers alternate by image: image i's X lives in buffer i & 1
+// and its T in the other, which is free once i's last conv2 MMAs are done --
+// so image i + 1's X loads into it while i's last epilogues and projection
+// run.
+//
+// The MMAs (M=128, N=64 + N=32 per K=16 step) cost ~44 cycles each whatever
+// their N, so the kernel is bound by MMA count (36 per tile) plus the
+// bubbles at layer boundaries, where tile 0 of layer l + 1 waits for the
+// epilogues of tiles 0 and 1 of layer l: both epilogue groups therefore work
+// on every tile (group g: channels 16g .. 16g + 15), halving the epilogue
+// latency per tile. The epilogue keeps its non-operand traffic out of shared
+// memory (the MMAs' operand reads use most of its bandwidth): residual and
+// biases in TMEM columns, one merged predicated store per edge direction,
+// partial maxima reduced across lanes. TMEM (512 columns): [0, 128) two
+// accumulators (hi x hi | cross terms), [128, 128 + 32 T) the fp32 block
+// input per tile, [224, 224 + 32 NL) every layer's bias (the same in all
+// 128 lanes).
+//
+// Measured and rejected: CTA pairs (cta_group::2, M=256 MMAs issued by the
+// leader over both CTAs' tiles). An M=256 pair MMA costs the same ~44 cycles
+// as an M=128 one (tools/micro/mma2_rate.cu), i.e. no more rows per SM per
+// cycle, and the cross-CTA tile / accumulator barriers added latency: 1.89
+// ms per CIFAR-8192 launch against 1.63 for single CTAs.
+//
+// Scales (the per-image bounds of tc3_block_kernel): each epilogue layer
+// needs the exact max of its input over the whole image, so the epilogue
+// warps meet at a named barrier after every conv layer and reduce per-tile
+// partial maxima. Arithmetic (MMA K order, epilogue roundings, scales) is
+// that of tc3_block_kernel + tc3_conv_kernel<1, TC3_Z>: z is bit-identical
+// to the per-block path.
+constexpr int kThreadsET = 320;
+constexpr int kEtMaxTiles = 3;
+constexpr int kEtMaxLayers = 9;  // 2B + 1 with B <= 4: the biases fill TMEM columns 224 .. 511
+constexpr uint32_t kEtX32Col = 128, kEtBiasCol = 224;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float *v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+// 16 consecutive f32 columns of this thread's lane, no wait (tmem_wait_ld before use)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, float *v) {
+    uint32_t *r = reinterpret_cast<uint32_t *>(v);
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// store_px with the edge copies merged per direction: ex = -1 / +1 (left /
+// right column), ey = -Wp / +Wp (top / bottom row); `rows` / `corner` are
+// warp-uniform (some lane of the warp has an edge row / a corner), so most
+// warps issue the main store and one column-edge store only
+__device__ __forceinline__ void store_px_m(uint8_t *slab_base, int r, uint4 v, bool valid, int ex, int ey,
+                                           bool rows, bool corner) {
+    uint4 *p = reinterpret_cast<uint4 *>(slab_base);
+    if (valid) p[r] = v;
+    if (valid && ex) p[r + ex] = v;
+    if (rows) {
+        if (valid && ey) p[r + ey] = v;
+        if (corner && valid && ex && ey) p[r + ey + ex] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsET, 1) enc_trunk_kernel(EncTrunk P) {
+    constexpr int N = 32, N2 = 64, NH = 4;
+    constexpr uint32_t WB = 36 * N2 * 16;
+    const int Wp = P.Wp, HW = P.Hp * Wp;
+    const int T = (HW + 127) >> 7;
+    const int M0 = Wp + 1;
+    const int RX = M0 + 128 * T + M0;
+    const uint32_t slab = (uint32_t)RX * 16u;
+    const int nrows = HW + 2 * M0;
+    const int B = P.n_blocks, NL = 2 * B + 1;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_w = smem;                   // [2][WB] weight ring
+    uint8_t *s_buf = s_w + 2 * WB;         // [2][8 slabs] operand buffers
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_buf + 16 * (size_t)slab);
+    uint64_t *wfull = bars, *wempty = bars + 2, *xfull = bars + 4, *xfree = bars + 6;
+    uint64_t *tfull = bars + 8, *tempty = bars + 10;
+    uint64_t *hrdy = bars + 12;  // [kEtMaxTiles]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(hrdy + kEtMaxTiles);
+    uint32_t *part = tmem_slot + 4;                                   // [2][kEtMaxTiles][4][2]
+    float *s_m = reinterpret_cast<float *>(part + 2 * kEtMaxTiles * 8);  // [NL][4] {kw, L1, max|b|, -}
+
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < NL * 4; i += blockDim.x) s_m[i] = (i & 3) < 3 ? P.meta[i >> 2][i & 3] : 0.f;
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&wfull[a], 1);
+            mbar_init(&wempty[a], 1);
+            mbar_init(&xfull[a], 1);
+            mbar_init(&xfree[a], 1);
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);  // both epilogue groups read every accumulator
+        }
+        for (int j = 0; j < kEtMaxTiles; ++j) mbar_init(&hrdy[j], 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
+    const int64_t n_img = P.n_img;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int lc = 0, it = 0;
+            for (int64_t n = blockIdx.x; n < n_img; n += gridDim.x, ++it) {
+                const int b = it & 1;
+                // X hi / lo (tile halos included) into buffer b, once the image
+                // that used b for its T has issued its last conv2 MMAs
+                if (it > 0) mbar_wait(&xfree[b], ((it - 1) >> 1) & 1);
+                mbar_expect_tx(&xfull[b], 8u * (uint32_t)nrows * 16u);
+                const int64_t q_lo = n * HW - M0;
+#pragma unroll 1
+                for (int g = 0; g < 8; ++g)
+                    bulk_g2s(s_buf + (size_t)(b * 8 + g) * slab, P.in + ((int64_t)g * P.gstride + P.margin + q_lo) * 8,
+                             (uint32_t)nrows * 16u, &xfull[b]);
+#pragma unroll 1
+                for (int l = 0; l < NL; ++l, ++lc) {
+                    const int s = lc & 1;
+                    if (lc >= 2) mbar_wait(&wempty[s], ((lc >> 1) - 1) & 1);
+                    const uint32_t bytes = l < 2 * B ? WB : 4u * N2 * 16u;
+                    mbar_expect_tx(&wfull[s], bytes);
+                    bulk_g2s(s_w + (size_t)s * WB, P.w[l], bytes, &wfull[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc64 = idesc_f16(128, N2);
+        constexpr uint32_t idesc32 = idesc_f16(128, N);
+        const uint64_t dBuf = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_buf), 0), slab, 128u);
+        const uint64_t dW = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w), 0), (uint32_t)N2 * 16u, 128u);
+        const uint32_t rx = (uint32_t)RX;
+        const uint32_t bstep = (8u * slab) >> 4;
+        const uint32_t d0 = tmem, d1 = tmem + (uint32_t)N2;
+        int64_t ti = 0;
+        int lc = 0, it = 0;
+        for (int64_t n = blockIdx.x; n < n_img; n += gridDim.x, ++it) {
+            const int bx = it & 1;
+            mbar_wait(&xfull[bx], (it >> 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int l = 0; l < NL; ++l, ++lc) {
+                const int s = lc & 1;
+                mbar_wait(&wfull[s], (lc >> 1) & 1);
+                tc_fence_after();
+                const bool conv = l < 2 * B;
+                const int ab = (conv && (l & 1)) ? (bx ^ 1) : bx;  // conv2 reads T, conv1 / proj read X
+                const uint64_t dA = dBuf + (uint64_t)((uint32_t)ab * bstep);
+                const uint64_t dB = dW + (uint64_t)((uint32_t)s * (WB >> 4));
+#pragma unroll 1
+                for (int j = 0; j < T; ++j, ++ti) {
+                    if (l > 0) {  // the previous layer's tiles j - 1 .. j + 1 (proj: j) are in place
+                        if (conv) {
+                            if (j == 0) mbar_wait(&hrdy[0], (lc - 1) & 1);
+                            if (j + 1 < T) mbar_wait(&hrdy[j + 1], (lc - 1) & 1);
+                        } else {
+                            mbar_wait(&hrdy[j], (lc - 1) & 1);
+                        }
+                    }
+                    const int a = (int)(ti & 1);
+                    const int64_t u = ti >> 1;
+                    if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
+                    tc_fence_after();
+                    const uint32_t d = a ? d1 : d0;
+                    const uint32_t bl = (uint32_t)dB, bh = (uint32_t)(dB >> 32), ah = (uint32_t)(dA >> 32);
+                    if (conv) {
+                        const uint32_t al = (uint32_t)dA + (uint32_t)(M0 + 128 * j - Wp - 1);
+#pragma unroll
+                        for (int tap = 0; tap < 9; ++tap) {
+                            const uint32_t off = (uint32_t)((tap / 3) * Wp + tap % 3);
+#pragma unroll
+                            for (int ks = 0; ks < NH / 2; ++ks) {
+                                const uint32_t ao = 2u * ks * rx + off;
+                                const uint32_t bo = (uint32_t)((tap * NH + 2 * ks) * N2);
+                                mma_f16_elect_w(d, al + ao, ah, bl + bo, bh, idesc64, (tap | ks) ? 1u : 0u);
+                                mma_f16_elect_w(d + N, al + ao + NH * rx, ah, bl + bo, bh, idesc32, 1u);
+                            }
+                        }
+                    } else {
+                        const uint32_t al = (uint32_t)dA + (uint32_t)(M0 + 128 * j);
+#pragma unroll
+                        for (int ks = 0; ks < NH / 2; ++ks) {
+                            const uint32_t ao = 2u * ks * rx;
+                            const uint32_t bo = (uint32_t)(2 * ks * N2);
+                            mma_f16_elect_w(d, al + ao, ah, bl + bo, bh, idesc64, ks ? 1u : 0u);
+                            mma_f16_elect_w(d + N, al + ao + NH * rx, ah, bl + bo, bh, idesc32, 1u);
+                        }
+                    }
+                    mma_commit_elect(&tfull[a]);
+                }
+                mma_commit_elect(&wempty[s]);
+                if (l == 2 * B - 1) mma_commit_elect(&xfree[bx ^ 1]);  // T buffer: the next image's X
+            }
+        }
+    } else if (warp >= 2) {
+        // two epilogue groups of four warps (one per TMEM lane quarter); both
+        // take every tile, group g its channels 16g .. 16g + 15
+        const int grp = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int H = P.H, W = P.W;
+        const bool thin = H == 1 || W == 1;
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t ch = 16u * (uint32_t)grp;  // this group's first channel
+        // biases into TMEM, every lane: group g writes layers l = g mod 2
+        for (int l = grp; l < NL; l += 2) {
+            float bv[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) bv[c] = __ldg(P.bias[l] + c);
+            tmem_st32(lane_base + kEtBiasCol + 32u * l, bv);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        tc_fence_after();
+        int64_t ti = 0;
+        int it = 0;
+        int kx_nx = 0;
+        uint32_t mx_nx = 0;
+        if (blockIdx.x < n_img) {
+            kx_nx = P.kx_in[blockIdx.x];
+            mx_nx = P.mx_in[blockIdx.x];
+        }
+        for (int64_t n = blockIdx.x; n < n_img; n += gridDim.x, ++it) {
+            const int bx = it & 1;
+            uint8_t *bufX = s_buf + (size_t)bx * 8 * slab + (size_t)M0 * 16;
+            uint8_t *bufT = s_buf + (size_t)(bx ^ 1) * 8 * slab + (size_t)M0 * 16;
+            int kX = kx_nx;
+            float mxX = __uint_as_float(mx_nx);
+            if (n + gridDim.x < n_img) {
+                kx_nx = P.kx_in[n + gridDim.x];
+                mx_nx = P.mx_in[n + gridDim.x];
+            }
+            int kT = 0;
+            float mxT = 0.f;
+#pragma unroll 1
+            for (int l = 0; l < NL; ++l) {
+                const int kw = __float_as_int(s_m[4 * l]);
+                const float l1 = s_m[4 * l + 1], bm = s_m[4 * l + 2];
+                const bool conv = l < 2 * B, conv2 = conv && (l & 1);
+                // this layer's input scale and its output scale
+                int ko = 0;
+                float inv;
+                if (!conv) {
+                    inv = exp2i(-kX - kw);
+                } else if (!conv2) {  // T = relu(conv1(X)), |T| <= max|X| L1 + max|b|
+                    ko = act_exp(__float_as_uint(__fadd_rn(__fmul_rn(mxX, l1), bm)));
+                    inv = exp2i(-kX - kw);
+                } else {              // X' = relu(X + conv2(T)), |X'| <= max|T| L1 + max|b| + max|X|
+                    ko = act_exp(__float_as_uint(__fadd_rn(__fadd_rn(__fmul_rn(mxT, l1), bm), mxX)));
+                    inv = exp2i(-kT - kw);
+                }
+                const float osc = exp2i(ko);
+                uint32_t *pt = part + (l & 1) * kEtMaxTiles * 8;
+                uint8_t *dst = conv2 ? bufX : bufT;
+#pragma unroll 1
+                for (int j = 0; j < T; ++j, ++ti) {
+                    const int a = (int)(ti & 1);
+                    const uint32_t u = (uint32_t)(ti >> 1);
+                    const int r = 128 * j + row;
+                    const int y = r / Wp, x = r - (r / Wp) * Wp;
+                    const bool valid = r < HW && y >= 1 && y <= H && x >= 1 && x <= W;
+                    const uint32_t x32col = lane_base + kEtX32Col + 32u * j + ch;
+                    float rr[16];  // conv2: the fp32 block input of this row (this group's channels)
+                    if (l == 1) {  // block 0's input from the front's fp32 slabs, in flight during the MMAs
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (valid)
+                                f = __ldg(reinterpret_cast<const float4 *>(P.in32) + (int64_t)(4 * grp + g) * P.gstride +
+                                          P.margin + n * HW + r);
+                            rr[4 * g] = f.x;
+                            rr[4 * g + 1] = f.y;
+                            rr[4 * g + 2] = f.z;
+                            rr[4 * g + 3] = f.w;
+                        }
+                    }
+                    mbar_wait(&tfull[a], u & 1);
+                    tc_fence_after();
+                    const uint32_t taddr = lane_base + (uint32_t)(a * N2) + ch;
+                    float v[16];
+                    {
+                        float w[16], bias[16];
+                        tmem_ld16_nw(taddr, v);
+                        tmem_ld16_nw(taddr + 32, w);
+                        tmem_ld16_nw(lane_base + kEtBiasCol + 32u * l + ch, bias);
+                        if (conv2 && l > 1) tmem_ld16_nw(x32col, rr);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) v[c] = __fmaf_rn(__fmaf_rn(w[c], 0.00048828125f, v[c]), inv, bias[c]);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[a]);
+                    if (!conv) {
+                        // z = acc + bias as tf32 hi / fp32 lo 128-latent tiles (tc3_conv_kernel<1, TC3_Z>)
+                        if (valid) {
+                            const int64_t vix = ((int64_t)n * H + (y - 1)) * (int64_t)W + (x - 1);
+                            float4 *zo = P.z ? reinterpret_cast<float4 *>(P.z + vix * 32) + 4 * grp : nullptr;
+                            float4 *zt = reinterpret_cast<float4 *>(P.zt) + (vix >> 7) * (2 * 8 * 128) + (vix & 127) +
+                                         4 * grp * 128;
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) {
+                                float hi[4], lo[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    hi[e] = tf32_rna(v[4 * g + e]);
+                                    lo[e] = __fsub_rn(v[4 * g + e], hi[e]);
+                                }
+                                if (zo) zo[g] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+                                zt[g * 128] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                                zt[(8 + g) * 128] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+                            }
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&hrdy[j]);
+                        continue;
+                    }
+                    float mx = 0.f;
+                    if (conv2) {
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) v[c] = fmaxf(__fadd_rn(rr[c], v[c]), 0.f);
+                        if (l < 2 * B - 1) tmem_st16(x32col, v);  // the next block's residual
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) v[c] = fmaxf(v[c], 0.f);
+                    }
+                    if (valid) {
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) mx = fmaxf(mx, fabsf(v[c]));
+                    }
+                    const int ex = x == 1 ? -1 : (x == W ? 1 : 0);
+                    const int ey = y == 1 ? -Wp : (y == H ? Wp : 0);
+                    const bool rows = __any_sync(0xFFFFFFFFu, valid && ey != 0);
+                    const bool corner = __any_sync(0xFFFFFFFFu, valid && ey != 0 && ex != 0);
+#pragma unroll
+                    for (int gg = 0; gg < 2; ++gg) {
+                        const int g = 2 * grp + gg;  // channel group (8 channels)
+                        uint4 h, lo;
+                        split2(__fmul_rn(v[8 * gg + 0], osc), __fmul_rn(v[8 * gg + 1], osc), h.x, lo.x);
+                        split2(__fmul_rn(v[8 * gg + 2], osc), __fmul_rn(v[8 * gg + 3], osc), h.y, lo.y);
+                        split2(__fmul_rn(v[8 * gg + 4], osc), __fmul_rn(v[8 * gg + 5], osc), h.z, lo.z);
+                        split2(__fmul_rn(v[8 * gg + 6], osc), __fmul_rn(v[8 * gg + 7], osc), h.w, lo.w);
+                        if (thin) {  // one-pixel-wide grids: a pixel is both edges
+                            if (valid) {
+                                store_px(reinterpret_cast<uint16_t *>(dst + (size_t)g * slab), r, h, y, x, H, W, Wp);
+                                store_px(reinterpret_cast<uint16_t *>(dst + (size_t)(NH + g) * slab), r, lo, y, x, H, W, Wp);
+                            }
+                        } else {
+                            store_px_m(dst + (size_t)g * slab, r, h, valid, ex, ey, rows, corner);
+                            store_px_m(dst + (size_t)(NH + g) * slab, r, lo, valid, ex, ey, rows, corner);
+                        }
+                    }
+                    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, __float_as_uint(mx));
+                    fence_async_smem();  // operand rows -> the next layer's MMAs
+                    __syncwarp();
+                    if (lane == 0) {
+                        pt[(j * 4 + quarter) * 2 + grp] = m;
+                        mbar_arrive(&hrdy[j]);
+                    }
+                }
+                if (!conv) break;
+                // every tile of the layer is through: the image's exact max |out|
+                // (and the residual columns written above are visible to all)
+                if (conv2) tmem_wait_st();
+                tc_fence_before();
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                tc_fence_after();
+                const uint32_t mt = __reduce_max_sync(0xFFFFFFFFu, lane < 8 * T ? pt[lane] : 0u);
+                if (conv2) {
+                    mxX = __uint_as_float(mt);
+                    kX = ko;
+                } else {
+                    mxT = __uint_as_float(mt);
+                    kT = ko;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
+}
+
+size_t enc_trunk_smem(int Hp, int Wp, int B) {
+    const int HW = Hp * Wp, T = (HW + 127) / 128, M0 = Wp + 1;
+    const size_t RX = (size_t)2 * M0 + (size_t)T * 128;
+    const int NL = 2 * B + 1;
+    (void)HW;
+    return 2 * 36 * 64 * 16 + 2 * 8 * RX * 16 + (12 + kEtMaxTiles) * 8 + 16 + 2 * kEtMaxTiles * 8 * 4 +
+           (size_t)NL * 4 * 4;
+}
+
 // ---- decoder trunk in shared memory (vqvae.py:80-100) -----------------------
 // dec.proj (as the gathered table T[idx], see dec_table_kernel) and all 2B
 // residual-block convs of a group of G images in one persistent kernel: the
@@ -1339,14 +1806,15 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk_kernel(DecTrunk P) {
                     if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
                     tc_fence_after();
                     const uint32_t d = tmem + (uint32_t)(a * N);
-                    const uint32_t r0 = (uint32_t)(M0 + 128 * j - Wp - 1);
+                    const uint32_t al = (uint32_t)dA + (uint32_t)(M0 + 128 * j - Wp - 1), ah = (uint32_t)(dA >> 32);
+                    const uint32_t bl = (uint32_t)dB, bh = (uint32_t)(dB >> 32);
 #pragma unroll
                     for (int tap = 0; tap < 9; ++tap) {
-                        const uint32_t off = r0 + (uint32_t)((tap / 3) * Wp + tap % 3);
+                        const uint32_t off = (uint32_t)((tap / 3) * Wp + tap % 3);
 #pragma unroll
                         for (int ks = 0; ks < NG / 2; ++ks)
-                            mma_bf16_elect(d, dA + (uint64_t)(2u * ks * rs + off),
-                                           dB + (uint64_t)((tap * NG + 2 * ks) * N), idesc, (tap | ks) ? 1u : 0u);
+                            mma_bf16_elect_w(d, al + 2u * ks * rs + off, ah, bl + (uint32_t)((tap * NG + 2 * ks) * N), bh,
+                                             idesc, (tap | ks) ? 1u : 0u);
                     }
                     mma_commit_elect(&tfull[a]);
                 }
@@ -2244,6 +2712,23 @@ int tc3_block_launch(const Tc3Block &b, cudaStream_t s) {
     const double flops = 2.0 * 2.0 * b.n_img * b.H * b.W * 32.0 * 32 * 9;
     ProfScope _ps(PROF_TC3_BLOCK, s, flops);
     tc3_block_kernel<<<(unsigned)grid, kThreadsBK, smem, s>>>(b);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+int enc_trunk_launch(const EncTrunk &p, cudaStream_t s) {
+    if (p.n_blocks < 1 || 2 * p.n_blocks + 1 > kEtMaxLayers) return PILC_E_UNSUPPORTED;
+    const int HW = p.Hp * p.Wp;
+    if ((HW + 127) / 128 > kEtMaxTiles) return PILC_E_UNSUPPORTED;
+    const size_t smem = enc_trunk_smem(p.Hp, p.Wp, p.n_blocks);
+    if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
+    if ((uint64_t)p.n_img * HW >= (1ull << 31)) return PILC_E_UNSUPPORTED;
+    cudaFuncSetAttribute(enc_trunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int64_t grid = sm_count();
+    if (grid > p.n_img) grid = p.n_img;
+    if (grid < 1) return PILC_OK;
+    const double flops = 2.0 * p.n_img * p.H * p.W * 32.0 * 32 * (18.0 * p.n_blocks + 1);
+    ProfScope _ps(PROF_ENC_TRUNK, s, flops);
+    enc_trunk_kernel<<<(unsigned)grid, kThreadsET, smem, s>>>(p);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

@@ -95,6 +95,28 @@ struct Tc3Block {
 };
 int tc3_block_launch(const Tc3Block &b, cudaStream_t s);
 
+// Encoder trunk: all B residual blocks and the 1x1 projection of one image
+// per CTA iteration with the activations (hi / lo operands and the fp32
+// block input) resident in shared memory; z leaves as the argmin's tiles.
+// Same arithmetic as the per-block kernels plus the TC3_Z projection.
+constexpr int kEtMaxBlocks = 8;
+struct EncTrunk {
+    const uint16_t *in;   // hi / lo slabs of the front output
+    const float *in32;    // its fp32 slabs
+    int64_t gstride, margin;
+    int Hp, Wp, H, W;
+    int64_t n_img;
+    int n_blocks;                               // B, 1 .. kEtMaxBlocks
+    const uint16_t *w[2 * kEtMaxBlocks + 1];    // [36][64][8] fp16 B operands; [2B] = proj [4][64][8]
+    const float *meta[2 * kEtMaxBlocks + 1];    // {kw, L1, max|b|}
+    const float *bias[2 * kEtMaxBlocks + 1];
+    const int32_t *kx_in;                       // front output scale exponent per image
+    const uint32_t *mx_in;                      // front output max |x| per image
+    float *z;                                   // (n, H, W, 32) fp32 (nullable)
+    float *zt;                                  // 128-latent tiles [tile][hi|lo][8][128][4]
+};
+int enc_trunk_launch(const EncTrunk &p, cudaStream_t s);
+
 // Encoder front (stem and the stride-2 down conv as 3-product fp16 MMAs, the
 // down GEMM over the space-to-depth stem, tc_conv.cu); outputs like the
 // block convs.

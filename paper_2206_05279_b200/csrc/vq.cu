@@ -1224,6 +1224,44 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
     float *X32 = w.X32, *Y32 = w.Y32;
     uint16_t *XH = w.XH, *YH = w.YH;
     const float *meta = model + L.tf_meta;
+    ArgminTc am;
+    am.zt = w.ZT;
+    am.n_vec = n_img * gh * gw;
+    am.n_tiles = ceil_div64(am.n_vec, 128);
+    am.cbt = model + L.tf_cb;
+    am.K = K;
+    am.idx = idx_out;
+    if (g_tuning[PILC_TUNE_ENC_TRUNK] && B >= 1 && B <= kEtMaxBlocks) {
+        // every block + the projection in one kernel, activations in shared
+        // memory (bit-identical to the per-block path below)
+        EncTrunk et;
+        memset(&et, 0, sizeof(et));
+        et.in = XH;
+        et.in32 = X32;
+        et.gstride = w.gs;
+        et.margin = w.margin;
+        et.Hp = b.Hp;
+        et.Wp = b.Wp;
+        et.H = gh;
+        et.W = gw;
+        et.n_img = n_img;
+        et.n_blocks = B;
+        for (int l = 0; l < 2 * B; ++l) {
+            et.w[l] = reinterpret_cast<const uint16_t *>(model + L.tf_blk[l]);
+            et.meta[l] = meta + 4 * l;
+            et.bias[l] = model + L.enc[2 + l].b_off;
+        }
+        et.w[2 * B] = reinterpret_cast<const uint16_t *>(model + L.tf_proj);
+        et.meta[2 * B] = meta + 4 * (2 * B);
+        et.bias[2 * B] = model + L.enc[2 + 2 * B].b_off;
+        et.kx_in = w.kx;
+        et.mx_in = w.mx;
+        et.z = z_out;
+        et.zt = w.ZT;
+        rc = enc_trunk_launch(et, s);
+        if (rc == PILC_OK) return argmin_tc_launch(am, s);
+        if (rc != PILC_E_UNSUPPORTED) return rc;
+    }
     for (int i = 0; i < B; ++i) {
         if (g_tuning[PILC_TUNE_BLOCK_FUSION]) {  // both convs in one kernel, T stays in shared memory
             Tc3Block k;
@@ -1299,13 +1337,6 @@ int tf_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const flo
     pj.z = z_out;
     pj.zt = w.ZT;
     if ((rc = tc3_launch(pj, 1, TC3_Z, s))) return rc;
-    ArgminTc am;
-    am.zt = w.ZT;
-    am.n_vec = n_img * gh * gw;
-    am.n_tiles = ceil_div64(am.n_vec, 128);
-    am.cbt = model + L.tf_cb;
-    am.K = K;
-    am.idx = idx_out;
     return argmin_tc_launch(am, s);
 }
 

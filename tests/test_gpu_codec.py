@@ -546,10 +546,14 @@ def test_trained_model_round_trip_and_vs_oracle():
         assert np.array_equal(pc.decompress(blob, m), img)
 
 
-@pytest.mark.parametrize("shape,n", [((32, 32), 301), ((30, 18), 7), ((1, 1), 3), ((17, 33), 5), ((64, 64), 2)])
+@pytest.mark.parametrize("shape,n", [((32, 32), 301), ((30, 18), 7), ((1, 1), 3), ((17, 33), 5), ((34, 34), 150),
+                                     ((33, 2), 9), ((64, 64), 2)])
 def test_fused_encoder_blocks_bit_identical(full_model, shape, n):
-    """tc3_block_kernel (conv1 + conv2 of a block, T in shared memory) gives
-    exactly the z and indices of two separate tc3 launches per block."""
+    """enc_trunk_kernel (every block + the projection, activations in shared
+    memory, two images in flight per CTA), tc3_block_kernel (conv1 + conv2 of
+    a block, T in shared memory) and two separate tc3 launches per block give
+    exactly the same z and indices. n = 301 / 150 leave the CTAs uneven image
+    counts (odd and even per-CTA sequences through the two operand buffers)."""
     from paper_2206_05279_b200 import _lib
     from paper_2206_05279_b200.device import as_device_u8, require_device
 
@@ -559,7 +563,8 @@ def test_fused_encoder_blocks_bit_identical(full_model, shape, n):
     gh, gw = vqvae.latent_shape(*shape)
     img_d = as_device_u8(imgs, dev, stream)
     out = []
-    for fused in (1, 0):
+    for trunk, fused in ((1, 1), (0, 1), (0, 0)):
+        prev_t = _lib.set_tuning(_lib.TUNE_ENC_TRUNK, trunk)
         prev = _lib.set_tuning(_lib.TUNE_BLOCK_FUSION, fused)
         try:
             z = torch.empty((n, gh, gw, 32), dtype=torch.float32, device=dev)
@@ -567,8 +572,12 @@ def test_fused_encoder_blocks_bit_identical(full_model, shape, n):
             out.append((z.cpu().numpy(), idx.cpu().numpy()))
         finally:
             _lib.set_tuning(_lib.TUNE_BLOCK_FUSION, prev)
-    assert np.array_equal(out[0][0].view(np.uint32), out[1][0].view(np.uint32))
-    assert np.array_equal(out[0][1], out[1][1])
+            _lib.set_tuning(_lib.TUNE_ENC_TRUNK, prev_t)
+    z0 = out[0][0]
+    assert np.isfinite(z0).all() and np.abs(z0).max() > 0 and len(np.unique(z0)) > z0.size // 4  # a live z
+    for o in out[1:]:
+        assert np.array_equal(z0.view(np.uint32), o[0].view(np.uint32))
+        assert np.array_equal(out[0][1], o[1])
 
 
 @pytest.mark.parametrize("shape,n", [((32, 32), 301), ((30, 18), 7), ((1, 1), 3), ((17, 33), 5), ((64, 64), 3)])
