@@ -88,6 +88,226 @@ __global__ void twar_forward_kernel(const uint8_t *__restrict__ img, uint8_t *__
     }
 }
 
+// Rows of W = 8 m pixels: a thread per 8-pixel run (24 bytes) of a row,
+// loaded as three 8-byte vectors (plus the same run of the row above and
+// the 4 bytes before each, for the left / up-left neighbours), 24 residual
+// bytes stored as three vectors. Same arithmetic per pixel as
+// twar_forward_kernel (INTEGRAL: the integer-weight predictor in integer
+// arithmetic, exact as in predict()); the scalar kernel is issue bound at
+// ~85 instructions per pixel, this one at ~10 per subpixel and HBM.
+__device__ __forceinline__ uint32_t byte_at(const uint32_t *w, int i) { return (w[i >> 2] >> (8 * (i & 3))) & 0xFFu; }
+
+template <int INTEGRAL>
+__device__ __forceinline__ uint32_t predict8(uint32_t c0, uint32_t c1, uint32_t c2, const Params &p, const int *wi, int k) {
+    if (INTEGRAL) return (uint32_t)(wi[3 * k] * (int)c0 + wi[3 * k + 1] * (int)c1 + wi[3 * k + 2] * (int)c2 + wi[9 + k]) & 255u;
+    return predict((float)c0, (float)c1, (float)c2, p.w + 3 * k, p.b[k], 0);
+}
+
+// the residual bytes of an npx-pixel run (npx = 8 or 16) from its bytes c,
+// the same run of the row above a, and the 4 bytes before each (cl, al).
+// INTEGRAL == 2: the default predictor (W_r = (-1, 1, 1), W_g = W_b =
+// (1, -1, 1), no bias) four bytes at a time: t = x + X - Y - Z + 128 (mod
+// 256) with (X, Y, Z) = (up-left, up, left) on red bytes and (the left
+// pixel's red / green, the left subpixel, the previous subpixel) on green /
+// blue ones; even and odd bytes go through 16-bit lanes.
+template <int INTEGRAL>
+__device__ __forceinline__ void run_residual(const uint32_t *c, const uint32_t *a, uint32_t cl, uint32_t al, int npx,
+                                             const Params &p, const int *wi, uint32_t *o) {
+    if (INTEGRAL == 2) {
+#pragma unroll
+        for (int j = 0; j < 3 * npx / 4; ++j) {
+            const uint32_t M = (j % 3 == 0) ? 0xFF0000FFu : (j % 3 == 1 ? 0x00FF0000u : 0x0000FF00u);
+            const uint32_t Cm = j ? c[j - 1] : cl, Um = j ? a[j - 1] : al;
+            const uint32_t c3 = __funnelshift_l(Cm, c[j], 24), c1 = __funnelshift_l(Cm, c[j], 8);
+            const uint32_t u3 = __funnelshift_l(Um, a[j], 24);
+            const uint32_t X = (Cm & ~M) | (u3 & M), Y = (c3 & ~M) | (a[j] & M), Z = (c1 & ~M) | (c3 & M);
+            constexpr uint32_t LO = 0x00FF00FFu, K = 0x02800280u;
+            const uint32_t e = (c[j] & LO) + (X & LO) + K - (Y & LO) - (Z & LO);
+            const uint32_t d = ((c[j] >> 8) & LO) + ((X >> 8) & LO) + K - ((Y >> 8) & LO) - ((Z >> 8) & LO);
+            o[j] = (e & LO) | ((d & LO) << 8);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 3 * npx / 4; ++j) o[j] = 0u;
+#pragma unroll
+        for (int i = 0; i < npx; ++i) {
+            const uint32_t r = byte_at(c, 3 * i), gg = byte_at(c, 3 * i + 1), bb = byte_at(c, 3 * i + 2);
+            const uint32_t rl = i ? byte_at(c, 3 * i - 3) : (cl >> 8) & 0xFFu;
+            const uint32_t gl = i ? byte_at(c, 3 * i - 2) : (cl >> 16) & 0xFFu;
+            const uint32_t bl = i ? byte_at(c, 3 * i - 1) : cl >> 24;
+            const uint32_t ru = byte_at(a, 3 * i);
+            const uint32_t rul = i ? byte_at(a, 3 * i - 3) : (al >> 8) & 0xFFu;
+            const uint32_t pr = predict8<INTEGRAL>(rul, ru, rl, p, wi, 0);
+            const uint32_t pg = predict8<INTEGRAL>(gl, rl, r, p, wi, 1);
+            const uint32_t pb = predict8<INTEGRAL>(bl, gl, gg, p, wi, 2);
+            o[(3 * i) >> 2] |= ((r - pr + 128u) & 0xFFu) << (8 * ((3 * i) & 3));
+            o[(3 * i + 1) >> 2] |= ((gg - pg + 128u) & 0xFFu) << (8 * ((3 * i + 1) & 3));
+            o[(3 * i + 2) >> 2] |= ((bb - pb + 128u) & 0xFFu) << (8 * ((3 * i + 2) & 3));
+        }
+    }
+}
+
+// one 8-pixel run's inputs: the run, the same run of the row above, and
+// the 4 bytes before each (left / up-left neighbours in bytes 1..3)
+struct Run8 {
+    uint32_t c[6], a[6], cl, al;
+};
+
+__device__ __forceinline__ void load_run8(Run8 &r, const uint8_t *img, int64_t g, int upr, int rb, int H) {
+    int64_t R;  // global row (image n, row u)
+    int k, u;   // run within the row, row within the image
+    if (g < (1ll << 32) / 2) {  // 32-bit divisions (the 64-bit ones are a long software sequence)
+        const uint32_t R32 = (uint32_t)g / (uint32_t)upr;
+        R = R32;
+        k = (int)((uint32_t)g - R32 * (uint32_t)upr);
+        u = (int)(R32 % (uint32_t)H);
+    } else {
+        R = g / upr;
+        k = (int)(g - R * upr);
+        u = (int)(R % H);
+    }
+    const uint8_t *rp = img + R * rb + 24 * k;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(rp) + q);
+        r.c[2 * q] = v.x, r.c[2 * q + 1] = v.y;
+    }
+    r.cl = k > 0 ? __ldg(reinterpret_cast<const uint32_t *>(rp) - 1) : 0u;
+    r.al = 0u;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) r.a[q] = 0u;
+    if (u > 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2 *>(rp - rb) + q);
+            r.a[2 * q] = v.x, r.a[2 * q + 1] = v.y;
+        }
+        if (k > 0) r.al = __ldg(reinterpret_cast<const uint32_t *>(rp - rb) - 1);
+    }
+}
+
+template <int INTEGRAL>
+__global__ void __launch_bounds__(256) twar_forward8_kernel(const uint8_t *__restrict__ img, uint8_t *__restrict__ res,
+                                                            int64_t n_units, int H, int W, Params p) {
+    const int upr = W >> 3;  // 8-pixel runs per row
+    const int rb = 3 * W;    // row bytes
+    int wi[12];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wi[k] = (int)p.w[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) wi[9 + k] = (int)p.b[k];
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_units; g += (int64_t)gridDim.x * blockDim.x) {
+        Run8 cur;
+        load_run8(cur, img, g, upr, rb, H);
+        const uint32_t *c = cur.c, *a = cur.a;
+        const uint32_t cl = cur.cl, al = cur.al;
+        uint32_t o[6];
+        run_residual<INTEGRAL>(c, a, cl, al, 8, p, wi, o);
+        uint2 *op = reinterpret_cast<uint2 *>(res + g * 24);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) op[q] = make_uint2(o[2 * q], o[2 * q + 1]);
+    }
+}
+
+// Whole images through shared memory (W = 16 m, at most 12 KB per image):
+// each block takes G images at a time, brought in by one bulk copy (TMA
+// engine, double-buffered one group ahead) and written back by one bulk
+// store from a staged output buffer, so HBM sees only long contiguous
+// transfers; a thread computes 16-pixel runs from shared memory (the row
+// above included: no second global read of it). Per pixel the arithmetic of
+// twar_forward8_kernel.
+__device__ __forceinline__ uint32_t s_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+constexpr int kTwTileBytes = 12288;  // input (and output) bytes per group buffer
+
+template <int INTEGRAL>
+__global__ void __launch_bounds__(256) twar_forward_tile_kernel(const uint8_t *__restrict__ img, uint8_t *__restrict__ res,
+                                                                int64_t n_img, int H, int W, int G, Params p) {
+    extern __shared__ __align__(128) uint8_t s_tw[];  // in[2][kTwTileBytes], out[2][kTwTileBytes]
+    uint8_t(*s_in)[kTwTileBytes] = reinterpret_cast<uint8_t(*)[kTwTileBytes]>(s_tw);
+    uint8_t(*s_out)[kTwTileBytes] = reinterpret_cast<uint8_t(*)[kTwTileBytes]>(s_tw + 2 * kTwTileBytes);
+    __shared__ uint64_t bar[2];
+    const int rb = 3 * W, ib = H * rb;  // row / image bytes
+    const int upr = W >> 4;             // 16-pixel runs per row
+    int wi[12];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wi[k] = (int)p.w[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) wi[9 + k] = (int)p.b[k];
+    const int64_t n_groups = (n_img + G - 1) / G;
+    auto load = [&](int64_t gi, int b) {  // thread 0: group gi into buffer b
+        const int64_t n0 = gi * G;
+        const uint32_t bytes = (uint32_t)(min((int64_t)G, n_img - n0) * ib);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&bar[b])), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         s_u32(s_in[b])),
+                     "l"(img + n0 * ib), "r"(bytes), "r"(s_u32(&bar[b]))
+                     : "memory");
+    };
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (blockIdx.x < n_groups) load(blockIdx.x, 0);
+    }
+    __syncthreads();
+    int it = 0;
+    for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (threadIdx.x == 0) {
+            if (gi + gridDim.x < n_groups) load(gi + gridDim.x, b ^ 1);  // its buffer was released by the last __syncthreads
+            // s_out[b] is reused: its bulk store of two groups ago must have read it
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@P1 bra D;\n\tbra W;\n\tD:\n\t}" ::"r"(
+                s_u32(&bar[b])),
+            "r"((uint32_t)((it >> 1) & 1))
+            : "memory");
+        __syncthreads();  // s_out[b] free (thread 0 waited above)
+        const int64_t n0 = gi * G;
+        const int g_act = (int)min((int64_t)G, n_img - n0);
+        const int units = g_act * H * upr;
+        for (int t = threadIdx.x; t < units; t += blockDim.x) {
+            const int R = t / upr, k = t - R * upr;  // row within the group, run within the row
+            const int u = R % H;
+            const uint8_t *rp = s_in[b] + R * rb + 48 * k;
+            uint32_t c[12], a[12], cl = 0u, al = 0u;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const uint4 v = reinterpret_cast<const uint4 *>(rp)[q];
+                c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+            }
+            if (k > 0) cl = reinterpret_cast<const uint32_t *>(rp)[-1];
+            if (u > 0) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const uint4 v = reinterpret_cast<const uint4 *>(rp - rb)[q];
+                    a[4 * q] = v.x, a[4 * q + 1] = v.y, a[4 * q + 2] = v.z, a[4 * q + 3] = v.w;
+                }
+                if (k > 0) al = reinterpret_cast<const uint32_t *>(rp - rb)[-1];
+            } else {
+#pragma unroll
+                for (int q = 0; q < 12; ++q) a[q] = 0u;
+            }
+            uint32_t o[12];
+            run_residual<INTEGRAL>(c, a, cl, al, 16, p, wi, o);
+            uint4 *op = reinterpret_cast<uint4 *>(s_out[b] + R * rb + 48 * k);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) op[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the staged bytes -> the bulk store
+        __syncthreads();  // s_in[b] consumed, s_out[b] complete
+        if (threadIdx.x == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(res + n0 * ib),
+                         "r"(s_u32(s_out[b])), "r"((uint32_t)(g_act * ib))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Inverse (_kernels.py:146-170 wavefront schedule). One warp per image;
 // the image is staged in shared memory when it fits, else decoded in place
 // in the output buffer. Red: lanes take rows of two 32-row strips at a time
@@ -325,13 +545,38 @@ extern "C" int pilc_twar_forward(const uint8_t *img, uint8_t *res, int64_t n_img
     const int64_t n_px = n_img * (int64_t)H * W;
     if (n_px == 0) return PILC_OK;
     const int threads = 256;
-    int64_t blocks = ceil_div64(n_px, threads);
-    const int64_t cap = (int64_t)sm_count() * 32;
-    if (blocks > cap) blocks = cap;
-{
-        ProfScope _ps(PROF_TWAR_FWD, as_stream(stream), 3.0 * n_px);
-        twar_forward_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(
-        img, res, n_px, H, W, load_params(params12_host));
+    const Params prm = load_params(params12_host);
+    ProfScope _ps(PROF_TWAR_FWD, as_stream(stream), 3.0 * n_px);
+    static const float kDefault[9] = {-1.f, 1.f, 1.f, 1.f, -1.f, 1.f, 1.f, -1.f, 1.f};
+    bool unit = prm.b[0] == 0.f && prm.b[1] == 0.f && prm.b[2] == 0.f;
+    for (int k = 0; k < 9; ++k) unit = unit && prm.w[k] == kDefault[k];
+    const int64_t ib = (int64_t)H * W * 3;
+    if ((W & 15) == 0 && ib <= kTwTileBytes && ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(res)) & 15) == 0) {
+        const int G = (int)(kTwTileBytes / ib);
+        const int64_t groups = (n_img + G - 1) / G;
+        int64_t blocks = groups;
+        const int64_t cap = (int64_t)sm_count() * 4;
+        if (blocks > cap) blocks = cap;
+        const int sm = 4 * kTwTileBytes;
+        auto kern = unit ? twar_forward_tile_kernel<2> : (prm.integral ? twar_forward_tile_kernel<1> : twar_forward_tile_kernel<0>);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        kern<<<(unsigned)blocks, threads, sm, as_stream(stream)>>>(img, res, n_img, H, W, G, prm);
+    } else if ((W & 7) == 0 && ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(res)) & 7) == 0) {
+        const int64_t n_units = n_px >> 3;
+        int64_t blocks = ceil_div64(n_units, threads);
+        const int64_t cap = (int64_t)sm_count() * 32;
+        if (blocks > cap) blocks = cap;
+        if (unit)
+            twar_forward8_kernel<2><<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(img, res, n_units, H, W, prm);
+        else if (prm.integral)
+            twar_forward8_kernel<1><<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(img, res, n_units, H, W, prm);
+        else
+            twar_forward8_kernel<0><<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(img, res, n_units, H, W, prm);
+    } else {
+        int64_t blocks = ceil_div64(n_px, threads);
+        const int64_t cap = (int64_t)sm_count() * 32;
+        if (blocks > cap) blocks = cap;
+        twar_forward_kernel<<<(unsigned)blocks, threads, 0, as_stream(stream)>>>(img, res, n_px, H, W, prm);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;

@@ -94,6 +94,29 @@ def test_twar_exhaustive_2x2_sample():
         assert np.array_equal(predictor.decode_parallel_batch(res, p), imgs)
 
 
+@pytest.mark.parametrize("shape,n", [((32, 32), 13), ((16, 48), 9), ((64, 64), 3), ((24, 40), 5), ((100, 128), 2),
+                                     ((5, 37), 4), ((8, 8), 300)])
+@pytest.mark.parametrize("kind", ["default", "integral", "float"])
+def test_twar_forward_paths_vs_oracle(shape, n, kind):
+    """Every forward-residual kernel (whole images through shared memory for
+    W = 16 m up to 12 KB, 8-pixel runs for W = 8 m, the per-pixel kernel
+    otherwise) with each predictor arithmetic (the default predictor's
+    byte-lane path, integer weights, float weights) against the oracle,
+    partial image groups included."""
+    rng = np.random.default_rng(n * 31 + shape[1])
+    imgs = rng.integers(0, 256, (n, *shape, 3), dtype=np.uint8)
+    if kind == "default":
+        p = pc.default_params()
+    elif kind == "integral":
+        p = predictor.PredictorParams(np.array([[1, 0, -2], [2, -1, 1], [0, 3, -1]], np.float32),
+                                      np.array([5, -7, 300], np.float32))
+    else:
+        p = predictor.PredictorParams(rng.normal(0, 2, (3, 3)).astype(np.float32), rng.normal(0, 20, 3).astype(np.float32))
+    res = predictor.forward_residual_batch(imgs, p)
+    assert np.array_equal(res, O.twar_forward(imgs, p.weights, p.bias))
+    assert np.array_equal(predictor.decode_parallel_batch(res, p), imgs)
+
+
 # --- coder lanes --------------------------------------------------------------
 
 
