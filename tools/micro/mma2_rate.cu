@@ -149,8 +149,8 @@ int main() {
                 for (int i = 0; i < 148; ++i)
                     if (h[i]) s += h[i], ++k;
                 const double cyc = s / (k ? k : 1) / R;
-                printf("cta_group::%d %s N=%3d: %6.1f cyc/MMA instr (issuer), per SM-equivalent M=128 MMA %6.1f  %s\n", cg,
-                       mode ? "pair 64+32" : "single    ", N, cyc, cyc / cg, cudaGetErrorString(e));
+                printf("cta_group::%d %s N=%3d: %6.1f cycles per MMA instruction (each SM: one 128-row half)  %s\n", cg,
+                       mode ? "pair 64+32" : "single    ", N, cyc, cudaGetErrorString(e));
             }
     return 0;
 }
