@@ -738,7 +738,7 @@ def run_gpu(args):
             cpu, cpu_port = cpu_port, None
 
     if rank == 0:
-        roofline, stages = _roofline(prof, clk, args.steps)
+        roofline, stages = _roofline(prof, clk, args.steps, wl)
         line = {
             "metric": METRIC,
             "value": round(head["value"], 3),
@@ -781,11 +781,45 @@ def _round(e2e: dict) -> dict:
             for k, v in e2e.items()}
 
 
-def _roofline(prof, clk, steps):
+def _smem_operand_bytes(name, wl, K=256, B=4):
+    """Shared-memory bytes the tcgen05 MMAs of one launch read as operands
+    (SS mode: every MMA reads its A tile, 128 rows x 32 B per K=16 step, and
+    its B tile), for the trunk kernels on workload wl -- their other bound:
+    these N <= 64 convs read ~4-11 KB of operands per 128 x 32 x 16 step
+    against 128 B per cycle per SM."""
+    n, H, W = wl["N"], wl["H"], wl["W"]
+    gh, gw = (H + 1) // 2, (W + 1) // 2
+    Hp, Wp = gh + 2, gw + 2
+    if name == "enc_trunk_kernel":
+        tiles = (Hp * Wp + 127) // 128  # per image
+        per_step = 2 * (4096 + 2048) - 1024  # A_hi + [W_hi|W_lo] (N=64), A_lo + W_hi (N=32)
+        return n * tiles * (2 * B * 18 + 2) * per_step
+    if name == "dec_trunk_kernel":
+        def smem(G):  # dec_trunk_smem (tc_conv.cu)
+            rows = G * Hp * Wp
+            T = (rows + 127) // 128
+            RS = 2 * (Wp + 1) + rows
+            pad = ((128 * T - rows + 16) * 16 + 127) // 128 * 128
+            return 2 * 36 * 32 * 16 + K * 64 + 2 * 4 * RS * 16 + pad + (6 + 2 * 3 + 16) * 8 + 16 + 2 * B * 32 * 4, T
+        G = 0
+        for g in range(1, 65):
+            sm, T = smem(g)
+            if sm > 227 * 1024 or T > 16:
+                break
+            G = g
+        if not G:
+            return None
+        tiles = ((G * Hp * Wp + 127) // 128) * ((n + G - 1) // G)
+        return tiles * 2 * B * 18 * (4096 + 1024)
+    return None
+
+
+def _roofline(prof, clk, steps, wl=None):
     """Dominant kernel against its roofline (live per-launch CUDA events),
     plus every stage's rate: tensor kernels against the dense bf16 peak and
     the per-MMA floor, every kernel's DRAM bytes (committed ncu capture, per
-    launch) against the measured HBM bandwidth."""
+    launch) against the measured HBM bandwidth, and the trunk kernels' MMA
+    operand reads against the shared-memory bandwidth (128 B / cycle / SM)."""
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
             peaks = json.load(f)
@@ -846,6 +880,16 @@ def _roofline(prof, clk, steps):
                                      "frac": round(roofline["achieved"] / att, 4),
                                      "note": f"{floor_cyc:.0f} cycles per 128x32x16 step (measured per-MMA floor), "
                                              f"{sm} SMs at the sampled SM clock; ignores the padded border rows"}
+        ob = _smem_operand_bytes(name, wl) if wl else None
+        if ob and roofline:
+            smem_peak = 128.0 * sm * mhz * 1e6 / 1e9  # GB/s
+            got = ob / (ms / n / 1e3) / 1e9
+            roofline["smem_operand"] = {
+                "achieved": round(got, 1), "peak": round(smem_peak, 1), "unit": "GB/s", "frac": round(got / smem_peak, 4),
+                "bytes_per_launch": ob,
+                "note": "tcgen05 SS-mode operand reads (A 128 rows x 32 B + B per K=16 step, padded rows included) "
+                        "against 128 B/cycle/SM at the sampled clock: with N <= 64 outputs per MMA these convs are "
+                        "bound by operand reads / per-MMA cost, not by the dense tensor peak"}
         tr = _traffic(name)
         if tr is not None and roofline:
             roofline["traffic"] = tr
@@ -871,6 +915,9 @@ def _roofline(prof, clk, steps):
             if k in floor:
                 att = 2.0 * 128 * 32 * 16 / floor[k] * sm * mhz * 1e6 / 1e12
                 e["mma_floor_frac"] = round(tf / att, 4)
+            ob = _smem_operand_bytes(k, wl) if wl else None
+            if ob:
+                e["smem_operand_frac"] = round(ob * n / (ms / 1e3) / (128.0 * sm * mhz * 1e6), 4)
         elif ms > 0 and units > 0 and k.startswith("rans"):
             e["msym_s"] = round(units / (ms / 1e3) / 1e6, 1)
         stages[k] = e
