@@ -532,10 +532,11 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
     raw_all = raw_bytes * ctx.ws
 
     # the same steps through the pipelined public API (stream.StreamCodec):
-    # step k + 1's compress is queued before step k's decompress, so uploads
-    # and downloads run under other steps' kernels; every step still uploads
-    # its images and blobs and downloads its blobs and images. L2 is flushed
-    # on the kernel stream before each step's kernels.
+    # steps k + 1 and k + 2's compresses are queued before step k's
+    # decompress, so uploads and downloads run under other steps' kernels;
+    # every step still uploads its images and blobs and downloads its blobs
+    # and images. L2 is flushed on the kernel stream before each step's
+    # kernels.
     e_s = None
     if frames is None:
         from paper_2206_05279_b200.stream import StreamCodec
@@ -549,11 +550,14 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
                     with torch.cuda.stream(codec.kern):
                         ctx.flush.fill_(k & 0xFF)
                     return codec.compress(imgs)
-                fc, pend, last = comp(0), None, None
+                # two compress requests ahead: the kernel stream always holds
+                # the next step's work while this step's blobs make their round
+                # trip through host memory
+                fcs, pend, last = [comp(k) for k in range(min(2, k_steps))], None, None
                 for k in range(k_steps):
-                    buf_k, off_k = fc.result()
-                    if k + 1 < k_steps:
-                        fc = comp(k + 1)
+                    buf_k, off_k = fcs.pop(0).result()
+                    if k + 2 < k_steps:
+                        fcs.append(comp(k + 2))
                     fd = codec.decompress(buf_k, off_k)
                     if pend is not None:
                         last = pend.result()
@@ -565,7 +569,9 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
 
         stream_steps(max(3, warmup))
         ctx.barrier()
-        last, done = stream_steps(max(6, steps + 1))
+        # at least 12 intervals: the host-side completion thread makes single
+        # intervals jitter by ~10%
+        last, done = stream_steps(max(13, 2 * steps + 3))
         torch.cuda.synchronize(dev)
         assert np.array_equal(last, imgs)
         # steady-state step time: the median interval between consecutive
@@ -580,8 +586,8 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
         e2e = {"value": raw_all / 1e6 / e_s, "unit": "MB/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "api": "stream.StreamCodec: per step compress(images) then decompress(blobs) of the result, "
-                      "step k+1's compress queued before step k's decompress (copies under other steps' kernels); "
-                      "median interval between consecutive steps' completions",
+                      "steps k+1 and k+2's compresses queued before step k's decompress (copies under other steps' "
+                      "kernels); median interval between consecutive steps' completions",
                "sync": e2e_sync}
     else:
         e2e = e2e_sync
@@ -896,7 +902,8 @@ def _roofline(prof, clk, steps, wl=None):
             roofline["traffic_gbs"] = round(tr / (ms / n / 1e3) / 1e9, 1)
             roofline["traffic_frac_of_hbm"] = round(tr / (ms / n / 1e3) / 1e9 / peaks.get("hbm_gbs"), 4)
     ncu_name = {"enc_front_kernel": "enc_front_tc_kernel", "argmin_kernel": "argmin_tc_kernel",
-                "gather_kernel": "dec_table_kernel", "blob_sizes+scan": "blob_sizes_kernel"}
+                "gather_kernel": "dec_table_kernel", "blob_sizes+scan": "blob_sizes_kernel",
+                "twar_forward_kernel": "twar_forward_tile_kernel"}
     hbm_peak = peaks.get("hbm_gbs")
     tpeak = peaks.get("bf16_tflops")
     floor = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0, "enc_trunk_kernel": 92.0}

@@ -15,7 +15,7 @@ ids = []
 for r in rows[hi + 1:]:
     if len(r) > ki and (not ids or ids[-1][0] != r[ii]):
         ids.append((r[ii], r[ki]))
-starts = [n for n, (_, k) in enumerate(ids) if "twar_forward_kernel" in k]
+starts = [n for n, (_, k) in enumerate(ids) if "twar_forward" in k]
 print(starts[-1], len(ids) - starts[-1])
 PY
 )
