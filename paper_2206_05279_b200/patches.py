@@ -19,6 +19,17 @@ from .errors import FormatError
 from .device import h2d, pinned, require_device
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(dev, i: int) -> torch.cuda.Stream:
+    """Per-device side streams for the shape groups of a frame batch."""
+    key = (dev.index, i)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(dev)
+    return _SIDE[key]
+
+
 def patch_grid(H: int, W: int, ph: int = 64, pw: int = 64):
     """[(y0, y1, x0, x1)] in raster order."""
     return [(y, min(y + ph, H), x, min(x + pw, W)) for y in range(0, H, ph) for x in range(0, W, pw)]
@@ -89,17 +100,28 @@ def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph:
     groups = _groups(H, W, ph, pw)
     ridx = _raster_index(H, W, ph, pw)
     per = sum(len(r) for r in ridx)
-    parts = []
-    for g in groups:
-        out_d, off_d, _ = compress_batch(_group_patches(frames_d, g), model, config, device=dev, return_device=True)
-        parts.append((out_d, off_d))
-    offs_h = []
-    for out_d, off_d in parts:
-        h = pinned(off_d.numel() * 8)
-        with torch.cuda.stream(stream):
+    # every shape group compresses on its own stream (their latency-bound
+    # coder kernels overlap); offsets are read once all are queued
+    ev_in = torch.cuda.Event()
+    ev_in.record(stream)
+    parts, offs_h, evs = [], [], []
+    for gi, g in enumerate(groups):
+        s = stream if gi == 0 else _side_stream(dev, gi)
+        s.wait_event(ev_in)
+        frames_d.record_stream(s)
+        with torch.cuda.stream(s):
+            out_d, off_d, _ = compress_batch(_group_patches(frames_d, g), model, config, device=dev,
+                                             return_device=True)
+            h = pinned(off_d.numel() * 8)
             h.copy_(off_d.view(torch.uint8), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s)
+        parts.append((out_d, off_d))
         offs_h.append(h)
-    stream.synchronize()
+        evs.append(ev)
+    for ev in evs:
+        ev.synchronize()
+        stream.wait_event(ev)
     goffs = [h.numpy().view(np.uint64) for h in offs_h]
     sizes = np.zeros((F, per), np.uint64)
     for off, r in zip(goffs, ridx):
@@ -142,14 +164,25 @@ def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None
                           f"{per} patches")
     buf_d = h2d(buffer[: int(offsets[F * per])], dev, stream)
     frames_d = torch.empty((F, H, W, 3), dtype=torch.uint8, device=dev)
-    with torch.cuda.stream(stream):
-        for g, r in zip(groups, ridx):
-            rows, cols, nr, nc, h, w = g
-            k = len(r)
-            pos = (np.arange(F)[:, None] * per + r[None, :]).reshape(-1)
-            lens = offsets[pos + 1] - offsets[pos]
-            goff = np.zeros(F * k + 1, np.uint64)
-            np.cumsum(lens, out=goff[1:])
+    ev_buf = torch.cuda.Event()
+    ev_buf.record(stream)
+    # every shape group decodes on its own stream (the groups' latency-bound
+    # coder and wavefront kernels overlap), launched before any host read;
+    # the results are checked afterwards
+    launched = []
+    for gi, (g, r) in enumerate(zip(groups, ridx)):
+        k = len(r)
+        s = stream if gi == 0 else _side_stream(dev, gi)
+        s.wait_event(ev_buf)
+        buf_d.record_stream(s)
+        frames_d.record_stream(s)
+        pos = (np.arange(F)[:, None] * per + r[None, :]).reshape(-1)
+        lens = offsets[pos + 1] - offsets[pos]
+        goff_h = pinned(8 * (F * k + 1))
+        goff = goff_h.numpy().view(np.uint64)
+        goff[0] = 0
+        np.cumsum(lens, out=goff[1:])
+        with torch.cuda.stream(s):
             gbuf = torch.empty(int(goff[-1]) + 16, dtype=torch.uint8, device=dev)
             gbuf[int(goff[-1]):].zero_()
             contiguous = bool(np.all(np.diff(r) == 1))
@@ -159,18 +192,26 @@ def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None
                     s0, s1 = int(offsets[f * per + r[j0]]), int(offsets[f * per + r[j1 - 1] + 1])
                     d0 = int(goff[f * k + j0])
                     gbuf[d0:d0 + s1 - s0].copy_(buf_d[s0:s1], non_blocking=True)
-            goff_d = torch.from_numpy(goff.view(np.int64)).to(dev, non_blocking=False)
-            results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, stream)
+            goff_d = torch.empty(F * k + 1, dtype=torch.int64, device=dev)
+            goff_d.view(torch.uint8).copy_(goff_h, non_blocking=True)
+            res = _decompress_device(gbuf, goff_d, F * k, model, dev, s)
+        launched.append((g, s, gbuf, goff_d, goff_h, res, k))
+    for g, s, gbuf, goff_d, goff_h, (results, errors, hdr), k in launched:
+        rows, cols, nr, nc, h, w = g
+        with torch.cuda.stream(s):
             try:
                 _verify(results)
             except SpeculationMiss:
-                results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, stream, speculate=False)
+                results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, s, speculate=False)
             errors = _resolve_errors(results, errors, hdr)
             if errors:
                 raise errors[min(errors)]
             img = results[0][1]
             frames_d[:, rows, cols] = img.reshape(F, nr, nc, h, w, 3).permute(0, 1, 3, 2, 4, 5).reshape(
                 F, nr * h, nc * w, 3)
+            ev = torch.cuda.Event()
+            ev.record(s)
+        stream.wait_event(ev)
     host = pinned(frames_d.numel())
     with torch.cuda.stream(stream):
         host.copy_(frames_d.view(-1), non_blocking=True)
