@@ -500,7 +500,7 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
     def api_round():
         if frames is not None:
             from paper_2206_05279_b200 import patches as pt
-            buf, off = pt.compress_frames(frames, model, cfg, wl["P"], wl["P"])
+            buf, off = pt.compress_frames(imgs, model, cfg, wl["P"], wl["P"])  # the page-locked copy
             torch.cuda.synchronize(dev)
             t1 = time.perf_counter()
             out = pt.decompress_frames(buf, off, len(frames), wl["H"], wl["W"], model, wl["P"], wl["P"])
@@ -538,7 +538,7 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
     # and images. L2 is flushed on the kernel stream before each step's
     # kernels.
     e_s = None
-    if frames is None:
+    if True:
         from paper_2206_05279_b200.stream import StreamCodec
 
         def stream_steps(k_steps):
@@ -549,7 +549,14 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
                 def comp(k):
                     with torch.cuda.stream(codec.kern):
                         ctx.flush.fill_(k & 0xFF)
+                    if frames is not None:
+                        return codec.compress_frames(imgs, wl["P"], wl["P"])
                     return codec.compress(imgs)
+
+                def decomp(b, o):
+                    if frames is not None:
+                        return codec.decompress_frames(b, o, len(frames), wl["H"], wl["W"], wl["P"], wl["P"])
+                    return codec.decompress(b, o)
                 # two compress requests ahead: the kernel stream always holds
                 # the next step's work while this step's blobs make their round
                 # trip through host memory
@@ -558,7 +565,7 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
                     buf_k, off_k = fcs.pop(0).result()
                     if k + 2 < k_steps:
                         fcs.append(comp(k + 2))
-                    fd = codec.decompress(buf_k, off_k)
+                    fd = decomp(buf_k, off_k)
                     if pend is not None:
                         last = pend.result()
                         done.append(time.perf_counter())
@@ -581,11 +588,13 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
     e2e_sync = {"value": raw_all / 1e6 / e_t, "unit": "MB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "compress_mb_s": round(raw_all / 1e6 / e_c, 3),
                 "decompress_mb_s": round(raw_all / 1e6 / e_d, 3),
-                "api": "compress_batch + decompress_batch, one synchronous call each per step"}
+                "api": ("patches.compress_frames + decompress_frames" if frames is not None else
+                        "compress_batch + decompress_batch") + ", one synchronous call each per step"}
     if e_s is not None:
         e2e = {"value": raw_all / 1e6 / e_s, "unit": "MB/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
-               "api": "stream.StreamCodec: per step compress(images) then decompress(blobs) of the result, "
+               "api": "stream.StreamCodec: per step compress" + ("_frames(frames)" if frames is not None else
+                                                                 "(images)") + " then decompress of the result, "
                       "steps k+1 and k+2's compresses queued before step k's decompress (copies under other steps' "
                       "kernels); median interval between consecutive steps' completions",
                "sync": e2e_sync}

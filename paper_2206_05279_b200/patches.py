@@ -85,29 +85,15 @@ def _group_patches(frames, g):
     return np.ascontiguousarray(v.transpose(0, 1, 3, 2, 4, 5)).reshape(F * nr * nc, h, w, 3)
 
 
-def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph: int = 64, pw: int = 64,
-                    device=None):
-    """Frames (F, H, W, 3) -> (buffer, offsets) of F * n_patches blobs, frame
-    by frame, raster order within a frame. The frames go to the GPU once; each
-    shape group of the patch grid is cut there and compressed as one batch;
-    each (frame, group) run of blobs is copied from the device straight to its
-    place in the page-locked result (no host-side shuffling)."""
-    dev = require_device(device)
-    stream = torch.cuda.current_stream(dev)
-    frames_d = frames if isinstance(frames, torch.Tensor) else torch.from_numpy(np.asarray(frames, dtype=np.uint8))
-    frames_d = frames_d.to(dev)
+def _compress_launch(frames_d, model, config, ph, pw, dev, streams, after):
+    """Queue every shape group's compress (group i on streams[i], after the
+    event `after`) and the D2H of its offsets; returns (parts, pinned
+    offsets, events)."""
     F, H, W = frames_d.shape[:3]
-    groups = _groups(H, W, ph, pw)
-    ridx = _raster_index(H, W, ph, pw)
-    per = sum(len(r) for r in ridx)
-    # every shape group compresses on its own stream (their latency-bound
-    # coder kernels overlap); offsets are read once all are queued
-    ev_in = torch.cuda.Event()
-    ev_in.record(stream)
     parts, offs_h, evs = [], [], []
-    for gi, g in enumerate(groups):
-        s = stream if gi == 0 else _side_stream(dev, gi)
-        s.wait_event(ev_in)
+    for gi, g in enumerate(_groups(H, W, ph, pw)):
+        s = streams[gi]
+        s.wait_event(after)
         frames_d.record_stream(s)
         with torch.cuda.stream(s):
             out_d, off_d, _ = compress_batch(_group_patches(frames_d, g), model, config, device=dev,
@@ -119,9 +105,15 @@ def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph:
         parts.append((out_d, off_d))
         offs_h.append(h)
         evs.append(ev)
-    for ev in evs:
-        ev.synchronize()
-        stream.wait_event(ev)
+    return parts, offs_h, evs
+
+
+def _compress_gather(parts, offs_h, F, H, W, ph, pw, stream):
+    """Frame-ordered offsets (host, once the groups' offsets are back) and
+    the D2H of each (frame, group) run of blobs into its place in one
+    page-locked buffer, on `stream`; returns (host tensor, offsets)."""
+    ridx = _raster_index(H, W, ph, pw)
+    per = sum(len(r) for r in ridx)
     goffs = [h.numpy().view(np.uint64) for h in offs_h]
     sizes = np.zeros((F, per), np.uint64)
     for off, r in zip(goffs, ridx):
@@ -131,6 +123,7 @@ def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph:
     host = pinned(int(offsets[-1]) + 8)
     with torch.cuda.stream(stream):
         for (out_d, _), off, r in zip(parts, goffs, ridx):
+            out_d.record_stream(stream)
             k = len(r)
             for f in range(F):
                 if bool(np.all(np.diff(r) == 1)):  # one run per frame
@@ -141,41 +134,62 @@ def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph:
                     s0, s1 = int(off[f * k + j0]), int(off[f * k + j1])
                     d0 = int(offsets[f * per + r[j0]])
                     host[d0:d0 + s1 - s0].copy_(out_d[s0:s1], non_blocking=True)
+    return host, offsets
+
+
+def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph: int = 64, pw: int = 64,
+                    device=None):
+    """Frames (F, H, W, 3) -> (buffer, offsets) of F * n_patches blobs, frame
+    by frame, raster order within a frame. The frames go to the GPU once; each
+    shape group of the patch grid is cut there and compressed as one batch
+    (each group on its own stream: their latency-bound coder kernels
+    overlap); each (frame, group) run of blobs is copied from the device
+    straight to its place in the page-locked result (no host-side
+    shuffling)."""
+    dev = require_device(device)
+    stream = torch.cuda.current_stream(dev)
+    if isinstance(frames, torch.Tensor):
+        frames_d = frames.to(dev)
+    else:  # page-locked frames (e.g. ones this package returned) upload asynchronously
+        arr = np.asarray(frames, dtype=np.uint8)
+        frames_d = h2d(arr, dev, stream).view(arr.shape)
+    F, H, W = frames_d.shape[:3]
+    ev_in = torch.cuda.Event()
+    ev_in.record(stream)
+    n_groups = len(_groups(H, W, ph, pw))
+    streams = [stream] + [_side_stream(dev, i) for i in range(1, n_groups)]
+    parts, offs_h, evs = _compress_launch(frames_d, model, config, ph, pw, dev, streams, ev_in)
+    for ev in evs:
+        ev.synchronize()
+        stream.wait_event(ev)
+    host, offsets = _compress_gather(parts, offs_h, F, H, W, ph, pw, stream)
     stream.synchronize()
     return host.numpy()[: int(offsets[-1])], offsets
 
 
-def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None, ph: int = 64, pw: int = 64,
-                      device=None):
-    """Inverse of compress_frames: the blob buffer goes to the GPU once, each
-    shape group is gathered there (device copies of its (frame, group) runs),
-    decoded as one batch, written into device frames, and the frames come
-    back in one copy."""
-    dev = require_device(device)
-    stream = torch.cuda.current_stream(dev)
+def _check_frame_offsets(buffer, offsets, n_frames, H, W, ph, pw):
     buffer = np.asarray(buffer, dtype=np.uint8)
     offsets = check_offsets(offsets)
+    per = sum(len(r) for r in _raster_index(H, W, ph, pw))
+    if offsets.size != n_frames * per + 1 or int(offsets[-1]) > buffer.size:
+        raise FormatError(f"expected {n_frames * per + 1} blob offsets within the buffer for {n_frames} frame(s) of "
+                          f"{per} patches")
+    return buffer, offsets
+
+
+def _decode_launch(buf_d, offsets, F, H, W, model, ph, pw, dev, streams, after):
+    """Queue every shape group's decode (group i on streams[i], after the
+    event `after`): its blobs gathered on the device, then the speculative
+    decode; no host read. Returns the launched groups."""
     groups = _groups(H, W, ph, pw)
     ridx = _raster_index(H, W, ph, pw)
     per = sum(len(r) for r in ridx)
-    F = n_frames
-    if offsets.size != F * per + 1 or int(offsets[-1]) > buffer.size:
-        raise FormatError(f"expected {F * per + 1} blob offsets within the buffer for {F} frame(s) of "
-                          f"{per} patches")
-    buf_d = h2d(buffer[: int(offsets[F * per])], dev, stream)
-    frames_d = torch.empty((F, H, W, 3), dtype=torch.uint8, device=dev)
-    ev_buf = torch.cuda.Event()
-    ev_buf.record(stream)
-    # every shape group decodes on its own stream (the groups' latency-bound
-    # coder and wavefront kernels overlap), launched before any host read;
-    # the results are checked afterwards
     launched = []
     for gi, (g, r) in enumerate(zip(groups, ridx)):
         k = len(r)
-        s = stream if gi == 0 else _side_stream(dev, gi)
-        s.wait_event(ev_buf)
+        s = streams[gi]
+        s.wait_event(after)
         buf_d.record_stream(s)
-        frames_d.record_stream(s)
         pos = (np.arange(F)[:, None] * per + r[None, :]).reshape(-1)
         lens = offsets[pos + 1] - offsets[pos]
         goff_h = pinned(8 * (F * k + 1))
@@ -196,6 +210,16 @@ def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None
             goff_d.view(torch.uint8).copy_(goff_h, non_blocking=True)
             res = _decompress_device(gbuf, goff_d, F * k, model, dev, s)
         launched.append((g, s, gbuf, goff_d, goff_h, res, k))
+    return launched
+
+
+def _decode_finish(launched, frames_d, model, dev, out_stream=None):
+    """Check each launched group (blocks on its summary), raise its first
+    error, and write its patches into frames_d (on the group's stream, or on
+    out_stream after the group's decode when given); returns the events the
+    frames are complete after."""
+    F = frames_d.shape[0]
+    evs = []
     for g, s, gbuf, goff_d, goff_h, (results, errors, hdr), k in launched:
         rows, cols, nr, nc, h, w = g
         with torch.cuda.stream(s):
@@ -203,14 +227,45 @@ def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None
                 _verify(results)
             except SpeculationMiss:
                 results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, s, speculate=False)
+            done = torch.cuda.Event()
+            done.record(s)
+        ws = out_stream if out_stream is not None else s
+        with torch.cuda.stream(ws):
+            ws.wait_event(done)
             errors = _resolve_errors(results, errors, hdr)
             if errors:
                 raise errors[min(errors)]
             img = results[0][1]
+            img.record_stream(ws)
+            frames_d.record_stream(ws)
             frames_d[:, rows, cols] = img.reshape(F, nr, nc, h, w, 3).permute(0, 1, 3, 2, 4, 5).reshape(
                 F, nr * h, nc * w, 3)
             ev = torch.cuda.Event()
-            ev.record(s)
+            ev.record(ws)
+        evs.append(ev)
+    return evs
+
+
+def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None, ph: int = 64, pw: int = 64,
+                      device=None):
+    """Inverse of compress_frames: the blob buffer goes to the GPU once, each
+    shape group is gathered there (device copies of its (frame, group) runs)
+    and decoded as one batch on its own stream (the groups' latency-bound
+    coder and wavefront kernels overlap; every group is queued before any
+    host read), written into device frames, and the frames come back in one
+    copy."""
+    dev = require_device(device)
+    stream = torch.cuda.current_stream(dev)
+    buffer, offsets = _check_frame_offsets(buffer, offsets, n_frames, H, W, ph, pw)
+    F = n_frames
+    buf_d = h2d(buffer[: int(offsets[-1])], dev, stream)
+    frames_d = torch.empty((F, H, W, 3), dtype=torch.uint8, device=dev)
+    ev_buf = torch.cuda.Event()
+    ev_buf.record(stream)
+    n_groups = len(_groups(H, W, ph, pw))
+    streams = [stream] + [_side_stream(dev, i) for i in range(1, n_groups)]
+    launched = _decode_launch(buf_d, offsets, F, H, W, model, ph, pw, dev, streams, ev_buf)
+    for ev in _decode_finish(launched, frames_d, model, dev):
         stream.wait_event(ev)
     host = pinned(frames_d.numel())
     with torch.cuda.stream(stream):

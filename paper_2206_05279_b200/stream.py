@@ -16,6 +16,10 @@ composition).
     g = codec.decompress(*f.result())     # Future[images]
     images_back = g.result()
 
+Frames split into patch containers (patches.compress_frames /
+decompress_frames, BASELINE config 4) go through compress_frames /
+decompress_frames the same way.
+
 Kernels of different requests run in submission order on the one kernel
 stream (never concurrently: the persistent-grid kernels would only slow
 each other down).
@@ -32,6 +36,7 @@ from .container import (CodecConfig, SpeculationMiss, _compress_device, _decompr
                         _verify, check_offsets)
 from .device import pinned, require_device
 from .errors import FormatError, ParameterError
+from . import patches as _pt
 
 
 class StreamCodec:
@@ -166,5 +171,56 @@ class StreamCodec:
                 for j, i in enumerate(np.asarray(ids)):
                     imgs[int(i)] = arr[j]
             return imgs
+
+        return self._done.submit(finish)
+
+    # -- frames as patch containers (patches.py) ----------------------------
+
+    def compress_frames(self, frames, ph: int = 64, pw: int = 64) -> Future:
+        """Future[(buffer, offsets)] of patches.compress_frames(frames, ...)."""
+        arr = np.asarray(frames)
+        if arr.dtype != np.uint8 or arr.ndim != 4 or arr.shape[-1] != 3 or arr.shape[1] < 1 or arr.shape[2] < 1:
+            raise ParameterError("expected uint8 (F, H, W, 3) frames")
+        F, H, W = arr.shape[:3]
+        if F == 0:
+            f: Future = Future()
+            f.set_result((np.zeros(0, np.uint8), np.zeros(1, np.uint64)))
+            return f
+        fr_d, ev_up, keep = self._upload(arr)
+        n_groups = len(_pt._groups(H, W, ph, pw))
+        parts, offs_h, evs = _pt._compress_launch(fr_d.view(arr.shape), self.model, self.config, ph, pw, self.dev,
+                                                  [self.kern] * n_groups, ev_up)
+
+        def finish():
+            for ev in evs:
+                ev.synchronize()
+                self.down.wait_event(ev)
+            host, offsets = _pt._compress_gather(parts, offs_h, F, H, W, ph, pw, self.down)
+            done = torch.cuda.Event()
+            done.record(self.down)
+            done.synchronize()
+            assert keep is not None
+            return host.numpy()[: int(offsets[-1])], offsets
+
+        return self._done.submit(finish)
+
+    def decompress_frames(self, buffer, offsets, n_frames: int, H: int, W: int, ph: int = 64,
+                          pw: int = 64) -> Future:
+        """Future[frames] of patches.decompress_frames(buffer, offsets, ...)."""
+        buf_host, offs = _pt._check_frame_offsets(buffer, offsets, n_frames, H, W, ph, pw)
+        buf_d, ev_b, keep_b = self._upload(buf_host[: int(offs[-1])], nbytes_pad=16)
+        with torch.cuda.device(self.dev):
+            frames_d = torch.empty((n_frames, H, W, 3), dtype=torch.uint8, device=self.dev)
+        n_groups = len(_pt._groups(H, W, ph, pw))
+        launched = _pt._decode_launch(buf_d, offs, n_frames, H, W, self.model, ph, pw, self.dev,
+                                      [self.kern] * n_groups, ev_b)
+
+        def finish():
+            evs = _pt._decode_finish(launched, frames_d, self.model, self.dev, out_stream=self.down)
+            ev = evs[-1] if evs else torch.cuda.Event()
+            if not evs:
+                ev.record(self.down)
+            assert keep_b is not None
+            return self._download(frames_d, ev, frames_d.numel()).reshape(n_frames, H, W, 3)
 
         return self._done.submit(finish)

@@ -827,6 +827,30 @@ def test_edge_cases_of_the_batch_apis(small_model, full_model):
     assert np.array_equal(pc.decompress(blob, full_model), img)
 
 
+def test_stream_codec_frames_match_sync_calls(full_model):
+    """StreamCodec.compress_frames / decompress_frames (patch containers,
+    several requests in flight, two patch sizes with ragged edge groups)
+    return exactly what patches.compress_frames / decompress_frames return."""
+    from paper_2206_05279_b200 import patches as pt
+    from paper_2206_05279_b200.stream import StreamCodec
+
+    reqs = [(smooth_images(2, 150, 200, seed=s), 64) for s in range(3)] + [(smooth_images(3, 70, 90, seed=7), 32)]
+    with StreamCodec(full_model, FAST) as codec:
+        futs = [codec.compress_frames(fr, p, p) for fr, p in reqs]
+        packed = [f.result() for f in futs]
+        backs = [codec.decompress_frames(buf, off, len(fr), fr.shape[1], fr.shape[2], p, p)
+                 for (fr, p), (buf, off) in zip(reqs, packed)]
+        for (fr, p), (buf, off), g in zip(reqs, packed, backs):
+            rb, ro = pt.compress_frames(fr, full_model, FAST, p, p)
+            assert np.array_equal(off, ro) and buf.tobytes() == rb.tobytes()
+            assert np.array_equal(g.result(), fr)
+        bad = np.array(packed[0][0], copy=True)
+        bad[int(packed[0][1][5]) + 40] ^= 0x10
+        with pytest.raises(CorruptStreamError):
+            codec.decompress_frames(bad, packed[0][1], 2, 150, 200, 64, 64).result()
+        assert np.array_equal(codec.decompress_frames(*packed[1], 2, 150, 200, 64, 64).result(), reqs[1][0])
+
+
 def test_stream_codec_matches_sync_calls(full_model):
     """StreamCodec (stream.py): pipelined requests (uploads, kernels and
     downloads on separate streams, results as futures) return exactly what
