@@ -803,6 +803,8 @@ def _smem_operand_bytes(name, wl, K=256, B=4):
     these N <= 64 convs read ~4-11 KB of operands per 128 x 32 x 16 step
     against 128 B per cycle per SM."""
     n, H, W = wl["N"], wl["H"], wl["W"]
+    if wl.get("P"):  # frames as P x P patch containers (ragged edge patches counted as full ones)
+        n, H, W = n * (-(-H // wl["P"])) * (-(-W // wl["P"])), wl["P"], wl["P"]
     gh, gw = (H + 1) // 2, (W + 1) // 2
     Hp, Wp = gh + 2, gw + 2
     if name == "enc_trunk_kernel":
