@@ -43,12 +43,14 @@ __device__ __forceinline__ void mma_tap(uint32_t d, uint32_t a0, uint32_t a1, ui
 
 __global__ void bench(int mode, int tiles, long long *out) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, tb[2];
     __shared__ uint32_t slot;
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0;
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tb[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tb[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -101,7 +103,7 @@ __global__ void bench(int mode, int tiles, long long *out) {
                     }
                 }
             }
-        } else {
+        } else if (mode == 2) {
             const uint32_t ah = (uint32_t)(dA >> 32), bl = (uint32_t)dB, bh = (uint32_t)(dB >> 32);
             for (int t = 0; t < tiles; ++t) {
                 const uint32_t d = tmem + (uint32_t)((t & 1) * 64);
@@ -113,6 +115,33 @@ __global__ void bench(int mode, int tiles, long long *out) {
                     mma_tap(d, al + off, al + off + 4 * rx, al + off + 2 * rx, al + off + 6 * rx, ah, b0, b1, bh, id64, id32,
                             tap ? 1u : 0u);
                 }
+            }
+        } else {
+            // modes 3 / 4: as mode 1 plus a commit per tile onto the tile's
+            // accumulator barrier; mode 4 also waits, before tile t, for tile
+            // t - 2's commit (the accumulator it reuses) -- the trunk kernels'
+            // loop with an instantaneous epilogue
+            const uint32_t ah = (uint32_t)(dA >> 32), bl = (uint32_t)dB, bh = (uint32_t)(dB >> 32);
+            for (int t = 0; t < tiles; ++t) {
+                const int a = t & 1;
+                if (mode == 4 && t >= 2) {
+                    asm volatile("{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@P1 bra D;\n\tbra W;\n\tD:\n\t}" ::"r"(smem_u32(&tb[a])), "r"((uint32_t)(((t - 2) >> 1) & 1)) : "memory");
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                const uint32_t d = tmem + (uint32_t)(a * 64);
+                const uint32_t al = (uint32_t)dA + (uint32_t)(19 + 128 * (t % 3) - Wp - 1);
+#pragma unroll
+                for (int tap = 0; tap < 9; ++tap) {
+                    const uint32_t off = (uint32_t)((tap / 3) * Wp + tap % 3);
+#pragma unroll
+                    for (int ks = 0; ks < 2; ++ks) {
+                        const uint32_t ao = 2u * ks * rx + off;
+                        const uint32_t bo = (uint32_t)((tap * 4 + 2 * ks) * 64);
+                        mma_w(d, al + ao, ah, bl + bo, bh, id64, (tap | ks) ? 1u : 0u);
+                        mma_w(d + 32, al + ao + 4 * rx, ah, bl + bo, bh, id32, 1u);
+                    }
+                }
+                asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&tb[a])) : "memory");
             }
         }
         if (threadIdx.x == 32)
@@ -132,7 +161,7 @@ int main() {
     long long h[148];
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int tiles = 300;
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
         for (int rep = 0; rep < 2; ++rep) bench<<<148, 128, 200 * 1024>>>(mode, tiles, d);
         cudaError_t e = cudaDeviceSynchronize();
         cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
