@@ -15,7 +15,7 @@ import torch
 
 from .container import (CodecConfig, SpeculationMiss, _decompress_device, _resolve_errors, _verify, check_offsets,
                         compress_batch)
-from .errors import FormatError
+from .errors import FormatError, ParameterError
 from .device import h2d, pinned, require_device
 
 
@@ -146,6 +146,7 @@ def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph:
     overlap); each (frame, group) run of blobs is copied from the device
     straight to its place in the page-locked result (no host-side
     shuffling)."""
+    _check_patch(ph, pw)
     dev = require_device(device)
     stream = torch.cuda.current_stream(dev)
     if isinstance(frames, torch.Tensor):
@@ -153,7 +154,11 @@ def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph:
     else:  # page-locked frames (e.g. ones this package returned) upload asynchronously
         arr = np.asarray(frames, dtype=np.uint8)
         frames_d = h2d(arr, dev, stream).view(arr.shape)
+    if frames_d.dim() != 4 or frames_d.shape[-1] != 3 or frames_d.dtype != torch.uint8:
+        raise ParameterError("expected uint8 (F, H, W, 3) frames")
     F, H, W = frames_d.shape[:3]
+    if F == 0:
+        return np.zeros(0, np.uint8), np.zeros(1, np.uint64)
     ev_in = torch.cuda.Event()
     ev_in.record(stream)
     n_groups = len(_groups(H, W, ph, pw))
@@ -167,7 +172,15 @@ def compress_frames(frames, model=None, config: CodecConfig = CodecConfig(), ph:
     return host.numpy()[: int(offsets[-1])], offsets
 
 
+def _check_patch(ph: int, pw: int) -> None:
+    if int(ph) < 1 or int(pw) < 1:
+        raise ParameterError("patch sizes must be at least 1")
+
+
 def _check_frame_offsets(buffer, offsets, n_frames, H, W, ph, pw):
+    _check_patch(ph, pw)
+    if int(n_frames) < 0 or int(H) < 1 or int(W) < 1:
+        raise ParameterError("expected n_frames >= 0 frames of at least 1 x 1 pixels")
     buffer = np.asarray(buffer, dtype=np.uint8)
     offsets = check_offsets(offsets)
     per = sum(len(r) for r in _raster_index(H, W, ph, pw))
@@ -258,6 +271,8 @@ def decompress_frames(buffer, offsets, n_frames: int, H: int, W: int, model=None
     stream = torch.cuda.current_stream(dev)
     buffer, offsets = _check_frame_offsets(buffer, offsets, n_frames, H, W, ph, pw)
     F = n_frames
+    if F == 0:
+        return np.zeros((0, H, W, 3), np.uint8)
     buf_d = h2d(buffer[: int(offsets[-1])], dev, stream)
     frames_d = torch.empty((F, H, W, 3), dtype=torch.uint8, device=dev)
     ev_buf = torch.cuda.Event()

@@ -181,6 +181,7 @@ class StreamCodec:
         arr = np.asarray(frames)
         if arr.dtype != np.uint8 or arr.ndim != 4 or arr.shape[-1] != 3 or arr.shape[1] < 1 or arr.shape[2] < 1:
             raise ParameterError("expected uint8 (F, H, W, 3) frames")
+        _pt._check_patch(ph, pw)
         F, H, W = arr.shape[:3]
         if F == 0:
             f: Future = Future()
@@ -208,6 +209,10 @@ class StreamCodec:
                           pw: int = 64) -> Future:
         """Future[frames] of patches.decompress_frames(buffer, offsets, ...)."""
         buf_host, offs = _pt._check_frame_offsets(buffer, offsets, n_frames, H, W, ph, pw)
+        if n_frames == 0:
+            f: Future = Future()
+            f.set_result(np.zeros((0, H, W, 3), np.uint8))
+            return f
         buf_d, ev_b, keep_b = self._upload(buf_host[: int(offs[-1])], nbytes_pad=16)
         with torch.cuda.device(self.dev):
             frames_d = torch.empty((n_frames, H, W, 3), dtype=torch.uint8, device=self.dev)

@@ -919,3 +919,30 @@ def test_randomized_configs_round_trip_and_oracle(seed, small_model, full_model)
         else:
             assert blob == O.compress(imgs[k], om, backend=backend, M=M, L=L, debug_sched=dbg), \
                 (H, W, backend, numerics, M, L)
+
+
+def test_frame_api_edge_cases(small_model):
+    """Frame API arguments: zero frames, patch sizes below 1, patches larger
+    than the frame (one ragged group), one-pixel frames -- synchronous and
+    through StreamCodec."""
+    from paper_2206_05279_b200 import patches as pt
+    from paper_2206_05279_b200.errors import ParameterError
+    from paper_2206_05279_b200.stream import StreamCodec
+
+    empty = np.zeros((0, 20, 30, 3), np.uint8)
+    buf, off = pt.compress_frames(empty, small_model, EXACT, 16, 16)
+    assert buf.size == 0 and off.tolist() == [0]
+    assert pt.decompress_frames(buf, off, 0, 20, 30, small_model, 16, 16).shape == (0, 20, 30, 3)
+    with pytest.raises(ParameterError):
+        pt.compress_frames(smooth_images(1, 8, 8, seed=1), small_model, EXACT, 0, 8)
+    with pytest.raises(ParameterError):
+        pt.decompress_frames(buf, off, 0, 20, 30, small_model, 8, -1)
+    for shape, p in (((1, 20, 30), 64), ((2, 1, 1), 8), ((1, 9, 70), 4)):
+        fr = smooth_images(shape[0], shape[1], shape[2], seed=shape[2])
+        b, o = pt.compress_frames(fr, small_model, EXACT, p, p)
+        assert np.array_equal(pt.decompress_frames(b, o, shape[0], shape[1], shape[2], small_model, p, p), fr)
+    with StreamCodec(small_model, EXACT) as codec:
+        b, o = codec.compress_frames(empty, 16, 16).result()
+        assert b.size == 0 and codec.decompress_frames(b, o, 0, 20, 30, 16, 16).result().shape == (0, 20, 30, 3)
+        with pytest.raises(ParameterError):
+            codec.compress_frames(smooth_images(1, 8, 8, seed=1), 8, 0)
