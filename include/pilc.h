@@ -197,6 +197,14 @@ int pilc_vq_fast_decoder(int32_t K, int32_t Dc, int32_t C, int32_t B, int32_t H,
 int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model,
                    int32_t K, int32_t Dc, int32_t C, int32_t B, uint8_t *idx_out,
                    void *stream);
+/* The same on the tensor cores: the encoders' argmin (3xTF32 distance GEMM,
+ * proven error radius, exact float64 rescore), fed from plain z. Dc == 32
+ * and C == 32 only (PILC_E_UNSUPPORTED otherwise); workspace >=
+ * pilc_vq_argmin_tc_workspace(n_vec) bytes (z as 128-latent tiles). */
+int64_t pilc_vq_argmin_tc_workspace(int64_t n_vec);
+int pilc_vq_argmin_tc(const float *z, int64_t n_vec, const float *model,
+                      int32_t K, int32_t Dc, int32_t C, int32_t B, void *workspace,
+                      int64_t ws_bytes, uint8_t *idx_out, void *stream);
 /* decode_to_params (vqvae.py:79-113) fused with the logistic head
  * (logistic.round_half_away / scales_to_distributions, logistic.py:36-40,
  * 109-114): indices -> shift = round(mu) and d per subpixel (N, H, W, 3)

@@ -35,6 +35,8 @@ _SIGS = {
     "pilc_vq_encode_exact": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I64, P, P, P]),
     "pilc_vq_fast_decoder": (ctypes.c_int, [I32, I32, I32, I32, I32, I32]),
     "pilc_vq_argmin": (ctypes.c_int, [P, I64, P, I32, I32, I32, I32, P, P]),
+    "pilc_vq_argmin_tc_workspace": (I64, [I64]),
+    "pilc_vq_argmin_tc": (ctypes.c_int, [P, I64, P, I32, I32, I32, I32, P, I64, P, P]),
     "pilc_vq_decode": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, P]),
     "pilc_vq_decode_exact": (ctypes.c_int, [P, I64, I32, I32, P, I32, I32, I32, I32, P, I32, P, I64, P, P, P, P, P]),
     "pilc_static_scale": (ctypes.c_int, [P, I64, I64, P, I32, P, P]),

@@ -2660,7 +2660,39 @@ __global__ void gather_kernel(const uint8_t *__restrict__ idx, const uint16_t *_
 
 }  // namespace
 
+__global__ void pack_z_tiles_kernel(const float *__restrict__ z, int64_t n, float *__restrict__ zt) {
+    const int64_t nt = (n + 127) / 128;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nt * 128 * 8;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i >> 3;  // latent
+        const int g = (int)(i & 7);  // 4-component group
+        float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v < n) f = reinterpret_cast<const float4 *>(z)[v * 8 + g];
+        const float in[4] = {f.x, f.y, f.z, f.w};
+        float hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            hi[e] = tf32_rna(in[e]);
+            lo[e] = __fsub_rn(in[e], hi[e]);
+        }
+        float4 *t = reinterpret_cast<float4 *>(zt) + (v >> 7) * (2 * 8 * 128) + (v & 127);
+        t[g * 128] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        t[(8 + g) * 128] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+}
+
 int tc_launch_act(const TcLayer &L, cudaStream_t s) { return launch_tc<32, 3, TC_OUT_ACT>(L, s); }
+int pack_z_tiles(const float *z, int64_t n, float *zt, cudaStream_t s) {
+    if (n <= 0) return PILC_OK;
+    const int64_t work = ((n + 127) / 128) * 128 * 8;
+    int64_t blocks = ceil_div64(work, 256);
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    ProfScope _ps(PROF_GATHER, s, (double)n);
+    pack_z_tiles_kernel<<<(unsigned)blocks, 256, 0, s>>>(z, n, zt);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
 int argmin_tc_launch(const ArgminTc &a, cudaStream_t s) {
     if (a.n_tiles <= 0) return PILC_OK;
     if (a.K < 1 || a.K > 256) return PILC_E_ARG;

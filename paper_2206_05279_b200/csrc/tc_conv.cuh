@@ -149,6 +149,9 @@ struct ArgminTc {
     uint8_t *idx;
 };
 int argmin_tc_launch(const ArgminTc &a, cudaStream_t s);
+// z (n, 32) float32 -> the argmin's 128-latent tiles (tf32 hi / fp32 lo, as
+// the projection epilogues write them; tail rows zero)
+int pack_z_tiles(const float *z, int64_t n, float *zt, cudaStream_t s);
 
 int tc3_launch(const Tc3Layer &L, int ks, int mode, cudaStream_t s);
 

@@ -1110,6 +1110,32 @@ extern "C" int pilc_vq_argmin(const float *z, int64_t n_vec, const float *model,
     return launch_argmin(z, n_vec, model + L.cb_off, K, Dc, idx_out, as_stream(stream));
 }
 
+extern "C" int64_t pilc_vq_argmin_tc_workspace(int64_t n_vec) {
+    return n_vec < 0 ? -1 : ((n_vec + 127) / 128) * 128 * 32 * 4 * 2;
+}
+
+extern "C" int pilc_vq_argmin_tc(const float *z, int64_t n_vec, const float *model, int32_t K, int32_t Dc,
+                                 int32_t C, int32_t B, void *workspace, int64_t ws_bytes, uint8_t *idx_out,
+                                 void *stream) {
+    if (n_vec < 0 || !check_cfg(K, Dc, C, B)) return PILC_E_ARG;
+    const Layout L = make_layout(K, Dc, C, B);
+    if (!L.tf) return PILC_E_UNSUPPORTED;
+    if (ws_bytes < pilc_vq_argmin_tc_workspace(n_vec)) return PILC_E_ARG;
+    if (n_vec == 0) return PILC_OK;
+    cudaStream_t s = as_stream(stream);
+    float *zt = reinterpret_cast<float *>(workspace);
+    int rc = pack_z_tiles(z, n_vec, zt, s);
+    if (rc) return rc;
+    ArgminTc am;
+    am.zt = zt;
+    am.n_vec = n_vec;
+    am.n_tiles = ceil_div64(n_vec, 128);
+    am.cbt = model + L.tf_cb;
+    am.K = K;
+    am.idx = idx_out;
+    return argmin_tc_launch(am, s);
+}
+
 namespace {
 
 int exact_encode(const uint8_t *img, int64_t n_img, int32_t H, int32_t W, const float *model, int32_t K,

@@ -113,15 +113,23 @@ def encoder_latents(image, weights: ModelWeights, *, exact: bool = True) -> np.n
     return z[0].cpu().numpy()
 
 
-def argmin_codebook(z, weights: ModelWeights) -> np.ndarray:
-    """Codebook argmin alone on (..., Dc) latents (vqvae.py:66-76)."""
+def argmin_codebook(z, weights: ModelWeights, *, tensor_cores: bool = False) -> np.ndarray:
+    """Codebook argmin alone on (..., Dc) latents (vqvae.py:66-76): the
+    float32-screen kernel, or (tensor_cores=True, Dc = C = 32) the encoders'
+    tensor-core argmin (3xTF32 GEMM, proven radius, float64 rescore)."""
     z = np.ascontiguousarray(z, dtype=np.float32)
     dev = require_device()
     stream = torch.cuda.current_stream(dev)
     zd = torch.from_numpy(z.reshape(-1, z.shape[-1]).copy()).to(dev)
     out = torch.empty(zd.shape[0], dtype=torch.uint8, device=dev)
-    _lib.call("pilc_vq_argmin", ptr(zd), zd.shape[0], ptr(weights.device_model(dev)), *weights.cfg_tuple(),
-              ptr(out), sptr(stream))
+    if tensor_cores:
+        nb = _lib.load().pilc_vq_argmin_tc_workspace(zd.shape[0])
+        ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
+        _lib.call("pilc_vq_argmin_tc", ptr(zd), zd.shape[0], ptr(weights.device_model(dev)), *weights.cfg_tuple(),
+                  ptr(ws), ws.numel(), ptr(out), sptr(stream))
+    else:
+        _lib.call("pilc_vq_argmin", ptr(zd), zd.shape[0], ptr(weights.device_model(dev)), *weights.cfg_tuple(),
+                  ptr(out), sptr(stream))
     return out.cpu().numpy().reshape(z.shape[:-1])
 
 

@@ -946,3 +946,37 @@ def test_frame_api_edge_cases(small_model):
         assert b.size == 0 and codec.decompress_frames(b, o, 0, 20, 30, 16, 16).result().shape == (0, 20, 30, 3)
         with pytest.raises(ParameterError):
             codec.compress_frames(smooth_images(1, 8, 8, seed=1), 8, 0)
+
+
+@pytest.mark.parametrize("K", [256, 97])
+def test_argmin_near_ties(full_model, K):
+    """Both argmins -- the float32-screen kernel and the encoders'
+    tensor-core one (3xTF32 screen + proven error radius + exact float64
+    rescore) -- against the reference's float64 argmin on adversarial
+    latents: duplicated codes (exact ties: the lower code wins), codes one
+    ulp apart, latents on the midpoints between code pairs (plus noise well
+    inside the screen's error radius), and large-magnitude latents."""
+    rng = np.random.default_rng(K)
+    cb = rng.normal(0, 1, (K, 32)).astype(np.float32)
+    cb[K // 2] = cb[K // 3]                                      # exact duplicate
+    cb[K // 4] = cb[K // 5]
+    cb[K - 1] = cb[7]
+    cb[K - 2] = np.nextafter(cb[11], np.float32(np.inf))         # one ulp apart, every component
+    cb[K - 3] = cb[13]
+    cb[K - 3, 5] = np.nextafter(cb[13, 5], np.float32(-np.inf))  # one ulp apart, one component
+    cfg = pc.ModelConfig(K=K, Dc=32, channels=32, blocks=full_model.config.blocks)
+    tensors = dict(full_model.tensors) if K == full_model.config.K else \
+        {k: v for k, v in pc.random_weights(cfg, seed=3).tensors.items()}
+    tensors["codebook"] = cb
+    m = pc.ModelWeights(cfg, tensors)
+    a, b = rng.integers(0, K, 6000), rng.integers(0, K, 6000)
+    mid = 0.5 * (cb[a].astype(np.float64) + cb[b].astype(np.float64))
+    z = [mid.astype(np.float32),                                          # midpoints
+         (mid + rng.normal(0, 1e-6, mid.shape)).astype(np.float32),       # near them
+         cb[rng.integers(0, K, 2000)],                                    # on codes (duplicates included)
+         (cb[rng.integers(0, K, 2000)] + rng.normal(0, 1e-7, (2000, 32))).astype(np.float32),
+         (1e3 * rng.normal(0, 1, (2000, 32))).astype(np.float32)]         # far from every code
+    z = np.concatenate(z).reshape(-1, 8, 32)
+    ref = O.argmin_codebook(z, cb)
+    assert np.array_equal(vqvae.argmin_codebook(z, m), ref)
+    assert np.array_equal(vqvae.argmin_codebook(z, m, tensor_cores=True), ref)  # the encoders' argmin
