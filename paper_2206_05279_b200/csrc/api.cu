@@ -1,6 +1,8 @@
 // Library identity and device check.
 #include <atomic>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -122,4 +124,22 @@ extern "C" int pilc_device_arch(void) {
         return -1;
     }
     return p.major * 10 + p.minor;
+}
+
+int dyn_smem_limit(const void *func) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({func, dev});
+    if (it != cache.end()) return it->second;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    int v = optin;
+    if (cudaFuncGetAttributes(&fa, func) == cudaSuccess) v = optin - (int)fa.sharedSizeBytes;
+    else cudaGetLastError();
+    cache[{func, dev}] = v;
+    return v;
 }

@@ -56,6 +56,16 @@ extern int g_tuning[PILC_TUNE_N];
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Dynamic shared memory: every kernel's limit is raised once to the device
+// maximum (less its static shared memory) and launches pick their own,
+// smaller, sizes. Setting the attribute to each launch's own size raced
+// between host threads launching one kernel with different sizes (one
+// thread's setting undercut another's launch, cudaErrorInvalidValue).
+int dyn_smem_limit(const void *func);  // api.cu: cached per (device, kernel)
+static inline void allow_dyn_smem(const void *func) {
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit(func));
+}
+
 static inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Grid sizing: the B200 has 148 SMs; cap grids at a multiple of the SM

@@ -520,7 +520,7 @@ extern "C" int pilc_rans_encode(const uint8_t *syms, const uint8_t *shift, const
         ProfScope _ps(PROF_RANS_ENC, as_stream(stream), (double)n_img * n_sym);
         if (in_smem) {
             if (smem > 48 * 1024)
-                cudaFuncSetAttribute(rans_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                allow_dyn_smem(reinterpret_cast<const void *>(rans_encode_kernel<true>));
             rans_encode_kernel<true><<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
                 syms, shift, dsched, d_img, n_img, n_sym, lanes, enc_tab, D, X, M, scratch, lane_cap, nbits, states);
         } else {
@@ -558,13 +558,13 @@ extern "C" int pilc_rans_decode(const uint8_t *buf, const uint64_t *lane_off, co
         ProfScope _ps(PROF_RANS_DEC, as_stream(stream), (double)n_img * n_sym);
         if (in_smem) {
             if (smem > 48 * 1024)
-                cudaFuncSetAttribute(rans_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                allow_dyn_smem(reinterpret_cast<const void *>(rans_decode_kernel<true>));
             rans_decode_kernel<true><<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
                 buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, unshift, out,
                 lane_status);
         } else {
             if (smem > 48 * 1024)
-                cudaFuncSetAttribute(rans_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                allow_dyn_smem(reinterpret_cast<const void *>(rans_decode_kernel<false>));
             rans_decode_kernel<false><<<(unsigned)blocks, (unsigned)threads, smem, as_stream(stream)>>>(
                 buf, lane_off, nbits, states, dsched, d_img, n_img, n_sym, lanes, dec_tab, D, M, unshift, out,
                 lane_status);

@@ -945,7 +945,7 @@ int launch_tc3(const Tc3Layer &L, cudaStream_t s) {
     Tc3Layer Ls = L;
     Ls.n_stages = st;
     auto kern = tc3_conv_kernel<KS, MODE>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(kern));
     int per_sm = (int)((227 * 1024) / (smem + 1024));
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)sm_count() * per_sm;
@@ -2611,7 +2611,7 @@ int launch_tc(const TcLayer &L, cudaStream_t s) {
     if ((uint64_t)L.n_img * L.Hp * L.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;  // 32-bit pixel index
     if (smem == 0) return PILC_E_UNSUPPORTED;
     auto kern = tc_conv_kernel<N, KS, MODE>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(kern));
     // one persistent CTA per SM (two epilogue groups, an 8-deep copy ring);
     // the head's math-heavy epilogue (few registers) runs two CTAs per SM
     int64_t grid = (int64_t)sm_count() * ((MODE == TC_OUT_HEAD || MODE == TC_OUT_HEAD2) ? 2 : 1);
@@ -2698,7 +2698,7 @@ int argmin_tc_launch(const ArgminTc &a, cudaStream_t s) {
     if (a.K < 1 || a.K > 256) return PILC_E_ARG;
     const size_t smem = 2 * 8 * 256 * 16 + (size_t)kAmStages * 2 * 8 * 128 * 16 + 4 * 256 + 16 +
                         8 * (2 * kAmStages + 5) + 16;
-    cudaFuncSetAttribute(argmin_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(argmin_tc_kernel));
     int64_t grid = sm_count();
     if (grid > a.n_tiles) grid = a.n_tiles;
     ProfScope _ps(PROF_ARGMIN, s, 3.0 * a.n_vec * a.K * 32);
@@ -2722,7 +2722,7 @@ int enc_front_tc_launch(const EncFrontTc &a, cudaStream_t s) {
     const size_t smem = smem_of(b.n_quarters);
     if ((uint64_t)a.n_img * (a.gh + 2) * Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
-    cudaFuncSetAttribute(enc_front_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(enc_front_tc_kernel));
     int64_t grid = sm_count();
     if (grid > a.n_tiles) grid = a.n_tiles;
     if (grid < 1) return PILC_OK;
@@ -2742,7 +2742,7 @@ int tc3_block_launch(const Tc3Block &b, cudaStream_t s) {
     const size_t smem = tc3_block_smem(b.Hp, b.Wp);
     if ((b.Hp * b.Wp + 127) / 128 > kBkMaxTiles || smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     if ((uint64_t)b.n_img * b.Hp * b.Wp >= (1ull << 31)) return PILC_E_UNSUPPORTED;
-    cudaFuncSetAttribute(tc3_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(tc3_block_kernel));
     int64_t grid = sm_count();
     if (grid > b.n_img) grid = b.n_img;
     if (grid < 1) return PILC_OK;
@@ -2759,7 +2759,7 @@ int enc_trunk_launch(const EncTrunk &p, cudaStream_t s) {
     const size_t smem = enc_trunk_smem(p.Hp, p.Wp, p.n_blocks);
     if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
     if ((uint64_t)p.n_img * HW >= (1ull << 31)) return PILC_E_UNSUPPORTED;
-    cudaFuncSetAttribute(enc_trunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(enc_trunk_kernel));
     int64_t grid = sm_count();
     if (grid > p.n_img) grid = p.n_img;
     if (grid < 1) return PILC_OK;
@@ -2786,7 +2786,7 @@ int dec_trunk_launch(const DecTrunk &p0, cudaStream_t s) {
     if (G == 0) return PILC_E_UNSUPPORTED;
     p.G = G;
     p.pad_bytes = pad;
-    cudaFuncSetAttribute(dec_trunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(dec_trunk_kernel));
     const int64_t groups = (p.n_img + G - 1) / G;
     int64_t grid = sm_count();
     if (grid > groups) grid = groups;

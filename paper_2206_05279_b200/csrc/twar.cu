@@ -559,7 +559,7 @@ extern "C" int pilc_twar_forward(const uint8_t *img, uint8_t *res, int64_t n_img
         if (blocks > cap) blocks = cap;
         const int sm = 4 * kTwTileBytes;
         auto kern = unit ? twar_forward_tile_kernel<2> : (prm.integral ? twar_forward_tile_kernel<1> : twar_forward_tile_kernel<0>);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        allow_dyn_smem(reinterpret_cast<const void *>(kern));
         kern<<<(unsigned)blocks, threads, sm, as_stream(stream)>>>(img, res, n_img, H, W, G, prm);
     } else if ((W & 7) == 0 && ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(res)) & 7) == 0) {
         const int64_t n_units = n_px >> 3;
@@ -593,7 +593,7 @@ extern "C" int pilc_twar_decode(const uint8_t *coded, const uint8_t *shift, uint
     const int rp = stage ? rp_s : 3 * W;
     const size_t smem = stage ? (size_t)((int64_t)H * rp * kDecWarps) : 0;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(twar_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allow_dyn_smem(reinterpret_cast<const void *>(twar_decode_kernel));
     int64_t blocks = ceil_div64(n_img, kDecWarps);
     const int64_t cap = (int64_t)sm_count() * 16;
     if (blocks > cap) blocks = cap;

@@ -628,10 +628,10 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
     const size_t smem = conv_smem(a);
     dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
     if (ppt == 8) {
-        cudaFuncSetAttribute(conv_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<8>));
         conv_kernel<8><<<grid, threads, smem, s>>>(a);
     } else {
-        cudaFuncSetAttribute(conv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4>));
         conv_kernel<4><<<grid, threads, smem, s>>>(a);
     }
     PILC_CHECK_LAUNCH();
@@ -794,7 +794,7 @@ int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc,
     if (n_vec == 0) return PILC_OK;
     const size_t smem = sizeof(float) * ((((size_t)K * (Dc + 1) + K + 3) & ~(size_t)3) + (size_t)kArgWarps * Dc * 8);
     if (smem > 200 * 1024) return PILC_E_UNSUPPORTED;
-    cudaFuncSetAttribute(argmin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_dyn_smem(reinterpret_cast<const void *>(argmin_kernel));
     int64_t blocks = ceil_div64(ceil_div64(n_vec, kArgVec), kArgWarps);
     const int64_t cap = (int64_t)sm_count() * 8;
     if (blocks > cap) blocks = cap;

@@ -42,17 +42,19 @@ def _pool(k: int) -> ThreadPoolExecutor:
 
 
 def _run(k: int, fn):
-    """fn(i) on k threads; the first exception (in share order) is raised."""
+    """fn(i) on k threads; the first exception (in share order) is raised --
+    a share's own error before the broken barriers it left the others."""
     futs = [_pool(k).submit(fn, i) for i in range(k)]
-    res, err = [], None
+    res, errs = [], []
     for f in futs:
         try:
             res.append(f.result())
         except BaseException as e:  # noqa: BLE001
             res.append(None)
-            err = err or e
-    if err is not None:
-        raise err
+            errs.append(e)
+    if errs:
+        own = [e for e in errs if not isinstance(e, threading.BrokenBarrierError)]
+        raise (own or errs)[0]
     return res
 
 

@@ -980,3 +980,37 @@ def test_argmin_near_ties(full_model, K):
     ref = O.argmin_codebook(z, cb)
     assert np.array_equal(vqvae.argmin_codebook(z, m), ref)
     assert np.array_equal(vqvae.argmin_codebook(z, m, tensor_cores=True), ref)  # the encoders' argmin
+
+
+def test_concurrent_host_threads_one_device(full_model, small_model):
+    """Host threads driving one GPU at once (each on its own stream, with
+    different image shapes, models and numerics, so the same kernels launch
+    concurrently with different shared-memory sizes): every result equals
+    the single-threaded one. (Per-launch shared-memory attributes used to
+    race here: one thread's setting undercut another's launch.)"""
+    from concurrent.futures import ThreadPoolExecutor
+
+    jobs = []
+    for j in range(8):
+        shape = [(32, 32), (17, 29), (64, 64), (40, 24)][j % 4]
+        m = full_model if j % 3 else small_model
+        cfg = EXACT if j % 2 else FAST
+        jobs.append((smooth_images(6 + j, *shape, seed=70 + j), m, cfg))
+    want = [pc.compress_batch(im, m, cfg) for im, m, cfg in jobs]
+    dev = torch.device("cuda", 0)
+
+    def run(job):
+        im, m, cfg = job
+        with torch.cuda.stream(torch.cuda.Stream(dev)):
+            outs = []
+            for _ in range(3):
+                buf, off = pc.compress_batch(im, m, cfg)
+                outs.append((buf.tobytes(), off.copy(), pc.decompress_batch(buf, off, m)))
+            return outs
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        got = list(ex.map(run, jobs))
+    for (im, _, _), (wb, wo), outs in zip(jobs, want, got):
+        for buf, off, back in outs:
+            assert buf == wb.tobytes() and np.array_equal(off, wo)
+            assert np.array_equal(back, im)
