@@ -828,6 +828,10 @@ def _smem_operand_bytes(name, wl, K=256, B=4):
             return None
         tiles = ((G * Hp * Wp + 127) // 128) * ((n + G - 1) // G)
         return tiles * 2 * B * 18 * (4096 + 1024)
+    if name == "dec_uphead_kernel":  # up conv (N=128, 18 MMAs per tile) + pair head (N=16, 24 per tile)
+        tu = (Hp * Wp + 127) // 128
+        th = ((2 * gh + 2) * (gw + 1) + 127) // 128
+        return n * (tu * 18 * (4096 + 4096) + th * 24 * (4096 + 512))
     return None
 
 
@@ -861,6 +865,9 @@ def _roofline(prof, clk, steps, wl=None):
                             "FLOPs = (2B x 9 + 1) x 2*N*H*W*32*32 (MMA FLOPs issued = 3x that)",
         "dec_trunk_kernel": "decoder trunk (gather + all 2B bf16 block convs, activations in shared memory, G images per "
                             "CTA iteration); algorithmic FLOPs = 2B x 2*N*gh*gw*32*32*9",
+        "dec_uphead_kernel": "decoder output stage (bf16 up conv 32 -> 128 + pixel shuffle + the logistic head over "
+                             "pixel pairs, one image per CTA iteration, hi-res activations in shared memory); "
+                             "algorithmic FLOPs = 2*N*gh*gw*32*9*(128 + 4*6)",
         "argmin_kernel": "codebook distance GEMM (3xTF32 tcgen05) + proven-margin screen + exact f64 rescore (3*n*K*Dc FLOPs)",
     }
     mhz = clk.summary().get("sm_mhz") or 1965.0

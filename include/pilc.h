@@ -98,8 +98,11 @@ const char *pilc_version(void);
  * checks). key 0: encoder residual blocks as one fused kernel per block
  * (default 1) instead of two conv launches; key 1: decoder trunk (gather +
  * block convs) as one kernel with activations in shared memory (default 1)
- * instead of per-layer launches. Both bit-identical to the unfused path, so
- * no switch changes any output byte.
+ * instead of per-layer launches; key 2: encoder trunk (every residual block
+ * + the projection in one kernel, default 1); key 3: decoder output stage (up
+ * conv + pixel shuffle + head in one kernel with the hi-res activations in
+ * shared memory, default 1) instead of two launches through HBM. All
+ * bit-identical to the unfused path, so no switch changes any output byte.
  * Returns the previous value, or -PILC_E_ARG for an unknown key. */
 int pilc_set_tuning(int32_t key, int32_t value);
 /* Device sanity: returns 100 for sm_100 etc., or -1 if no usable device. */

@@ -120,6 +120,7 @@ def call(name: str, *args) -> int:
 TUNE_BLOCK_FUSION = 0
 TUNE_DEC_TRUNK = 1
 TUNE_ENC_TRUNK = 2
+TUNE_DEC_UPHEAD = 3
 
 
 def set_tuning(key: int, value: int) -> int:

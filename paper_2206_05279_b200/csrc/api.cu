@@ -13,7 +13,8 @@ const char *kCatNames[PROF_NCAT] = {"conv_kernel",        "argmin_kernel",  "ran
                                     "static_scale_kernel", "blob_sizes+scan", "pack_kernel",
                                     "parse_kernel",       "lanes_kernel",   "crc_kernel",
                                     "sched_crc_kernel",   "tc_conv_kernel", "gather_kernel",
-                                    "tc3_conv_kernel", "enc_front_kernel", "tc3_block_kernel", "dec_trunk_kernel", "enc_trunk_kernel"};
+                                    "tc3_conv_kernel", "enc_front_kernel", "tc3_block_kernel", "dec_trunk_kernel", "enc_trunk_kernel",
+                                    "dec_uphead_kernel"};
 struct Rec {
     int cat;
     cudaEvent_t e0, e1;
@@ -101,7 +102,7 @@ extern "C" int pilc_prof_read(int32_t cat, int64_t *launches, double *total_ms, 
     return PILC_OK;
 }
 
-int g_tuning[PILC_TUNE_N] = {1, 1, 1};
+int g_tuning[PILC_TUNE_N] = {1, 1, 1, 1};
 
 extern "C" int pilc_set_tuning(int32_t key, int32_t value) {
     if (key < 0 || key >= PILC_TUNE_N) return -PILC_E_ARG;

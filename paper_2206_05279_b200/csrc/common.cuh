@@ -39,6 +39,7 @@ enum ProfCat {
     PROF_TC3_BLOCK,
     PROF_DEC_TRUNK,
     PROF_ENC_TRUNK,
+    PROF_DEC_UPHEAD,
     PROF_NCAT
 };
 void *prof_begin(int cat, cudaStream_t s, double units);
@@ -51,7 +52,7 @@ struct ProfScope {
 };
 
 // Library tuning switches (pilc_set_tuning); defaults are the production path.
-enum { PILC_TUNE_BLOCK_FUSION = 0, PILC_TUNE_DEC_TRUNK = 1, PILC_TUNE_ENC_TRUNK = 2, PILC_TUNE_N };
+enum { PILC_TUNE_BLOCK_FUSION = 0, PILC_TUNE_DEC_TRUNK = 1, PILC_TUNE_ENC_TRUNK = 2, PILC_TUNE_DEC_UPHEAD = 3, PILC_TUNE_N };
 extern int g_tuning[PILC_TUNE_N];
 
 static inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -1936,6 +1936,323 @@ size_t dec_trunk_smem(int Hp, int Wp, int G, int K, int n_conv, int *pad) {
            (size_t)n_conv * 32 * 4;
 }
 
+// ---- decoder output stage in shared memory (vqvae.py:101-112) ---------------
+// The up conv (3x3, 32 -> 128), pixel shuffle + ReLU and the logistic head of
+// one image per CTA iteration; the 2x hi-res activations (the largest tensor
+// of the decoder) never leave shared memory. The image's padded latent grid
+// arrives by one bulk copy per channel group; the up conv runs as
+// tc_conv_kernel<128, 3, SHUFFLE> (18 MMAs of N = 128 per 128-row tile), its
+// epilogue writes the shuffled bf16 activations in the pair head's layout
+// (row = two horizontally adjacent pixels, 8 channel groups; edges
+// replicated) into a shared buffer, and the head runs as tc_conv_kernel<16,
+// 3, HEAD2> (24 MMAs of N = 16 per tile) from there. Same MMAs, same K order,
+// same epilogue roundings: shift / d / mu / s are bit-identical to the two
+// launches.
+//
+// Overlap: every tile of an image has its own TMEM accumulator (up tiles at
+// columns 128 t, head tiles at 384 + 16 k), so the tensor core runs image i's
+// up tiles, then its head tiles (each waiting only for the up tile that
+// writes its last input row, `hrdy`), then image i + 1's up tiles while
+// image i's head epilogue drains. The hi-res buffer is single: image i + 1's
+// up epilogue waits for image i's head MMAs (`hfree`), which the tensor core
+// has finished before image i + 1's up MMAs anyway. The latent buffer is
+// reloaded as soon as an image's up MMAs complete.
+//
+// Warps: 0 bulk-copy producer, 1 TMEM allocator + MMA issuer, 2..5 up
+// epilogue, 6..13 head epilogue (two groups of four, alternate tiles).
+constexpr int kUhMaxUp = 3, kUhMaxHead = 8;  // tiles per image: TMEM 128 x 3 + 16 x 8 = 512 columns
+constexpr int kThreadsUH = 448;
+constexpr uint32_t kUhWUp = 36 * 128 * 16, kUhWHead = 48 * 16 * 16;
+constexpr int kUhBars = 32;  // >= 4 + 3 kUhMaxUp + 2 kUhMaxHead, even
+static_assert(kUhBars >= 4 + 3 * kUhMaxUp + 2 * kUhMaxHead && kUhBars % 2 == 0, "barrier block");
+
+struct UhGeom {
+    int Wp, HW, Tu, M0, RSu;  // latent grid, up tiles, slab rows
+    int Wq, HWq, Th, M0q, RSh;  // hi-res pair grid, head tiles, slab rows
+};
+__host__ __device__ inline UhGeom uh_geom(int gh, int gw) {
+    UhGeom g;
+    g.Wp = gw + 2;
+    g.HW = (gh + 2) * g.Wp;
+    g.Tu = (g.HW + 127) / 128;
+    g.M0 = g.Wp + 1;
+    g.RSu = g.M0 + 128 * g.Tu + g.M0;
+    g.Wq = gw + 1;
+    g.HWq = (2 * gh + 2) * g.Wq;
+    g.Th = (g.HWq + 127) / 128;
+    g.M0q = g.Wq + 1;
+    g.RSh = g.M0q + 128 * g.Th + g.M0q;
+    return g;
+}
+size_t dec_uphead_smem(const UhGeom &g) {
+    return kUhWUp + kUhWHead + 4 * (size_t)g.RSu * 16 + 8 * (size_t)g.RSh * 16 +
+           8 * kUhBars + 16 + (128 + 16 + 256) * 4;
+}
+
+__global__ void __launch_bounds__(kThreadsUH, 1) dec_uphead_kernel(DecUpHead P) {
+    const UhGeom G = uh_geom(P.gh, P.gw);
+    const int gh = P.gh, gw = P.gw, Wp = G.Wp, Wq = G.Wq, Tu = G.Tu, Th = G.Th;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_wu = smem;                                   // [36][128][8] bf16
+    uint8_t *s_wh = s_wu + kUhWUp;                          // [48][16][8] bf16
+    uint8_t *s_x = s_wh + kUhWHead;                         // 4 slabs x RSu rows: latent
+    uint8_t *s_q = s_x + 4 * (size_t)G.RSu * 16;            // 8 slabs x RSh rows: hi-res pairs
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_q + 8 * (size_t)G.RSh * 16);
+    uint64_t *wbar = bars, *lfull = bars + 1, *lempty = bars + 2, *hfree = bars + 3;
+    uint64_t *ufull = bars + 4, *uempty = ufull + kUhMaxUp, *hrdy = uempty + kUhMaxUp;
+    uint64_t *qfull = hrdy + kUhMaxUp, *qempty = qfull + kUhMaxHead;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + kUhBars);
+    float *s_bu = reinterpret_cast<float *>(tmem_slot + 4);  // 128 up biases (16-byte aligned: float4 reads)
+    float *s_bh = s_bu + 128;                                // 6 head biases
+    float *s_thr = s_bh + 16;                                // rd32 thresholds
+
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    for (int c = threadIdx.x; c < 128; c += blockDim.x) s_bu[c] = P.b_up[c];
+    for (int c = threadIdx.x; c < 16; c += blockDim.x) s_bh[c] = c < 6 ? P.b_head[c] : 0.f;
+    for (int k = threadIdx.x; k < P.n_thresh; k += blockDim.x) s_thr[k] = __double2float_rd(P.thresh[k]);
+    // finite operands everywhere: rows no image writes (tile tails, margins)
+    // are read by the pair head's zero-weight K segments (0 x NaN = NaN)
+    {
+        uint4 *z = reinterpret_cast<uint4 *>(s_x);
+        const int n16 = 4 * G.RSu + 8 * G.RSh;
+        for (int e = threadIdx.x; e < n16; e += blockDim.x) z[e] = make_uint4(0u, 0u, 0u, 0u);
+        fence_async_smem();
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(wbar, 1);
+        mbar_init(lfull, 1);
+        mbar_init(lempty, 1);
+        mbar_init(hfree, 1);
+        for (int t = 0; t < kUhMaxUp; ++t) {
+            mbar_init(&ufull[t], 1);
+            mbar_init(&uempty[t], 4);
+            mbar_init(&hrdy[t], 4);
+        }
+        for (int k = 0; k < kUhMaxHead; ++k) {
+            mbar_init(&qfull[k], 1);
+            mbar_init(&qempty[k], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(wbar, kUhWUp + kUhWHead);
+            bulk_g2s(s_wu, P.w_up, kUhWUp, wbar);
+            bulk_g2s(s_wh, P.w_head, kUhWHead, wbar);
+            const uint32_t bytes = (uint32_t)G.HW * 16u;
+            int i = 0;
+            for (int64_t n = blockIdx.x; n < P.n_img; n += gridDim.x, ++i) {
+                if (i > 0) mbar_wait(lempty, (i - 1) & 1);
+                mbar_expect_tx(lfull, 4 * bytes);
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+                    bulk_g2s(s_x + ((size_t)g * G.RSu + G.M0) * 16,
+                             P.in + ((int64_t)g * P.gstride + P.margin + n * G.HW) * 8, bytes, lfull);
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idu = idesc_bf16(128, 128), idh = idesc_bf16(128, 16);
+        mbar_wait(wbar, 0);
+        tc_fence_after();
+        const uint64_t dX = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_x), 0), (uint32_t)G.RSu * 16u, 128u);
+        const uint64_t dQ = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_q), 0), (uint32_t)G.RSh * 16u, 128u);
+        const uint64_t dWu = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_wu), 0), 128u * 16u, 128u);
+        const uint64_t dWh = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_wh), 0), 16u * 16u, 128u);
+        const uint32_t rsu = (uint32_t)G.RSu, rsh = (uint32_t)G.RSh;
+        int i = 0;
+        for (int64_t n = blockIdx.x; n < P.n_img; n += gridDim.x, ++i) {
+            mbar_wait(lfull, i & 1);
+            tc_fence_after();
+            for (int t = 0; t < Tu; ++t) {
+                if (i > 0) mbar_wait(&uempty[t], (i - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(128 * t);
+                // tile rows q0 = 128 t; tap (di, dj) reads from q0 - Wp - 1 + di Wp + dj (slab row + M0)
+                const uint32_t al = (uint32_t)dX + (uint32_t)(128 * t), ah = (uint32_t)(dX >> 32);
+                const uint32_t bl = (uint32_t)dWu, bh = (uint32_t)(dWu >> 32);
+#pragma unroll
+                for (int tap = 0; tap < 9; ++tap) {
+                    const uint32_t off = (uint32_t)((tap / 3) * Wp + tap % 3);
+#pragma unroll
+                    for (int ks = 0; ks < 2; ++ks)
+                        mma_bf16_elect_w(d, al + 2u * ks * rsu + off, ah, bl + (uint32_t)((tap * 4 + 2 * ks) * 128), bh,
+                                         idu, (tap | ks) ? 1u : 0u);
+                }
+                mma_commit_elect(&ufull[t]);
+            }
+            mma_commit_elect(lempty);
+            int waited = -1;
+            for (int k = 0; k < Th; ++k) {
+                // the up tile writing this head tile's last input row (pair row
+                // 128 k + 128 + Wq): hi-res row Y comes from latent row (Y + 1) / 2
+                int Y = (128 * k + 128 + Wq) / Wq;
+                Y = Y > 2 * gh + 1 ? 2 * gh + 1 : Y;
+                int y = (Y + 1) >> 1;
+                y = y < 1 ? 1 : (y > gh ? gh : y);
+                int tn = (y * Wp + gw) >> 7;
+                tn = tn > Tu - 1 ? Tu - 1 : tn;
+                if (tn > waited) {
+                    mbar_wait(&hrdy[tn], i & 1);
+                    waited = tn;
+                }
+                if (i > 0) mbar_wait(&qempty[k], (i - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(384 + 16 * k);
+                const uint32_t al = (uint32_t)dQ + (uint32_t)(128 * k), ah = (uint32_t)(dQ >> 32);
+                const uint32_t bl = (uint32_t)dWh, bh = (uint32_t)(dWh >> 32);
+                // per row tap di, 8 K steps: the left pair's odd pixel (groups
+                // 4-7), this pair (0-7), the right pair's even pixel (0-3)
+#pragma unroll
+                for (int di = 0; di < 3; ++di) {
+#pragma unroll
+                    for (int sg = 0; sg < 8; ++sg) {
+                        const uint32_t slab = (sg < 2) ? 4u + 2u * sg : (sg < 6 ? 2u * (sg - 2) : 2u * (sg - 6));
+                        const uint32_t dj = sg < 2 ? 0u : (sg < 6 ? 1u : 2u);
+                        const uint32_t off = (uint32_t)di * (uint32_t)Wq + dj;
+                        mma_bf16_elect_w(d, al + slab * rsh + off, ah, bl + (uint32_t)((2 * (di * 8 + sg)) * 16), bh,
+                                         idh, (di | sg) ? 1u : 0u);
+                    }
+                }
+                mma_commit_elect(&qfull[k]);
+            }
+            mma_commit_elect(hfree);
+        }
+    } else if (warp < 6) {
+        // up epilogue: bias, ReLU, bf16, pixel shuffle into the pair buffer
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int H2 = 2 * gh, W2 = 2 * gw, Wp2 = 2 * Wq;
+        int i = 0;
+        for (int64_t n = blockIdx.x; n < P.n_img; n += gridDim.x, ++i) {
+            for (int t = 0; t < Tu; ++t) {
+                const int q = 128 * t + row;
+                const int y = q / Wp, x = q - y * Wp;
+                const bool valid = q < G.HW && y >= 1 && y <= gh && x >= 1 && x <= gw;
+                mbar_wait(&ufull[t], i & 1);
+                if (t == 0 && i > 0) mbar_wait(hfree, (i - 1) & 1);  // image i - 1's head MMAs are done reading
+                tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(128 * t);
+#pragma unroll 1
+                for (int z = 0; z < 4; ++z) {
+                    float v[32];
+                    tmem_ld32(taddr + (uint32_t)(32 * z), v);
+                    if (z == 3) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&uempty[t]);
+                    }
+                    if (!valid) continue;
+                    float bz[32];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float4 b4 = reinterpret_cast<const float4 *>(s_bu + 32 * z)[e];
+                        bz[4 * e] = b4.x;
+                        bz[4 * e + 1] = b4.y;
+                        bz[4 * e + 2] = b4.z;
+                        bz[4 * e + 3] = b4.w;
+                    }
+#pragma unroll
+                    for (int sub = 0; sub < 4; ++sub) {
+                        const int dy = sub >> 1, dx = sub & 1;
+                        float o[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) o[e] = fmaxf(__fadd_rn(v[4 * e + sub], bz[4 * e + sub]), 0.f);
+                        const int Y = 2 * (y - 1) + dy + 1, X = 2 * (x - 1) + dx + 1;
+                        const uint4 w4 = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]),
+                                                    pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
+                        auto put = [&](int qq) {
+                            reinterpret_cast<uint4 *>(s_q + ((size_t)(z + 4 * (qq & 1)) * G.RSh + G.M0q) * 16)[qq >> 1] =
+                                w4;
+                        };
+                        const int q2 = Y * Wp2 + X;
+                        put(q2);
+                        const int ey = (Y == 1 ? -Wp2 : (Y == H2 ? Wp2 : 0));
+                        const int ex = (X == 1 ? -1 : (X == W2 ? 1 : 0));
+                        if (ex) put(q2 + ex);
+                        if (ey) put(q2 + ey);
+                        if (ex && ey) put(q2 + ey + ex);
+                    }
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&hrdy[t]);
+            }
+        }
+    } else {
+        // head epilogue (vqvae.py:105-112, logistic.py:36-40, 109-114): as
+        // tc_conv_kernel's TC_OUT_HEAD2, two groups of four warps taking
+        // alternate tiles (the epilogue is math-heavy: one group cannot keep up
+        // with the tensor core)
+        const int hg = (warp - 6) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int H2 = 2 * gh, W2 = 2 * gw;
+        const int nt = P.n_thresh;
+        float thr[8];  // the usual grids (D <= 9) compare against registers
+#pragma unroll
+        for (int e = 0; e < 8; ++e) thr[e] = e < nt ? s_thr[e] : __int_as_float(0x7f800000);
+        int i = 0;
+        for (int64_t n = blockIdx.x; n < P.n_img; n += gridDim.x, ++i) {
+            for (int k = hg; k < Th; k += 2) {
+                const int p = 128 * k + row;
+                const int Y = p / Wq, X = 2 * (p - Y * Wq);
+                mbar_wait(&qfull[k], i & 1);
+                tc_fence_after();
+                float v[16];
+                tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(384 + 16 * k), v);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&qempty[k]);
+                auto head_px = [&](const float *vv, int xx) {
+                    if (!(Y >= 1 && Y <= H2 && xx >= 1 && xx <= W2)) return;
+                    if (!((Y - 1) < P.crop_h && (xx - 1) < P.crop_w)) return;
+                    const int64_t px = ((int64_t)n * P.crop_h + (Y - 1)) * (int64_t)P.crop_w + (xx - 1);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        float av = __fadd_rn(vv[c], s_bh[c]);
+                        av = fminf(fmaxf(av, -15.f), 15.f);
+                        const float mu = __fmul_rn(255.f, __fdividef(1.f, 1.f + __expf(-av)));
+                        float bv = __fadd_rn(vv[3 + c], s_bh[3 + c]);
+                        bv = fminf(fmaxf(bv, P.log_s_min), P.log_s_max);
+                        float sv = fminf(fmaxf(__expf(bv), 0.5f), 64.f);
+                        const float fl = floorf(mu);
+                        const int shift = (int)fl + (__fsub_rn(mu, fl) >= 0.5f ? 1 : 0);
+                        int d = 0;
+                        if (nt <= 8) {
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) d += sv > thr[e];
+                        } else {
+                            for (int e = 0; e < nt; ++e) d += sv > s_thr[e];
+                        }
+                        P.shift[px * 3 + c] = (uint8_t)shift;
+                        P.dsel[px * 3 + c] = (uint8_t)d;
+                        if (P.mu) P.mu[px * 3 + c] = mu;
+                        if (P.s) P.s[px * 3 + c] = sv;
+                    }
+                };
+                head_px(v, X);
+                head_px(v + 6, X + 1);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
+}
+
 // ---- encoder front on tcgen05 (vqvae.py:55-57) -----------------------------
 // stem (3x3, 3 -> 32, ReLU) and down (3x3 stride 2, 32 -> 32, ReLU), both as
 // 3-product fp16 MMAs, in one kernel: the stem never leaves the SM.
@@ -2794,6 +3111,23 @@ int dec_trunk_launch(const DecTrunk &p0, cudaStream_t s) {
     const double flops = 2.0 * p.n_img * (p.Hp - 2) * (p.Wp - 2) * 32.0 * 32 * 9 * p.n_conv;
     ProfScope _ps(PROF_DEC_TRUNK, s, flops);
     dec_trunk_kernel<<<(unsigned)grid, kThreadsDT, smem, s>>>(p);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+int dec_uphead_launch(const DecUpHead &p, cudaStream_t s) {
+    if (p.gh < 1 || p.gw < 1 || p.n_thresh < 0 || p.n_thresh > 255) return PILC_E_UNSUPPORTED;
+    const UhGeom g = uh_geom(p.gh, p.gw);
+    if (g.Tu > kUhMaxUp || g.Th > kUhMaxHead) return PILC_E_UNSUPPORTED;
+    const size_t smem = dec_uphead_smem(g);
+    if (smem > 227 * 1024) return PILC_E_UNSUPPORTED;
+    if ((uint64_t)p.n_img * g.HW >= (1ull << 31)) return PILC_E_UNSUPPORTED;
+    allow_dyn_smem(reinterpret_cast<const void *>(dec_uphead_kernel));
+    int64_t grid = sm_count();
+    if (grid > p.n_img) grid = p.n_img;
+    if (grid < 1) return PILC_OK;
+    const double flops = 2.0 * p.n_img * p.gh * p.gw * 32.0 * 9 * (128 + 4 * 6);
+    ProfScope _ps(PROF_DEC_UPHEAD, s, flops);
+    dec_uphead_kernel<<<(unsigned)grid, kThreadsUH, smem, s>>>(p);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

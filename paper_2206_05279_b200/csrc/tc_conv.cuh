@@ -45,6 +45,28 @@ struct DecTrunk {
 };
 int dec_trunk_launch(const DecTrunk &p, cudaStream_t s);
 
+// Decoder output stage: up conv + pixel shuffle + logistic head of one image
+// per CTA iteration, the hi-res activations kept in shared memory (same
+// arithmetic as tc_launch_shuffle + tc_launch_head2). PILC_E_UNSUPPORTED for
+// grids whose tiles do not fit; the caller then runs those two kernels.
+struct DecUpHead {
+    const uint16_t *in;        // trunk output: padded group-major bf16 slabs (32 channels)
+    int64_t gstride, margin;
+    int gh, gw;                // latent grid (interior)
+    int64_t n_img;
+    const uint16_t *w_up;      // [36][128][8] bf16
+    const float *b_up;         // 128
+    const uint16_t *w_head;    // pair head [48][16][8] bf16
+    const float *b_head;       // 6
+    uint8_t *shift, *dsel;
+    float *mu, *s;             // nullable
+    int crop_h, crop_w;
+    const double *thresh;
+    int n_thresh;
+    float log_s_min, log_s_max;
+};
+int dec_uphead_launch(const DecUpHead &p, cudaStream_t s);
+
 // Encoder layers (3-product fp16 split, tc_conv.cu). Operands: the scaled
 // fp16 hi / lo slab sets of a tensor (8-channel groups, 16 B per pixel: hi
 // groups 0..3 then lo groups 4..7), padded group-major like the bf16 path;

@@ -1541,6 +1541,33 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
         X = Y;
         Y = tmp;
     }
+    if (!rc && g_tuning[PILC_TUNE_DEC_UPHEAD]) {  // up conv + shuffle + head, hi-res in shared memory
+        DecUpHead p;
+        memset(&p, 0, sizeof(p));
+        p.in = X;
+        p.gstride = tw.gs;
+        p.margin = tw.margin;
+        p.gh = gh;
+        p.gw = gw;
+        p.n_img = n_img;
+        p.w_up = hb + L.tc_up;
+        p.b_up = model + L.dec[1 + 2 * B].b_off;
+        p.w_head = hb + L.tc_head2;
+        p.b_head = model + L.dec[2 + 2 * B].b_off;
+        p.shift = shift_out;
+        p.dsel = d_out;
+        p.mu = mu_out;
+        p.s = s_out;
+        p.crop_h = H;
+        p.crop_w = W;
+        p.thresh = thr;
+        p.n_thresh = D - 1;
+        p.log_s_min = (float)log(0.5);
+        p.log_s_max = (float)log(64.0);
+        rc = dec_uphead_launch(p, s);
+        if (rc != PILC_E_UNSUPPORTED) return rc;
+        rc = PILC_OK;
+    }
     if (!rc) {
         TcLayer up = b;
         up.in = X;

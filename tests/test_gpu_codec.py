@@ -631,6 +631,39 @@ def test_decoder_trunk_kernel_bit_identical(full_model, shape, n):
         assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
+@pytest.mark.parametrize("shape,n", [((32, 32), 301), ((30, 18), 7), ((1, 1), 3), ((17, 33), 5), ((34, 34), 150),
+                                     ((33, 2), 9), ((2, 200), 4), ((64, 64), 2)])
+def test_decoder_output_stage_bit_identical(full_model, shape, n):
+    """dec_uphead_kernel (up conv + pixel shuffle + head of one image per CTA
+    iteration, the hi-res activations in shared memory) gives exactly the mu /
+    s / shift / scale index of the two launches through HBM (up conv, then
+    the pair head); 64 x 64 does not fit its tiles and takes the two launches
+    either way. n = 301 / 150 leave the CTAs uneven image counts."""
+    from paper_2206_05279_b200 import _lib
+    from paper_2206_05279_b200.device import require_device
+
+    dev = require_device()
+    stream = torch.cuda.current_stream(dev)
+    H, W = shape
+    gh, gw = vqvae.latent_shape(H, W)
+    rng = np.random.default_rng(11)
+    idx = torch.from_numpy(rng.integers(0, 256, (n, gh, gw), dtype=np.uint8)).to(dev)
+    grid = default_grid()
+    out = []
+    for on in (1, 0):
+        prev = _lib.set_tuning(_lib.TUNE_DEC_UPHEAD, on)
+        try:
+            r = vqvae.decode_head_device(idx, full_model, H, W, grid, dev, stream, want_params=True, exact=False)
+            out.append([t.cpu().numpy() for t in r])
+        finally:
+            _lib.set_tuning(_lib.TUNE_DEC_UPHEAD, prev)
+    mu = out[0][2] if len(out[0]) > 2 else None
+    if mu is not None:
+        assert np.isfinite(mu).all() and len(np.unique(mu)) > min(mu.size // 8, 50)  # a live decoder
+    for a, b in zip(*out):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
 def test_report_rows_in_reference_format():
     """report.run_bench (report.py:47-104 twin): rows carry the reference's
     keys; the GPU coder rows come from a checked round trip."""
