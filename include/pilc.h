@@ -97,8 +97,9 @@ const char *pilc_version(void);
 /* Tuning switches of the fast path (no reference counterpart; for A/B
  * checks). key 0: encoder residual blocks as one fused kernel per block
  * (default 1) instead of two conv launches; key 1: decoder trunk (gather +
- * block convs) as one kernel with activations in shared memory (default 1)
- * instead of per-layer launches; key 2: encoder trunk (every residual block
+ * block convs) as one kernel with activations in shared memory, 2 (default)
+ * with the activations in pixel pairs (N = 64 MMAs), 1 one pixel per MMA
+ * row, 0 per-layer launches; key 2: encoder trunk (every residual block
  * + the projection in one kernel, default 1); key 3: decoder output stage (up
  * conv + pixel shuffle + head in one kernel with the hi-res activations in
  * shared memory, default 1) instead of two launches through HBM. All

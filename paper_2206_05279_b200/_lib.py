@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpilc_sm100a.so")
+# PILC_LIB_PATH: an alternative build of the same library (A/B timing of
+# kernel variants); the in-tree build by default
+LIB_PATH = os.environ.get("PILC_LIB_PATH") or os.path.join(HERE, "libpilc_sm100a.so")
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32

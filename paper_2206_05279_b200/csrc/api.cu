@@ -102,7 +102,7 @@ extern "C" int pilc_prof_read(int32_t cat, int64_t *launches, double *total_ms, 
     return PILC_OK;
 }
 
-int g_tuning[PILC_TUNE_N] = {1, 1, 1, 1};
+int g_tuning[PILC_TUNE_N] = {1, 2, 1, 1};
 
 extern "C" int pilc_set_tuning(int32_t key, int32_t value) {
     if (key < 0 || key >= PILC_TUNE_N) return -PILC_E_ARG;

@@ -1936,6 +1936,304 @@ size_t dec_trunk_smem(int Hp, int Wp, int G, int K, int n_conv, int *pad) {
            (size_t)n_conv * 32 * 4;
 }
 
+// ---- decoder trunk over pixel pairs (vqvae.py:80-100) ------------------------
+// dec_trunk_kernel with the activations in the pair layout of the head (row
+// = two horizontally adjacent pixels of the padded grid, 8 channel groups:
+// even pixel 0..3, odd pixel 4..7; padded width rounded up to even), so one
+// MMA row produces both pixels' 32 outputs (N = 64): per row tap 8 K steps
+// (the left pair's odd pixel, this pair, the right pair's even pixel, 16
+// channels each), 24 MMAs per 256 pixels instead of 36, and each 4 KB A tile
+// feeds 64 outputs instead of 32 -- the N=32 convs are bound by the MMAs'
+// shared-memory operand reads. Per output pixel the non-zero K chunks come
+// in the per-pixel kernel's order (taps row-major, 16 channels per chunk)
+// with zero-weight chunks in between, which add exact zeros: the output is
+// bit-identical to dec_trunk_kernel / the per-layer path.
+//
+// The pair weights (48 K groups x 64 rows, 48 KB per conv) stream through a
+// ring of four 16 KB slots, one per row tap: a layer's three taps stay
+// resident for all its tiles, the fourth slot prefetches the next layer's
+// first tap, and each tap's slot is released as soon as the layer's last
+// tile has issued that tap's MMAs.
+constexpr int kD2Slots = 4;
+constexpr uint32_t kD2Chunk = 16 * 64 * 16;  // one row tap: 16 K groups x 64 rows x 16 B
+constexpr int kD2MaxTiles = 16;
+
+
+__global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
+    constexpr int NG = 4;
+    const int Wp = P.Wp, Wpp = (Wp + 1) & ~1, Wq = Wpp >> 1, gh = P.Hp - 2, gw = Wp - 2;
+    const int HWq = P.Hp * Wq;  // pair rows per image
+    const int G = P.G;
+    const int rows = G * HWq;
+    const int T = (rows + 127) >> 7;
+    const int M0 = Wq + 1;
+    const int RS = M0 + rows + M0;
+    const uint32_t slab = (uint32_t)RS * 16u;
+    const int L = P.n_conv;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *s_w = smem;                                         // [4][16][64][8] bf16
+    uint8_t *s_tab = s_w + kD2Slots * kD2Chunk;                  // K x 64 B
+    uint8_t *s_x = s_tab + (size_t)P.K * 64;                     // 8 slabs
+    uint8_t *s_h = s_x + 8 * (size_t)slab;                       // 8 slabs
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s_h + 8 * (size_t)slab + P.pad_bytes);
+    uint64_t *wfull = bars, *wempty = bars + kD2Slots, *tfull = bars + 2 * kD2Slots, *tempty = tfull + kDtGroups;
+    uint64_t *xready = tempty + kDtGroups, *tbar = xready + 1, *hrdy = xready + 2;  // hrdy[kD2MaxTiles]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(hrdy + kD2MaxTiles);
+    float *s_b = reinterpret_cast<float *>(tmem_slot + 4);      // [L][32]
+
+    const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < L * 32; i += blockDim.x) s_b[i] = P.bias[i / 32][i % 32];
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < kD2Slots; ++a) {
+            mbar_init(&wfull[a], 1);
+            mbar_init(&wempty[a], 1);
+        }
+        for (int a = 0; a < kDtGroups; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);
+        }
+        mbar_init(xready, 4 * kDtGroups);
+        mbar_init(tbar, 1);
+        for (int j = 0; j < kD2MaxTiles; ++j) mbar_init(&hrdy[j], 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // finite operands in the rows no image writes (margins, tile tails): the
+    // zero-weight K chunks read them (0 x NaN = NaN)
+    {
+        uint4 *z = reinterpret_cast<uint4 *>(s_x);
+        const int n16 = 2 * 8 * RS + P.pad_bytes / 16;
+        for (int e = threadIdx.x; e < n16; e += blockDim.x) z[e] = make_uint4(0u, 0u, 0u, 0u);
+        fence_async_smem();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(256u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = __shfl_sync(0xFFFFFFFFu, *tmem_slot, 0);
+    const int64_t n_groups = (P.n_img + G - 1) / G;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(tbar, (uint32_t)P.K * 64u);
+            bulk_g2s(s_tab, P.table, (uint32_t)P.K * 64u, tbar);
+            int cs = 0;  // chunk sequence: (group, layer, row tap)
+            for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+                for (int l = 0; l < L; ++l) {
+                    for (int c = 0; c < 3; ++c, ++cs) {
+                        const int s = cs & (kD2Slots - 1);
+                        if (cs >= kD2Slots) mbar_wait(&wempty[s], ((cs / kD2Slots) - 1) & 1);
+                        mbar_expect_tx(&wfull[s], kD2Chunk);
+                        bulk_g2s(s_w + (size_t)s * kD2Chunk, P.w + ((size_t)l * 3 + c) * (kD2Chunk / 2), kD2Chunk,
+                                 &wfull[s]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_bf16(128, 64);
+        const uint64_t dX = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_x), 0), slab, 128u);
+        const uint64_t dH = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_h), 0), slab, 128u);
+        const uint64_t dW = umma_desc(__shfl_sync(0xFFFFFFFFu, smem_u32(s_w), 0), 64u * 16u, 128u);
+        const uint32_t rs = (uint32_t)RS;
+        int64_t ti = 0;
+        int cs = 0, gc = 0;
+        for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x, ++gc) {
+            mbar_wait(xready, gc & 1);
+            tc_fence_after();
+            for (int l = 0; l < L; ++l, cs += 3) {
+                const uint64_t dA = (l & 1) ? dH : dX;
+                for (int j = 0; j < T; ++j, ++ti) {
+                    if (l > 0) {  // tiles j - 1 .. j + 1 of the previous layer are in place
+                        if (j == 0) mbar_wait(&hrdy[0], (cs / 3 - 1) & 1);
+                        if (j + 1 < T) mbar_wait(&hrdy[j + 1], (cs / 3 - 1) & 1);
+                        tc_fence_after();
+                    }
+                    const int a = (int)(ti % kDtGroups);
+                    const int64_t u = ti / kDtGroups;
+                    if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
+                    tc_fence_after();
+                    const uint32_t d = tmem + (uint32_t)(a * 64);
+                    const uint32_t al = (uint32_t)dA + (uint32_t)(128 * j), ah = (uint32_t)(dA >> 32);
+                    const uint32_t bh = (uint32_t)(dW >> 32);
+#pragma unroll
+                    for (int di = 0; di < 3; ++di) {
+                        if (j == 0) {  // each row tap's weights just before its first use (the ring refills late)
+                            mbar_wait(&wfull[(cs + di) & (kD2Slots - 1)], ((cs + di) / kD2Slots) & 1);
+                            tc_fence_after();
+                        }
+                        const uint32_t bl = (uint32_t)dW + (uint32_t)(((cs + di) & (kD2Slots - 1)) * (kD2Chunk >> 4));
+#pragma unroll
+                        for (int sg = 0; sg < 8; ++sg) {
+                            const uint32_t sl = (sg < 2) ? 4u + 2u * sg : (sg < 6 ? 2u * (sg - 2) : 2u * (sg - 6));
+                            const uint32_t dj = sg < 2 ? 0u : (sg < 6 ? 1u : 2u);
+                            mma_bf16_elect_w(d, al + sl * rs + (uint32_t)di * (uint32_t)Wq + dj, ah,
+                                             bl + (uint32_t)(2 * sg * 64), bh, idesc, (di | sg) ? 1u : 0u);
+                        }
+                        if (j == T - 1) mma_commit_elect(&wempty[(cs + di) & (kD2Slots - 1)]);
+                    }
+                    mma_commit_elect(&tfull[a]);
+                }
+            }
+        }
+    } else {
+        const int grp = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0 .. 128 kDtGroups - 1
+        const int HWpp = P.Hp * Wpp, HW = P.Hp * Wp;
+        const FastDiv div_hw{(uint32_t)HWq, (uint32_t)(0x100000000ull / (uint32_t)HWq)};
+        const FastDiv div_w{(uint32_t)Wq, (uint32_t)(0x100000000ull / (uint32_t)Wq)};
+        const FastDiv div_hwp{(uint32_t)HWpp, (uint32_t)(0x100000000ull / (uint32_t)HWpp)};
+        const FastDiv div_wp{(uint32_t)Wpp, (uint32_t)(0x100000000ull / (uint32_t)Wpp)};
+        mbar_wait(tbar, 0);
+        int64_t ti = 0;
+        int lc = 0;
+        for (int64_t gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+            const int64_t n0 = gi * G;
+            const int g_act = (int)min((int64_t)G, P.n_img - n0);
+            // gather: X = T[idx] at every padded position of the group (edges by
+            // clamping; the extra even-width column too)
+            constexpr int kStep = 128 * kDtGroups;
+            for (int p0 = et; p0 < g_act * HWpp; p0 += 4 * kStep) {
+                int kk[4];  // four index loads in flight before any use
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int p = p0 + u * kStep;
+                    kk[u] = 0;
+                    if (p < g_act * HWpp) {
+                        const int n = (int)fdiv((uint32_t)p, div_hwp), rem = p - n * HWpp;
+                        const int yy = (int)fdiv((uint32_t)rem, div_wp), xx = rem - yy * Wpp;
+                        int y = yy - 1, x = xx - 1;
+                        y = y < 0 ? 0 : (y >= gh ? gh - 1 : y);
+                        x = x < 0 ? 0 : (x >= gw ? gw - 1 : x);
+                        kk[u] = P.idx[((n0 + n) * gh + y) * gw + x];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int p = p0 + u * kStep;
+                    if (p >= g_act * HWpp) break;
+                    const uint4 *src = reinterpret_cast<const uint4 *>(s_tab + (size_t)kk[u] * 64);
+                    uint8_t *dst = s_x + ((size_t)(4 * (p & 1)) * slab + (size_t)(M0 + (p >> 1)) * 16);
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) reinterpret_cast<uint4 *>(dst + (size_t)g * slab)[0] = src[g];
+                }
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xready);
+            for (int l = 0; l < L; ++l, ++lc) {
+                const bool conv2 = (l & 1) != 0, last = l == L - 1;
+                const float *bias = s_b + l * 32;
+                uint8_t *dst = conv2 ? s_x : s_h;
+                for (int j = 0; j < T; ++j, ++ti) {
+                    // tile ti: accumulator a = ti % 3; its even pixels go to group
+                    // a, its odd pixels to group a + 1 (mod 3), halving the
+                    // epilogue latency per tile (a layer has few tiles, and tile
+                    // j of the next layer waits for tiles j - 1 .. j + 1)
+                    const int a = (int)(ti % kDtGroups);
+                    const int h = a == grp ? 0 : (a == (grp + kDtGroups - 1) % kDtGroups ? 1 : -1);
+                    if (h < 0) continue;
+                    const uint32_t u = (uint32_t)(ti / kDtGroups);
+                    const int r = 128 * j + row;
+                    const int n = (int)fdiv((uint32_t)r, div_hw), rem = r - n * HWq;
+                    const int y = (int)fdiv((uint32_t)rem, div_w), x = 2 * (rem - y * Wq) + h;
+                    mbar_wait(&tfull[a], u & 1);
+                    tc_fence_after();
+                    {
+                        float v[32];
+                        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(a * 64 + 32 * h), v);
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[a]);
+                        if (!(n < g_act && y >= 1 && y <= gh && x >= 1 && x <= gw)) goto tile_done;
+                        uint4 w4[NG];
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) {
+                            float o[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(v[8 * g + e], bias[8 * g + e]);
+                            if (conv2) {
+                                const uint4 rv = reinterpret_cast<const uint4 *>(
+                                    s_x + (size_t)(g + 4 * h) * slab + (size_t)(M0 + r) * 16)[0];
+                                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    o[2 * e] = __fadd_rn(bf16_lo(rw[e]), o[2 * e]);
+                                    o[2 * e + 1] = __fadd_rn(bf16_hi(rw[e]), o[2 * e + 1]);
+                                }
+                            }
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) o[e] = fmaxf(o[e], 0.f);
+                            w4[g] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]),
+                                               pack_bf16(o[6], o[7]));
+                        }
+                        if (last) {
+                            const int64_t q = (n0 + n) * HW + (int64_t)y * Wp + x;
+#pragma unroll
+                            for (int g = 0; g < NG; ++g)
+                                store_px(P.out + ((int64_t)g * P.out_gstride + P.out_margin) * 8, q, w4[g], y, x, gh,
+                                         gw, Wp);
+                        } else {
+                            // pixel q of the group at slab g + 4 (q & 1), row q / 2, plus its edge copies
+                            const int q = n * HWpp + y * Wpp + x;
+                            const int ey = (y == 1 ? -Wpp : (y == gh ? Wpp : 0)), ey2 = (y == 1 && y == gh) ? Wpp : 0;
+                            const int ex = (x == 1 ? -1 : (x == gw ? 1 : 0)), ex2 = (x == 1 && x == gw) ? 1 : 0;
+#pragma unroll
+                            for (int g = 0; g < NG; ++g) {
+                                auto put = [&](int qq) {
+                                    reinterpret_cast<uint4 *>(dst + (size_t)(g + 4 * (qq & 1)) * slab +
+                                                              (size_t)(M0 + (qq >> 1)) * 16)[0] = w4[g];
+                                };
+                                put(q);
+                                if (ex) put(q + ex);
+                                if (ex2) put(q + ex2);
+                                if (ey) {
+                                    put(q + ey);
+                                    if (ex) put(q + ey + ex);
+                                    if (ex2) put(q + ey + ex2);
+                                }
+                                if (ey2) {
+                                    put(q + ey2);
+                                    if (ex) put(q + ey2 + ex);
+                                    if (ex2) put(q + ey2 + ex2);
+                                }
+                            }
+                        }
+                    }
+                tile_done:
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&hrdy[j]);
+                }
+            }
+            // the next group's gather overwrites X: every epilogue warp is past its residual reads
+            asm volatile("bar.sync 1, %0;" ::"n"(128 * kDtGroups) : "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u));
+    }
+}
+
+size_t dec_trunk2_smem(int Hp, int Wp, int G, int K, int n_conv, int *pad) {
+    const int Wq = ((Wp + 1) & ~1) / 2;
+    const int rows = G * Hp * Wq, T = (rows + 127) / 128, M0 = Wq + 1;
+    const size_t RS = (size_t)M0 + rows + M0;
+    const int p = ((128 * T - rows + 16) * 16 + 127) / 128 * 128;
+    if (pad) *pad = p;
+    return kD2Slots * kD2Chunk + (size_t)K * 64 + 2 * 8 * RS * 16 + p +
+           (2 * kD2Slots + 2 * kDtGroups + 2 + kD2MaxTiles) * 8 + 16 + (size_t)n_conv * 32 * 4;
+}
+
 // ---- decoder output stage in shared memory (vqvae.py:101-112) ---------------
 // The up conv (3x3, 32 -> 128), pixel shuffle + ReLU and the logistic head of
 // one image per CTA iteration; the 2x hi-res activations (the largest tensor
@@ -3128,6 +3426,41 @@ int dec_uphead_launch(const DecUpHead &p, cudaStream_t s) {
     const double flops = 2.0 * p.n_img * p.gh * p.gw * 32.0 * 9 * (128 + 4 * 6);
     ProfScope _ps(PROF_DEC_UPHEAD, s, flops);
     dec_uphead_kernel<<<(unsigned)grid, kThreadsUH, smem, s>>>(p);
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+int dec_trunk2_launch(const DecTrunk &p0, cudaStream_t s) {
+    DecTrunk p = p0;
+    if (p.n_conv < 1 || p.n_conv > kDtMaxConvs || p.K < 1 || p.K > 256) return PILC_E_UNSUPPORTED;
+    const int Wq = ((p.Wp + 1) & ~1) / 2;
+    if (Wq + 1 > 128) return PILC_E_UNSUPPORTED;  // a tile's halo reaches one tile either way
+    if ((uint64_t)p.n_img * p.Hp * 2 * Wq >= (1ull << 31)) return PILC_E_UNSUPPORTED;
+    // images per group: the most images per MMA tile (fewest padded rows), then the most images
+    int G = 0, pad = 0, bestT = 1;
+    size_t smem = 0;
+    for (int g = 1; g <= 64; ++g) {
+        int pd;
+        const size_t sm = dec_trunk2_smem(p.Hp, p.Wp, g, p.K, p.n_conv, &pd);
+        const int T = (g * p.Hp * Wq + 127) / 128;
+        if (sm > 227 * 1024 || T > kD2MaxTiles) break;
+        if (G == 0 || (int64_t)g * bestT >= (int64_t)G * T) {
+            G = g;
+            bestT = T;
+            pad = pd;
+            smem = sm;
+        }
+    }
+    if (G == 0) return PILC_E_UNSUPPORTED;
+    p.G = G;
+    p.pad_bytes = pad;
+    allow_dyn_smem(reinterpret_cast<const void *>(dec_trunk2_kernel));
+    const int64_t groups = (p.n_img + G - 1) / G;
+    int64_t grid = sm_count();
+    if (grid > groups) grid = groups;
+    if (grid < 1) return PILC_OK;
+    const double flops = 2.0 * p.n_img * (p.Hp - 2) * (p.Wp - 2) * 32.0 * 32 * 9 * p.n_conv;
+    ProfScope _ps(PROF_DEC_TRUNK, s, flops);
+    dec_trunk2_kernel<<<(unsigned)grid, kThreadsDT, smem, s>>>(p);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }

@@ -37,13 +37,16 @@ struct DecTrunk {
     int Hp, Wp;                // padded latent grid
     int64_t n_img;
     int n_conv;                // 2B, <= 16
-    const uint16_t *w;         // 2B consecutive [36][32][8] bf16 B operands
+    const uint16_t *w;         // 2B consecutive [36][32][8] bf16 B operands (pairs: [48][64][8])
     const float *bias[16];
     uint16_t *out;             // padded group-major bf16 slabs (the up conv's input)
     int64_t out_gstride, out_margin;
     int G, pad_bytes;          // set by the launcher
 };
 int dec_trunk_launch(const DecTrunk &p, cudaStream_t s);
+// The same over pixel pairs (N = 64 MMAs, 24 per 256 pixels; w = 2B
+// consecutive [48][64][8] bf16 pair operands, vq.cu tc_blk2); bit-identical.
+int dec_trunk2_launch(const DecTrunk &p, cudaStream_t s);
 
 // Decoder output stage: up conv + pixel shuffle + logistic head of one image
 // per CTA iteration, the hi-res activations kept in shared memory (same

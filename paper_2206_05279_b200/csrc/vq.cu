@@ -53,6 +53,7 @@ struct Layout {
     // uint16 units from the model base; see tc_conv.cu
     bool tc;
     std::vector<int64_t> tc_blk;  // 2B block convs, N = 32
+    int64_t tc_blk2;              // the same over pixel pairs: 2B x [48][64][8] (dec_trunk2_kernel)
     int64_t tc_up, tc_head;       // N = 128, N = 16 (mu 0..2, s 3..5)
     int64_t tc_head2;             // the head over pixel pairs: K = 3 x 128, N = 16 (even px 0..5, odd 6..11)
     // tcgen05 encoder (C == 32, Dc == 32): fp16-split B operands
@@ -110,6 +111,8 @@ Layout make_layout(int K, int Dc, int C, int B) {
             L.tc_blk.push_back(h);
             h += 36 * 32 * 8;
         }
+        L.tc_blk2 = h;
+        h += (int64_t)2 * B * 48 * 64 * 8;
         L.tc_up = h;
         h += 36 * 128 * 8;
         L.tc_head = h;
@@ -952,6 +955,22 @@ extern "C" int pilc_model_pack(const float *src, int32_t K, int32_t Dc, int32_t 
                     }
         };
         for (int i = 0; i < 2 * B; ++i) put_b(L.tc_blk[i], L.dec[1 + i], 32, 0, 32);
+        // block convs over pixel pairs: K = row tap di (3) x [left odd px | even
+        // px | odd px | right even px] x 32 ch, N = even pixel's 32 outputs,
+        // then the odd pixel's (zero where a part is not that pixel's tap)
+        for (int i = 0; i < 2 * B; ++i) {
+            const ConvSpec &sp = L.dec[1 + i];
+            const int64_t off = L.tc_blk2 + (int64_t)i * 48 * 64 * 8;
+            for (int kk = 0; kk < 384; ++kk) {
+                const int st = kk / 16, di = st / 8, sg = st % 8, ci = (sg & 1) * 16 + kk % 16, part = sg >> 1;
+                for (int n = 0; n < 64; ++n) {
+                    const int co = n & 31;
+                    const int dj = n < 32 ? (part < 3 ? part : -1) : (part > 0 ? part - 1 : -1);
+                    const float w = dj < 0 ? 0.f : dst[sp.w_off + ((int64_t)(di * 3 + dj) * sp.ci_pad + ci) * sp.co_pad + co];
+                    h[off + ((int64_t)(kk >> 3) * 64 + n) * 8 + (kk & 7)] = bf16(w);
+                }
+            }
+        }
         put_b(L.tc_up, L.dec[1 + 2 * B], 128, 0, 128);
         put_b(L.tc_head, L.dec[2 + 2 * B], 16, 0, 6);
         {  // pair head: K = row tap di (3) x [left odd px | even px | odd px | right even px] x 32 ch
@@ -1505,7 +1524,13 @@ int tc_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *mode
         p.out = tw.X;
         p.out_gstride = tw.gs;
         p.out_margin = tw.margin;
-        rc = dec_trunk_launch(p, s);
+        rc = PILC_E_UNSUPPORTED;
+        if (g_tuning[PILC_TUNE_DEC_TRUNK] == 2) {  // over pixel pairs
+            DecTrunk p2 = p;
+            p2.w = hb + L.tc_blk2;
+            rc = dec_trunk2_launch(p2, s);
+        }
+        if (rc == PILC_E_UNSUPPORTED) rc = dec_trunk_launch(p, s);
         if (rc == PILC_OK) trunk_done = true;
         else if (rc == PILC_E_UNSUPPORTED) rc = PILC_OK;
     }

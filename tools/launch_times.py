@@ -9,6 +9,9 @@ H = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
 dev = torch.device("cuda", 0); stream = torch.cuda.current_stream(dev)
 NUM = sys.argv[3] if len(sys.argv) > 3 else "fast"
+for kv in filter(None, os.environ.get("PILC_TUNING", "").split(",")):  # e.g. PILC_TUNING=1=1,3=0
+    k, v = kv.split("=")
+    _lib.set_tuning(int(k), int(v))
 model = pc.random_weights(seed=1); cfg = pc.CodecConfig(backend="twar-vqvae", numerics=NUM)
 img_d = torch.from_numpy(smooth_images(N, H, H, seed=0)).to(dev)
 def step():
