@@ -301,14 +301,41 @@ __device__ inline uint32_t warp_crc32_fast(const CrcConsts *cc, const CrcSlices 
             }
             if (s < 4) w[0] ^= 0xFFFFFFFFu >> (8 * s);  // the init register, folded into bytes 0..3
             c = crc_raw64(cc->tab, sl, w);
-        } else if (s + 64 > 0) {  // the chunk holding the first byte: what precedes p is zero
-#pragma unroll 1
+        } else if (s + 64 > 0) {
+            // the chunk holding the first byte: what precedes p is zero. The
+            // bytes come from the 16-byte vectors from align_down(p) on (never
+            // below the buffer, which is 16-byte aligned), re-aligned to the
+            // chunk's start s < 0 relative to p and masked below p
+            const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+            const uint4 *a0 = reinterpret_cast<const uint4 *>(a & ~(uintptr_t)15);
+            const int d = (int)(a & 15);
+            uint32_t W[20];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                const uint4 v = (16 * k < d + (int)(s + 64)) ? a0[k] : make_uint4(0u, 0u, 0u, 0u);
+                W[4 * k] = v.x;
+                W[4 * k + 1] = v.y;
+                W[4 * k + 2] = v.z;
+                W[4 * k + 3] = v.w;
+            }
+            const int s32 = (int)s;  // -63 .. -1
+            // words from align_down(p) with 16 zero words in front: word i of
+            // the chunk starts at byte s + 4 i + d of that window (one lane per
+            // message takes this path; the dynamic index goes to local memory)
+            uint32_t Z[37];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) Z[k] = 0u;
+#pragma unroll
+            for (int k = 0; k < 20; ++k) Z[16 + k] = W[k];
+            Z[36] = 0u;
+            const int o0 = s32 + d + 64;  // >= 1
+            const int q0 = o0 >> 2, sh = 8 * (o0 & 3);
+#pragma unroll
             for (int i = 0; i < 16; ++i) {
-                uint32_t v = 0;
-                for (int b = 0; b < 4; ++b) {
-                    const int64_t j = s + 4 * i + b;
-                    if (j >= 0) v |= (uint32_t)(p[j] ^ (j < 4 ? 0xFF : 0)) << (8 * b);
-                }
+                uint32_t v = __funnelshift_r(Z[q0 + i], Z[q0 + i + 1], sh);
+                const int j0 = s32 + 4 * i;  // offset of the word's byte 0 from p
+                if (j0 < 0) v = j0 > -4 ? v & (0xFFFFFFFFu << (8 * -j0)) : 0u;
+                if (j0 > -4 && j0 < 4) v ^= j0 >= 0 ? 0xFFFFFFFFu >> (8 * j0) : 0xFFFFFFFFu << (8 * -j0);
                 w[i] = v;
             }
             c = crc_raw64(cc->tab, sl, w);
