@@ -828,6 +828,23 @@ def _smem_operand_bytes(name, wl, K=256, B=4):
             return None
         tiles = ((G * Hp * Wp + 127) // 128) * ((n + G - 1) // G)
         return tiles * 2 * B * 18 * (4096 + 1024)
+    if name == "dec_trunk2_kernel":  # pixel pairs: 24 MMAs of N=64 per 128 pair rows (dec_trunk2_launch's G)
+        Wq = (Wp + 1) // 2 * 2 // 2
+        best = None
+        for g in range(1, 65):
+            rows = g * Hp * Wq
+            T = (rows + 127) // 128
+            RS = 2 * (Wq + 1) + rows
+            pad = ((128 * T - rows + 16) * 16 + 127) // 128 * 128
+            sm = 4 * 16384 + K * 64 + 2 * 8 * RS * 16 + pad + (8 + 6 + 2 + 16) * 8 + 16 + 2 * B * 32 * 4
+            if sm > 227 * 1024 or T > 16:
+                break
+            if best is None or g * best[1] >= best[0] * T:
+                best = (g, T)
+        if not best:
+            return None
+        G, T = best
+        return T * ((n + G - 1) // G) * 2 * B * 24 * (4096 + 2048)
     if name == "dec_uphead_kernel":  # up conv (N=128, 18 MMAs per tile) + pair head (N=16, 24 per tile)
         tu = (Hp * Wp + 127) // 128
         th = ((2 * gh + 2) * (gw + 1) + 127) // 128
@@ -865,6 +882,9 @@ def _roofline(prof, clk, steps, wl=None):
                             "FLOPs = (2B x 9 + 1) x 2*N*H*W*32*32 (MMA FLOPs issued = 3x that)",
         "dec_trunk_kernel": "decoder trunk (gather + all 2B bf16 block convs, activations in shared memory, G images per "
                             "CTA iteration); algorithmic FLOPs = 2B x 2*N*gh*gw*32*32*9",
+        "dec_trunk2_kernel": "decoder trunk over pixel pairs (gather + all 2B bf16 block convs, activations in shared "
+                             "memory, one MMA row = two adjacent pixels, N=64); algorithmic FLOPs = 2B x "
+                             "2*N*gh*gw*32*32*9",
         "dec_uphead_kernel": "decoder output stage (bf16 up conv 32 -> 128 + pixel shuffle + the logistic head over "
                              "pixel pairs, one image per CTA iteration, hi-res activations in shared memory); "
                              "algorithmic FLOPs = 2*N*gh*gw*32*9*(128 + 4*6)",
@@ -895,9 +915,11 @@ def _roofline(prof, clk, steps, wl=None):
         # B200 (tools/micro/mma_rate.cu: N=16/32 44, N=64 48, N=128 64), so
         # N=32-output convs cannot approach the dense peak. Cycles per
         # 128-row K=16 step (algorithmic 2*128*32*16 FLOP): bf16 convs 44;
-        # the 3-product fp16 encoder (N=64 + N=32 MMAs) 92.
-        floor_cyc = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0,
-                     "enc_trunk_kernel": 92.0}.get(name)
+        # the pair trunk 32 (one N=64 MMA, 48 cycles, carries 1.5 such steps:
+        # 24 MMAs per 36 steps); the 3-product fp16 encoder (N=64 + N=32
+        # MMAs) 92.
+        floor_cyc = {"dec_trunk_kernel": 44.0, "dec_trunk2_kernel": 32.0, "tc3_block_kernel": 92.0,
+                     "tc3_conv_kernel": 92.0, "enc_trunk_kernel": 92.0}.get(name)
         if floor_cyc and roofline and roofline.get("bound") == "tensor":
             att = 2.0 * 128 * 32 * 16 / floor_cyc * sm * mhz * 1e6 / 1e12
             roofline["mma_floor"] = {"peak": round(att, 1), "unit": "TFLOP/s",
@@ -924,7 +946,8 @@ def _roofline(prof, clk, steps, wl=None):
                 "twar_forward_kernel": "twar_forward_tile_kernel"}
     hbm_peak = peaks.get("hbm_gbs")
     tpeak = peaks.get("bf16_tflops")
-    floor = {"dec_trunk_kernel": 44.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0, "enc_trunk_kernel": 92.0}
+    floor = {"dec_trunk_kernel": 44.0, "dec_trunk2_kernel": 32.0, "tc3_block_kernel": 92.0, "tc3_conv_kernel": 92.0,
+             "enc_trunk_kernel": 92.0}
     stages = {}
     for k, (n, ms, units) in prof.items():
         e = {"launches": n, "ms_per_step": round(ms / steps, 4)}

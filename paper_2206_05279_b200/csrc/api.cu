@@ -14,7 +14,7 @@ const char *kCatNames[PROF_NCAT] = {"conv_kernel",        "argmin_kernel",  "ran
                                     "parse_kernel",       "lanes_kernel",   "crc_kernel",
                                     "sched_crc_kernel",   "tc_conv_kernel", "gather_kernel",
                                     "tc3_conv_kernel", "enc_front_kernel", "tc3_block_kernel", "dec_trunk_kernel", "enc_trunk_kernel",
-                                    "dec_uphead_kernel"};
+                                    "dec_uphead_kernel", "dec_trunk2_kernel"};
 struct Rec {
     int cat;
     cudaEvent_t e0, e1;

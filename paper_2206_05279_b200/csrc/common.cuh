@@ -40,6 +40,7 @@ enum ProfCat {
     PROF_DEC_TRUNK,
     PROF_ENC_TRUNK,
     PROF_DEC_UPHEAD,
+    PROF_DEC_TRUNK2,
     PROF_NCAT
 };
 void *prof_begin(int cat, cudaStream_t s, double units);

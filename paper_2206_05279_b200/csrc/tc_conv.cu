@@ -3459,7 +3459,7 @@ int dec_trunk2_launch(const DecTrunk &p0, cudaStream_t s) {
     if (grid > groups) grid = groups;
     if (grid < 1) return PILC_OK;
     const double flops = 2.0 * p.n_img * (p.Hp - 2) * (p.Wp - 2) * 32.0 * 32 * 9 * p.n_conv;
-    ProfScope _ps(PROF_DEC_TRUNK, s, flops);
+    ProfScope _ps(PROF_DEC_TRUNK2, s, flops);
     dec_trunk2_kernel<<<(unsigned)grid, kThreadsDT, smem, s>>>(p);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
