@@ -583,7 +583,10 @@ def measure(ctx, groups_h, model, cfg, steps: int, warmup: int, profile: bool = 
         assert np.array_equal(last, imgs)
         # steady-state step time: the median interval between consecutive
         # steps' completions (the sync figure above is a median step too)
-        t_s = statistics.median([b - a for a, b in zip(done[:-1], done[1:])])
+        ivs = [b - a for a, b in zip(done[:-1], done[1:])]
+        if os.environ.get("PILC_BENCH_DEBUG"):
+            print("stream intervals ms: " + " ".join(f"{1e3 * x:.2f}" for x in ivs), file=sys.stderr)
+        t_s = statistics.median(ivs)
         e_s = ctx.max([t_s])[0]
     e2e_sync = {"value": raw_all / 1e6 / e_t, "unit": "MB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "compress_mb_s": round(raw_all / 1e6 / e_c, 3),

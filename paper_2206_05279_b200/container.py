@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import CACHE, as_device_u8, h2d, pinned, ptr, require_device, sptr
+from .device import CACHE, as_device_u8, h2d, pinned, ptr, readback, require_device, sptr
 from .errors import CorruptStreamError, FormatError, ModelError, ParameterError
 from .logistic import ScaleGrid, default_grid, residual_distributions
 from .predictor import PredictorParams, decode_device, default_params, forward_residual_device, validate_image
@@ -406,10 +406,7 @@ def _parse_begin(buf_d, off_d, n, model, dev, stream):
     summ_d = torch.empty(_lib.SUMMARY_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     _lib.call("pilc_container_summary", ptr(buf_d), ptr(off_d), ptr(hdr_d), n, ptr(summ_d), sptr(stream))
     host = pinned(summ_d.numel())
-    with torch.cuda.stream(stream):
-        host.copy_(summ_d, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(stream)
+    ev = readback(host, summ_d, stream)
     return hdr_d, host, ev
 
 

@@ -52,6 +52,31 @@ def pinned(nbytes: int) -> torch.Tensor:
     return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
 
 
+_READBACK: dict = {}
+
+
+def readback(host: torch.Tensor, src: torch.Tensor, stream: torch.cuda.Stream) -> torch.cuda.Event:
+    """Small device result -> page-locked host, after `stream`'s work so far,
+    on a per-device read-back stream; returns the copy's completion event.
+    Issued on `stream` itself the copy would wait on the copy engine behind
+    other streams' large transfers (a pipelined caller's image and blob
+    downloads) and hold back every kernel queued after it (measured: +0.7 ms
+    per CIFAR-8192 decompress under StreamCodec)."""
+    key = src.device.index
+    rb = _READBACK.get(key)
+    if rb is None:
+        rb = _READBACK.setdefault(key, torch.cuda.Stream(src.device))
+    after = torch.cuda.Event()
+    after.record(stream)
+    rb.wait_event(after)
+    src.record_stream(rb)
+    with torch.cuda.stream(rb):
+        host.copy_(src, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(rb)
+    return ev
+
+
 def h2d(arr: np.ndarray, dev: torch.device, stream: torch.cuda.Stream, pad: int = 0) -> torch.Tensor:
     """Host numpy -> device tensor on `stream`. Page-locked sources (any
     cudaHostAlloc'd / registered memory, e.g. buffers this package returned)

@@ -16,7 +16,7 @@ import torch
 from .container import (CodecConfig, SpeculationMiss, _decompress_device, _resolve_errors, _verify, check_offsets,
                         compress_batch)
 from .errors import FormatError, ParameterError
-from .device import h2d, pinned, require_device
+from .device import h2d, pinned, readback, require_device
 
 
 _SIDE: dict = {}
@@ -99,9 +99,7 @@ def _compress_launch(frames_d, model, config, ph, pw, dev, streams, after):
             out_d, off_d, _ = compress_batch(_group_patches(frames_d, g), model, config, device=dev,
                                              return_device=True)
             h = pinned(off_d.numel() * 8)
-            h.copy_(off_d.view(torch.uint8), non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(s)
+            ev = readback(h, off_d.view(torch.uint8), s)
         parts.append((out_d, off_d))
         offs_h.append(h)
         evs.append(ev)

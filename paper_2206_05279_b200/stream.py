@@ -34,7 +34,7 @@ import torch
 
 from .container import (CodecConfig, SpeculationMiss, _compress_device, _decompress_device, _resolve_errors,
                         _verify, check_offsets)
-from .device import pinned, require_device
+from .device import pinned, readback, require_device
 from .errors import FormatError, ParameterError
 from . import patches as _pt
 
@@ -106,9 +106,7 @@ class StreamCodec:
         with torch.cuda.stream(self.kern):
             out_d, off_d = _compress_device(img_d.view(arr.shape), self.model, self.config, self.dev, self.kern)
             offs_h = pinned(8 * (n + 1))
-            offs_h.copy_(off_d.view(torch.uint8), non_blocking=True)
-            ev_k = torch.cuda.Event()
-            ev_k.record(self.kern)
+            ev_k = readback(offs_h, off_d.view(torch.uint8), self.kern)  # after the kernels; off the kernel stream
 
         def finish():
             ev_k.synchronize()
