@@ -13,8 +13,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .container import (CodecConfig, SpeculationMiss, _decompress_device, _resolve_errors, _verify, check_offsets,
-                        compress_batch)
+from .container import (CodecConfig, SpeculationMiss, _compress_device, _decompress_device, _resolve_errors, _verify,
+                        check_offsets)
 from .errors import FormatError, ParameterError
 from .device import h2d, pinned, readback, require_device
 
@@ -96,8 +96,9 @@ def _compress_launch(frames_d, model, config, ph, pw, dev, streams, after):
         s.wait_event(after)
         frames_d.record_stream(s)
         with torch.cuda.stream(s):
-            out_d, off_d, _ = compress_batch(_group_patches(frames_d, g), model, config, device=dev,
-                                             return_device=True)
+            # straight to the device compress: no host read before the next
+            # group (or the next request) is queued
+            out_d, off_d = _compress_device(_group_patches(frames_d, g), model, config, dev, s)
             h = pinned(off_d.numel() * 8)
             ev = readback(h, off_d.view(torch.uint8), s)
         parts.append((out_d, off_d))
@@ -220,40 +221,55 @@ def _decode_launch(buf_d, offsets, F, H, W, model, ph, pw, dev, streams, after):
             goff_d = torch.empty(F * k + 1, dtype=torch.int64, device=dev)
             goff_d.view(torch.uint8).copy_(goff_h, non_blocking=True)
             res = _decompress_device(gbuf, goff_d, F * k, model, dev, s)
-        launched.append((g, s, gbuf, goff_d, goff_h, res, k))
+            ev_dec = torch.cuda.Event()  # this group's decode, recorded now (later work may follow on s)
+            ev_dec.record(s)
+        launched.append((g, s, gbuf, goff_d, goff_h, res, k, ev_dec))
     return launched
 
 
-def _decode_finish(launched, frames_d, model, dev, out_stream=None):
+def _assemble(g, img, frames_d, stream):
+    """The group's decoded patches into their places in frames_d, on stream."""
+    rows, cols, nr, nc, h, w = g
+    F = frames_d.shape[0]
+    with torch.cuda.stream(stream):
+        img.record_stream(stream)
+        frames_d.record_stream(stream)
+        frames_d[:, rows, cols] = img.reshape(F, nr, nc, h, w, 3).permute(0, 1, 3, 2, 4, 5).reshape(
+            F, nr * h, nc * w, 3)
+
+
+def _decode_finish(launched, frames_d, model, dev, out_stream=None, assembled=None):
     """Check each launched group (blocks on its summary), raise its first
     error, and write its patches into frames_d (on the group's stream, or on
-    out_stream after the group's decode when given); returns the events the
-    frames are complete after."""
+    out_stream after the group's decode when given). `assembled`: per group
+    the event recorded right after its patches were written into frames_d
+    on its stream at launch (redone there only when the speculated batch
+    layout missed). Returns the events the frames are complete after."""
     F = frames_d.shape[0]
     evs = []
-    for g, s, gbuf, goff_d, goff_h, (results, errors, hdr), k in launched:
-        rows, cols, nr, nc, h, w = g
+    for gi, (g, s, gbuf, goff_d, goff_h, (results, errors, hdr), k, done) in enumerate(launched):
+        redo = False
         with torch.cuda.stream(s):
             try:
                 _verify(results)
             except SpeculationMiss:
                 results, errors, hdr = _decompress_device(gbuf, goff_d, F * k, model, dev, s, speculate=False)
-            done = torch.cuda.Event()
-            done.record(s)
+                redo = True
+                done = torch.cuda.Event()
+                done.record(s)
         ws = out_stream if out_stream is not None else s
         with torch.cuda.stream(ws):
             ws.wait_event(done)
             errors = _resolve_errors(results, errors, hdr)
             if errors:
                 raise errors[min(errors)]
-            img = results[0][1]
-            img.record_stream(ws)
-            frames_d.record_stream(ws)
-            frames_d[:, rows, cols] = img.reshape(F, nr, nc, h, w, 3).permute(0, 1, 3, 2, 4, 5).reshape(
-                F, nr * h, nc * w, 3)
-            ev = torch.cuda.Event()
-            ev.record(ws)
-        evs.append(ev)
+        if assembled is not None and assembled[gi] is not None and not redo:
+            done = assembled[gi]
+        else:
+            _assemble(g, results[0][1], frames_d, s if assembled is not None else ws)
+            done = torch.cuda.Event()
+            done.record(s if assembled is not None else ws)
+        evs.append(done)
     return evs
 
 

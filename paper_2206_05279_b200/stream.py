@@ -217,9 +217,25 @@ class StreamCodec:
         n_groups = len(_pt._groups(H, W, ph, pw))
         launched = _pt._decode_launch(buf_d, offs, n_frames, H, W, self.model, ph, pw, self.dev,
                                       [self.kern] * n_groups, ev_b)
+        # the patches into the frames right behind each group's decode, on the
+        # kernel stream (speculatively: redone there if the batch layout
+        # missed); a copy kernel on another stream would share the SMs with
+        # the next request's persistent kernels
+        assembled = []
+        for g, s, _gb, _go, _gh, res, _k, _ev in launched:
+            ev = None
+            _r, _c, nr, nc, h, w = g
+            # only when the speculated layout has this group's shape (else the
+            # speculation misses and finish() redoes decode + assembly)
+            if res[0] and tuple(res[0][0][1].shape) == (n_frames * nr * nc, h, w, 3):
+                _pt._assemble(g, res[0][0][1], frames_d, s)
+                ev = torch.cuda.Event()
+                ev.record(s)
+            assembled.append(ev)
 
         def finish():
-            evs = _pt._decode_finish(launched, frames_d, self.model, self.dev, out_stream=self.down)
+            evs = _pt._decode_finish(launched, frames_d, self.model, self.dev, out_stream=self.down,
+                                     assembled=assembled)
             ev = evs[-1] if evs else torch.cuda.Event()
             if not evs:
                 ev.record(self.down)
