@@ -268,13 +268,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int PPT>
+template <int PPT, int CO_T>
 __global__ void __launch_bounds__(128, 3) conv_kernel(ConvArgs a) {
     constexpr int CPT = 8;
     constexpr int PGR = 16 / PPT;  // pixel groups per tile row
     extern __shared__ __align__(16) float smem[];
-    const int ks = a.ks, st = a.stride, pad = ks >> 1, TR = a.TR, RP = a.RP, CK = a.CK, CIP = a.CIP,
-              CO_T = a.CO_T;
+    const int ks = a.ks, st = a.stride, pad = ks >> 1, TR = a.TR, RP = a.RP, CK = a.CK, CIP = a.CIP;
     const int IR = (TR - 1) * st + ks, ICW = 15 * st + ks;
     const int ntap = ks * ks;
     const int nchunk = (a.Ci_pad + CK - 1) / CK;
@@ -366,20 +365,31 @@ __global__ void __launch_bounds__(128, 3) conv_kernel(ConvArgs a) {
                 __syncthreads();
                 wcur = s_w;
             }
-            const float *pin = s_in + ((pr * st + ti) * RP + pq * st + tj) * CIP;
+            // per-pixel row pointers advanced by four channels per step, so
+            // the loads inside a step take immediate offsets (cn is a
+            // multiple of 4: CK and Ci_pad are); fmaf order per output as before
+            const float *px[PPT];
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) px[p] = s_in + ((pr * st + ti) * RP + pq * st + tj + p * PGR * st) * CIP;
             const float *pw = wcur + cg * CPT;
-#pragma unroll 2
-            for (int ci = 0; ci < cn; ++ci) {
-                float x[PPT];
+#pragma unroll 1
+            for (int ci = 0; ci < cn; ci += 4) {
 #pragma unroll
-                for (int p = 0; p < PPT; ++p) x[p] = pin[p * PGR * st * CIP + ci];
-                const float4 w0 = *reinterpret_cast<const float4 *>(pw + ci * CO_T);
-                const float4 w1 = *reinterpret_cast<const float4 *>(pw + ci * CO_T + 4);
-                const float w[CPT] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                for (int u = 0; u < 4; ++u) {
+                    float x[PPT];
 #pragma unroll
-                for (int c = 0; c < CPT; ++c)
+                    for (int p = 0; p < PPT; ++p) x[p] = px[p][u];
+                    const float4 w0 = *reinterpret_cast<const float4 *>(pw + u * CO_T);
+                    const float4 w1 = *reinterpret_cast<const float4 *>(pw + u * CO_T + 4);
+                    const float w[CPT] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-                    for (int p = 0; p < PPT; ++p) acc[c][p] = fmaf(w[c], x[p], acc[c][p]);
+                    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+                        for (int p = 0; p < PPT; ++p) acc[c][p] = fmaf(w[c], x[p], acc[c][p]);
+                }
+#pragma unroll
+                for (int p = 0; p < PPT; ++p) px[p] += 4;
+                pw += 4 * CO_T;
             }
         }
 #pragma unroll
@@ -630,12 +640,15 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
     }
     const size_t smem = conv_smem(a);
     dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
-    if (ppt == 8) {
-        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<8>));
-        conv_kernel<8><<<grid, threads, smem, s>>>(a);
+    if (co_t == 32) {
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<8, 32>));
+        conv_kernel<8, 32><<<grid, threads, smem, s>>>(a);
+    } else if (co_t == 16) {
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<8, 16>));
+        conv_kernel<8, 16><<<grid, threads, smem, s>>>(a);
     } else {
-        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4>));
-        conv_kernel<4><<<grid, threads, smem, s>>>(a);
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 8>));
+        conv_kernel<4, 8><<<grid, threads, smem, s>>>(a);
     }
     PILC_CHECK_LAUNCH();
     return PILC_OK;
