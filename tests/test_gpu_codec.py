@@ -889,6 +889,42 @@ def test_stream_codec_frames_match_sync_calls(full_model):
         assert np.array_equal(codec.decompress_frames(*packed[1], 2, 150, 200, 64, 64).result(), reqs[1][0])
 
 
+def test_stream_codec_frames_after_other_layouts(full_model, monkeypatch):
+    """Frame decodes right after batches with the same blob count but another
+    shape, then another M (a decode speculates on the last layout seen for its
+    batch size and StreamCodec writes the patches into the frames before the
+    guess is checked): the frames come back exact, the early write redone."""
+    from paper_2206_05279_b200 import patches as pt
+    from paper_2206_05279_b200.stream import StreamCodec
+
+    misses = []
+    verify = pt._verify
+
+    def counting(results):
+        try:
+            verify(results)
+        except ct.SpeculationMiss:
+            misses.append(1)
+            raise
+
+    monkeypatch.setattr(pt, "_verify", counting)
+
+    frames = smooth_images(3, 64, 128, seed=21)  # 32x32 patches: 8 per frame, one shape group of 24 blobs
+    other_shape = smooth_images(24, 24, 40, seed=22)
+    other_m = smooth_images(24, 32, 32, seed=23)
+    m11 = pc.CodecConfig(backend="twar-vqvae", numerics="fast", M=11)
+    with StreamCodec(full_model, FAST) as codec, StreamCodec(full_model, m11) as codec11:
+        fb, fo = codec.compress_frames(frames, 32, 32).result()
+        b, o = codec.compress(other_shape).result()
+        assert np.array_equal(codec.decompress(b, o).result(), other_shape)
+        assert np.array_equal(codec.decompress_frames(fb, fo, 3, 64, 128, 32, 32).result(), frames)
+        b, o = codec11.compress(other_m).result()
+        assert np.array_equal(codec11.decompress(b, o).result(), other_m)
+        assert np.array_equal(codec.decompress_frames(fb, fo, 3, 64, 128, 32, 32).result(), frames)
+        assert np.array_equal(codec.decompress_frames(fb, fo, 3, 64, 128, 32, 32).result(), frames)
+    assert len(misses) >= 2  # both layout changes were caught and redone
+
+
 def test_stream_codec_matches_sync_calls(full_model):
     """StreamCodec (stream.py): pipelined requests (uploads, kernels and
     downloads on separate streams, results as futures) return exactly what
