@@ -269,7 +269,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int PPT, int CO_T>
-__global__ void __launch_bounds__(128, 3) conv_kernel(ConvArgs a) {
+__global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs a) {
     constexpr int CPT = 8;
     constexpr int PGR = 16 / PPT;  // pixel groups per tile row
     extern __shared__ __align__(16) float smem[];
@@ -570,7 +570,7 @@ int tail_mode_of(const ConvArgs &a, int co_real, int64_t *start, int *count) {
 // co_real: the reference's output channel count of one conv call (the
 // merged mu|s head is two Co = 3 convs)
 int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side, int co_real) {
-    const int ppt = co_t >= 16 ? 8 : 4;
+    const int ppt = 4;  // 4 pixels x 8 channels per thread: ~100 registers, 5 CTAs per SM (8 pixels: 168, 3)
     a.CO_T = co_t;
     const int ncg = co_t / 8;
     const int threads_per_row = (16 / ppt) * ncg;
@@ -641,11 +641,11 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
     const size_t smem = conv_smem(a);
     dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
     if (co_t == 32) {
-        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<8, 32>));
-        conv_kernel<8, 32><<<grid, threads, smem, s>>>(a);
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 32>));
+        conv_kernel<4, 32><<<grid, threads, smem, s>>>(a);
     } else if (co_t == 16) {
-        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<8, 16>));
-        conv_kernel<8, 16><<<grid, threads, smem, s>>>(a);
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 16>));
+        conv_kernel<4, 16><<<grid, threads, smem, s>>>(a);
     } else {
         allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 8>));
         conv_kernel<4, 8><<<grid, threads, smem, s>>>(a);
