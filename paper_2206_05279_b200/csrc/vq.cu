@@ -374,11 +374,27 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
             const float *pw = wcur + cg * CPT;
 #pragma unroll 1
             for (int ci = 0; ci < cn; ci += 4) {
+                // the heads (one channel group per thread, few accumulators):
+                // four channels of a pixel in one 16-byte load, whose
+                // quarter-warp slots the launcher's pitches spread (the
+                // 4-byte loads of these layers hit 4-way bank conflicts);
+                // wider tiles keep 4-byte loads (16-byte ones spill there)
+                float4 xv[PPT];
+                if constexpr (CO_T == 8) {
+#pragma unroll
+                    for (int p = 0; p < PPT; ++p) xv[p] = *reinterpret_cast<const float4 *>(px[p]);
+                }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     float x[PPT];
+                    if constexpr (CO_T == 8) {
 #pragma unroll
-                    for (int p = 0; p < PPT; ++p) x[p] = px[p][u];
+                        for (int p = 0; p < PPT; ++p)
+                            x[p] = u == 0 ? xv[p].x : (u == 1 ? xv[p].y : (u == 2 ? xv[p].z : xv[p].w));
+                    } else {
+#pragma unroll
+                        for (int p = 0; p < PPT; ++p) x[p] = px[p][u];
+                    }
                     const float4 w0 = *reinterpret_cast<const float4 *>(pw + u * CO_T);
                     const float4 w1 = *reinterpret_cast<const float4 *>(pw + u * CO_T + 4);
                     const float w[CPT] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
@@ -598,10 +614,27 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
             for (int cip = ck; cip < ck + 36; ++cip) {
                 if ((cip * 4) % 16 && (cip * 4) % cw) continue;  // copy alignment (weights use 16 B separately)
                 if ((size_t)IR * rp * cip + 2 * (size_t)ck * co_t > 100 * 1024 / 4) continue;
-                // conflict degree of the first activation load of warp 0
+                // conflict degree of the first activation load of warp 0 (the
+                // heads' 16-byte loads: per quarter warp, 16-byte bank slots)
                 int cnt[32][4], deg = 1;
                 int addr_seen[32][4];
                 for (int k = 0; k < 32; ++k) cnt[k][0] = 0;
+                if (co_t == 8) {
+                    for (int qw = 0; qw < 4; ++qw) {
+                        int slot_ad[8][8], slot_n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        for (int l = 8 * qw; l < 8 * qw + 8; ++l) {
+                            const int pg = l / ncg, pr = pg / (16 / ppt), pq = pg % (16 / ppt);
+                            const int ad = ((pr * a.stride) * rp + pq * a.stride) * cip;
+                            const int sl = (ad >> 2) & 7;
+                            bool dup = false;
+                            for (int j = 0; j < slot_n[sl]; ++j) dup |= slot_ad[sl][j] == ad;
+                            if (!dup) {
+                                slot_ad[sl][slot_n[sl]++] = ad;
+                                deg = deg > slot_n[sl] ? deg : slot_n[sl];
+                            }
+                        }
+                    }
+                } else
                 for (int l = 0; l < 32; ++l) {
                     const int pg = l / ncg, pr = pg / (16 / ppt), pq = pg % (16 / ppt);
                     const int ad = ((pr * a.stride) * rp + pq * a.stride) * cip;
