@@ -636,9 +636,10 @@ def test_decoder_trunk_kernel_bit_identical(full_model, shape, n):
             assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
-@pytest.mark.parametrize("shape,n", [((32, 32), 301), ((30, 18), 7), ((1, 1), 3), ((17, 33), 5), ((34, 34), 150),
-                                     ((33, 2), 9), ((2, 200), 4), ((64, 64), 2)])
-def test_decoder_output_stage_bit_identical(full_model, shape, n):
+@pytest.mark.parametrize("shape,n,D", [((32, 32), 301, 8), ((30, 18), 7, 8), ((1, 1), 3, 8), ((17, 33), 5, 8),
+                                       ((34, 34), 150, 8), ((33, 2), 9, 8), ((2, 200), 4, 8), ((64, 64), 2, 8),
+                                       ((32, 32), 40, 20), ((18, 30), 6, 1)])
+def test_decoder_output_stage_bit_identical(full_model, shape, n, D):
     """dec_uphead_kernel (up conv + pixel shuffle + head of one image per CTA
     iteration, the hi-res activations in shared memory) gives exactly the mu /
     s / shift / scale index of the two launches through HBM (up conv, then
@@ -653,7 +654,7 @@ def test_decoder_output_stage_bit_identical(full_model, shape, n):
     gh, gw = vqvae.latent_shape(H, W)
     rng = np.random.default_rng(11)
     idx = torch.from_numpy(rng.integers(0, 256, (n, gh, gw), dtype=np.uint8)).to(dev)
-    grid = default_grid()
+    grid = default_grid(D)  # D > 9: the head epilogue's threshold loop in shared memory
     out = []
     for on in (1, 0):
         prev = _lib.set_tuning(_lib.TUNE_DEC_UPHEAD, on)
