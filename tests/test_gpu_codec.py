@@ -670,6 +670,34 @@ def test_decoder_output_stage_bit_identical(full_model, shape, n, D):
         assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
 
 
+@pytest.mark.parametrize("K,B", [(97, 2), (256, 1), (13, 3)])
+def test_decoder_kernels_other_model_sizes(K, B):
+    """The pair decoder trunk (its weight-chunk ring over 2B layers, the
+    K-row table) and the output stage on models with other codebook sizes
+    and block counts: exactly the per-layer decoder's mu / s / shift / d."""
+    from paper_2206_05279_b200 import _lib
+    from paper_2206_05279_b200.device import require_device
+
+    model = pc.random_weights(pc.ModelConfig(K=K, Dc=32, channels=32, blocks=B), seed=K + B)
+    dev = require_device()
+    stream = torch.cuda.current_stream(dev)
+    rng = np.random.default_rng(K)
+    idx = torch.from_numpy(rng.integers(0, K, (50, 16, 16), dtype=np.uint8)).to(dev)
+    out = []
+    for trunk, uphead in ((2, 1), (0, 0)):
+        p1 = _lib.set_tuning(_lib.TUNE_DEC_TRUNK, trunk)
+        p2 = _lib.set_tuning(_lib.TUNE_DEC_UPHEAD, uphead)
+        try:
+            r = vqvae.decode_head_device(idx, model, 32, 32, default_grid(), dev, stream, want_params=True,
+                                         exact=False)
+            out.append([t.cpu().numpy() for t in r])
+        finally:
+            _lib.set_tuning(_lib.TUNE_DEC_TRUNK, p1)
+            _lib.set_tuning(_lib.TUNE_DEC_UPHEAD, p2)
+    for a, b in zip(*out):
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
 def test_report_rows_in_reference_format():
     """report.run_bench (report.py:47-104 twin): rows carry the reference's
     keys; the GPU coder rows come from a checked round trip."""
