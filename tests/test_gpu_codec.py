@@ -979,6 +979,29 @@ def test_stream_codec_matches_sync_calls(full_model):
         assert np.array_equal(fok.result(), batches[2])
 
 
+def test_stream_codec_exact_numerics_matches_reference(full_model, golden):
+    """StreamCodec with the default numerics (the exact network): the
+    containers it makes for the reference's own fixture images are the
+    reference's bytes (lanes 1..3 as the fixtures were made), requests of
+    several codecs in flight at once, and they decode back exactly."""
+    from paper_2206_05279_b200.stream import StreamCodec
+
+    z = golden("vqvae_full.npz")
+    n = int(z["n"])
+    codecs = [StreamCodec(full_model, pc.CodecConfig(backend="twar-vqvae", lanes=1 + j)) for j in range(3)]
+    try:
+        futs = [codecs[k % 3].compress(z[f"img{k}"][None]) for k in range(n)]
+        packed = [f.result() for f in futs]
+        backs = [codecs[k % 3].decompress(*packed[k]) for k in range(n)]
+        for k in range(n):
+            buf, off = packed[k]
+            assert buf[off[0]:off[1]].tobytes() == z["buf"][z["offs"][k]: z["offs"][k + 1]].tobytes()
+            assert np.array_equal(backs[k].result()[0], z[f"img{k}"])
+    finally:
+        for c in codecs:
+            c.close()
+
+
 @pytest.mark.parametrize("seed", range(16))
 def test_randomized_configs_round_trip_and_oracle(seed, small_model, full_model):
     """Randomised sweep over the container's parameter space: shapes 1..70 x
