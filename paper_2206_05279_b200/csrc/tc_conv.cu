@@ -1957,9 +1957,11 @@ size_t dec_trunk_smem(int Hp, int Wp, int G, int K, int n_conv, int *pad) {
 constexpr int kD2Slots = 4;
 constexpr uint32_t kD2Chunk = 16 * 64 * 16;  // one row tap: 16 K groups x 64 rows x 16 B
 constexpr int kD2MaxTiles = 16;
+constexpr int kD2Groups = 3;  // epilogue groups of four warps, one 64-column accumulator each (4: within 1%)
+constexpr int kThreadsD2 = 64 + 128 * kD2Groups;
 
 
-__global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
+__global__ void __launch_bounds__(kThreadsD2, 1) dec_trunk2_kernel(DecTrunk P) {
     constexpr int NG = 4;
     const int Wp = P.Wp, Wpp = (Wp + 1) & ~1, Wq = Wpp >> 1, gh = P.Hp - 2, gw = Wp - 2;
     const int HWq = P.Hp * Wq;  // pair rows per image
@@ -1977,8 +1979,8 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
     uint8_t *s_x = s_tab + (size_t)P.K * 64;                     // 8 slabs
     uint8_t *s_h = s_x + 8 * (size_t)slab;                       // 8 slabs
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_h + 8 * (size_t)slab + P.pad_bytes);
-    uint64_t *wfull = bars, *wempty = bars + kD2Slots, *tfull = bars + 2 * kD2Slots, *tempty = tfull + kDtGroups;
-    uint64_t *xready = tempty + kDtGroups, *tbar = xready + 1, *hrdy = xready + 2;  // hrdy[kD2MaxTiles]
+    uint64_t *wfull = bars, *wempty = bars + kD2Slots, *tfull = bars + 2 * kD2Slots, *tempty = tfull + kD2Groups;
+    uint64_t *xready = tempty + kD2Groups, *tbar = xready + 1, *hrdy = xready + 2;  // hrdy[kD2MaxTiles]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(hrdy + kD2MaxTiles);
     float *s_b = reinterpret_cast<float *>(tmem_slot + 4);      // [L][32]
 
@@ -1989,11 +1991,11 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
             mbar_init(&wfull[a], 1);
             mbar_init(&wempty[a], 1);
         }
-        for (int a = 0; a < kDtGroups; ++a) {
+        for (int a = 0; a < kD2Groups; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 8);
         }
-        mbar_init(xready, 4 * kDtGroups);
+        mbar_init(xready, 4 * kD2Groups);
         mbar_init(tbar, 1);
         for (int j = 0; j < kD2MaxTiles; ++j) mbar_init(&hrdy[j], 8);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -2053,8 +2055,8 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
                         if (j + 1 < T) mbar_wait(&hrdy[j + 1], (cs / 3 - 1) & 1);
                         tc_fence_after();
                     }
-                    const int a = (int)(ti % kDtGroups);
-                    const int64_t u = ti / kDtGroups;
+                    const int a = (int)(ti % kD2Groups);
+                    const int64_t u = ti / kD2Groups;
                     if (u > 0) mbar_wait(&tempty[a], (uint32_t)((u - 1) & 1));
                     tc_fence_after();
                     const uint32_t d = tmem + (uint32_t)(a * 64);
@@ -2084,7 +2086,7 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
         const int grp = (warp - 2) >> 2;
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
-        const int et = threadIdx.x - 64;  // 0 .. 128 kDtGroups - 1
+        const int et = threadIdx.x - 64;  // 0 .. 128 kD2Groups - 1
         const int HWpp = P.Hp * Wpp, HW = P.Hp * Wp;
         const FastDiv div_hw{(uint32_t)HWq, (uint32_t)(0x100000000ull / (uint32_t)HWq)};
         const FastDiv div_w{(uint32_t)Wq, (uint32_t)(0x100000000ull / (uint32_t)Wq)};
@@ -2098,7 +2100,7 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
             const int g_act = (int)min((int64_t)G, P.n_img - n0);
             // gather: X = T[idx] at every padded position of the group (edges by
             // clamping; the extra even-width column too)
-            constexpr int kStep = 128 * kDtGroups;
+            constexpr int kStep = 128 * kD2Groups;
             for (int p0 = et; p0 < g_act * HWpp; p0 += 4 * kStep) {
                 int kk[4];  // four index loads in flight before any use
 #pragma unroll
@@ -2136,10 +2138,10 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
                     // a, its odd pixels to group a + 1 (mod 3), halving the
                     // epilogue latency per tile (a layer has few tiles, and tile
                     // j of the next layer waits for tiles j - 1 .. j + 1)
-                    const int a = (int)(ti % kDtGroups);
-                    const int h = a == grp ? 0 : (a == (grp + kDtGroups - 1) % kDtGroups ? 1 : -1);
+                    const int a = (int)(ti % kD2Groups);
+                    const int h = a == grp ? 0 : (a == (grp + kD2Groups - 1) % kD2Groups ? 1 : -1);
                     if (h < 0) continue;
-                    const uint32_t u = (uint32_t)(ti / kDtGroups);
+                    const uint32_t u = (uint32_t)(ti / kD2Groups);
                     const int r = 128 * j + row;
                     const int n = (int)fdiv((uint32_t)r, div_hw), rem = r - n * HWq;
                     const int y = (int)fdiv((uint32_t)rem, div_w), x = 2 * (rem - y * Wq) + h;
@@ -2213,7 +2215,7 @@ __global__ void __launch_bounds__(kThreadsDT, 1) dec_trunk2_kernel(DecTrunk P) {
                 }
             }
             // the next group's gather overwrites X: every epilogue warp is past its residual reads
-            asm volatile("bar.sync 1, %0;" ::"n"(128 * kDtGroups) : "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(128 * kD2Groups) : "memory");
         }
     }
     tc_fence_before();
@@ -2231,7 +2233,7 @@ size_t dec_trunk2_smem(int Hp, int Wp, int G, int K, int n_conv, int *pad) {
     const int p = ((128 * T - rows + 16) * 16 + 127) / 128 * 128;
     if (pad) *pad = p;
     return kD2Slots * kD2Chunk + (size_t)K * 64 + 2 * 8 * RS * 16 + p +
-           (2 * kD2Slots + 2 * kDtGroups + 2 + kD2MaxTiles) * 8 + 16 + (size_t)n_conv * 32 * 4;
+           (2 * kD2Slots + 2 * kD2Groups + 2 + kD2MaxTiles) * 8 + 16 + (size_t)n_conv * 32 * 4;
 }
 
 // ---- decoder output stage in shared memory (vqvae.py:101-112) ---------------
@@ -3460,7 +3462,7 @@ int dec_trunk2_launch(const DecTrunk &p0, cudaStream_t s) {
     if (grid < 1) return PILC_OK;
     const double flops = 2.0 * p.n_img * (p.Hp - 2) * (p.Wp - 2) * 32.0 * 32 * 9 * p.n_conv;
     ProfScope _ps(PROF_DEC_TRUNK2, s, flops);
-    dec_trunk2_kernel<<<(unsigned)grid, kThreadsDT, smem, s>>>(p);
+    dec_trunk2_kernel<<<(unsigned)grid, kThreadsD2, smem, s>>>(p);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
