@@ -268,9 +268,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int PPT, int CO_T>
+template <int PPT, int CO_T, int CPT = 8>  // CPT: channels computed of each thread's group of 8 (6: the heads)
 __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs a) {
-    constexpr int CPT = 8;
+    constexpr int CG = 8;  // output channels per thread group
     constexpr int PGR = 16 / PPT;  // pixel groups per tile row
     extern __shared__ __align__(16) float smem[];
     const int ks = a.ks, st = a.stride, pad = ks >> 1, TR = a.TR, RP = a.RP, CK = a.CK, CIP = a.CIP;
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
     const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
     const int oy0 = ty * TR, ox0 = tx * 16;
     const int co0 = blockIdx.y * CO_T;
-    const int NCG = CO_T / CPT;
+    const int NCG = CO_T / CG;
     const int t = threadIdx.x, nt = blockDim.x;
     const int cg = t % NCG, pg = t / NCG;
     const int pr = pg / PGR, pq = pg - pr * PGR;  // tile row, first column
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
             const float *px[PPT];
 #pragma unroll
             for (int p = 0; p < PPT; ++p) px[p] = s_in + ((pr * st + ti) * RP + pq * st + tj + p * PGR * st) * CIP;
-            const float *pw = wcur + cg * CPT;
+            const float *pw = wcur + cg * CG;
 #pragma unroll 1
             for (int ci = 0; ci < cn; ci += 4) {
                 // the heads (one channel group per thread, few accumulators):
@@ -396,8 +396,15 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
                         for (int p = 0; p < PPT; ++p) x[p] = px[p][u];
                     }
                     const float4 w0 = *reinterpret_cast<const float4 *>(pw + u * CO_T);
-                    const float4 w1 = *reinterpret_cast<const float4 *>(pw + u * CO_T + 4);
-                    const float w[CPT] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                    float w[CPT];
+                    w[0] = w0.x, w[1] = w0.y, w[2] = w0.z, w[3] = w0.w;
+                    if constexpr (CPT == 8) {
+                        const float4 w1 = *reinterpret_cast<const float4 *>(pw + u * CO_T + 4);
+                        w[4] = w1.x, w[5] = w1.y, w[6] = w1.z, w[7] = w1.w;
+                    } else {
+                        const float2 w1 = *reinterpret_cast<const float2 *>(pw + u * CO_T + 4);
+                        w[4] = w1.x, w[5] = w1.y;
+                    }
 #pragma unroll
                     for (int c = 0; c < CPT; ++c)
 #pragma unroll
@@ -424,7 +431,7 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
         float v[CPT];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-            const int co = co0 + cg * CPT + c;
+            const int co = co0 + cg * CG + c;
             float oc = o[c][p];
             if (praster >= a.tail_start) oc = a.side[((n * 8) + (praster - a.tail_start)) * a.Co_pad + co];
             v[c] = __fadd_rn(oc, __ldg(a.b + co));
@@ -433,14 +440,14 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
             const int64_t base = (((int64_t)n * a.Ho + oy) * a.Wo + ox) * a.Co;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
-                const int co = co0 + cg * CPT + c;
+                const int co = co0 + cg * CG + c;
                 if (co >= a.Co) break;
                 float r = v[c];
                 if (a.resid) r = __fadd_rn(a.resid[base + co], r);  // nn.residual_block: relu(x + conv)
                 if (a.relu) r = fmaxf(r, 0.f);
                 a.out[base + co] = r;
             }
-            if (a.zt) {  // tf32 hi / fp32 lo tiles (tc_conv.cu tc3 TC3_Z layout): exact, z = hi + lo
+            if (CPT == 8 && a.zt) {  // tf32 hi / fp32 lo tiles (tc_conv.cu tc3 TC3_Z layout): exact, z = hi + lo
                 const int64_t vix = (int64_t)n * a.Ho * a.Wo + praster;
                 float4 *zt = reinterpret_cast<float4 *>(a.zt) + (vix >> 7) * (2 * 8 * 128) + (vix & 127);
 #pragma unroll
@@ -449,8 +456,8 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
                     float hi[4], lo[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        hi[e] = tf32_rna(v[4 * h + e]);
-                        lo[e] = __fsub_rn(v[4 * h + e], hi[e]);
+                        hi[e] = tf32_rna(v[(4 * h + e) % CPT]);
+                        lo[e] = __fsub_rn(v[(4 * h + e) % CPT], hi[e]);
                     }
                     zt[g * 128] = make_float4(hi[0], hi[1], hi[2], hi[3]);
                     zt[(8 + g) * 128] = make_float4(lo[0], lo[1], lo[2], lo[3]);
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
             const int Hs = a.Ho * 2, Ws = a.Wo * 2;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
-                const int co = co0 + cg * CPT + c;
+                const int co = co0 + cg * CG + c;
                 if (co >= a.Co) break;
                 const int cc = co >> 2, dy = (co >> 1) & 1, dx = co & 1;
                 a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = fmaxf(v[c], 0.f);
@@ -679,6 +686,9 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
     } else if (co_t == 16) {
         allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 16>));
         conv_kernel<4, 16><<<grid, threads, smem, s>>>(a);
+    } else if (a.Co <= 6) {  // the heads: 6 of the 8 channels computed
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 8, 6>));
+        conv_kernel<4, 8, 6><<<grid, threads, smem, s>>>(a);
     } else {
         allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 8>));
         conv_kernel<4, 8><<<grid, threads, smem, s>>>(a);
