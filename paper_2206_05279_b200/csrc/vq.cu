@@ -553,6 +553,69 @@ __global__ void xtail_kernel(ConvArgs a, int64_t n_img, int n_tail, int mode) {
     a.side[(n * 8 + j) * a.Co_pad + co] = o;
 }
 
+// dec.proj (1x1 over the gathered codebook rows, ReLU): every output pixel
+// is a function of its code alone, so the layer is computed once per
+// codebook entry with conv_kernel's exact operations (the fmaf chain over the
+// padded input channels from zero, o = 0 + chain, + bias, ReLU) and
+// gathered; the raster tail pixels OpenBLAS orders differently come from
+// xtail_kernel as in conv_kernel.
+__global__ void proj_table_kernel(ConvArgs a, int K, float *__restrict__ tab) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K * a.Co_pad) return;
+    const int k = i / a.Co_pad, co = i - k * a.Co_pad;
+    float acc = 0.f;
+    for (int ci = 0; ci < a.Ci_pad; ++ci) {
+        const float x = ci < a.Ci ? a.codebook[(int64_t)k * a.Ci + ci] : 0.f;
+        acc = fmaf(a.w[(int64_t)ci * a.Co_pad + co], x, acc);
+    }
+    const float v = __fadd_rn(__fadd_rn(0.f, acc), a.b[co]);
+    tab[i] = a.relu ? fmaxf(v, 0.f) : v;
+}
+
+__global__ void proj_gather_kernel(ConvArgs a, int64_t n_img, const float *__restrict__ tab) {
+    const int64_t npx = (int64_t)a.Ho * a.Wo;
+    if ((a.Co & 3) == 0) {  // four channels per thread: 16-byte table reads and stores
+        const int ncv = a.Co >> 2;
+        const int64_t total4 = n_img * npx * ncv;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total4;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t q = i / ncv;  // n * npx + praster
+            const int c4 = (int)(i - q * ncv);
+            const int64_t praster = q % npx;
+            float4 r;
+            if (praster >= a.tail_start) {
+                const int64_t n = q / npx;
+                const float *sd = a.side + ((n * 8) + (praster - a.tail_start)) * a.Co_pad + 4 * c4;
+                float v[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    v[e] = __fadd_rn(sd[e], a.b[4 * c4 + e]);
+                    if (a.relu) v[e] = fmaxf(v[e], 0.f);
+                }
+                r = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+                r = __ldg(reinterpret_cast<const float4 *>(tab + (int64_t)a.in_u8[q] * a.Co_pad) + c4);
+            }
+            reinterpret_cast<float4 *>(a.out)[i] = r;
+        }
+        return;
+    }
+    const int64_t total = n_img * npx * a.Co;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int co = (int)(i % a.Co);
+        const int64_t q = i / a.Co;  // n * npx + praster
+        const int64_t n = q / npx, praster = q - n * npx;
+        float r;
+        if (praster >= a.tail_start) {
+            const float v = __fadd_rn(a.side[((n * 8) + (praster - a.tail_start)) * a.Co_pad + co], a.b[co]);
+            r = a.relu ? fmaxf(v, 0.f) : v;
+        } else {
+            r = tab[(int64_t)a.in_u8[q] * a.Co_pad + co];
+        }
+        a.out[i] = r;
+    }
+}
+
 // shared-memory footprint of one conv_kernel CTA
 size_t conv_smem(const ConvArgs &a) {
     const int IR = (a.TR - 1) * a.stride + a.ks;
@@ -693,6 +756,31 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
         allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 8>));
         conv_kernel<4, 8><<<grid, threads, smem, s>>>(a);
     }
+    PILC_CHECK_LAUNCH();
+    return PILC_OK;
+}
+
+// dec.proj through proj_table_kernel + proj_gather_kernel (same values as
+// launch_conv of the 1x1 IN_CODEBOOK layer)
+int launch_proj_table(ConvArgs a, int K, int64_t n_img, cudaStream_t s, float *side, float *tab, int co_real) {
+    int n_tail = 0;
+    const int tmode = tail_mode_of(a, co_real, &a.tail_start, &n_tail);
+    if (tmode < 0) return PILC_E_UNSUPPORTED;
+    a.side = side;
+    const double flops = 2.0 * n_img * a.Ho * a.Wo * (double)a.Co * a.Ci;
+    ProfScope _ps(PROF_CONV, s, flops);
+    if (tmode > 0) {
+        const int64_t total = n_img * n_tail * a.Co;
+        xtail_kernel<<<(unsigned)ceil_div64(total, 128), 128, 0, s>>>(a, n_img, n_tail, tmode);
+        PILC_CHECK_LAUNCH();
+    }
+    proj_table_kernel<<<(unsigned)ceil_div64((int64_t)K * a.Co_pad, 128), 128, 0, s>>>(a, K, tab);
+    PILC_CHECK_LAUNCH();
+    const int64_t total = n_img * a.Ho * a.Wo * (int64_t)a.Co / ((a.Co & 3) == 0 ? 4 : 1);
+    int64_t blocks = ceil_div64(total, 256);
+    const int64_t cap = (int64_t)sm_count() * 32;
+    if (blocks > cap) blocks = cap;
+    proj_gather_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(a, n_img, tab);
     PILC_CHECK_LAUNCH();
     return PILC_OK;
 }
@@ -866,7 +954,7 @@ int launch_argmin(const float *z, int64_t n_vec, const float *cb, int K, int Dc,
 }
 
 struct Work {
-    float *A, *B, *T, *Z, *side, *ZT;
+    float *A, *B, *T, *Z, *side, *ZT, *tab;
 };
 
 int64_t ws_parts(int64_t n, int H, int W, int Dc, int C, Work *w, char *base) {
@@ -878,6 +966,7 @@ int64_t ws_parts(int64_t n, int H, int W, int Dc, int C, Work *w, char *base) {
     const int64_t cmax = 4 * (int64_t)round_up(C > Dc ? C : Dc, 32);
     const int64_t sd = n * 8 * cmax * 4;  // tail outputs (launch_conv)
     const int64_t zt = Dc == 32 ? ((n * gh * gw + 127) / 128) * 128 * 32 * 4 * 2 : 0;  // argmin_tc tiles
+    const int64_t tb = 256 * cmax * 4;  // dec.proj per codebook entry (proj_table_kernel)
     auto al = [](int64_t v) { return (v + 255) / 256 * 256; };
     if (w) {
         w->A = reinterpret_cast<float *>(base);
@@ -886,8 +975,9 @@ int64_t ws_parts(int64_t n, int H, int W, int Dc, int C, Work *w, char *base) {
         w->Z = reinterpret_cast<float *>(base + al(a) + 2 * al(b));
         w->side = reinterpret_cast<float *>(base + al(a) + 2 * al(b) + al(z));
         w->ZT = reinterpret_cast<float *>(base + al(a) + 2 * al(b) + al(z) + al(sd));
+        w->tab = reinterpret_cast<float *>(base + al(a) + 2 * al(b) + al(z) + al(sd) + al(zt));
     }
-    return al(a) + 2 * al(b) + al(z) + al(sd) + al(zt);
+    return al(a) + 2 * al(b) + al(z) + al(sd) + al(zt) + al(tb);
 }
 
 // tcgen05 decoder scratch: three latent slabs X, T, Y and the shuffled
@@ -1507,7 +1597,7 @@ int exact_decode(const uint8_t *idx, int64_t n_img, int H, int W, const float *m
     a.Wi = a.Wo = gw;
     a.relu = 1;
     a.out = w.B;
-    rc = launch_conv(a, L.dec[0].co_t, n_img, s, w.side, L.dec[0].co);
+    rc = launch_proj_table(a, L.K, n_img, s, w.side, w.tab, L.dec[0].co);
     for (int i = 0; !rc && i < B; ++i) {
         a = base_args(model, L.dec[1 + 2 * i]);
         a.in = w.B;
