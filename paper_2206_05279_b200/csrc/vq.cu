@@ -438,14 +438,34 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
         }
         if (a.out_mode == OUT_F32) {
             const int64_t base = (((int64_t)n * a.Ho + oy) * a.Wo + ox) * a.Co;
+            const int cb0 = co0 + cg * CG;
+            if (CPT == 8 && (a.Co & 3) == 0 && cb0 + 8 <= a.Co) {  // two 16-byte stores (and residual loads)
+                float r[8];
 #pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-                const int co = co0 + cg * CG + c;
-                if (co >= a.Co) break;
-                float r = v[c];
-                if (a.resid) r = __fadd_rn(a.resid[base + co], r);  // nn.residual_block: relu(x + conv)
-                if (a.relu) r = fmaxf(r, 0.f);
-                a.out[base + co] = r;
+                for (int c = 0; c < 8; ++c) r[c] = v[c % CPT];
+                if (a.resid) {  // nn.residual_block: relu(x + conv)
+                    const float4 x0 = *reinterpret_cast<const float4 *>(a.resid + base + cb0);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(a.resid + base + cb0 + 4);
+                    const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) r[c] = __fadd_rn(xs[c], r[c]);
+                }
+                if (a.relu) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) r[c] = fmaxf(r[c], 0.f);
+                }
+                *reinterpret_cast<float4 *>(a.out + base + cb0) = make_float4(r[0], r[1], r[2], r[3]);
+                *reinterpret_cast<float4 *>(a.out + base + cb0 + 4) = make_float4(r[4], r[5], r[6], r[7]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    const int co = cb0 + c;
+                    if (co >= a.Co) break;
+                    float r = v[c];
+                    if (a.resid) r = __fadd_rn(a.resid[base + co], r);  // nn.residual_block: relu(x + conv)
+                    if (a.relu) r = fmaxf(r, 0.f);
+                    a.out[base + co] = r;
+                }
             }
             if (CPT == 8 && a.zt) {  // tf32 hi / fp32 lo tiles (tc_conv.cu tc3 TC3_Z layout): exact, z = hi + lo
                 const int64_t vix = (int64_t)n * a.Ho * a.Wo + praster;
