@@ -488,12 +488,22 @@ __global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs 
             // latent (u, v) lands at (2u + dy, 2v + dx), channel c; then ReLU
             const int Cs = a.Co >> 2;
             const int Hs = a.Ho * 2, Ws = a.Wo * 2;
+            const int cb0 = co0 + cg * CG;
+            if (CPT == 8 && cb0 + 8 <= a.Co) {  // per sub-pixel two adjacent channels: one 8-byte store
 #pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-                const int co = co0 + cg * CG + c;
-                if (co >= a.Co) break;
-                const int cc = co >> 2, dy = (co >> 1) & 1, dx = co & 1;
-                a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = fmaxf(v[c], 0.f);
+                for (int sp = 0; sp < 4; ++sp) {
+                    const int dy = sp >> 1, dx = sp & 1, cc = cb0 >> 2;
+                    *reinterpret_cast<float2 *>(a.out + (((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc) =
+                        make_float2(fmaxf(v[sp], 0.f), fmaxf(v[(sp + 4) % CPT], 0.f));
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    const int co = cb0 + c;
+                    if (co >= a.Co) break;
+                    const int cc = co >> 2, dy = (co >> 1) & 1, dx = co & 1;
+                    a.out[(((int64_t)n * Hs + 2 * oy + dy) * Ws + 2 * ox + dx) * Cs + cc] = fmaxf(v[c], 0.f);
+                }
             }
         } else {
             // logistic head (vqvae.py:105-112, logistic.py:36-40, 109-114)
