@@ -269,7 +269,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int PPT, int CO_T, int CPT = 8>  // CPT: channels computed of each thread's group of 8 (6: the heads)
-__global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : 3) conv_kernel(ConvArgs a) {
+__global__ void __launch_bounds__(128, CO_T >= 16 ? 5 : (PPT == 2 ? 4 : 3)) conv_kernel(ConvArgs a) {
     constexpr int CG = 8;  // output channels per thread group
     constexpr int PGR = 16 / PPT;  // pixel groups per tile row
     extern __shared__ __align__(16) float smem[];
@@ -686,7 +686,10 @@ int tail_mode_of(const ConvArgs &a, int co_real, int64_t *start, int *count) {
 // co_real: the reference's output channel count of one conv call (the
 // merged mu|s head is two Co = 3 convs)
 int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side, int co_real) {
-    const int ppt = 4;  // 4 pixels x 8 channels per thread: ~100 registers, 5 CTAs per SM (8 pixels: 168, 3)
+    // 4 pixels x 8 channels per thread: ~100 registers, 5 CTAs per SM (8
+    // pixels: 168, 3); the heads (one channel group) 2 pixels, so their
+    // 16-row tiles take half the shared memory of 32-row ones
+    const int ppt = (co_t == 8 && a.Co <= 6) ? 2 : 4;
     a.CO_T = co_t;
     const int ncg = co_t / 8;
     const int threads_per_row = (16 / ppt) * ncg;
@@ -780,8 +783,8 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
         allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 16>));
         conv_kernel<4, 16><<<grid, threads, smem, s>>>(a);
     } else if (a.Co <= 6) {  // the heads: 6 of the 8 channels computed
-        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 8, 6>));
-        conv_kernel<4, 8, 6><<<grid, threads, smem, s>>>(a);
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<2, 8, 6>));
+        conv_kernel<2, 8, 6><<<grid, threads, smem, s>>>(a);
     } else {
         allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 8>));
         conv_kernel<4, 8><<<grid, threads, smem, s>>>(a);
