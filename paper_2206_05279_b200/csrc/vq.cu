@@ -687,9 +687,9 @@ int tail_mode_of(const ConvArgs &a, int co_real, int64_t *start, int *count) {
 // merged mu|s head is two Co = 3 convs)
 int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side, int co_real) {
     // 4 pixels x 8 channels per thread: ~100 registers, 5 CTAs per SM (8
-    // pixels: 168, 3); the heads (one channel group) 2 pixels, so their
-    // 16-row tiles take half the shared memory of 32-row ones
-    const int ppt = (co_t == 8 && a.Co <= 6) ? 2 : 4;
+    // pixels: 168, 3); the heads (one channel group) and the stride-2 conv
+    // 2 pixels, so their tiles take half the shared memory
+    const int ppt = ((co_t == 8 && a.Co <= 6) || (a.stride == 2 && co_t == 32)) ? 2 : 4;
     a.CO_T = co_t;
     const int ncg = co_t / 8;
     const int threads_per_row = (16 / ppt) * ncg;
@@ -776,7 +776,10 @@ int launch_conv(ConvArgs a, int co_t, int64_t n_img, cudaStream_t s, float *side
     }
     const size_t smem = conv_smem(a);
     dim3 grid((unsigned)blocks, (unsigned)(a.Co_pad / co_t));
-    if (co_t == 32) {
+    if (co_t == 32 && ppt == 2) {  // the stride-2 down conv: smaller tiles, more CTAs per SM
+        allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<2, 32>));
+        conv_kernel<2, 32><<<grid, threads, smem, s>>>(a);
+    } else if (co_t == 32) {
         allow_dyn_smem(reinterpret_cast<const void *>(conv_kernel<4, 32>));
         conv_kernel<4, 32><<<grid, threads, smem, s>>>(a);
     } else if (co_t == 16) {
