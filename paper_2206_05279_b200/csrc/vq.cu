@@ -168,7 +168,12 @@ Layout make_layout(int K, int Dc, int C, int B) {
 // arrives by cp.async straight from the NHWC activations (edge-replicate
 // padding = clamped source pixels); the weights of one tap ([ci][CO_T]) are
 // double-buffered so tap t + 1's copy overlaps tap t's math. Channels beyond
-// CK (wide models) are re-staged per tap, synchronously.
+// CK (wide models) are re-staged per tap, synchronously. PPT is 4 (96
+// registers: five CTAs per SM), 2 for the heads and the stride-2 conv (half
+// the shared memory per CTA); the heads load four channels per 16-byte
+// access and compute only their 6 channels (CPT); the epilogue reads the
+// residual and writes 8 channels as two 16-byte accesses. dec.proj, whose
+// output depends on the code alone, goes through proj_table_kernel instead.
 enum InMode { IN_F32 = 0, IN_U8 = 1, IN_CODEBOOK = 2 };
 enum OutMode { OUT_F32 = 0, OUT_SHUFFLE = 1, OUT_HEAD = 2 };
 
